@@ -1,0 +1,302 @@
+// Warp-specialised tcgen05 (kind::tf32) GEMM core used by every dense
+// contraction of the training step: CONV forward / dgrad / wgrad as
+// implicit GEMMs and the FC layers as plain GEMMs.
+//
+//   D[M x N] (+)= A[M x K] . B[N x K]^T          fp32 in HBM, tf32 MMA, fp32 acc
+//
+// One CTA computes one BM=128 x BN tile for a range of K blocks (split-K over
+// gridDim.z).  Warps 0-3 are producers (cp.async 16 B into SWIZZLE_128B smem
+// stages, zero fill for padding / out-of-range rows) and afterwards the
+// epilogue (tcgen05.ld of the TMEM accumulator); warp 4 allocates TMEM and one
+// elected lane issues the tcgen05.mma chain.  Operands are either K-major
+// (128-byte rows hold 32 consecutive k of one row) or MN-major (128-byte rows
+// hold 32 consecutive rows of one k), so transposed operands (dgrad/wgrad) are
+// fed directly from their NHWC layout without a transpose pass.
+//
+// The operand gathers are policy objects (see conv loaders in conv_tc.cu):
+//   struct Loader { __device__ void tile_init(int r0, void* scratch, int tid);
+//                   __device__ void load(uint32_t smem_tile, int kb, int tid); };
+#pragma once
+#include "tc_common.cuh"
+
+namespace sn {
+
+constexpr int kBM = 128;     // MMA M (rows of the tile, TMEM lanes)
+constexpr int kBK = 32;      // fp32 elements per k block (= one 128 B swizzle row)
+constexpr int kProducers = 128;
+constexpr int kGemmThreads = 160;
+constexpr int kScratchBytes = 4096;  // per-operand tile_init scratch (row tables)
+
+template <int BN, int STAGES>
+struct GemmSmem {
+  static constexpr int A_BYTES = kBM * 128;
+  static constexpr int B_BYTES = BN * 128;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+  static constexpr int SCRATCH_OFF = BAR_OFF + 256;
+  static constexpr int TOTAL = SCRATCH_OFF + 2 * kScratchBytes + 1024;  // +1024 alignment slack
+};
+
+template <int BN>
+__host__ __device__ constexpr uint32_t tmem_cols() {
+  return BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
+}
+
+// MN-major tile of 32 k-rows x R mn-elements in the SWIZZLE_128B_BASE32B
+// canonical layout: MN atoms (32 elements x 4 k rows = 512 B) are adjacent
+// (LBO = 512), K atoms (4 k rows) are R*16 B apart (SBO).
+template <int R>
+struct MNTile {
+  static constexpr uint32_t LBO = 512;
+  static constexpr uint32_t SBO = (R / 32) * 512;
+};
+template <int R>
+__device__ __forceinline__ uint32_t mn_tile_off(uint32_t krow, uint32_t mchunk) {
+  const uint32_t r4 = krow & 3u;
+  const uint32_t c16 = mchunk & 7u;
+  return (krow >> 2) * MNTile<R>::SBO + (mchunk >> 3) * MNTile<R>::LBO + (r4 << 7) +
+         ((((c16 >> 1) ^ r4) & 3u) << 5) + ((c16 & 1u) << 4);
+}
+
+template <int BN, int STAGES, bool A_MN, bool B_MN, class LA, class LB, class EPI>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    tc_gemm_kernel(LA la, LB lb, EPI epi, int num_kb, int kb_per_split) {
+  using L = GemmSmem<BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * L::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
+  uint64_t* empty = full + STAGES;
+  uint64_t* done = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  uint8_t* scratch_a = smem + L::SCRATCH_OFF;
+  uint8_t* scratch_b = scratch_a + kScratchBytes;
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int lane = tid & 31;
+  const int m0 = blockIdx.x * kBM;
+  const int n0 = blockIdx.y * BN;
+  const int kb0 = blockIdx.z * kb_per_split;
+  const int kb1 = min(num_kb, kb0 + kb_per_split);
+  const int nkb = kb1 - kb0;
+
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], kProducers);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 4) tmem_alloc(tmem_slot, tmem_cols<BN>());
+  if (tid < kProducers) {
+    la.tile_init(m0, scratch_a, tid);
+    lb.tile_init(n0, scratch_b, tid);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < 4) {
+    // ---------------- producers ----------------
+    constexpr int LAG = STAGES - 1;
+    for (int i = 0; i < nkb; ++i) {
+      const int s = i % STAGES;
+      if (i >= STAGES) mbar_wait(&empty[s], ((i / STAGES) - 1) & 1);
+      la.load(smem_u32(sA + s * L::A_BYTES), kb0 + i, tid);
+      lb.load(smem_u32(sB + s * L::B_BYTES), kb0 + i, tid);
+      cp_async_commit();
+      if (i >= LAG) {
+        cp_async_wait<LAG>();
+        fence_proxy_async();
+        mbar_arrive(&full[(i - LAG) % STAGES]);
+      }
+    }
+    cp_async_wait<0>();
+    fence_proxy_async();
+    for (int j = (nkb > LAG ? nkb - LAG : 0); j < nkb; ++j) mbar_arrive(&full[j % STAGES]);
+
+    // ---------------- epilogue ----------------
+    mbar_wait(done, 0);
+    tc_fence_after();
+    const int row = warp * 32 + lane;
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      float v[32];
+      tmem_ld32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + static_cast<uint32_t>(c), v);
+      epi.store(m0 + row, n0 + c, v, blockIdx.z);
+    }
+    tc_fence_before();
+  } else if (lane == 0) {
+    // ---------------- MMA issuer ----------------
+    constexpr uint32_t idesc = idesc_tf32(kBM, BN, A_MN, B_MN);
+    for (int i = 0; i < nkb; ++i) {
+      const int s = i % STAGES;
+      mbar_wait(&full[s], (i / STAGES) & 1);
+      tc_fence_after();
+      const uint32_t a0 = smem_u32(sA + s * L::A_BYTES);
+      const uint32_t b0 = smem_u32(sB + s * L::B_BYTES);
+#pragma unroll
+      for (int kk = 0; kk < kBK / 8; ++kk) {
+        // One MMA consumes K = 8: 32 B of each K-major row, or two 4-row K
+        // atoms of an MN-major tile.
+        const uint64_t ad =
+            A_MN ? umma_desc(a0 + kk * 2 * MNTile<kBM>::SBO, MNTile<kBM>::LBO, MNTile<kBM>::SBO,
+                             kLayoutSW128Base32)
+                 : umma_desc(a0 + kk * 32, 16, 1024, kLayoutSW128);
+        const uint64_t bd =
+            B_MN ? umma_desc(b0 + kk * 2 * MNTile<BN>::SBO, MNTile<BN>::LBO, MNTile<BN>::SBO,
+                             kLayoutSW128Base32)
+                 : umma_desc(b0 + kk * 32, 16, 1024, kLayoutSW128);
+        umma_tf32(tmem, ad, bd, idesc, (i | kk) != 0 ? 1u : 0u);
+      }
+      umma_commit(&empty[s]);
+    }
+    umma_commit(done);
+  }
+  __syncthreads();
+  if (warp == 4) {
+    tc_fence_after();
+    tmem_dealloc(tmem, tmem_cols<BN>());
+  }
+}
+
+template <int BN, int STAGES, bool A_MN, bool B_MN, class LA, class LB, class EPI>
+inline cudaError_t launch_tc_gemm(const LA& la, const LB& lb, const EPI& epi, int M, int N, int K,
+                                  int splits, cudaStream_t stream) {
+  using L = GemmSmem<BN, STAGES>;
+  auto kern = tc_gemm_kernel<BN, STAGES, A_MN, B_MN, LA, LB, EPI>;
+  static bool attr_set = false;  // per template instantiation
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int num_kb = (K + kBK - 1) / kBK;
+  if (splits < 1) splits = 1;
+  if (splits > num_kb) splits = num_kb;
+  const int kps = (num_kb + splits - 1) / splits;
+  splits = (num_kb + kps - 1) / kps;  // every split owns >= 1 k block
+  dim3 grid((M + kBM - 1) / kBM, (N + BN - 1) / BN, splits);
+  kern<<<grid, kGemmThreads, L::TOTAL, stream>>>(la, lb, epi, num_kb, kps);
+  return cudaGetLastError();
+}
+
+// Split count actually used by launch_tc_gemm for a requested count.
+inline int effective_splits(int K, int splits) {
+  const int num_kb = (K + kBK - 1) / kBK;
+  if (splits < 1) splits = 1;
+  if (splits > num_kb) splits = num_kb;
+  const int kps = (num_kb + splits - 1) / splits;
+  return (num_kb + kps - 1) / kps;
+}
+
+// ===========================================================================
+// Generic strided-matrix loaders (FC layers, tests).
+// ===========================================================================
+
+// K-major operand: element (r, k) at base[r * ld + k], R rows per tile.
+template <int R>
+struct MatKLoader {
+  const float* base;
+  int rows, K, ld;
+  int fast;  // base 16 B aligned and ld % 4 == 0 and K % 4 == 0
+  int r0;
+  __device__ void tile_init(int r0_, void*, int) { r0 = r0_; }
+  __device__ void load(uint32_t tile, int kb, int tid) {
+    const int warp = tid >> 5, lane = tid & 31;
+    const int chunk = lane & 7;
+    const int k = kb * kBK + chunk * 4;
+#pragma unroll 4
+    for (int it = 0; it < R / 16; ++it) {
+      const int row = warp * (R / 4) + it * 4 + (lane >> 3);
+      const int r = r0 + row;
+      const uint32_t dst = tile + sw128_off(row, chunk);
+      if (fast) {
+        const bool ok = (r < rows) && (k < K);
+        cp_async16(dst, ok ? base + static_cast<size_t>(r) * ld + k : base, ok ? 16u : 0u);
+      } else {
+        float v[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          v[e] = (r < rows && k + e < K) ? __ldg(base + static_cast<size_t>(r) * ld + k + e) : 0.f;
+        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(dst), "f"(v[0]), "f"(v[1]),
+                     "f"(v[2]), "f"(v[3])
+                     : "memory");
+      }
+    }
+  }
+};
+
+// MN-major operand: element (r, k) at base[k * ld + r], R rows per tile.
+template <int R>
+struct MatMNLoader {
+  const float* base;
+  int rows, K, ld;
+  int fast;  // base 16 B aligned and ld % 4 == 0 and rows % 4 == 0
+  int r0;
+  __device__ void tile_init(int r0_, void*, int) { r0 = r0_; }
+  __device__ void load(uint32_t tile, int kb, int tid) {
+    constexpr int CPR = R / 4;             // 16-byte chunks per k row
+    constexpr int TOTAL = 32 * CPR;        // chunks per tile
+#pragma unroll 4
+    for (int f = tid; f < TOTAL; f += kProducers) {
+      const int krow = f / CPR, mc = f % CPR;
+      const int k = kb * kBK + krow;
+      const int r = r0 + mc * 4;
+      const uint32_t dst = tile + mn_tile_off<R>(krow, mc);
+      if (fast) {
+        const bool ok = (k < K) && (r < rows);
+        cp_async16(dst, ok ? base + static_cast<size_t>(k) * ld + r : base, ok ? 16u : 0u);
+      } else {
+        float v[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          v[e] = (k < K && r + e < rows) ? __ldg(base + static_cast<size_t>(k) * ld + r + e) : 0.f;
+        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(dst), "f"(v[0]), "f"(v[1]),
+                     "f"(v[2]), "f"(v[3])
+                     : "memory");
+      }
+    }
+  }
+};
+
+// Row-major output D[m * ldd + n] = alpha*acc + (beta ? D : 0) + bias[n].
+struct EpiRowMajor {
+  float* D;
+  const float* bias;  // may be null
+  int M, N, ldd;
+  int accumulate;     // 1: D += acc, 0: D = acc
+  __device__ void store(int m, int n0, const float* v, int) const {
+    if (m >= M) return;
+    float* d = D + static_cast<size_t>(m) * ldd;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int n = n0 + j;
+      if (n < N) {
+        float x = v[j];
+        if (bias) x += __ldg(bias + n);
+        d[n] = accumulate ? d[n] + x : x;
+      }
+    }
+  }
+};
+
+// Split-K partial store: P[split][m][n] (no bias, no accumulation).
+struct EpiPartial {
+  float* P;
+  int M, N;
+  __device__ void store(int m, int n0, const float* v, int split) const {
+    if (m >= M) return;
+    float* d = P + (static_cast<size_t>(split) * M + m) * N;
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (n0 + j < N) d[n0 + j] = v[j];
+  }
+};
+
+}  // namespace sn
