@@ -175,6 +175,8 @@ int sn_plan_demands(const sn_plan* plan, int64_t* demands, size_t cap, size_t* n
 /* Planning without simulation (analysis entry points of the reference API):
  * shapes/costs, forward order, per-step demands; cfg->pool_bytes ignored. */
 int sn_analyze(const sn_net_desc* net, const sn_sim_config* cfg, sn_plan** out);
+/* Cost table only, with costmodel.build_costs' error semantics (no schedule). */
+int sn_build_costs(const sn_net_desc* net, const sn_sim_config* cfg, sn_plan** out);
 
 /* Test hook: CPython set iteration order emulation (see planner/pyset.hpp). */
 int sn_debug_pyset(const int64_t* a, size_t na, const int64_t* b, size_t nb, const int64_t* a2,
