@@ -1,0 +1,400 @@
+"""Benchmark: images/sec of the memory-scheduled training step on B200.
+
+Default workload (BASELINE.json configs[1]): ResNet-50g = gen_resnet(3,4,6,3)
+(the reference's generated residual net), batch 256 per GPU, fp32 storage
+with tf32 tensor-core math, a 24 GiB pool budget, all five SuperNeurons
+features (liveness, offload, LRU cache, cost-aware recompute, conv workspace
+selection).  One step = forward + backward + SGD update of one batch.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+
+Under torchrun each rank is one replica (weak scaling, fixed per-GPU batch)
+and the weight gradients are all-reduced over NCCL.  Rank 0 prints ONE JSON
+line.  ``--impl reference`` times the CPU restatement of the same training
+step (oracle/numerics.py; the reference itself has no numerics and cannot
+run here) on a bounded sample, with all host threads.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+ALL = "liveness,offload,cache,recompute=cost-aware,convselect"
+GiB = 1 << 30
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--net", default="resnet50g", choices=["resnet50g", "resnet152g", "alexnet", "alex32"])
+    ap.add_argument("--batch", type=int, default=256)
+    ap.add_argument("--pool-gib", type=float, default=24.0)
+    ap.add_argument("--features", default=ALL)
+    ap.add_argument("--no-extras", action="store_true", help="skip the unconstrained / profile / baseline legs")
+    return ap.parse_args()
+
+
+def build_net(name: str):
+    import paper_1801_04380_b200 as sn
+    from paper_1801_04380_b200.netgen import gen_resnet
+    if name == "resnet50g":
+        return gen_resnet(3, 4, 6, 3)
+    if name == "resnet152g":
+        return gen_resnet(3, 8, 36, 3)
+    return sn.load_network(os.path.join(ROOT, "paper_1801_04380_b200", "fixtures", f"{name}.net"))
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int) -> None:
+        self.index = index
+        self.samples: list[list[str]] = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self) -> None:
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self) -> dict:
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def measured_peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh)
+    except OSError:
+        return {}
+
+
+def tf32_gemm_peak(device) -> float:
+    """cuBLAS tf32 GEMM 8192^3, best of 5 (TF/s) -- the tensor roofline for tf32 kernels."""
+    import torch
+    torch.backends.cuda.matmul.allow_tf32 = True
+    a = torch.randn(8192, 8192, device=device)
+    b = torch.randn(8192, 8192, device=device)
+    for _ in range(2):
+        a @ b
+    best = math.inf
+    for _ in range(5):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        a @ b
+        e.record()
+        torch.cuda.synchronize()
+        best = min(best, s.elapsed_time(e))
+    del a, b
+    torch.cuda.empty_cache()
+    return 2 * 8192 ** 3 / (best / 1e3) / 1e12
+
+
+def conv_flops(net, batch: int):
+    """Algorithmic tensor FLOPs per iteration: CONV fwd + wgrad + dgrad (dgrad
+    skipped when the input is DATA), FC fwd + wgrad + dgrad."""
+    import paper_1801_04380_b200 as sn
+    shapes = sn.propagate_shapes(net)
+    per_layer = {}
+    for lay in net.layers:
+        if lay.kind not in (sn.LayerKind.CONV, sn.LayerKind.FC):
+            continue
+        cin_shape = shapes[lay.prev[0]]
+        out = shapes[lay.id]
+        if lay.kind is sn.LayerKind.CONV:
+            k = lay.params["k"]
+            mac = batch * out[0] * out[1] * out[2] * cin_shape[0] * k * k
+        else:
+            mac = batch * out[0] * math.prod(cin_shape)
+        has_dgrad = net.layers[lay.prev[0]].kind is not sn.LayerKind.DATA
+        per_layer[lay.id] = (2 * mac, 2 * mac * (2 if has_dgrad else 1))  # (fwd, bwd)
+    return per_layer
+
+
+def run_ours(args) -> None:
+    import torch
+    import paper_1801_04380_b200 as sn
+    from paper_1801_04380_b200.training import Executor
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+
+    net = build_net(args.net)
+    B = args.batch
+    pool = int(args.pool_gib * GiB)
+    cfg = sn.SimConfig(pool_bytes=pool, features=sn.parse_features(args.features), cost=sn.CostConfig(batch=B))
+    ex = Executor(net, cfg, device=local, seed=2, lr=0.01, grad_scale=1.0 / world)
+    rep = ex.report
+    c, h, w = sn.propagate_shapes(net)[net.data_id]
+    n_cls = math.prod(sn.propagate_shapes(net)[net.terminal_id])
+    gen = torch.Generator().manual_seed(1000 + rank)
+    images = torch.randn(B, c, h, w, generator=gen)
+    labels = torch.randint(0, n_cls, (B,), generator=gen)
+    ex.set_inputs(images, labels)
+    grads = ex.grads_tensor()
+
+    def step():
+        if world == 1:
+            return ex.step(update=True)
+        loss, t = ex.step(update=False)
+        dist.all_reduce(grads)
+        ex.apply_update(0.01, 1.0 / world)
+        return loss, t
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    kernels = 0
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        start.record()
+        losses = []
+        for _ in range(args.steps):
+            loss, t = step()
+            kernels += t.kernels
+            losses.append(loss)
+        end.record()
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    elapsed_ms = start.elapsed_time(end)
+    if dist:
+        tt = torch.tensor([elapsed_ms], device=f"cuda:{local}")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        elapsed_ms = tt.item()
+    ms_per_step = elapsed_ms / args.steps
+    value = world * B * args.steps / (elapsed_ms / 1e3)
+
+    # ---- end to end through the public API: pinned host batch in, loss out ----
+    img_host = images.permute(0, 2, 3, 1).contiguous()
+    if ex.data_channels != ex.c_real:
+        img_host = torch.nn.functional.pad(img_host, (0, ex.data_channels - ex.c_real))
+    img_host = img_host.pin_memory()
+    lab_host = labels.to(torch.int32).pin_memory()
+    for _ in range(2):
+        ex.step_host(img_host, lab_host)
+    torch.cuda.synchronize()
+    e_steps = max(3, min(args.steps, 10))
+    t0 = time.perf_counter()
+    e_ms = []
+    for _ in range(e_steps):
+        _, t = ex.step_host(img_host, lab_host)
+        e_ms.append(t.step_ms)
+    e2e_wall = time.perf_counter() - t0
+    e2e_dev_ms = sum(e_ms) / len(e_ms)
+    h2d = img_host.numel() * 4 + lab_host.numel() * 4
+    line = {
+        "metric": "images/sec under memory budget (ResNet-50g b256/GPU, 24 GiB pool, all SuperNeurons features)",
+        "value": round(value, 2), "unit": "images/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "fp32 storage, tf32 tensor-core math (fp32 accumulate)",
+        "data": "synthetic N(0,1) images, uniform labels; He-uniform weights (seed 2)",
+        "config": {"workload": f"{args.net}_b{B}_pool{args.pool_gib:g}GiB_{args.features.replace(',', '+')}",
+                   "model": args.net, "global_batch": B * world, "per_gpu_batch": B, "image": [c, h, w],
+                   "parallelism": f"dp{world}", "pool_bytes": pool, "features": args.features,
+                   "l2": "no flush needed: per-step working set (~3.3 GB arena) >> 126 MB L2"},
+        "e2e": {"value": round(B * world / (e2e_dev_ms / 1e3), 2), "unit": "images/s",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4,
+                "wall_images_per_s": round(B * e_steps / e2e_wall, 2)},
+        "gpu_launches": int(kernels),
+        "memory": {"peak_bytes": rep.peak_bytes, "min_pool_bytes_max_i_l_i": rep.min_pool_bytes,
+                   "peak_over_floor": round(rep.peak_bytes / rep.min_pool_bytes, 4),
+                   "pool_high_water_bytes": rep.pool_high_water_bytes,
+                   "baseline_peak_bytes_features_none": rep.baseline_peak_bytes,
+                   "offload_d2h_bytes_per_step_issued": int(t.d2h_bytes),
+                   "offload_scheduled_bytes_per_step_planned": rep.scheduled_transfer_bytes,
+                   "replays_per_step": rep.extra_forward_steps},
+        "clocks": clocks.summary(),
+        "losses": [round(l, 5) for l in losses[:3]] + [round(losses[-1], 5)],
+    }
+    if not args.no_extras and rank == 0:
+        line.update(extras(args, net, cfg, ex, ms_per_step, local))
+    ex.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def extras(args, net, cfg, ex, ms_per_step, local) -> dict:
+    """Roofline of the dominant kernel class, unconstrained-run overhead, CPU baseline."""
+    import torch
+    import paper_1801_04380_b200 as sn
+    from paper_1801_04380_b200.training import Executor
+    out: dict = {}
+    # per-action device time of one eager iteration
+    prof = ex.profile()
+    flops = conv_flops(net, args.batch)
+    t_tensor = 0.0
+    f_tensor = 0.0
+    t_other = 0.0
+    by_kind: dict = {}
+    for ms, lid, typ in prof:
+        if lid < 0:
+            continue
+        kind = net.layers[lid].kind.value
+        key = f"{kind}:{['fwd', 'replay', 'bwd'][typ]}"
+        by_kind[key] = by_kind.get(key, 0.0) + ms
+        if lid in flops and typ in (0, 2):
+            t_tensor += ms
+            f_tensor += flops[lid][0 if typ == 0 else 1]
+        else:
+            t_other += ms
+    peaks = measured_peaks()
+    tf32 = tf32_gemm_peak(f"cuda:{local}")
+    achieved = f_tensor / (t_tensor / 1e3) / 1e12 if t_tensor else 0.0
+    out["roofline"] = {"bound": "tensor", "kernel": "CONV/FC implicit-GEMM tcgen05 kind::tf32 (fwd+wgrad+dgrad)",
+                       "achieved": round(achieved, 2), "peak": round(tf32, 2), "unit": "TFLOP/s",
+                       "frac": round(achieved / tf32, 4) if tf32 else None,
+                       "peak_source": "cuBLAS tf32 GEMM 8192^3 measured in this run (MEASURED_PEAKS.json has bf16 "
+                                      f"only: {peaks.get('bf16_tflops')} TF/s burst)",
+                       "traffic": None, "algorithmic_tflop_per_step": round(f_tensor / 1e12, 4),
+                       "share_of_step": round(t_tensor / sum(p[0] for p in prof), 4)}
+    out["time_by_layer_kind_ms"] = {k: round(v, 3) for k, v in sorted(by_kind.items(), key=lambda kv: -kv[1])}
+    # unconstrained reference run: all features off, pool = whole-iteration residency
+    try:
+        base_pool = ex.report.baseline_peak_bytes + (256 << 20)
+        ucfg = sn.SimConfig(pool_bytes=base_pool, features=sn.Features(), cost=cfg.cost)
+        uex = Executor(net, ucfg, device=local, seed=2)
+        uex.set_inputs(*_inputs(net, args.batch))
+        for _ in range(3):
+            uex.step()
+        ums = []
+        for _ in range(5):
+            ums.append(uex.step()[1].step_ms)
+        uex.close()
+        u = statistics.median(ums)
+        out["unconstrained"] = {"features": "none", "pool_bytes": base_pool, "ms_per_step": round(u, 4),
+                                "overhead_of_memory_schedule": round(ms_per_step / u - 1.0, 4)}
+    except Exception as exc:  # report, never hide
+        out["unconstrained"] = {"error": str(exc)[:200]}
+    out["cpu_baseline"] = cpu_baseline(net, sample=4)
+    return out
+
+
+def _inputs(net, B):
+    import torch
+    import paper_1801_04380_b200 as sn
+    c, h, w = sn.propagate_shapes(net)[net.data_id]
+    n_cls = math.prod(sn.propagate_shapes(net)[net.terminal_id])
+    g = torch.Generator().manual_seed(1000)
+    return torch.randn(B, c, h, w, generator=g), torch.randint(0, n_cls, (B,), generator=g)
+
+
+def cpu_baseline(net, sample: int) -> dict:
+    """The CPU restatement (oracle/numerics.py) timed on the host cores."""
+    import torch
+    from paper_1801_04380_b200.training import init_parameters
+    from oracle.numerics import forward_backward
+    threads = len(os.sched_getaffinity(0))
+    torch.set_num_threads(threads)
+    params = init_parameters(net, seed=2)
+    images, labels = _inputs(net, sample)
+    forward_backward(net, params, images, labels)  # warm
+    t0 = time.perf_counter()
+    reps = 0
+    while reps < 2 or time.perf_counter() - t0 < 5.0:
+        forward_backward(net, params, images, labels)
+        reps += 1
+        if time.perf_counter() - t0 > 25.0:
+            break
+    dt = (time.perf_counter() - t0) / reps
+    return {"value": round(sample / dt, 3), "unit": "images/s", "cores": threads, "kind": "port",
+            "sample": f"{reps} fp32 fwd+bwd passes of {sample} images ({net.name}), torch CPU restatement "
+                      "(oracle/numerics.py)"}
+
+
+def run_reference(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import torch
+    from paper_1801_04380_b200.training import init_parameters
+    from oracle.numerics import forward_backward, sgd_step
+    net = build_net(args.net)
+    threads = len(os.sched_getaffinity(0))
+    torch.set_num_threads(threads)
+    sample = 4
+    params = init_parameters(net, seed=2)
+    images, labels = _inputs(net, sample)
+    for _ in range(max(1, min(args.warmup, 2))):
+        forward_backward(net, params, images, labels)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        _, grads = forward_backward(net, params, images, labels)
+        params = sgd_step(params, grads, 0.01)
+    dt = time.perf_counter() - t0
+    value = sample * args.steps / dt
+    print(json.dumps({
+        "impl": "reference", "metric": "images/sec under memory budget (ResNet-50g b256/GPU, 24 GiB pool, "
+        "all SuperNeurons features)", "value": round(value, 3), "unit": "images/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
+        "data": "synthetic", "config": {"workload": f"{args.net} fwd+bwd+SGD, bounded sample of {sample} images "
+                                                    "per step (the b256 workload at CPU scale)",
+                                        "model": args.net, "parallelism": "cpu"},
+        "cpu_baseline": {"value": round(value, 3), "unit": "images/s", "cores": threads, "kind": "port",
+                         "sample": f"{sample} images/step, torch CPU restatement oracle/numerics.py; the reference "
+                                   "memsched package is a simulator with no tensor numerics"},
+        "e2e": {"value": round(value, 3), "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main() -> None:
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

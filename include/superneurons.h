@@ -215,6 +215,10 @@ typedef struct sn_step_timing {
 
 typedef struct sn_exec sn_exec;
 
+/* Executor errors (thread-local, separate from the planner's). */
+const char* sn_exec_last_error(void);
+int sn_exec_last_error_kind(void);
+
 int sn_exec_create(const sn_plan* plan, const sn_net_desc* net, const sn_layer_numerics* numerics,
                    const sn_exec_options* opts, sn_exec** out);
 void sn_exec_destroy(sn_exec* ex);
@@ -234,6 +238,11 @@ int sn_exec_step_host(sn_exec* ex, const float* images_host, const int32_t* labe
 /* Copy a layer's current forward output (if resident in the arena) or its
  * gradient buffer to device memory `dst`; used by parity tests. */
 int sn_exec_read_tensor(sn_exec* ex, int32_t kind, int32_t layer, float* dst, int64_t n_floats);
+/* Run one iteration eagerly with a CUDA event between consecutive actions on
+ * the compute stream; per action: device ms, layer id (-1 none) and type
+ * (0 forward, 1 replay, 2 backward, 3 copy/sync).  For roofline accounting. */
+int sn_exec_profile(sn_exec* ex, float* action_ms, int32_t* action_layer, int32_t* action_type, size_t cap,
+                    size_t* n);
 /* Launch the SGD update alone (after an external gradient all-reduce). */
 int sn_exec_apply_update(sn_exec* ex, float lr, float grad_scale);
 /* Stream the executor launches on (for cross-library ordering). */

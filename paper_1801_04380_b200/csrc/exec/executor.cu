@@ -1,0 +1,893 @@
+// The B200 executor: replays a plan's event tape on one device.
+//
+//  * One cudaMalloc'd arena of the planner's pool capacity; a tensor lives at
+//    base + block_offset * 1024 exactly where the planner's BlockPool put it.
+//    The executor itself never allocates during a step.
+//  * Three streams: compute (S0), copy-out D2H (S1), fetch H2D (S2).  Copies
+//    are ordered against compute with events derived statically from the tape:
+//      - a copy-out waits for its producer; a freed region whose copy-out may
+//        still be reading it is not rewritten before that copy completes;
+//      - a fetch waits for every earlier compute on the stream (previous
+//        occupants' readers) and for the tensor's own copy-out; the first
+//        kernel that reads a fetched tensor waits for the fetch.
+//  * The whole iteration (all three streams) is captured once into a CUDA
+//    graph, legal because the tape is iteration-invariant.
+//  * Gradient buffers follow the planner's windows; the first write into a
+//    freshly allocated buffer overwrites, later writes accumulate.
+//  * Optional plan-driven backup elision: a copy-out whose tensor the tape
+//    never fetches back is not issued (residency/offsets are unchanged).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../kernels/kernels.hpp"
+#include "../planner/handle.hpp"
+#include "superneurons.h"
+
+namespace {
+
+using snp::Net;
+thread_local std::string g_xerr;
+thread_local int g_xerr_kind = SN_EK_NONE;
+
+struct ExecError {
+  int kind;
+  std::string msg;
+};
+[[noreturn]] void xfail(int kind, const std::string& msg) { throw ExecError{kind, msg}; }
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) xfail(SN_EK_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+int xset(int kind, const std::string& msg) {
+  g_xerr = msg;
+  g_xerr_kind = kind;
+  return kind == SN_EK_CUDA ? SN_ERR_CUDA : SN_ERR_OTHER;
+}
+
+constexpr int64_t kAlignFloats = 64;  // 256 B parameter slice alignment
+int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+
+struct LayerRt {
+  int kind = 0;
+  int C = 1, H = 1, W = 1;   // output per sample (stored channels for DATA)
+  int64_t per_sample = 0;    // output elements per sample (stored)
+  int64_t w_off = -1, w_n = 0, b_off = -1, b_n = 0;
+  int64_t state_off = -1;    // BN: stats[2C] then running[2C]
+  sn_layer_numerics num{};
+  sn::ConvShape conv{};
+  sn::PoolShape pool{};
+  int fc_in = 0, fc_splits = 1, wgrad_splits = 1;
+};
+
+struct Action {
+  std::function<void()> fn;
+  int kernels = 0;
+  int layer = -1;
+  int type = 3;  // 0 forward, 1 replay, 2 backward, 3 copy / sync / other
+};
+
+}  // namespace
+
+struct sn_exec {
+  const sn_plan* plan = nullptr;
+  const Net* net = nullptr;
+  int B = 0;
+  int device = 0;
+  sn_exec_options opt{};
+  std::vector<LayerRt> L;
+  int terminal = -1;
+  // device memory
+  char* arena = nullptr;
+  int64_t arena_bytes = 0;
+  float* params = nullptr;
+  float* grads = nullptr;
+  int64_t n_params = 0;
+  float* state = nullptr;
+  int64_t n_state = 0;
+  float* images = nullptr;
+  int64_t image_floats = 0;
+  int32_t* labels = nullptr;
+  float* loss_rows = nullptr;
+  float* loss = nullptr;
+  uint32_t* iteration = nullptr;
+  float* wt_scratch = nullptr;
+  float* partial = nullptr;
+  int64_t partial_cap = 0;
+  float* red = nullptr;
+  const float** ptr_table = nullptr;
+  std::vector<const float*> ptr_host;
+  // host stash
+  std::unordered_map<int, char*> stash;
+  // streams / events
+  cudaStream_t s0 = nullptr, s1 = nullptr, s2 = nullptr;
+  std::vector<cudaEvent_t> events;
+  cudaEvent_t t_begin = nullptr, t_end = nullptr;
+  // compiled program
+  std::vector<Action> prog;
+  int64_t kernels_per_step = 0;
+  int64_t d2h_bytes = 0, h2d_bytes = 0;
+  std::unordered_map<int64_t, std::pair<int64_t, int64_t>> final_keys;  // key -> (off, blocks) at tape end
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  bool graph_ready = false;
+
+  cudaEvent_t new_event() {
+    cudaEvent_t e;
+    ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+    events.push_back(e);
+    return e;
+  }
+};
+
+namespace {
+
+int64_t key_code(int kind, int64_t id) { return snp::key_code(kind, id); }
+
+void setup_layers(sn_exec* ex, const sn_layer_numerics* numerics) {
+  const snp::Plan& P = ex->plan->plan;
+  const Net& net = P.net;
+  const int n = net.n;
+  ex->L.assign(n, LayerRt{});
+  ex->terminal = net.terminal_id();
+  if (net.kind[ex->terminal] != snp::SOFTMAX)
+    xfail(SN_EK_UNSUPPORTED, "numeric execution needs a SOFTMAX terminal (cross-entropy loss)");
+  // DATA is stored with channels padded to 4 when only CONVs read it, so the
+  // stem convolution keeps 16-byte aligned cp.async gathers.
+  int64_t poff = 0, soff = 0;
+  for (int i = 0; i < n; ++i) {
+    LayerRt& l = ex->L[i];
+    l.kind = net.kind[i];
+    if (numerics) l.num = numerics[i];
+    const auto& shp = P.costs[i].shape;
+    if (shp.size() == 3) {
+      l.C = static_cast<int>(shp[0]);
+      l.H = static_cast<int>(shp[1]);
+      l.W = static_cast<int>(shp[2]);
+    } else {
+      l.C = static_cast<int>(shp[0]);
+      l.H = l.W = 1;
+    }
+    if (l.kind == snp::DATA && l.C % 4 != 0) {
+      bool only_conv = true;
+      for (int nx : net.next[i]) only_conv &= net.kind[nx] == snp::CONV;
+      if (only_conv) l.C = (l.C + 3) / 4 * 4;
+    }
+    l.per_sample = static_cast<int64_t>(l.C) * l.H * l.W;
+    if (static_cast<int64_t>(ex->B) * l.per_sample >= (1ll << 31))
+      xfail(SN_EK_UNSUPPORTED, "tensor of layer '" + net.names[i] + "' exceeds 2^31 elements");
+  }
+  for (int i = 0; i < n; ++i) {
+    LayerRt& l = ex->L[i];
+    const int k = l.kind;
+    if (snp::is_inplace(k)) {
+      const int p = net.prev[i][0];
+      if (net.next[p].size() != 1)
+        xfail(SN_EK_UNSUPPORTED, "in-place gradient of '" + net.names[i] + "' aliases a fork at '" + net.names[p] +
+                                     "' (other consumers' gradients would be overwritten)");
+    }
+    if (k == snp::SOFTMAX && i != ex->terminal)
+      xfail(SN_EK_UNSUPPORTED, "SOFTMAX is only supported as the terminal layer");
+    if (k == snp::CONV || k == snp::POOL) {
+      const LayerRt& in = ex->L[net.prev[i][0]];
+      const int K = static_cast<int>(net.pint[i][SN_P_K]);
+      const int s = net.pstate[i][SN_P_S] == 1 ? static_cast<int>(net.pint[i][SN_P_S]) : (k == snp::CONV ? 1 : K);
+      const int pd = net.pstate[i][SN_P_P] == 1 ? static_cast<int>(net.pint[i][SN_P_P]) : 0;
+      if (s < 1 || pd < 0) xfail(SN_EK_UNSUPPORTED, "non-positive stride / negative pad in '" + net.names[i] + "'");
+      if (k == snp::CONV) {
+        l.conv = sn::ConvShape{ex->B, in.H, in.W, in.C, l.C, K, K, l.H, l.W, s, pd};
+        l.w_off = poff;
+        l.w_n = static_cast<int64_t>(l.C) * K * K * in.C;
+        poff = align_up(poff + l.w_n, kAlignFloats);
+        l.b_off = poff;
+        l.b_n = l.C;
+        poff = align_up(poff + l.b_n, kAlignFloats);
+      } else {
+        l.pool = sn::PoolShape{ex->B, in.H, in.W, in.C, l.H, l.W, K, s, pd, l.num.pool_mode};
+      }
+    } else if (k == snp::FC) {
+      const LayerRt& in = ex->L[net.prev[i][0]];
+      l.fc_in = static_cast<int>(in.per_sample);
+      l.w_off = poff;
+      l.w_n = static_cast<int64_t>(l.C) * l.fc_in;
+      poff = align_up(poff + l.w_n, kAlignFloats);
+      l.b_off = poff;
+      l.b_n = l.C;
+      poff = align_up(poff + l.b_n, kAlignFloats);
+    } else if (k == snp::BN) {
+      l.w_off = poff;  // gamma
+      l.w_n = l.C;
+      poff = align_up(poff + l.w_n, kAlignFloats);
+      l.b_off = poff;  // beta
+      l.b_n = l.C;
+      poff = align_up(poff + l.b_n, kAlignFloats);
+      l.state_off = soff;
+      soff = align_up(soff + 4 * static_cast<int64_t>(l.C), kAlignFloats);
+    }
+  }
+  ex->n_params = std::max<int64_t>(poff, kAlignFloats);
+  ex->n_state = std::max<int64_t>(soff, kAlignFloats);
+}
+
+void alloc_device(sn_exec* ex) {
+  const snp::Plan& P = ex->plan->plan;
+  const Net& net = P.net;
+  ex->arena_bytes = P.pool_capacity_blocks * snp::kBlockBytes;
+  ck(cudaMalloc(&ex->arena, static_cast<size_t>(ex->arena_bytes)), "cudaMalloc(arena)");
+  ck(cudaMalloc(&ex->params, ex->n_params * sizeof(float)), "cudaMalloc(params)");
+  ck(cudaMalloc(&ex->grads, ex->n_params * sizeof(float)), "cudaMalloc(grads)");
+  ck(cudaMemset(ex->grads, 0, ex->n_params * sizeof(float)), "memset");
+  ck(cudaMalloc(&ex->state, ex->n_state * sizeof(float)), "cudaMalloc(state)");
+  // BN state: stats {mean 0, invstd 1}, running {mean 0, var 1}
+  std::vector<float> st(ex->n_state, 0.f);
+  int64_t wt = 0, red = sn::red_scratch_floats(4), partial = 0;
+  for (int i = 0; i < net.n; ++i) {
+    LayerRt& l = ex->L[i];
+    if (l.kind == snp::BN) {
+      for (int c = 0; c < l.C; ++c) {
+        st[l.state_off + l.C + c] = 1.f;
+        st[l.state_off + 3 * l.C + c] = 1.f;
+      }
+    }
+    if (l.kind == snp::BN || l.kind == snp::CONV || l.kind == snp::FC)
+      red = std::max(red, sn::red_scratch_floats(l.C));
+    if (l.kind == snp::CONV) wt = std::max(wt, l.w_n);
+  }
+  ck(cudaMemcpy(ex->state, st.data(), st.size() * sizeof(float), cudaMemcpyHostToDevice), "memcpy(state)");
+  // split-K partial scratch (outside the arena, like cuDNN's internal buffers):
+  // sized by the largest layer at its chosen split count, capped at 64 Mi floats.
+  const int64_t cap = 64ll << 20;
+  for (int i = 0; i < net.n; ++i) {
+    LayerRt& l = ex->L[i];
+    if (l.kind == snp::CONV) {
+      l.wgrad_splits = sn::conv_wgrad_splits(l.conv, cap);
+      partial = std::max(partial, static_cast<int64_t>(l.wgrad_splits) * l.conv.R * l.conv.S * l.conv.C * l.conv.K);
+    } else if (l.kind == snp::FC) {
+      l.fc_splits = sn::fc_splits(ex->B, l.fc_in, l.C, cap);
+      partial = std::max(partial, static_cast<int64_t>(l.fc_splits) * ex->B * std::max(l.fc_in, l.C));
+    }
+  }
+  ex->partial_cap = std::max<int64_t>(partial, 64);
+  ck(cudaMalloc(&ex->partial, ex->partial_cap * sizeof(float)), "cudaMalloc(partial)");
+  ck(cudaMalloc(&ex->wt_scratch, std::max<int64_t>(wt, 64) * sizeof(float)), "cudaMalloc(wt)");
+  ck(cudaMalloc(&ex->red, red * sizeof(float)), "cudaMalloc(red)");
+  int data_id = 0;
+  for (int i = 0; i < net.n; ++i)
+    if (net.kind[i] == snp::DATA) data_id = i;
+  const LayerRt& data = ex->L[data_id];
+  ex->image_floats = static_cast<int64_t>(ex->B) * data.per_sample;
+  ck(cudaMalloc(&ex->images, ex->image_floats * sizeof(float)), "cudaMalloc(images)");
+  ck(cudaMemset(ex->images, 0, ex->image_floats * sizeof(float)), "memset(images)");
+  ck(cudaMalloc(&ex->labels, ex->B * sizeof(int32_t)), "cudaMalloc(labels)");
+  ck(cudaMemset(ex->labels, 0, ex->B * sizeof(int32_t)), "memset(labels)");
+  ck(cudaMalloc(&ex->loss_rows, ex->B * sizeof(float)), "cudaMalloc(loss_rows)");
+  ck(cudaMalloc(&ex->loss, 4 * sizeof(float)), "cudaMalloc(loss)");
+  ck(cudaMalloc(&ex->iteration, sizeof(uint32_t) * 4), "cudaMalloc(iteration)");
+  ck(cudaMemset(ex->iteration, 0, sizeof(uint32_t) * 4), "memset(iteration)");
+}
+
+// ---------------------------------------------------------------------------
+// Tape compilation.
+
+struct Compiler {
+  sn_exec* ex;
+  const snp::Plan& P;
+  const Net& net;
+  std::unordered_map<int64_t, std::pair<int64_t, int64_t>> where;  // key -> (block off, blocks)
+  std::unordered_map<int, bool> fresh;                             // grad owner -> not yet written
+  std::unordered_map<int, cudaEvent_t> d2h_live;                   // act lid -> copy-out event
+  std::vector<std::pair<std::pair<int64_t, int64_t>, cudaEvent_t>> freed_reading;  // region being read by D2H
+  std::unordered_map<int, cudaEvent_t> h2d_live;                   // act lid -> fetch event (not yet waited)
+  std::vector<char> fetched;                                       // lids fetched anywhere in the tape
+  bool used_s1 = false, used_s2 = false;
+  int data_id = -1;
+
+  Compiler(sn_exec* e) : ex(e), P(e->plan->plan), net(e->plan->plan.net) {
+    fetched.assign(net.n, 0);
+    for (const auto& ev : P.tape)
+      if (ev.op == 'P' || ev.op == 'D') fetched[ev.b] = 1;
+    for (int i = 0; i < net.n; ++i)
+      if (net.kind[i] == snp::DATA) data_id = i;
+  }
+
+  int cur_layer = -1, cur_type = 3;
+  void push(std::function<void()> fn, int kernels) {
+    ex->prog.push_back(Action{std::move(fn), kernels, kernels ? cur_layer : -1, kernels ? cur_type : 3});
+  }
+
+  float* ptr(int kind, int id) {
+    if (kind == snp::K_ACT && id == data_id) return ex->images;
+    auto it = where.find(key_code(kind, id));
+    if (it == where.end())
+      xfail(SN_EK_INTERNAL, std::string("tape references non-resident ") + (kind == 0 ? "act " : kind == 1 ? "grad " : "ws ") +
+                                std::to_string(id));
+    return reinterpret_cast<float*>(ex->arena + it->second.first * snp::kBlockBytes);
+  }
+
+  void s0_wait(cudaEvent_t e) {
+    cudaStream_t s0 = ex->s0;
+    push([s0, e] { ck(cudaStreamWaitEvent(s0, e, 0), "wait"); }, 0);
+  }
+
+  void wait_fetch(int lid) {
+    auto it = h2d_live.find(lid);
+    if (it != h2d_live.end()) {
+      s0_wait(it->second);
+      h2d_live.erase(it);
+    }
+  }
+
+  static bool overlap(int64_t a0, int64_t an, int64_t b0, int64_t bn) { return a0 < b0 + bn && b0 < a0 + an; }
+
+  void on_alloc(const snp::Event& e) {
+    const int64_t key = key_code(e.a, e.b);
+    where[key] = {e.c, e.d};
+    if (e.a == snp::K_GRAD) fresh[e.b] = true;
+    for (size_t i = 0; i < freed_reading.size();) {
+      if (overlap(e.c, e.d, freed_reading[i].first.first, freed_reading[i].first.second)) {
+        s0_wait(freed_reading[i].second);
+        freed_reading.erase(freed_reading.begin() + i);
+      } else {
+        ++i;
+      }
+    }
+  }
+
+  void on_free(const snp::Event& e) {
+    const int64_t key = key_code(e.a, e.b);
+    auto it = where.find(key);
+    if (it == where.end()) xfail(SN_EK_INTERNAL, "tape frees an unknown key");
+    if (e.a == snp::K_ACT) {
+      auto d = d2h_live.find(e.b);
+      if (d != d2h_live.end()) {
+        freed_reading.push_back({it->second, d->second});
+        // the stash keeps its copy; further fetches wait on the same event
+      }
+      wait_fetch(e.b);
+    }
+    where.erase(it);
+  }
+
+  void on_copy_out(int lid) {
+    if (ex->opt.elide_backups && !fetched[lid]) return;
+    const int64_t nbytes = P.costs[lid].device_bytes;
+    char* host = ex->stash[lid];
+    if (!host) {
+      ck(cudaHostAlloc(&host, static_cast<size_t>(nbytes), cudaHostAllocPortable), "cudaHostAlloc(stash)");
+      ex->stash[lid] = host;
+    }
+    const float* src = ptr(snp::K_ACT, lid);
+    cudaEvent_t prod = ex->new_event(), done = ex->new_event();
+    cudaStream_t s0 = ex->s0, s1 = ex->s1;
+    push([=] {
+      ck(cudaEventRecord(prod, s0), "record");
+      ck(cudaStreamWaitEvent(s1, prod, 0), "wait");
+      ck(cudaMemcpyAsync(host, src, static_cast<size_t>(nbytes), cudaMemcpyDeviceToHost, s1), "D2H");
+      ck(cudaEventRecord(done, s1), "record");
+    }, 0);
+    d2h_live[lid] = done;
+    ex->d2h_bytes += nbytes;
+    used_s1 = true;
+  }
+
+  void on_fetch(int lid) {
+    const int64_t nbytes = P.costs[lid].device_bytes;
+    auto d = d2h_live.find(lid);
+    if (d == d2h_live.end()) xfail(SN_EK_INTERNAL, "fetch of a tensor that was never copied out");
+    char* host = ex->stash[lid];
+    float* dst = ptr(snp::K_ACT, lid);
+    cudaEvent_t before = ex->new_event(), done = ex->new_event(), out = d->second;
+    cudaStream_t s0 = ex->s0, s2 = ex->s2;
+    push([=] {
+      ck(cudaEventRecord(before, s0), "record");
+      ck(cudaStreamWaitEvent(s2, before, 0), "wait");
+      ck(cudaStreamWaitEvent(s2, out, 0), "wait");
+      ck(cudaMemcpyAsync(dst, host, static_cast<size_t>(nbytes), cudaMemcpyHostToDevice, s2), "H2D");
+      ck(cudaEventRecord(done, s2), "record");
+    }, 0);
+    h2d_live[lid] = done;
+    ex->h2d_bytes += nbytes;
+    used_s2 = true;
+  }
+
+  // ---- layer kernels ----
+  void forward(int lid, bool replay) {
+    const LayerRt& l = ex->L[lid];
+    for (int p : net.prev[lid]) wait_fetch(p);
+    float* y = ptr(snp::K_ACT, lid);
+    const float* x = net.prev[lid].empty() ? nullptr : ptr(snp::K_ACT, net.prev[lid][0]);
+    const int64_t n = static_cast<int64_t>(ex->B) * l.per_sample;
+    cudaStream_t st = ex->s0;
+    sn_exec* e = ex;
+    switch (l.kind) {
+      case snp::CONV: {
+        const float* w = ex->params + l.w_off;
+        const float* b = ex->params + l.b_off;
+        const sn::ConvShape cs = l.conv;
+        push([=] { ck(sn::conv_fwd(cs, x, w, b, y, st), "conv_fwd"); }, 1);
+        break;
+      }
+      case snp::FC: {
+        const float* w = ex->params + l.w_off;
+        const float* b = ex->params + l.b_off;
+        const int B = ex->B, I = l.fc_in, O = l.C, sp = l.fc_splits;
+        float* part = ex->partial;
+        push([=] { ck(sn::fc_fwd(B, I, O, x, w, b, y, part, sp, st), "fc_fwd"); }, 2);
+        break;
+      }
+      case snp::BN: {
+        const float* g = ex->params + l.w_off;
+        const float* b = ex->params + l.b_off;
+        float* stats = ex->state + l.state_off;
+        float* running = replay ? nullptr : ex->state + l.state_off + 2 * l.C;
+        const int64_t rows = static_cast<int64_t>(ex->B) * l.H * l.W;
+        const int C = l.C;
+        const float eps = l.num.bn_eps, mom = l.num.bn_momentum;
+        const int compute = replay ? 0 : 1;
+        float* red = ex->red;
+        push([=] { ck(sn::bn_fwd(x, rows, C, g, b, y, stats, running, eps, mom, compute, red, st), "bn_fwd"); },
+             replay ? 1 : 4);
+        break;
+      }
+      case snp::ACT:
+        push([=] { ck(sn::relu_fwd(x, y, n, st), "relu_fwd"); }, 1);
+        break;
+      case snp::POOL: {
+        const sn::PoolShape ps = l.pool;
+        push([=] { ck(sn::pool_fwd(ps, x, y, st), "pool_fwd"); }, 1);
+        break;
+      }
+      case snp::LRN: {
+        const int64_t pix = static_cast<int64_t>(ex->B) * l.H * l.W;
+        const sn_layer_numerics nm = l.num;
+        const int C = l.C;
+        push([=] { ck(sn::lrn_fwd(x, y, pix, C, nm.lrn_size, nm.lrn_alpha, nm.lrn_beta, nm.lrn_k, st), "lrn_fwd"); }, 1);
+        break;
+      }
+      case snp::DROPOUT: {
+        const float rate = l.num.dropout_rate;
+        const uint64_t seed = ex->opt.seed;
+        push([=] { ck(sn::dropout_fwd(x, y, n, rate, seed, lid, e->iteration, st), "dropout_fwd"); }, 1);
+        break;
+      }
+      case snp::SOFTMAX: {
+        const int B = ex->B, F = static_cast<int>(l.per_sample);
+        float* rows = replay ? nullptr : ex->loss_rows;
+        const int32_t* lab = ex->labels;
+        float* loss = ex->loss;
+        push([=] {
+          ck(sn::softmax_fwd(x, y, B, F, lab, rows, st), "softmax_fwd");
+          if (rows) ck(sn::loss_reduce(rows, B, loss, st), "loss_reduce");
+        }, replay ? 1 : 2);
+        break;
+      }
+      case snp::JOIN: {
+        const size_t at = ex->ptr_host.size();
+        for (int p : net.prev[lid]) ex->ptr_host.push_back(ptr(snp::K_ACT, p));
+        const int nin = static_cast<int>(net.prev[lid].size());
+        push([=] { ck(sn::join_fwd(e->ptr_table + at, nin, y, n, st), "join_fwd"); }, 1);
+        break;
+      }
+      default:
+        xfail(SN_EK_UNSUPPORTED, "forward of unsupported layer kind");
+    }
+  }
+
+  // Destination for d(input pid) and whether it is the first write.
+  float* dx_target(int pid, int* accumulate) {
+    const int owner = net.grad_owner(pid);
+    if (owner < 0) return nullptr;
+    float* p = ptr(snp::K_GRAD, owner);
+    auto it = fresh.find(owner);
+    *accumulate = (it != fresh.end() && it->second) ? 0 : 1;
+    fresh[owner] = false;
+    return p;
+  }
+
+  void backward(int lid) {
+    const LayerRt& l = ex->L[lid];
+    for (int r : net.backward_reads_unique(lid)) wait_fetch(r);
+    cudaStream_t st = ex->s0;
+    sn_exec* e = ex;
+    const int64_t n = static_cast<int64_t>(ex->B) * l.per_sample;
+    const int owner = net.grad_owner(lid);
+    float* dy = (owner >= 0 && lid != ex->terminal) ? ptr(snp::K_GRAD, owner) : nullptr;
+    const int pid = net.prev[lid].empty() ? -1 : net.prev[lid][0];
+    switch (l.kind) {
+      case snp::CONV: {
+        const float* x = ptr(snp::K_ACT, pid);
+        const sn::ConvShape cs = l.conv;
+        int acc = 0;
+        float* dx = dx_target(pid, &acc);
+        const float* w = ex->params + l.w_off;
+        float* dw = ex->grads + l.w_off;
+        float* db = ex->grads + l.b_off;
+        float* wt = ex->wt_scratch;
+        float* part = ex->partial;
+        float* red = ex->red;
+        const int sp = l.wgrad_splits;
+        push([=] {
+          ck(sn::conv_wgrad(cs, x, dy, dw, db, part, sp, red, st), "conv_wgrad");
+          if (dx) ck(sn::conv_dgrad(cs, dy, w, wt, dx, acc, st), "conv_dgrad");
+        }, dx ? 7 : 5);
+        break;
+      }
+      case snp::FC: {
+        const float* x = ptr(snp::K_ACT, pid);
+        int acc = 0;
+        float* dx = dx_target(pid, &acc);
+        const int B = ex->B, I = l.fc_in, O = l.C, sp = l.fc_splits;
+        const float* w = ex->params + l.w_off;
+        float* dw = ex->grads + l.w_off;
+        float* db = ex->grads + l.b_off;
+        float* part = ex->partial;
+        float* red = ex->red;
+        push([=] {
+          ck(sn::fc_wgrad(B, I, O, x, dy, dw, db, red, st), "fc_wgrad");
+          if (dx) ck(sn::fc_dgrad(B, I, O, dy, w, dx, acc, part, sp, st), "fc_dgrad");
+        }, dx ? 6 : 4);
+        break;
+      }
+      case snp::BN: {
+        const float* x = ptr(snp::K_ACT, pid);
+        int acc = 0;
+        float* dx = dx_target(pid, &acc);
+        const float* g = ex->params + l.w_off;
+        float* dg = ex->grads + l.w_off;
+        float* dbt = ex->grads + l.b_off;
+        const float* stats = ex->state + l.state_off;
+        const int64_t rows = static_cast<int64_t>(ex->B) * l.H * l.W;
+        const int C = l.C;
+        float* red = ex->red;
+        push([=] { ck(sn::bn_bwd(x, dy, rows, C, g, stats, dx, acc, dg, dbt, red, st), "bn_bwd"); }, dx ? 4 : 3);
+        break;
+      }
+      case snp::ACT: {
+        const float* y = ptr(snp::K_ACT, lid);
+        int acc = 0;
+        float* g = dx_target(pid, &acc);
+        if (g && dy && g != dy) xfail(SN_EK_INTERNAL, "in-place gradient buffer mismatch");
+        if (g) push([=] { ck(sn::relu_bwd_inplace(y, g, n, st), "relu_bwd"); }, 1);
+        break;
+      }
+      case snp::DROPOUT: {
+        int acc = 0;
+        float* g = dx_target(pid, &acc);
+        const float rate = l.num.dropout_rate;
+        const uint64_t seed = ex->opt.seed;
+        if (g) push([=] { ck(sn::dropout_bwd_inplace(g, n, rate, seed, lid, e->iteration, st), "dropout_bwd"); }, 1);
+        break;
+      }
+      case snp::POOL: {
+        const float* x = ptr(snp::K_ACT, pid);
+        const float* y = ptr(snp::K_ACT, lid);
+        int acc = 0;
+        float* dx = dx_target(pid, &acc);
+        const sn::PoolShape ps = l.pool;
+        if (dx) push([=] { ck(sn::pool_bwd(ps, x, y, dy, dx, acc, st), "pool_bwd"); }, 1);
+        break;
+      }
+      case snp::LRN: {
+        const float* x = ptr(snp::K_ACT, pid);
+        const float* y = ptr(snp::K_ACT, lid);
+        int acc = 0;
+        float* dx = dx_target(pid, &acc);
+        const int64_t pix = static_cast<int64_t>(ex->B) * l.H * l.W;
+        const sn_layer_numerics nm = l.num;
+        const int C = l.C;
+        if (dx)
+          push([=] {
+            ck(sn::lrn_bwd(x, y, dy, dx, pix, C, nm.lrn_size, nm.lrn_alpha, nm.lrn_beta, nm.lrn_k, acc, st), "lrn_bwd");
+          }, 1);
+        break;
+      }
+      case snp::SOFTMAX: {
+        const float* y = ptr(snp::K_ACT, lid);
+        int acc = 0;
+        float* dx = dx_target(pid, &acc);
+        const int B = ex->B, F = static_cast<int>(l.per_sample);
+        const int32_t* lab = ex->labels;
+        if (dx) push([=] { ck(sn::softmax_ce_bwd(y, lab, dx, B, F, acc, st), "softmax_bwd"); }, 1);
+        break;
+      }
+      case snp::JOIN: {
+        for (int p : net.prev[lid]) {
+          int acc = 0;
+          float* dx = dx_target(p, &acc);
+          if (dx) push([=] { ck(sn::grad_copy(dy, dx, n, acc, st), "join_bwd"); }, 1);
+        }
+        break;
+      }
+      default:
+        xfail(SN_EK_UNSUPPORTED, "backward of unsupported layer kind");
+    }
+  }
+
+  void compile() {
+    for (const snp::Event& ev : P.tape) {
+      switch (ev.op) {
+        case 'A': on_alloc(ev); break;
+        case 'F': on_free(ev); break;
+        case 'C':
+          cur_layer = ev.b, cur_type = 0;
+          forward(ev.b, false);
+          break;
+        case 'R':
+          cur_layer = ev.b, cur_type = 1;
+          forward(ev.b, true);
+          break;
+        case 'B':
+          cur_layer = ev.b, cur_type = 2;
+          backward(ev.b);
+          break;
+        case 'O': on_copy_out(ev.b); break;
+        case 'P':
+        case 'D': on_fetch(ev.b); break;
+        default: break;  // cache bookkeeping and step markers need no device work
+      }
+    }
+    // Join the copy streams back into the compute stream.
+    cudaStream_t s0 = ex->s0;
+    if (used_s1) {
+      cudaEvent_t j = ex->new_event();
+      cudaStream_t s1 = ex->s1;
+      push([=] {
+        ck(cudaEventRecord(j, s1), "record");
+        ck(cudaStreamWaitEvent(s0, j, 0), "wait");
+      }, 0);
+    }
+    if (used_s2) {
+      cudaEvent_t j = ex->new_event();
+      cudaStream_t s2 = ex->s2;
+      push([=] {
+        ck(cudaEventRecord(j, s2), "record");
+        ck(cudaStreamWaitEvent(s0, j, 0), "wait");
+      }, 0);
+    }
+    uint32_t* it = ex->iteration;
+    push([=] { ck(sn::bump_iteration(it, s0), "bump"); }, 1);
+    ex->final_keys = where;
+    for (const Action& a : ex->prog) ex->kernels_per_step += a.kernels;
+  }
+};
+
+void run_program(sn_exec* ex) {
+  for (const Action& a : ex->prog) a.fn();
+}
+
+void ensure_graph(sn_exec* ex) {
+  if (ex->graph_ready) return;
+  ck(cudaStreamBeginCapture(ex->s0, cudaStreamCaptureModeThreadLocal), "BeginCapture");
+  try {
+    run_program(ex);
+  } catch (...) {
+    cudaGraph_t g;
+    cudaStreamEndCapture(ex->s0, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  ck(cudaStreamEndCapture(ex->s0, &ex->graph), "EndCapture");
+  ck(cudaGraphInstantiate(&ex->gexec, ex->graph, 0), "GraphInstantiate");
+  ex->graph_ready = true;
+}
+
+template <class F>
+int xguard(F&& f) {
+  try {
+    f();
+    g_xerr_kind = SN_EK_NONE;
+    return SN_OK;
+  } catch (const ExecError& e) {
+    return xset(e.kind, e.msg);
+  } catch (const snp::PlanError& e) {
+    return xset(e.kind, e.what());
+  } catch (const std::exception& e) {
+    return xset(SN_EK_INTERNAL, e.what());
+  }
+}
+
+void destroy(sn_exec* ex) {
+  if (!ex) return;
+  if (ex->gexec) cudaGraphExecDestroy(ex->gexec);
+  if (ex->graph) cudaGraphDestroy(ex->graph);
+  for (cudaEvent_t e : ex->events) cudaEventDestroy(e);
+  if (ex->t_begin) cudaEventDestroy(ex->t_begin);
+  if (ex->t_end) cudaEventDestroy(ex->t_end);
+  for (auto& kv : ex->stash)
+    if (kv.second) cudaFreeHost(kv.second);
+  void* bufs[] = {ex->arena, ex->params, ex->grads, ex->state, ex->images, ex->labels, ex->loss_rows, ex->loss,
+                  ex->iteration, ex->wt_scratch, ex->partial, ex->red, const_cast<float**>(ex->ptr_table)};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  if (ex->s0) cudaStreamDestroy(ex->s0);
+  if (ex->s1) cudaStreamDestroy(ex->s1);
+  if (ex->s2) cudaStreamDestroy(ex->s2);
+  delete ex;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sn_exec_last_error(void) { return g_xerr.c_str(); }
+int sn_exec_last_error_kind(void) { return g_xerr_kind; }
+
+int sn_exec_create(const sn_plan* plan, const sn_net_desc* /*net*/, const sn_layer_numerics* numerics,
+                   const sn_exec_options* opts, sn_exec** out) {
+  if (!plan || !opts || !out) return xset(SN_EK_INTERNAL, "null argument");
+  *out = nullptr;
+  sn_exec* ex = new sn_exec;
+  const int rc = xguard([&] {
+    ex->plan = plan;
+    ex->net = &plan->plan.net;
+    ex->opt = *opts;
+    ex->device = opts->device;
+    ex->B = static_cast<int>(plan->plan.cost_cfg.batch);
+    if (plan->plan.cost_cfg.dtype_bytes != 4)
+      xfail(SN_EK_UNSUPPORTED, "the executor computes in fp32: CostConfig.dtype_bytes must be 4");
+    ck(cudaSetDevice(ex->device), "cudaSetDevice");
+    ck(cudaStreamCreateWithFlags(&ex->s0, cudaStreamNonBlocking), "stream");
+    ck(cudaStreamCreateWithFlags(&ex->s1, cudaStreamNonBlocking), "stream");
+    ck(cudaStreamCreateWithFlags(&ex->s2, cudaStreamNonBlocking), "stream");
+    ck(cudaEventCreate(&ex->t_begin), "event");
+    ck(cudaEventCreate(&ex->t_end), "event");
+    setup_layers(ex, numerics);
+    alloc_device(ex);
+    Compiler comp(ex);
+    comp.compile();
+    const size_t nptr = std::max<size_t>(1, ex->ptr_host.size());
+    ck(cudaMalloc(&ex->ptr_table, nptr * sizeof(float*)), "cudaMalloc(ptr_table)");
+    if (!ex->ptr_host.empty())
+      ck(cudaMemcpy(ex->ptr_table, ex->ptr_host.data(), ex->ptr_host.size() * sizeof(float*), cudaMemcpyHostToDevice),
+         "memcpy(ptr_table)");
+    ck(cudaDeviceSynchronize(), "sync");
+  });
+  if (rc != SN_OK) {
+    destroy(ex);
+    return rc;
+  }
+  *out = ex;
+  return SN_OK;
+}
+
+void sn_exec_destroy(sn_exec* ex) { destroy(ex); }
+
+int sn_exec_params(sn_exec* ex, float** params, float** grads, int64_t* n_floats) {
+  if (!ex) return xset(SN_EK_INTERNAL, "null argument");
+  if (params) *params = ex->params;
+  if (grads) *grads = ex->grads;
+  if (n_floats) *n_floats = ex->n_params;
+  return SN_OK;
+}
+
+int sn_exec_param_slice(sn_exec* ex, int32_t layer, int64_t* w_off, int64_t* w_n, int64_t* b_off, int64_t* b_n) {
+  if (!ex || layer < 0 || layer >= static_cast<int>(ex->L.size())) return xset(SN_EK_INTERNAL, "bad layer");
+  const LayerRt& l = ex->L[layer];
+  if (w_off) *w_off = l.w_off;
+  if (w_n) *w_n = l.w_n;
+  if (b_off) *b_off = l.b_off;
+  if (b_n) *b_n = l.b_n;
+  return SN_OK;
+}
+
+int sn_exec_inputs(sn_exec* ex, float** images, int32_t** labels, int64_t* image_floats) {
+  if (!ex) return xset(SN_EK_INTERNAL, "null argument");
+  if (images) *images = ex->images;
+  if (labels) *labels = ex->labels;
+  if (image_floats) *image_floats = ex->image_floats;
+  return SN_OK;
+}
+
+void* sn_exec_stream(sn_exec* ex) { return ex ? ex->s0 : nullptr; }
+
+int sn_exec_step(sn_exec* ex, int32_t update, float* loss_host, sn_step_timing* timing) {
+  if (!ex) return xset(SN_EK_INTERNAL, "null argument");
+  return xguard([&] {
+    ck(cudaSetDevice(ex->device), "cudaSetDevice");
+    if (ex->opt.use_graph) ensure_graph(ex);
+    ck(cudaEventRecord(ex->t_begin, ex->s0), "record");
+    if (ex->opt.use_graph)
+      ck(cudaGraphLaunch(ex->gexec, ex->s0), "GraphLaunch");
+    else
+      run_program(ex);
+    if (update) ck(sn::sgd_update(ex->params, ex->grads, ex->n_params, ex->opt.lr, ex->opt.grad_scale, ex->s0), "sgd");
+    ck(cudaEventRecord(ex->t_end, ex->s0), "record");
+    if (loss_host) ck(cudaMemcpyAsync(loss_host, ex->loss, sizeof(float), cudaMemcpyDeviceToHost, ex->s0), "loss D2H");
+    ck(cudaStreamSynchronize(ex->s0), "sync");
+    if (timing) {
+      float ms = 0.f;
+      ck(cudaEventElapsedTime(&ms, ex->t_begin, ex->t_end), "elapsed");
+      timing->step_ms = ms;
+      timing->h2d_ms = timing->d2h_ms = 0.f;
+      timing->kernels = ex->kernels_per_step + (update ? 1 : 0);
+      timing->d2h_bytes = ex->d2h_bytes;
+      timing->h2d_bytes = ex->h2d_bytes;
+      timing->arena_high_water = ex->plan->plan.report.pool_high_water_bytes;
+    }
+  });
+}
+
+int sn_exec_step_host(sn_exec* ex, const float* images_host, const int32_t* labels_host, int32_t update,
+                      float* loss_host, sn_step_timing* timing) {
+  if (!ex) return xset(SN_EK_INTERNAL, "null argument");
+  const int rc = xguard([&] {
+    ck(cudaSetDevice(ex->device), "cudaSetDevice");
+    if (ex->opt.use_graph) ensure_graph(ex);
+    ck(cudaEventRecord(ex->t_begin, ex->s0), "record");
+    ck(cudaMemcpyAsync(ex->images, images_host, ex->image_floats * sizeof(float), cudaMemcpyHostToDevice, ex->s0),
+       "images H2D");
+    ck(cudaMemcpyAsync(ex->labels, labels_host, ex->B * sizeof(int32_t), cudaMemcpyHostToDevice, ex->s0),
+       "labels H2D");
+    if (ex->opt.use_graph)
+      ck(cudaGraphLaunch(ex->gexec, ex->s0), "GraphLaunch");
+    else
+      run_program(ex);
+    if (update) ck(sn::sgd_update(ex->params, ex->grads, ex->n_params, ex->opt.lr, ex->opt.grad_scale, ex->s0), "sgd");
+    ck(cudaMemcpyAsync(loss_host, ex->loss, sizeof(float), cudaMemcpyDeviceToHost, ex->s0), "loss D2H");
+    ck(cudaEventRecord(ex->t_end, ex->s0), "record");
+    ck(cudaStreamSynchronize(ex->s0), "sync");
+    if (timing) {
+      float ms = 0.f;
+      ck(cudaEventElapsedTime(&ms, ex->t_begin, ex->t_end), "elapsed");
+      timing->step_ms = ms;
+      timing->kernels = ex->kernels_per_step + (update ? 1 : 0);
+      timing->d2h_bytes = ex->d2h_bytes;
+      timing->h2d_bytes = ex->h2d_bytes;
+      timing->arena_high_water = ex->plan->plan.report.pool_high_water_bytes;
+    }
+  });
+  return rc;
+}
+
+int sn_exec_profile(sn_exec* ex, float* action_ms, int32_t* action_layer, int32_t* action_type, size_t cap,
+                    size_t* n) {
+  if (!ex || !n) return xset(SN_EK_INTERNAL, "null argument");
+  *n = ex->prog.size();
+  if (!action_ms) return SN_OK;
+  if (cap < ex->prog.size()) return xset(SN_EK_INTERNAL, "output buffer too small");
+  return xguard([&] {
+    ck(cudaSetDevice(ex->device), "cudaSetDevice");
+    std::vector<cudaEvent_t> ev(ex->prog.size() + 1);
+    for (auto& e : ev) ck(cudaEventCreate(&e), "event");
+    ck(cudaEventRecord(ev[0], ex->s0), "record");
+    for (size_t i = 0; i < ex->prog.size(); ++i) {
+      ex->prog[i].fn();
+      ck(cudaEventRecord(ev[i + 1], ex->s0), "record");
+    }
+    ck(cudaStreamSynchronize(ex->s0), "sync");
+    for (size_t i = 0; i < ex->prog.size(); ++i) {
+      float ms = 0.f;
+      ck(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]), "elapsed");
+      action_ms[i] = ms;
+      if (action_layer) action_layer[i] = ex->prog[i].layer;
+      if (action_type) action_type[i] = ex->prog[i].type;
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+  });
+}
+
+int sn_exec_apply_update(sn_exec* ex, float lr, float grad_scale) {
+  if (!ex) return xset(SN_EK_INTERNAL, "null argument");
+  return xguard([&] {
+    ck(sn::sgd_update(ex->params, ex->grads, ex->n_params, lr, grad_scale, ex->s0), "sgd");
+    ck(cudaStreamSynchronize(ex->s0), "sync");
+  });
+}
+
+int sn_exec_read_tensor(sn_exec* ex, int32_t kind, int32_t layer, float* dst, int64_t n_floats) {
+  if (!ex) return xset(SN_EK_INTERNAL, "null argument");
+  return xguard([&] {
+    auto it = ex->final_keys.find(snp::key_code(kind, layer));
+    if (it == ex->final_keys.end()) xfail(SN_EK_INTERNAL, "tensor is not resident at the end of the iteration");
+    const float* src = reinterpret_cast<const float*>(ex->arena + it->second.first * snp::kBlockBytes);
+    ck(cudaMemcpy(dst, src, static_cast<size_t>(n_floats) * sizeof(float), cudaMemcpyDeviceToDevice), "read");
+  });
+}
+
+}  // extern "C"

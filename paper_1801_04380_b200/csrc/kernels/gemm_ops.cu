@@ -1,0 +1,535 @@
+// CONV and FC as tcgen05 GEMMs (gemm_tc.cuh) with implicit-GEMM operand
+// gathers straight from the NHWC activations in the arena:
+//
+//   forward  D[npq][k]  = sum_{rsc} im2col(x)[npq][rsc] * w[k][rsc]      A K-major, B K-major
+//   dgrad    D[nhw][c]  = sum_{rsk} dy[n, (h+pad-r)/st, (w+pad-s)/st, k]
+//                                   * wt[c][rsk]                         A K-major, B K-major
+//   wgrad    D[rsc][k]  = sum_{npq} im2col(x)[npq][rsc] * dy[npq][k]     A MN-major, B MN-major
+//
+// Padding, stride holes and tile overhang are zero-filled by cp.async with
+// src-size 0, so no im2col buffer is ever materialised.  The wgrad reduction
+// over N*P*Q is split across CTAs (split-K) into fp32 partials reduced in a
+// fixed order by splitk_reduce (deterministic: the same split count gives
+// bit-identical gradients on every replay of the schedule).
+#include <algorithm>
+
+#include "gemm_tc.cuh"
+#include "kernels.hpp"
+
+namespace sn {
+namespace {
+
+// n / d for n < 2^31 via multiply-high (d is a runtime constant per launch).
+struct FastDiv {
+  uint32_t d = 1, mul = 1, shift = 0;
+  FastDiv() = default;
+  explicit FastDiv(uint32_t div) : d(div) {
+    uint32_t l = 0;
+    while ((1ull << l) < div) ++l;
+    shift = l;
+    mul = static_cast<uint32_t>(((1ull << 32) * ((1ull << l) - div)) / div + 1);
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const { return (__umulhi(n, mul) + n) >> shift; }
+};
+
+__device__ __forceinline__ void st_shared_v4(uint32_t dst, const float (&v)[4]) {
+  asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(dst), "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3])
+               : "memory");
+}
+
+struct ConvGeomDev {
+  int N, H, W, C, K, R, S, P, Q, stride, pad;
+  int Ktot;  // R*S*C (fwd), R*S*K (dgrad)
+  FastDiv fPQ, fQ, fC, fS, fK, fHW, fW;
+};
+
+ConvGeomDev make_geom(const ConvShape& s) {
+  ConvGeomDev g;
+  g.N = s.N; g.H = s.H; g.W = s.W; g.C = s.C; g.K = s.K; g.R = s.R; g.S = s.S; g.P = s.P; g.Q = s.Q;
+  g.stride = s.stride; g.pad = s.pad;
+  g.Ktot = s.R * s.S * s.C;
+  g.fPQ = FastDiv(s.P * s.Q); g.fQ = FastDiv(s.Q); g.fC = FastDiv(s.C); g.fS = FastDiv(s.S);
+  g.fK = FastDiv(s.K); g.fHW = FastDiv(s.H * s.W); g.fW = FastDiv(s.W);
+  return g;
+}
+
+// ---------------------------------------------------------------------------
+// forward A: rows = output pixels, k = (r, s, c)
+struct FwdA {
+  ConvGeomDev g;
+  const float* x;
+  int mode;  // 2: C % 32 == 0, 1: C % 4 == 0, 0: scalar
+  int M;
+  int4* rows;  // smem row table: {pixel base index n*H*W, h0, w0, valid}
+  __device__ void tile_init(int m0, void* scratch, int tid) {
+    rows = reinterpret_cast<int4*>(scratch);
+    const int m = m0 + tid;
+    int4 r = make_int4(0, -(1 << 28), -(1 << 28), 0);
+    if (m < M) {
+      const uint32_t n = g.fPQ.div(m);
+      const uint32_t pq = m - n * (g.P * g.Q);
+      const uint32_t p = g.fQ.div(pq);
+      const uint32_t q = pq - p * g.Q;
+      r = make_int4(static_cast<int>(n) * g.H * g.W, static_cast<int>(p) * g.stride - g.pad,
+                    static_cast<int>(q) * g.stride - g.pad, 1);
+    }
+    rows[tid] = r;
+  }
+  __device__ __forceinline__ void decode(int k, int& r, int& s, int& c) const {
+    const uint32_t rs = g.fC.div(k);
+    c = k - static_cast<int>(rs) * g.C;
+    r = static_cast<int>(g.fS.div(rs));
+    s = static_cast<int>(rs) - r * g.S;
+  }
+  __device__ void load(uint32_t tile, int kb, int tid) {
+    const int warp = tid >> 5, lane = tid & 31, chunk = lane & 7;
+    const int k = kb * kBK + chunk * 4;
+    if (mode >= 1) {
+      int r = 0, s = 0, c = 0;
+      const bool kin = k < g.Ktot;
+      if (kin) decode(k, r, s, c);
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {
+        const int row = warp * 32 + it * 4 + (lane >> 3);
+        const int4 ri = rows[row];
+        const int h = ri.y + r, w = ri.z + s;
+        const bool ok = kin && ri.w && static_cast<unsigned>(h) < static_cast<unsigned>(g.H) &&
+                        static_cast<unsigned>(w) < static_cast<unsigned>(g.W);
+        const float* src = ok ? x + (static_cast<size_t>(ri.x + h * g.W + w) * g.C + c) : x;
+        cp_async16(tile + sw128_off(row, chunk), src, ok ? 16u : 0u);
+      }
+    } else {
+      for (int it = 0; it < 8; ++it) {
+        const int row = warp * 32 + it * 4 + (lane >> 3);
+        const int4 ri = rows[row];
+        float v[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          v[e] = 0.f;
+          if (k + e < g.Ktot && ri.w) {
+            int r, s, c;
+            decode(k + e, r, s, c);
+            const int h = ri.y + r, w = ri.z + s;
+            if (static_cast<unsigned>(h) < static_cast<unsigned>(g.H) &&
+                static_cast<unsigned>(w) < static_cast<unsigned>(g.W))
+              v[e] = __ldg(x + static_cast<size_t>(ri.x + h * g.W + w) * g.C + c);
+          }
+        }
+        st_shared_v4(tile + sw128_off(row, chunk), v);
+      }
+    }
+  }
+};
+
+// dgrad A: rows = input pixels (n, h, w), k = (r, s, kout)
+struct DgradA {
+  ConvGeomDev g;
+  const float* dy;
+  int mode;  // 1: K % 4 == 0, 0: scalar
+  int M;     // N*H*W
+  int4* rows;  // {n*P*Q, h+pad, w+pad, valid}
+  __device__ void tile_init(int m0, void* scratch, int tid) {
+    rows = reinterpret_cast<int4*>(scratch);
+    const int m = m0 + tid;
+    int4 r = make_int4(0, -(1 << 28), -(1 << 28), 0);
+    if (m < M) {
+      const uint32_t n = g.fHW.div(m);
+      const uint32_t hw = m - n * (g.H * g.W);
+      const uint32_t h = g.fW.div(hw);
+      const uint32_t w = hw - h * g.W;
+      r = make_int4(static_cast<int>(n) * g.P * g.Q, static_cast<int>(h) + g.pad, static_cast<int>(w) + g.pad, 1);
+    }
+    rows[tid] = r;
+  }
+  __device__ __forceinline__ bool tap(const int4& ri, int r, int s, int& pix) const {
+    const int ph = ri.y - r, pw = ri.z - s;
+    if (!ri.w || ph < 0 || pw < 0) return false;
+    int p = ph, q = pw;
+    if (g.stride != 1) {
+      if (ph % g.stride || pw % g.stride) return false;
+      p = ph / g.stride;
+      q = pw / g.stride;
+    }
+    if (p >= g.P || q >= g.Q) return false;
+    pix = ri.x + p * g.Q + q;
+    return true;
+  }
+  __device__ __forceinline__ void decode(int k, int& r, int& s, int& ko) const {
+    const uint32_t rs = g.fK.div(k);
+    ko = k - static_cast<int>(rs) * g.K;
+    r = static_cast<int>(g.fS.div(rs));
+    s = static_cast<int>(rs) - r * g.S;
+  }
+  __device__ void load(uint32_t tile, int kb, int tid) {
+    const int warp = tid >> 5, lane = tid & 31, chunk = lane & 7;
+    const int k = kb * kBK + chunk * 4;
+    const int Ktot = g.R * g.S * g.K;
+    if (mode == 1) {
+      int r = 0, s = 0, ko = 0;
+      const bool kin = k < Ktot;
+      if (kin) decode(k, r, s, ko);
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {
+        const int row = warp * 32 + it * 4 + (lane >> 3);
+        int pix = 0;
+        const bool ok = kin && tap(rows[row], r, s, pix);
+        const float* src = ok ? dy + (static_cast<size_t>(pix) * g.K + ko) : dy;
+        cp_async16(tile + sw128_off(row, chunk), src, ok ? 16u : 0u);
+      }
+    } else {
+      for (int it = 0; it < 8; ++it) {
+        const int row = warp * 32 + it * 4 + (lane >> 3);
+        const int4 ri = rows[row];
+        float v[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          v[e] = 0.f;
+          int r, s, ko, pix;
+          if (k + e < Ktot) {
+            decode(k + e, r, s, ko);
+            if (tap(ri, r, s, pix)) v[e] = __ldg(dy + static_cast<size_t>(pix) * g.K + ko);
+          }
+        }
+        st_shared_v4(tile + sw128_off(row, chunk), v);
+      }
+    }
+  }
+};
+
+// wgrad A (MN-major): k rows = output pixels, mn = (r, s, c)
+struct WgradA {
+  ConvGeomDev g;
+  const float* x;
+  int mode;   // 1: C % 4 == 0, 0: scalar
+  int NPQ, RSC;
+  int m0;
+  __device__ void tile_init(int m0_, void*, int) { m0 = m0_; }
+  __device__ void load(uint32_t tile, int kb, int tid) {
+    const int warp = tid >> 5, lane = tid & 31;
+    const int m = m0 + lane * 4;  // this thread's 4 consecutive rsc
+    int r = 0, s = 0, c = 0;
+    const bool min_ok = m < RSC;
+    if (min_ok) {
+      const uint32_t rs = g.fC.div(m);
+      c = m - static_cast<int>(rs) * g.C;
+      r = static_cast<int>(g.fS.div(rs));
+      s = static_cast<int>(rs) - r * g.S;
+    }
+#pragma unroll 2
+    for (int i = 0; i < 8; ++i) {
+      const int krow = warp + 4 * i;
+      const int pix = kb * kBK + krow;
+      const uint32_t dst = tile + mn_tile_off<kBM>(krow, lane);
+      int n = 0, h0 = 0, w0 = 0;
+      const bool pix_ok = pix < NPQ;
+      if (pix_ok) {
+        n = static_cast<int>(g.fPQ.div(pix));
+        const int pq = pix - n * g.P * g.Q;
+        const int p = static_cast<int>(g.fQ.div(pq));
+        const int q = pq - p * g.Q;
+        h0 = p * g.stride - g.pad;
+        w0 = q * g.stride - g.pad;
+      }
+      if (mode == 1) {
+        const int h = h0 + r, w = w0 + s;
+        const bool ok = pix_ok && min_ok && static_cast<unsigned>(h) < static_cast<unsigned>(g.H) &&
+                        static_cast<unsigned>(w) < static_cast<unsigned>(g.W);
+        const float* src = ok ? x + (static_cast<size_t>((n * g.H + h) * g.W + w) * g.C + c) : x;
+        cp_async16(dst, src, ok ? 16u : 0u);
+      } else {
+        float v[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          v[e] = 0.f;
+          const int me = m + e;
+          if (pix_ok && me < RSC) {
+            const uint32_t rs = g.fC.div(me);
+            const int ce = me - static_cast<int>(rs) * g.C;
+            const int re = static_cast<int>(g.fS.div(rs));
+            const int se = static_cast<int>(rs) - re * g.S;
+            const int h = h0 + re, w = w0 + se;
+            if (static_cast<unsigned>(h) < static_cast<unsigned>(g.H) &&
+                static_cast<unsigned>(w) < static_cast<unsigned>(g.W))
+              v[e] = __ldg(x + static_cast<size_t>((n * g.H + h) * g.W + w) * g.C + ce);
+          }
+        }
+        st_shared_v4(dst, v);
+      }
+    }
+  }
+};
+
+// Row-major epilogue with per-column bias and optional accumulate.
+struct EpiStore {
+  float* D;
+  const float* bias;
+  int M, N, ldd, accumulate;
+  __device__ void store(int m, int n0, const float* v, int) const {
+    if (m >= M) return;
+    float* d = D + static_cast<size_t>(m) * ldd;
+    if ((N & 3) == 0 && n0 + 32 <= N) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 4) {
+        float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        if (bias) {
+          const float4 b = *reinterpret_cast<const float4*>(bias + n0 + j);
+          o.x += b.x; o.y += b.y; o.z += b.z; o.w += b.w;
+        }
+        float4* dp = reinterpret_cast<float4*>(d + n0 + j);
+        if (accumulate) {
+          const float4 old = *dp;
+          o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
+        }
+        *dp = o;
+      }
+      return;
+    }
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int n = n0 + j;
+      if (n < N) {
+        float o = v[j];
+        if (bias) o += bias[n];
+        d[n] = accumulate ? d[n] + o : o;
+      }
+    }
+  }
+};
+
+// D[M][N] = sum_split P[split][M][N] (+bias[n]) (+D if accumulate); optionally
+// written transposed (D^T[N][M], for wgrad partials laid out [rsc][k]).
+__global__ void splitk_reduce_kernel(const float* __restrict__ P, int splits, int M, int N, float* D,
+                                     const float* bias, int accumulate, int transpose) {
+  __shared__ float tile[32][33];
+  const int m0 = blockIdx.y * 32, n0 = blockIdx.x * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  for (int i = ty; i < 32; i += 8) {
+    const int m = m0 + i, n = n0 + tx;
+    float acc = 0.f;
+    if (m < M && n < N) {
+      const size_t stride = static_cast<size_t>(M) * N;
+      const float* p = P + static_cast<size_t>(m) * N + n;
+      for (int s = 0; s < splits; ++s) acc += p[s * stride];
+      if (bias) acc += bias[n];
+    }
+    tile[i][tx] = acc;
+  }
+  if (!transpose) {
+    for (int i = ty; i < 32; i += 8) {
+      const int m = m0 + i, n = n0 + tx;
+      if (m < M && n < N) {
+        float* d = D + static_cast<size_t>(m) * N + n;
+        *d = accumulate ? *d + tile[i][tx] : tile[i][tx];
+      }
+    }
+    return;
+  }
+  __syncthreads();
+  for (int i = ty; i < 32; i += 8) {
+    const int n = n0 + i, m = m0 + tx;
+    if (m < M && n < N) {
+      float* d = D + static_cast<size_t>(n) * M + m;
+      *d = accumulate ? *d + tile[tx][i] : tile[tx][i];
+    }
+  }
+}
+
+cudaError_t splitk_reduce(const float* P, int splits, int M, int N, float* D, const float* bias, int accumulate,
+                          int transpose, cudaStream_t st) {
+  dim3 grid((N + 31) / 32, (M + 31) / 32), block(32, 8);
+  splitk_reduce_kernel<<<grid, block, 0, st>>>(P, splits, M, N, D, bias, accumulate, transpose);
+  return cudaGetLastError();
+}
+
+// wt[c][r][s][k] = w[k][r][s][c]
+__global__ void transpose_w_kernel(const float* __restrict__ w, float* __restrict__ wt, int K, int RS, int C) {
+  __shared__ float tile[32][33];
+  const int rs = blockIdx.z;
+  const int k0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int k = k0 + i, c = c0 + threadIdx.x;
+    tile[i][threadIdx.x] = (k < K && c < C) ? w[(static_cast<size_t>(k) * RS + rs) * C + c] : 0.f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int c = c0 + i, k = k0 + threadIdx.x;
+    if (k < K && c < C) wt[(static_cast<size_t>(c) * RS + rs) * K + k] = tile[threadIdx.x][i];
+  }
+}
+
+template <int BN>
+cudaError_t conv_fwd_bn(const ConvShape& s, const float* x, const float* w, const float* bias, float* y,
+                        cudaStream_t st) {
+  const ConvGeomDev g = make_geom(s);
+  FwdA la{g, x, (s.C % 32 == 0) ? 2 : (s.C % 4 == 0 ? 1 : 0), s.N * s.P * s.Q, nullptr};
+  MatKLoader<BN> lb{};
+  lb.base = w; lb.rows = s.K; lb.K = g.Ktot; lb.ld = g.Ktot; lb.fast = (g.Ktot % 4 == 0);
+  EpiStore e{y, bias, la.M, s.K, s.K, 0};
+  return launch_tc_gemm<BN, 4, false, false>(la, lb, e, la.M, s.K, g.Ktot, 1, st);
+}
+
+template <int BN>
+cudaError_t conv_dgrad_bn(const ConvShape& s, const float* dy, const float* wt, float* dx, int accumulate,
+                          cudaStream_t st) {
+  const ConvGeomDev g = make_geom(s);
+  const int Ktot = s.R * s.S * s.K;
+  DgradA la{g, dy, (s.K % 4 == 0) ? 1 : 0, s.N * s.H * s.W, nullptr};
+  MatKLoader<BN> lb{};
+  lb.base = wt; lb.rows = s.C; lb.K = Ktot; lb.ld = Ktot; lb.fast = (Ktot % 4 == 0);
+  EpiStore e{dx, nullptr, la.M, s.C, s.C, accumulate};
+  return launch_tc_gemm<BN, 4, false, false>(la, lb, e, la.M, s.C, Ktot, 1, st);
+}
+
+template <int BN>
+cudaError_t conv_wgrad_bn(const ConvShape& s, const float* x, const float* dy, float* partial, int splits,
+                          cudaStream_t st) {
+  const ConvGeomDev g = make_geom(s);
+  const int NPQ = s.N * s.P * s.Q, RSC = s.R * s.S * s.C;
+  WgradA la{g, x, (s.C % 4 == 0) ? 1 : 0, NPQ, RSC, 0};
+  MatMNLoader<BN> lb{};
+  lb.base = dy; lb.rows = s.K; lb.K = NPQ; lb.ld = s.K; lb.fast = (s.K % 4 == 0);
+  EpiPartial e{partial, RSC, s.K};
+  return launch_tc_gemm<BN, 4, true, true>(la, lb, e, RSC, s.K, NPQ, splits, st);
+}
+
+template <int BN>
+cudaError_t fc_gemm_bn(int a_mn, int b_mn, const float* A, int lda, const float* B, int ldb, int M, int N, int K,
+                       float* partial, int splits, cudaStream_t st) {
+  EpiPartial e{partial, M, N};
+  auto setK = [](auto& l, const float* p, int rows, int KK, int ld) {
+    l.base = p; l.rows = rows; l.K = KK; l.ld = ld;
+    l.fast = (reinterpret_cast<uintptr_t>(p) % 16 == 0) && ld % 4 == 0 && KK % 4 == 0;
+  };
+  auto setMN = [](auto& l, const float* p, int rows, int KK, int ld) {
+    l.base = p; l.rows = rows; l.K = KK; l.ld = ld;
+    l.fast = (reinterpret_cast<uintptr_t>(p) % 16 == 0) && ld % 4 == 0 && rows % 4 == 0;
+  };
+  if (!a_mn && !b_mn) {
+    MatKLoader<kBM> la{}; MatKLoader<BN> lb{};
+    setK(la, A, M, K, lda); setK(lb, B, N, K, ldb);
+    return launch_tc_gemm<BN, 4, false, false>(la, lb, e, M, N, K, splits, st);
+  }
+  if (!a_mn && b_mn) {
+    MatKLoader<kBM> la{}; MatMNLoader<BN> lb{};
+    setK(la, A, M, K, lda); setMN(lb, B, N, K, ldb);
+    return launch_tc_gemm<BN, 4, false, true>(la, lb, e, M, N, K, splits, st);
+  }
+  MatMNLoader<kBM> la{}; MatMNLoader<BN> lb{};
+  setMN(la, A, M, K, lda); setMN(lb, B, N, K, ldb);
+  return launch_tc_gemm<BN, 4, true, true>(la, lb, e, M, N, K, splits, st);
+}
+
+cudaError_t fc_gemm(int a_mn, int b_mn, const float* A, int lda, const float* B, int ldb, int M, int N, int K,
+                    float* partial, int splits, cudaStream_t st) {
+  if (N <= 64) return fc_gemm_bn<64>(a_mn, b_mn, A, lda, B, ldb, M, N, K, partial, splits, st);
+  if (N <= 128) return fc_gemm_bn<128>(a_mn, b_mn, A, lda, B, ldb, M, N, K, partial, splits, st);
+  return fc_gemm_bn<256>(a_mn, b_mn, A, lda, B, ldb, M, N, K, partial, splits, st);
+}
+
+int bn_for(int n) { return n <= 64 ? 64 : (n <= 128 ? 128 : 256); }
+
+}  // namespace
+
+cudaError_t conv_fwd(const ConvShape& s, const float* x, const float* w, const float* bias, float* y,
+                     cudaStream_t st) {
+  switch (bn_for(s.K)) {
+    case 64: return conv_fwd_bn<64>(s, x, w, bias, y, st);
+    case 128: return conv_fwd_bn<128>(s, x, w, bias, y, st);
+    default: return conv_fwd_bn<256>(s, x, w, bias, y, st);
+  }
+}
+
+cudaError_t conv_dgrad(const ConvShape& s, const float* dy, const float* w, float* wt, float* dx, int accumulate,
+                       cudaStream_t st) {
+  dim3 grid((s.C + 31) / 32, (s.K + 31) / 32, s.R * s.S), block(32, 8);
+  transpose_w_kernel<<<grid, block, 0, st>>>(w, wt, s.K, s.R * s.S, s.C);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  switch (bn_for(s.C)) {
+    case 64: return conv_dgrad_bn<64>(s, dy, wt, dx, accumulate, st);
+    case 128: return conv_dgrad_bn<128>(s, dy, wt, dx, accumulate, st);
+    default: return conv_dgrad_bn<256>(s, dy, wt, dx, accumulate, st);
+  }
+}
+
+int conv_wgrad_splits(const ConvShape& s, int64_t partial_floats_cap) {
+  const int64_t RSC = static_cast<int64_t>(s.R) * s.S * s.C;
+  const int bn = bn_for(s.K);
+  const int64_t tiles = ((RSC + kBM - 1) / kBM) * ((s.K + bn - 1) / bn);
+  const int64_t NPQ = static_cast<int64_t>(s.N) * s.P * s.Q;
+  const int64_t nkb = (NPQ + kBK - 1) / kBK;
+  int64_t want = (2 * 148 + tiles - 1) / tiles;
+  want = std::min<int64_t>(want, std::max<int64_t>(1, nkb / 8));
+  const int64_t per = RSC * s.K;
+  want = std::min<int64_t>(want, std::max<int64_t>(1, partial_floats_cap / per));
+  return effective_splits(static_cast<int>(NPQ), static_cast<int>(std::max<int64_t>(1, want)));
+}
+
+cudaError_t conv_wgrad(const ConvShape& s, const float* x, const float* dy, float* dw, float* db, float* partial,
+                       int splits, float* red_scratch, cudaStream_t st) {
+  cudaError_t e;
+  switch (bn_for(s.K)) {
+    case 64: e = conv_wgrad_bn<64>(s, x, dy, partial, splits, st); break;
+    case 128: e = conv_wgrad_bn<128>(s, x, dy, partial, splits, st); break;
+    default: e = conv_wgrad_bn<256>(s, x, dy, partial, splits, st); break;
+  }
+  if (e != cudaSuccess) return e;
+  const int RSC = s.R * s.S * s.C;
+  e = splitk_reduce(partial, splits, RSC, s.K, dw, nullptr, 0, 1, st);
+  if (e != cudaSuccess) return e;
+  return bias_grad(dy, static_cast<int64_t>(s.N) * s.P * s.Q, s.K, db, red_scratch, st);
+}
+
+int fc_splits(int B, int I, int O, int64_t partial_floats_cap) {
+  // forward: M=B, N=O, K=I ; dgrad: M=B, N=I, K=O.  Same split count for both.
+  const int64_t tiles = static_cast<int64_t>((B + kBM - 1) / kBM) * ((std::max(I, O) + 255) / 256);
+  const int64_t nkb = (std::min(I, O) + kBK - 1) / kBK;
+  int64_t want = (2 * 148 + tiles - 1) / tiles;
+  want = std::min<int64_t>(want, std::max<int64_t>(1, nkb / 4));
+  want = std::min<int64_t>(want, std::max<int64_t>(1, partial_floats_cap / (static_cast<int64_t>(B) * std::max(I, O))));
+  return static_cast<int>(std::max<int64_t>(1, want));
+}
+
+cudaError_t fc_fwd(int B, int I, int O, const float* x, const float* w, const float* bias, float* y, float* partial,
+                   int splits, cudaStream_t st) {
+  const int eff = effective_splits(I, splits);
+  cudaError_t e = fc_gemm(0, 0, x, I, w, I, B, O, I, partial, eff, st);
+  if (e != cudaSuccess) return e;
+  return splitk_reduce(partial, eff, B, O, y, bias, 0, 0, st);
+}
+
+cudaError_t fc_dgrad(int B, int I, int O, const float* dy, const float* w, float* dx, int accumulate, float* partial,
+                     int splits, cudaStream_t st) {
+  // dx[b][i] = sum_o dy[b][o] w[o][i]: A = dy (K-major, ld O), B[i][o] = w[o][i] (MN-major, ld I)
+  const int eff = effective_splits(O, splits);
+  cudaError_t e = fc_gemm(0, 1, dy, O, w, I, B, I, O, partial, eff, st);
+  if (e != cudaSuccess) return e;
+  return splitk_reduce(partial, eff, B, I, dx, nullptr, accumulate, 0, st);
+}
+
+cudaError_t fc_wgrad(int B, int I, int O, const float* x, const float* dy, float* dw, float* db, float* red_scratch,
+                     cudaStream_t st) {
+  // dw[o][i] = sum_b dy[b][o] x[b][i]: A[o][b] = dy (MN-major, ld O), B[i][b] = x (MN-major, ld I)
+  EpiStore e{dw, nullptr, O, I, I, 0};
+  MatMNLoader<kBM> la{};
+  la.base = dy; la.rows = O; la.K = B; la.ld = O;
+  la.fast = (reinterpret_cast<uintptr_t>(dy) % 16 == 0) && O % 4 == 0;
+  cudaError_t err;
+  if (I <= 64) {
+    MatMNLoader<64> lb{};
+    lb.base = x; lb.rows = I; lb.K = B; lb.ld = I; lb.fast = (reinterpret_cast<uintptr_t>(x) % 16 == 0) && I % 4 == 0;
+    err = launch_tc_gemm<64, 4, true, true>(la, lb, e, O, I, B, 1, st);
+  } else if (I <= 128) {
+    MatMNLoader<128> lb{};
+    lb.base = x; lb.rows = I; lb.K = B; lb.ld = I; lb.fast = (reinterpret_cast<uintptr_t>(x) % 16 == 0) && I % 4 == 0;
+    err = launch_tc_gemm<128, 4, true, true>(la, lb, e, O, I, B, 1, st);
+  } else {
+    MatMNLoader<256> lb{};
+    lb.base = x; lb.rows = I; lb.K = B; lb.ld = I; lb.fast = (reinterpret_cast<uintptr_t>(x) % 16 == 0) && I % 4 == 0;
+    err = launch_tc_gemm<256, 4, true, true>(la, lb, e, O, I, B, 1, st);
+  }
+  if (err != cudaSuccess) return err;
+  return bias_grad(dy, B, O, db, red_scratch, st);
+}
+
+}  // namespace sn

@@ -2,6 +2,7 @@
 // kernel-level parity tests (tests/test_gpu_kernels.py).  Not on the training
 // path; the executor calls the same template through its conv/FC wrappers.
 #include "gemm_tc.cuh"
+#include "kernels.hpp"
 
 namespace {
 
@@ -52,3 +53,32 @@ extern "C" int sn_test_gemm(int a_mn, int b_mn, int bn, const float* A, const fl
 }
 
 extern "C" int sn_test_effective_splits(int K, int splits) { return sn::effective_splits(K, splits); }
+
+// Conv kernels on caller buffers.  shape = {N,H,W,C,K,R,S,P,Q,stride,pad}.
+//   op 0 forward:  p = {x, w, bias, y}
+//   op 1 dgrad:    p = {dy, w, wt_scratch, dx}, flag = accumulate
+//   op 2 wgrad:    p = {x, dy, dw, db, partial, red_scratch}, flag = splits (<=0: auto)
+extern "C" int sn_test_conv(int op, const int* shape, void** p, int flag) {
+  sn::ConvShape s{shape[0], shape[1], shape[2], shape[3], shape[4], shape[5], shape[6],
+                  shape[7], shape[8], shape[9], shape[10]};
+  cudaError_t e;
+  if (op == 0) {
+    e = sn::conv_fwd(s, (const float*)p[0], (const float*)p[1], (const float*)p[2], (float*)p[3], 0);
+  } else if (op == 1) {
+    e = sn::conv_dgrad(s, (const float*)p[0], (const float*)p[1], (float*)p[2], (float*)p[3], flag, 0);
+  } else {
+    const int splits = flag > 0 ? flag : sn::conv_wgrad_splits(s, 64ll << 20);
+    e = sn::conv_wgrad(s, (const float*)p[0], (const float*)p[1], (float*)p[2], (float*)p[3], (float*)p[4],
+                       splits, (float*)p[5], 0);
+  }
+  if (e != cudaSuccess) return 4;
+  return cudaDeviceSynchronize() == cudaSuccess ? 0 : 4;
+}
+
+extern "C" int sn_test_wgrad_splits(const int* shape) {
+  sn::ConvShape s{shape[0], shape[1], shape[2], shape[3], shape[4], shape[5], shape[6],
+                  shape[7], shape[8], shape[9], shape[10]};
+  return sn::conv_wgrad_splits(s, 64ll << 20);
+}
+
+extern "C" long long sn_test_red_scratch_floats(int C) { return sn::red_scratch_floats(C); }

@@ -1,0 +1,93 @@
+// Host-side launch API of the sm_100a kernels used by the executor.
+// All tensors are fp32, NHWC (channels innermost), batch-major.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace sn {
+
+struct ConvShape {
+  int N, H, W, C;   // input (C = stored channels; the DATA stem is padded to 4)
+  int K, R, S;      // output channels, kernel rows, kernel cols
+  int P, Q;         // output spatial
+  int stride, pad;
+};
+
+// ---- tensor-core GEMM based ops (gemm_ops.cu) --------------------------------
+// y[N*P*Q][K] = conv(x, w[K][R][S][C]) + bias
+cudaError_t conv_fwd(const ConvShape& s, const float* x, const float* w, const float* bias, float* y,
+                     cudaStream_t st);
+// dx[N*H*W][C] (+)= conv_transpose(dy, w); wt = scratch of K*R*S*C floats.
+cudaError_t conv_dgrad(const ConvShape& s, const float* dy, const float* w, float* wt, float* dx,
+                       int accumulate, cudaStream_t st);
+// dw[K][R*S*C] = sum_pixels im2col(x)^T dy ; db[K] = column sums of dy.
+// partial: scratch of splits*R*S*C*K floats (see conv_wgrad_splits).
+int conv_wgrad_splits(const ConvShape& s, int64_t partial_floats_cap);
+cudaError_t conv_wgrad(const ConvShape& s, const float* x, const float* dy, float* dw, float* db,
+                       float* partial, int splits, float* red_scratch, cudaStream_t st);
+
+// FC: x[B][I], w[O][I], y[B][O]
+int fc_splits(int B, int I, int O, int64_t partial_floats_cap);
+cudaError_t fc_fwd(int B, int I, int O, const float* x, const float* w, const float* bias, float* y,
+                   float* partial, int splits, cudaStream_t st);
+cudaError_t fc_dgrad(int B, int I, int O, const float* dy, const float* w, float* dx, int accumulate,
+                     float* partial, int splits, cudaStream_t st);
+cudaError_t fc_wgrad(int B, int I, int O, const float* x, const float* dy, float* dw, float* db,
+                     float* red_scratch, cudaStream_t st);
+
+// ---- memory-bound layer kernels (layers.cu) ------------------------------------
+// Per-channel column reductions over a [rows][C] matrix need a scratch of
+// kRedChunks*C*2 doubles.
+constexpr int kRedChunks = 296;
+int64_t red_scratch_floats(int C);
+
+cudaError_t bias_grad(const float* dy, int64_t rows, int C, float* db, float* red_scratch, cudaStream_t st);
+
+// BatchNorm (training statistics).  stats = {mean[C], invstd[C]} saved outside
+// the arena; running = {mean[C], var[C]} updated only when update_running.
+cudaError_t bn_fwd(const float* x, int64_t rows, int C, const float* gamma, const float* beta, float* y,
+                   float* stats, float* running, float eps, float momentum, int compute_stats,
+                   float* red_scratch, cudaStream_t st);
+cudaError_t bn_bwd(const float* x, const float* dy, int64_t rows, int C, const float* gamma,
+                   const float* stats, float* dx, int accumulate, float* dgamma, float* dbeta,
+                   float* red_scratch, cudaStream_t st);
+
+cudaError_t relu_fwd(const float* x, float* y, int64_t n, cudaStream_t st);
+cudaError_t relu_bwd_inplace(const float* y, float* g, int64_t n, cudaStream_t st);
+
+struct PoolShape {
+  int N, H, W, C, P, Q, K, stride, pad, mode;  // mode 0 max, 1 avg
+};
+cudaError_t pool_fwd(const PoolShape& s, const float* x, float* y, cudaStream_t st);
+cudaError_t pool_bwd(const PoolShape& s, const float* x, const float* y, const float* dy, float* dx,
+                     int accumulate, cudaStream_t st);
+
+cudaError_t lrn_fwd(const float* x, float* y, int64_t pixels, int C, int size, float alpha, float beta,
+                    float k, cudaStream_t st);
+cudaError_t lrn_bwd(const float* x, const float* y, const float* dy, float* dx, int64_t pixels, int C,
+                    int size, float alpha, float beta, float k, int accumulate, cudaStream_t st);
+
+// Dropout: mask bit = hash(seed, layer, *iteration, index) >= rate * 2^32.
+cudaError_t dropout_fwd(const float* x, float* y, int64_t n, float rate, uint64_t seed, int layer,
+                        const uint32_t* iteration, cudaStream_t st);
+cudaError_t dropout_bwd_inplace(float* g, int64_t n, float rate, uint64_t seed, int layer,
+                                const uint32_t* iteration, cudaStream_t st);
+
+// Softmax over F features per row + cross entropy vs labels; loss_rows[B].
+cudaError_t softmax_fwd(const float* x, float* y, int B, int F, const int32_t* labels, float* loss_rows,
+                        cudaStream_t st);
+cudaError_t softmax_ce_bwd(const float* y, const int32_t* labels, float* dx, int B, int F, int accumulate,
+                           cudaStream_t st);
+cudaError_t loss_reduce(const float* loss_rows, int B, float* loss, cudaStream_t st);
+
+// y = sum_i inputs[i] (device array of n_in pointers), n elements.
+cudaError_t join_fwd(const float* const* inputs, int n_in, float* y, int64_t n, cudaStream_t st);
+// dst (+)= src
+cudaError_t grad_copy(const float* src, float* dst, int64_t n, int accumulate, cudaStream_t st);
+
+cudaError_t sgd_update(float* params, const float* grads, int64_t n, float lr, float grad_scale,
+                       cudaStream_t st);
+cudaError_t bump_iteration(uint32_t* iteration, cudaStream_t st);
+cudaError_t fill_zero(float* p, int64_t n, cudaStream_t st);
+
+}  // namespace sn

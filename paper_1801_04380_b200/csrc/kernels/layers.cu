@@ -1,0 +1,634 @@
+// Memory-bound layer kernels of the training step (HBM roofline): BN, ReLU,
+// POOL, LRN, DROPOUT, SOFTMAX+CE, JOIN, gradient copies and the SGD update.
+// NHWC fp32; float4 paths whenever the channel count allows.  Every reduction
+// is two-stage with a fixed combination order, so a replayed (recomputed)
+// forward and every feature set produce bit-identical values.
+#include <cfloat>
+#include <cmath>
+
+#include "kernels.hpp"
+
+namespace sn {
+namespace {
+
+constexpr int kThreads = 256;
+
+inline int blocks_for(int64_t n, int per_block = kThreads, int cap = 148 * 16) {
+  int64_t b = (n + per_block - 1) / per_block;
+  if (b < 1) b = 1;
+  return static_cast<int>(b < cap ? b : cap);
+}
+
+// ---------------------------------------------------------------------------
+// Deterministic per-channel column sums over a [rows][C] matrix.
+// Stage 1: block b reduces rows [b*chunk, (b+1)*chunk) into part[b][2][C]
+// (doubles); stage 2 sums the blocks in order.  Two sums per channel:
+// f1 and f2 of the functor.
+
+struct RedBiasOp {  // f1 = dy
+  const float* dy;
+  __device__ void eval(int64_t row, int c, int C, float& a, float& b) const {
+    a = dy[row * C + c];
+    b = 0.f;
+  }
+};
+struct RedBnStatsOp {  // f1 = x - x[0][c], f2 = (x - x[0][c])^2
+  const float* x;
+  __device__ void eval(int64_t row, int c, int C, float& a, float& b) const {
+    const float d = x[row * C + c] - x[c];
+    a = d;
+    b = d * d;
+  }
+};
+struct RedBnBwdOp {  // f1 = dy, f2 = dy * xhat
+  const float* x;
+  const float* dy;
+  const float* stats;  // mean[C], invstd[C]
+  __device__ void eval(int64_t row, int c, int C, float& a, float& b) const {
+    const float g = dy[row * C + c];
+    const float xh = (x[row * C + c] - stats[c]) * stats[C + c];
+    a = g;
+    b = g * xh;
+  }
+};
+
+template <class Op>
+__global__ void colred_stage1(Op op, int64_t rows, int C, int64_t chunk, double* part) {
+  __shared__ double s1[kThreads], s2[kThreads];
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * chunk;
+  const int64_t r1 = r0 + chunk < rows ? r0 + chunk : rows;
+  const int cb = C < kThreads ? C : kThreads;  // channels covered per pass
+  const int lanes = kThreads / cb;             // row lanes
+  const int t = threadIdx.x;
+  const int lane = t / cb, cc = t % cb;
+  for (int c0 = 0; c0 < C; c0 += cb) {
+    const int c = c0 + cc;
+    float a = 0.f, b = 0.f;
+    if (lane < lanes && c < C) {
+      for (int64_t r = r0 + lane; r < r1; r += lanes) {
+        float fa, fb;
+        op.eval(r, c, C, fa, fb);
+        a += fa;
+        b += fb;
+      }
+    }
+    s1[t] = a;
+    s2[t] = b;
+    __syncthreads();
+    if (lane == 0 && c < C) {
+      double A = 0.0, B = 0.0;
+      for (int l = 0; l < lanes; ++l) {
+        A += s1[l * cb + cc];
+        B += s2[l * cb + cc];
+      }
+      part[(static_cast<size_t>(blockIdx.x) * 2) * C + c] = A;
+      part[(static_cast<size_t>(blockIdx.x) * 2 + 1) * C + c] = B;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void colred_stage2(const double* part, int nblocks, int C, double* out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  double A = 0.0, B = 0.0;
+  for (int b = 0; b < nblocks; ++b) {
+    A += part[(static_cast<size_t>(b) * 2) * C + c];
+    B += part[(static_cast<size_t>(b) * 2 + 1) * C + c];
+  }
+  out[c] = A;
+  out[C + c] = B;
+}
+
+// Runs both stages; result sums land in sums[0..2C) (doubles) inside scratch.
+template <class Op>
+cudaError_t colred(Op op, int64_t rows, int C, float* scratch_f, double** sums_out, cudaStream_t st) {
+  double* part = reinterpret_cast<double*>(scratch_f);
+  int64_t nb = rows < kRedChunks ? rows : kRedChunks;
+  if (nb < 1) nb = 1;
+  const int64_t chunk = (rows + nb - 1) / nb;
+  nb = (rows + chunk - 1) / chunk;
+  if (nb < 1) nb = 1;
+  colred_stage1<<<static_cast<int>(nb), kThreads, 0, st>>>(op, rows, C, chunk, part);
+  double* sums = part + static_cast<size_t>(kRedChunks) * 2 * C;
+  colred_stage2<<<(C + 255) / 256, 256, 0, st>>>(part, static_cast<int>(nb), C, sums);
+  *sums_out = sums;
+  return cudaGetLastError();
+}
+
+__global__ void bias_finalize(const double* sums, int C, float* db) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < C) db[c] = static_cast<float>(sums[c]);
+}
+
+__global__ void bn_stats_finalize(const double* sums, const float* x, int64_t rows, int C, float eps, float momentum,
+                                  float* stats, float* running) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const double n = static_cast<double>(rows);
+  const double m1 = sums[c] / n;
+  double var = sums[C + c] / n - m1 * m1;
+  if (var < 0.0) var = 0.0;
+  const double mean = static_cast<double>(x[c]) + m1;
+  stats[c] = static_cast<float>(mean);
+  stats[C + c] = static_cast<float>(1.0 / sqrt(var + static_cast<double>(eps)));
+  if (running) {
+    const double unbiased = rows > 1 ? var * n / (n - 1.0) : var;
+    running[c] = static_cast<float>((1.0 - momentum) * running[c] + momentum * mean);
+    running[C + c] = static_cast<float>((1.0 - momentum) * running[C + c] + momentum * unbiased);
+  }
+}
+
+template <int VEC>
+__global__ void bn_apply_kernel(const float* __restrict__ x, int64_t n, int C, const float* __restrict__ gamma,
+                                const float* __restrict__ beta, const float* __restrict__ stats, float* __restrict__ y) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  if (VEC == 4) {
+    const int64_t n4 = n / 4;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4; i += stride) {
+      const int c = static_cast<int>((i * 4) % C);
+      float4 v = reinterpret_cast<const float4*>(x)[i];
+      float o[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) o[e] = (o[e] - stats[c + e]) * stats[C + c + e] * gamma[c + e] + beta[c + e];
+      reinterpret_cast<float4*>(y)[i] = make_float4(o[0], o[1], o[2], o[3]);
+    }
+  } else {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride) {
+      const int c = static_cast<int>(i % C);
+      y[i] = (x[i] - stats[c]) * stats[C + c] * gamma[c] + beta[c];
+    }
+  }
+}
+
+__global__ void bn_bwd_finalize(const double* sums, int C, float* dgamma, float* dbeta, float* coef) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  dbeta[c] = static_cast<float>(sums[c]);
+  dgamma[c] = static_cast<float>(sums[C + c]);
+  coef[c] = static_cast<float>(sums[c]);
+  coef[C + c] = static_cast<float>(sums[C + c]);
+}
+
+template <int VEC>
+__global__ void bn_dx_kernel(const float* __restrict__ x, const float* __restrict__ dy, int64_t n, int64_t rows, int C,
+                             const float* __restrict__ gamma, const float* __restrict__ stats,
+                             const float* __restrict__ coef, float* dx, int accumulate) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const float inv_m = 1.0f / static_cast<float>(rows);
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n / VEC; i += stride) {
+    const int c0 = static_cast<int>((i * VEC) % C);
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      const int64_t j = i * VEC + e;
+      const int c = c0 + e;
+      const float xh = (x[j] - stats[c]) * stats[C + c];
+      const float v = gamma[c] * stats[C + c] * (dy[j] - coef[c] * inv_m - xh * coef[C + c] * inv_m);
+      dx[j] = accumulate ? dx[j] + v : v;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+__global__ void relu_fwd_kernel(const float4* __restrict__ x, float4* __restrict__ y, int64_t n4) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4; i += stride) {
+    float4 v = x[i];
+    v.x = v.x > 0.f ? v.x : 0.f;
+    v.y = v.y > 0.f ? v.y : 0.f;
+    v.z = v.z > 0.f ? v.z : 0.f;
+    v.w = v.w > 0.f ? v.w : 0.f;
+    y[i] = v;
+  }
+}
+__global__ void relu_fwd_tail(const float* x, float* y, int64_t from, int64_t n) {
+  const int64_t i = from + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) y[i] = x[i] > 0.f ? x[i] : 0.f;
+}
+__global__ void relu_bwd_kernel(const float4* __restrict__ y, float4* g, int64_t n4) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4; i += stride) {
+    const float4 yy = y[i];
+    float4 v = g[i];
+    v.x = yy.x > 0.f ? v.x : 0.f;
+    v.y = yy.y > 0.f ? v.y : 0.f;
+    v.z = yy.z > 0.f ? v.z : 0.f;
+    v.w = yy.w > 0.f ? v.w : 0.f;
+    g[i] = v;
+  }
+}
+__global__ void relu_bwd_tail(const float* y, float* g, int64_t from, int64_t n) {
+  const int64_t i = from + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) g[i] = y[i] > 0.f ? g[i] : 0.f;
+}
+
+// ---------------------------------------------------------------------------
+__global__ void pool_fwd_kernel(PoolShape s, const float* __restrict__ x, float* __restrict__ y, int64_t total) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total; i += stride) {
+    const int c = static_cast<int>(i % s.C);
+    int64_t t = i / s.C;
+    const int q = static_cast<int>(t % s.Q);
+    t /= s.Q;
+    const int p = static_cast<int>(t % s.P);
+    const int n = static_cast<int>(t / s.P);
+    const int h0 = p * s.stride - s.pad, w0 = q * s.stride - s.pad;
+    float acc = s.mode == 0 ? -FLT_MAX : 0.f;
+    bool any = false;
+    for (int r = 0; r < s.K; ++r) {
+      const int h = h0 + r;
+      if (h < 0 || h >= s.H) continue;
+      for (int u = 0; u < s.K; ++u) {
+        const int w = w0 + u;
+        if (w < 0 || w >= s.W) continue;
+        const float v = x[((static_cast<int64_t>(n) * s.H + h) * s.W + w) * s.C + c];
+        if (s.mode == 0) {
+          if (!any || v > acc) acc = v;
+          any = true;
+        } else {
+          acc += v;
+        }
+      }
+    }
+    y[i] = s.mode == 0 ? acc : acc / static_cast<float>(s.K * s.K);
+  }
+}
+
+__global__ void pool_bwd_kernel(PoolShape s, const float* __restrict__ x, const float* __restrict__ y,
+                                const float* __restrict__ dy, float* dx, int accumulate, int64_t total) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const float inv = 1.0f / static_cast<float>(s.K * s.K);
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total; i += stride) {
+    const int c = static_cast<int>(i % s.C);
+    int64_t t = i / s.C;
+    const int w = static_cast<int>(t % s.W);
+    t /= s.W;
+    const int h = static_cast<int>(t % s.H);
+    const int n = static_cast<int>(t / s.H);
+    // output rows/cols whose window covers (h, w)
+    int plo = h + s.pad - s.K + 1, qlo = w + s.pad - s.K + 1;
+    plo = plo <= 0 ? 0 : (plo + s.stride - 1) / s.stride;
+    qlo = qlo <= 0 ? 0 : (qlo + s.stride - 1) / s.stride;
+    int phi = (h + s.pad) / s.stride, qhi = (w + s.pad) / s.stride;
+    if (phi > s.P - 1) phi = s.P - 1;
+    if (qhi > s.Q - 1) qhi = s.Q - 1;
+    float acc = 0.f;
+    for (int p = plo; p <= phi; ++p) {
+      for (int q = qlo; q <= qhi; ++q) {
+        const int64_t o = ((static_cast<int64_t>(n) * s.P + p) * s.Q + q) * s.C + c;
+        if (s.mode == 1) {
+          acc += dy[o] * inv;
+          continue;
+        }
+        // first position of the window (row-major) holding the maximum
+        const float m = y[o];
+        const int h0 = p * s.stride - s.pad, w0 = q * s.stride - s.pad;
+        int fh = -1, fw = -1;
+        for (int r = 0; r < s.K && fh < 0; ++r) {
+          const int hh = h0 + r;
+          if (hh < 0 || hh >= s.H) continue;
+          for (int u = 0; u < s.K; ++u) {
+            const int ww = w0 + u;
+            if (ww < 0 || ww >= s.W) continue;
+            if (x[((static_cast<int64_t>(n) * s.H + hh) * s.W + ww) * s.C + c] == m) {
+              fh = hh;
+              fw = ww;
+              break;
+            }
+          }
+        }
+        if (fh == h && fw == w) acc += dy[o];
+      }
+    }
+    dx[i] = accumulate ? dx[i] + acc : acc;
+  }
+}
+
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float lrn_scale(const float* xp, int c, int C, int lo, int hi, float alpha_n, float k) {
+  float s = 0.f;
+  for (int j = c - lo; j <= c + hi; ++j)
+    if (j >= 0 && j < C) s += xp[j] * xp[j];
+  return k + alpha_n * s;
+}
+
+__global__ void lrn_fwd_kernel(const float* __restrict__ x, float* __restrict__ y, int64_t total, int C, int size,
+                               float alpha, float beta, float k) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int lo = size / 2, hi = (size - 1) / 2;
+  const float an = alpha / static_cast<float>(size);
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total; i += stride) {
+    const int c = static_cast<int>(i % C);
+    const float* xp = x + (i - c);
+    const float s = lrn_scale(xp, c, C, lo, hi, an, k);
+    y[i] = x[i] / powf(s, beta);
+  }
+}
+
+__global__ void lrn_bwd_kernel(const float* __restrict__ x, const float* __restrict__ y, const float* __restrict__ dy,
+                               float* dx, int64_t total, int C, int size, float alpha, float beta, float k,
+                               int accumulate) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int lo = size / 2, hi = (size - 1) / 2;
+  const float an = alpha / static_cast<float>(size);
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total; i += stride) {
+    const int ci = static_cast<int>(i % C);
+    const int64_t base = i - ci;
+    const float* xp = x + base;
+    const float si = lrn_scale(xp, ci, C, lo, hi, an, k);
+    float acc = 0.f;
+    // channels c whose window [c-lo, c+hi] contains ci
+    for (int c = ci - hi; c <= ci + lo; ++c) {
+      if (c < 0 || c >= C) continue;
+      const float sc = lrn_scale(xp, c, C, lo, hi, an, k);
+      acc += dy[base + c] * y[base + c] / sc;
+    }
+    const float v = dy[i] / powf(si, beta) - 2.f * an * beta * x[i] * acc;
+    dx[i] = accumulate ? dx[i] + v : v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t mix32(uint32_t v) {
+  v ^= v >> 16;
+  v *= 0x7feb352dU;
+  v ^= v >> 15;
+  v *= 0x846ca68bU;
+  v ^= v >> 16;
+  return v;
+}
+__device__ __forceinline__ bool drop_keep(uint64_t seed, int layer, uint32_t iter, uint32_t idx, uint32_t thresh) {
+  const uint32_t key = mix32(static_cast<uint32_t>(seed) ^ mix32(static_cast<uint32_t>(seed >> 32) ^
+                                                               mix32(iter * 0x9E3779B9U + static_cast<uint32_t>(layer))));
+  return mix32(idx ^ key) >= thresh;
+}
+
+__global__ void dropout_fwd_kernel(const float* __restrict__ x, float* __restrict__ y, int64_t n, uint32_t thresh,
+                                   float scale, uint64_t seed, int layer, const uint32_t* iteration) {
+  const uint32_t it = *iteration;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride)
+    y[i] = drop_keep(seed, layer, it, static_cast<uint32_t>(i), thresh) ? x[i] * scale : 0.f;
+}
+__global__ void dropout_bwd_kernel(float* g, int64_t n, uint32_t thresh, float scale, uint64_t seed, int layer,
+                                   const uint32_t* iteration) {
+  const uint32_t it = *iteration;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride)
+    g[i] = drop_keep(seed, layer, it, static_cast<uint32_t>(i), thresh) ? g[i] * scale : 0.f;
+}
+
+// ---------------------------------------------------------------------------
+// One warp per row.
+__global__ void softmax_fwd_kernel(const float* __restrict__ x, float* __restrict__ y, int B, int F,
+                                   const int32_t* __restrict__ labels, float* loss_rows) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= B) return;
+  const float* xr = x + static_cast<int64_t>(warp) * F;
+  float m = -FLT_MAX;
+  for (int f = lane; f < F; f += 32) m = fmaxf(m, xr[f]);
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  float s = 0.f;
+  for (int f = lane; f < F; f += 32) s += expf(xr[f] - m);
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const float inv = 1.f / s;
+  float* yr = y + static_cast<int64_t>(warp) * F;
+  for (int f = lane; f < F; f += 32) yr[f] = expf(xr[f] - m) * inv;
+  if (lane == 0 && loss_rows) {
+    int lab = labels[warp];
+    lab = lab < 0 ? 0 : (lab >= F ? F - 1 : lab);
+    loss_rows[warp] = logf(s) - (xr[lab] - m);
+  }
+}
+
+__global__ void softmax_bwd_kernel(const float* __restrict__ y, const int32_t* __restrict__ labels, float* dx, int B,
+                                   int F, int accumulate) {
+  const int64_t total = static_cast<int64_t>(B) * F;
+  const float invb = 1.f / static_cast<float>(B);
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total; i += stride) {
+    const int b = static_cast<int>(i / F), f = static_cast<int>(i % F);
+    int lab = labels[b];
+    lab = lab < 0 ? 0 : (lab >= F ? F - 1 : lab);
+    const float v = (y[i] - (f == lab ? 1.f : 0.f)) * invb;
+    dx[i] = accumulate ? dx[i] + v : v;
+  }
+}
+
+__global__ void loss_reduce_kernel(const float* loss_rows, int B, float* loss) {
+  __shared__ double part[256];
+  double a = 0.0;
+  for (int i = threadIdx.x; i < B; i += 256) a += loss_rows[i];
+  part[threadIdx.x] = a;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < 256; ++i) s += part[i];
+    *loss = static_cast<float>(s / B);
+  }
+}
+
+// ---------------------------------------------------------------------------
+__global__ void join_fwd_kernel(const float* const* __restrict__ in, int n_in, float* __restrict__ y, int64_t n) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t n4 = n / 4;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4; i += stride) {
+    float4 acc = reinterpret_cast<const float4*>(in[0])[i];
+    for (int k = 1; k < n_in; ++k) {
+      const float4 v = reinterpret_cast<const float4*>(in[k])[i];
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    reinterpret_cast<float4*>(y)[i] = acc;
+  }
+  for (int64_t i = n4 * 4 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride) {
+    float acc = in[0][i];
+    for (int k = 1; k < n_in; ++k) acc += in[k][i];
+    y[i] = acc;
+  }
+}
+
+__global__ void grad_copy_kernel(const float* __restrict__ src, float* dst, int64_t n, int accumulate) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t n4 = n / 4;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4; i += stride) {
+    float4 v = reinterpret_cast<const float4*>(src)[i];
+    if (accumulate) {
+      const float4 o = reinterpret_cast<const float4*>(dst)[i];
+      v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+    }
+    reinterpret_cast<float4*>(dst)[i] = v;
+  }
+  for (int64_t i = n4 * 4 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride)
+    dst[i] = accumulate ? dst[i] + src[i] : src[i];
+}
+
+__global__ void sgd_kernel(float* p, const float* __restrict__ g, int64_t n, float lr, float scale) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride)
+    p[i] -= lr * (g[i] * scale);
+}
+
+__global__ void bump_kernel(uint32_t* it) { *it += 1; }
+
+__global__ void zero_kernel(float* p, int64_t n) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride) p[i] = 0.f;
+}
+
+}  // namespace
+
+int64_t red_scratch_floats(int C) {
+  // kRedChunks*2*C partial doubles + 2*C sums + 2*C float coefficients
+  return (static_cast<int64_t>(kRedChunks) * 2 * C + 2 * C) * 2 + 2 * C + 64;
+}
+
+cudaError_t bias_grad(const float* dy, int64_t rows, int C, float* db, float* red_scratch, cudaStream_t st) {
+  double* sums;
+  cudaError_t e = colred(RedBiasOp{dy}, rows, C, red_scratch, &sums, st);
+  if (e != cudaSuccess) return e;
+  bias_finalize<<<(C + 255) / 256, 256, 0, st>>>(sums, C, db);
+  return cudaGetLastError();
+}
+
+cudaError_t bn_fwd(const float* x, int64_t rows, int C, const float* gamma, const float* beta, float* y, float* stats,
+                   float* running, float eps, float momentum, int compute_stats, float* red_scratch, cudaStream_t st) {
+  cudaError_t e;
+  if (compute_stats) {
+    double* sums;
+    e = colred(RedBnStatsOp{x}, rows, C, red_scratch, &sums, st);
+    if (e != cudaSuccess) return e;
+    bn_stats_finalize<<<(C + 255) / 256, 256, 0, st>>>(sums, x, rows, C, eps, momentum, stats, running);
+  }
+  const int64_t n = rows * C;
+  if (C % 4 == 0)
+    bn_apply_kernel<4><<<blocks_for(n / 4), kThreads, 0, st>>>(x, n, C, gamma, beta, stats, y);
+  else
+    bn_apply_kernel<1><<<blocks_for(n), kThreads, 0, st>>>(x, n, C, gamma, beta, stats, y);
+  return cudaGetLastError();
+}
+
+cudaError_t bn_bwd(const float* x, const float* dy, int64_t rows, int C, const float* gamma, const float* stats,
+                   float* dx, int accumulate, float* dgamma, float* dbeta, float* red_scratch, cudaStream_t st) {
+  double* sums;
+  cudaError_t e = colred(RedBnBwdOp{x, dy, stats}, rows, C, red_scratch, &sums, st);
+  if (e != cudaSuccess) return e;
+  float* coef = reinterpret_cast<float*>(sums + 2 * C);
+  bn_bwd_finalize<<<(C + 255) / 256, 256, 0, st>>>(sums, C, dgamma, dbeta, coef);
+  const int64_t n = rows * C;
+  if (dx) {
+    if (C % 4 == 0)
+      bn_dx_kernel<4><<<blocks_for(n / 4), kThreads, 0, st>>>(x, dy, n, rows, C, gamma, stats, coef, dx, accumulate);
+    else
+      bn_dx_kernel<1><<<blocks_for(n), kThreads, 0, st>>>(x, dy, n, rows, C, gamma, stats, coef, dx, accumulate);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t relu_fwd(const float* x, float* y, int64_t n, cudaStream_t st) {
+  const int64_t n4 = n / 4;
+  if (n4) relu_fwd_kernel<<<blocks_for(n4), kThreads, 0, st>>>(reinterpret_cast<const float4*>(x),
+                                                                   reinterpret_cast<float4*>(y), n4);
+  if (n % 4) relu_fwd_tail<<<1, 4, 0, st>>>(x, y, n4 * 4, n);
+  return cudaGetLastError();
+}
+
+cudaError_t relu_bwd_inplace(const float* y, float* g, int64_t n, cudaStream_t st) {
+  const int64_t n4 = n / 4;
+  if (n4) relu_bwd_kernel<<<blocks_for(n4), kThreads, 0, st>>>(reinterpret_cast<const float4*>(y),
+                                                                   reinterpret_cast<float4*>(g), n4);
+  if (n % 4) relu_bwd_tail<<<1, 4, 0, st>>>(y, g, n4 * 4, n);
+  return cudaGetLastError();
+}
+
+cudaError_t pool_fwd(const PoolShape& s, const float* x, float* y, cudaStream_t st) {
+  const int64_t total = static_cast<int64_t>(s.N) * s.P * s.Q * s.C;
+  pool_fwd_kernel<<<blocks_for(total), kThreads, 0, st>>>(s, x, y, total);
+  return cudaGetLastError();
+}
+
+cudaError_t pool_bwd(const PoolShape& s, const float* x, const float* y, const float* dy, float* dx, int accumulate,
+                     cudaStream_t st) {
+  const int64_t total = static_cast<int64_t>(s.N) * s.H * s.W * s.C;
+  pool_bwd_kernel<<<blocks_for(total), kThreads, 0, st>>>(s, x, y, dy, dx, accumulate, total);
+  return cudaGetLastError();
+}
+
+cudaError_t lrn_fwd(const float* x, float* y, int64_t pixels, int C, int size, float alpha, float beta, float k,
+                    cudaStream_t st) {
+  const int64_t total = pixels * C;
+  lrn_fwd_kernel<<<blocks_for(total), kThreads, 0, st>>>(x, y, total, C, size, alpha, beta, k);
+  return cudaGetLastError();
+}
+
+cudaError_t lrn_bwd(const float* x, const float* y, const float* dy, float* dx, int64_t pixels, int C, int size,
+                    float alpha, float beta, float k, int accumulate, cudaStream_t st) {
+  const int64_t total = pixels * C;
+  lrn_bwd_kernel<<<blocks_for(total), kThreads, 0, st>>>(x, y, dy, dx, total, C, size, alpha, beta, k, accumulate);
+  return cudaGetLastError();
+}
+
+static uint32_t drop_thresh(float rate) {
+  double t = static_cast<double>(rate) * 4294967296.0;
+  if (t < 0) t = 0;
+  if (t > 4294967295.0) t = 4294967295.0;
+  return static_cast<uint32_t>(t);
+}
+
+cudaError_t dropout_fwd(const float* x, float* y, int64_t n, float rate, uint64_t seed, int layer,
+                        const uint32_t* iteration, cudaStream_t st) {
+  dropout_fwd_kernel<<<blocks_for(n), kThreads, 0, st>>>(x, y, n, drop_thresh(rate), 1.0f / (1.0f - rate), seed, layer,
+                                                         iteration);
+  return cudaGetLastError();
+}
+
+cudaError_t dropout_bwd_inplace(float* g, int64_t n, float rate, uint64_t seed, int layer, const uint32_t* iteration,
+                                cudaStream_t st) {
+  dropout_bwd_kernel<<<blocks_for(n), kThreads, 0, st>>>(g, n, drop_thresh(rate), 1.0f / (1.0f - rate), seed, layer,
+                                                         iteration);
+  return cudaGetLastError();
+}
+
+cudaError_t softmax_fwd(const float* x, float* y, int B, int F, const int32_t* labels, float* loss_rows,
+                        cudaStream_t st) {
+  const int threads = 256;
+  softmax_fwd_kernel<<<(B * 32 + threads - 1) / threads, threads, 0, st>>>(x, y, B, F, labels, loss_rows);
+  return cudaGetLastError();
+}
+
+cudaError_t softmax_ce_bwd(const float* y, const int32_t* labels, float* dx, int B, int F, int accumulate,
+                           cudaStream_t st) {
+  softmax_bwd_kernel<<<blocks_for(static_cast<int64_t>(B) * F), kThreads, 0, st>>>(y, labels, dx, B, F, accumulate);
+  return cudaGetLastError();
+}
+
+cudaError_t loss_reduce(const float* loss_rows, int B, float* loss, cudaStream_t st) {
+  loss_reduce_kernel<<<1, 256, 0, st>>>(loss_rows, B, loss);
+  return cudaGetLastError();
+}
+
+cudaError_t join_fwd(const float* const* inputs, int n_in, float* y, int64_t n, cudaStream_t st) {
+  join_fwd_kernel<<<blocks_for(n / 4 + 1), kThreads, 0, st>>>(inputs, n_in, y, n);
+  return cudaGetLastError();
+}
+
+cudaError_t grad_copy(const float* src, float* dst, int64_t n, int accumulate, cudaStream_t st) {
+  grad_copy_kernel<<<blocks_for(n / 4 + 1), kThreads, 0, st>>>(src, dst, n, accumulate);
+  return cudaGetLastError();
+}
+
+cudaError_t sgd_update(float* params, const float* grads, int64_t n, float lr, float grad_scale, cudaStream_t st) {
+  sgd_kernel<<<blocks_for(n), kThreads, 0, st>>>(params, grads, n, lr, grad_scale);
+  return cudaGetLastError();
+}
+
+cudaError_t bump_iteration(uint32_t* iteration, cudaStream_t st) {
+  bump_kernel<<<1, 1, 0, st>>>(iteration);
+  return cudaGetLastError();
+}
+
+cudaError_t fill_zero(float* p, int64_t n, cudaStream_t st) {
+  zero_kernel<<<blocks_for(n), kThreads, 0, st>>>(p, n);
+  return cudaGetLastError();
+}
+
+}  // namespace sn

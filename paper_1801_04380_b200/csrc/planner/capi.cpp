@@ -4,11 +4,7 @@
 #include <new>
 #include <string>
 
-#include "sim.hpp"
-
-struct sn_plan {
-  snp::Plan plan;
-};
+#include "handle.hpp"
 
 namespace {
 thread_local std::string g_err;

@@ -79,3 +79,78 @@ def test_tc_gemm_unaligned_fallback(cuda):
     rc = lib.sn_test_gemm(1, 1, 64, Ad.data_ptr(), Bd.data_ptr(), D.data_ptr(), M, N, K, M, N, 1)
     assert rc == 0
     _check(D.cpu(), ref, K)
+
+
+# ---------------------------------------------------------------------------
+# Convolution kernels (implicit GEMM on tcgen05) vs torch fp64 on CPU.
+
+CONV_CASES = [
+    # N, C, H, W, K, k, stride, pad
+    (2, 4, 32, 32, 64, 7, 2, 3),     # padded stem (C=3 -> 4)
+    (2, 64, 14, 14, 64, 3, 1, 1),    # resnet stage 1 (C % 32 == 0)
+    (2, 64, 14, 14, 128, 3, 2, 1),   # stride-2 block
+    (2, 96, 13, 13, 256, 5, 1, 2),   # AlexNet conv2 (C = 96)
+    (3, 16, 9, 9, 8, 1, 1, 0),       # 1x1, C % 32 != 0
+    (2, 3, 11, 11, 16, 3, 1, 1),     # C = 3: scalar gather path
+    (1, 32, 20, 20, 96, 11, 4, 0),   # AlexNet-style 11x11 stride 4
+]
+
+
+def _conv_lib():
+    from paper_1801_04380_b200 import _native
+    lib = _native.executor()
+    lib.sn_test_conv.restype = ctypes.c_int
+    lib.sn_test_conv.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_void_p),
+                                 ctypes.c_int]
+    lib.sn_test_red_scratch_floats.restype = ctypes.c_longlong
+    return lib
+
+
+def _shape_arr(N, C, H, W, K, k, s, p):
+    P = (H + 2 * p - k) // s + 1
+    Q = (W + 2 * p - k) // s + 1
+    return (ctypes.c_int * 11)(N, H, W, C, K, k, k, P, Q, s, p), P, Q
+
+
+@pytest.mark.parametrize("case", CONV_CASES)
+def test_conv_fwd_dgrad_wgrad(cuda, case):
+    N, C, H, W, K, k, s, p = case
+    lib = _conv_lib()
+    shape, P, Q = _shape_arr(*case)
+    g = torch.Generator().manual_seed(sum(case))
+    x = torch.randn(N, C, H, W, generator=g)
+    w = torch.randn(K, C, k, k, generator=g) / (C * k * k) ** 0.5
+    b = torch.randn(K, generator=g)
+    dy = torch.randn(N, K, P, Q, generator=g)
+    xd = x.double().requires_grad_(True)
+    wd = w.double().requires_grad_(True)
+    bd = b.double().requires_grad_(True)
+    y = torch.nn.functional.conv2d(xd, wd, bd, stride=s, padding=p)
+    y.backward(dy.double())
+    nhwc = lambda t: t.permute(0, 2, 3, 1).contiguous().to(cuda)
+    x_d, dy_d = nhwc(x), nhwc(dy)
+    w_d = w.permute(0, 2, 3, 1).contiguous().to(cuda)   # KRSC
+    b_d = b.to(cuda)
+    y_d = torch.full((N, P, Q, K), float("nan"), device=cuda)
+    ptrs = (ctypes.c_void_p * 4)(x_d.data_ptr(), w_d.data_ptr(), b_d.data_ptr(), y_d.data_ptr())
+    assert lib.sn_test_conv(0, shape, ptrs, 0) == 0
+    _check(y_d.permute(0, 3, 1, 2).cpu(), y.detach(), C * k * k)
+    # dgrad, overwrite then accumulate
+    wt = torch.empty(K * k * k * C, device=cuda)
+    dx_d = torch.full((N, H, W, C), float("nan"), device=cuda)
+    ptrs = (ctypes.c_void_p * 4)(dy_d.data_ptr(), w_d.data_ptr(), wt.data_ptr(), dx_d.data_ptr())
+    assert lib.sn_test_conv(1, shape, ptrs, 0) == 0
+    _check(dx_d.permute(0, 3, 1, 2).cpu(), xd.grad, K * k * k)
+    assert lib.sn_test_conv(1, shape, ptrs, 1) == 0
+    _check(dx_d.permute(0, 3, 1, 2).cpu(), 2 * xd.grad, K * k * k)
+    # wgrad + bias grad
+    dw_d = torch.full((K, k, k, C), float("nan"), device=cuda)
+    db_d = torch.full((K,), float("nan"), device=cuda)
+    part = torch.empty(64 << 20 // 64, device=cuda)
+    red = torch.empty(int(lib.sn_test_red_scratch_floats(K)), device=cuda)
+    ptrs = (ctypes.c_void_p * 6)(x_d.data_ptr(), dy_d.data_ptr(), dw_d.data_ptr(), db_d.data_ptr(),
+                                 part.data_ptr(), red.data_ptr())
+    for splits in (1, 3):
+        assert lib.sn_test_conv(2, shape, ptrs, splits) == 0
+        _check(dw_d.permute(0, 3, 1, 2).cpu(), wd.grad, N * P * Q)
+        _check(db_d.cpu(), bd.grad, N * P * Q)
