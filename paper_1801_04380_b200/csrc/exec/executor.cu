@@ -101,6 +101,7 @@ struct sn_exec {
   float* partial = nullptr;
   int64_t partial_cap = 0;
   float* red = nullptr;
+  void* pool_scratch = nullptr;
   const float** ptr_table = nullptr;
   std::vector<const float*> ptr_host;
   // host stash
@@ -257,6 +258,10 @@ void alloc_device(sn_exec* ex) {
   ck(cudaMalloc(&ex->partial, ex->partial_cap * sizeof(float)), "cudaMalloc(partial)");
   ck(cudaMalloc(&ex->wt_scratch, std::max<int64_t>(wt, 64) * sizeof(float)), "cudaMalloc(wt)");
   ck(cudaMalloc(&ex->red, red * sizeof(float)), "cudaMalloc(red)");
+  int64_t pool_bytes = 256;
+  for (int i = 0; i < net.n; ++i)
+    if (ex->L[i].kind == snp::POOL) pool_bytes = std::max(pool_bytes, sn::pool_scratch_bytes(ex->L[i].pool));
+  ck(cudaMalloc(&ex->pool_scratch, static_cast<size_t>(pool_bytes)), "cudaMalloc(pool scratch)");
   int data_id = 0;
   for (int i = 0; i < net.n; ++i)
     if (net.kind[i] == snp::DATA) data_id = i;
@@ -570,7 +575,9 @@ struct Compiler {
         int acc = 0;
         float* dx = dx_target(pid, &acc);
         const sn::PoolShape ps = l.pool;
-        if (dx) push([=] { ck(sn::pool_bwd(ps, x, y, dy, dx, acc, st), "pool_bwd"); }, 1);
+        void* scratch = ex->pool_scratch;
+        const int nk = (ps.C % 4 == 0 && ps.mode == 0) ? 2 : 1;
+        if (dx) push([=] { ck(sn::pool_bwd(ps, x, y, dy, dx, acc, scratch, st), "pool_bwd"); }, nk);
         break;
       }
       case snp::LRN: {
@@ -702,7 +709,8 @@ void destroy(sn_exec* ex) {
   for (auto& kv : ex->stash)
     if (kv.second) cudaFreeHost(kv.second);
   void* bufs[] = {ex->arena, ex->params, ex->grads, ex->state, ex->images, ex->labels, ex->loss_rows, ex->loss,
-                  ex->iteration, ex->wt_scratch, ex->partial, ex->red, const_cast<float**>(ex->ptr_table)};
+                  ex->iteration, ex->wt_scratch, ex->partial, ex->red, ex->pool_scratch,
+                  const_cast<float**>(ex->ptr_table)};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (ex->s0) cudaStreamDestroy(ex->s0);

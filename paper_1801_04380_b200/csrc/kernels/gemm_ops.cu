@@ -12,6 +12,7 @@
 // fixed order by splitk_reduce (deterministic: the same split count gives
 // bit-identical gradients on every replay of the schedule).
 #include <algorithm>
+#include <cstdlib>
 
 #include "gemm_tc.cuh"
 #include "kernels.hpp"
@@ -259,43 +260,6 @@ struct WgradA {
   }
 };
 
-// Row-major epilogue with per-column bias and optional accumulate.
-struct EpiStore {
-  float* D;
-  const float* bias;
-  int M, N, ldd, accumulate;
-  __device__ void store(int m, int n0, const float* v, int) const {
-    if (m >= M) return;
-    float* d = D + static_cast<size_t>(m) * ldd;
-    if ((N & 3) == 0 && n0 + 32 <= N) {
-#pragma unroll
-      for (int j = 0; j < 32; j += 4) {
-        float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-        if (bias) {
-          const float4 b = *reinterpret_cast<const float4*>(bias + n0 + j);
-          o.x += b.x; o.y += b.y; o.z += b.z; o.w += b.w;
-        }
-        float4* dp = reinterpret_cast<float4*>(d + n0 + j);
-        if (accumulate) {
-          const float4 old = *dp;
-          o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
-        }
-        *dp = o;
-      }
-      return;
-    }
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const int n = n0 + j;
-      if (n < N) {
-        float o = v[j];
-        if (bias) o += bias[n];
-        d[n] = accumulate ? d[n] + o : o;
-      }
-    }
-  }
-};
-
 // D[M][N] = sum_split P[split][M][N] (+bias[n]) (+D if accumulate); optionally
 // written transposed (D^T[N][M], for wgrad partials laid out [rsc][k]).
 __global__ void splitk_reduce_kernel(const float* __restrict__ P, int splits, int M, int N, float* D,
@@ -341,14 +305,17 @@ cudaError_t splitk_reduce(const float* P, int splits, int M, int N, float* D, co
   return cudaGetLastError();
 }
 
-// wt[c][r][s][k] = w[k][r][s][c]
-__global__ void transpose_w_kernel(const float* __restrict__ w, float* __restrict__ wt, int K, int RS, int C) {
+// wt[c][rs'][k] = w[k][rs][c] with rs' = rs (flip = 0) or RS-1-rs (flip = 1,
+// the rotated filter of the stride-1 dgrad-as-forward-convolution).
+__global__ void transpose_w_kernel(const float* __restrict__ w, float* __restrict__ wt, int K, int RS, int C,
+                                   int flip) {
   __shared__ float tile[32][33];
-  const int rs = blockIdx.z;
+  const int rs_in = blockIdx.z;
+  const int rs = flip ? RS - 1 - rs_in : rs_in;
   const int k0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
   for (int i = threadIdx.y; i < 32; i += 8) {
     const int k = k0 + i, c = c0 + threadIdx.x;
-    tile[i][threadIdx.x] = (k < K && c < C) ? w[(static_cast<size_t>(k) * RS + rs) * C + c] : 0.f;
+    tile[i][threadIdx.x] = (k < K && c < C) ? w[(static_cast<size_t>(k) * RS + rs_in) * C + c] : 0.f;
   }
   __syncthreads();
   for (int i = threadIdx.y; i < 32; i += 8) {
@@ -430,8 +397,19 @@ int bn_for(int n) { return n <= 64 ? 64 : (n <= 128 ? 128 : 256); }
 
 }  // namespace
 
+static int g_use_tma = -1;  // SN_CONV_TMA=0 forces the cp.async gather path (tests, A/B)
+bool use_tma() {
+  if (g_use_tma < 0) {
+    const char* v = std::getenv("SN_CONV_TMA");
+    g_use_tma = (v && v[0] == '0') ? 0 : 1;
+  }
+  return g_use_tma == 1;
+}
+void set_conv_tma(int on) { g_use_tma = on ? 1 : 0; }
+
 cudaError_t conv_fwd(const ConvShape& s, const float* x, const float* w, const float* bias, float* y,
                      cudaStream_t st) {
+  if (use_tma() && conv_tma_ok_fwd(s)) return conv_fwd_tma(s, x, w, bias, y, st);
   switch (bn_for(s.K)) {
     case 64: return conv_fwd_bn<64>(s, x, w, bias, y, st);
     case 128: return conv_fwd_bn<128>(s, x, w, bias, y, st);
@@ -442,9 +420,11 @@ cudaError_t conv_fwd(const ConvShape& s, const float* x, const float* w, const f
 cudaError_t conv_dgrad(const ConvShape& s, const float* dy, const float* w, float* wt, float* dx, int accumulate,
                        cudaStream_t st) {
   dim3 grid((s.C + 31) / 32, (s.K + 31) / 32, s.R * s.S), block(32, 8);
-  transpose_w_kernel<<<grid, block, 0, st>>>(w, wt, s.K, s.R * s.S, s.C);
+  const bool tma = use_tma() && conv_tma_ok_dgrad(s);
+  transpose_w_kernel<<<grid, block, 0, st>>>(w, wt, s.K, s.R * s.S, s.C, tma ? 1 : 0);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
+  if (tma) return conv_dgrad_tma(s, dy, wt, dx, accumulate, st);
   switch (bn_for(s.C)) {
     case 64: return conv_dgrad_bn<64>(s, dy, wt, dx, accumulate, st);
     case 128: return conv_dgrad_bn<128>(s, dy, wt, dx, accumulate, st);
@@ -468,10 +448,15 @@ int conv_wgrad_splits(const ConvShape& s, int64_t partial_floats_cap) {
 cudaError_t conv_wgrad(const ConvShape& s, const float* x, const float* dy, float* dw, float* db, float* partial,
                        int splits, float* red_scratch, cudaStream_t st) {
   cudaError_t e;
-  switch (bn_for(s.K)) {
-    case 64: e = conv_wgrad_bn<64>(s, x, dy, partial, splits, st); break;
-    case 128: e = conv_wgrad_bn<128>(s, x, dy, partial, splits, st); break;
-    default: e = conv_wgrad_bn<256>(s, x, dy, partial, splits, st); break;
+  splits = effective_splits(s.N * s.P * s.Q, splits);  // the count the launch will really use
+  if (use_tma() && conv_tma_ok_wgrad(s)) {
+    e = conv_wgrad_tma(s, x, dy, partial, splits, st);
+  } else {
+    switch (bn_for(s.K)) {
+      case 64: e = conv_wgrad_bn<64>(s, x, dy, partial, splits, st); break;
+      case 128: e = conv_wgrad_bn<128>(s, x, dy, partial, splits, st); break;
+      default: e = conv_wgrad_bn<256>(s, x, dy, partial, splits, st); break;
+    }
   }
   if (e != cudaSuccess) return e;
   const int RSC = s.R * s.S * s.C;

@@ -82,3 +82,6 @@ extern "C" int sn_test_wgrad_splits(const int* shape) {
 }
 
 extern "C" long long sn_test_red_scratch_floats(int C) { return sn::red_scratch_floats(C); }
+
+// 1: TMA-fed conv kernels where the shape allows (default), 0: cp.async gathers.
+extern "C" void sn_test_set_conv_tma(int on) { sn::set_conv_tma(on); }

@@ -286,6 +286,43 @@ struct EpiRowMajor {
   }
 };
 
+// Row-major epilogue with per-column bias and optional accumulate.
+struct EpiStore {
+  float* D;
+  const float* bias;
+  int M, N, ldd, accumulate;
+  __device__ void store(int m, int n0, const float* v, int) const {
+    if (m >= M) return;
+    float* d = D + static_cast<size_t>(m) * ldd;
+    if ((N & 3) == 0 && n0 + 32 <= N) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 4) {
+        float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        if (bias) {
+          const float4 b = *reinterpret_cast<const float4*>(bias + n0 + j);
+          o.x += b.x; o.y += b.y; o.z += b.z; o.w += b.w;
+        }
+        float4* dp = reinterpret_cast<float4*>(d + n0 + j);
+        if (accumulate) {
+          const float4 old = *dp;
+          o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
+        }
+        *dp = o;
+      }
+      return;
+    }
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int n = n0 + j;
+      if (n < N) {
+        float o = v[j];
+        if (bias) o += bias[n];
+        d[n] = accumulate ? d[n] + o : o;
+      }
+    }
+  }
+};
+
 // Split-K partial store: P[split][m][n] (no bias, no accumulation).
 struct EpiPartial {
   float* P;

@@ -26,6 +26,19 @@ int conv_wgrad_splits(const ConvShape& s, int64_t partial_floats_cap);
 cudaError_t conv_wgrad(const ConvShape& s, const float* x, const float* dy, float* dw, float* db,
                        float* partial, int splits, float* red_scratch, cudaStream_t st);
 
+// TMA-fed variants (conv_tma.cu); conv_fwd/conv_dgrad/conv_wgrad dispatch to
+// them when the shapes allow (C % 32 == 0; dgrad stride 1) unless SN_CONV_TMA=0.
+bool conv_tma_ok_fwd(const ConvShape& s);
+bool conv_tma_ok_dgrad(const ConvShape& s);
+bool conv_tma_ok_wgrad(const ConvShape& s);
+cudaError_t conv_fwd_tma(const ConvShape& s, const float* x, const float* w, const float* bias, float* y,
+                         cudaStream_t st);
+cudaError_t conv_dgrad_tma(const ConvShape& s, const float* dy, const float* wt_flip, float* dx, int accumulate,
+                           cudaStream_t st);
+cudaError_t conv_wgrad_tma(const ConvShape& s, const float* x, const float* dy, float* partial, int splits,
+                           cudaStream_t st);
+void set_conv_tma(int on);
+
 // FC: x[B][I], w[O][I], y[B][O]
 int fc_splits(int B, int I, int O, int64_t partial_floats_cap);
 cudaError_t fc_fwd(int B, int I, int O, const float* x, const float* w, const float* bias, float* y,
@@ -59,8 +72,12 @@ struct PoolShape {
   int N, H, W, C, P, Q, K, stride, pad, mode;  // mode 0 max, 1 avg
 };
 cudaError_t pool_fwd(const PoolShape& s, const float* x, float* y, cudaStream_t st);
+// Max-pool backward recomputes each window's first argmax from x and y (the
+// reference's backward reads) into a byte per output (executor scratch of
+// pool_scratch_bytes), then gathers; avg-pool gathers directly.
+int64_t pool_scratch_bytes(const PoolShape& s);
 cudaError_t pool_bwd(const PoolShape& s, const float* x, const float* y, const float* dy, float* dx,
-                     int accumulate, cudaStream_t st);
+                     int accumulate, void* scratch, cudaStream_t st);
 
 cudaError_t lrn_fwd(const float* x, float* y, int64_t pixels, int C, int size, float alpha, float beta,
                     float k, cudaStream_t st);

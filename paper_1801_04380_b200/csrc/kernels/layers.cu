@@ -304,6 +304,87 @@ __global__ void pool_bwd_kernel(PoolShape s, const float* __restrict__ x, const 
   }
 }
 
+// Max-pool backward, pass 1: for every output, the window offset r*K+s of the
+// first element (row-major) equal to the forward maximum y (255: none).
+// Vectorised over 4 channels.
+__global__ void pool_argmax_kernel(PoolShape s, const float* __restrict__ x, const float* __restrict__ y,
+                                   uchar4* __restrict__ arg, int64_t total4) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int C4 = s.C / 4;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total4; i += stride) {
+    const int c4 = static_cast<int>(i % C4);
+    int64_t t = i / C4;
+    const int q = static_cast<int>(t % s.Q);
+    t /= s.Q;
+    const int p = static_cast<int>(t % s.P);
+    const int n = static_cast<int>(t / s.P);
+    const float4 m = reinterpret_cast<const float4*>(y)[i];
+    const int h0 = p * s.stride - s.pad, w0 = q * s.stride - s.pad;
+    int a0 = 255, a1 = 255, a2 = 255, a3 = 255;
+    for (int r = 0; r < s.K; ++r) {
+      const int h = h0 + r;
+      if (h < 0 || h >= s.H) continue;
+      for (int u = 0; u < s.K; ++u) {
+        const int w = w0 + u;
+        if (w < 0 || w >= s.W) continue;
+        const float4 v = reinterpret_cast<const float4*>(x)[((static_cast<int64_t>(n) * s.H + h) * s.W + w) * C4 + c4];
+        const int off = r * s.K + u;
+        if (a0 == 255 && v.x == m.x) a0 = off;
+        if (a1 == 255 && v.y == m.y) a1 = off;
+        if (a2 == 255 && v.z == m.z) a2 = off;
+        if (a3 == 255 && v.w == m.w) a3 = off;
+      }
+    }
+    arg[i] = make_uchar4(a0, a1, a2, a3);
+  }
+}
+
+// Pass 2 (and the whole of avg-pool backward): gather over the <= ceil(K/s)^2
+// windows covering each input element.
+__global__ void pool_gather_kernel(PoolShape s, const uchar4* __restrict__ arg, const float* __restrict__ dy,
+                                   float* dx, int accumulate, int64_t total4) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int C4 = s.C / 4;
+  const float inv = 1.0f / static_cast<float>(s.K * s.K);
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total4; i += stride) {
+    const int c4 = static_cast<int>(i % C4);
+    int64_t t = i / C4;
+    const int w = static_cast<int>(t % s.W);
+    t /= s.W;
+    const int h = static_cast<int>(t % s.H);
+    const int n = static_cast<int>(t / s.H);
+    int plo = h + s.pad - s.K + 1, qlo = w + s.pad - s.K + 1;
+    plo = plo <= 0 ? 0 : (plo + s.stride - 1) / s.stride;
+    qlo = qlo <= 0 ? 0 : (qlo + s.stride - 1) / s.stride;
+    int phi = (h + s.pad) / s.stride, qhi = (w + s.pad) / s.stride;
+    if (phi > s.P - 1) phi = s.P - 1;
+    if (qhi > s.Q - 1) qhi = s.Q - 1;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int p = plo; p <= phi; ++p) {
+      for (int q = qlo; q <= qhi; ++q) {
+        const int64_t o = ((static_cast<int64_t>(n) * s.P + p) * s.Q + q) * C4 + c4;
+        const float4 g = reinterpret_cast<const float4*>(dy)[o];
+        if (s.mode == 1) {
+          acc.x += g.x * inv; acc.y += g.y * inv; acc.z += g.z * inv; acc.w += g.w * inv;
+          continue;
+        }
+        const int off = (h - (p * s.stride - s.pad)) * s.K + (w - (q * s.stride - s.pad));
+        const uchar4 a = arg[o];
+        if (a.x == off) acc.x += g.x;
+        if (a.y == off) acc.y += g.y;
+        if (a.z == off) acc.z += g.z;
+        if (a.w == off) acc.w += g.w;
+      }
+    }
+    float4* d = reinterpret_cast<float4*>(dx) + i;
+    if (accumulate) {
+      const float4 o = *d;
+      acc.x += o.x; acc.y += o.y; acc.z += o.z; acc.w += o.w;
+    }
+    *d = acc;
+  }
+}
+
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ float lrn_scale(const float* xp, int c, int C, int lo, int hi, float alpha_n, float k) {
   float s = 0.f;
@@ -546,8 +627,20 @@ cudaError_t pool_fwd(const PoolShape& s, const float* x, float* y, cudaStream_t 
   return cudaGetLastError();
 }
 
+int64_t pool_scratch_bytes(const PoolShape& s) {
+  return (s.C % 4 == 0 && s.mode == 0 && s.K * s.K < 255) ? static_cast<int64_t>(s.N) * s.P * s.Q * s.C : 0;
+}
+
 cudaError_t pool_bwd(const PoolShape& s, const float* x, const float* y, const float* dy, float* dx, int accumulate,
-                     cudaStream_t st) {
+                     void* scratch, cudaStream_t st) {
+  if (s.C % 4 == 0 && (s.mode == 1 || (scratch && s.K * s.K < 255))) {
+    const int64_t in4 = static_cast<int64_t>(s.N) * s.H * s.W * s.C / 4;
+    const int64_t out4 = static_cast<int64_t>(s.N) * s.P * s.Q * s.C / 4;
+    uchar4* arg = reinterpret_cast<uchar4*>(scratch);
+    if (s.mode == 0) pool_argmax_kernel<<<blocks_for(out4), kThreads, 0, st>>>(s, x, y, arg, out4);
+    pool_gather_kernel<<<blocks_for(in4), kThreads, 0, st>>>(s, arg, dy, dx, accumulate, in4);
+    return cudaGetLastError();
+  }
   const int64_t total = static_cast<int64_t>(s.N) * s.H * s.W * s.C;
   pool_bwd_kernel<<<blocks_for(total), kThreads, 0, st>>>(s, x, y, dy, dx, accumulate, total);
   return cudaGetLastError();

@@ -105,13 +105,17 @@ def param_layout(net: NetworkDef, shapes: dict[int, tuple[int, ...]]) -> dict[in
     return out
 
 
-def init_parameters(net: NetworkDef, seed: int = 2) -> dict[int, dict]:
+def init_parameters(net: NetworkDef, seed: int = 2, head_scale: float = 1.0) -> dict[int, dict]:
     """He-uniform CONV/FC weights (bound sqrt(6/fan_in)), small uniform biases,
-    BN gamma = 1 / beta = 0; torch CPU generator, layer order."""
+    BN gamma = 1 / beta = 0; torch CPU generator, layer order.  ``head_scale``
+    multiplies the classifier (the FC feeding the terminal SOFTMAX): small
+    values keep the initial softmax away from saturation, which keeps
+    gradient comparisons well conditioned."""
     import torch
     from .costmodel import propagate_shapes
     shapes = propagate_shapes(net)
     g = torch.Generator().manual_seed(seed)
+    head = {p for l in net.layers if l.kind is LayerKind.SOFTMAX for p in l.prev}
     params: dict[int, dict] = {}
     for lid, spec in param_layout(net, shapes).items():
         kind = net.layers[lid].kind
@@ -122,6 +126,8 @@ def init_parameters(net: NetworkDef, seed: int = 2) -> dict[int, dict]:
         bound = math.sqrt(6.0 / fan_in)
         w = (torch.rand(spec["w"], generator=g) * 2 - 1) * bound
         b = (torch.rand(spec["b"], generator=g) * 2 - 1) / math.sqrt(fan_in)
+        if lid in head:
+            w, b = w * head_scale, b * head_scale
         params[lid] = {"w": w, "b": b}
     return params
 

