@@ -419,6 +419,7 @@ cudaError_t conv_fwd(const ConvShape& s, const float* x, const float* w, const f
 
 cudaError_t conv_dgrad(const ConvShape& s, const float* dy, const float* w, float* wt, float* dx, int accumulate,
                        cudaStream_t st) {
+  if (use_tma() && conv_tma_ok_dgrad_strided(s)) return conv_dgrad_strided_tma(s, dy, w, wt, dx, accumulate, st);
   dim3 grid((s.C + 31) / 32, (s.K + 31) / 32, s.R * s.S), block(32, 8);
   const bool tma = use_tma() && conv_tma_ok_dgrad(s);
   transpose_w_kernel<<<grid, block, 0, st>>>(w, wt, s.K, s.R * s.S, s.C, tma ? 1 : 0);
@@ -438,7 +439,9 @@ int conv_wgrad_splits(const ConvShape& s, int64_t partial_floats_cap) {
   const int64_t tiles = ((RSC + kBM - 1) / kBM) * ((s.K + bn - 1) / bn);
   const int64_t NPQ = static_cast<int64_t>(s.N) * s.P * s.Q;
   const int64_t nkb = (NPQ + kBK - 1) / kBK;
-  int64_t want = (2 * 148 + tiles - 1) / tiles;
+  // Fill exactly one wave of resident CTAs (2 per SM for N tiles <= 128).
+  const int64_t slots = 148 * (bn <= 128 ? 2 : 1);
+  int64_t want = std::max<int64_t>(1, slots / tiles);
   want = std::min<int64_t>(want, std::max<int64_t>(1, nkb / 8));
   const int64_t per = RSC * s.K;
   want = std::min<int64_t>(want, std::max<int64_t>(1, partial_floats_cap / per));

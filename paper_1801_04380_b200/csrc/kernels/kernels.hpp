@@ -37,6 +37,9 @@ cudaError_t conv_dgrad_tma(const ConvShape& s, const float* dy, const float* wt_
                            cudaStream_t st);
 cudaError_t conv_wgrad_tma(const ConvShape& s, const float* x, const float* dy, float* partial, int splits,
                            cudaStream_t st);
+bool conv_tma_ok_dgrad_strided(const ConvShape& s);
+cudaError_t conv_dgrad_strided_tma(const ConvShape& s, const float* dy, const float* w, float* wt_scratch, float* dx,
+                                   int accumulate, cudaStream_t st);
 void set_conv_tma(int on);
 
 // FC: x[B][I], w[O][I], y[B][O]

@@ -25,11 +25,17 @@ inline int blocks_for(int64_t n, int per_block = kThreads, int cap = 148 * 16) {
 // (doubles); stage 2 sums the blocks in order.  Two sums per channel:
 // f1 and f2 of the functor.
 
+__device__ __forceinline__ float4 ld4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+
 struct RedBiasOp {  // f1 = dy
   const float* dy;
   __device__ void eval(int64_t row, int c, int C, float& a, float& b) const {
     a = dy[row * C + c];
     b = 0.f;
+  }
+  __device__ void eval4(int64_t row, int c, int C, float4& a, float4& b) const {
+    a = ld4(dy + row * C + c);
+    b = make_float4(0.f, 0.f, 0.f, 0.f);
   }
 };
 struct RedBnStatsOp {  // f1 = x - x[0][c], f2 = (x - x[0][c])^2
@@ -38,6 +44,11 @@ struct RedBnStatsOp {  // f1 = x - x[0][c], f2 = (x - x[0][c])^2
     const float d = x[row * C + c] - x[c];
     a = d;
     b = d * d;
+  }
+  __device__ void eval4(int64_t row, int c, int C, float4& a, float4& b) const {
+    const float4 v = ld4(x + row * C + c), s = ld4(x + c);
+    a = make_float4(v.x - s.x, v.y - s.y, v.z - s.z, v.w - s.w);
+    b = make_float4(a.x * a.x, a.y * a.y, a.z * a.z, a.w * a.w);
   }
 };
 struct RedBnBwdOp {  // f1 = dy, f2 = dy * xhat
@@ -50,7 +61,58 @@ struct RedBnBwdOp {  // f1 = dy, f2 = dy * xhat
     a = g;
     b = g * xh;
   }
+  __device__ void eval4(int64_t row, int c, int C, float4& a, float4& b) const {
+    const float4 g = ld4(dy + row * C + c), v = ld4(x + row * C + c);
+    const float4 m = ld4(stats + c), is = ld4(stats + C + c);
+    a = g;
+    b = make_float4(g.x * ((v.x - m.x) * is.x), g.y * ((v.y - m.y) * is.y), g.z * ((v.z - m.z) * is.z),
+                    g.w * ((v.w - m.w) * is.w));
+  }
 };
+
+// float4 variant for C % 4 == 0: a thread owns 4 adjacent channels and 4
+// independent row streams in flight (fixed per-thread order, fixed merge).
+template <class Op>
+__global__ void colred_stage1_v4(Op op, int64_t rows, int C, int64_t chunk, double* part) {
+  __shared__ float4 s1[kThreads], s2[kThreads];
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * chunk;
+  const int64_t r1 = r0 + chunk < rows ? r0 + chunk : rows;
+  const int C4 = C / 4;
+  const int cb = C4 < kThreads ? C4 : kThreads;
+  const int lanes = kThreads / cb;
+  const int t = threadIdx.x;
+  const int lane = t / cb, cc = t % cb;
+  for (int c0 = 0; c0 < C4; c0 += cb) {
+    const int c4 = c0 + cc;
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+    if (lane < lanes && c4 < C4) {
+      for (int64_t r = r0 + lane; r < r1; r += lanes) {
+        float4 fa, fb;
+        op.eval4(r, c4 * 4, C, fa, fb);
+        a.x += fa.x; a.y += fa.y; a.z += fa.z; a.w += fa.w;
+        b.x += fb.x; b.y += fb.y; b.z += fb.z; b.w += fb.w;
+      }
+    }
+    s1[t] = a;
+    s2[t] = b;
+    __syncthreads();
+    if (lane == 0 && c4 < C4) {
+      double A[4] = {0, 0, 0, 0}, Bv[4] = {0, 0, 0, 0};
+      for (int l = 0; l < lanes; ++l) {
+        const float4 x = s1[l * cb + cc], y = s2[l * cb + cc];
+        A[0] += x.x; A[1] += x.y; A[2] += x.z; A[3] += x.w;
+        Bv[0] += y.x; Bv[1] += y.y; Bv[2] += y.z; Bv[3] += y.w;
+      }
+      double* pa = part + (static_cast<size_t>(blockIdx.x) * 2) * C + c4 * 4;
+      double* pb = part + (static_cast<size_t>(blockIdx.x) * 2 + 1) * C + c4 * 4;
+      for (int e = 0; e < 4; ++e) {
+        pa[e] = A[e];
+        pb[e] = Bv[e];
+      }
+    }
+    __syncthreads();
+  }
+}
 
 template <class Op>
 __global__ void colred_stage1(Op op, int64_t rows, int C, int64_t chunk, double* part) {
@@ -88,16 +150,32 @@ __global__ void colred_stage1(Op op, int64_t rows, int C, int64_t chunk, double*
   }
 }
 
+// 32 channels per block (lane = channel), 8 warps take interleaved stage-1
+// blocks, then warp sums are combined in warp order: fixed order, so the result
+// is deterministic.
 __global__ void colred_stage2(const double* part, int nblocks, int C, double* out) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= C) return;
+  __shared__ double sa[8][32], sb[8][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane;
   double A = 0.0, B = 0.0;
-  for (int b = 0; b < nblocks; ++b) {
-    A += part[(static_cast<size_t>(b) * 2) * C + c];
-    B += part[(static_cast<size_t>(b) * 2 + 1) * C + c];
+  if (c < C) {
+    for (int b = w; b < nblocks; b += 8) {
+      A += part[(static_cast<size_t>(b) * 2) * C + c];
+      B += part[(static_cast<size_t>(b) * 2 + 1) * C + c];
+    }
   }
-  out[c] = A;
-  out[C + c] = B;
+  sa[w][lane] = A;
+  sb[w][lane] = B;
+  __syncthreads();
+  if (w == 0 && c < C) {
+    double a = 0.0, b = 0.0;
+    for (int i = 0; i < 8; ++i) {
+      a += sa[i][lane];
+      b += sb[i][lane];
+    }
+    out[c] = a;
+    out[C + c] = b;
+  }
 }
 
 // Runs both stages; result sums land in sums[0..2C) (doubles) inside scratch.
@@ -109,9 +187,12 @@ cudaError_t colred(Op op, int64_t rows, int C, float* scratch_f, double** sums_o
   const int64_t chunk = (rows + nb - 1) / nb;
   nb = (rows + chunk - 1) / chunk;
   if (nb < 1) nb = 1;
-  colred_stage1<<<static_cast<int>(nb), kThreads, 0, st>>>(op, rows, C, chunk, part);
+  if (C % 4 == 0)
+    colred_stage1_v4<<<static_cast<int>(nb), kThreads, 0, st>>>(op, rows, C, chunk, part);
+  else
+    colred_stage1<<<static_cast<int>(nb), kThreads, 0, st>>>(op, rows, C, chunk, part);
   double* sums = part + static_cast<size_t>(kRedChunks) * 2 * C;
-  colred_stage2<<<(C + 255) / 256, 256, 0, st>>>(part, static_cast<int>(nb), C, sums);
+  colred_stage2<<<(C + 31) / 32, 256, 0, st>>>(part, static_cast<int>(nb), C, sums);
   *sums_out = sums;
   return cudaGetLastError();
 }
@@ -254,6 +335,45 @@ __global__ void pool_fwd_kernel(PoolShape s, const float* __restrict__ x, float*
   }
 }
 
+// float4 over channels (C % 4 == 0); 32-bit index math (tensors < 2^31 elements).
+__global__ void pool_fwd_v4_kernel(PoolShape s, const float4* __restrict__ x, float4* __restrict__ y, int total4) {
+  const int C4 = s.C >> 2;
+  const float inv = 1.0f / static_cast<float>(s.K * s.K);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total4; i += gridDim.x * blockDim.x) {
+    const int c4 = i % C4;
+    int t = i / C4;
+    const int q = t % s.Q;
+    t /= s.Q;
+    const int p = t % s.P;
+    const int n = t / s.P;
+    const int h0 = p * s.stride - s.pad, w0 = q * s.stride - s.pad;
+    const int hb = h0 < 0 ? 0 : h0, he = min(h0 + s.K, s.H);
+    const int wb = w0 < 0 ? 0 : w0, we = min(w0 + s.K, s.W);
+    const float4* xb = x + static_cast<size_t>(n) * s.H * s.W * C4 + c4;
+    float4 acc;
+    if (s.mode == 0) {
+      acc = xb[(hb * s.W + wb) * C4];
+      for (int h = hb; h < he; ++h)
+        for (int w = wb; w < we; ++w) {
+          const float4 v = xb[(h * s.W + w) * C4];
+          acc.x = v.x > acc.x ? v.x : acc.x;
+          acc.y = v.y > acc.y ? v.y : acc.y;
+          acc.z = v.z > acc.z ? v.z : acc.z;
+          acc.w = v.w > acc.w ? v.w : acc.w;
+        }
+    } else {
+      acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int h = hb; h < he; ++h)
+        for (int w = wb; w < we; ++w) {
+          const float4 v = xb[(h * s.W + w) * C4];
+          acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        }
+      acc.x *= inv; acc.y *= inv; acc.z *= inv; acc.w *= inv;
+    }
+    y[i] = acc;
+  }
+}
+
 __global__ void pool_bwd_kernel(PoolShape s, const float* __restrict__ x, const float* __restrict__ y,
                                 const float* __restrict__ dy, float* dx, int accumulate, int64_t total) {
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
@@ -308,12 +428,12 @@ __global__ void pool_bwd_kernel(PoolShape s, const float* __restrict__ x, const 
 // first element (row-major) equal to the forward maximum y (255: none).
 // Vectorised over 4 channels.
 __global__ void pool_argmax_kernel(PoolShape s, const float* __restrict__ x, const float* __restrict__ y,
-                                   uchar4* __restrict__ arg, int64_t total4) {
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+                                   uchar4* __restrict__ arg, int total4) {
+  const int stride = gridDim.x * blockDim.x;
   const int C4 = s.C / 4;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total4; i += stride) {
-    const int c4 = static_cast<int>(i % C4);
-    int64_t t = i / C4;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total4; i += stride) {
+    const int c4 = i % C4;
+    int t = i / C4;
     const int q = static_cast<int>(t % s.Q);
     t /= s.Q;
     const int p = static_cast<int>(t % s.P);
@@ -342,13 +462,13 @@ __global__ void pool_argmax_kernel(PoolShape s, const float* __restrict__ x, con
 // Pass 2 (and the whole of avg-pool backward): gather over the <= ceil(K/s)^2
 // windows covering each input element.
 __global__ void pool_gather_kernel(PoolShape s, const uchar4* __restrict__ arg, const float* __restrict__ dy,
-                                   float* dx, int accumulate, int64_t total4) {
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+                                   float* dx, int accumulate, int total4) {
+  const int stride = gridDim.x * blockDim.x;
   const int C4 = s.C / 4;
   const float inv = 1.0f / static_cast<float>(s.K * s.K);
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total4; i += stride) {
-    const int c4 = static_cast<int>(i % C4);
-    int64_t t = i / C4;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total4; i += stride) {
+    const int c4 = i % C4;
+    int t = i / C4;
     const int w = static_cast<int>(t % s.W);
     t /= s.W;
     const int h = static_cast<int>(t % s.H);
@@ -623,6 +743,12 @@ cudaError_t relu_bwd_inplace(const float* y, float* g, int64_t n, cudaStream_t s
 
 cudaError_t pool_fwd(const PoolShape& s, const float* x, float* y, cudaStream_t st) {
   const int64_t total = static_cast<int64_t>(s.N) * s.P * s.Q * s.C;
+  if (s.C % 4 == 0 && static_cast<int64_t>(s.N) * s.H * s.W * s.C < (1ll << 31)) {
+    const int total4 = static_cast<int>(total / 4);
+    pool_fwd_v4_kernel<<<blocks_for(total4), kThreads, 0, st>>>(s, reinterpret_cast<const float4*>(x),
+                                                                  reinterpret_cast<float4*>(y), total4);
+    return cudaGetLastError();
+  }
   pool_fwd_kernel<<<blocks_for(total), kThreads, 0, st>>>(s, x, y, total);
   return cudaGetLastError();
 }
@@ -634,8 +760,8 @@ int64_t pool_scratch_bytes(const PoolShape& s) {
 cudaError_t pool_bwd(const PoolShape& s, const float* x, const float* y, const float* dy, float* dx, int accumulate,
                      void* scratch, cudaStream_t st) {
   if (s.C % 4 == 0 && (s.mode == 1 || (scratch && s.K * s.K < 255))) {
-    const int64_t in4 = static_cast<int64_t>(s.N) * s.H * s.W * s.C / 4;
-    const int64_t out4 = static_cast<int64_t>(s.N) * s.P * s.Q * s.C / 4;
+    const int in4 = static_cast<int>(static_cast<int64_t>(s.N) * s.H * s.W * s.C / 4);
+    const int out4 = static_cast<int>(static_cast<int64_t>(s.N) * s.P * s.Q * s.C / 4);
     uchar4* arg = reinterpret_cast<uchar4*>(scratch);
     if (s.mode == 0) pool_argmax_kernel<<<blocks_for(out4), kThreads, 0, st>>>(s, x, y, arg, out4);
     pool_gather_kernel<<<blocks_for(in4), kThreads, 0, st>>>(s, arg, dy, dx, accumulate, in4);

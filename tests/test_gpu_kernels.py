@@ -95,6 +95,9 @@ CONV_CASES = [
     (1, 32, 20, 20, 96, 11, 4, 0),   # AlexNet-style 11x11 stride 4
     (4, 128, 7, 7, 256, 3, 1, 1),    # 7x7 tiles straddle images
     (2, 256, 14, 14, 64, 1, 1, 0),   # 1x1, K = 64
+    (2, 64, 15, 15, 128, 3, 2, 1),   # odd extent, stride 2 (uneven phases)
+    (2, 32, 16, 16, 64, 1, 2, 0),    # 1x1 stride 2: phases without taps
+    (1, 64, 23, 23, 96, 5, 3, 2),    # stride 3, 5x5
 ]
 
 
