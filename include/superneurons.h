@@ -178,7 +178,22 @@ int sn_analyze(const sn_net_desc* net, const sn_sim_config* cfg, sn_plan** out);
 /* Cost table only, with costmodel.build_costs' error semantics (no schedule). */
 int sn_build_costs(const sn_net_desc* net, const sn_sim_config* cfg, sn_plan** out);
 
-/* Test hook: CPython set iteration order emulation (see planner/pyset.hpp). */
+/* The planner's block pool on its own (poolalloc.BlockPool, poolalloc.py:35-163):
+ * 1 KiB blocks, two-ended first fit, coalescing free.  Keys are caller ids. */
+typedef struct sn_pool sn_pool;
+int sn_pool_create(int64_t capacity_bytes, sn_pool** out);
+void sn_pool_destroy(sn_pool* pool);
+int sn_pool_alloc(sn_pool* pool, int64_t key, int64_t nbytes, int32_t high, int64_t* block_offset);
+int sn_pool_free(sn_pool* pool, int64_t key);
+int sn_pool_check(const sn_pool* pool);
+/* used / free / high-water in bytes, capacity in blocks, number of live keys */
+int sn_pool_stats(const sn_pool* pool, int64_t* used, int64_t* free_bytes, int64_t* high_water,
+                  int64_t* capacity_blocks, int64_t* n_keys);
+/* Free spans (is_free=1) or allocated spans with their keys (is_free=0), by offset. */
+int sn_pool_spans(const sn_pool* pool, int32_t is_free, int64_t* offsets, int64_t* lengths, int64_t* keys,
+                  size_t cap, size_t* n);
+
+/* Test hook: CPython set iteration order emulation (see planner/pool.hpp). */
 int sn_debug_pyset(const int64_t* a, size_t na, const int64_t* b, size_t nb, const int64_t* a2,
                    size_t na2, int64_t* out, size_t cap, size_t* n);
 

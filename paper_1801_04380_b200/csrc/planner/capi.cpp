@@ -1,4 +1,6 @@
 // C ABI of the planner (declared in include/superneurons.h).
+#include <algorithm>
+#include <array>
 #include <cstring>
 #include <exception>
 #include <new>
@@ -205,6 +207,69 @@ int sn_plan_order(const sn_plan* plan, int32_t* ids, size_t cap, size_t* n) {
 int sn_plan_demands(const sn_plan* plan, int64_t* demands, size_t cap, size_t* n) {
   if (!plan) return set_err(SN_EK_INTERNAL, "null argument");
   return copy_out_array(plan->plan.demands, demands, cap, n, [](int64_t v) { return v; });
+}
+
+struct sn_pool {
+  snp::BlockPool pool;
+  explicit sn_pool(int64_t cap) : pool(cap) {}
+};
+
+int sn_pool_create(int64_t capacity_bytes, sn_pool** out) {
+  if (!out) return set_err(SN_EK_INTERNAL, "null argument");
+  *out = nullptr;
+  return guarded([&] { *out = new sn_pool(capacity_bytes); });
+}
+
+void sn_pool_destroy(sn_pool* pool) { delete pool; }
+
+int sn_pool_alloc(sn_pool* pool, int64_t key, int64_t nbytes, int32_t high, int64_t* block_offset) {
+  if (!pool) return set_err(SN_EK_INTERNAL, "null argument");
+  return guarded([&] {
+    const int64_t off = pool->pool.alloc(key, nbytes, high != 0);
+    if (block_offset) *block_offset = off;
+  });
+}
+
+int sn_pool_free(sn_pool* pool, int64_t key) {
+  if (!pool) return set_err(SN_EK_INTERNAL, "null argument");
+  return guarded([&] { pool->pool.free(key); });
+}
+
+int sn_pool_check(const sn_pool* pool) {
+  if (!pool) return set_err(SN_EK_INTERNAL, "null argument");
+  return guarded([&] { pool->pool.check(); });
+}
+
+int sn_pool_stats(const sn_pool* pool, int64_t* used, int64_t* free_bytes, int64_t* high_water,
+                  int64_t* capacity_blocks, int64_t* n_keys) {
+  if (!pool) return set_err(SN_EK_INTERNAL, "null argument");
+  if (used) *used = pool->pool.used_bytes();
+  if (free_bytes) *free_bytes = pool->pool.free_bytes();
+  if (high_water) *high_water = pool->pool.high_water_bytes();
+  if (capacity_blocks) *capacity_blocks = pool->pool.capacity_blocks();
+  if (n_keys) *n_keys = static_cast<int64_t>(pool->pool.n_keys());
+  return SN_OK;
+}
+
+int sn_pool_spans(const sn_pool* pool, int32_t is_free, int64_t* offsets, int64_t* lengths, int64_t* keys,
+                  size_t cap, size_t* n) {
+  if (!pool || !n) return set_err(SN_EK_INTERNAL, "null argument");
+  std::vector<std::array<int64_t, 3>> spans;
+  if (is_free) {
+    for (const auto& f : pool->pool.free_spans()) spans.push_back({f.first, f.second, -1});
+  } else {
+    for (const auto& kv : pool->pool.allocated()) spans.push_back({kv.second.first, kv.second.second, kv.first});
+    std::sort(spans.begin(), spans.end());
+  }
+  *n = spans.size();
+  if (!offsets) return SN_OK;
+  if (cap < spans.size()) return set_err(SN_EK_INTERNAL, "output buffer too small");
+  for (size_t i = 0; i < spans.size(); ++i) {
+    offsets[i] = spans[i][0];
+    if (lengths) lengths[i] = spans[i][1];
+    if (keys) keys[i] = spans[i][2];
+  }
+  return SN_OK;
 }
 
 int sn_debug_pyset(const int64_t* a, size_t na, const int64_t* b, size_t nb, const int64_t* a2, size_t na2,

@@ -44,6 +44,9 @@ class BlockPool {
   int64_t free_bytes() const { return (cap_ - used_) * kBlockBytes; }
   int64_t high_water_bytes() const { return high_ * kBlockBytes; }
   int64_t capacity_blocks() const { return cap_; }
+  size_t n_keys() const { return alloc_.size(); }
+  const std::vector<std::pair<int64_t, int64_t>>& free_spans() const { return free_; }
+  const std::unordered_map<int64_t, std::pair<int64_t, int64_t>>& allocated() const { return alloc_; }
   void check() const;
 
  private:

@@ -299,6 +299,77 @@ def cases() -> list[dict]:
     return out
 
 
+def analysis_case(text: str, name: str, batch: int) -> dict:
+    """Every analysis entry point of the reference API on one network."""
+    from memsched import liveness as lv, offload as ol, recompute as rc
+    net = memsched.parse_network(text, name=name)
+    costs = build_costs(net, memsched.CostConfig(batch=batch))
+    sched = memsched.build_schedule(net)
+    out: dict = {"text": text, "name": name, "batch": batch}
+    out["forward_ids"] = sched.forward_ids
+    out["costs"] = [[list(c.shape), c.out_elems, c.out_bytes, c.device_bytes, c.grad_bytes, c.param_bytes,
+                     c.fwd_time, c.bwd_time] for c in costs.values()]
+    out["fwd_uses"] = {str(k): v for k, v in lv.forward_use_steps(net, sched).items()}
+    out["bwd_uses"] = {str(k): v for k, v in lv.backward_use_steps(net, sched).items()}
+    out["last_use"] = {str(k): v for k, v in lv.last_use_step(net, sched).items()}
+    out["last_fwd_use"] = {str(k): v for k, v in lv.last_forward_use_step(net, sched).items()}
+    for seed in (False, True):
+        out[f"grad_buffers_{int(seed)}"] = [dataclasses.astuple(b) for b in
+                                             lv.grad_buffers(net, costs, sched, seed).values()]
+    out["liveness_table"] = [dataclasses.astuple(r) for r in lv.liveness_table(net, costs, sched)]
+    out["liveness_csv"] = lv.dump_liveness_csv(net, costs, sched)
+    out["curve_liveness"] = lv.resident_curve(net, costs, sched, "liveness")
+    out["curve_baseline"] = lv.resident_curve(net, costs, sched, "baseline")
+    out["liveness_peak"] = list(lv.liveness_peak(net, costs, sched))
+    bufs = lv.grad_buffers(net, costs, sched, False)
+    out["working_set"] = [lv.working_set_bytes(net, costs, sched, bufs, s) for s in range(sched.num_steps)]
+    op = ol.build_offload_plan(net, sched)
+    out["offload_plan"] = [list(op.cp_ids), {str(k): v for k, v in op.drop_after.items()},
+                           {str(k): v for k, v in op.prefetch_issue.items()},
+                           {str(k): v for k, v in op.first_backward_use.items()},
+                           {str(k): v for k, v in op.last_backward_use.items()}]
+    segs = rc.build_segments(net, sched)
+    out["segments"] = [[s.index, list(s.members), list(s.anchors), rc.first_backward_use(net, sched, s),
+                        rc.memory_extras(net, s), rc.speed_extras(net, sched, s),
+                        rc.speed_prediction(net, costs, sched, s)] for s in segs]
+    plans = {}
+    for pol in rc.POLICIES:
+        for off in (False, True):
+            p = rc.plan(net, costs, sched, pol, frozenset(op.cp_ids) if off else frozenset())
+            plans[f"{pol}/{int(off)}"] = [list(p.modes), sorted(p.spill_ids), p.extra_forward_steps,
+                                         list(p.predictions)]
+    out["plans"] = plans
+    out["step_demands"] = rc.step_demands(net, costs, sched)
+    dp = rc.demand_peak(net, costs, sched)
+    out["demand_peak"] = [dp.nbytes, dp.step, dp.layer_id]
+    return out
+
+
+def pool_trace(seed: int, ops: int, capacity_blocks: int) -> dict:
+    """A random alloc/free trace through the reference BlockPool."""
+    import random
+    from memsched.poolalloc import BLOCK_BYTES, BlockPool, PoolExhausted
+    pool = BlockPool(capacity_blocks * BLOCK_BYTES)
+    rng = random.Random(seed)
+    live, trace, nxt = [], [], 0
+    for _ in range(ops):
+        if live and rng.random() < 0.4:
+            key = live.pop(rng.randrange(len(live)))
+            pool.free(key)
+            trace.append(["F", key])
+        else:
+            key, nxt = nxt, nxt + 1
+            nbytes = rng.randrange(0, 40 * BLOCK_BYTES)
+            high = rng.random() < 0.3
+            try:
+                off = pool.alloc(key, nbytes, high=high)
+                live.append(key)
+            except PoolExhausted as exc:
+                off = str(exc)
+            trace.append(["A", key, nbytes, int(high), off, pool.used_bytes, pool.high_water_bytes])
+    return {"seed": seed, "capacity_blocks": capacity_blocks, "trace": trace}
+
+
 def main() -> None:
     t0 = time.time()
     results = []
@@ -316,6 +387,19 @@ def main() -> None:
                "nets": texts, "cases": results}
     with gzip.open(OUT, "wt") as fh:
         json.dump(payload, fh, separators=(",", ":"))
+    # analysis entry points + allocator traces
+    nets = [(fixture_text("alexnet"), "alexnet", 200), (ALEX32, "alex32", 16),
+            (fixture_text("fan12"), "fan12", 8), (fixture_text("nested_fan10"), "nested_fan10", 4)]
+    nets.append(capture_text(netgen.gen_resnet, 3, 4, 6, 3) + (256,))
+    for n, cps in [(9, (3, 6)), (12, (3, 6, 9))]:
+        nets.append(capture_text(netgen.make_uniform_chain, n, cps) + (200,))
+    for seed in range(0, 200, 10):
+        nets.append(capture_text(netgen.random_fanjoin, seed) + (8,))
+    analysis = [analysis_case(t, n, b) for t, n, b in nets]
+    traces = [pool_trace(90210, 20000, 256), pool_trace(577, 2000, 64), pool_trace(1, 5000, 1024)]
+    with gzip.open(HERE / "analysis_golden.json.gz", "wt") as fh:
+        json.dump({"generator": "tests/golden/make_golden.py", "analysis": analysis, "pool_traces": traces}, fh,
+                  separators=(",", ":"))
     n_err = sum(1 for r in results if "error" in r)
     print(f"{len(results)} cases ({n_err} errors) in {time.time() - t0:.1f}s -> {OUT}")
 
