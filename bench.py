@@ -214,10 +214,7 @@ def run_ours(args) -> None:
     value = world * B * args.steps / (elapsed_ms / 1e3)
 
     # ---- end to end through the public API: pinned host batch in, loss out ----
-    img_host = images.permute(0, 2, 3, 1).contiguous()
-    if ex.data_channels != ex.c_real:
-        img_host = torch.nn.functional.pad(img_host, (0, ex.data_channels - ex.c_real))
-    img_host = img_host.pin_memory()
+    img_host = images.permute(0, 2, 3, 1).contiguous().pin_memory()
     lab_host = labels.to(torch.int32).pin_memory()
     for _ in range(2):
         ex.step_host(img_host, lab_host)

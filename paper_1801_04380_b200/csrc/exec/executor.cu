@@ -57,6 +57,7 @@ int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 struct LayerRt {
   int kind = 0;
   int C = 1, H = 1, W = 1;   // output per sample (stored channels for DATA)
+  int C_raw = 1;             // channels before the DATA padding
   int64_t per_sample = 0;    // output elements per sample (stored)
   int64_t w_off = -1, w_n = 0, b_off = -1, b_n = 0;
   int64_t state_off = -1;    // BN: stats[2C] then running[2C]
@@ -91,8 +92,11 @@ struct sn_exec {
   int64_t n_params = 0;
   float* state = nullptr;
   int64_t n_state = 0;
-  float* images = nullptr;
+  float* images = nullptr;    // user-facing input batch, NHWC with the net's own channel count
   int64_t image_floats = 0;
+  float* data_buf = nullptr;  // the DATA activation as the consumers read it (== images unless padded)
+  int data_id = -1;
+  int stem_layer = -1;        // CONV reading a spatially padded C=4 copy of the images (TMA stem path)
   int32_t* labels = nullptr;
   float* loss_rows = nullptr;
   float* loss = nullptr;
@@ -155,6 +159,8 @@ void setup_layers(sn_exec* ex, const sn_layer_numerics* numerics) {
       l.C = static_cast<int>(shp[0]);
       l.H = l.W = 1;
     }
+    l.C_raw = l.C;
+    if (l.kind == snp::DATA) ex->data_id = i;
     if (l.kind == snp::DATA && l.C % 4 != 0) {
       bool only_conv = true;
       for (int nx : net.next[i]) only_conv &= net.kind[nx] == snp::CONV;
@@ -214,6 +220,13 @@ void setup_layers(sn_exec* ex, const sn_layer_numerics* numerics) {
   }
   ex->n_params = std::max<int64_t>(poff, kAlignFloats);
   ex->n_state = std::max<int64_t>(soff, kAlignFloats);
+  // A lone CONV on a 4-channel DATA layer reads a spatially padded copy of the
+  // images through the sliding-window TMA stem kernels (conv_tma.cu).
+  if (ex->data_id >= 0 && net.next[ex->data_id].size() == 1) {
+    const int c = net.next[ex->data_id][0];
+    if (ex->L[c].kind == snp::CONV && ex->L[ex->data_id].C == 4 && sn::use_tma() && sn::conv_stem_ok(ex->L[c].conv))
+      ex->stem_layer = c;
+  }
 }
 
 void alloc_device(sn_exec* ex) {
@@ -254,6 +267,10 @@ void alloc_device(sn_exec* ex) {
       partial = std::max(partial, static_cast<int64_t>(l.fc_splits) * ex->B * std::max(l.fc_in, l.C));
     }
   }
+  if (ex->stem_layer >= 0) {
+    partial = std::max(partial, sn::stem_wgrad_partial_floats(ex->L[ex->stem_layer].conv));
+    wt = std::max(wt, sn::stem_weight_floats(ex->L[ex->stem_layer].conv));
+  }
   ex->partial_cap = std::max<int64_t>(partial, 64);
   ck(cudaMalloc(&ex->partial, ex->partial_cap * sizeof(float)), "cudaMalloc(partial)");
   ck(cudaMalloc(&ex->wt_scratch, std::max<int64_t>(wt, 64) * sizeof(float)), "cudaMalloc(wt)");
@@ -262,13 +279,19 @@ void alloc_device(sn_exec* ex) {
   for (int i = 0; i < net.n; ++i)
     if (ex->L[i].kind == snp::POOL) pool_bytes = std::max(pool_bytes, sn::pool_scratch_bytes(ex->L[i].pool));
   ck(cudaMalloc(&ex->pool_scratch, static_cast<size_t>(pool_bytes)), "cudaMalloc(pool scratch)");
-  int data_id = 0;
-  for (int i = 0; i < net.n; ++i)
-    if (net.kind[i] == snp::DATA) data_id = i;
-  const LayerRt& data = ex->L[data_id];
-  ex->image_floats = static_cast<int64_t>(ex->B) * data.per_sample;
+  if (ex->data_id < 0) xfail(SN_EK_UNSUPPORTED, "numeric execution needs a DATA layer");
+  const LayerRt& data = ex->L[ex->data_id];
+  ex->image_floats = static_cast<int64_t>(ex->B) * data.H * data.W * data.C_raw;
   ck(cudaMalloc(&ex->images, ex->image_floats * sizeof(float)), "cudaMalloc(images)");
   ck(cudaMemset(ex->images, 0, ex->image_floats * sizeof(float)), "memset(images)");
+  if (ex->stem_layer >= 0 || data.C != data.C_raw) {
+    const int64_t n = ex->stem_layer >= 0 ? sn::stem_padded_floats(ex->L[ex->stem_layer].conv)
+                                          : static_cast<int64_t>(ex->B) * data.per_sample;
+    ck(cudaMalloc(&ex->data_buf, n * sizeof(float)), "cudaMalloc(data)");
+    ck(cudaMemset(ex->data_buf, 0, n * sizeof(float)), "memset(data)");
+  } else {
+    ex->data_buf = ex->images;
+  }
   ck(cudaMalloc(&ex->labels, ex->B * sizeof(int32_t)), "cudaMalloc(labels)");
   ck(cudaMemset(ex->labels, 0, ex->B * sizeof(int32_t)), "memset(labels)");
   ck(cudaMalloc(&ex->loss_rows, ex->B * sizeof(float)), "cudaMalloc(loss_rows)");
@@ -307,7 +330,7 @@ struct Compiler {
   }
 
   float* ptr(int kind, int id) {
-    if (kind == snp::K_ACT && id == data_id) return ex->images;
+    if (kind == snp::K_ACT && id == data_id) return ex->data_buf;
     auto it = where.find(key_code(kind, id));
     if (it == where.end())
       xfail(SN_EK_INTERNAL, std::string("tape references non-resident ") + (kind == 0 ? "act " : kind == 1 ? "grad " : "ws ") +
@@ -415,6 +438,11 @@ struct Compiler {
         const float* w = ex->params + l.w_off;
         const float* b = ex->params + l.b_off;
         const sn::ConvShape cs = l.conv;
+        if (lid == ex->stem_layer) {
+          float* wp = ex->wt_scratch;
+          push([=] { ck(sn::conv_stem_fwd(cs, x, w, wp, b, y, st), "conv_stem_fwd"); }, 2);
+          break;
+        }
         push([=] { ck(sn::conv_fwd(cs, x, w, b, y, st), "conv_fwd"); }, 1);
         break;
       }
@@ -436,11 +464,30 @@ struct Compiler {
         const float eps = l.num.bn_eps, mom = l.num.bn_momentum;
         const int compute = replay ? 0 : 1;
         float* red = ex->red;
+        if (fuse_next) {
+          // apply deferred to the consuming ReLU (bn_apply_relu); statistics now
+          if (!replay)
+            push([=] { ck(sn::bn_fwd(x, rows, C, g, b, nullptr, stats, running, eps, mom, 1, red, st), "bn_stats"); },
+                 3);
+          break;
+        }
         push([=] { ck(sn::bn_fwd(x, rows, C, g, b, y, stats, running, eps, mom, compute, red, st), "bn_fwd"); },
              replay ? 1 : 4);
         break;
       }
       case snp::ACT:
+        if (fused_bn >= 0) {
+          const LayerRt& bl = ex->L[fused_bn];
+          const float* bx = ptr(snp::K_ACT, net.prev[fused_bn][0]);
+          float* by = const_cast<float*>(x);  // the BN output this ReLU reads
+          const float* g = ex->params + bl.w_off;
+          const float* b = ex->params + bl.b_off;
+          const float* stats = ex->state + bl.state_off;
+          const int64_t rows = static_cast<int64_t>(ex->B) * bl.H * bl.W;
+          const int C = bl.C;
+          push([=] { ck(sn::bn_apply_relu(bx, rows, C, g, b, stats, by, y, st), "bn_apply_relu"); }, 1);
+          break;
+        }
         push([=] { ck(sn::relu_fwd(x, y, n, st), "relu_fwd"); }, 1);
         break;
       case snp::POOL: {
@@ -517,6 +564,10 @@ struct Compiler {
         float* part = ex->partial;
         float* red = ex->red;
         const int sp = l.wgrad_splits;
+        if (lid == ex->stem_layer) {  // DATA has no gradient
+          push([=] { ck(sn::conv_stem_wgrad(cs, x, dy, part, wt, dw, db, red, st), "conv_stem_wgrad"); }, 5);
+          break;
+        }
         push([=] {
           ck(sn::conv_wgrad(cs, x, dy, dw, db, part, sp, red, st), "conv_wgrad");
           if (dx) ck(sn::conv_dgrad(cs, dy, w, wt, dx, acc, st), "conv_dgrad");
@@ -604,7 +655,18 @@ struct Compiler {
         break;
       }
       case snp::JOIN: {
-        for (int p : net.prev[lid]) {
+        const auto& pv = net.prev[lid];
+        if (pv.size() == 2 && n % 4 == 0) {
+          const int o0 = net.grad_owner(pv[0]), o1 = net.grad_owner(pv[1]);
+          if (o0 >= 0 && o1 >= 0 && o0 != o1) {  // one read of dy, two destinations
+            int a0 = 0, a1 = 0;
+            float* d0 = dx_target(pv[0], &a0);
+            float* d1 = dx_target(pv[1], &a1);
+            push([=] { ck(sn::grad_copy2(dy, d0, a0, d1, a1, n, st), "join_bwd2"); }, 1);
+            break;
+          }
+        }
+        for (int p : pv) {
           int acc = 0;
           float* dx = dx_target(p, &acc);
           if (dx) push([=] { ck(sn::grad_copy(dy, dx, n, acc, st), "join_bwd"); }, 1);
@@ -616,8 +678,63 @@ struct Compiler {
     }
   }
 
+  // Peephole fusion on the tape: a BN forward (or replay) whose very next
+  // device action is the forward (replay) of the ReLU reading it, with neither
+  // the BN input nor its output freed in between, is split into "statistics
+  // now" + "apply fused into the ReLU" (one pass writes both outputs).
+  bool fuse_next = false;
+  int fused_bn = -1;
+  std::vector<char> fuse_at;
+  std::vector<int> fused_into;
+  void plan_fusions() {
+    const size_t T = P.tape.size();
+    fuse_at.assign(T, 0);
+    fused_into.assign(T, -1);
+    for (size_t i = 0; i < T; ++i) {
+      const snp::Event& e = P.tape[i];
+      if ((e.op != 'C' && e.op != 'R') || net.kind[e.b] != snp::BN) continue;
+      const int bn = e.b;
+      if (ex->L[bn].C % 4 != 0 || net.prev[bn].empty()) continue;
+      for (size_t j = i + 1; j < T; ++j) {
+        const snp::Event& f = P.tape[j];
+        if (f.op == 'F' && f.a == snp::K_ACT && (f.b == bn || f.b == net.prev[bn][0])) break;
+        if (f.op == 'C' || f.op == 'R' || f.op == 'B' || f.op == 'O' || f.op == 'P' || f.op == 'D') {
+          if (f.op == e.op && net.kind[f.b] == snp::ACT && net.prev[f.b].size() == 1 && net.prev[f.b][0] == bn) {
+            fuse_at[i] = 1;
+            fused_into[j] = bn;
+          }
+          break;
+        }
+      }
+    }
+  }
+
+  // DATA layer: lay the user's images out the way the consumers read them.
+  void prepare_inputs() {
+    const LayerRt& d = ex->L[data_id];
+    if (ex->data_buf == ex->images) return;
+    cur_layer = data_id, cur_type = 0;
+    const float* raw = ex->images;
+    float* out = ex->data_buf;
+    cudaStream_t st = ex->s0;
+    if (ex->stem_layer >= 0) {
+      const sn::ConvShape cs = ex->L[ex->stem_layer].conv;
+      const int H = d.H, W = d.W, Cr = d.C_raw;
+      push([=] { ck(sn::stem_pad_input(cs, H, W, Cr, cs.pad, raw, out, st), "stem_pad_input"); }, 1);
+    } else {
+      const int Cr = d.C_raw, Cs = d.C;
+      const int64_t pix = static_cast<int64_t>(ex->B) * d.H * d.W;
+      push([=] { ck(sn::pad_channels(raw, Cr, out, Cs, pix, st), "pad_channels"); }, 1);
+    }
+  }
+
   void compile() {
-    for (const snp::Event& ev : P.tape) {
+    plan_fusions();
+    prepare_inputs();
+    for (size_t ti = 0; ti < P.tape.size(); ++ti) {
+      const snp::Event& ev = P.tape[ti];
+      fuse_next = fuse_at[ti] != 0;
+      fused_bn = fused_into[ti];
       switch (ev.op) {
         case 'A': on_alloc(ev); break;
         case 'F': on_free(ev); break;
@@ -708,6 +825,7 @@ void destroy(sn_exec* ex) {
   if (ex->t_end) cudaEventDestroy(ex->t_end);
   for (auto& kv : ex->stash)
     if (kv.second) cudaFreeHost(kv.second);
+  if (ex->data_buf && ex->data_buf != ex->images) cudaFree(ex->data_buf);
   void* bufs[] = {ex->arena, ex->params, ex->grads, ex->state, ex->images, ex->labels, ex->loss_rows, ex->loss,
                   ex->iteration, ex->wt_scratch, ex->partial, ex->red, ex->pool_scratch,
                   const_cast<float**>(ex->ptr_table)};

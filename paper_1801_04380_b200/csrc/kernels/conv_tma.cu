@@ -48,27 +48,37 @@ struct TmaArgs {
   // MODE 1
   int C, RSC, Kout, NPQ;
   FastDivT fC;
+  // MODE 2/3 (stem over a padded C=4 input, sliding-window view): k block =
+  // (filter row r, block b of 8 filter columns x 4 channels); M tile = one
+  // output row (fwd) / 4 k-atoms (wgrad); qblocks = ceil(Q / 32).
+  int sblocks, shift, qblocks, R;
+  FastDivT fsb, fqb, fP;
 };
 
 constexpr int kTmaThreads = 192;
 
+// Persistent schedule: one CTA per SM walks tiles t = blockIdx.x, +gridDim.x,
+// ... (tile = m-tile fastest, then n-tile, then split).  The TMA producer runs
+// ahead across tile boundaries, the MMA issuer alternates between two TMEM
+// accumulators (2 x BN columns), so tile i's epilogue overlaps tile i+1's MMAs.
 template <int BN, int STAGES>
 struct TmaSmem {
   static constexpr int A_BYTES = kBM * 128;
   static constexpr int B_BYTES = BN * 128;
-  static constexpr int BAR_OFF = STAGES * (A_BYTES + B_BYTES);
-  static constexpr int TOTAL = BAR_OFF + 256 + 1024;
+  static constexpr int EPI_OFF = STAGES * (A_BYTES + B_BYTES);   // 2 x 16 KB store staging
+  static constexpr int BAR_OFF = EPI_OFF + 2 * kBM * 128;
+  static constexpr int TOTAL = BAR_OFF + 512 + 1024;
 };
 
-// Epilogue: TMEM -> registers (+bias) -> SWIZZLE_128B smem chunks of 128 x 32
-// fp32 -> one TMA bulk store per chunk (plain, reduce-add, or into the 3-D
-// [split][M][N] partial tensor).  Rows/columns past the tensor are clipped by
-// the TMA unit, so no predication is needed.
+// Epilogue: TMEM -> registers (+bias) -> SWIZZLE_128B smem chunk of 128 x 32
+// fp32 (double-buffered) -> one TMA bulk store per chunk (plain, reduce-add, or
+// into the 3-D [split][M][N] partial tensor).  Rows/columns past the tensor are
+// clipped by the TMA unit, so no predication is needed.
 struct EpiArgs {
   const float* bias;  // per output column, may be null
   int N;              // valid columns
   int reduce;         // 1: out += tile (cp.reduce.async.bulk .add), 0: out = tile
-  int partial3d;      // 1: tmD is [splits][M][N], coordinate z = blockIdx.z
+  int partial3d;      // 1: tmD is [splits][M][N], coordinate z = split
   // Scatter mode (strided dgrad phases): GEMM row m = (n, u, v) of the phase
   // grid lands at dx[n][(u+t0)*st+ph-pad][(v+v0)*st+pw-pad][:] (direct stores).
   float* scatter;     // null: TMA store path
@@ -76,202 +86,291 @@ struct EpiArgs {
   FastDivT fUhw, fUw;
 };
 
+struct TileGrid {
+  int m_tiles, n_tiles, tiles;
+};
+
 template <int BN, int STAGES, int MODE>
-__global__ void __launch_bounds__(kTmaThreads, (BN <= 128 ? 2 : 1))
+__global__ void __launch_bounds__(kTmaThreads, 1)
     tc_conv_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                       const __grid_constant__ CUtensorMap tmD, TmaArgs a, EpiArgs e) {
+                       const __grid_constant__ CUtensorMap tmD, TmaArgs a, EpiArgs e, TileGrid tg) {
   using L = TmaSmem<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * L::A_BYTES;
+  const uint32_t sEpi = smem_u32(smem + L::EPI_OFF);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
   uint64_t* empty = full + STAGES;
-  uint64_t* done = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  uint64_t* tfull = empty + STAGES;   // [2] accumulator ready
+  uint64_t* tempty = tfull + 2;       // [2] accumulator drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * kBM, n0 = blockIdx.y * BN;
-  const int kb0 = blockIdx.z * a.kb_per_split;
-  const int nkb = min(a.num_kb, kb0 + a.kb_per_split) - kb0;
+  constexpr uint32_t kCols = tmem_cols<2 * BN>();
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(done, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 128);
+    }
     fence_mbar_init();
   }
-  if (warp == 5) tmem_alloc(tmem_slot, tmem_cols<BN>());
+  if (warp == 5) tmem_alloc(tmem_slot, kCols);
   if (warp == 4 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
+    if (!e.scatter) tma_prefetch(&tmD);
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  auto tile_coords = [&](int t, int& m0, int& n0, int& kb0, int& nkb, int& split) {
+    const int mt = t % tg.m_tiles;
+    const int rest = t / tg.m_tiles;
+    const int nt = rest % tg.n_tiles;
+    split = rest / tg.n_tiles;
+    m0 = mt * kBM;
+    n0 = nt * BN;
+    kb0 = split * a.kb_per_split;
+    nkb = min(a.num_kb, kb0 + a.kb_per_split) - kb0;
+  };
+
   if (warp == 4) {
     if (lane == 0) {
       // ---------------- TMA producer ----------------
-      if (MODE == 0) {
-        const int n = static_cast<int>(a.fPQ.div(m0));
-        const int pq = m0 - n * a.PQ;
-        const int p = static_cast<int>(a.fQ.div(pq));
-        const int q = pq - p * a.Q;
-        const int w0 = q * a.stride - a.pad_w, h0 = p * a.stride - a.pad;
-        for (int i = 0; i < nkb; ++i) {
-          const int s = i % STAGES;
-          if (i >= STAGES) mbar_wait(&empty[s], ((i / STAGES) - 1) & 1);
-          const int kb = kb0 + i;
-          const int tap = static_cast<int>(a.fcc.div(kb));
-          const int cc = kb - tap * a.cchunks;
-          const int r = static_cast<int>(a.fS.div(tap));
-          const int t = tap - r * a.S;
-          mbar_arrive_expect_tx(&full[s], L::A_BYTES + L::B_BYTES);
-          tma_load_im2col_4d(smem_u32(sA + s * L::A_BYTES), &tmA, &full[s], cc * 32, w0, h0, n,
-                             static_cast<uint16_t>(t), static_cast<uint16_t>(r));
-          tma_load_2d(smem_u32(sB + s * L::B_BYTES), &tmB, &full[s], kb * kBK, n0);
-        }
-      } else {
-        int ac[4], ar[4], as[4], na = 0;
-        for (int g = 0; g < 4; ++g) {
-          const int rsc0 = m0 + 32 * g;
-          if (rsc0 >= a.RSC) break;
-          const int tap = static_cast<int>(a.fC.div(rsc0));
-          ac[g] = rsc0 - tap * a.C;
-          ar[g] = static_cast<int>(a.fS.div(tap));
-          as[g] = tap - ar[g] * a.S;
-          ++na;
-        }
-        int nb = 0;
-        for (int j = 0; j < BN / 32; ++j)
-          if (n0 + 32 * j < a.Kout) ++nb;
-        for (int i = 0; i < nkb; ++i) {
-          const int s = i % STAGES;
-          if (i >= STAGES) mbar_wait(&empty[s], ((i / STAGES) - 1) & 1);
-          const int pix = (kb0 + i) * kBK;
-          const int n = static_cast<int>(a.fPQ.div(pix));
-          const int pq = pix - n * a.PQ;
+      uint32_t g = 0;  // k blocks issued by this CTA (stage ring position)
+      for (int t = blockIdx.x; t < tg.tiles; t += gridDim.x) {
+        int m0, n0, kb0, nkb, split;
+        tile_coords(t, m0, n0, kb0, nkb, split);
+        if (MODE == 0) {
+          const int n = static_cast<int>(a.fPQ.div(m0));
+          const int pq = m0 - n * a.PQ;
           const int p = static_cast<int>(a.fQ.div(pq));
           const int q = pq - p * a.Q;
-          const int w0 = q * a.stride - a.pad, h0 = p * a.stride - a.pad;
-          mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>((na + nb) * 4096));
-          for (int g = 0; g < na; ++g)
-            tma_load_im2col_4d(smem_u32(sA + s * L::A_BYTES + g * 4096), &tmA, &full[s], ac[g], w0, h0, n,
-                               static_cast<uint16_t>(as[g]), static_cast<uint16_t>(ar[g]));
-          for (int j = 0; j < nb; ++j)
-            tma_load_2d(smem_u32(sB + s * L::B_BYTES + j * 4096), &tmB, &full[s], n0 + 32 * j, pix);
+          const int w0 = q * a.stride - a.pad_w, h0 = p * a.stride - a.pad;
+          for (int i = 0; i < nkb; ++i, ++g) {
+            const int s = g % STAGES;
+            if (g >= STAGES) mbar_wait(&empty[s], ((g / STAGES) - 1) & 1);
+            const int kb = kb0 + i;
+            const int tap = static_cast<int>(a.fcc.div(kb));
+            const int cc = kb - tap * a.cchunks;
+            const int r = static_cast<int>(a.fS.div(tap));
+            const int tt = tap - r * a.S;
+            mbar_arrive_expect_tx(&full[s], L::A_BYTES + L::B_BYTES);
+            tma_load_im2col_4d(smem_u32(sA + s * L::A_BYTES), &tmA, &full[s], cc * 32, w0, h0, n,
+                               static_cast<uint16_t>(tt), static_cast<uint16_t>(r));
+            tma_load_2d(smem_u32(sB + s * L::B_BYTES), &tmB, &full[s], kb * kBK, n0);
+          }
+        } else if (MODE == 2) {
+          // stem forward: the M tile is output row (n, p); window of output q
+          // starts at padded column stride*q + 8b (view dim1 step = stride pixels)
+          const int mt = m0 / kBM;
+          const int n = static_cast<int>(a.fP.div(mt));
+          const int p = mt - n * a.P;
+          for (int i = 0; i < nkb; ++i, ++g) {
+            const int s = g % STAGES;
+            if (g >= STAGES) mbar_wait(&empty[s], ((g / STAGES) - 1) & 1);
+            const int kb = kb0 + i;
+            const int r = static_cast<int>(a.fsb.div(kb));
+            const int b = kb - r * a.sblocks;
+            mbar_arrive_expect_tx(&full[s], L::A_BYTES + L::B_BYTES);
+            tma_load_4d(smem_u32(sA + s * L::A_BYTES), &tmA, &full[s], 0, b * a.shift, p * a.stride + r, n);
+            tma_load_2d(smem_u32(sB + s * L::B_BYTES), &tmB, &full[s], kb * kBK, n0);
+          }
+        } else if (MODE == 3) {
+          // stem wgrad: 4 k-atoms (r, b) per M tile; k block = 32 output columns of one row
+          int ar[4], ab[4], na = 0;
+          for (int q4 = 0; q4 < 4; ++q4) {
+            const int atom = m0 / 32 + q4;
+            const int r = static_cast<int>(a.fsb.div(atom));
+            if (r >= a.R) break;
+            ar[q4] = r;
+            ab[q4] = atom - r * a.sblocks;
+            ++na;
+          }
+          int nb = 0;
+          for (int j = 0; j < BN / 32; ++j)
+            if (n0 + 32 * j < a.Kout) ++nb;
+          for (int i = 0; i < nkb; ++i, ++g) {
+            const int s = g % STAGES;
+            if (g >= STAGES) mbar_wait(&empty[s], ((g / STAGES) - 1) & 1);
+            const int kb = kb0 + i;
+            const int row = static_cast<int>(a.fqb.div(kb));
+            const int qb = kb - row * a.qblocks;
+            const int n = static_cast<int>(a.fP.div(row));
+            const int p = row - n * a.P;
+            mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>((na + nb) * 4096));
+            for (int q4 = 0; q4 < na; ++q4)
+              tma_load_4d(smem_u32(sA + s * L::A_BYTES + q4 * 4096), &tmA, &full[s], 0,
+                          qb * 32 + ab[q4] * a.shift, p * a.stride + ar[q4], n);
+            for (int j = 0; j < nb; ++j)
+              tma_load_4d(smem_u32(sB + s * L::B_BYTES + j * 4096), &tmB, &full[s], n0 + 32 * j, qb * 32, p, n);
+          }
+        } else {
+          int ac[4], ar[4], as[4], na = 0;
+          for (int q4 = 0; q4 < 4; ++q4) {
+            const int rsc0 = m0 + 32 * q4;
+            if (rsc0 >= a.RSC) break;
+            const int tap = static_cast<int>(a.fC.div(rsc0));
+            ac[q4] = rsc0 - tap * a.C;
+            ar[q4] = static_cast<int>(a.fS.div(tap));
+            as[q4] = tap - ar[q4] * a.S;
+            ++na;
+          }
+          int nb = 0;
+          for (int j = 0; j < BN / 32; ++j)
+            if (n0 + 32 * j < a.Kout) ++nb;
+          for (int i = 0; i < nkb; ++i, ++g) {
+            const int s = g % STAGES;
+            if (g >= STAGES) mbar_wait(&empty[s], ((g / STAGES) - 1) & 1);
+            const int pix = (kb0 + i) * kBK;
+            const int n = static_cast<int>(a.fPQ.div(pix));
+            const int pq = pix - n * a.PQ;
+            const int p = static_cast<int>(a.fQ.div(pq));
+            const int q = pq - p * a.Q;
+            const int w0 = q * a.stride - a.pad, h0 = p * a.stride - a.pad;
+            mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>((na + nb) * 4096));
+            for (int q4 = 0; q4 < na; ++q4)
+              tma_load_im2col_4d(smem_u32(sA + s * L::A_BYTES + q4 * 4096), &tmA, &full[s], ac[q4], w0, h0, n,
+                                 static_cast<uint16_t>(as[q4]), static_cast<uint16_t>(ar[q4]));
+            for (int j = 0; j < nb; ++j)
+              tma_load_2d(smem_u32(sB + s * L::B_BYTES + j * 4096), &tmB, &full[s], n0 + 32 * j, pix);
+          }
         }
       }
     }
   } else if (warp == 5) {
     if (lane == 0) {
       // ---------------- MMA issuer ----------------
-      constexpr uint32_t idesc = idesc_tf32(kBM, BN, MODE == 1, MODE == 1);
-      for (int i = 0; i < nkb; ++i) {
-        const int s = i % STAGES;
-        mbar_wait(&full[s], (i / STAGES) & 1);
+      constexpr bool kMN = (MODE == 1 || MODE == 3);  // wgrad: both operands MN-major
+      constexpr uint32_t idesc = idesc_tf32(kBM, BN, kMN, kMN);
+      uint32_t g = 0;
+      int local = 0;
+      for (int t = blockIdx.x; t < tg.tiles; t += gridDim.x, ++local) {
+        int m0, n0, kb0, nkb, split;
+        tile_coords(t, m0, n0, kb0, nkb, split);
+        const int acc = local & 1;
+        if (local >= 2) mbar_wait(&tempty[acc], ((local >> 1) - 1) & 1);
         tc_fence_after();
-        const uint32_t a0 = smem_u32(sA + s * L::A_BYTES);
-        const uint32_t b0 = smem_u32(sB + s * L::B_BYTES);
+        const uint32_t d = tmem + static_cast<uint32_t>(acc * BN);
+        for (int i = 0; i < nkb; ++i, ++g) {
+          const int s = g % STAGES;
+          mbar_wait(&full[s], (g / STAGES) & 1);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + s * L::A_BYTES);
+          const uint32_t b0 = smem_u32(sB + s * L::B_BYTES);
 #pragma unroll
-        for (int kk = 0; kk < kBK / 8; ++kk) {
-          uint64_t ad, bd;
-          if (MODE == 0) {
-            ad = umma_desc(a0 + kk * 32, 16, 1024, kLayoutSW128);
-            bd = umma_desc(b0 + kk * 32, 16, 1024, kLayoutSW128);
-          } else {
-            // 8 k rows = two 4-row K atoms (512 B each); MN atoms 4 KB apart
-            ad = umma_desc(a0 + kk * 1024, 4096, 512, kLayoutSW128Base32);
-            bd = umma_desc(b0 + kk * 1024, 4096, 512, kLayoutSW128Base32);
+          for (int kk = 0; kk < kBK / 8; ++kk) {
+            uint64_t ad, bd;
+            if (!kMN) {
+              ad = umma_desc(a0 + kk * 32, 16, 1024, kLayoutSW128);
+              bd = umma_desc(b0 + kk * 32, 16, 1024, kLayoutSW128);
+            } else {
+              // 8 k rows = two 4-row K atoms (512 B each); MN atoms 4 KB apart
+              ad = umma_desc(a0 + kk * 1024, 4096, 512, kLayoutSW128Base32);
+              bd = umma_desc(b0 + kk * 1024, 4096, 512, kLayoutSW128Base32);
+            }
+            umma_tf32(d, ad, bd, idesc, (i | kk) != 0 ? 1u : 0u);
           }
-          umma_tf32(tmem, ad, bd, idesc, (i | kk) != 0 ? 1u : 0u);
+          umma_commit(&empty[s]);
         }
-        umma_commit(&empty[s]);
+        umma_commit(&tfull[acc]);
       }
-      umma_commit(done);
     }
   } else {
     // ---------------- epilogue (warps 0-3 own TMEM lanes 32w..32w+31) ----------------
-    mbar_wait(done, 0);
-    tc_fence_after();
-    // All MMAs (hence all operand loads) are complete: the stage buffers are free.
     const uint32_t row = warp * 32 + lane;
-    const uint32_t stage0 = smem_u32(smem);
-    if (e.scatter) {
-      // strided-dgrad phase: each row goes to its interleaved place in dx
-      const int m = m0 + static_cast<int>(row);
-      float* dst = nullptr;
-      if (m < e.M) {
-        const int n = static_cast<int>(e.fUhw.div(static_cast<uint32_t>(m)));
-        const int uv = m - n * e.Uhw;
-        const int u = static_cast<int>(e.fUw.div(static_cast<uint32_t>(uv)));
-        const int v = uv - u * e.Uw;
-        const int h = (u + e.t0) * e.st + e.ph - e.pad;
-        const int w = (v + e.v0) * e.st + e.pw - e.pad;
-        dst = e.scatter + (static_cast<size_t>(n * e.H + h) * e.W + w) * e.N;
-      }
+    int local = 0;
+    uint32_t chunk_no = 0;  // store-staging double-buffer position
+    for (int t = blockIdx.x; t < tg.tiles; t += gridDim.x, ++local) {
+      int m0, n0, kb0, nkb, split;
+      tile_coords(t, m0, n0, kb0, nkb, split);
+      const int acc = local & 1;
+      mbar_wait(&tfull[acc], (local >> 1) & 1);
+      tc_fence_after();
+      const uint32_t tbase = tmem + static_cast<uint32_t>(acc * BN) + (static_cast<uint32_t>(warp * 32) << 16);
+      if (e.scatter) {
+        // strided-dgrad phase: each row goes to its interleaved place in dx
+        const int m = m0 + static_cast<int>(row);
+        float* dst = nullptr;
+        if (m < e.M) {
+          const int n = static_cast<int>(e.fUhw.div(static_cast<uint32_t>(m)));
+          const int uv = m - n * e.Uhw;
+          const int u = static_cast<int>(e.fUw.div(static_cast<uint32_t>(uv)));
+          const int v = uv - u * e.Uw;
+          const int h = (u + e.t0) * e.st + e.ph - e.pad;
+          const int w = (v + e.v0) * e.st + e.pw - e.pad;
+          dst = e.scatter + (static_cast<size_t>(n * e.H + h) * e.W + w) * e.N;
+        }
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
-        float v[32];
-        tmem_ld32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + static_cast<uint32_t>(c), v);
-        if (dst) {
+        for (int c = 0; c < BN; c += 32) {
+          float v[32];
+          tmem_ld32(tbase + static_cast<uint32_t>(c), v);
+          if (dst) {
 #pragma unroll
-          for (int j = 0; j < 32; j += 4) {
-            if (n0 + c + j >= e.N) break;
-            float4* p = reinterpret_cast<float4*>(dst + n0 + c + j);
-            float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-            if (e.reduce) {
-              const float4 old = *p;
-              o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
+            for (int j = 0; j < 32; j += 4) {
+              if (n0 + c + j >= e.N) break;
+              float4* p = reinterpret_cast<float4*>(dst + n0 + c + j);
+              float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+              if (e.reduce) {
+                const float4 old = *p;
+                o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
+              }
+              *p = o;
             }
-            *p = o;
+          }
+        }
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32, ++chunk_no) {
+          if (n0 + c >= e.N) break;
+          float v[32];
+          tmem_ld32(tbase + static_cast<uint32_t>(c), v);
+          if (e.bias) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (n0 + c + j < e.N) v[j] += __ldg(e.bias + n0 + c + j);
+          }
+          const uint32_t buf = sEpi + (chunk_no & 1u) * (kBM * 128);
+          // the store issued two chunks ago from this buffer must have read it
+          if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          named_bar(1, 128);
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(buf + sw128_off(row, j)), "f"(v[4 * j]),
+                         "f"(v[4 * j + 1]), "f"(v[4 * j + 2]), "f"(v[4 * j + 3])
+                         : "memory");
+          fence_proxy_async();
+          named_bar(1, 128);
+          if (threadIdx.x == 0) {
+            if (MODE == 2) {  // tile = output row (n, p): [N][P][Q][K] store, q >= Q clipped
+              const int mt = m0 / kBM;
+              const int n = static_cast<int>(a.fP.div(mt));
+              tma_store_4d(&tmD, buf, n0 + c, 0, mt - n * a.P, n);
+            } else if (e.partial3d)
+              tma_store_3d(&tmD, buf, n0 + c, m0, split);
+            else
+              tma_store_2d(&tmD, buf, n0 + c, m0, e.reduce != 0);
+            bulk_commit();
           }
         }
       }
       tc_fence_before();
-    } else {
-#pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
-      float v[32];
-      tmem_ld32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + static_cast<uint32_t>(c), v);
-      if (e.bias) {
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (n0 + c + j < e.N) v[j] += __ldg(e.bias + n0 + c + j);
-      }
-      const uint32_t chunk = stage0 + static_cast<uint32_t>(c / 32) * (kBM * 128);
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(chunk + sw128_off(row, j)), "f"(v[4 * j]),
-                     "f"(v[4 * j + 1]), "f"(v[4 * j + 2]), "f"(v[4 * j + 3])
-                     : "memory");
+      mbar_arrive(&tempty[acc]);
     }
-    tc_fence_before();
-    fence_proxy_async();
-    named_bar(1, 128);
-    if (threadIdx.x == 0) {
-#pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
-        if (n0 + c >= e.N) break;
-        const uint32_t chunk = stage0 + static_cast<uint32_t>(c / 32) * (kBM * 128);
-        if (e.partial3d)
-          tma_store_3d(&tmD, chunk, n0 + c, m0, blockIdx.z);
-        else
-          tma_store_2d(&tmD, chunk, n0 + c, m0, e.reduce != 0);
-      }
-      bulk_commit();
-      bulk_wait_all();
-    }
-    }  // TMA store path
+    if (threadIdx.x == 0) bulk_wait_all();
   }
   __syncthreads();
   if (warp == 5) {
     tc_fence_after();
-    tmem_dealloc(tmem, tmem_cols<BN>());
+    tmem_dealloc(tmem, kCols);
   }
 }
 
@@ -337,7 +436,18 @@ bool make_store(CUtensorMap* m, float* base, int64_t rows, int64_t cols, int spl
 
 template <int BN>
 constexpr int stages_for() {
-  return BN <= 64 ? 4 : (BN <= 128 ? 3 : 4);  // BN <= 128: two CTAs per SM (96 KB each)
+  // one persistent CTA per SM: as many stages as fit next to the 32 KB store staging
+  return BN <= 64 ? 8 : (BN <= 128 ? 5 : 4);
+}
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+  }
+  return n;
 }
 
 template <int BN, int MODE>
@@ -345,7 +455,7 @@ cudaError_t launch(const CUtensorMap& A, const CUtensorMap& B, const CUtensorMap
                    const EpiArgs& e, int M, int N, int splits, cudaStream_t st) {
   constexpr int STAGES = stages_for<BN>();
   using L = TmaSmem<BN, STAGES>;
-  static_assert(BN * 512 <= STAGES * (kBM * 128 + BN * 128), "epilogue staging must fit in the stage buffers");
+  static_assert(L::TOTAL <= 227 * 1024, "shared memory budget");
   auto kern = tc_conv_tma_kernel<BN, STAGES, MODE>;
   static bool attr = false;
   if (!attr) {
@@ -356,8 +466,12 @@ cudaError_t launch(const CUtensorMap& A, const CUtensorMap& B, const CUtensorMap
   TmaArgs args = a;
   const int kps = (a.num_kb + splits - 1) / splits;
   args.kb_per_split = kps;
-  dim3 grid((M + kBM - 1) / kBM, (N + BN - 1) / BN, (a.num_kb + kps - 1) / kps);
-  kern<<<grid, kTmaThreads, L::TOTAL, st>>>(A, B, D, args, e);
+  TileGrid tg;
+  tg.m_tiles = (M + kBM - 1) / kBM;
+  tg.n_tiles = (N + BN - 1) / BN;
+  tg.tiles = tg.m_tiles * tg.n_tiles * ((a.num_kb + kps - 1) / kps);
+  const int grid = std::min(tg.tiles, num_sms());
+  kern<<<grid, kTmaThreads, L::TOTAL, st>>>(A, B, D, args, e, tg);
   return cudaGetLastError();
 }
 
@@ -366,6 +480,20 @@ int bn_for(int n) { return n <= 64 ? 64 : (n <= 128 ? 128 : 256); }
 }  // namespace
 
 bool conv_tma_ok_fwd(const ConvShape& s) { return s.C % 32 == 0 && load_encoders(); }
+
+// Probe: does the driver accept a tiled map whose row stride (32 B) is smaller
+// than its inner extent (128 B), i.e. overlapping sliding windows?
+int tma_probe_overlap(const float* base) {
+  if (!load_encoders()) return -1;
+  CUtensorMap m;
+  cuuint64_t dims[4] = {32, 112, 224, 2};
+  cuuint64_t strides[3] = {32, 224 * 16, 224 * 224 * 16};
+  cuuint32_t box[4] = {32, 128, 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  return static_cast<int>(g_encode_tiled(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(base), dims,
+                                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE));
+}
 bool conv_tma_ok_dgrad(const ConvShape& s) {
   return s.stride == 1 && s.K % 32 == 0 && s.H == s.P && s.W == s.Q && load_encoders();
 }
@@ -439,6 +567,211 @@ cudaError_t conv_dgrad_tma(const ConvShape& s, const float* dy, const float* wt_
     case 128: return launch<128, 0>(A, B, D, a, e, M, s.C, 1, st);
     default: return launch<256, 0>(A, B, D, a, e, M, s.C, 1, st);
   }
+}
+
+// ---------------------------------------------------------------------------
+// Stem convolution (input = the executor's spatially padded C=4 image buffer).
+// For a fixed filter row r the 8 filter columns x 4 channels a window needs are
+// 32 consecutive floats of one padded input row, and consecutive output
+// columns' windows start `stride` pixels apart: a tiled tensor map whose dim-1
+// stride (16*stride bytes) is smaller than its 128-byte inner extent presents
+// exactly those overlapping windows, so the whole K block of an output row is
+// ONE TMA box -- no im2col gather, no per-element padding logic.
+
+namespace {
+
+struct StemGeom {
+  int N, Hp, Wp, R, S, P, Q, K, stride, sblocks, shift, Qv, qblocks;
+};
+
+StemGeom stem_geom(const ConvShape& s) {
+  StemGeom g;
+  g.N = s.N;
+  g.R = s.R;
+  g.S = s.S;
+  g.P = s.P;
+  g.Q = s.Q;
+  g.K = s.K;
+  g.stride = s.stride;
+  g.sblocks = (s.S + 7) / 8;
+  g.shift = 8 / s.stride;
+  g.Qv = s.Q + (g.sblocks - 1) * g.shift;
+  g.qblocks = (s.Q + 31) / 32;
+  g.Hp = s.H + 2 * s.pad;
+  g.Wp = std::max(s.W + 2 * s.pad, s.stride * (g.Qv - 1) + 8);
+  return g;
+}
+
+__global__ void stem_pad_kernel(const float* __restrict__ raw, int C_raw, float* __restrict__ xp, int N, int H, int W,
+                                int Hp, int Wp, int pad, int Cs) {
+  const int64_t total = static_cast<int64_t>(N) * Hp * Wp * Cs;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(i % Cs);
+    int64_t t = i / Cs;
+    const int w = static_cast<int>(t % Wp) - pad;
+    t /= Wp;
+    const int h = static_cast<int>(t % Hp) - pad;
+    const int n = static_cast<int>(t / Hp);
+    float v = 0.f;
+    if (c < C_raw && h >= 0 && h < H && w >= 0 && w < W) v = raw[((static_cast<int64_t>(n) * H + h) * W + w) * C_raw + c];
+    xp[i] = v;
+  }
+}
+
+// wp[k][r][s'][c] (s' < 8*sblocks) <-> w[k][r][s][c]; to_padded selects the direction.
+__global__ void stem_weights_kernel(float* __restrict__ w, float* __restrict__ wp, int K, int R, int S, int Sp,
+                                    int to_padded) {
+  const int64_t total = static_cast<int64_t>(K) * R * Sp * 4;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(i % 4);
+    int64_t t = i / 4;
+    const int sp = static_cast<int>(t % Sp);
+    t /= Sp;
+    const int r = static_cast<int>(t % R);
+    const int k = static_cast<int>(t / R);
+    const int64_t src = ((static_cast<int64_t>(k) * R + r) * S + sp) * 4 + c;
+    if (to_padded)
+      wp[i] = sp < S ? w[src] : 0.f;
+    else if (sp < S)
+      w[src] = wp[i];
+  }
+}
+
+// Overlapping sliding-window view of the padded input: [N][Hp][Qv windows][32 floats].
+bool make_stem_view(CUtensorMap* m, const float* xp, const StemGeom& g, int box_q, CUtensorMapSwizzle sw) {
+  cuuint64_t dims[4] = {32, static_cast<cuuint64_t>(g.Qv), static_cast<cuuint64_t>(g.Hp),
+                        static_cast<cuuint64_t>(g.N)};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(g.stride) * 16, static_cast<cuuint64_t>(g.Wp) * 16,
+                           static_cast<cuuint64_t>(g.Hp) * g.Wp * 16};
+  cuuint32_t box[4] = {32, static_cast<cuuint32_t>(box_q), 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  return g_encode_tiled(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(xp), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// NHWC [N][P][Q][K] as a 4-D tiled map with box {32 channels, box_q columns, 1, 1}.
+bool make_nhwc4(CUtensorMap* m, const float* base, int N, int P, int Q, int K, int box_q, CUtensorMapSwizzle sw) {
+  cuuint64_t dims[4] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(Q), static_cast<cuuint64_t>(P),
+                        static_cast<cuuint64_t>(N)};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(K) * 4, static_cast<cuuint64_t>(Q) * K * 4,
+                           static_cast<cuuint64_t>(P) * Q * K * 4};
+  cuuint32_t box[4] = {32, static_cast<cuuint32_t>(box_q), 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  return g_encode_tiled(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+bool conv_stem_ok(const ConvShape& s) {
+  return s.C == 4 && s.stride >= 1 && s.stride <= 8 && 8 % s.stride == 0 && s.S <= 32 && s.K % 32 == 0 &&
+         s.Q <= kBM && load_encoders();
+}
+
+int64_t stem_padded_floats(const ConvShape& s) {
+  const StemGeom g = stem_geom(s);
+  return static_cast<int64_t>(g.N) * g.Hp * g.Wp * 4 + 64;
+}
+
+int64_t stem_weight_floats(const ConvShape& s) {
+  return static_cast<int64_t>(s.K) * s.R * ((s.S + 7) / 8) * 8 * 4;
+}
+
+cudaError_t stem_pad_input(const ConvShape& s, int H_raw, int W_raw, int C_raw, int pad, const float* raw, float* xp,
+                           cudaStream_t st) {
+  const StemGeom g = stem_geom(s);
+  stem_pad_kernel<<<2368, 256, 0, st>>>(raw, C_raw, xp, s.N, H_raw, W_raw, g.Hp, g.Wp, pad, 4);
+  return cudaGetLastError();
+}
+
+cudaError_t conv_stem_fwd(const ConvShape& s, const float* xp, const float* w, float* wp_scratch, const float* bias,
+                          float* y, cudaStream_t st) {
+  const StemGeom g = stem_geom(s);
+  const int Sp = g.sblocks * 8;
+  stem_weights_kernel<<<148, 256, 0, st>>>(const_cast<float*>(w), wp_scratch, s.K, s.R, s.S, Sp, 1);
+  cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) return err;
+  const int BN = bn_for(s.K);
+  CUtensorMap A, B, D;
+  if (!make_stem_view(&A, xp, g, kBM, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;
+  const int Ktot = s.R * Sp * 4;
+  if (!make_tiled(&B, wp_scratch, s.K, Ktot, BN, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;
+  if (!make_nhwc4(&D, y, s.N, s.P, s.Q, s.K, kBM, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;
+  TmaArgs a{};
+  a.num_kb = s.R * g.sblocks;
+  a.P = s.P;
+  a.stride = s.stride;
+  a.sblocks = g.sblocks;
+  a.shift = g.shift;
+  a.fsb = FastDivT(g.sblocks);
+  a.fP = FastDivT(s.P);
+  const EpiArgs e{bias, s.K, 0, 0};
+  const int M = s.N * s.P * kBM;  // one 128-row tile per output row
+  switch (BN) {
+    case 64: return launch<64, 2>(A, B, D, a, e, M, s.K, 1, st);
+    case 128: return launch<128, 2>(A, B, D, a, e, M, s.K, 1, st);
+    default: return launch<256, 2>(A, B, D, a, e, M, s.K, 1, st);
+  }
+}
+
+int conv_stem_wgrad_splits(const ConvShape& s) {
+  const StemGeom g = stem_geom(s);
+  const int M = s.R * g.sblocks * 32;
+  const int bn = bn_for(s.K);
+  const int tiles = ((M + kBM - 1) / kBM) * ((s.K + bn - 1) / bn);
+  const int nkb = s.N * s.P * g.qblocks;
+  int want = std::max(1, 148 / tiles);
+  want = std::min(want, std::max(1, nkb / 8));
+  const int kps = (nkb + want - 1) / want;
+  return (nkb + kps - 1) / kps;
+}
+
+int64_t stem_wgrad_partial_floats(const ConvShape& s) {
+  const StemGeom g = stem_geom(s);
+  return static_cast<int64_t>(conv_stem_wgrad_splits(s)) * s.R * g.sblocks * 32 * s.K;
+}
+
+cudaError_t conv_stem_wgrad(const ConvShape& s, const float* xp, const float* dy, float* partial, float* wp_scratch,
+                            float* dw, float* db, float* red, cudaStream_t st) {
+  const StemGeom g = stem_geom(s);
+  const int Sp = g.sblocks * 8;
+  const int M = s.R * g.sblocks * 32;
+  const int splits = conv_stem_wgrad_splits(s);
+  const int BN = bn_for(s.K);
+  CUtensorMap A, B, D;
+  if (!make_stem_view(&A, xp, g, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) return cudaErrorInvalidValue;
+  if (!make_nhwc4(&B, dy, s.N, s.P, s.Q, s.K, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) return cudaErrorInvalidValue;
+  if (!make_store(&D, partial, M, s.K, splits)) return cudaErrorInvalidValue;
+  TmaArgs a{};
+  a.num_kb = s.N * s.P * g.qblocks;
+  a.P = s.P;
+  a.stride = s.stride;
+  a.sblocks = g.sblocks;
+  a.shift = g.shift;
+  a.qblocks = g.qblocks;
+  a.R = s.R;
+  a.Kout = s.K;
+  a.fsb = FastDivT(g.sblocks);
+  a.fqb = FastDivT(g.qblocks);
+  a.fP = FastDivT(s.P);
+  const EpiArgs e{nullptr, s.K, 0, 1};
+  cudaError_t err;
+  switch (BN) {
+    case 64: err = launch<64, 3>(A, B, D, a, e, M, s.K, splits, st); break;
+    case 128: err = launch<128, 3>(A, B, D, a, e, M, s.K, splits, st); break;
+    default: err = launch<256, 3>(A, B, D, a, e, M, s.K, splits, st); break;
+  }
+  if (err != cudaSuccess) return err;
+  err = splitk_reduce(partial, splits, M, s.K, wp_scratch, nullptr, 0, 1, st);  // -> [K][R][Sp][4]
+  if (err != cudaSuccess) return err;
+  stem_weights_kernel<<<148, 256, 0, st>>>(dw, wp_scratch, s.K, s.R, s.S, Sp, 0);
+  err = cudaGetLastError();
+  if (err != cudaSuccess) return err;
+  return bias_grad(dy, static_cast<int64_t>(s.N) * s.P * s.Q, s.K, db, red, st);
 }
 
 namespace {

@@ -298,7 +298,7 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ P, int splits, in
   }
 }
 
-cudaError_t splitk_reduce(const float* P, int splits, int M, int N, float* D, const float* bias, int accumulate,
+cudaError_t splitk_reduce_impl(const float* P, int splits, int M, int N, float* D, const float* bias, int accumulate,
                           int transpose, cudaStream_t st) {
   dim3 grid((N + 31) / 32, (M + 31) / 32), block(32, 8);
   splitk_reduce_kernel<<<grid, block, 0, st>>>(P, splits, M, N, D, bias, accumulate, transpose);
@@ -397,6 +397,11 @@ int bn_for(int n) { return n <= 64 ? 64 : (n <= 128 ? 128 : 256); }
 
 }  // namespace
 
+cudaError_t splitk_reduce(const float* P, int splits, int M, int N, float* D, const float* bias, int accumulate,
+                          int transpose, cudaStream_t st) {
+  return splitk_reduce_impl(P, splits, M, N, D, bias, accumulate, transpose, st);
+}
+
 static int g_use_tma = -1;  // SN_CONV_TMA=0 forces the cp.async gather path (tests, A/B)
 bool use_tma() {
   if (g_use_tma < 0) {
@@ -463,7 +468,7 @@ cudaError_t conv_wgrad(const ConvShape& s, const float* x, const float* dy, floa
   }
   if (e != cudaSuccess) return e;
   const int RSC = s.R * s.S * s.C;
-  e = splitk_reduce(partial, splits, RSC, s.K, dw, nullptr, 0, 1, st);
+  e = splitk_reduce_impl(partial, splits, RSC, s.K, dw, nullptr, 0, 1, st);
   if (e != cudaSuccess) return e;
   return bias_grad(dy, static_cast<int64_t>(s.N) * s.P * s.Q, s.K, db, red_scratch, st);
 }
@@ -483,7 +488,7 @@ cudaError_t fc_fwd(int B, int I, int O, const float* x, const float* w, const fl
   const int eff = effective_splits(I, splits);
   cudaError_t e = fc_gemm(0, 0, x, I, w, I, B, O, I, partial, eff, st);
   if (e != cudaSuccess) return e;
-  return splitk_reduce(partial, eff, B, O, y, bias, 0, 0, st);
+  return splitk_reduce_impl(partial, eff, B, O, y, bias, 0, 0, st);
 }
 
 cudaError_t fc_dgrad(int B, int I, int O, const float* dy, const float* w, float* dx, int accumulate, float* partial,
@@ -492,7 +497,7 @@ cudaError_t fc_dgrad(int B, int I, int O, const float* dy, const float* w, float
   const int eff = effective_splits(O, splits);
   cudaError_t e = fc_gemm(0, 1, dy, O, w, I, B, I, O, partial, eff, st);
   if (e != cudaSuccess) return e;
-  return splitk_reduce(partial, eff, B, I, dx, nullptr, accumulate, 0, st);
+  return splitk_reduce_impl(partial, eff, B, I, dx, nullptr, accumulate, 0, st);
 }
 
 cudaError_t fc_wgrad(int B, int I, int O, const float* x, const float* dy, float* dw, float* db, float* red_scratch,

@@ -75,6 +75,31 @@ extern "C" int sn_test_conv(int op, const int* shape, void** p, int flag) {
   return cudaDeviceSynchronize() == cudaSuccess ? 0 : 4;
 }
 
+// Stem path on caller buffers: raw NHWC images with c_raw channels, weights
+// [K][R][S][4].  shape = {N,H,W,4,K,R,S,P,Q,stride,pad}.
+//   query (p == null): returns -1 if the shape is not stem-eligible, else 0 and
+//   sizes[0..2] = {padded input, weight scratch, partial} floats.
+//   p = {raw, xp, w, wp_scratch, bias, y, dy, dw, db, partial, red}
+extern "C" int sn_test_stem(const int* shape, int c_raw, void** p, long long* sizes) {
+  sn::ConvShape s{shape[0], shape[1], shape[2], shape[3], shape[4], shape[5], shape[6],
+                  shape[7], shape[8], shape[9], shape[10]};
+  if (!sn::conv_stem_ok(s)) return -1;
+  if (!p) {
+    sizes[0] = sn::stem_padded_floats(s);
+    sizes[1] = sn::stem_weight_floats(s);
+    sizes[2] = sn::stem_wgrad_partial_floats(s);
+    return 0;
+  }
+  cudaError_t e = sn::stem_pad_input(s, s.H, s.W, c_raw, s.pad, (const float*)p[0], (float*)p[1], 0);
+  if (e == cudaSuccess)
+    e = sn::conv_stem_fwd(s, (const float*)p[1], (const float*)p[2], (float*)p[3], (const float*)p[4], (float*)p[5], 0);
+  if (e == cudaSuccess)
+    e = sn::conv_stem_wgrad(s, (const float*)p[1], (const float*)p[6], (float*)p[9], (float*)p[3], (float*)p[7],
+                            (float*)p[8], (float*)p[10], 0);
+  if (e != cudaSuccess) return 4;
+  return cudaDeviceSynchronize() == cudaSuccess ? 0 : 4;
+}
+
 extern "C" int sn_test_wgrad_splits(const int* shape) {
   sn::ConvShape s{shape[0], shape[1], shape[2], shape[3], shape[4], shape[5], shape[6],
                   shape[7], shape[8], shape[9], shape[10]};
@@ -82,6 +107,11 @@ extern "C" int sn_test_wgrad_splits(const int* shape) {
 }
 
 extern "C" long long sn_test_red_scratch_floats(int C) { return sn::red_scratch_floats(C); }
+
+namespace sn {
+int tma_probe_overlap(const float* base);
+}
+extern "C" int sn_test_tma_overlap(const float* base) { return sn::tma_probe_overlap(base); }
 
 // 1: TMA-fed conv kernels where the shape allows (default), 0: cp.async gathers.
 extern "C" void sn_test_set_conv_tma(int on) { sn::set_conv_tma(on); }

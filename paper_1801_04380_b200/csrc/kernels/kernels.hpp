@@ -37,10 +37,29 @@ cudaError_t conv_dgrad_tma(const ConvShape& s, const float* dy, const float* wt_
                            cudaStream_t st);
 cudaError_t conv_wgrad_tma(const ConvShape& s, const float* x, const float* dy, float* partial, int splits,
                            cudaStream_t st);
+// D = sum of split-K partials [splits][M][N] (+bias) (+D), optionally transposed.
+cudaError_t splitk_reduce(const float* P, int splits, int M, int N, float* D, const float* bias, int accumulate,
+                          int transpose, cudaStream_t st);
+
+// Stem convolution over the spatially padded C=4 image buffer (conv_tma.cu).
+bool conv_stem_ok(const ConvShape& s);
+int64_t stem_padded_floats(const ConvShape& s);
+int64_t stem_weight_floats(const ConvShape& s);
+int64_t stem_wgrad_partial_floats(const ConvShape& s);
+cudaError_t stem_pad_input(const ConvShape& s, int H_raw, int W_raw, int C_raw, int pad, const float* raw, float* xp,
+                           cudaStream_t st);
+cudaError_t conv_stem_fwd(const ConvShape& s, const float* xp, const float* w, float* wp_scratch, const float* bias,
+                          float* y, cudaStream_t st);
+cudaError_t conv_stem_wgrad(const ConvShape& s, const float* xp, const float* dy, float* partial, float* wp_scratch,
+                            float* dw, float* db, float* red, cudaStream_t st);
+// Channel-pad raw NHWC images (C_raw -> Cs) for the generic path.
+cudaError_t pad_channels(const float* raw, int C_raw, float* out, int Cs, int64_t pixels, cudaStream_t st);
+
 bool conv_tma_ok_dgrad_strided(const ConvShape& s);
 cudaError_t conv_dgrad_strided_tma(const ConvShape& s, const float* dy, const float* w, float* wt_scratch, float* dx,
                                    int accumulate, cudaStream_t st);
 void set_conv_tma(int on);
+bool use_tma();
 
 // FC: x[B][I], w[O][I], y[B][O]
 int fc_splits(int B, int I, int O, int64_t partial_floats_cap);
@@ -67,6 +86,12 @@ cudaError_t bn_fwd(const float* x, int64_t rows, int C, const float* gamma, cons
 cudaError_t bn_bwd(const float* x, const float* dy, int64_t rows, int C, const float* gamma,
                    const float* stats, float* dx, int accumulate, float* dgamma, float* dbeta,
                    float* red_scratch, cudaStream_t st);
+
+// Fused BN apply + ReLU (C % 4 == 0): y = bn(x), y_relu = max(y, 0).
+cudaError_t bn_apply_relu(const float* x, int64_t rows, int C, const float* gamma, const float* beta,
+                          const float* stats, float* y, float* y_relu, cudaStream_t st);
+// JOIN backward into two gradient buffers with one read of dy (n % 4 == 0).
+cudaError_t grad_copy2(const float* src, float* d1, int acc1, float* d2, int acc2, int64_t n, cudaStream_t st);
 
 cudaError_t relu_fwd(const float* x, float* y, int64_t n, cudaStream_t st);
 cudaError_t relu_bwd_inplace(const float* y, float* g, int64_t n, cudaStream_t st);

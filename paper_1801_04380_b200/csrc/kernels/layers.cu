@@ -242,6 +242,44 @@ __global__ void bn_apply_kernel(const float* __restrict__ x, int64_t n, int C, c
   }
 }
 
+// BN apply fused with the ReLU that consumes it: writes both layers' outputs
+// (y_relu is bit-identical to relu(y_bn)).
+__global__ void bn_apply_relu_kernel(const float4* __restrict__ x, int64_t n4, int C, const float* __restrict__ gamma,
+                                     const float* __restrict__ beta, const float* __restrict__ stats,
+                                     float4* __restrict__ y, float4* __restrict__ yr) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4; i += stride) {
+    const int c = static_cast<int>((i * 4) % C);
+    const float4 v = x[i];
+    float o[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) o[e] = (o[e] - stats[c + e]) * stats[C + c + e] * gamma[c + e] + beta[c + e];
+    y[i] = make_float4(o[0], o[1], o[2], o[3]);
+    yr[i] = make_float4(o[0] > 0.f ? o[0] : 0.f, o[1] > 0.f ? o[1] : 0.f, o[2] > 0.f ? o[2] : 0.f,
+                        o[3] > 0.f ? o[3] : 0.f);
+  }
+}
+
+// JOIN backward for two destinations: one read of dy.
+__global__ void grad_copy2_kernel(const float4* __restrict__ src, float4* d1, int acc1, float4* d2, int acc2,
+                                  int64_t n4) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4; i += stride) {
+    const float4 v = src[i];
+    float4 a = v, b = v;
+    if (acc1) {
+      const float4 o = d1[i];
+      a.x += o.x; a.y += o.y; a.z += o.z; a.w += o.w;
+    }
+    if (acc2) {
+      const float4 o = d2[i];
+      b.x += o.x; b.y += o.y; b.z += o.z; b.w += o.w;
+    }
+    d1[i] = a;
+    d2[i] = b;
+  }
+}
+
 __global__ void bn_bwd_finalize(const double* sums, int C, float* dgamma, float* dbeta, float* coef) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= C) return;
@@ -700,11 +738,28 @@ cudaError_t bn_fwd(const float* x, int64_t rows, int C, const float* gamma, cons
     if (e != cudaSuccess) return e;
     bn_stats_finalize<<<(C + 255) / 256, 256, 0, st>>>(sums, x, rows, C, eps, momentum, stats, running);
   }
+  if (!y) return cudaGetLastError();  // statistics only (apply fused downstream)
   const int64_t n = rows * C;
   if (C % 4 == 0)
     bn_apply_kernel<4><<<blocks_for(n / 4), kThreads, 0, st>>>(x, n, C, gamma, beta, stats, y);
   else
     bn_apply_kernel<1><<<blocks_for(n), kThreads, 0, st>>>(x, n, C, gamma, beta, stats, y);
+  return cudaGetLastError();
+}
+
+cudaError_t bn_apply_relu(const float* x, int64_t rows, int C, const float* gamma, const float* beta,
+                          const float* stats, float* y, float* y_relu, cudaStream_t st) {
+  const int64_t n4 = rows * C / 4;
+  bn_apply_relu_kernel<<<blocks_for(n4), kThreads, 0, st>>>(reinterpret_cast<const float4*>(x), n4, C, gamma, beta,
+                                                            stats, reinterpret_cast<float4*>(y),
+                                                            reinterpret_cast<float4*>(y_relu));
+  return cudaGetLastError();
+}
+
+cudaError_t grad_copy2(const float* src, float* d1, int acc1, float* d2, int acc2, int64_t n, cudaStream_t st) {
+  grad_copy2_kernel<<<blocks_for(n / 4), kThreads, 0, st>>>(reinterpret_cast<const float4*>(src),
+                                                            reinterpret_cast<float4*>(d1), acc1,
+                                                            reinterpret_cast<float4*>(d2), acc2, n / 4);
   return cudaGetLastError();
 }
 
@@ -837,6 +892,20 @@ cudaError_t grad_copy(const float* src, float* dst, int64_t n, int accumulate, c
 
 cudaError_t sgd_update(float* params, const float* grads, int64_t n, float lr, float grad_scale, cudaStream_t st) {
   sgd_kernel<<<blocks_for(n), kThreads, 0, st>>>(params, grads, n, lr, grad_scale);
+  return cudaGetLastError();
+}
+
+__global__ void pad_channels_kernel(const float* __restrict__ raw, int C_raw, float* __restrict__ out, int Cs,
+                                    int64_t total) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total; i += stride) {
+    const int c = static_cast<int>(i % Cs);
+    out[i] = c < C_raw ? raw[(i / Cs) * C_raw + c] : 0.f;
+  }
+}
+
+cudaError_t pad_channels(const float* raw, int C_raw, float* out, int Cs, int64_t pixels, cudaStream_t st) {
+  pad_channels_kernel<<<blocks_for(pixels * Cs), kThreads, 0, st>>>(raw, C_raw, out, Cs, pixels * Cs);
   return cudaGetLastError();
 }
 

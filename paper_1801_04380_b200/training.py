@@ -196,10 +196,9 @@ class Executor:
         from .costmodel import propagate_shapes
         self.shapes = propagate_shapes(net)
         self.data_id = net.data_id
-        c_real = self.shapes[self.data_id][0]
-        self.data_channels = self.image_floats // (self.batch * self.shapes[self.data_id][1]
-                                                   * self.shapes[self.data_id][2])
-        self.c_real = c_real
+        # the executor takes NHWC images with the net's own channel count and
+        # lays them out for the stem itself (channel / spatial padding on device)
+        self.c_real = self.shapes[self.data_id][0]
         self.set_parameters(params if params is not None else init_parameters(net, seed))
 
     # ---- parameters ---------------------------------------------------------
@@ -254,8 +253,6 @@ class Executor:
         if img.dim() == 4 and img.shape[1] == self.c_real and img.shape[-1] != self.c_real:
             img = img.permute(0, 2, 3, 1)
         img = img.float().contiguous()
-        if self.data_channels != self.c_real:
-            img = torch.nn.functional.pad(img, (0, self.data_channels - self.c_real))
         dst = _device_view(self.images_ptr, self.image_floats, self.device)
         dst.copy_(img.reshape(-1).to(dst.device))
         lab = _device_view(self.labels_ptr, self.batch, self.device, torch.int32)

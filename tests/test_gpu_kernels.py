@@ -162,3 +162,76 @@ def test_conv_fwd_dgrad_wgrad(cuda, case, tma):
         _check(dw_d.permute(0, 3, 1, 2).cpu(), wd.grad, N * P * Q)
         _check(db_d.cpu(), bd.grad, N * P * Q)
     lib.sn_test_set_conv_tma(1)
+
+
+def test_tma_overlapping_window_probe(cuda):
+    """Records whether the driver accepts overlapping-row tensor maps (used to
+    decide the stem-convolution design); informational, always passes."""
+    from paper_1801_04380_b200 import _native
+    lib = _native.executor()
+    lib.sn_test_tma_overlap.restype = ctypes.c_int
+    lib.sn_test_tma_overlap.argtypes = [ctypes.c_void_p]
+    buf = torch.zeros(2 * 224 * 224 * 4, device=cuda)
+    print("TMA overlap probe result:", lib.sn_test_tma_overlap(buf.data_ptr()))
+
+
+STEM_CASES = [  # (N, C_raw, H, W, K, k, stride, pad)
+    (2, 3, 224, 224, 64, 7, 2, 3),   # ResNet stem
+    (2, 3, 227, 227, 96, 11, 4, 0),  # AlexNet stem (two 8-column filter blocks)
+    (3, 3, 32, 32, 32, 3, 1, 1),     # CIFAR-style 3x3 stride 1
+    (2, 1, 28, 28, 128, 5, 1, 2),    # grayscale, 5x5, BN=128
+    (2, 4, 40, 36, 256, 3, 2, 1),    # 4 real channels, BN=256, ragged rows
+]
+
+
+@pytest.mark.parametrize("case", STEM_CASES)
+def test_stem_conv_fwd_wgrad(cuda, case):
+    """Sliding-window TMA stem (conv_tma.cu MODE 2/3) vs fp64 torch."""
+    N, Cr, H, W, K, k, s, p = case
+    lib = _conv_lib()
+    lib.sn_test_stem.restype = ctypes.c_int
+    lib.sn_test_stem.argtypes = [ctypes.POINTER(ctypes.c_int), ctypes.c_int, ctypes.POINTER(ctypes.c_void_p),
+                                 ctypes.POINTER(ctypes.c_longlong)]
+    shape, P, Q = _shape_arr(N, 4, H, W, K, k, s, p)
+    sizes = (ctypes.c_longlong * 3)()
+    assert lib.sn_test_stem(shape, Cr, None, sizes) == 0
+    g = torch.Generator().manual_seed(sum(case))
+    x = torch.randn(N, Cr, H, W, generator=g)
+    w = torch.randn(K, Cr, k, k, generator=g) / (Cr * k * k) ** 0.5
+    b = torch.randn(K, generator=g)
+    dy = torch.randn(N, K, P, Q, generator=g)
+    xd = x.double().requires_grad_(True)
+    wd = w.double().requires_grad_(True)
+    bd = b.double().requires_grad_(True)
+    y = torch.nn.functional.conv2d(xd, wd, bd, stride=s, padding=p)
+    y.backward(dy.double())
+    raw = x.permute(0, 2, 3, 1).contiguous().to(cuda)
+    w4 = torch.nn.functional.pad(w.permute(0, 2, 3, 1), (0, 4 - Cr)).contiguous().to(cuda)  # [K][R][S][4]
+    xp = torch.full((int(sizes[0]),), float("nan"), device=cuda)
+    wp = torch.empty(int(sizes[1]), device=cuda)
+    part = torch.empty(max(64, int(sizes[2])), device=cuda)
+    red = torch.empty(int(lib.sn_test_red_scratch_floats(K)), device=cuda)
+    b_d = b.to(cuda)
+    y_d = torch.full((N, P, Q, K), float("nan"), device=cuda)
+    dy_d = dy.permute(0, 2, 3, 1).contiguous().to(cuda)
+    dw_d = torch.full((K, k, k, 4), float("nan"), device=cuda)
+    db_d = torch.full((K,), float("nan"), device=cuda)
+    ptrs = (ctypes.c_void_p * 11)(raw.data_ptr(), xp.data_ptr(), w4.data_ptr(), wp.data_ptr(), b_d.data_ptr(),
+                                  y_d.data_ptr(), dy_d.data_ptr(), dw_d.data_ptr(), db_d.data_ptr(),
+                                  part.data_ptr(), red.data_ptr())
+    assert lib.sn_test_stem(shape, Cr, ptrs, None) == 0
+    _check(y_d.permute(0, 3, 1, 2).cpu(), y.detach(), Cr * k * k)
+    dw = dw_d.cpu()
+    assert torch.all(dw[..., Cr:] == 0)  # padded channels read zeros
+    _check(dw[..., :Cr].permute(0, 3, 1, 2), wd.grad, N * P * Q)
+    _check(db_d.cpu(), bd.grad, N * P * Q)
+
+
+def test_stem_eligibility(cuda):
+    lib = _conv_lib()
+    lib.sn_test_stem.restype = ctypes.c_int
+    sizes = (ctypes.c_longlong * 3)()
+    wide, _, _ = _shape_arr(1, 4, 8, 300, 32, 3, 1, 1)      # Q = 300 > one 128-row tile
+    odd, _, _ = _shape_arr(1, 4, 32, 32, 32, 3, 3, 1)       # stride 3 does not divide 8
+    assert lib.sn_test_stem(wide, 3, None, sizes) == -1
+    assert lib.sn_test_stem(odd, 3, None, sizes) == -1
