@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <map>
@@ -97,6 +98,7 @@ struct sn_exec {
   float* data_buf = nullptr;  // the DATA activation as the consumers read it (== images unless padded)
   int data_id = -1;
   int stem_layer = -1;        // CONV reading a spatially padded C=4 copy of the images (TMA stem path)
+  std::vector<char> elided;   // per layer: output fused away (never written)
   int32_t* labels = nullptr;
   float* loss_rows = nullptr;
   float* loss = nullptr;
@@ -479,7 +481,8 @@ struct Compiler {
         if (fused_bn >= 0) {
           const LayerRt& bl = ex->L[fused_bn];
           const float* bx = ptr(snp::K_ACT, net.prev[fused_bn][0]);
-          float* by = const_cast<float*>(x);  // the BN output this ReLU reads
+          // the BN output this ReLU reads; not written when nothing else reads it
+          float* by = elide_out[fused_bn] ? nullptr : const_cast<float*>(x);
           const float* g = ex->params + bl.w_off;
           const float* b = ex->params + bl.b_off;
           const float* stats = ex->state + bl.state_off;
@@ -597,18 +600,22 @@ struct Compiler {
         const float* g = ex->params + l.w_off;
         float* dg = ex->grads + l.w_off;
         float* dbt = ex->grads + l.b_off;
+        const float* beta = ex->params + l.b_off;
         const float* stats = ex->state + l.state_off;
         const int64_t rows = static_cast<int64_t>(ex->B) * l.H * l.W;
         const int C = l.C;
         float* red = ex->red;
-        push([=] { ck(sn::bn_bwd(x, dy, rows, C, g, stats, dx, acc, dg, dbt, red, st), "bn_bwd"); }, dx ? 4 : 3);
+        const int relu = bwd_relu ? 1 : 0;
+        push([=] { ck(sn::bn_bwd(x, dy, rows, C, g, beta, stats, relu, dx, acc, dg, dbt, red, st), "bn_bwd"); },
+             dx ? 4 : 3);
         break;
       }
       case snp::ACT: {
-        const float* y = ptr(snp::K_ACT, lid);
         int acc = 0;
         float* g = dx_target(pid, &acc);
         if (g && dy && g != dy) xfail(SN_EK_INTERNAL, "in-place gradient buffer mismatch");
+        if (bwd_skip) break;  // folded into the next action, the BN backward
+        const float* y = ptr(snp::K_ACT, lid);
         if (g) push([=] { ck(sn::relu_bwd_inplace(y, g, n, st), "relu_bwd"); }, 1);
         break;
       }
@@ -682,14 +689,35 @@ struct Compiler {
   // device action is the forward (replay) of the ReLU reading it, with neither
   // the BN input nor its output freed in between, is split into "statistics
   // now" + "apply fused into the ReLU" (one pass writes both outputs).
+  //
+  // Backward: a ReLU backward whose next compute action is the backward of the
+  // BN it reads (its only consumer) is folded into that BN backward, which
+  // recomputes the mask from the BN input.  When every forward / replay of the
+  // pair is fused as well, nothing reads the BN output, so it is not written.
   bool fuse_next = false;
   int fused_bn = -1;
-  std::vector<char> fuse_at;
+  bool bwd_skip = false, bwd_relu = false;
+  std::vector<char> fuse_at, act_bwd_skip, bn_bwd_relu;
   std::vector<int> fused_into;
+  std::vector<char> elide_out;  // per layer: output never materialised
+  static bool is_compute(char op) { return op == 'C' || op == 'R' || op == 'B'; }
+  bool bn_relu_pair(int act) const {
+    if (net.kind[act] != snp::ACT || net.prev[act].size() != 1) return false;
+    const int bn = net.prev[act][0];
+    return net.kind[bn] == snp::BN && net.next[bn].size() == 1 && ex->L[bn].C % 4 == 0 && !net.prev[bn].empty();
+  }
   void plan_fusions() {
     const size_t T = P.tape.size();
     fuse_at.assign(T, 0);
     fused_into.assign(T, -1);
+    act_bwd_skip.assign(T, 0);
+    bn_bwd_relu.assign(T, 0);
+    elide_out.assign(net.n, 0);
+    const char* env = std::getenv("SN_FUSE");  // SN_FUSE=0: one kernel per layer (A/B and bitwise tests)
+    if (env && env[0] == '0') {
+      ex->elided = elide_out;
+      return;
+    }
     for (size_t i = 0; i < T; ++i) {
       const snp::Event& e = P.tape[i];
       if ((e.op != 'C' && e.op != 'R') || net.kind[e.b] != snp::BN) continue;
@@ -707,6 +735,37 @@ struct Compiler {
         }
       }
     }
+    std::vector<int> act_fwd(net.n, 0), act_fwd_fused(net.n, 0), bn_fwd(net.n, 0), bn_fwd_fused(net.n, 0);
+    std::vector<char> act_bwd_fused(net.n, 0);
+    for (size_t i = 0; i < T; ++i) {
+      const snp::Event& e = P.tape[i];
+      if (e.op == 'C' || e.op == 'R') {
+        if (net.kind[e.b] == snp::ACT) {
+          ++act_fwd[e.b];
+          act_fwd_fused[e.b] += fused_into[i] >= 0;
+        } else if (net.kind[e.b] == snp::BN) {
+          ++bn_fwd[e.b];
+          bn_fwd_fused[e.b] += fuse_at[i];
+        }
+      }
+      if (e.op != 'B' || !bn_relu_pair(e.b)) continue;
+      const int bn = net.prev[e.b][0];
+      for (size_t j = i + 1; j < T; ++j) {
+        if (!is_compute(P.tape[j].op)) continue;
+        if (P.tape[j].op == 'B' && P.tape[j].b == bn) {
+          act_bwd_skip[i] = 1;
+          bn_bwd_relu[j] = 1;
+          act_bwd_fused[e.b] = 1;
+        }
+        break;
+      }
+    }
+    for (int a = 0; a < net.n; ++a) {
+      if (!bn_relu_pair(a) || !act_bwd_fused[a]) continue;
+      const int bn = net.prev[a][0];
+      if (act_fwd[a] == act_fwd_fused[a] && bn_fwd[bn] == bn_fwd_fused[bn]) elide_out[bn] = 1;
+    }
+    ex->elided = elide_out;
   }
 
   // DATA layer: lay the user's images out the way the consumers read them.
@@ -735,6 +794,8 @@ struct Compiler {
       const snp::Event& ev = P.tape[ti];
       fuse_next = fuse_at[ti] != 0;
       fused_bn = fused_into[ti];
+      bwd_skip = act_bwd_skip[ti] != 0;
+      bwd_relu = bn_bwd_relu[ti] != 0;
       switch (ev.op) {
         case 'A': on_alloc(ev); break;
         case 'F': on_free(ev); break;
@@ -1009,6 +1070,9 @@ int sn_exec_apply_update(sn_exec* ex, float lr, float grad_scale) {
 int sn_exec_read_tensor(sn_exec* ex, int32_t kind, int32_t layer, float* dst, int64_t n_floats) {
   if (!ex) return xset(SN_EK_INTERNAL, "null argument");
   return xguard([&] {
+    if (kind == snp::K_ACT && layer >= 0 && layer < static_cast<int>(ex->elided.size()) && ex->elided[layer])
+      xfail(SN_EK_UNSUPPORTED, "output of '" + ex->net->names[layer] +
+                                   "' is fused into its ReLU and never materialised (SN_FUSE=0 keeps it)");
     auto it = ex->final_keys.find(snp::key_code(kind, layer));
     if (it == ex->final_keys.end()) xfail(SN_EK_INTERNAL, "tensor is not resident at the end of the iteration");
     const float* src = reinterpret_cast<const float*>(ex->arena + it->second.first * snp::kBlockBytes);

@@ -602,20 +602,25 @@ StemGeom stem_geom(const ConvShape& s) {
   return g;
 }
 
-__global__ void stem_pad_kernel(const float* __restrict__ raw, int C_raw, float* __restrict__ xp, int N, int H, int W,
-                                int Hp, int Wp, int pad, int Cs) {
-  const int64_t total = static_cast<int64_t>(N) * Hp * Wp * Cs;
+// One thread per padded pixel: reads the C_raw (<= 4) image channels, writes
+// one float4 (zeros in the border and the padding channels).
+__global__ void stem_pad_kernel(const float* __restrict__ raw, int C_raw, float4* __restrict__ xp, int N, int H, int W,
+                                int Hp, int Wp, int pad) {
+  const int64_t total = static_cast<int64_t>(N) * Hp * Wp;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int c = static_cast<int>(i % Cs);
-    int64_t t = i / Cs;
-    const int w = static_cast<int>(t % Wp) - pad;
-    t /= Wp;
+    const int w = static_cast<int>(i % Wp) - pad;
+    const int64_t t = i / Wp;
     const int h = static_cast<int>(t % Hp) - pad;
     const int n = static_cast<int>(t / Hp);
-    float v = 0.f;
-    if (c < C_raw && h >= 0 && h < H && w >= 0 && w < W) v = raw[((static_cast<int64_t>(n) * H + h) * W + w) * C_raw + c];
-    xp[i] = v;
+    float v[4] = {0.f, 0.f, 0.f, 0.f};
+    if (h >= 0 && h < H && w >= 0 && w < W) {
+      const float* src = raw + ((static_cast<int64_t>(n) * H + h) * W + w) * C_raw;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (c < C_raw) v[c] = __ldg(src + c);
+    }
+    xp[i] = make_float4(v[0], v[1], v[2], v[3]);
   }
 }
 
@@ -684,7 +689,9 @@ int64_t stem_weight_floats(const ConvShape& s) {
 cudaError_t stem_pad_input(const ConvShape& s, int H_raw, int W_raw, int C_raw, int pad, const float* raw, float* xp,
                            cudaStream_t st) {
   const StemGeom g = stem_geom(s);
-  stem_pad_kernel<<<2368, 256, 0, st>>>(raw, C_raw, xp, s.N, H_raw, W_raw, g.Hp, g.Wp, pad, 4);
+  if (C_raw > 4) return cudaErrorInvalidValue;
+  stem_pad_kernel<<<148 * 8, 256, 0, st>>>(raw, C_raw, reinterpret_cast<float4*>(xp), s.N, H_raw, W_raw, g.Hp, g.Wp,
+                                           pad);
   return cudaGetLastError();
 }
 

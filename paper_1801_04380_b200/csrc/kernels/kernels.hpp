@@ -73,7 +73,7 @@ cudaError_t fc_wgrad(int B, int I, int O, const float* x, const float* dy, float
 // ---- memory-bound layer kernels (layers.cu) ------------------------------------
 // Per-channel column reductions over a [rows][C] matrix need a scratch of
 // kRedChunks*C*2 doubles.
-constexpr int kRedChunks = 296;
+constexpr int kRedChunks = 592;
 int64_t red_scratch_floats(int C);
 
 cudaError_t bias_grad(const float* dy, int64_t rows, int C, float* db, float* red_scratch, cudaStream_t st);
@@ -83,11 +83,15 @@ cudaError_t bias_grad(const float* dy, int64_t rows, int C, float* db, float* re
 cudaError_t bn_fwd(const float* x, int64_t rows, int C, const float* gamma, const float* beta, float* y,
                    float* stats, float* running, float eps, float momentum, int compute_stats,
                    float* red_scratch, cudaStream_t st);
-cudaError_t bn_bwd(const float* x, const float* dy, int64_t rows, int C, const float* gamma,
-                   const float* stats, float* dx, int accumulate, float* dgamma, float* dbeta,
+// relu = 1 fuses the backward of the ReLU consuming this BN: dy is then the
+// gradient w.r.t. the ReLU output and the mask bn(x) > 0 is recomputed from x
+// (bit-identical to the forward's, see bn_affine in layers.cu).
+cudaError_t bn_bwd(const float* x, const float* dy, int64_t rows, int C, const float* gamma, const float* beta,
+                   const float* stats, int relu, float* dx, int accumulate, float* dgamma, float* dbeta,
                    float* red_scratch, cudaStream_t st);
 
-// Fused BN apply + ReLU (C % 4 == 0): y = bn(x), y_relu = max(y, 0).
+// Fused BN apply + ReLU (C % 4 == 0): y = bn(x) (skipped when y is null),
+// y_relu = max(bn(x), 0).
 cudaError_t bn_apply_relu(const float* x, int64_t rows, int C, const float* gamma, const float* beta,
                           const float* stats, float* y, float* y_relu, cudaStream_t st);
 // JOIN backward into two gradient buffers with one read of dy (n % 4 == 0).

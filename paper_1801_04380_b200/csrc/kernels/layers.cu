@@ -26,52 +26,126 @@ inline int blocks_for(int64_t n, int per_block = kThreads, int cap = 148 * 16) {
 // f1 and f2 of the functor.
 
 __device__ __forceinline__ float4 ld4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+__device__ __forceinline__ float4 zero4() { return make_float4(0.f, 0.f, 0.f, 0.f); }
+__device__ __forceinline__ void add4(float4& a, const float4& b) {
+  a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+}
+__device__ __forceinline__ float relu1(float v) { return v > 0.f ? v : 0.f; }
+__device__ __forceinline__ float4 relu4(const float4& v) {
+  return make_float4(relu1(v.x), relu1(v.y), relu1(v.z), relu1(v.w));
+}
+
+// BN normalisation, written with explicit-rounding intrinsics so that the
+// forward, its replays and the ReLU mask recomputed in the fused backward are
+// bit-identical (no compiler FMA contraction choices).
+__device__ __forceinline__ float bn_xhat(float x, float m, float is) { return __fmul_rn(__fsub_rn(x, m), is); }
+__device__ __forceinline__ float bn_affine(float x, float m, float is, float g, float b) {
+  return __fmaf_rn(bn_xhat(x, m, is), g, b);
+}
+struct Bn4 {
+  float4 m, is, g, b;
+};
+__device__ __forceinline__ Bn4 bn_params4(const float* stats, const float* gamma, const float* beta, int c, int C) {
+  return Bn4{ld4(stats + c), ld4(stats + C + c), ld4(gamma + c), beta ? ld4(beta + c) : zero4()};
+}
+__device__ __forceinline__ float4 bn_affine4(const float4& v, const Bn4& p) {
+  return make_float4(bn_affine(v.x, p.m.x, p.is.x, p.g.x, p.b.x), bn_affine(v.y, p.m.y, p.is.y, p.g.y, p.b.y),
+                     bn_affine(v.z, p.m.z, p.is.z, p.g.z, p.b.z), bn_affine(v.w, p.m.w, p.is.w, p.g.w, p.b.w));
+}
+
+// Element loops keep kUnroll independent 16-byte loads in flight per thread
+// (grid-stride loop unrolled by hand, loads before math): with ~2k threads per
+// SM that is enough outstanding bytes to cover HBM latency.
+constexpr int kUnroll = 4;
+constexpr int kEltBlocks = 148 * 8;  // 2048 threads per SM
+
+inline int elt_blocks(int64_t n4, int min_threads = 1) {
+  int64_t b = (n4 + kThreads - 1) / kThreads;
+  b = b < 1 ? 1 : (b > kEltBlocks ? kEltBlocks : b);
+  const int64_t need = (min_threads + kThreads - 1) / kThreads;
+  return static_cast<int>(b > need ? b : need);
+}
+
+// Per-channel loops: the stride is a multiple of C/4, so each thread's channel
+// quad is fixed and its per-channel parameters stay in registers.
+struct ChanLoop {
+  int64_t S, start;
+  int c;
+  bool active;
+};
+__device__ __forceinline__ ChanLoop chan_loop(int C4) {
+  const int64_t T = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  ChanLoop L;
+  L.S = (T / C4) * C4;
+  L.start = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  L.active = L.start < L.S;
+  L.c = static_cast<int>(L.start % C4) * 4;
+  return L;
+}
 
 struct RedBiasOp {  // f1 = dy
   const float* dy;
+  struct P {};
+  __device__ P prep4(int, int) const { return P{}; }
   __device__ void eval(int64_t row, int c, int C, float& a, float& b) const {
     a = dy[row * C + c];
     b = 0.f;
   }
-  __device__ void eval4(int64_t row, int c, int C, float4& a, float4& b) const {
+  __device__ void eval4(const P&, int64_t row, int c, int C, float4& a, float4& b) const {
     a = ld4(dy + row * C + c);
-    b = make_float4(0.f, 0.f, 0.f, 0.f);
+    b = zero4();
   }
 };
 struct RedBnStatsOp {  // f1 = x - x[0][c], f2 = (x - x[0][c])^2
   const float* x;
+  struct P {
+    float4 s;
+  };
+  __device__ P prep4(int c, int) const { return P{ld4(x + c)}; }
   __device__ void eval(int64_t row, int c, int C, float& a, float& b) const {
     const float d = x[row * C + c] - x[c];
     a = d;
     b = d * d;
   }
-  __device__ void eval4(int64_t row, int c, int C, float4& a, float4& b) const {
-    const float4 v = ld4(x + row * C + c), s = ld4(x + c);
-    a = make_float4(v.x - s.x, v.y - s.y, v.z - s.z, v.w - s.w);
+  __device__ void eval4(const P& p, int64_t row, int c, int C, float4& a, float4& b) const {
+    const float4 v = ld4(x + row * C + c);
+    a = make_float4(v.x - p.s.x, v.y - p.s.y, v.z - p.s.z, v.w - p.s.w);
     b = make_float4(a.x * a.x, a.y * a.y, a.z * a.z, a.w * a.w);
   }
 };
-struct RedBnBwdOp {  // f1 = dy, f2 = dy * xhat
+// f1 = g, f2 = g * xhat with g = dy, or (relu: the fused ReLU backward) g = dy
+// where the recomputed BN output is positive, else 0.
+struct RedBnBwdOp {
   const float* x;
   const float* dy;
   const float* stats;  // mean[C], invstd[C]
+  const float* gamma;
+  const float* beta;
+  int relu;
+  __device__ Bn4 prep4(int c, int C) const { return bn_params4(stats, gamma, beta, c, C); }
   __device__ void eval(int64_t row, int c, int C, float& a, float& b) const {
-    const float g = dy[row * C + c];
-    const float xh = (x[row * C + c] - stats[c]) * stats[C + c];
+    const float v = x[row * C + c];
+    float g = dy[row * C + c];
+    if (relu && !(bn_affine(v, stats[c], stats[C + c], gamma[c], beta[c]) > 0.f)) g = 0.f;
     a = g;
-    b = g * xh;
+    b = g * bn_xhat(v, stats[c], stats[C + c]);
   }
-  __device__ void eval4(int64_t row, int c, int C, float4& a, float4& b) const {
-    const float4 g = ld4(dy + row * C + c), v = ld4(x + row * C + c);
-    const float4 m = ld4(stats + c), is = ld4(stats + C + c);
+  __device__ void eval4(const Bn4& p, int64_t row, int c, int C, float4& a, float4& b) const {
+    float4 g = ld4(dy + row * C + c);
+    const float4 v = ld4(x + row * C + c);
+    if (relu) {
+      const float4 y = bn_affine4(v, p);
+      g = make_float4(y.x > 0.f ? g.x : 0.f, y.y > 0.f ? g.y : 0.f, y.z > 0.f ? g.z : 0.f, y.w > 0.f ? g.w : 0.f);
+    }
     a = g;
-    b = make_float4(g.x * ((v.x - m.x) * is.x), g.y * ((v.y - m.y) * is.y), g.z * ((v.z - m.z) * is.z),
-                    g.w * ((v.w - m.w) * is.w));
+    b = make_float4(g.x * bn_xhat(v.x, p.m.x, p.is.x), g.y * bn_xhat(v.y, p.m.y, p.is.y),
+                    g.z * bn_xhat(v.z, p.m.z, p.is.z), g.w * bn_xhat(v.w, p.m.w, p.is.w));
   }
 };
 
-// float4 variant for C % 4 == 0: a thread owns 4 adjacent channels and 4
-// independent row streams in flight (fixed per-thread order, fixed merge).
+// float4 variant for C % 4 == 0: a thread owns 4 adjacent channels and walks
+// its rows with kUnroll independent accumulators (fixed per-thread order,
+// fixed merge), so kUnroll loads per operand are in flight.
 template <class Op>
 __global__ void colred_stage1_v4(Op op, int64_t rows, int C, int64_t chunk, double* part) {
   __shared__ float4 s1[kThreads], s2[kThreads];
@@ -84,13 +158,35 @@ __global__ void colred_stage1_v4(Op op, int64_t rows, int C, int64_t chunk, doub
   const int lane = t / cb, cc = t % cb;
   for (int c0 = 0; c0 < C4; c0 += cb) {
     const int c4 = c0 + cc;
-    float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+    float4 a = zero4(), b = a;
     if (lane < lanes && c4 < C4) {
-      for (int64_t r = r0 + lane; r < r1; r += lanes) {
+      const auto p = op.prep4(c4 * 4, C);
+      float4 au[kUnroll], bu[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) au[u] = bu[u] = zero4();
+      int64_t r = r0 + lane;
+      for (; r + (kUnroll - 1) * lanes < r1; r += kUnroll * lanes) {
+        float4 fa[kUnroll], fb[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) op.eval4(p, r + u * lanes, c4 * 4, C, fa[u], fb[u]);
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          add4(au[u], fa[u]);
+          add4(bu[u], fb[u]);
+        }
+      }
+      for (; r < r1; r += lanes) {
         float4 fa, fb;
-        op.eval4(r, c4 * 4, C, fa, fb);
-        a.x += fa.x; a.y += fa.y; a.z += fa.z; a.w += fa.w;
-        b.x += fb.x; b.y += fb.y; b.z += fb.z; b.w += fb.w;
+        op.eval4(p, r, c4 * 4, C, fa, fb);
+        add4(au[0], fa);
+        add4(bu[0], fb);
+      }
+      a = au[0];
+      b = bu[0];
+#pragma unroll
+      for (int u = 1; u < kUnroll; ++u) {
+        add4(a, au[u]);
+        add4(b, bu[u]);
       }
     }
     s1[t] = a;
@@ -220,63 +316,63 @@ __global__ void bn_stats_finalize(const double* sums, const float* x, int64_t ro
   }
 }
 
-template <int VEC>
-__global__ void bn_apply_kernel(const float* __restrict__ x, int64_t n, int C, const float* __restrict__ gamma,
+__global__ void bn_apply_scalar(const float* __restrict__ x, int64_t n, int C, const float* __restrict__ gamma,
                                 const float* __restrict__ beta, const float* __restrict__ stats, float* __restrict__ y) {
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  if (VEC == 4) {
-    const int64_t n4 = n / 4;
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4; i += stride) {
-      const int c = static_cast<int>((i * 4) % C);
-      float4 v = reinterpret_cast<const float4*>(x)[i];
-      float o[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-      for (int e = 0; e < 4; ++e) o[e] = (o[e] - stats[c + e]) * stats[C + c + e] * gamma[c + e] + beta[c + e];
-      reinterpret_cast<float4*>(y)[i] = make_float4(o[0], o[1], o[2], o[3]);
-    }
-  } else {
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride) {
-      const int c = static_cast<int>(i % C);
-      y[i] = (x[i] - stats[c]) * stats[C + c] * gamma[c] + beta[c];
-    }
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride) {
+    const int c = static_cast<int>(i % C);
+    y[i] = bn_affine(x[i], stats[c], stats[C + c], gamma[c], beta[c]);
   }
 }
 
-// BN apply fused with the ReLU that consumes it: writes both layers' outputs
-// (y_relu is bit-identical to relu(y_bn)).
-__global__ void bn_apply_relu_kernel(const float4* __restrict__ x, int64_t n4, int C, const float* __restrict__ gamma,
-                                     const float* __restrict__ beta, const float* __restrict__ stats,
-                                     float4* __restrict__ y, float4* __restrict__ yr) {
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4; i += stride) {
-    const int c = static_cast<int>((i * 4) % C);
-    const float4 v = x[i];
-    float o[4] = {v.x, v.y, v.z, v.w};
+// BN apply (C % 4 == 0), optionally fused with the ReLU that consumes it:
+// y = bn(x) (skipped when null), yr = relu(y) (skipped when null).
+__global__ void bn_apply_v4(const float4* __restrict__ x, int64_t n4, int C, const float* __restrict__ gamma,
+                            const float* __restrict__ beta, const float* __restrict__ stats, float4* __restrict__ y,
+                            float4* __restrict__ yr) {
+  const ChanLoop L = chan_loop(C / 4);
+  if (!L.active) return;
+  const Bn4 p = bn_params4(stats, gamma, beta, L.c, C);
+  for (int64_t i0 = L.start; i0 < n4; i0 += kUnroll * L.S) {
+    float4 v[kUnroll];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) o[e] = (o[e] - stats[c + e]) * stats[C + c + e] * gamma[c + e] + beta[c + e];
-    y[i] = make_float4(o[0], o[1], o[2], o[3]);
-    yr[i] = make_float4(o[0] > 0.f ? o[0] : 0.f, o[1] > 0.f ? o[1] : 0.f, o[2] > 0.f ? o[2] : 0.f,
-                        o[3] > 0.f ? o[3] : 0.f);
+    for (int u = 0; u < kUnroll; ++u) v[u] = i0 + u * L.S < n4 ? x[i0 + u * L.S] : zero4();
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t i = i0 + u * L.S;
+      if (i < n4) {
+        const float4 o = bn_affine4(v[u], p);
+        if (y) y[i] = o;
+        if (yr) yr[i] = relu4(o);
+      }
+    }
   }
 }
 
 // JOIN backward for two destinations: one read of dy.
 __global__ void grad_copy2_kernel(const float4* __restrict__ src, float4* d1, int acc1, float4* d2, int acc2,
                                   int64_t n4) {
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4; i += stride) {
-    const float4 v = src[i];
-    float4 a = v, b = v;
-    if (acc1) {
-      const float4 o = d1[i];
-      a.x += o.x; a.y += o.y; a.z += o.z; a.w += o.w;
+  const int64_t T = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i0 < n4; i0 += kUnroll * T) {
+    float4 v[kUnroll], o1[kUnroll], o2[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t i = i0 + u * T;
+      v[u] = i < n4 ? src[i] : zero4();
+      o1[u] = (acc1 && i < n4) ? d1[i] : zero4();
+      o2[u] = (acc2 && i < n4) ? d2[i] : zero4();
     }
-    if (acc2) {
-      const float4 o = d2[i];
-      b.x += o.x; b.y += o.y; b.z += o.z; b.w += o.w;
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t i = i0 + u * T;
+      if (i < n4) {
+        float4 a = v[u], b = v[u];
+        if (acc1) add4(a, o1[u]);
+        if (acc2) add4(b, o2[u]);
+        d1[i] = a;
+        d2[i] = b;
+      }
     }
-    d1[i] = a;
-    d2[i] = b;
   }
 }
 
@@ -289,35 +385,76 @@ __global__ void bn_bwd_finalize(const double* sums, int C, float* dgamma, float*
   coef[C + c] = static_cast<float>(sums[C + c]);
 }
 
-template <int VEC>
-__global__ void bn_dx_kernel(const float* __restrict__ x, const float* __restrict__ dy, int64_t n, int64_t rows, int C,
-                             const float* __restrict__ gamma, const float* __restrict__ stats,
-                             const float* __restrict__ coef, float* dx, int accumulate) {
+// dx (+)= gamma*invstd*(g - sum(g)/m - xhat*sum(g*xhat)/m), g = dy or the
+// ReLU-masked dy (relu: mask recomputed from x, see RedBnBwdOp).
+__global__ void bn_dx_scalar(const float* __restrict__ x, const float* __restrict__ dy, int64_t n, int64_t rows, int C,
+                             const float* __restrict__ gamma, const float* __restrict__ beta,
+                             const float* __restrict__ stats, const float* __restrict__ coef, float* dx,
+                             int accumulate, int relu) {
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   const float inv_m = 1.0f / static_cast<float>(rows);
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n / VEC; i += stride) {
-    const int c0 = static_cast<int>((i * VEC) % C);
+  for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < n; j += stride) {
+    const int c = static_cast<int>(j % C);
+    float g = dy[j];
+    if (relu && !(bn_affine(x[j], stats[c], stats[C + c], gamma[c], beta[c]) > 0.f)) g = 0.f;
+    const float xh = bn_xhat(x[j], stats[c], stats[C + c]);
+    const float v = gamma[c] * stats[C + c] * (g - coef[c] * inv_m - xh * (coef[C + c] * inv_m));
+    dx[j] = accumulate ? dx[j] + v : v;
+  }
+}
+
+__global__ void bn_dx_v4(const float4* __restrict__ x, const float4* __restrict__ dy, int64_t n4, int64_t rows,
+                         int C, const float* __restrict__ gamma, const float* __restrict__ beta,
+                         const float* __restrict__ stats, const float* __restrict__ coef, float4* dx, int accumulate,
+                         int relu) {
+  const ChanLoop L = chan_loop(C / 4);
+  if (!L.active) return;
+  const float inv_m = 1.0f / static_cast<float>(rows);
+  const Bn4 p = bn_params4(stats, gamma, beta, L.c, C);
+  const float4 c1 = ld4(coef + L.c), c2 = ld4(coef + C + L.c);
+  const float k1[4] = {c1.x * inv_m, c1.y * inv_m, c1.z * inv_m, c1.w * inv_m};
+  const float k2[4] = {c2.x * inv_m, c2.y * inv_m, c2.z * inv_m, c2.w * inv_m};
+  const float gs[4] = {p.g.x * p.is.x, p.g.y * p.is.y, p.g.z * p.is.z, p.g.w * p.is.w};
+  const float m[4] = {p.m.x, p.m.y, p.m.z, p.m.w}, is[4] = {p.is.x, p.is.y, p.is.z, p.is.w};
+  for (int64_t i0 = L.start; i0 < n4; i0 += kUnroll * L.S) {
+    float4 xv[kUnroll], gv[kUnroll], ov[kUnroll];
 #pragma unroll
-    for (int e = 0; e < VEC; ++e) {
-      const int64_t j = i * VEC + e;
-      const int c = c0 + e;
-      const float xh = (x[j] - stats[c]) * stats[C + c];
-      const float v = gamma[c] * stats[C + c] * (dy[j] - coef[c] * inv_m - xh * coef[C + c] * inv_m);
-      dx[j] = accumulate ? dx[j] + v : v;
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t i = i0 + u * L.S;
+      xv[u] = i < n4 ? x[i] : zero4();
+      gv[u] = i < n4 ? dy[i] : zero4();
+      ov[u] = (accumulate && i < n4) ? dx[i] : zero4();
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t i = i0 + u * L.S;
+      if (i >= n4) break;
+      if (relu) {
+        const float4 y = bn_affine4(xv[u], p);
+        gv[u] = make_float4(y.x > 0.f ? gv[u].x : 0.f, y.y > 0.f ? gv[u].y : 0.f, y.z > 0.f ? gv[u].z : 0.f,
+                            y.w > 0.f ? gv[u].w : 0.f);
+      }
+      const float xs[4] = {xv[u].x, xv[u].y, xv[u].z, xv[u].w}, gg[4] = {gv[u].x, gv[u].y, gv[u].z, gv[u].w};
+      float r[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) r[e] = gs[e] * (gg[e] - k1[e] - bn_xhat(xs[e], m[e], is[e]) * k2[e]);
+      float4 o = make_float4(r[0], r[1], r[2], r[3]);
+      if (accumulate) add4(o, ov[u]);
+      dx[i] = o;
     }
   }
 }
 
 // ---------------------------------------------------------------------------
 __global__ void relu_fwd_kernel(const float4* __restrict__ x, float4* __restrict__ y, int64_t n4) {
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4; i += stride) {
-    float4 v = x[i];
-    v.x = v.x > 0.f ? v.x : 0.f;
-    v.y = v.y > 0.f ? v.y : 0.f;
-    v.z = v.z > 0.f ? v.z : 0.f;
-    v.w = v.w > 0.f ? v.w : 0.f;
-    y[i] = v;
+  const int64_t T = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i0 < n4; i0 += kUnroll * T) {
+    float4 v[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) v[u] = i0 + u * T < n4 ? x[i0 + u * T] : zero4();
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u)
+      if (i0 + u * T < n4) y[i0 + u * T] = relu4(v[u]);
   }
 }
 __global__ void relu_fwd_tail(const float* x, float* y, int64_t from, int64_t n) {
@@ -325,15 +462,22 @@ __global__ void relu_fwd_tail(const float* x, float* y, int64_t from, int64_t n)
   if (i < n) y[i] = x[i] > 0.f ? x[i] : 0.f;
 }
 __global__ void relu_bwd_kernel(const float4* __restrict__ y, float4* g, int64_t n4) {
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4; i += stride) {
-    const float4 yy = y[i];
-    float4 v = g[i];
-    v.x = yy.x > 0.f ? v.x : 0.f;
-    v.y = yy.y > 0.f ? v.y : 0.f;
-    v.z = yy.z > 0.f ? v.z : 0.f;
-    v.w = yy.w > 0.f ? v.w : 0.f;
-    g[i] = v;
+  const int64_t T = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i0 < n4; i0 += kUnroll * T) {
+    float4 yy[kUnroll], v[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t i = i0 + u * T;
+      yy[u] = i < n4 ? y[i] : zero4();
+      v[u] = i < n4 ? g[i] : zero4();
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t i = i0 + u * T;
+      if (i < n4)
+        g[i] = make_float4(yy[u].x > 0.f ? v[u].x : 0.f, yy[u].y > 0.f ? v[u].y : 0.f, yy[u].z > 0.f ? v[u].z : 0.f,
+                           yy[u].w > 0.f ? v[u].w : 0.f);
+    }
   }
 }
 __global__ void relu_bwd_tail(const float* y, float* g, int64_t from, int64_t n) {
@@ -668,18 +812,39 @@ __global__ void loss_reduce_kernel(const float* loss_rows, int B, float* loss) {
 }
 
 // ---------------------------------------------------------------------------
+// Two-input joins (the residual add) read both operands with kUnroll loads in
+// flight; wider joins walk the inputs in order.
 __global__ void join_fwd_kernel(const float* const* __restrict__ in, int n_in, float* __restrict__ y, int64_t n) {
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t T = static_cast<int64_t>(gridDim.x) * blockDim.x;
   const int64_t n4 = n / 4;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4; i += stride) {
-    float4 acc = reinterpret_cast<const float4*>(in[0])[i];
-    for (int k = 1; k < n_in; ++k) {
-      const float4 v = reinterpret_cast<const float4*>(in[k])[i];
-      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+  const float4* a = reinterpret_cast<const float4*>(in[0]);
+  if (n_in == 2) {
+    const float4* b = reinterpret_cast<const float4*>(in[1]);
+    for (int64_t i0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i0 < n4; i0 += kUnroll * T) {
+      float4 va[kUnroll], vb[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int64_t i = i0 + u * T;
+        va[u] = i < n4 ? a[i] : zero4();
+        vb[u] = i < n4 ? b[i] : zero4();
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int64_t i = i0 + u * T;
+        if (i < n4) {
+          add4(va[u], vb[u]);
+          reinterpret_cast<float4*>(y)[i] = va[u];
+        }
+      }
     }
-    reinterpret_cast<float4*>(y)[i] = acc;
+  } else {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4; i += T) {
+      float4 acc = a[i];
+      for (int k = 1; k < n_in; ++k) add4(acc, reinterpret_cast<const float4*>(in[k])[i]);
+      reinterpret_cast<float4*>(y)[i] = acc;
+    }
   }
-  for (int64_t i = n4 * 4 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride) {
+  for (int64_t i = n4 * 4 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += T) {
     float acc = in[0][i];
     for (int k = 1; k < n_in; ++k) acc += in[k][i];
     y[i] = acc;
@@ -687,17 +852,28 @@ __global__ void join_fwd_kernel(const float* const* __restrict__ in, int n_in, f
 }
 
 __global__ void grad_copy_kernel(const float* __restrict__ src, float* dst, int64_t n, int accumulate) {
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t T = static_cast<int64_t>(gridDim.x) * blockDim.x;
   const int64_t n4 = n / 4;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4; i += stride) {
-    float4 v = reinterpret_cast<const float4*>(src)[i];
-    if (accumulate) {
-      const float4 o = reinterpret_cast<const float4*>(dst)[i];
-      v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+  const float4* s4 = reinterpret_cast<const float4*>(src);
+  float4* d4 = reinterpret_cast<float4*>(dst);
+  for (int64_t i0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i0 < n4; i0 += kUnroll * T) {
+    float4 v[kUnroll], o[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t i = i0 + u * T;
+      v[u] = i < n4 ? s4[i] : zero4();
+      o[u] = (accumulate && i < n4) ? d4[i] : zero4();
     }
-    reinterpret_cast<float4*>(dst)[i] = v;
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t i = i0 + u * T;
+      if (i < n4) {
+        if (accumulate) add4(v[u], o[u]);
+        d4[i] = v[u];
+      }
+    }
   }
-  for (int64_t i = n4 * 4 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride)
+  for (int64_t i = n4 * 4 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += T)
     dst[i] = accumulate ? dst[i] + src[i] : src[i];
 }
 
@@ -741,48 +917,53 @@ cudaError_t bn_fwd(const float* x, int64_t rows, int C, const float* gamma, cons
   if (!y) return cudaGetLastError();  // statistics only (apply fused downstream)
   const int64_t n = rows * C;
   if (C % 4 == 0)
-    bn_apply_kernel<4><<<blocks_for(n / 4), kThreads, 0, st>>>(x, n, C, gamma, beta, stats, y);
+    bn_apply_v4<<<elt_blocks(n / 4, C / 4), kThreads, 0, st>>>(reinterpret_cast<const float4*>(x), n / 4, C, gamma,
+                                                                beta, stats, reinterpret_cast<float4*>(y), nullptr);
   else
-    bn_apply_kernel<1><<<blocks_for(n), kThreads, 0, st>>>(x, n, C, gamma, beta, stats, y);
+    bn_apply_scalar<<<blocks_for(n), kThreads, 0, st>>>(x, n, C, gamma, beta, stats, y);
   return cudaGetLastError();
 }
 
 cudaError_t bn_apply_relu(const float* x, int64_t rows, int C, const float* gamma, const float* beta,
                           const float* stats, float* y, float* y_relu, cudaStream_t st) {
   const int64_t n4 = rows * C / 4;
-  bn_apply_relu_kernel<<<blocks_for(n4), kThreads, 0, st>>>(reinterpret_cast<const float4*>(x), n4, C, gamma, beta,
-                                                            stats, reinterpret_cast<float4*>(y),
-                                                            reinterpret_cast<float4*>(y_relu));
+  bn_apply_v4<<<elt_blocks(n4, C / 4), kThreads, 0, st>>>(reinterpret_cast<const float4*>(x), n4, C, gamma, beta,
+                                                           stats, reinterpret_cast<float4*>(y),
+                                                           reinterpret_cast<float4*>(y_relu));
   return cudaGetLastError();
 }
 
 cudaError_t grad_copy2(const float* src, float* d1, int acc1, float* d2, int acc2, int64_t n, cudaStream_t st) {
-  grad_copy2_kernel<<<blocks_for(n / 4), kThreads, 0, st>>>(reinterpret_cast<const float4*>(src),
+  grad_copy2_kernel<<<elt_blocks(n / 4), kThreads, 0, st>>>(reinterpret_cast<const float4*>(src),
                                                             reinterpret_cast<float4*>(d1), acc1,
                                                             reinterpret_cast<float4*>(d2), acc2, n / 4);
   return cudaGetLastError();
 }
 
-cudaError_t bn_bwd(const float* x, const float* dy, int64_t rows, int C, const float* gamma, const float* stats,
-                   float* dx, int accumulate, float* dgamma, float* dbeta, float* red_scratch, cudaStream_t st) {
+cudaError_t bn_bwd(const float* x, const float* dy, int64_t rows, int C, const float* gamma, const float* beta,
+                   const float* stats, int relu, float* dx, int accumulate, float* dgamma, float* dbeta,
+                   float* red_scratch, cudaStream_t st) {
   double* sums;
-  cudaError_t e = colred(RedBnBwdOp{x, dy, stats}, rows, C, red_scratch, &sums, st);
+  cudaError_t e = colred(RedBnBwdOp{x, dy, stats, gamma, beta, relu}, rows, C, red_scratch, &sums, st);
   if (e != cudaSuccess) return e;
   float* coef = reinterpret_cast<float*>(sums + 2 * C);
   bn_bwd_finalize<<<(C + 255) / 256, 256, 0, st>>>(sums, C, dgamma, dbeta, coef);
   const int64_t n = rows * C;
   if (dx) {
     if (C % 4 == 0)
-      bn_dx_kernel<4><<<blocks_for(n / 4), kThreads, 0, st>>>(x, dy, n, rows, C, gamma, stats, coef, dx, accumulate);
+      bn_dx_v4<<<elt_blocks(n / 4, C / 4), kThreads, 0, st>>>(
+          reinterpret_cast<const float4*>(x), reinterpret_cast<const float4*>(dy), n / 4, rows, C, gamma, beta, stats,
+          coef, reinterpret_cast<float4*>(dx), accumulate, relu);
     else
-      bn_dx_kernel<1><<<blocks_for(n), kThreads, 0, st>>>(x, dy, n, rows, C, gamma, stats, coef, dx, accumulate);
+      bn_dx_scalar<<<blocks_for(n), kThreads, 0, st>>>(x, dy, n, rows, C, gamma, beta, stats, coef, dx, accumulate,
+                                                       relu);
   }
   return cudaGetLastError();
 }
 
 cudaError_t relu_fwd(const float* x, float* y, int64_t n, cudaStream_t st) {
   const int64_t n4 = n / 4;
-  if (n4) relu_fwd_kernel<<<blocks_for(n4), kThreads, 0, st>>>(reinterpret_cast<const float4*>(x),
+  if (n4) relu_fwd_kernel<<<elt_blocks(n4), kThreads, 0, st>>>(reinterpret_cast<const float4*>(x),
                                                                    reinterpret_cast<float4*>(y), n4);
   if (n % 4) relu_fwd_tail<<<1, 4, 0, st>>>(x, y, n4 * 4, n);
   return cudaGetLastError();
@@ -790,7 +971,7 @@ cudaError_t relu_fwd(const float* x, float* y, int64_t n, cudaStream_t st) {
 
 cudaError_t relu_bwd_inplace(const float* y, float* g, int64_t n, cudaStream_t st) {
   const int64_t n4 = n / 4;
-  if (n4) relu_bwd_kernel<<<blocks_for(n4), kThreads, 0, st>>>(reinterpret_cast<const float4*>(y),
+  if (n4) relu_bwd_kernel<<<elt_blocks(n4), kThreads, 0, st>>>(reinterpret_cast<const float4*>(y),
                                                                    reinterpret_cast<float4*>(g), n4);
   if (n % 4) relu_bwd_tail<<<1, 4, 0, st>>>(y, g, n4 * 4, n);
   return cudaGetLastError();
@@ -881,12 +1062,12 @@ cudaError_t loss_reduce(const float* loss_rows, int B, float* loss, cudaStream_t
 }
 
 cudaError_t join_fwd(const float* const* inputs, int n_in, float* y, int64_t n, cudaStream_t st) {
-  join_fwd_kernel<<<blocks_for(n / 4 + 1), kThreads, 0, st>>>(inputs, n_in, y, n);
+  join_fwd_kernel<<<elt_blocks(n / 4 + 1), kThreads, 0, st>>>(inputs, n_in, y, n);
   return cudaGetLastError();
 }
 
 cudaError_t grad_copy(const float* src, float* dst, int64_t n, int accumulate, cudaStream_t st) {
-  grad_copy_kernel<<<blocks_for(n / 4 + 1), kThreads, 0, st>>>(src, dst, n, accumulate);
+  grad_copy_kernel<<<elt_blocks(n / 4 + 1), kThreads, 0, st>>>(src, dst, n, accumulate);
   return cudaGetLastError();
 }
 

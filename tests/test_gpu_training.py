@@ -238,3 +238,21 @@ def test_sgd_training_reduces_loss(cuda, alex32_case):
     losses = [ex.step(update=True)[0] for _ in range(40)]
     ex.close()
     assert min(losses[-5:]) < 0.8 * losses[0], losses
+
+
+def test_layer_fusions_are_bit_identical(cuda, monkeypatch):
+    """BN+ReLU forward/backward fusion (mask recomputed from the BN input), the
+    elided BN output and the two-way JOIN backward give exactly the unfused
+    one-kernel-per-layer results (SN_FUSE=0)."""
+    from paper_1801_04380_b200.netgen import gen_resnet
+    from paper_1801_04380_b200.training import init_parameters
+    net = gen_resnet(1, 1, 2, 1)
+    params = init_parameters(net, seed=6, head_scale=0.1)
+    images, labels = _inputs(net, 4, seed=3)
+    for feats in ("none", ALL):
+        loss, grads, _, t = _run(net, 4, 4 << 30, feats, params, images, labels)
+        monkeypatch.setenv("SN_FUSE", "0")
+        loss0, grads0, _, t0 = _run(net, 4, 4 << 30, feats, params, images, labels)
+        monkeypatch.delenv("SN_FUSE")
+        assert t.kernels < t0.kernels
+        assert loss == loss0 and _bitwise(grads, grads0)
