@@ -83,16 +83,23 @@ __device__ __forceinline__ ChanLoop chan_loop(int C4) {
   return L;
 }
 
+// Reduction operands: load() issues the raw 16-byte loads of one row (all of
+// them before any math, so kUnroll rows x operands are in flight per thread),
+// comp() turns them into the two summands.
 struct RedBiasOp {  // f1 = dy
   const float* dy;
   struct P {};
+  struct R {
+    float4 g;
+  };
   __device__ P prep4(int, int) const { return P{}; }
   __device__ void eval(int64_t row, int c, int C, float& a, float& b) const {
     a = dy[row * C + c];
     b = 0.f;
   }
-  __device__ void eval4(const P&, int64_t row, int c, int C, float4& a, float4& b) const {
-    a = ld4(dy + row * C + c);
+  __device__ R load(int64_t off) const { return R{ld4(dy + off)}; }
+  __device__ void comp(const P&, const R& r, float4& a, float4& b) const {
+    a = r.g;
     b = zero4();
   }
 };
@@ -101,15 +108,18 @@ struct RedBnStatsOp {  // f1 = x - x[0][c], f2 = (x - x[0][c])^2
   struct P {
     float4 s;
   };
+  struct R {
+    float4 v;
+  };
   __device__ P prep4(int c, int) const { return P{ld4(x + c)}; }
   __device__ void eval(int64_t row, int c, int C, float& a, float& b) const {
     const float d = x[row * C + c] - x[c];
     a = d;
     b = d * d;
   }
-  __device__ void eval4(const P& p, int64_t row, int c, int C, float4& a, float4& b) const {
-    const float4 v = ld4(x + row * C + c);
-    a = make_float4(v.x - p.s.x, v.y - p.s.y, v.z - p.s.z, v.w - p.s.w);
+  __device__ R load(int64_t off) const { return R{ld4(x + off)}; }
+  __device__ void comp(const P& p, const R& r, float4& a, float4& b) const {
+    a = make_float4(r.v.x - p.s.x, r.v.y - p.s.y, r.v.z - p.s.z, r.v.w - p.s.w);
     b = make_float4(a.x * a.x, a.y * a.y, a.z * a.z, a.w * a.w);
   }
 };
@@ -122,7 +132,11 @@ struct RedBnBwdOp {
   const float* gamma;
   const float* beta;
   int relu;
-  __device__ Bn4 prep4(int c, int C) const { return bn_params4(stats, gamma, beta, c, C); }
+  using P = Bn4;
+  struct R {
+    float4 g, v;
+  };
+  __device__ P prep4(int c, int C) const { return bn_params4(stats, gamma, beta, c, C); }
   __device__ void eval(int64_t row, int c, int C, float& a, float& b) const {
     const float v = x[row * C + c];
     float g = dy[row * C + c];
@@ -130,9 +144,10 @@ struct RedBnBwdOp {
     a = g;
     b = g * bn_xhat(v, stats[c], stats[C + c]);
   }
-  __device__ void eval4(const Bn4& p, int64_t row, int c, int C, float4& a, float4& b) const {
-    float4 g = ld4(dy + row * C + c);
-    const float4 v = ld4(x + row * C + c);
+  __device__ R load(int64_t off) const { return R{ld4(dy + off), ld4(x + off)}; }
+  __device__ void comp(const P& p, const R& r, float4& a, float4& b) const {
+    float4 g = r.g;
+    const float4 v = r.v;
     if (relu) {
       const float4 y = bn_affine4(v, p);
       g = make_float4(y.x > 0.f ? g.x : 0.f, y.y > 0.f ? g.y : 0.f, y.z > 0.f ? g.z : 0.f, y.w > 0.f ? g.w : 0.f);
@@ -143,41 +158,46 @@ struct RedBnBwdOp {
   }
 };
 
-// float4 variant for C % 4 == 0: a thread owns 4 adjacent channels and walks
-// its rows with kUnroll independent accumulators (fixed per-thread order,
-// fixed merge), so kUnroll loads per operand are in flight.
+// Stage 1, float4 variant for C % 4 == 0: block b reduces rows [b*chunk,
+// (b+1)*chunk) into part[b][2][C] (doubles).  A thread owns 4 adjacent
+// channels and walks its rows with kUnroll independent accumulators (fixed
+// per-thread order, fixed merge).
+constexpr int kRedThreads = 512;
 template <class Op>
-__global__ void colred_stage1_v4(Op op, int64_t rows, int C, int64_t chunk, double* part) {
-  __shared__ float4 s1[kThreads], s2[kThreads];
+__global__ void __launch_bounds__(kRedThreads) colred_stage1_v4(Op op, int64_t rows, int C, int64_t chunk,
+                                                                double* part) {
+  __shared__ float4 s1[kRedThreads], s2[kRedThreads];
   const int64_t r0 = static_cast<int64_t>(blockIdx.x) * chunk;
   const int64_t r1 = r0 + chunk < rows ? r0 + chunk : rows;
   const int C4 = C / 4;
-  const int cb = C4 < kThreads ? C4 : kThreads;
-  const int lanes = kThreads / cb;
+  const int cb = C4 < kRedThreads ? C4 : kRedThreads;
+  const int lanes = kRedThreads / cb;
   const int t = threadIdx.x;
   const int lane = t / cb, cc = t % cb;
   for (int c0 = 0; c0 < C4; c0 += cb) {
     const int c4 = c0 + cc;
     float4 a = zero4(), b = a;
     if (lane < lanes && c4 < C4) {
-      const auto p = op.prep4(c4 * 4, C);
+      const typename Op::P p = op.prep4(c4 * 4, C);
       float4 au[kUnroll], bu[kUnroll];
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) au[u] = bu[u] = zero4();
       int64_t r = r0 + lane;
       for (; r + (kUnroll - 1) * lanes < r1; r += kUnroll * lanes) {
-        float4 fa[kUnroll], fb[kUnroll];
+        typename Op::R raw[kUnroll];
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) op.eval4(p, r + u * lanes, c4 * 4, C, fa[u], fb[u]);
+        for (int u = 0; u < kUnroll; ++u) raw[u] = op.load((r + u * lanes) * C + c4 * 4);
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
-          add4(au[u], fa[u]);
-          add4(bu[u], fb[u]);
+          float4 fa, fb;
+          op.comp(p, raw[u], fa, fb);
+          add4(au[u], fa);
+          add4(bu[u], fb);
         }
       }
       for (; r < r1; r += lanes) {
         float4 fa, fb;
-        op.eval4(p, r, c4 * 4, C, fa, fb);
+        op.comp(p, op.load(r * C + c4 * 4), fa, fb);
         add4(au[0], fa);
         add4(bu[0], fb);
       }
@@ -246,16 +266,34 @@ __global__ void colred_stage1(Op op, int64_t rows, int C, int64_t chunk, double*
   }
 }
 
-// 32 channels per block (lane = channel), 8 warps take interleaved stage-1
-// blocks, then warp sums are combined in warp order: fixed order, so the result
-// is deterministic.
-__global__ void colred_stage2(const double* part, int nblocks, int C, double* out) {
-  __shared__ double sa[8][32], sb[8][32];
+// Stage 2: 32 channels per block (lane = channel); the 32 warps take
+// interleaved stage-1 blocks (4 loads in flight per operand), then the warp
+// sums are combined in warp order -- a fixed order, so the result is
+// deterministic -- and handed to the finaliser (no extra launch).
+constexpr int kStage2Threads = 1024;
+template <class Fin>
+__global__ void __launch_bounds__(kStage2Threads) colred_stage2(const double* __restrict__ part, int nblocks, int C,
+                                                                Fin fin) {
+  __shared__ double sa[32][33], sb[32][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + lane;
   double A = 0.0, B = 0.0;
   if (c < C) {
-    for (int b = w; b < nblocks; b += 8) {
+    int b = w;
+    for (; b + 3 * 32 < nblocks; b += 4 * 32) {
+      double va[4], vb[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        va[u] = part[(static_cast<size_t>(b + 32 * u) * 2) * C + c];
+        vb[u] = part[(static_cast<size_t>(b + 32 * u) * 2 + 1) * C + c];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        A += va[u];
+        B += vb[u];
+      }
+    }
+    for (; b < nblocks; b += 32) {
       A += part[(static_cast<size_t>(b) * 2) * C + c];
       B += part[(static_cast<size_t>(b) * 2 + 1) * C + c];
     }
@@ -265,56 +303,76 @@ __global__ void colred_stage2(const double* part, int nblocks, int C, double* ou
   __syncthreads();
   if (w == 0 && c < C) {
     double a = 0.0, b = 0.0;
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < 32; ++i) {
       a += sa[i][lane];
       b += sb[i][lane];
     }
-    out[c] = a;
-    out[C + c] = b;
+    fin(c, a, b);
   }
 }
 
-// Runs both stages; result sums land in sums[0..2C) (doubles) inside scratch.
-template <class Op>
-cudaError_t colred(Op op, int64_t rows, int C, float* scratch_f, double** sums_out, cudaStream_t st) {
+// Blocks of stage 1: enough rows per thread (>= ~64 float4 per operand) that
+// the double partials stay small next to the input, at most kRedChunks.
+template <class Op, class Fin>
+cudaError_t colred(Op op, Fin fin, int64_t rows, int C, float* scratch_f, cudaStream_t st) {
   double* part = reinterpret_cast<double*>(scratch_f);
-  int64_t nb = rows < kRedChunks ? rows : kRedChunks;
+  const bool v4 = C % 4 == 0;
+  const int64_t per_block = v4 ? static_cast<int64_t>(kRedThreads) * 64 * 4 : static_cast<int64_t>(kThreads) * 64;
+  int64_t nb = (rows * C + per_block - 1) / per_block;
+  nb = nb < 148 ? 148 : (nb > kRedChunks ? kRedChunks : nb);
+  if (nb > rows) nb = rows;
   if (nb < 1) nb = 1;
   const int64_t chunk = (rows + nb - 1) / nb;
   nb = (rows + chunk - 1) / chunk;
   if (nb < 1) nb = 1;
-  if (C % 4 == 0)
-    colred_stage1_v4<<<static_cast<int>(nb), kThreads, 0, st>>>(op, rows, C, chunk, part);
+  if (v4)
+    colred_stage1_v4<<<static_cast<int>(nb), kRedThreads, 0, st>>>(op, rows, C, chunk, part);
   else
     colred_stage1<<<static_cast<int>(nb), kThreads, 0, st>>>(op, rows, C, chunk, part);
-  double* sums = part + static_cast<size_t>(kRedChunks) * 2 * C;
-  colred_stage2<<<(C + 31) / 32, 256, 0, st>>>(part, static_cast<int>(nb), C, sums);
-  *sums_out = sums;
+  colred_stage2<<<(C + 31) / 32, kStage2Threads, 0, st>>>(part, static_cast<int>(nb), C, fin);
   return cudaGetLastError();
 }
 
-__global__ void bias_finalize(const double* sums, int C, float* db) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c < C) db[c] = static_cast<float>(sums[c]);
-}
+struct BiasFin {
+  float* db;
+  __device__ void operator()(int c, double a, double) const { db[c] = static_cast<float>(a); }
+};
 
-__global__ void bn_stats_finalize(const double* sums, const float* x, int64_t rows, int C, float eps, float momentum,
-                                  float* stats, float* running) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= C) return;
-  const double n = static_cast<double>(rows);
-  const double m1 = sums[c] / n;
-  double var = sums[C + c] / n - m1 * m1;
-  if (var < 0.0) var = 0.0;
-  const double mean = static_cast<double>(x[c]) + m1;
-  stats[c] = static_cast<float>(mean);
-  stats[C + c] = static_cast<float>(1.0 / sqrt(var + static_cast<double>(eps)));
-  if (running) {
-    const double unbiased = rows > 1 ? var * n / (n - 1.0) : var;
-    running[c] = static_cast<float>((1.0 - momentum) * running[c] + momentum * mean);
-    running[C + c] = static_cast<float>((1.0 - momentum) * running[C + c] + momentum * unbiased);
+struct BnStatsFin {
+  const float* x;
+  int64_t rows;
+  int C;
+  float eps, momentum;
+  float* stats;
+  float* running;
+  __device__ void operator()(int c, double s1, double s2) const {
+    const double n = static_cast<double>(rows);
+    const double m1 = s1 / n;
+    double var = s2 / n - m1 * m1;
+    if (var < 0.0) var = 0.0;
+    const double mean = static_cast<double>(x[c]) + m1;
+    stats[c] = static_cast<float>(mean);
+    stats[C + c] = static_cast<float>(1.0 / sqrt(var + static_cast<double>(eps)));
+    if (running) {
+      const double unbiased = rows > 1 ? var * n / (n - 1.0) : var;
+      running[c] = static_cast<float>((1.0 - momentum) * running[c] + momentum * mean);
+      running[C + c] = static_cast<float>((1.0 - momentum) * running[C + c] + momentum * unbiased);
+    }
   }
-}
+};
+
+struct BnBwdFin {
+  int C;
+  float* dgamma;
+  float* dbeta;
+  float* coef;  // {sum g, sum g*xhat} as floats for the dx pass
+  __device__ void operator()(int c, double s1, double s2) const {
+    dbeta[c] = static_cast<float>(s1);
+    dgamma[c] = static_cast<float>(s2);
+    coef[c] = static_cast<float>(s1);
+    coef[C + c] = static_cast<float>(s2);
+  }
+};
 
 __global__ void bn_apply_scalar(const float* __restrict__ x, int64_t n, int C, const float* __restrict__ gamma,
                                 const float* __restrict__ beta, const float* __restrict__ stats, float* __restrict__ y) {
@@ -376,14 +434,6 @@ __global__ void grad_copy2_kernel(const float4* __restrict__ src, float4* d1, in
   }
 }
 
-__global__ void bn_bwd_finalize(const double* sums, int C, float* dgamma, float* dbeta, float* coef) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= C) return;
-  dbeta[c] = static_cast<float>(sums[c]);
-  dgamma[c] = static_cast<float>(sums[C + c]);
-  coef[c] = static_cast<float>(sums[c]);
-  coef[C + c] = static_cast<float>(sums[C + c]);
-}
 
 // dx (+)= gamma*invstd*(g - sum(g)/m - xhat*sum(g*xhat)/m), g = dy or the
 // ReLU-masked dy (relu: mask recomputed from x, see RedBnBwdOp).
@@ -893,26 +943,20 @@ __global__ void zero_kernel(float* p, int64_t n) {
 }  // namespace
 
 int64_t red_scratch_floats(int C) {
-  // kRedChunks*2*C partial doubles + 2*C sums + 2*C float coefficients
-  return (static_cast<int64_t>(kRedChunks) * 2 * C + 2 * C) * 2 + 2 * C + 64;
+  // kRedChunks*2*C partial doubles + 2*C float coefficients
+  return static_cast<int64_t>(kRedChunks) * 2 * C * 2 + 2 * C + 64;
 }
 
 cudaError_t bias_grad(const float* dy, int64_t rows, int C, float* db, float* red_scratch, cudaStream_t st) {
-  double* sums;
-  cudaError_t e = colred(RedBiasOp{dy}, rows, C, red_scratch, &sums, st);
-  if (e != cudaSuccess) return e;
-  bias_finalize<<<(C + 255) / 256, 256, 0, st>>>(sums, C, db);
-  return cudaGetLastError();
+  return colred(RedBiasOp{dy}, BiasFin{db}, rows, C, red_scratch, st);
 }
 
 cudaError_t bn_fwd(const float* x, int64_t rows, int C, const float* gamma, const float* beta, float* y, float* stats,
                    float* running, float eps, float momentum, int compute_stats, float* red_scratch, cudaStream_t st) {
   cudaError_t e;
   if (compute_stats) {
-    double* sums;
-    e = colred(RedBnStatsOp{x}, rows, C, red_scratch, &sums, st);
+    e = colred(RedBnStatsOp{x}, BnStatsFin{x, rows, C, eps, momentum, stats, running}, rows, C, red_scratch, st);
     if (e != cudaSuccess) return e;
-    bn_stats_finalize<<<(C + 255) / 256, 256, 0, st>>>(sums, x, rows, C, eps, momentum, stats, running);
   }
   if (!y) return cudaGetLastError();  // statistics only (apply fused downstream)
   const int64_t n = rows * C;
@@ -943,11 +987,10 @@ cudaError_t grad_copy2(const float* src, float* d1, int acc1, float* d2, int acc
 cudaError_t bn_bwd(const float* x, const float* dy, int64_t rows, int C, const float* gamma, const float* beta,
                    const float* stats, int relu, float* dx, int accumulate, float* dgamma, float* dbeta,
                    float* red_scratch, cudaStream_t st) {
-  double* sums;
-  cudaError_t e = colred(RedBnBwdOp{x, dy, stats, gamma, beta, relu}, rows, C, red_scratch, &sums, st);
+  float* coef = red_scratch + static_cast<int64_t>(kRedChunks) * 2 * C * 2;  // past the partials
+  cudaError_t e = colred(RedBnBwdOp{x, dy, stats, gamma, beta, relu}, BnBwdFin{C, dgamma, dbeta, coef}, rows, C,
+                         red_scratch, st);
   if (e != cudaSuccess) return e;
-  float* coef = reinterpret_cast<float*>(sums + 2 * C);
-  bn_bwd_finalize<<<(C + 255) / 256, 256, 0, st>>>(sums, C, dgamma, dbeta, coef);
   const int64_t n = rows * C;
   if (dx) {
     if (C % 4 == 0)
