@@ -66,6 +66,7 @@ struct LayerRt {
   sn::ConvShape conv{};
   sn::PoolShape pool{};
   int fc_in = 0, fc_splits = 1, wgrad_splits = 1;
+  int stats_tiles = 0, stats_rows = 0;  // CONV: BN statistics tiles its forward can emit
 };
 
 struct Action {
@@ -107,6 +108,7 @@ struct sn_exec {
   float* partial = nullptr;
   int64_t partial_cap = 0;
   float* red = nullptr;
+  float* tstats = nullptr;  // per-tile BN statistics from a CONV forward to the BN right after it
   void* pool_scratch = nullptr;
   const float** ptr_table = nullptr;
   std::vector<const float*> ptr_host;
@@ -273,6 +275,14 @@ void alloc_device(sn_exec* ex) {
     partial = std::max(partial, sn::stem_wgrad_partial_floats(ex->L[ex->stem_layer].conv));
     wt = std::max(wt, sn::stem_weight_floats(ex->L[ex->stem_layer].conv));
   }
+  int64_t tstats = 64;
+  for (int i = 0; i < net.n; ++i) {
+    LayerRt& l = ex->L[i];
+    if (l.kind != snp::CONV) continue;
+    l.stats_tiles = sn::conv_fwd_stats_tiles(l.conv, i == ex->stem_layer, &l.stats_rows);
+    tstats = std::max(tstats, static_cast<int64_t>(l.stats_tiles) * 3 * l.C);
+  }
+  ck(cudaMalloc(&ex->tstats, tstats * sizeof(float)), "cudaMalloc(tile stats)");
   ex->partial_cap = std::max<int64_t>(partial, 64);
   ck(cudaMalloc(&ex->partial, ex->partial_cap * sizeof(float)), "cudaMalloc(partial)");
   ck(cudaMalloc(&ex->wt_scratch, std::max<int64_t>(wt, 64) * sizeof(float)), "cudaMalloc(wt)");
@@ -440,12 +450,13 @@ struct Compiler {
         const float* w = ex->params + l.w_off;
         const float* b = ex->params + l.b_off;
         const sn::ConvShape cs = l.conv;
+        float* ts = conv_stats_now ? ex->tstats : nullptr;
         if (lid == ex->stem_layer) {
           float* wp = ex->wt_scratch;
-          push([=] { ck(sn::conv_stem_fwd(cs, x, w, wp, b, y, st), "conv_stem_fwd"); }, 2);
+          push([=] { ck(sn::conv_stem_fwd(cs, x, w, wp, b, y, ts, st), "conv_stem_fwd"); }, 2);
           break;
         }
-        push([=] { ck(sn::conv_fwd(cs, x, w, b, y, st), "conv_fwd"); }, 1);
+        push([=] { ck(sn::conv_fwd(cs, x, w, b, y, st, ts), "conv_fwd"); }, 1);
         break;
       }
       case snp::FC: {
@@ -466,6 +477,17 @@ struct Compiler {
         const float eps = l.num.bn_eps, mom = l.num.bn_momentum;
         const int compute = replay ? 0 : 1;
         float* red = ex->red;
+        if (bn_tiles_now && !replay) {
+          // statistics from the producing CONV's epilogue tiles
+          const float* ts = ex->tstats;
+          const int nt = ex->L[net.prev[lid][0]].stats_tiles, tr = ex->L[net.prev[lid][0]].stats_rows;
+          push([=] {
+            ck(sn::bn_stats_from_tiles(ts, nt, tr, x, rows, C, stats, running, eps, mom, red, st), "bn_tile_stats");
+          }, 2);
+          if (!fuse_next)
+            push([=] { ck(sn::bn_fwd(x, rows, C, g, b, y, stats, nullptr, eps, mom, 0, red, st), "bn_apply"); }, 1);
+          break;
+        }
         if (fuse_next) {
           // apply deferred to the consuming ReLU (bn_apply_relu); statistics now
           if (!replay)
@@ -478,6 +500,7 @@ struct Compiler {
         break;
       }
       case snp::ACT:
+        if (fused_bn >= 0 && join_fuse_at[cur_ti] >= 0) break;  // launched at the JOIN (bn_apply_relu_join)
         if (fused_bn >= 0) {
           const LayerRt& bl = ex->L[fused_bn];
           const float* bx = ptr(snp::K_ACT, net.prev[fused_bn][0]);
@@ -523,6 +546,24 @@ struct Compiler {
         break;
       }
       case snp::JOIN: {
+        if (join_from[cur_ti] >= 0) {
+          // BN apply + ReLU + JOIN in one pass (peephole, see plan_fusions)
+          const int ra = P.tape[join_from[cur_ti]].b;
+          const int bn = net.prev[ra][0];
+          const LayerRt& bl = ex->L[bn];
+          const float* bx = ptr(snp::K_ACT, net.prev[bn][0]);
+          float* by = elide_out[bn] ? nullptr : ptr(snp::K_ACT, bn);
+          float* ry = elide_out[ra] ? nullptr : ptr(snp::K_ACT, ra);
+          const int other = net.prev[lid][0] == ra ? net.prev[lid][1] : net.prev[lid][0];
+          const float* oth = ptr(snp::K_ACT, other);
+          const float* g = ex->params + bl.w_off;
+          const float* b = ex->params + bl.b_off;
+          const float* stats = ex->state + bl.state_off;
+          const int64_t rows = static_cast<int64_t>(ex->B) * bl.H * bl.W;
+          const int C = bl.C;
+          push([=] { ck(sn::bn_apply_relu(bx, rows, C, g, b, stats, by, ry, st, oth, y), "bn_apply_relu_join"); }, 1);
+          break;
+        }
         const size_t at = ex->ptr_host.size();
         for (int p : net.prev[lid]) ex->ptr_host.push_back(ptr(snp::K_ACT, p));
         const int nin = static_cast<int>(net.prev[lid].size());
@@ -567,14 +608,18 @@ struct Compiler {
         float* part = ex->partial;
         float* red = ex->red;
         const int sp = l.wgrad_splits;
+        if (conv_bias_done[lid]) db = nullptr;  // summed by the BN backward's dx pass
+        const int nbias = db ? 2 : 0;
         if (lid == ex->stem_layer) {  // DATA has no gradient
-          push([=] { ck(sn::conv_stem_wgrad(cs, x, dy, part, wt, dw, db, red, st), "conv_stem_wgrad"); }, 5);
+          push([=] { ck(sn::conv_stem_wgrad(cs, x, dy, part, wt, dw, db, red, st), "conv_stem_wgrad"); },
+               3 + nbias);
           break;
         }
+        const int ndgrad = !dx ? 0 : (cs.stride > 1 ? 2 * cs.stride * cs.stride : 2);
         push([=] {
           ck(sn::conv_wgrad(cs, x, dy, dw, db, part, sp, red, st), "conv_wgrad");
           if (dx) ck(sn::conv_dgrad(cs, dy, w, wt, dx, acc, st), "conv_dgrad");
-        }, dx ? 7 : 5);
+        }, 2 + nbias + ndgrad);
         break;
       }
       case snp::FC: {
@@ -606,8 +651,13 @@ struct Compiler {
         const int C = l.C;
         float* red = ex->red;
         const int relu = bwd_relu ? 1 : 0;
-        push([=] { ck(sn::bn_bwd(x, dy, rows, C, g, beta, stats, relu, dx, acc, dg, dbt, red, st), "bn_bwd"); },
-             dx ? 4 : 3);
+        float* dcb = nullptr;
+        if (bn_bias_now && dx) {
+          dcb = ex->grads + ex->L[pid].b_off;
+          conv_bias_done[pid] = 1;
+        }
+        push([=] { ck(sn::bn_bwd(x, dy, rows, C, g, beta, stats, relu, dx, acc, dg, dbt, red, st, dcb), "bn_bwd"); },
+             dx ? (dcb ? 4 : 3) : 2);
         break;
       }
       case snp::ACT: {
@@ -634,7 +684,7 @@ struct Compiler {
         float* dx = dx_target(pid, &acc);
         const sn::PoolShape ps = l.pool;
         void* scratch = ex->pool_scratch;
-        const int nk = (ps.C % 4 == 0 && ps.mode == 0) ? 2 : 1;
+        const int nk = sn::pool_bwd_kernels(ps);
         if (dx) push([=] { ck(sn::pool_bwd(ps, x, y, dy, dx, acc, scratch, st), "pool_bwd"); }, nk);
         break;
       }
@@ -696,6 +746,20 @@ struct Compiler {
   // pair is fused as well, nothing reads the BN output, so it is not written.
   bool fuse_next = false;
   int fused_bn = -1;
+  size_t cur_ti = 0;
+  // BN+ReLU (fused) forward / replay whose next compute action is the same op
+  // of a 2-input JOIN reading the ReLU: the whole chain runs at the JOIN.
+  std::vector<int> join_fuse_at, join_from;
+  // CONV forward -> BN forward (next compute action, reading that output): the
+  // CONV epilogue emits per-tile statistics, the BN only combines them.
+  bool conv_stats_now = false, bn_tiles_now = false;
+  std::vector<char> conv_stats_at, bn_tiles_at;
+  // BN backward whose input is a CONV output consumed only by this BN: the dx
+  // pass also sums the CONV's bias gradient (the CONV's gradient buffer gets
+  // nothing else; replays in between do not touch it).
+  bool bn_bias_now = false;
+  std::vector<char> bn_bias_at;
+  std::vector<char> conv_bias_done;
   bool bwd_skip = false, bwd_relu = false;
   std::vector<char> fuse_at, act_bwd_skip, bn_bwd_relu;
   std::vector<int> fused_into;
@@ -713,10 +777,43 @@ struct Compiler {
     act_bwd_skip.assign(T, 0);
     bn_bwd_relu.assign(T, 0);
     elide_out.assign(net.n, 0);
+    conv_stats_at.assign(T, 0);
+    bn_tiles_at.assign(T, 0);
+    join_fuse_at.assign(T, -1);
+    join_from.assign(T, -1);
+    bn_bias_at.assign(T, 0);
+    conv_bias_done.assign(net.n, 0);
     const char* env = std::getenv("SN_FUSE");  // SN_FUSE=0: one kernel per layer (A/B and bitwise tests)
     if (env && env[0] == '0') {
       ex->elided = elide_out;
       return;
+    }
+    // SN_FUSE_REASSOC=0: keep the fusions that reorder floating-point sums off
+    // (CONV-epilogue BN statistics, BN-backward CONV bias gradient), so the
+    // remaining fusions can be checked bit-exactly against SN_FUSE=0
+    const char* env_ra = std::getenv("SN_FUSE_REASSOC");
+    const bool reassoc = !(env_ra && env_ra[0] == '0');
+    if (reassoc) {
+      for (size_t i = 0; i < T; ++i) {
+        const snp::Event& e = P.tape[i];
+        if (e.op != 'C' || net.kind[e.b] != snp::CONV || ex->L[e.b].stats_tiles <= 0) continue;
+        for (size_t j = i + 1; j < T; ++j) {
+          const snp::Event& f = P.tape[j];
+          if (!is_compute(f.op)) continue;
+          if (f.op == 'C' && net.kind[f.b] == snp::BN && net.prev[f.b].size() == 1 && net.prev[f.b][0] == e.b) {
+            conv_stats_at[i] = 1;
+            bn_tiles_at[j] = 1;
+          }
+          break;
+        }
+      }
+    }
+    for (size_t i = 0; i < T && reassoc; ++i) {
+      const snp::Event& e = P.tape[i];
+      if (e.op != 'B' || net.kind[e.b] != snp::BN || net.prev[e.b].size() != 1) continue;
+      const int cv = net.prev[e.b][0];
+      if (net.kind[cv] != snp::CONV || net.next[cv].size() != 1 || !sn::bn_bwd_bias_ok(ex->L[e.b].C)) continue;
+      bn_bias_at[i] = 1;
     }
     for (size_t i = 0; i < T; ++i) {
       const snp::Event& e = P.tape[i];
@@ -765,6 +862,35 @@ struct Compiler {
       const int bn = net.prev[a][0];
       if (act_fwd[a] == act_fwd_fused[a] && bn_fwd[bn] == bn_fwd_fused[bn]) elide_out[bn] = 1;
     }
+    // ReLU -> JOIN: every event between the two may allocate (the JOIN output)
+    // or touch unrelated tensors, but must not free / copy the BN input, the
+    // BN output or the ReLU output (they are read or written at the JOIN).
+    std::vector<int> act_join_fused(net.n, 0);
+    for (size_t i = 0; i < T; ++i) {
+      if (fused_into[i] < 0) continue;
+      const snp::Event& e = P.tape[i];
+      const int ra = e.b, bn = fused_into[i], bin = net.prev[bn][0];
+      for (size_t j = i + 1; j < T; ++j) {
+        const snp::Event& f = P.tape[j];
+        if (f.op == 'F' || f.op == 'O' || f.op == 'P' || f.op == 'D') {
+          if (f.b == ra || f.b == bn || f.b == bin) break;
+          continue;
+        }
+        if (!is_compute(f.op)) continue;
+        const auto& pv = net.prev[f.b];
+        if (f.op == e.op && net.kind[f.b] == snp::JOIN && pv.size() == 2 && (pv[0] == ra) != (pv[1] == ra) &&
+            ex->L[f.b].C % 4 == 0) {
+          join_fuse_at[i] = static_cast<int>(j);
+          join_from[j] = static_cast<int>(i);
+          ++act_join_fused[ra];
+        }
+        break;
+      }
+    }
+    for (int a = 0; a < net.n; ++a) {
+      if (!bn_relu_pair(a) || !act_bwd_fused[a] || net.next[a].size() != 1) continue;
+      if (act_fwd[a] == act_join_fused[a]) elide_out[a] = 1;  // read only by the fused chains
+    }
     ex->elided = elide_out;
   }
 
@@ -792,8 +918,12 @@ struct Compiler {
     prepare_inputs();
     for (size_t ti = 0; ti < P.tape.size(); ++ti) {
       const snp::Event& ev = P.tape[ti];
+      cur_ti = ti;
       fuse_next = fuse_at[ti] != 0;
       fused_bn = fused_into[ti];
+      conv_stats_now = conv_stats_at[ti] != 0;
+      bn_tiles_now = bn_tiles_at[ti] != 0;
+      bn_bias_now = bn_bias_at[ti] != 0;
       bwd_skip = act_bwd_skip[ti] != 0;
       bwd_relu = bn_bwd_relu[ti] != 0;
       switch (ev.op) {
@@ -888,7 +1018,7 @@ void destroy(sn_exec* ex) {
     if (kv.second) cudaFreeHost(kv.second);
   if (ex->data_buf && ex->data_buf != ex->images) cudaFree(ex->data_buf);
   void* bufs[] = {ex->arena, ex->params, ex->grads, ex->state, ex->images, ex->labels, ex->loss_rows, ex->loss,
-                  ex->iteration, ex->wt_scratch, ex->partial, ex->red, ex->pool_scratch,
+                  ex->iteration, ex->wt_scratch, ex->partial, ex->red, ex->tstats, ex->pool_scratch,
                   const_cast<float**>(ex->ptr_table)};
   for (void* b : bufs)
     if (b) cudaFree(b);

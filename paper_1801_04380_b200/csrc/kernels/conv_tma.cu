@@ -67,7 +67,8 @@ struct TmaSmem {
   static constexpr int B_BYTES = BN * 128;
   static constexpr int EPI_OFF = STAGES * (A_BYTES + B_BYTES);   // 2 x 16 KB store staging
   static constexpr int BAR_OFF = EPI_OFF + 2 * kBM * 128;
-  static constexpr int TOTAL = BAR_OFF + 512 + 1024;
+  static constexpr int STATS_OFF = BAR_OFF + 512;  // [4 warps][32 columns][2] floats
+  static constexpr int TOTAL = STATS_OFF + 1024 + 1024;
 };
 
 // Epilogue: TMEM -> registers (+bias) -> SWIZZLE_128B smem chunk of 128 x 32
@@ -84,6 +85,10 @@ struct EpiArgs {
   float* scatter;     // null: TMA store path
   int M, Uhw, Uw, t0, v0, st, ph, pw, pad, H, W;
   FastDivT fUhw, fUw;
+  // BatchNorm statistics of the output (forward; the consumer is a BN):
+  // per M tile and column, {shift = tile row 0, sum(y - shift), sum((y - shift)^2)}
+  // over the tile's valid rows, into stats[tile][3][N] (see bn_stats_from_tiles).
+  float* stats;
 };
 
 struct TileGrid {
@@ -360,6 +365,35 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
               tma_store_2d(&tmD, buf, n0 + c, m0, e.reduce != 0);
             bulk_commit();
           }
+          if (e.stats) {
+            // column `lane` of the staged 128 x 32 chunk, rows 32*warp.. of this warp
+            const int nv = MODE == 2 ? a.Q : min(kBM, e.M - m0);
+            const uint8_t* sb = smem + L::EPI_OFF + (chunk_no & 1u) * (kBM * 128);
+            const uint32_t cq = static_cast<uint32_t>(lane) >> 2, cr = (static_cast<uint32_t>(lane) & 3u) * 4;
+            const float shift = *reinterpret_cast<const float*>(sb + sw128_off(0, cq) + cr);
+            float s1 = 0.f, s2 = 0.f;
+            const int r1 = min(nv, 32 * (warp + 1));
+            for (int r = 32 * warp; r < r1; ++r) {
+              const float d = *reinterpret_cast<const float*>(sb + sw128_off(r, cq) + cr) - shift;
+              s1 += d;
+              s2 = fmaf(d, d, s2);
+            }
+            float* sred = reinterpret_cast<float*>(smem + L::STATS_OFF);
+            sred[(warp * 32 + lane) * 2] = s1;
+            sred[(warp * 32 + lane) * 2 + 1] = s2;
+            named_bar(1, 128);
+            if (warp == 0 && n0 + c + lane < e.N) {
+              float t1 = sred[lane * 2], t2 = sred[lane * 2 + 1];
+              for (int w = 1; w < 4; ++w) {
+                t1 += sred[(w * 32 + lane) * 2];
+                t2 += sred[(w * 32 + lane) * 2 + 1];
+              }
+              float* out = e.stats + static_cast<size_t>(m0 / kBM) * 3 * e.N + n0 + c + lane;
+              out[0] = shift;
+              out[e.N] = t1;
+              out[2 * static_cast<size_t>(e.N)] = t2;
+            }
+          }
         }
       }
       tc_fence_before();
@@ -481,6 +515,16 @@ int bn_for(int n) { return n <= 64 ? 64 : (n <= 128 ? 128 : 256); }
 
 bool conv_tma_ok_fwd(const ConvShape& s) { return s.C % 32 == 0 && load_encoders(); }
 
+int conv_fwd_stats_tiles(const ConvShape& s, bool stem, int* tile_rows) {
+  if (stem) {
+    *tile_rows = s.Q;
+    return s.N * s.P;
+  }
+  if (!use_tma() || !conv_tma_ok_fwd(s)) return 0;
+  *tile_rows = kBM;
+  return (s.N * s.P * s.Q + kBM - 1) / kBM;
+}
+
 // Probe: does the driver accept a tiled map whose row stride (32 B) is smaller
 // than its inner extent (128 B), i.e. overlapping sliding windows?
 int tma_probe_overlap(const float* base) {
@@ -500,7 +544,7 @@ bool conv_tma_ok_dgrad(const ConvShape& s) {
 bool conv_tma_ok_wgrad(const ConvShape& s) { return s.C % 32 == 0 && s.K % 32 == 0 && load_encoders(); }
 
 cudaError_t conv_fwd_tma(const ConvShape& s, const float* x, const float* w, const float* bias, float* y,
-                         cudaStream_t st) {
+                         float* stats, cudaStream_t st) {
   const int BN = bn_for(s.K);
   CUtensorMap A, B;
   if (!make_im2col(&A, x, s.N, s.H, s.W, s.C, -s.pad, -s.pad, s.pad - (s.R - 1), s.pad - (s.S - 1), s.stride, kBM,
@@ -525,7 +569,9 @@ cudaError_t conv_fwd_tma(const ConvShape& s, const float* x, const float* w, con
   const int M = s.N * s.P * s.Q;
   CUtensorMap D;
   if (!make_store(&D, y, M, s.K, 0)) return cudaErrorInvalidValue;
-  const EpiArgs e{bias, s.K, 0, 0};
+  EpiArgs e{bias, s.K, 0, 0};
+  e.M = M;
+  e.stats = stats;
   switch (BN) {
     case 64: return launch<64, 0>(A, B, D, a, e, M, s.K, 1, st);
     case 128: return launch<128, 0>(A, B, D, a, e, M, s.K, 1, st);
@@ -696,7 +742,7 @@ cudaError_t stem_pad_input(const ConvShape& s, int H_raw, int W_raw, int C_raw, 
 }
 
 cudaError_t conv_stem_fwd(const ConvShape& s, const float* xp, const float* w, float* wp_scratch, const float* bias,
-                          float* y, cudaStream_t st) {
+                          float* y, float* stats, cudaStream_t st) {
   const StemGeom g = stem_geom(s);
   const int Sp = g.sblocks * 8;
   stem_weights_kernel<<<148, 256, 0, st>>>(const_cast<float*>(w), wp_scratch, s.K, s.R, s.S, Sp, 1);
@@ -716,7 +762,9 @@ cudaError_t conv_stem_fwd(const ConvShape& s, const float* xp, const float* w, f
   a.shift = g.shift;
   a.fsb = FastDivT(g.sblocks);
   a.fP = FastDivT(s.P);
-  const EpiArgs e{bias, s.K, 0, 0};
+  a.Q = s.Q;
+  EpiArgs e{bias, s.K, 0, 0};
+  e.stats = stats;
   const int M = s.N * s.P * kBM;  // one 128-row tile per output row
   switch (BN) {
     case 64: return launch<64, 2>(A, B, D, a, e, M, s.K, 1, st);
@@ -778,6 +826,7 @@ cudaError_t conv_stem_wgrad(const ConvShape& s, const float* xp, const float* dy
   stem_weights_kernel<<<148, 256, 0, st>>>(dw, wp_scratch, s.K, s.R, s.S, Sp, 0);
   err = cudaGetLastError();
   if (err != cudaSuccess) return err;
+  if (!db) return cudaSuccess;  // bias gradient fused into the consuming BN's backward
   return bias_grad(dy, static_cast<int64_t>(s.N) * s.P * s.Q, s.K, db, red, st);
 }
 

@@ -413,8 +413,9 @@ bool use_tma() {
 void set_conv_tma(int on) { g_use_tma = on ? 1 : 0; }
 
 cudaError_t conv_fwd(const ConvShape& s, const float* x, const float* w, const float* bias, float* y,
-                     cudaStream_t st) {
-  if (use_tma() && conv_tma_ok_fwd(s)) return conv_fwd_tma(s, x, w, bias, y, st);
+                     cudaStream_t st, float* stats) {
+  if (use_tma() && conv_tma_ok_fwd(s)) return conv_fwd_tma(s, x, w, bias, y, stats, st);
+  if (stats) return cudaErrorInvalidValue;  // only the TMA kernels emit BN tile statistics
   switch (bn_for(s.K)) {
     case 64: return conv_fwd_bn<64>(s, x, w, bias, y, st);
     case 128: return conv_fwd_bn<128>(s, x, w, bias, y, st);
@@ -470,6 +471,7 @@ cudaError_t conv_wgrad(const ConvShape& s, const float* x, const float* dy, floa
   const int RSC = s.R * s.S * s.C;
   e = splitk_reduce_impl(partial, splits, RSC, s.K, dw, nullptr, 0, 1, st);
   if (e != cudaSuccess) return e;
+  if (!db) return cudaSuccess;  // bias gradient fused into the consuming BN's backward
   return bias_grad(dy, static_cast<int64_t>(s.N) * s.P * s.Q, s.K, db, red_scratch, st);
 }
 

@@ -92,7 +92,7 @@ extern "C" int sn_test_stem(const int* shape, int c_raw, void** p, long long* si
   }
   cudaError_t e = sn::stem_pad_input(s, s.H, s.W, c_raw, s.pad, (const float*)p[0], (float*)p[1], 0);
   if (e == cudaSuccess)
-    e = sn::conv_stem_fwd(s, (const float*)p[1], (const float*)p[2], (float*)p[3], (const float*)p[4], (float*)p[5], 0);
+    e = sn::conv_stem_fwd(s, (const float*)p[1], (const float*)p[2], (float*)p[3], (const float*)p[4], (float*)p[5], nullptr, 0);
   if (e == cudaSuccess)
     e = sn::conv_stem_wgrad(s, (const float*)p[1], (const float*)p[6], (float*)p[9], (float*)p[3], (float*)p[7],
                             (float*)p[8], (float*)p[10], 0);
@@ -115,3 +115,20 @@ extern "C" int sn_test_tma_overlap(const float* base) { return sn::tma_probe_ove
 
 // 1: TMA-fed conv kernels where the shape allows (default), 0: cp.async gathers.
 extern "C" void sn_test_set_conv_tma(int on) { sn::set_conv_tma(on); }
+
+// Pool layer kernels on caller buffers.  shape = {N,H,W,C,P,Q,K,stride,pad,mode}.
+//   op 0 forward:  p = {x, y}
+//   op 1 backward: p = {x, y, dy, dx, scratch}, flag = accumulate
+//   op 2 query:    returns pool_scratch_bytes (bytes) / 2^0 units, clipped to int
+extern "C" long long sn_test_pool(int op, const int* shape, void** p, int flag) {
+  sn::PoolShape s{shape[0], shape[1], shape[2], shape[3], shape[4], shape[5], shape[6], shape[7], shape[8], shape[9]};
+  if (op == 2) return sn::pool_scratch_bytes(s);
+  if (op == 3) return sn::pool_bwd_kernels(s);
+  cudaError_t e;
+  if (op == 0)
+    e = sn::pool_fwd(s, (const float*)p[0], (float*)p[1], 0);
+  else
+    e = sn::pool_bwd(s, (const float*)p[0], (const float*)p[1], (const float*)p[2], (float*)p[3], flag, p[4], 0);
+  if (e != cudaSuccess) return 4;
+  return cudaDeviceSynchronize() == cudaSuccess ? 0 : 4;
+}

@@ -14,13 +14,18 @@ struct ConvShape {
 };
 
 // ---- tensor-core GEMM based ops (gemm_ops.cu) --------------------------------
-// y[N*P*Q][K] = conv(x, w[K][R][S][C]) + bias
+// y[N*P*Q][K] = conv(x, w[K][R][S][C]) + bias.  stats (optional): BatchNorm
+// statistics of y per M tile, [tiles][3][K] floats (conv_fwd_stats_tiles), for
+// a BN consuming y (bn_stats_from_tiles) -- saves that BN's statistics pass.
 cudaError_t conv_fwd(const ConvShape& s, const float* x, const float* w, const float* bias, float* y,
-                     cudaStream_t st);
+                     cudaStream_t st, float* stats = nullptr);
+// Number of statistics tiles the forward (stem: conv_stem_fwd) emits, 0 if it
+// cannot; *tile_rows = output rows per tile (the last tile may hold fewer).
+int conv_fwd_stats_tiles(const ConvShape& s, bool stem, int* tile_rows);
 // dx[N*H*W][C] (+)= conv_transpose(dy, w); wt = scratch of K*R*S*C floats.
 cudaError_t conv_dgrad(const ConvShape& s, const float* dy, const float* w, float* wt, float* dx,
                        int accumulate, cudaStream_t st);
-// dw[K][R*S*C] = sum_pixels im2col(x)^T dy ; db[K] = column sums of dy.
+// dw[K][R*S*C] = sum_pixels im2col(x)^T dy ; db[K] = column sums of dy (skipped if db is null).
 // partial: scratch of splits*R*S*C*K floats (see conv_wgrad_splits).
 int conv_wgrad_splits(const ConvShape& s, int64_t partial_floats_cap);
 cudaError_t conv_wgrad(const ConvShape& s, const float* x, const float* dy, float* dw, float* db,
@@ -32,7 +37,7 @@ bool conv_tma_ok_fwd(const ConvShape& s);
 bool conv_tma_ok_dgrad(const ConvShape& s);
 bool conv_tma_ok_wgrad(const ConvShape& s);
 cudaError_t conv_fwd_tma(const ConvShape& s, const float* x, const float* w, const float* bias, float* y,
-                         cudaStream_t st);
+                         float* stats, cudaStream_t st);
 cudaError_t conv_dgrad_tma(const ConvShape& s, const float* dy, const float* wt_flip, float* dx, int accumulate,
                            cudaStream_t st);
 cudaError_t conv_wgrad_tma(const ConvShape& s, const float* x, const float* dy, float* partial, int splits,
@@ -49,7 +54,7 @@ int64_t stem_wgrad_partial_floats(const ConvShape& s);
 cudaError_t stem_pad_input(const ConvShape& s, int H_raw, int W_raw, int C_raw, int pad, const float* raw, float* xp,
                            cudaStream_t st);
 cudaError_t conv_stem_fwd(const ConvShape& s, const float* xp, const float* w, float* wp_scratch, const float* bias,
-                          float* y, cudaStream_t st);
+                          float* y, float* stats, cudaStream_t st);
 cudaError_t conv_stem_wgrad(const ConvShape& s, const float* xp, const float* dy, float* partial, float* wp_scratch,
                             float* dw, float* db, float* red, cudaStream_t st);
 // Channel-pad raw NHWC images (C_raw -> Cs) for the generic path.
@@ -83,17 +88,29 @@ cudaError_t bias_grad(const float* dy, int64_t rows, int C, float* db, float* re
 cudaError_t bn_fwd(const float* x, int64_t rows, int C, const float* gamma, const float* beta, float* y,
                    float* stats, float* running, float eps, float momentum, int compute_stats,
                    float* red_scratch, cudaStream_t st);
+// Statistics from the producing convolution's per-tile partials
+// ({shift, sum(y - shift), sum((y - shift)^2)} per tile and channel, tile t
+// holding min(tile_rows, rows - t*tile_rows) rows); x = the BN input (row 0
+// is the global shift).  Same outputs as bn_fwd(compute_stats=1, y=null).
+cudaError_t bn_stats_from_tiles(const float* tiles, int ntiles, int tile_rows, const float* x, int64_t rows, int C,
+                                float* stats, float* running, float eps, float momentum, float* red_scratch,
+                                cudaStream_t st);
 // relu = 1 fuses the backward of the ReLU consuming this BN: dy is then the
 // gradient w.r.t. the ReLU output and the mask bn(x) > 0 is recomputed from x
 // (bit-identical to the forward's, see bn_affine in layers.cu).
+// dbias (optional; dx not null, bn_bwd_bias_ok(C)): the column sums of this
+// call's dx contribution -- the bias gradient of the CONV whose output only
+// this BN consumes -- computed in the dx pass (saves that CONV's bias pass).
+bool bn_bwd_bias_ok(int C);
 cudaError_t bn_bwd(const float* x, const float* dy, int64_t rows, int C, const float* gamma, const float* beta,
                    const float* stats, int relu, float* dx, int accumulate, float* dgamma, float* dbeta,
-                   float* red_scratch, cudaStream_t st);
+                   float* red_scratch, cudaStream_t st, float* dbias = nullptr);
 
-// Fused BN apply + ReLU (C % 4 == 0): y = bn(x) (skipped when y is null),
-// y_relu = max(bn(x), 0).
+// Fused BN apply + ReLU (+ 2-input JOIN) (C % 4 == 0): y = bn(x), y_relu =
+// max(bn(x), 0), y_join = y_relu + join_other; null outputs are not written.
 cudaError_t bn_apply_relu(const float* x, int64_t rows, int C, const float* gamma, const float* beta,
-                          const float* stats, float* y, float* y_relu, cudaStream_t st);
+                          const float* stats, float* y, float* y_relu, cudaStream_t st,
+                          const float* join_other = nullptr, float* y_join = nullptr);
 // JOIN backward into two gradient buffers with one read of dy (n % 4 == 0).
 cudaError_t grad_copy2(const float* src, float* d1, int acc1, float* d2, int acc2, int64_t n, cudaStream_t st);
 
@@ -108,6 +125,7 @@ cudaError_t pool_fwd(const PoolShape& s, const float* x, float* y, cudaStream_t 
 // reference's backward reads) into a byte per output (executor scratch of
 // pool_scratch_bytes), then gathers; avg-pool gathers directly.
 int64_t pool_scratch_bytes(const PoolShape& s);
+int pool_bwd_kernels(const PoolShape& s);  // launches one pool_bwd issues
 cudaError_t pool_bwd(const PoolShape& s, const float* x, const float* y, const float* dy, float* dx,
                      int accumulate, void* scratch, cudaStream_t st);
 

@@ -385,23 +385,35 @@ __global__ void bn_apply_scalar(const float* __restrict__ x, int64_t n, int C, c
 
 // BN apply (C % 4 == 0), optionally fused with the ReLU that consumes it:
 // y = bn(x) (skipped when null), yr = relu(y) (skipped when null).
+// y = bn(x), yr = relu(y), yj = relu(y) + add (the 2-input JOIN fed by the
+// ReLU; a + b == b + a in IEEE arithmetic, so the JOIN's input order does not
+// matter).  Null outputs are skipped.
 __global__ void bn_apply_v4(const float4* __restrict__ x, int64_t n4, int C, const float* __restrict__ gamma,
                             const float* __restrict__ beta, const float* __restrict__ stats, float4* __restrict__ y,
-                            float4* __restrict__ yr) {
+                            float4* __restrict__ yr, const float4* __restrict__ add, float4* __restrict__ yj) {
   const ChanLoop L = chan_loop(C / 4);
   if (!L.active) return;
   const Bn4 p = bn_params4(stats, gamma, beta, L.c, C);
   for (int64_t i0 = L.start; i0 < n4; i0 += kUnroll * L.S) {
-    float4 v[kUnroll];
+    float4 v[kUnroll], w[kUnroll];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) v[u] = i0 + u * L.S < n4 ? x[i0 + u * L.S] : zero4();
+    for (int u = 0; u < kUnroll; ++u) {
+      v[u] = i0 + u * L.S < n4 ? x[i0 + u * L.S] : zero4();
+      w[u] = (yj && i0 + u * L.S < n4) ? add[i0 + u * L.S] : zero4();
+    }
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       const int64_t i = i0 + u * L.S;
       if (i < n4) {
         const float4 o = bn_affine4(v[u], p);
         if (y) y[i] = o;
-        if (yr) yr[i] = relu4(o);
+        const float4 r = relu4(o);
+        if (yr) yr[i] = r;
+        if (yj) {
+          float4 j = r;
+          add4(j, w[u]);
+          yj[i] = j;
+        }
       }
     }
   }
@@ -453,12 +465,47 @@ __global__ void bn_dx_scalar(const float* __restrict__ x, const float* __restric
   }
 }
 
+// Block-level combination of per-thread channel-quad sums (threads t and
+// t + C/4 share a quad; 256 % (C/4) == 0) in thread order, into
+// part[blockIdx.x][0][C] (doubles) and a zero second plane.
+__device__ void bias_block_reduce(const float4& v, int C, double* part) {
+  __shared__ float4 sb[kThreads];
+  sb[threadIdx.x] = v;
+  __syncthreads();
+  const int C4 = C / 4;
+  for (int c4 = threadIdx.x; c4 < C4; c4 += blockDim.x) {
+    double a[4] = {0, 0, 0, 0};
+    // the block's first thread need not sit on quad 0: thread t holds quad (base + t) % C4
+    const int base = static_cast<int>((static_cast<int64_t>(blockIdx.x) * blockDim.x) % C4);
+    const int t0 = (c4 - base + C4) % C4;
+    for (int t = t0; t < static_cast<int>(blockDim.x); t += C4) {
+      const float4 w = sb[t];
+      a[0] += w.x; a[1] += w.y; a[2] += w.z; a[3] += w.w;
+    }
+    double* p0 = part + static_cast<size_t>(blockIdx.x) * 2 * C + c4 * 4;
+    double* p1 = p0 + C;
+    for (int e = 0; e < 4; ++e) {
+      p0[e] = a[e];
+      p1[e] = 0.0;
+    }
+  }
+}
+
+// dbias (optional, 256 % (C/4) == 0): also the column sums of this pass's dx
+// contribution -- the bias gradient of the CONV producing x, whose only
+// consumer this BN is (its gradient buffer holds nothing else) -- as per-block partials part[block][2][C] (doubles; second plane 0) for
+// colred_stage2: a fixed thread -> (channel quad, row lane) map, so the sums
+// are deterministic.
 __global__ void bn_dx_v4(const float4* __restrict__ x, const float4* __restrict__ dy, int64_t n4, int64_t rows,
                          int C, const float* __restrict__ gamma, const float* __restrict__ beta,
                          const float* __restrict__ stats, const float* __restrict__ coef, float4* dx, int accumulate,
-                         int relu) {
+                         int relu, double* dbias_part) {
   const ChanLoop L = chan_loop(C / 4);
-  if (!L.active) return;
+  float4 bsum = zero4();
+  if (!L.active) {
+    if (dbias_part) bias_block_reduce(bsum, C, dbias_part);
+    return;
+  }
   const float inv_m = 1.0f / static_cast<float>(rows);
   const Bn4 p = bn_params4(stats, gamma, beta, L.c, C);
   const float4 c1 = ld4(coef + L.c), c2 = ld4(coef + C + L.c);
@@ -489,10 +536,12 @@ __global__ void bn_dx_v4(const float4* __restrict__ x, const float4* __restrict_
 #pragma unroll
       for (int e = 0; e < 4; ++e) r[e] = gs[e] * (gg[e] - k1[e] - bn_xhat(xs[e], m[e], is[e]) * k2[e]);
       float4 o = make_float4(r[0], r[1], r[2], r[3]);
+      if (dbias_part) add4(bsum, o);
       if (accumulate) add4(o, ov[u]);
       dx[i] = o;
     }
   }
+  if (dbias_part) bias_block_reduce(bsum, C, dbias_part);
 }
 
 // ---------------------------------------------------------------------------
@@ -737,6 +786,124 @@ __global__ void pool_gather_kernel(PoolShape s, const uchar4* __restrict__ arg, 
   }
 }
 
+// Max-pool backward, fused (argmax + gather, one pass over x, y, dy, dx).
+// Block = (16-channel chunk, band of PB output rows, image).  The block owns the
+// input rows h whose floor((h + pad) / stride) lies in its band; phase 1
+// computes, for every window covering those rows, the first (row-major)
+// position holding the forward maximum y and stages it with dy in shared
+// memory; phase 2 gathers each owned input element from the <= ceil(K/s)^2
+// windows covering it.  Windows on a band edge are evaluated by both
+// neighbouring blocks (cheap) so that no element has two writers.
+constexpr int kPoolCv = 4;  // float4s per pixel chunk (16 channels)
+
+// KC = compile-time window size (0: runtime s.K): with it the window's loads
+// are unrolled and all in flight at once.
+template <int KC>
+__global__ void __launch_bounds__(256) pool_max_bwd_fused(PoolShape s, const float4* __restrict__ x,
+                                                          const float4* __restrict__ y,
+                                                          const float4* __restrict__ dy, float4* dx,
+                                                          int accumulate, int PB, int WR) {
+  extern __shared__ float4 psm[];
+  float4* sdy = psm;                                                  // [WR][Q][kPoolCv]
+  uchar4* sarg = reinterpret_cast<uchar4*>(psm + WR * s.Q * kPoolCv);  // [WR][Q][kPoolCv]
+  const int C4 = s.C / 4;
+  const int c4 = blockIdx.x * kPoolCv;
+  const int band = blockIdx.y, n = blockIdx.z;
+  int h_lo = band * PB * s.stride - s.pad;
+  int h_hi = (band + 1) * PB * s.stride - s.pad - 1;
+  if (band == 0) h_lo = 0;
+  if (band == gridDim.y - 1) h_hi = s.H - 1;
+  if (h_lo < 0) h_lo = 0;
+  if (h_hi > s.H - 1) h_hi = s.H - 1;
+  const int t = h_lo + s.pad - s.K + 1;
+  const int pl = t <= 0 ? 0 : (t + s.stride - 1) / s.stride;
+  int ph = (h_hi + s.pad) / s.stride;
+  if (ph > s.P - 1) ph = s.P - 1;
+  const int nwin = (ph - pl + 1) * s.Q * kPoolCv;
+  const float4* xn = x + static_cast<int64_t>(n) * s.H * s.W * C4 + c4;
+  for (int i = threadIdx.x; i < nwin; i += blockDim.x) {
+    const int cv = i % kPoolCv;
+    const int pq = i / kPoolCv;
+    const int q = pq % s.Q, pr = pq / s.Q;
+    const int p = pl + pr;
+    const int64_t o = ((static_cast<int64_t>(n) * s.P + p) * s.Q + q) * C4 + c4 + cv;
+    const float4 m = y[o];
+    const int h0 = p * s.stride - s.pad, w0 = q * s.stride - s.pad;
+    int a0 = 255, a1 = 255, a2 = 255, a3 = 255;
+    const float4 g = dy[o];
+    if constexpr (KC > 0) {
+      float4 v[KC * KC];
+#pragma unroll
+      for (int r = 0; r < KC; ++r)
+#pragma unroll
+        for (int u = 0; u < KC; ++u) {
+          const int h = h0 + r, w = w0 + u;
+          const bool in = h >= 0 && h < s.H && w >= 0 && w < s.W;
+          // out-of-image taps can never equal the maximum: NaN
+          v[r * KC + u] = in ? xn[(static_cast<int64_t>(h) * s.W + w) * C4 + cv]
+                             : make_float4(NAN, NAN, NAN, NAN);
+        }
+#pragma unroll
+      for (int k = KC * KC - 1; k >= 0; --k) {  // descending: the first (row-major) match wins
+        if (v[k].x == m.x) a0 = k;
+        if (v[k].y == m.y) a1 = k;
+        if (v[k].z == m.z) a2 = k;
+        if (v[k].w == m.w) a3 = k;
+      }
+    } else {
+      for (int r = 0; r < s.K; ++r) {
+        const int h = h0 + r;
+        if (h < 0 || h >= s.H) continue;
+        for (int u = 0; u < s.K; ++u) {
+          const int w = w0 + u;
+          if (w < 0 || w >= s.W) continue;
+          const float4 v = xn[(static_cast<int64_t>(h) * s.W + w) * C4 + cv];
+          const int off = r * s.K + u;
+          if (a0 == 255 && v.x == m.x) a0 = off;
+          if (a1 == 255 && v.y == m.y) a1 = off;
+          if (a2 == 255 && v.z == m.z) a2 = off;
+          if (a3 == 255 && v.w == m.w) a3 = off;
+        }
+      }
+    }
+    sarg[i] = make_uchar4(a0, a1, a2, a3);
+    sdy[i] = g;
+  }
+  __syncthreads();
+  const int nin = (h_hi - h_lo + 1) * s.W * kPoolCv;
+  float4* dxn = dx + static_cast<int64_t>(n) * s.H * s.W * C4 + c4;
+  for (int i = threadIdx.x; i < nin; i += blockDim.x) {
+    const int cv = i % kPoolCv;
+    const int hw = i / kPoolCv;
+    const int w = hw % s.W, h = h_lo + hw / s.W;
+    int plo = h + s.pad - s.K + 1, qlo = w + s.pad - s.K + 1;
+    plo = plo <= 0 ? 0 : (plo + s.stride - 1) / s.stride;
+    qlo = qlo <= 0 ? 0 : (qlo + s.stride - 1) / s.stride;
+    int phi = (h + s.pad) / s.stride, qhi = (w + s.pad) / s.stride;
+    if (phi > s.P - 1) phi = s.P - 1;
+    if (qhi > s.Q - 1) qhi = s.Q - 1;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int p = plo; p <= phi; ++p) {
+      for (int q = qlo; q <= qhi; ++q) {
+        const int j = ((p - pl) * s.Q + q) * kPoolCv + cv;
+        const int off = (h - (p * s.stride - s.pad)) * s.K + (w - (q * s.stride - s.pad));
+        const uchar4 a = sarg[j];
+        const float4 g = sdy[j];
+        if (a.x == off) acc.x += g.x;
+        if (a.y == off) acc.y += g.y;
+        if (a.z == off) acc.z += g.z;
+        if (a.w == off) acc.w += g.w;
+      }
+    }
+    float4* d = dxn + (static_cast<int64_t>(h) * s.W + w) * C4 + cv;
+    if (accumulate) {
+      const float4 o = *d;
+      acc.x += o.x; acc.y += o.y; acc.z += o.z; acc.w += o.w;
+    }
+    *d = acc;
+  }
+}
+
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ float lrn_scale(const float* xp, int c, int C, int lo, int hi, float alpha_n, float k) {
   float s = 0.f;
@@ -943,8 +1110,9 @@ __global__ void zero_kernel(float* p, int64_t n) {
 }  // namespace
 
 int64_t red_scratch_floats(int C) {
-  // kRedChunks*2*C partial doubles + 2*C float coefficients
-  return static_cast<int64_t>(kRedChunks) * 2 * C * 2 + 2 * C + 64;
+  // kRedChunks*2*C partial doubles + 2*C float coefficients (+ pad), then the
+  // fused bias-gradient partials of bn_bwd: kEltBlocks*2*C doubles
+  return static_cast<int64_t>(kRedChunks) * 2 * C * 2 + 2 * C + 64 + static_cast<int64_t>(kEltBlocks) * 2 * C * 2;
 }
 
 cudaError_t bias_grad(const float* dy, int64_t rows, int C, float* db, float* red_scratch, cudaStream_t st) {
@@ -962,18 +1130,83 @@ cudaError_t bn_fwd(const float* x, int64_t rows, int C, const float* gamma, cons
   const int64_t n = rows * C;
   if (C % 4 == 0)
     bn_apply_v4<<<elt_blocks(n / 4, C / 4), kThreads, 0, st>>>(reinterpret_cast<const float4*>(x), n / 4, C, gamma,
-                                                                beta, stats, reinterpret_cast<float4*>(y), nullptr);
+                                                                beta, stats, reinterpret_cast<float4*>(y), nullptr,
+                                                                nullptr, nullptr);
   else
     bn_apply_scalar<<<blocks_for(n), kThreads, 0, st>>>(x, n, C, gamma, beta, stats, y);
   return cudaGetLastError();
 }
 
+namespace {
+
+// Stage 1 over the convolution's tile partials: block b combines tiles
+// [b*chunk, (b+1)*chunk) into {sum(y - x0), sum((y - x0)^2)} (doubles) about the
+// global shift x0 = x[0][c]:  with d = shift_t - x0,
+//   sum(y - x0)     = S1_t + n_t d
+//   sum((y - x0)^2) = S2_t + 2 d S1_t + n_t d^2.
+__global__ void tile_stats_stage1(const float* __restrict__ tiles, int ntiles, int tile_rows, int64_t rows, int C,
+                                  const float* __restrict__ x, int chunk, double* part) {
+  __shared__ double s1[kThreads], s2[kThreads];
+  const int t0 = blockIdx.x * chunk;
+  const int t1 = min(ntiles, t0 + chunk);
+  const int cb = C < kThreads ? C : kThreads;
+  const int lanes = kThreads / cb;
+  const int lane = threadIdx.x / cb, cc = threadIdx.x % cb;
+  for (int c0 = 0; c0 < C; c0 += cb) {
+    const int c = c0 + cc;
+    double a = 0.0, b = 0.0;
+    if (lane < lanes && c < C) {
+      const double x0 = x[c];
+      for (int t = t0 + lane; t < t1; t += lanes) {
+        const float* p = tiles + static_cast<size_t>(t) * 3 * C + c;
+        const int64_t left = rows - static_cast<int64_t>(t) * tile_rows;
+        const double n = static_cast<double>(left < tile_rows ? left : tile_rows);
+        const double d = static_cast<double>(p[0]) - x0;
+        const double S1 = p[C], S2 = p[2 * C];
+        a += S1 + n * d;
+        b += S2 + 2.0 * d * S1 + n * d * d;
+      }
+    }
+    s1[threadIdx.x] = a;
+    s2[threadIdx.x] = b;
+    __syncthreads();
+    if (lane == 0 && c < C) {
+      double A = 0.0, B = 0.0;
+      for (int l = 0; l < lanes; ++l) {
+        A += s1[l * cb + cc];
+        B += s2[l * cb + cc];
+      }
+      part[(static_cast<size_t>(blockIdx.x) * 2) * C + c] = A;
+      part[(static_cast<size_t>(blockIdx.x) * 2 + 1) * C + c] = B;
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+cudaError_t bn_stats_from_tiles(const float* tiles, int ntiles, int tile_rows, const float* x, int64_t rows, int C,
+                                float* stats, float* running, float eps, float momentum, float* red_scratch,
+                                cudaStream_t st) {
+  double* part = reinterpret_cast<double*>(red_scratch);
+  int nb = (ntiles + 15) / 16;
+  nb = nb < 1 ? 1 : (nb > kRedChunks ? kRedChunks : nb);
+  const int chunk = (ntiles + nb - 1) / nb;
+  nb = (ntiles + chunk - 1) / chunk;
+  tile_stats_stage1<<<nb, kThreads, 0, st>>>(tiles, ntiles, tile_rows, rows, C, x, chunk, part);
+  colred_stage2<<<(C + 31) / 32, kStage2Threads, 0, st>>>(part, nb, C,
+                                                          BnStatsFin{x, rows, C, eps, momentum, stats, running});
+  return cudaGetLastError();
+}
+
 cudaError_t bn_apply_relu(const float* x, int64_t rows, int C, const float* gamma, const float* beta,
-                          const float* stats, float* y, float* y_relu, cudaStream_t st) {
+                          const float* stats, float* y, float* y_relu, cudaStream_t st, const float* join_other,
+                          float* y_join) {
   const int64_t n4 = rows * C / 4;
-  bn_apply_v4<<<elt_blocks(n4, C / 4), kThreads, 0, st>>>(reinterpret_cast<const float4*>(x), n4, C, gamma, beta,
-                                                           stats, reinterpret_cast<float4*>(y),
-                                                           reinterpret_cast<float4*>(y_relu));
+  bn_apply_v4<<<elt_blocks(n4, C / 4), kThreads, 0, st>>>(
+      reinterpret_cast<const float4*>(x), n4, C, gamma, beta, stats, reinterpret_cast<float4*>(y),
+      reinterpret_cast<float4*>(y_relu), reinterpret_cast<const float4*>(join_other),
+      reinterpret_cast<float4*>(y_join));
   return cudaGetLastError();
 }
 
@@ -984,22 +1217,32 @@ cudaError_t grad_copy2(const float* src, float* d1, int acc1, float* d2, int acc
   return cudaGetLastError();
 }
 
+bool bn_bwd_bias_ok(int C) { return C % 4 == 0 && kThreads % (C / 4) == 0; }
+
 cudaError_t bn_bwd(const float* x, const float* dy, int64_t rows, int C, const float* gamma, const float* beta,
                    const float* stats, int relu, float* dx, int accumulate, float* dgamma, float* dbeta,
-                   float* red_scratch, cudaStream_t st) {
+                   float* red_scratch, cudaStream_t st, float* dbias) {
   float* coef = red_scratch + static_cast<int64_t>(kRedChunks) * 2 * C * 2;  // past the partials
   cudaError_t e = colred(RedBnBwdOp{x, dy, stats, gamma, beta, relu}, BnBwdFin{C, dgamma, dbeta, coef}, rows, C,
                          red_scratch, st);
   if (e != cudaSuccess) return e;
   const int64_t n = rows * C;
+  if (dbias && (!dx || !bn_bwd_bias_ok(C))) return cudaErrorInvalidValue;
   if (dx) {
-    if (C % 4 == 0)
-      bn_dx_v4<<<elt_blocks(n / 4, C / 4), kThreads, 0, st>>>(
-          reinterpret_cast<const float4*>(x), reinterpret_cast<const float4*>(dy), n / 4, rows, C, gamma, beta, stats,
-          coef, reinterpret_cast<float4*>(dx), accumulate, relu);
-    else
+    if (C % 4 == 0) {
+      const int nb = elt_blocks(n / 4, C / 4);
+      // bias partials past the colred partials and coef (see red_scratch_floats)
+      double* part = dbias ? reinterpret_cast<double*>(red_scratch + static_cast<int64_t>(kRedChunks) * 2 * C * 2 +
+                                                       ((2 * C + 63) / 64) * 64)
+                           : nullptr;
+      bn_dx_v4<<<nb, kThreads, 0, st>>>(reinterpret_cast<const float4*>(x), reinterpret_cast<const float4*>(dy),
+                                        n / 4, rows, C, gamma, beta, stats, coef, reinterpret_cast<float4*>(dx),
+                                        accumulate, relu, part);
+      if (dbias) colred_stage2<<<(C + 31) / 32, kStage2Threads, 0, st>>>(part, nb, C, BiasFin{dbias});
+    } else {
       bn_dx_scalar<<<blocks_for(n), kThreads, 0, st>>>(x, dy, n, rows, C, gamma, beta, stats, coef, dx, accumulate,
                                                        relu);
+    }
   }
   return cudaGetLastError();
 }
@@ -1032,12 +1275,39 @@ cudaError_t pool_fwd(const PoolShape& s, const float* x, float* y, cudaStream_t 
   return cudaGetLastError();
 }
 
+static bool pool_fused_ok(const PoolShape& s, int* PB, int* WR, size_t* smem) {
+  if (s.mode != 0 || s.C % (4 * kPoolCv) != 0 || s.K * s.K >= 255 || s.stride < 1) return false;
+  // band of PB output rows: enough windows per block to amortise the edge re-evaluation
+  *PB = s.P >= 8 ? 4 : s.P;
+  *WR = *PB + (s.K - 1) / s.stride + 1;
+  *smem = static_cast<size_t>(*WR) * s.Q * kPoolCv * (sizeof(float4) + sizeof(uchar4));
+  return *smem <= 48 * 1024;
+}
+
+int pool_bwd_kernels(const PoolShape& s) {
+  int PB, WR;
+  size_t smem;
+  if (pool_fused_ok(s, &PB, &WR, &smem)) return 1;
+  return (s.C % 4 == 0 && s.mode == 0 && s.K * s.K < 255) ? 2 : 1;
+}
+
 int64_t pool_scratch_bytes(const PoolShape& s) {
+  if (pool_bwd_kernels(s) == 1) return 0;
   return (s.C % 4 == 0 && s.mode == 0 && s.K * s.K < 255) ? static_cast<int64_t>(s.N) * s.P * s.Q * s.C : 0;
 }
 
 cudaError_t pool_bwd(const PoolShape& s, const float* x, const float* y, const float* dy, float* dx, int accumulate,
                      void* scratch, cudaStream_t st) {
+  int PB, WR;
+  size_t smem;
+  if (pool_fused_ok(s, &PB, &WR, &smem)) {
+    dim3 grid(s.C / (4 * kPoolCv), (s.P + PB - 1) / PB, s.N);
+    auto k = s.K == 3 ? pool_max_bwd_fused<3> : (s.K == 2 ? pool_max_bwd_fused<2> : pool_max_bwd_fused<0>);
+    k<<<grid, 256, smem, st>>>(s, reinterpret_cast<const float4*>(x), reinterpret_cast<const float4*>(y),
+                               reinterpret_cast<const float4*>(dy), reinterpret_cast<float4*>(dx), accumulate, PB,
+                               WR);
+    return cudaGetLastError();
+  }
   if (s.C % 4 == 0 && (s.mode == 1 || (scratch && s.K * s.K < 255))) {
     const int in4 = static_cast<int>(static_cast<int64_t>(s.N) * s.H * s.W * s.C / 4);
     const int out4 = static_cast<int>(static_cast<int64_t>(s.N) * s.P * s.Q * s.C / 4);

@@ -235,3 +235,70 @@ def test_stem_eligibility(cuda):
     odd, _, _ = _shape_arr(1, 4, 32, 32, 32, 3, 3, 1)       # stride 3 does not divide 8
     assert lib.sn_test_stem(wide, 3, None, sizes) == -1
     assert lib.sn_test_stem(odd, 3, None, sizes) == -1
+
+
+POOL_CASES = [
+    # N, C, H, W, K, stride, pad, mode
+    (4, 64, 112, 112, 3, 2, 1, 0),   # ResNet stem max-pool (fused argmax+gather path)
+    (3, 96, 55, 55, 3, 2, 0, 0),     # AlexNet pool1
+    (2, 48, 13, 13, 3, 2, 0, 0),     # C % 16 == 0, P < 8: one band
+    (2, 12, 17, 17, 3, 2, 1, 0),     # C % 16 != 0: two-pass argmax + gather
+    (2, 5, 9, 9, 2, 2, 0, 0),        # C % 4 != 0: scalar path
+    (2, 64, 14, 14, 7, 1, 0, 1),     # global-ish average pool
+    (2, 32, 20, 20, 3, 1, 1, 0),     # stride 1 (windows overlap by two)
+]
+
+
+def _pool_lib():
+    from paper_1801_04380_b200 import _native
+    lib = _native.executor()
+    lib.sn_test_pool.restype = ctypes.c_longlong
+    lib.sn_test_pool.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_void_p),
+                                 ctypes.c_int]
+    return lib
+
+
+@pytest.mark.parametrize("ties", [False, True])
+@pytest.mark.parametrize("case", POOL_CASES)
+def test_pool_fwd_bwd_exact(cuda, case, ties):
+    """Pool forward and backward vs torch fp64 (max: the first row-major
+    maximum of the window gets the gradient, as in torch's CPU kernel).
+    Forward max is bit-exact; gradients are sums of at most ceil(K/s)^2 dy
+    terms (fp32 vs fp64 accumulation): atol/rtol 1e-5 -- a wrong argmax moves
+    an element by O(1)."""
+    N, C, H, W, K, s, p, mode = case
+    lib = _pool_lib()
+    P = (H + 2 * p - K) // s + 1
+    Q = (W + 2 * p - K) // s + 1
+    shape = (ctypes.c_int * 10)(N, H, W, C, P, Q, K, s, p, mode)
+    g = torch.Generator().manual_seed(sum(case) + ties)
+    x = torch.randn(N, C, H, W, generator=g)
+    if ties:
+        x = torch.round(x * 2) / 2  # many equal values inside a window
+    dy = torch.randn(N, C, P, Q, generator=g)
+    xd = x.double().requires_grad_(True)
+    if mode == 0:
+        y = torch.nn.functional.max_pool2d(xd, K, s, p)
+    else:
+        y = torch.nn.functional.avg_pool2d(xd, K, s, p, count_include_pad=True)
+    y.backward(dy.double())
+    nhwc = lambda t: t.permute(0, 2, 3, 1).contiguous().to(cuda)
+    x_d, dy_d = nhwc(x), nhwc(dy)
+    y_d = torch.full((N, P, Q, C), float("nan"), device=cuda)
+    assert lib.sn_test_pool(0, shape, (ctypes.c_void_p * 2)(x_d.data_ptr(), y_d.data_ptr()), 0) == 0
+    y_ref = y.detach().float()
+    got = y_d.permute(0, 3, 1, 2).cpu()
+    if mode == 0:
+        assert torch.equal(got, y_ref)
+    else:
+        assert torch.allclose(got, y_ref, rtol=1e-6, atol=1e-6)
+    scratch = torch.empty(max(1, int(lib.sn_test_pool(2, shape, None, 0))), dtype=torch.uint8, device=cuda)
+    dx_d = torch.full((N, H, W, C), float("nan"), device=cuda)
+    ptrs = (ctypes.c_void_p * 5)(x_d.data_ptr(), y_d.data_ptr(), dy_d.data_ptr(), dx_d.data_ptr(), scratch.data_ptr())
+    assert lib.sn_test_pool(1, shape, ptrs, 0) == 0
+    ref = xd.grad.float()
+    got = dx_d.permute(0, 3, 1, 2).cpu()
+    assert torch.allclose(got, ref, rtol=1e-5, atol=1e-5), (got - ref).abs().max()
+    assert lib.sn_test_pool(1, shape, ptrs, 1) == 0  # accumulate
+    got2 = dx_d.permute(0, 3, 1, 2).cpu()
+    assert torch.allclose(got2, 2 * got, rtol=0, atol=0) if mode == 0 else torch.allclose(got2, 2 * got)

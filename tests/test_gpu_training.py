@@ -249,6 +249,10 @@ def test_layer_fusions_are_bit_identical(cuda, monkeypatch):
     net = gen_resnet(1, 1, 2, 1)
     params = init_parameters(net, seed=6, head_scale=0.1)
     images, labels = _inputs(net, 4, seed=3)
+    # the CONV-epilogue BN statistics and the BN-backward CONV bias gradient
+    # sum in a different order (checked separately below); this test pins the
+    # bit-exact fusions
+    monkeypatch.setenv("SN_FUSE_REASSOC", "0")
     for feats in ("none", ALL):
         loss, grads, _, t = _run(net, 4, 4 << 30, feats, params, images, labels)
         monkeypatch.setenv("SN_FUSE", "0")
@@ -256,3 +260,42 @@ def test_layer_fusions_are_bit_identical(cuda, monkeypatch):
         monkeypatch.delenv("SN_FUSE")
         assert t.kernels < t0.kernels
         assert loss == loss0 and _bitwise(grads, grads0)
+
+
+def test_reassociating_fusions(cuda, monkeypatch):
+    """BN statistics combined from the CONV epilogue's per-tile partials
+    (shifted sums per 128-row tile, fp64 combination) and the CONV bias
+    gradient summed in the BN backward's dx pass match the separate reduction
+    passes to fp32 rounding.  On a smooth net (no ReLU / max-pool masks that a
+    last-bit change can flip): loss rel. 1e-5, weight / BN gradients rel. 1e-4,
+    CONV biases (analytically zero before a BN, so pure rounding noise) abs.
+    1e-4 of the largest weight gradient.  The fused run is deterministic
+    (bit-identical on repeat), also on ResNet-50g-style blocks."""
+    from paper_1801_04380_b200.netgen import gen_resnet
+    from paper_1801_04380_b200.training import init_parameters
+    from oracle.numerics import relative_error
+    sn = _sn()
+    rnet = gen_resnet(1, 1, 2, 1)
+    rparams = init_parameters(rnet, seed=6, head_scale=0.1)
+    rimages, rlabels = _inputs(rnet, 8, seed=4)
+    loss, grads, _, _ = _run(rnet, 8, 4 << 30, ALL, rparams, rimages, rlabels)
+    loss_b, grads_b, _, _ = _run(rnet, 8, 4 << 30, ALL, rparams, rimages, rlabels)
+    assert loss == loss_b and _bitwise(grads, grads_b)
+
+    net = sn.parse_network(SMOOTH32, "smooth32")
+    params = init_parameters(net, seed=3, head_scale=0.1)
+    images, labels = _inputs(net, 8, seed=5)
+    loss, grads, _, t = _run(net, 8, 1 << 30, ALL, params, images, labels)
+    monkeypatch.setenv("SN_FUSE_REASSOC", "0")
+    loss0, grads0, _, t0 = _run(net, 8, 1 << 30, ALL, params, images, labels)
+    assert t.kernels < t0.kernels
+    assert abs(loss - loss0) <= 1e-5 * abs(loss0)
+    kinds = {l.id: l.kind.name for l in net.layers}
+    worst = max(relative_error(grads[l]["w"], grads0[l]["w"]) for l in grads)
+    assert worst <= 1e-4, worst
+    scale = max(float(grads0[l]["w"].abs().max()) for l in grads)
+    for l in grads:
+        if kinds[l] == "CONV" and kinds[net.layers[l].next[0]] == "BN":
+            assert float((grads[l]["b"] - grads0[l]["b"]).abs().max()) <= 1e-4 * scale, net.layers[l].name
+        else:
+            assert relative_error(grads[l]["b"], grads0[l]["b"]) <= 1e-4, net.layers[l].name
