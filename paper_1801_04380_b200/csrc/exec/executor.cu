@@ -501,6 +501,7 @@ struct Compiler {
       }
       case snp::ACT:
         if (fused_bn >= 0 && join_fuse_at[cur_ti] >= 0) break;  // launched at the JOIN (bn_apply_relu_join)
+        if (dead_at[cur_ti]) break;                                // output never read (plan_fusions)
         if (fused_bn >= 0) {
           const LayerRt& bl = ex->L[fused_bn];
           const float* bx = ptr(snp::K_ACT, net.prev[fused_bn][0]);
@@ -750,6 +751,7 @@ struct Compiler {
   // BN+ReLU (fused) forward / replay whose next compute action is the same op
   // of a 2-input JOIN reading the ReLU: the whole chain runs at the JOIN.
   std::vector<int> join_fuse_at, join_from;
+  std::vector<char> dead_at;  // forward / replay whose outputs are never read: not launched
   // CONV forward -> BN forward (next compute action, reading that output): the
   // CONV epilogue emits per-tile statistics, the BN only combines them.
   bool conv_stats_now = false, bn_tiles_now = false;
@@ -781,6 +783,7 @@ struct Compiler {
     bn_tiles_at.assign(T, 0);
     join_fuse_at.assign(T, -1);
     join_from.assign(T, -1);
+    dead_at.assign(T, 0);
     bn_bias_at.assign(T, 0);
     conv_bias_done.assign(net.n, 0);
     const char* env = std::getenv("SN_FUSE");  // SN_FUSE=0: one kernel per layer (A/B and bitwise tests)
@@ -864,7 +867,8 @@ struct Compiler {
     }
     // ReLU -> JOIN: every event between the two may allocate (the JOIN output)
     // or touch unrelated tensors, but must not free / copy the BN input, the
-    // BN output or the ReLU output (they are read or written at the JOIN).
+    // BN output (unless it is never materialised) or the ReLU output (they are
+    // read or written at the JOIN).
     std::vector<int> act_join_fused(net.n, 0);
     for (size_t i = 0; i < T; ++i) {
       if (fused_into[i] < 0) continue;
@@ -872,7 +876,9 @@ struct Compiler {
       const int ra = e.b, bn = fused_into[i], bin = net.prev[bn][0];
       for (size_t j = i + 1; j < T; ++j) {
         const snp::Event& f = P.tape[j];
-        if (f.op == 'F' || f.op == 'O' || f.op == 'P' || f.op == 'D') {
+        if ((f.op == 'F' && f.a == snp::K_ACT) || f.op == 'O' || f.op == 'P' || f.op == 'D') {
+          // the BN output, when never materialised, may be dropped in between
+          if (f.op == 'F' && f.b == bn && elide_out[bn]) continue;
           if (f.b == ra || f.b == bn || f.b == bin) break;
           continue;
         }
@@ -890,6 +896,30 @@ struct Compiler {
     for (int a = 0; a < net.n; ++a) {
       if (!bn_relu_pair(a) || !act_bwd_fused[a] || net.next[a].size() != 1) continue;
       if (act_fwd[a] == act_join_fused[a]) elide_out[a] = 1;  // read only by the fused chains
+    }
+    // Dead writes: a fused BN+ReLU forward / replay (BN output not
+    // materialised) whose ReLU output nobody reads before it is freed or
+    // rewritten -- typically a replay the reference schedules because the
+    // ReLU backward reads y, which here is folded into the BN backward.
+    for (size_t i = 0; i < T; ++i) {
+      if (fused_into[i] < 0 || join_fuse_at[i] >= 0 || !elide_out[fused_into[i]]) continue;
+      const int ra = P.tape[i].b;
+      bool read = false;
+      for (size_t j = i + 1; j < T && !read; ++j) {
+        const snp::Event& f = P.tape[j];
+        if (f.op == 'F' && f.a == snp::K_ACT && f.b == ra) break;
+        if ((f.op == 'C' || f.op == 'R') && f.b == ra) break;  // rewritten
+        if (f.op == 'O' && f.b == ra) read = true;
+        if ((f.op == 'C' || f.op == 'R') && join_from[j] < 0)
+          for (int p : net.prev[f.b]) read |= p == ra;
+        if (f.op == 'B') {
+          if (f.b == ra) read |= !act_bwd_skip[j];
+          const int k = net.kind[f.b];
+          if (k == snp::CONV || k == snp::BN || k == snp::POOL || k == snp::LRN || k == snp::FC)
+            for (int p : net.prev[f.b]) read |= p == ra;
+        }
+      }
+      if (!read) dead_at[i] = 1;
     }
     ex->elided = elide_out;
   }

@@ -19,6 +19,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -61,10 +62,16 @@ constexpr int kTmaThreads = 192;
 // ... (tile = m-tile fastest, then n-tile, then split).  The TMA producer runs
 // ahead across tile boundaries, the MMA issuer alternates between two TMEM
 // accumulators (2 x BN columns), so tile i's epilogue overlaps tile i+1's MMAs.
-template <int BN, int STAGES>
+//
+// CG = 2 (CTA pair, cluster of 2 on one TPC): the pair computes a 256 x BN
+// tile with tcgen05.mma.cta_group::2 issued by the even CTA; each CTA stages
+// its own 128 A rows and HALF of B (BN/2 rows), so the per-SM operand traffic
+// from L2 drops from (128 + BN) to (128 + BN/2) rows per k block -- the
+// im2col conv kernels are bound by that traffic (~12 TB/s chip-wide).
+template <int BN, int STAGES, int CG = 1>
 struct TmaSmem {
   static constexpr int A_BYTES = kBM * 128;
-  static constexpr int B_BYTES = BN * 128;
+  static constexpr int B_BYTES = (BN / CG) * 128;
   static constexpr int EPI_OFF = STAGES * (A_BYTES + B_BYTES);   // 2 x 16 KB store staging
   static constexpr int BAR_OFF = EPI_OFF + 2 * kBM * 128;
   static constexpr int STATS_OFF = BAR_OFF + 512;  // [4 warps][32 columns][2] floats
@@ -95,11 +102,63 @@ struct TileGrid {
   int m_tiles, n_tiles, tiles;
 };
 
-template <int BN, int STAGES, int MODE>
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of the same smem variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_u32(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cbar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cbar) : "memory");
+}
+// TMA loads whose completion is signalled on the pair leader's mbarrier (cbar: cluster address)
+__device__ __forceinline__ void tma2_load_2d(uint32_t dst, const void* tmap, uint32_t cbar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(cbar), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma2_load_im2col_4d(uint32_t dst, const void* tmap, uint32_t cbar, int c, int w, int h,
+                                                    int n, uint16_t ws, uint16_t hr) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.im2col.mbarrier::complete_tx::bytes [%0], [%1, "
+      "{%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(cbar), "r"(c), "r"(w), "r"(h), "r"(n), "h"(ws), "h"(hr)
+      : "memory");
+}
+__device__ __forceinline__ void umma2_tf32(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// commit the pair's MMAs to the same mbarrier in both CTAs
+__device__ __forceinline__ void umma2_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(static_cast<uint16_t>(3))
+      : "memory");
+}
+
+template <int BN, int STAGES, int MODE, int CG = 1>
 __global__ void __launch_bounds__(kTmaThreads, 1)
     tc_conv_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                        const __grid_constant__ CUtensorMap tmD, TmaArgs a, EpiArgs e, TileGrid tg) {
-  using L = TmaSmem<BN, STAGES>;
+  static_assert(CG == 1 || MODE <= 1, "CTA pairs: forward / dgrad (MODE 0) and wgrad (MODE 1) only");
+  using L = TmaSmem<BN, STAGES, CG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -121,11 +180,20 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 128);
+      mbar_init(&tempty[b], 128 * CG);  // both CTAs' epilogues drain the pair's accumulator
     }
     fence_mbar_init();
   }
-  if (warp == 5) tmem_alloc(tmem_slot, kCols);
+  if (warp == 5) {
+    if constexpr (CG == 1) {
+      tmem_alloc(tmem_slot, kCols);
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(kCols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+  }
   if (warp == 4 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
@@ -133,25 +201,32 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (CG == 2) cluster_sync_all();  // the peer's barriers are initialised before any remote signal
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const int rank = CG == 2 ? static_cast<int>(cluster_rank()) : 0;
+  const int unit = blockIdx.x / CG, units = gridDim.x / CG;  // CTA pair (or CTA) index / count
 
+  // m0: this CTA's first A row (the pair's tile is 128*CG rows, rank r owns
+  // rows [128 r, 128 r + 128)); n0: the tile's first column (rank r stages B
+  // columns [n0 + r BN/CG, n0 + (r+1) BN/CG)).
   auto tile_coords = [&](int t, int& m0, int& n0, int& kb0, int& nkb, int& split) {
     const int mt = t % tg.m_tiles;
     const int rest = t / tg.m_tiles;
     const int nt = rest % tg.n_tiles;
     split = rest / tg.n_tiles;
-    m0 = mt * kBM;
+    m0 = mt * kBM * CG + rank * kBM;
     n0 = nt * BN;
     kb0 = split * a.kb_per_split;
     nkb = min(a.num_kb, kb0 + a.kb_per_split) - kb0;
   };
+  constexpr int BH = BN / CG;  // B columns staged by this CTA
 
   if (warp == 4) {
     if (lane == 0) {
       // ---------------- TMA producer ----------------
       uint32_t g = 0;  // k blocks issued by this CTA (stage ring position)
-      for (int t = blockIdx.x; t < tg.tiles; t += gridDim.x) {
+      for (int t = unit; t < tg.tiles; t += units) {
         int m0, n0, kb0, nkb, split;
         tile_coords(t, m0, n0, kb0, nkb, split);
         if (MODE == 0) {
@@ -168,10 +243,19 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             const int cc = kb - tap * a.cchunks;
             const int r = static_cast<int>(a.fS.div(tap));
             const int tt = tap - r * a.S;
-            mbar_arrive_expect_tx(&full[s], L::A_BYTES + L::B_BYTES);
-            tma_load_im2col_4d(smem_u32(sA + s * L::A_BYTES), &tmA, &full[s], cc * 32, w0, h0, n,
-                               static_cast<uint16_t>(tt), static_cast<uint16_t>(r));
-            tma_load_2d(smem_u32(sB + s * L::B_BYTES), &tmB, &full[s], kb * kBK, n0);
+            if constexpr (CG == 1) {
+              mbar_arrive_expect_tx(&full[s], L::A_BYTES + L::B_BYTES);
+              tma_load_im2col_4d(smem_u32(sA + s * L::A_BYTES), &tmA, &full[s], cc * 32, w0, h0, n,
+                                 static_cast<uint16_t>(tt), static_cast<uint16_t>(r));
+              tma_load_2d(smem_u32(sB + s * L::B_BYTES), &tmB, &full[s], kb * kBK, n0);
+            } else {
+              // both CTAs' loads complete on the leader's full barrier
+              if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * (L::A_BYTES + L::B_BYTES));
+              const uint32_t cb = mapa_u32(&full[s], 0);
+              tma2_load_im2col_4d(smem_u32(sA + s * L::A_BYTES), &tmA, cb, cc * 32, w0, h0, n,
+                                  static_cast<uint16_t>(tt), static_cast<uint16_t>(r));
+              tma2_load_2d(smem_u32(sB + s * L::B_BYTES), &tmB, cb, kb * kBK, n0 + rank * BH);
+            }
           }
         } else if (MODE == 2) {
           // stem forward: the M tile is output row (n, p); window of output q
@@ -229,9 +313,19 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             as[q4] = tap - ar[q4] * a.S;
             ++na;
           }
+          const int nbase = n0 + rank * BH;
           int nb = 0;
-          for (int j = 0; j < BN / 32; ++j)
-            if (n0 + 32 * j < a.Kout) ++nb;
+          for (int j = 0; j < BH / 32; ++j)
+            if (nbase + 32 * j < a.Kout) ++nb;
+          // the pair's total (leader's expect_tx): the other CTA's boxes
+          int pair_boxes = na + nb;
+          if constexpr (CG == 2) {
+            const int om0 = m0 + (rank == 0 ? kBM : -kBM), onb0 = n0 + (rank == 0 ? BH : 0);
+            for (int q4 = 0; q4 < 4; ++q4)
+              if (om0 + 32 * q4 < a.RSC) ++pair_boxes;
+            for (int j = 0; j < BH / 32; ++j)
+              if (onb0 + 32 * j < a.Kout) ++pair_boxes;
+          }
           for (int i = 0; i < nkb; ++i, ++g) {
             const int s = g % STAGES;
             if (g >= STAGES) mbar_wait(&empty[s], ((g / STAGES) - 1) & 1);
@@ -241,24 +335,34 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             const int p = static_cast<int>(a.fQ.div(pq));
             const int q = pq - p * a.Q;
             const int w0 = q * a.stride - a.pad, h0 = p * a.stride - a.pad;
-            mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>((na + nb) * 4096));
-            for (int q4 = 0; q4 < na; ++q4)
-              tma_load_im2col_4d(smem_u32(sA + s * L::A_BYTES + q4 * 4096), &tmA, &full[s], ac[q4], w0, h0, n,
-                                 static_cast<uint16_t>(as[q4]), static_cast<uint16_t>(ar[q4]));
-            for (int j = 0; j < nb; ++j)
-              tma_load_2d(smem_u32(sB + s * L::B_BYTES + j * 4096), &tmB, &full[s], n0 + 32 * j, pix);
+            if constexpr (CG == 1) {
+              mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>((na + nb) * 4096));
+              for (int q4 = 0; q4 < na; ++q4)
+                tma_load_im2col_4d(smem_u32(sA + s * L::A_BYTES + q4 * 4096), &tmA, &full[s], ac[q4], w0, h0, n,
+                                   static_cast<uint16_t>(as[q4]), static_cast<uint16_t>(ar[q4]));
+              for (int j = 0; j < nb; ++j)
+                tma_load_2d(smem_u32(sB + s * L::B_BYTES + j * 4096), &tmB, &full[s], nbase + 32 * j, pix);
+            } else {
+              if (rank == 0) mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(pair_boxes * 4096));
+              const uint32_t cb = mapa_u32(&full[s], 0);
+              for (int q4 = 0; q4 < na; ++q4)
+                tma2_load_im2col_4d(smem_u32(sA + s * L::A_BYTES + q4 * 4096), &tmA, cb, ac[q4], w0, h0, n,
+                                    static_cast<uint16_t>(as[q4]), static_cast<uint16_t>(ar[q4]));
+              for (int j = 0; j < nb; ++j)
+                tma2_load_2d(smem_u32(sB + s * L::B_BYTES + j * 4096), &tmB, cb, nbase + 32 * j, pix);
+            }
           }
         }
       }
     }
   } else if (warp == 5) {
-    if (lane == 0) {
-      // ---------------- MMA issuer ----------------
+    if (lane == 0 && rank == 0) {
+      // ---------------- MMA issuer (the pair leader for CG = 2) ----------------
       constexpr bool kMN = (MODE == 1 || MODE == 3);  // wgrad: both operands MN-major
-      constexpr uint32_t idesc = idesc_tf32(kBM, BN, kMN, kMN);
+      constexpr uint32_t idesc = idesc_tf32(kBM * CG, BN, kMN, kMN);
       uint32_t g = 0;
       int local = 0;
-      for (int t = blockIdx.x; t < tg.tiles; t += gridDim.x, ++local) {
+      for (int t = unit; t < tg.tiles; t += units, ++local) {
         int m0, n0, kb0, nkb, split;
         tile_coords(t, m0, n0, kb0, nkb, split);
         const int acc = local & 1;
@@ -282,11 +386,20 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
               ad = umma_desc(a0 + kk * 1024, 4096, 512, kLayoutSW128Base32);
               bd = umma_desc(b0 + kk * 1024, 4096, 512, kLayoutSW128Base32);
             }
-            umma_tf32(d, ad, bd, idesc, (i | kk) != 0 ? 1u : 0u);
+            if constexpr (CG == 1)
+              umma_tf32(d, ad, bd, idesc, (i | kk) != 0 ? 1u : 0u);
+            else
+              umma2_tf32(d, ad, bd, idesc, (i | kk) != 0 ? 1u : 0u);
           }
-          umma_commit(&empty[s]);
+          if constexpr (CG == 1)
+            umma_commit(&empty[s]);
+          else
+            umma2_commit(&empty[s]);
         }
-        umma_commit(&tfull[acc]);
+        if constexpr (CG == 1)
+          umma_commit(&tfull[acc]);
+        else
+          umma2_commit(&tfull[acc]);
       }
     }
   } else {
@@ -294,7 +407,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     const uint32_t row = warp * 32 + lane;
     int local = 0;
     uint32_t chunk_no = 0;  // store-staging double-buffer position
-    for (int t = blockIdx.x; t < tg.tiles; t += gridDim.x, ++local) {
+    const uint32_t tempty_leader[2] = {CG == 2 ? mapa_u32(&tempty[0], 0) : 0u, CG == 2 ? mapa_u32(&tempty[1], 0) : 0u};
+    for (int t = unit; t < tg.tiles; t += units, ++local) {
       int m0, n0, kb0, nkb, split;
       tile_coords(t, m0, n0, kb0, nkb, split);
       const int acc = local & 1;
@@ -397,14 +511,21 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      if constexpr (CG == 1)
+        mbar_arrive(&tempty[acc]);
+      else
+        mbar_arrive_cluster(tempty_leader[acc]);
     }
     if (threadIdx.x == 0) bulk_wait_all();
   }
   __syncthreads();
+  if constexpr (CG == 2) cluster_sync_all();  // no CTA leaves while its peer may still signal it
   if (warp == 5) {
     tc_fence_after();
-    tmem_dealloc(tmem, kCols);
+    if constexpr (CG == 1)
+      tmem_dealloc(tmem, kCols);
+    else
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols) : "memory");
   }
 }
 
@@ -484,36 +605,78 @@ int num_sms() {
   return n;
 }
 
-template <int BN, int MODE>
+template <int BN, int CG = 1>
+constexpr int stages_for2() {
+  // one persistent CTA per SM: as many stages as fit next to the 32 KB store staging
+  return (227 * 1024 - 2 * kBM * 128 - 3 * 1024) / (kBM * 128 + (BN / CG) * 128);
+}
+
+template <int BN, int MODE, int CG = 1>
 cudaError_t launch(const CUtensorMap& A, const CUtensorMap& B, const CUtensorMap& D, const TmaArgs& a,
                    const EpiArgs& e, int M, int N, int splits, cudaStream_t st) {
-  constexpr int STAGES = stages_for<BN>();
-  using L = TmaSmem<BN, STAGES>;
+  constexpr int STAGES = CG == 1 ? stages_for<BN>() : stages_for2<BN, CG>();
+  using L = TmaSmem<BN, STAGES, CG>;
   static_assert(L::TOTAL <= 227 * 1024, "shared memory budget");
-  auto kern = tc_conv_tma_kernel<BN, STAGES, MODE>;
+  auto kern = tc_conv_tma_kernel<BN, STAGES, MODE, CG>;
   static bool attr = false;
   if (!attr) {
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
     if (err != cudaSuccess) return err;
+    if (CG == 2) {
+      err = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
+      (void)err;
+    }
     attr = true;
   }
   TmaArgs args = a;
   const int kps = (a.num_kb + splits - 1) / splits;
   args.kb_per_split = kps;
   TileGrid tg;
-  tg.m_tiles = (M + kBM - 1) / kBM;
+  tg.m_tiles = (M + kBM * CG - 1) / (kBM * CG);
   tg.n_tiles = (N + BN - 1) / BN;
   tg.tiles = tg.m_tiles * tg.n_tiles * ((a.num_kb + kps - 1) / kps);
-  const int grid = std::min(tg.tiles, num_sms());
-  kern<<<grid, kTmaThreads, L::TOTAL, st>>>(A, B, D, args, e, tg);
-  return cudaGetLastError();
+  if constexpr (CG == 1) {
+    const int grid = std::min(tg.tiles, num_sms());
+    kern<<<grid, kTmaThreads, L::TOTAL, st>>>(A, B, D, args, e, tg);
+    return cudaGetLastError();
+  } else {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * std::min(tg.tiles, num_sms() / 2));
+    cfg.blockDim = dim3(kTmaThreads);
+    cfg.dynamicSmemBytes = L::TOTAL;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, A, B, D, args, e, tg);
+  }
 }
+
+// CTA pairs (SN_CONV_PAIRS=0 disables): MODE 0 always when the tile count
+// keeps the pairs busy; MODE 1 (wgrad, M = R*S*C) when 256-row tiles waste
+// no more than 128-row ones.
+// 0 off, 1 by size (default), 2 always (tests)
+int g_pairs = -1;
+int pairs_mode() {
+  if (g_pairs < 0) {
+    const char* v = std::getenv("SN_CONV_PAIRS");
+    g_pairs = (v && v[0] == '0') ? 0 : 1;
+  }
+  return g_pairs;
+}
+bool use_pairs(int64_t rows) { return pairs_mode() == 2 || (pairs_mode() == 1 && rows >= 2 * kBM * 148); }
 
 int bn_for(int n) { return n <= 64 ? 64 : (n <= 128 ? 128 : 256); }
 
 }  // namespace
 
 bool conv_tma_ok_fwd(const ConvShape& s) { return s.C % 32 == 0 && load_encoders(); }
+
+void set_conv_pairs(int mode) { g_pairs = mode; }
 
 int conv_fwd_stats_tiles(const ConvShape& s, bool stem, int* tile_rows) {
   if (stem) {
@@ -551,7 +714,9 @@ cudaError_t conv_fwd_tma(const ConvShape& s, const float* x, const float* w, con
                    CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
   const int Ktot = s.R * s.S * s.C;
-  if (!make_tiled(&B, w, s.K, Ktot, BN, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;
+  const int M = s.N * s.P * s.Q;
+  const int CG = use_pairs(M) ? 2 : 1;
+  if (!make_tiled(&B, w, s.K, Ktot, BN / CG, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;
   TmaArgs a{};
   a.num_kb = Ktot / kBK;
   a.cchunks = s.C / 32;
@@ -566,12 +731,18 @@ cudaError_t conv_fwd_tma(const ConvShape& s, const float* x, const float* w, con
   a.fS = FastDivT(s.S);
   a.fPQ = FastDivT(a.PQ);
   a.fQ = FastDivT(s.Q);
-  const int M = s.N * s.P * s.Q;
   CUtensorMap D;
   if (!make_store(&D, y, M, s.K, 0)) return cudaErrorInvalidValue;
   EpiArgs e{bias, s.K, 0, 0};
   e.M = M;
   e.stats = stats;
+  if (CG == 2) {
+    switch (BN) {
+      case 64: return launch<64, 0, 2>(A, B, D, a, e, M, s.K, 1, st);
+      case 128: return launch<128, 0, 2>(A, B, D, a, e, M, s.K, 1, st);
+      default: return launch<256, 0, 2>(A, B, D, a, e, M, s.K, 1, st);
+    }
+  }
   switch (BN) {
     case 64: return launch<64, 0>(A, B, D, a, e, M, s.K, 1, st);
     case 128: return launch<128, 0>(A, B, D, a, e, M, s.K, 1, st);
@@ -589,7 +760,9 @@ cudaError_t conv_dgrad_tma(const ConvShape& s, const float* dy, const float* wt_
                    CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
   const int Ktot = s.R * s.S * s.K;
-  if (!make_tiled(&B, wt_flip, s.C, Ktot, BN, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;
+  const int M = s.N * s.H * s.W;
+  const int CG = use_pairs(M) ? 2 : 1;
+  if (!make_tiled(&B, wt_flip, s.C, Ktot, BN / CG, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;
   TmaArgs a{};
   a.num_kb = Ktot / kBK;
   a.cchunks = s.K / 32;
@@ -604,10 +777,16 @@ cudaError_t conv_dgrad_tma(const ConvShape& s, const float* dy, const float* wt_
   a.fS = FastDivT(s.S);
   a.fPQ = FastDivT(a.PQ);
   a.fQ = FastDivT(s.W);
-  const int M = s.N * s.H * s.W;
   CUtensorMap D;
   if (!make_store(&D, dx, M, s.C, 0)) return cudaErrorInvalidValue;
   const EpiArgs e{nullptr, s.C, accumulate, 0};
+  if (CG == 2) {
+    switch (BN) {
+      case 64: return launch<64, 0, 2>(A, B, D, a, e, M, s.C, 1, st);
+      case 128: return launch<128, 0, 2>(A, B, D, a, e, M, s.C, 1, st);
+      default: return launch<256, 0, 2>(A, B, D, a, e, M, s.C, 1, st);
+    }
+  }
   switch (BN) {
     case 64: return launch<64, 0>(A, B, D, a, e, M, s.C, 1, st);
     case 128: return launch<128, 0>(A, B, D, a, e, M, s.C, 1, st);
@@ -986,6 +1165,16 @@ cudaError_t conv_wgrad_tma(const ConvShape& s, const float* x, const float* dy, 
   CUtensorMap D;
   if (!make_store(&D, partial, a.RSC, s.K, splits)) return cudaErrorInvalidValue;
   const EpiArgs e{nullptr, s.K, 0, 1};
+  // pairs when 256-row tiles cover R*S*C as tightly as 128-row ones
+  const bool pair = pairs_mode() == 2 ||
+                    (pairs_mode() == 1 && (a.RSC + 2 * kBM - 1) / (2 * kBM) * 2 == (a.RSC + kBM - 1) / kBM);
+  if (pair) {
+    switch (BN) {
+      case 64: return launch<64, 1, 2>(A, B, D, a, e, a.RSC, s.K, splits, st);
+      case 128: return launch<128, 1, 2>(A, B, D, a, e, a.RSC, s.K, splits, st);
+      default: return launch<256, 1, 2>(A, B, D, a, e, a.RSC, s.K, splits, st);
+    }
+  }
   switch (BN) {
     case 64: return launch<64, 1>(A, B, D, a, e, a.RSC, s.K, splits, st);
     case 128: return launch<128, 1>(A, B, D, a, e, a.RSC, s.K, splits, st);
@@ -993,4 +1182,95 @@ cudaError_t conv_wgrad_tma(const ConvShape& s, const float* x, const float* dy, 
   }
 }
 
+}  // namespace sn
+
+// ---------------------------------------------------------------------------
+// Probe (tests only): does a UMMA smem descriptor whose start address is
+// shifted by `shift` 128-byte rows inside a TMA-written SWIZZLE_128B tile read
+// the shifted matrix, with or without the descriptor's base-offset field?
+//   mn = 0: A K-major [256 rows][32 k];    D = A[shift : shift+128] . B^T
+//   mn = 1: A MN-major [40 k][128 m];      D[m][n] = sum_k A[k + shift][m] B[n][k]
+// B: K-major [64][32].  D: [128][64].
+namespace sn {
+namespace {
+__global__ void __launch_bounds__(128, 1) umma_shift_probe(const __grid_constant__ CUtensorMap tA,
+                                                           const __grid_constant__ CUtensorMap tB, float* D, int mn,
+                                                           int shift, int base_off) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;                 // 32 KB (K-major) or 4 x 5 KB (MN-major)
+  uint8_t* sB = smem + 32768;         // 8 KB
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 32768 + 8192);
+  uint64_t* mbar = bar + 1;
+  uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    mbar_init(mbar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc(slot, 64);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *slot;
+  if (threadIdx.x == 0) {
+    if (!mn) {
+      mbar_arrive_expect_tx(bar, 32768 + 8192);
+      tma_load_2d(smem_u32(sA), &tA, bar, 0, 0);
+    } else {
+      mbar_arrive_expect_tx(bar, 4 * 5120 + 8192);
+      for (int j = 0; j < 4; ++j) tma_load_2d(smem_u32(sA + j * 5120), &tA, bar, 32 * j, 0);
+    }
+    tma_load_2d(smem_u32(sB), &tB, bar, 0, 0);
+    mbar_wait(bar, 0);
+    tc_fence_after();
+    const uint32_t idesc = idesc_tf32(128, 64, mn != 0, false);
+    for (int kk = 0; kk < 4; ++kk) {
+      uint64_t ad;
+      uint32_t start;
+      if (!mn) {
+        start = smem_u32(sA) + shift * 128 + kk * 32;
+        ad = umma_desc(start, 16, 1024, kLayoutSW128);
+      } else {
+        start = smem_u32(sA) + shift * 128 + kk * 1024;
+        ad = umma_desc(start, 5120, 512, kLayoutSW128Base32);
+      }
+      if (base_off) ad |= static_cast<uint64_t>((start >> 7) & 7u) << 49;
+      const uint64_t bd = umma_desc(smem_u32(sB) + kk * 32, 16, 1024, kLayoutSW128);
+      umma_tf32(tmem, ad, bd, idesc, kk ? 1u : 0u);
+    }
+    umma_commit(mbar);
+  }
+  __syncwarp();
+  mbar_wait(mbar, 0);
+  tc_fence_after();
+  for (int c = 0; c < 64; c += 32) {
+    float v[32];
+    tmem_ld32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c, v);
+    for (int j = 0; j < 32; ++j) D[(warp * 32 + lane) * 64 + c + j] = v[j];
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, 64);
+}
+}  // namespace
+
+int umma_shift_probe_run(const float* A, const float* B, float* D, int mn, int shift, int base_off) {
+  if (!load_encoders()) return 1;
+  CUtensorMap tA, tB;
+  bool ok;
+  if (!mn) {
+    ok = make_tiled(&tA, A, 256, 32, 256, CU_TENSOR_MAP_SWIZZLE_128B);
+  } else {
+    ok = make_tiled(&tA, A, 40, 128, 40, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  }
+  ok = ok && make_tiled(&tB, B, 64, 32, 64, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (!ok) return 2;
+  const int smem = 32768 + 8192 + 64 + 1024;
+  cudaFuncSetAttribute(umma_shift_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  umma_shift_probe<<<1, 128, smem>>>(tA, tB, D, mn, shift, base_off);
+  if (cudaGetLastError() != cudaSuccess) return 3;
+  return cudaDeviceSynchronize() == cudaSuccess ? 0 : 4;
+}
 }  // namespace sn

@@ -58,6 +58,9 @@ extern "C" int sn_test_effective_splits(int K, int splits) { return sn::effectiv
 //   op 0 forward:  p = {x, w, bias, y}
 //   op 1 dgrad:    p = {dy, w, wt_scratch, dx}, flag = accumulate
 //   op 2 wgrad:    p = {x, dy, dw, db, partial, red_scratch}, flag = splits (<=0: auto)
+static int g_test_sync = 1;  // 0: sn_test_conv returns after the launch (timing loops)
+extern "C" void sn_test_set_sync(int on) { g_test_sync = on; }
+
 extern "C" int sn_test_conv(int op, const int* shape, void** p, int flag) {
   sn::ConvShape s{shape[0], shape[1], shape[2], shape[3], shape[4], shape[5], shape[6],
                   shape[7], shape[8], shape[9], shape[10]};
@@ -72,6 +75,7 @@ extern "C" int sn_test_conv(int op, const int* shape, void** p, int flag) {
                        splits, (float*)p[5], 0);
   }
   if (e != cudaSuccess) return 4;
+  if (!g_test_sync) return 0;
   return cudaDeviceSynchronize() == cudaSuccess ? 0 : 4;
 }
 
@@ -115,6 +119,7 @@ extern "C" int sn_test_tma_overlap(const float* base) { return sn::tma_probe_ove
 
 // 1: TMA-fed conv kernels where the shape allows (default), 0: cp.async gathers.
 extern "C" void sn_test_set_conv_tma(int on) { sn::set_conv_tma(on); }
+extern "C" void sn_test_set_conv_pairs(int mode) { sn::set_conv_pairs(mode); }
 
 // Pool layer kernels on caller buffers.  shape = {N,H,W,C,P,Q,K,stride,pad,mode}.
 //   op 0 forward:  p = {x, y}
@@ -131,4 +136,11 @@ extern "C" long long sn_test_pool(int op, const int* shape, void** p, int flag) 
     e = sn::pool_bwd(s, (const float*)p[0], (const float*)p[1], (const float*)p[2], (float*)p[3], flag, p[4], 0);
   if (e != cudaSuccess) return 4;
   return cudaDeviceSynchronize() == cudaSuccess ? 0 : 4;
+}
+
+namespace sn {
+int umma_shift_probe_run(const float* A, const float* B, float* D, int mn, int shift, int base_off);
+}
+extern "C" int sn_test_umma_shift(const float* A, const float* B, float* D, int mn, int shift, int base_off) {
+  return sn::umma_shift_probe_run(A, B, D, mn, shift, base_off);
 }

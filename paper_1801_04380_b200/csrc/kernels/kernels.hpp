@@ -64,6 +64,9 @@ bool conv_tma_ok_dgrad_strided(const ConvShape& s);
 cudaError_t conv_dgrad_strided_tma(const ConvShape& s, const float* dy, const float* w, float* wt_scratch, float* dx,
                                    int accumulate, cudaStream_t st);
 void set_conv_tma(int on);
+// CTA-pair (cta_group::2) conv kernels: 0 off, 1 when the shape keeps the
+// pairs busy (default; env SN_CONV_PAIRS=0 turns them off), 2 always (tests).
+void set_conv_pairs(int mode);
 bool use_tma();
 
 // FC: x[B][I], w[O][I], y[B][O]

@@ -98,6 +98,8 @@ CONV_CASES = [
     (2, 64, 15, 15, 128, 3, 2, 1),   # odd extent, stride 2 (uneven phases)
     (2, 32, 16, 16, 64, 1, 2, 0),    # 1x1 stride 2: phases without taps
     (1, 64, 23, 23, 96, 5, 3, 2),    # stride 3, 5x5
+    (2, 128, 8, 8, 512, 3, 1, 1),    # K = 512: two N tiles of 256
+    (32, 64, 28, 28, 64, 3, 1, 1),   # several 256-row tiles per CTA pair (double-buffered TMEM)
 ]
 
 
@@ -117,12 +119,15 @@ def _shape_arr(N, C, H, W, K, k, s, p):
     return (ctypes.c_int * 11)(N, H, W, C, K, k, k, P, Q, s, p), P, Q
 
 
-@pytest.mark.parametrize("tma", [1, 0])
+@pytest.mark.parametrize("tma,pairs", [(1, 1), (1, 2), (0, 1)])
 @pytest.mark.parametrize("case", CONV_CASES)
-def test_conv_fwd_dgrad_wgrad(cuda, case, tma):
+def test_conv_fwd_dgrad_wgrad(cuda, case, tma, pairs):
+    """pairs=2 forces the CTA-pair (cta_group::2, M = 256) TMA kernels on
+    every shape (odd tile counts, rows past M in the peer CTA)."""
     N, C, H, W, K, k, s, p = case
     lib = _conv_lib()
     lib.sn_test_set_conv_tma(tma)
+    lib.sn_test_set_conv_pairs(pairs)
     shape, P, Q = _shape_arr(*case)
     g = torch.Generator().manual_seed(sum(case))
     x = torch.randn(N, C, H, W, generator=g)
@@ -162,6 +167,7 @@ def test_conv_fwd_dgrad_wgrad(cuda, case, tma):
         _check(dw_d.permute(0, 3, 1, 2).cpu(), wd.grad, N * P * Q)
         _check(db_d.cpu(), bd.grad, N * P * Q)
     lib.sn_test_set_conv_tma(1)
+    lib.sn_test_set_conv_pairs(1)
 
 
 def test_tma_overlapping_window_probe(cuda):

@@ -266,10 +266,12 @@ def test_reassociating_fusions(cuda, monkeypatch):
     """BN statistics combined from the CONV epilogue's per-tile partials
     (shifted sums per 128-row tile, fp64 combination) and the CONV bias
     gradient summed in the BN backward's dx pass match the separate reduction
-    passes to fp32 rounding.  On a smooth net (no ReLU / max-pool masks that a
-    last-bit change can flip): loss rel. 1e-5, weight / BN gradients rel. 1e-4,
-    CONV biases (analytically zero before a BN, so pure rounding noise) abs.
-    1e-4 of the largest weight gradient.  The fused run is deterministic
+    passes to rounding.  On a smooth net (no ReLU / max-pool masks that a
+    last-bit change can flip); a last-bit change of a BN output can still move
+    its tf32 rounding in the next CONV (1 tf32 ulp = 2^-11 relative), so:
+    loss rel. 1e-4, weight / BN gradients rel. 2e-3 (a wrong statistic or bias
+    sum is off by O(1)); CONV biases (analytically zero before a BN, so pure
+    rounding noise) abs. 2e-3 of the largest weight gradient.  The fused run is deterministic
     (bit-identical on repeat), also on ResNet-50g-style blocks."""
     from paper_1801_04380_b200.netgen import gen_resnet
     from paper_1801_04380_b200.training import init_parameters
@@ -289,13 +291,13 @@ def test_reassociating_fusions(cuda, monkeypatch):
     monkeypatch.setenv("SN_FUSE_REASSOC", "0")
     loss0, grads0, _, t0 = _run(net, 8, 1 << 30, ALL, params, images, labels)
     assert t.kernels < t0.kernels
-    assert abs(loss - loss0) <= 1e-5 * abs(loss0)
+    assert abs(loss - loss0) <= 1e-4 * abs(loss0)
     kinds = {l.id: l.kind.name for l in net.layers}
     worst = max(relative_error(grads[l]["w"], grads0[l]["w"]) for l in grads)
-    assert worst <= 1e-4, worst
+    assert worst <= 2e-3, worst
     scale = max(float(grads0[l]["w"].abs().max()) for l in grads)
     for l in grads:
         if kinds[l] == "CONV" and kinds[net.layers[l].next[0]] == "BN":
-            assert float((grads[l]["b"] - grads0[l]["b"]).abs().max()) <= 1e-4 * scale, net.layers[l].name
+            assert float((grads[l]["b"] - grads0[l]["b"]).abs().max()) <= 2e-3 * scale, net.layers[l].name
         else:
-            assert relative_error(grads[l]["b"], grads0[l]["b"]) <= 1e-4, net.layers[l].name
+            assert relative_error(grads[l]["b"], grads0[l]["b"]) <= 2e-3, net.layers[l].name
