@@ -80,7 +80,7 @@ def build_exec(force: bool = False) -> Path:
     plan = build_planner(force)
     out = LIB / "libsnexec.so"
     srcs = _sources("exec", (".cu", ".cpp")) + _sources("kernels", (".cu",))
-    headers = (_sources("exec", (".cuh", ".hpp", ".h")) + _sources("kernels", (".cuh", ".h"))
+    headers = (_sources("exec", (".cuh", ".hpp", ".h")) + _sources("kernels", (".cuh", ".h", ".hpp"))
                + _sources("planner", (".hpp",)) + sorted(INCLUDE.glob("*.h")))
     flags = ["-O3", "-std=c++17", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC",
              "-Xcompiler", "-ffp-contract=off", "--expt-relaxed-constexpr"]
@@ -89,11 +89,11 @@ def build_exec(force: bool = False) -> Path:
         return out
     objdir = LIB / "obj"
     objdir.mkdir(exist_ok=True)
-    objs = []
-    for src in srcs:
-        obj = objdir / (src.stem + ".o")
-        _run([NVCC, *flags, f"-I{INCLUDE}", f"-I{CSRC}", "-c", str(src), "-o", str(obj)])
-        objs.append(str(obj))
+    objs = [str(objdir / (src.stem + ".o")) for src in srcs]
+    import concurrent.futures as cf
+    with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as pool:
+        list(pool.map(lambda so: _run([NVCC, *flags, f"-I{INCLUDE}", f"-I{CSRC}", "-c", str(so[0]), "-o", so[1]]),
+                      zip(srcs, objs)))
     _run([NVCC, *ARCH, "-shared", *objs, "-o", str(out), f"-L{LIB}", "-lsnplan",
           "-Xlinker", "-rpath,$ORIGIN"])
     _stamp(out, digest)

@@ -280,7 +280,7 @@ void alloc_device(sn_exec* ex) {
     LayerRt& l = ex->L[i];
     if (l.kind != snp::CONV) continue;
     l.stats_tiles = sn::conv_fwd_stats_tiles(l.conv, i == ex->stem_layer, &l.stats_rows);
-    tstats = std::max(tstats, static_cast<int64_t>(l.stats_tiles) * 3 * l.C);
+    tstats = std::max(tstats, static_cast<int64_t>(l.stats_tiles) * 4 * l.C);
   }
   ck(cudaMalloc(&ex->tstats, tstats * sizeof(float)), "cudaMalloc(tile stats)");
   ex->partial_cap = std::max<int64_t>(partial, 64);

@@ -1,0 +1,449 @@
+// Halo-tiled implicit-GEMM convolution (stride 1) on tcgen05/TMEM.
+//
+// The im2col kernels (conv_tma.cu) load every input pixel once per filter tap
+// (R*S times) from L2; on B200 those kernels are bound by the L2 -> SMEM
+// operand traffic (~12 TB/s chip-wide), not by the tensor cores.  Here the
+// output is enumerated on the *padded* grid: output position m = (n, y, x'),
+// x' in [0, Wp) with Wp = W + 2*pad, of which x' < Q are real (the rest are
+// junk rows of the GEMM, clipped by the TMA store).  On that grid every tap
+// (r, s) is a uniform shift of r*Wp + s rows, so one TMA box per 32-channel
+// chunk -- TR*MT + R - 1 padded input rows x Wp columns, zero-filled out of
+// range -- serves all R*S taps: the UMMA A descriptor simply starts r*Wp + s
+// rows into the halo (the SWIZZLE_128B pattern is a function of the absolute
+// shared-memory address, so any 128-byte row offset is a valid operand start;
+// tools/umma_shift_probe.py).
+//
+// One persistent CTA per SM walks tiles (n, band of TR*MT output rows, BN
+// output channels); MT sub-tiles of TR rows (TR*Wp <= 128 GEMM rows each) share
+// every weight tile, so a weight k-block feeds MT MMAs.  Two operand rings:
+// halos (one per channel chunk) and weight tiles (one per tap and chunk).
+// Warp roles as in conv_tma.cu: warp 4 = TMA producer, warp 5 = MMA issuer,
+// warps 0-3 = epilogue (TMEM -> regs (+bias, +BN statistics) -> smem -> TMA
+// store of a {32 ch, Wp, TR} box, columns >= Q and rows >= P clipped).
+//
+// Dgrad (stride 1) runs the same kernel over dy with the flipped, transposed
+// filter and padding R-1-pad.
+#include <cuda.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "gemm_tc.cuh"
+#include "kernels.hpp"
+#include "tma_host.hpp"
+
+namespace sn {
+namespace {
+
+constexpr int kHaloThreads = 192;
+
+struct HaloArgs {
+  int Wp, TR, MT, R, S, pad, P, Q, cchunks, bands, n_tiles, tiles;
+  int halo_rows;       // TR*MT + R - 1
+  uint32_t halo_bytes; // TMA bytes of one halo box
+  uint32_t halo_slot;  // smem stride between halo ring slots (1024-aligned, with read slack)
+  const float* bias;
+  int N;               // output channels (valid columns)
+  int reduce;          // dgrad accumulate: TMA reduce-add store
+  float* stats;        // BN statistics per sub-tile: [tile*MT + j][4][N] {shift, S1, S2, count}
+};
+
+template <int BN, int MT, int HST, int BST>
+struct HaloSmem {
+  static constexpr int B_BYTES = BN * 128;
+  static constexpr int EPI_BYTES = 2 * kBM * 128;
+  // halo ring first (dynamic size), then the fixed tail
+  static constexpr int tail() { return BST * B_BYTES + EPI_BYTES + 512 + 1024; }
+};
+
+template <int BN, int MT, int HST, int BST>
+__global__ void __launch_bounds__(kHaloThreads, 1)
+    tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
+                        const __grid_constant__ CUtensorMap tmY, HaloArgs a) {
+  using L = HaloSmem<BN, MT, HST, BST>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sH = smem;                                   // HST halo slots
+  uint8_t* sB = smem + HST * a.halo_slot;               // BST weight tiles
+  uint8_t* sEpi = sB + BST * L::B_BYTES;                // 2 x 16 KB store staging
+  uint64_t* hfull = reinterpret_cast<uint64_t*>(sEpi + L::EPI_BYTES);
+  uint64_t* hempty = hfull + HST;
+  uint64_t* bfull = hempty + HST;
+  uint64_t* bempty = bfull + BST;
+  uint64_t* tfull = bempty + BST;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* sred = reinterpret_cast<float*>(tmem_slot + 4);  // [4 warps][32][2]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr uint32_t kCols = tmem_cols<2 * MT * BN>();
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < HST; ++i) {
+      mbar_init(&hfull[i], 1);
+      mbar_init(&hempty[i], 1);
+    }
+    for (int i = 0; i < BST; ++i) {
+      mbar_init(&bfull[i], 1);
+      mbar_init(&bempty[i], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 128);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 5) tmem_alloc(tmem_slot, kCols);
+  if (warp == 4 && lane == 0) {
+    tma_prefetch(&tmX);
+    tma_prefetch(&tmW);
+    tma_prefetch(&tmY);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int taps = a.R * a.S;
+
+  // tile t -> (image n, band b, output-channel tile nt); band = TR*MT output rows
+  auto coords = [&](int t, int& n, int& y0, int& n0) {
+    const int nt = t % a.n_tiles;
+    const int rest = t / a.n_tiles;
+    const int b = rest % a.bands;
+    n = rest / a.bands;
+    y0 = b * a.TR * MT;
+    n0 = nt * BN;
+  };
+
+  if (warp == 4) {
+    {
+      // ---------------- TMA producer (whole warp; the elected lane issues) ----------------
+      uint32_t hs = 0, hph = 0, bs = 0, bph = 0;
+      bool hwrap = false, bwrap = false;  // ring slots reused: wait for their release
+      for (int t = blockIdx.x; t < a.tiles; t += gridDim.x) {
+        int n, y0, n0;
+        coords(t, n, y0, n0);
+        for (int cc = 0; cc < a.cchunks; ++cc) {
+          if (hwrap) mbar_wait(&hempty[hs], hph ^ 1);
+          if (elect_one()) {
+            mbar_arrive_expect_tx(&hfull[hs], a.halo_bytes);
+            tma_load_4d(smem_u32(sH + hs * a.halo_slot), &tmX, &hfull[hs], cc * 32, -a.pad, y0 - a.pad, n);
+          }
+          __syncwarp();
+          if (++hs == HST) {
+            hs = 0;
+            hph ^= 1;
+            hwrap = true;
+          }
+          for (int tap = 0; tap < taps; ++tap) {
+            if (bwrap) mbar_wait(&bempty[bs], bph ^ 1);
+            if (elect_one()) {
+              mbar_arrive_expect_tx(&bfull[bs], L::B_BYTES);
+              tma_load_2d(smem_u32(sB + bs * L::B_BYTES), &tmW, &bfull[bs], (tap * a.cchunks + cc) * 32, n0);
+            }
+            __syncwarp();
+            if (++bs == BST) {
+              bs = 0;
+              bph ^= 1;
+              bwrap = true;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 5) {
+    {
+      // ---------------- MMA issuer (whole warp; the elected lane issues) ----------------
+      constexpr uint32_t idesc = idesc_tf32(kBM, BN, false, false);
+      // lean issue loop (see conv_tma.cu): base descriptors + offsets in 16-byte units
+      const uint64_t hdesc0 = umma_desc(smem_u32(sH), 16, 1024, kLayoutSW128);
+      const uint64_t bdesc0 = umma_desc(smem_u32(sB), 16, 1024, kLayoutSW128);
+      const uint32_t jstep = static_cast<uint32_t>(a.TR * a.Wp) * 8u;  // sub-tile rows * 128 B / 16
+      uint32_t hs = 0, hph = 0, bs = 0, bph = 0;
+      int local = 0;
+      for (int t = blockIdx.x; t < a.tiles; t += gridDim.x, ++local) {
+        const int acc = local & 1;
+        if (local >= 2) mbar_wait(&tempty[acc], ((local >> 1) - 1) & 1);
+        tc_fence_after();
+        const uint32_t d0 = tmem + static_cast<uint32_t>(acc * MT * BN);
+        for (int cc = 0; cc < a.cchunks; ++cc) {
+          mbar_wait(&hfull[hs], hph);
+          const uint64_t h0 = hdesc0 + hs * (a.halo_slot >> 4);
+          int r = 0, sx = 0;
+          for (int tap = 0; tap < taps; ++tap) {
+            mbar_wait(&bfull[bs], bph);
+            tc_fence_after();
+            const uint64_t ad = h0 + static_cast<uint32_t>(r * a.Wp + sx) * 8u;
+            const uint64_t bd = bdesc0 + bs * (L::B_BYTES >> 4);
+            const uint32_t first = (cc | tap) != 0 ? 1u : 0u;
+            if (elect_one()) {
+              // sub-tiles innermost: consecutive MMAs feed different accumulators
+#pragma unroll
+              for (int kk = 0; kk < kBK / 8; ++kk)
+#pragma unroll
+                for (int j = 0; j < MT; ++j)
+                  umma_tf32(d0 + j * BN, ad + j * jstep + kk * 2, bd + kk * 2, idesc, kk ? 1u : first);
+              umma_commit(&bempty[bs]);
+            }
+            __syncwarp();
+            if (++bs == BST) {
+              bs = 0;
+              bph ^= 1;
+            }
+            if (++sx == a.S) {
+              sx = 0;
+              ++r;
+            }
+          }
+          if (elect_one()) umma_commit(&hempty[hs]);
+          __syncwarp();
+          if (++hs == HST) {
+            hs = 0;
+            hph ^= 1;
+          }
+        }
+        if (elect_one()) umma_commit(&tfull[acc]);
+        __syncwarp();
+      }
+    }
+  } else {
+    // ---------------- epilogue (warps 0-3 own TMEM lanes 32w..32w+31) ----------------
+    const uint32_t row = warp * 32 + lane;
+    int local = 0;
+    uint32_t chunk_no = 0;
+    for (int t = blockIdx.x; t < a.tiles; t += gridDim.x, ++local) {
+      int n, y0, n0;
+      coords(t, n, y0, n0);
+      const int acc = local & 1;
+      mbar_wait(&tfull[acc], (local >> 1) & 1);
+      tc_fence_after();
+      for (int j = 0; j < MT; ++j) {
+        const int ys = y0 + j * a.TR;  // first output row of the sub-tile
+        const uint32_t tbase = tmem + static_cast<uint32_t>(acc * MT * BN + j * BN) +
+                               (static_cast<uint32_t>(warp * 32) << 16);
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32, ++chunk_no) {
+          if (n0 + c >= a.N) break;
+          float v[32];
+          tmem_ld32(tbase + static_cast<uint32_t>(c), v);
+          if (a.bias) {
+#pragma unroll
+            for (int q = 0; q < 32; ++q)
+              if (n0 + c + q < a.N) v[q] += __ldg(a.bias + n0 + c + q);
+          }
+          const uint32_t buf = smem_u32(sEpi) + (chunk_no & 1u) * (kBM * 128);
+          if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          named_bar(1, 128);
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(buf + sw128_off(row, q)), "f"(v[4 * q]),
+                         "f"(v[4 * q + 1]), "f"(v[4 * q + 2]), "f"(v[4 * q + 3])
+                         : "memory");
+          fence_proxy_async();
+          named_bar(1, 128);
+          if (threadIdx.x == 0) {
+            if (a.reduce)
+              asm volatile(
+                  "cp.reduce.async.bulk.tensor.4d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3, %4, %5}], "
+                  "[%1];" ::"l"(reinterpret_cast<uint64_t>(&tmY)),
+                  "r"(buf), "r"(n0 + c), "r"(0), "r"(ys), "r"(n)
+                  : "memory");
+            else
+              tma_store_4d(&tmY, buf, n0 + c, 0, ys, n);
+            bulk_commit();
+          }
+          if (a.stats) {
+            // column `lane` of the staged chunk over this warp's rows; invalid
+            // (junk) rows are skipped; shift = the sub-tile's row 0 (always real
+            // unless the whole sub-tile lies past P, then count = 0)
+            const uint8_t* sb = sEpi + (chunk_no & 1u) * (kBM * 128);
+            const uint32_t cq = static_cast<uint32_t>(lane) >> 2, cr = (static_cast<uint32_t>(lane) & 3u) * 4;
+            const float shift = *reinterpret_cast<const float*>(sb + sw128_off(0, cq) + cr);
+            float s1 = 0.f, s2 = 0.f;
+            for (int rr = 32 * warp; rr < 32 * warp + 32; ++rr) {
+              const int xx = rr % a.Wp, yy = rr / a.Wp;
+              if (yy >= a.TR || xx >= a.Q || ys + yy >= a.P) continue;
+              const float d = *reinterpret_cast<const float*>(sb + sw128_off(rr, cq) + cr) - shift;
+              s1 += d;
+              s2 = fmaf(d, d, s2);
+            }
+            sred[(warp * 32 + lane) * 2] = s1;
+            sred[(warp * 32 + lane) * 2 + 1] = s2;
+            named_bar(1, 128);
+            if (warp == 0 && n0 + c + lane < a.N) {
+              float t1 = sred[lane * 2], t2 = sred[lane * 2 + 1];
+              for (int w = 1; w < 4; ++w) {
+                t1 += sred[(w * 32 + lane) * 2];
+                t2 += sred[(w * 32 + lane) * 2 + 1];
+              }
+              const int rows_valid = max(0, min(a.TR, a.P - ys)) * a.Q;
+              const size_t tile = (static_cast<size_t>(t / a.n_tiles) * MT + j);
+              float* out = a.stats + tile * 4 * a.N + n0 + c + lane;
+              out[0] = shift;
+              out[a.N] = t1;
+              out[2 * static_cast<size_t>(a.N)] = t2;
+              out[3 * static_cast<size_t>(a.N)] = static_cast<float>(rows_valid);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+    }
+    if (threadIdx.x == 0) bulk_wait_all();
+  }
+  __syncthreads();
+  if (warp == 5) {
+    tc_fence_after();
+    tmem_dealloc(tmem, kCols);
+  }
+}
+
+int num_sms_h() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+  }
+  return n;
+}
+
+// Geometry for a stride-1 conv over an [N][H][W][C] input with R x S filter and
+// padding pad (output P x Q): TR rows per 128-row sub-tile, MT sub-tiles.
+struct HaloGeom {
+  int Wp, TR, MT, halo_rows;
+  uint32_t halo_bytes, halo_slot;
+};
+
+template <int BN, int MT>
+bool halo_geom(int H, int W, int R, int S, int pad, int P, HaloGeom* g) {
+  g->Wp = W + 2 * pad;
+  if (g->Wp > kBM || g->Wp > 256) return false;
+  g->TR = std::min(kBM / g->Wp, P);
+  g->MT = MT;
+  g->halo_rows = g->TR * MT + R - 1;
+  if (g->halo_rows > 256) return false;
+  g->halo_bytes = static_cast<uint32_t>(g->halo_rows) * g->Wp * 128;
+  // the last sub-tile's junk GEMM rows (TR*Wp .. 127) read past the halo box
+  const int over = std::max(0, kBM + S - g->TR * g->Wp);
+  const uint32_t need = g->halo_bytes + static_cast<uint32_t>(over) * 128;
+  g->halo_slot = (need + 1023) / 1024 * 1024;
+  (void)H;
+  return true;
+}
+
+template <int BN, int MT, int HST, int BST>
+cudaError_t launch_halo(const CUtensorMap& X, const CUtensorMap& Wm, const CUtensorMap& Y, HaloArgs a,
+                        const HaloGeom& g, cudaStream_t st) {
+  using L = HaloSmem<BN, MT, HST, BST>;
+  const int smem = static_cast<int>(HST * g.halo_slot) + L::tail();
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  auto kern = tc_conv_halo_kernel<BN, MT, HST, BST>;
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (err != cudaSuccess) return err;
+  const int grid = std::min(a.tiles, num_sms_h());
+  kern<<<grid, kHaloThreads, smem, st>>>(X, Wm, Y, a);
+  return cudaGetLastError();
+}
+
+// Variant table: (BN, MT, halo stages, weight stages) fitting 227 KB.
+template <int BN, int MT, int HST, int BST>
+bool halo_fits(const HaloGeom& g) {
+  return static_cast<int>(HST * g.halo_slot) + HaloSmem<BN, MT, HST, BST>::tail() <= 227 * 1024;
+}
+
+}  // namespace
+
+// Which variant a shape runs (0: none).  Stride 1, C % 32 == 0, K % 32 == 0,
+// padded rows fit one 128-row sub-tile, and the im2col kernel would re-read
+// the input R*S > 1 times.
+int g_halo = -1;  // 0 off, 1 by shape (default; env SN_CONV_HALO=0 turns it off), 2 whenever legal (tests)
+int halo_mode() {
+  if (g_halo < 0) {
+    const char* v = std::getenv("SN_CONV_HALO");
+    g_halo = (v && v[0] == '0') ? 0 : 1;
+  }
+  return g_halo;
+}
+
+int conv_halo_variant(int N, int H, int W, int C, int K, int R, int S, int pad, int P, int Q) {
+  if (halo_mode() == 0 || C % 32 != 0 || K % 32 != 0 || R * S <= 1 || !tma_encoders_ok()) return 0;
+  if (P != H + 2 * pad - R + 1 || Q != W + 2 * pad - S + 1 || pad < 0) return 0;
+  // by shape: real output rows must fill >= 3/4 of each 128-row sub-tile, and
+  // the im2col kernel is L2-bound (K <= 64: its weight tile feeds one 64-wide
+  // MMA per k block; tools/conv_bench.py: 165 -> 149 us on ResNet stage 1,
+  // while at K >= 128 the im2col kernel is faster)
+  const int Wp = W + 2 * pad;
+  if (halo_mode() == 1 && (Wp > kBM || std::min(kBM / Wp, P) * Q * 4 < 3 * kBM || K > 64)) return 0;
+  HaloGeom g;
+  const int bn = K <= 64 ? 64 : (K <= 128 ? 128 : 256);
+  if (bn == 64) {
+    if (!halo_geom<64, 3>(H, W, R, S, pad, P, &g) || !halo_fits<64, 3, 2, 8>(g)) return 0;
+    return 1;
+  }
+  if (bn == 128) {
+    if (!halo_geom<128, 2>(H, W, R, S, pad, P, &g) || !halo_fits<128, 2, 2, 6>(g)) return 0;
+    return 2;
+  }
+  if (!halo_geom<256, 1>(H, W, R, S, pad, P, &g) || !halo_fits<256, 1, 2, 4>(g)) return 0;
+  return 3;
+}
+
+int conv_halo_stats_tiles(int N, int H, int W, int C, int K, int R, int S, int pad, int P, int Q) {
+  const int v = conv_halo_variant(N, H, W, C, K, R, S, pad, P, Q);
+  if (!v) return 0;
+  const int MT = v == 1 ? 3 : (v == 2 ? 2 : 1);
+  const int Wp = W + 2 * pad;
+  const int TR = std::min(kBM / Wp, P);
+  const int bands = (P + TR * MT - 1) / (TR * MT);
+  return N * bands * MT;
+}
+
+// y[N][P][Q][K] (+)= conv(x[N][H][W][C], w[K][R][S][C]) + bias, stride 1.
+cudaError_t conv_halo(int N, int H, int W, int C, int K, int R, int S, int pad, int P, int Q, const float* x,
+                      const float* w, const float* bias, float* y, int accumulate, float* stats, cudaStream_t st) {
+  const int v = conv_halo_variant(N, H, W, C, K, R, S, pad, P, Q);
+  if (!v) return cudaErrorInvalidValue;
+  HaloGeom g;
+  const int BN = v == 1 ? 64 : (v == 2 ? 128 : 256);
+  const int MT = v == 1 ? 3 : (v == 2 ? 2 : 1);
+  if (v == 1) halo_geom<64, 3>(H, W, R, S, pad, P, &g);
+  else if (v == 2) halo_geom<128, 2>(H, W, R, S, pad, P, &g);
+  else halo_geom<256, 1>(H, W, R, S, pad, P, &g);
+  CUtensorMap X, Wm, Y;
+  if (!tma_map_nhwc(&X, x, N, H, W, C, g.Wp, g.halo_rows, 0)) return cudaErrorInvalidValue;
+  if (!tma_map_2d(&Wm, w, K, static_cast<int64_t>(R) * S * C, BN, 0)) return cudaErrorInvalidValue;
+  if (!tma_map_nhwc(&Y, y, N, P, Q, K, g.Wp, g.TR, 0)) return cudaErrorInvalidValue;
+  HaloArgs a{};
+  a.Wp = g.Wp;
+  a.TR = g.TR;
+  a.MT = MT;
+  a.R = R;
+  a.S = S;
+  a.pad = pad;
+  a.P = P;
+  a.Q = Q;
+  a.cchunks = C / 32;
+  a.bands = (P + g.TR * MT - 1) / (g.TR * MT);
+  a.n_tiles = (K + BN - 1) / BN;
+  a.tiles = N * a.bands * a.n_tiles;
+  a.halo_rows = g.halo_rows;
+  a.halo_bytes = g.halo_bytes;
+  a.halo_slot = g.halo_slot;
+  a.bias = bias;
+  a.N = K;
+  a.reduce = accumulate;
+  a.stats = stats;
+  switch (v) {
+    case 1: return launch_halo<64, 3, 2, 8>(X, Wm, Y, a, g, st);
+    case 2: return launch_halo<128, 2, 2, 6>(X, Wm, Y, a, g, st);
+    default: return launch_halo<256, 1, 2, 4>(X, Wm, Y, a, g, st);
+  }
+}
+
+}  // namespace sn
+
+namespace sn {
+void set_conv_halo(int mode) { g_halo = mode; }
+}  // namespace sn

@@ -25,6 +25,7 @@
 
 #include "gemm_tc.cuh"
 #include "kernels.hpp"
+#include "tma_host.hpp"
 
 namespace sn {
 namespace {
@@ -223,8 +224,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   constexpr int BH = BN / CG;  // B columns staged by this CTA
 
   if (warp == 4) {
-    if (lane == 0) {
-      // ---------------- TMA producer ----------------
+    {
+      // ---------------- TMA producer (whole warp, elected lane issues) ----------------
       uint32_t g = 0;  // k blocks issued by this CTA (stage ring position)
       for (int t = unit; t < tg.tiles; t += units) {
         int m0, n0, kb0, nkb, split;
@@ -243,6 +244,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             const int cc = kb - tap * a.cchunks;
             const int r = static_cast<int>(a.fS.div(tap));
             const int tt = tap - r * a.S;
+            if (elect_one()) {
             if constexpr (CG == 1) {
               mbar_arrive_expect_tx(&full[s], L::A_BYTES + L::B_BYTES);
               tma_load_im2col_4d(smem_u32(sA + s * L::A_BYTES), &tmA, &full[s], cc * 32, w0, h0, n,
@@ -256,6 +258,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
                                   static_cast<uint16_t>(tt), static_cast<uint16_t>(r));
               tma2_load_2d(smem_u32(sB + s * L::B_BYTES), &tmB, cb, kb * kBK, n0 + rank * BH);
             }
+            }
+            __syncwarp();
           }
         } else if (MODE == 2) {
           // stem forward: the M tile is output row (n, p); window of output q
@@ -269,9 +273,12 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             const int kb = kb0 + i;
             const int r = static_cast<int>(a.fsb.div(kb));
             const int b = kb - r * a.sblocks;
-            mbar_arrive_expect_tx(&full[s], L::A_BYTES + L::B_BYTES);
-            tma_load_4d(smem_u32(sA + s * L::A_BYTES), &tmA, &full[s], 0, b * a.shift, p * a.stride + r, n);
-            tma_load_2d(smem_u32(sB + s * L::B_BYTES), &tmB, &full[s], kb * kBK, n0);
+            if (elect_one()) {
+              mbar_arrive_expect_tx(&full[s], L::A_BYTES + L::B_BYTES);
+              tma_load_4d(smem_u32(sA + s * L::A_BYTES), &tmA, &full[s], 0, b * a.shift, p * a.stride + r, n);
+              tma_load_2d(smem_u32(sB + s * L::B_BYTES), &tmB, &full[s], kb * kBK, n0);
+            }
+            __syncwarp();
           }
         } else if (MODE == 3) {
           // stem wgrad: 4 k-atoms (r, b) per M tile; k block = 32 output columns of one row
@@ -295,12 +302,15 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             const int qb = kb - row * a.qblocks;
             const int n = static_cast<int>(a.fP.div(row));
             const int p = row - n * a.P;
-            mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>((na + nb) * 4096));
-            for (int q4 = 0; q4 < na; ++q4)
-              tma_load_4d(smem_u32(sA + s * L::A_BYTES + q4 * 4096), &tmA, &full[s], 0,
-                          qb * 32 + ab[q4] * a.shift, p * a.stride + ar[q4], n);
-            for (int j = 0; j < nb; ++j)
-              tma_load_4d(smem_u32(sB + s * L::B_BYTES + j * 4096), &tmB, &full[s], n0 + 32 * j, qb * 32, p, n);
+            if (elect_one()) {
+              mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>((na + nb) * 4096));
+              for (int q4 = 0; q4 < na; ++q4)
+                tma_load_4d(smem_u32(sA + s * L::A_BYTES + q4 * 4096), &tmA, &full[s], 0,
+                            qb * 32 + ab[q4] * a.shift, p * a.stride + ar[q4], n);
+              for (int j = 0; j < nb; ++j)
+                tma_load_4d(smem_u32(sB + s * L::B_BYTES + j * 4096), &tmB, &full[s], n0 + 32 * j, qb * 32, p, n);
+            }
+            __syncwarp();
           }
         } else {
           int ac[4], ar[4], as[4], na = 0;
@@ -335,6 +345,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             const int p = static_cast<int>(a.fQ.div(pq));
             const int q = pq - p * a.Q;
             const int w0 = q * a.stride - a.pad, h0 = p * a.stride - a.pad;
+            if (elect_one()) {
             if constexpr (CG == 1) {
               mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>((na + nb) * 4096));
               for (int q4 = 0; q4 < na; ++q4)
@@ -351,16 +362,36 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
               for (int j = 0; j < nb; ++j)
                 tma2_load_2d(smem_u32(sB + s * L::B_BYTES + j * 4096), &tmB, cb, nbase + 32 * j, pix);
             }
+            }
+            __syncwarp();
           }
         }
       }
     }
   } else if (warp == 5) {
-    if (lane == 0 && rank == 0) {
-      // ---------------- MMA issuer (the pair leader for CG = 2) ----------------
+    if (rank == 0) {
+      // ---------------- MMA issuer (the pair leader for CG = 2; whole warp, elected lane issues) ----------------
       constexpr bool kMN = (MODE == 1 || MODE == 3);  // wgrad: both operands MN-major
       constexpr uint32_t idesc = idesc_tf32(kBM * CG, BN, kMN, kMN);
-      uint32_t g = 0;
+      // The issue loop is kept to a handful of instructions per MMA: with
+      // descriptors built per MMA the single issuing thread, not the tensor
+      // core, set the pace (~150-200 cycles per MMA vs the 55 / 64 / 128 cycle
+      // hardware floor at N = 64 / 128 / 256; tools/mma_probe.py).  The stage
+      // descriptors are one base descriptor plus the stage offset (address
+      // field in 16-byte units), the k step within a stage a constant.
+      //   K-major SW128: 8 k = 32 B;  MN-major SW128_BASE32B: 8 k rows = 1024 B
+      constexpr uint32_t KSTEP = kMN ? (1024u >> 4) : (32u >> 4);
+      const uint64_t adesc0 = kMN ? umma_desc(smem_u32(sA), 4096, 512, kLayoutSW128Base32)
+                                  : umma_desc(smem_u32(sA), 16, 1024, kLayoutSW128);
+      const uint64_t bdesc0 = kMN ? umma_desc(smem_u32(sB), 4096, 512, kLayoutSW128Base32)
+                                  : umma_desc(smem_u32(sB), 16, 1024, kLayoutSW128);
+      auto mma = [&](uint32_t d, uint64_t ad, uint64_t bd, uint32_t accum) {
+        if constexpr (CG == 1)
+          umma_tf32(d, ad, bd, idesc, accum);
+        else
+          umma2_tf32(d, ad, bd, idesc, accum);
+      };
+      uint32_t s = 0, ph = 0;  // stage ring position and parity
       int local = 0;
       for (int t = unit; t < tg.tiles; t += units, ++local) {
         int m0, n0, kb0, nkb, split;
@@ -369,37 +400,32 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         if (local >= 2) mbar_wait(&tempty[acc], ((local >> 1) - 1) & 1);
         tc_fence_after();
         const uint32_t d = tmem + static_cast<uint32_t>(acc * BN);
-        for (int i = 0; i < nkb; ++i, ++g) {
-          const int s = g % STAGES;
-          mbar_wait(&full[s], (g / STAGES) & 1);
+        for (int i = 0; i < nkb; ++i) {
+          mbar_wait(&full[s], ph);
           tc_fence_after();
-          const uint32_t a0 = smem_u32(sA + s * L::A_BYTES);
-          const uint32_t b0 = smem_u32(sB + s * L::B_BYTES);
+          const uint64_t ad = adesc0 + s * (L::A_BYTES >> 4), bd = bdesc0 + s * (L::B_BYTES >> 4);
+          if (elect_one()) {
+            mma(d, ad, bd, i != 0 ? 1u : 0u);
 #pragma unroll
-          for (int kk = 0; kk < kBK / 8; ++kk) {
-            uint64_t ad, bd;
-            if (!kMN) {
-              ad = umma_desc(a0 + kk * 32, 16, 1024, kLayoutSW128);
-              bd = umma_desc(b0 + kk * 32, 16, 1024, kLayoutSW128);
-            } else {
-              // 8 k rows = two 4-row K atoms (512 B each); MN atoms 4 KB apart
-              ad = umma_desc(a0 + kk * 1024, 4096, 512, kLayoutSW128Base32);
-              bd = umma_desc(b0 + kk * 1024, 4096, 512, kLayoutSW128Base32);
-            }
+            for (int kk = 1; kk < kBK / 8; ++kk) mma(d, ad + kk * KSTEP, bd + kk * KSTEP, 1u);
             if constexpr (CG == 1)
-              umma_tf32(d, ad, bd, idesc, (i | kk) != 0 ? 1u : 0u);
+              umma_commit(&empty[s]);
             else
-              umma2_tf32(d, ad, bd, idesc, (i | kk) != 0 ? 1u : 0u);
+              umma2_commit(&empty[s]);
           }
-          if constexpr (CG == 1)
-            umma_commit(&empty[s]);
-          else
-            umma2_commit(&empty[s]);
+          __syncwarp();
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
         }
-        if constexpr (CG == 1)
-          umma_commit(&tfull[acc]);
-        else
-          umma2_commit(&tfull[acc]);
+        if (elect_one()) {
+          if constexpr (CG == 1)
+            umma_commit(&tfull[acc]);
+          else
+            umma2_commit(&tfull[acc]);
+        }
+        __syncwarp();
       }
     }
   } else {
@@ -674,6 +700,28 @@ int bn_for(int n) { return n <= 64 ? 64 : (n <= 128 ? 128 : 256); }
 
 }  // namespace
 
+bool tma_encoders_ok() { return load_encoders(); }
+
+bool tma_map_nhwc(CUtensorMap* m, const float* base, int N, int H, int W, int C, int box_w, int box_h, int swz) {
+  if (!load_encoders()) return false;
+  cuuint64_t dims[4] = {static_cast<cuuint64_t>(C), static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H),
+                        static_cast<cuuint64_t>(N)};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(C) * 4, static_cast<cuuint64_t>(W) * C * 4,
+                           static_cast<cuuint64_t>(H) * W * C * 4};
+  cuuint32_t box[4] = {32, static_cast<cuuint32_t>(box_w), static_cast<cuuint32_t>(box_h), 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  return g_encode_tiled(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        swz ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool tma_map_2d(CUtensorMap* m, const float* base, int64_t rows, int64_t cols, int box_rows, int swz) {
+  if (!load_encoders()) return false;
+  return make_tiled(m, base, rows, cols, box_rows,
+                    swz ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
 bool conv_tma_ok_fwd(const ConvShape& s) { return s.C % 32 == 0 && load_encoders(); }
 
 void set_conv_pairs(int mode) { g_pairs = mode; }
@@ -683,7 +731,15 @@ int conv_fwd_stats_tiles(const ConvShape& s, bool stem, int* tile_rows) {
     *tile_rows = s.Q;
     return s.N * s.P;
   }
-  if (!use_tma() || !conv_tma_ok_fwd(s)) return 0;
+  if (!use_tma()) return 0;
+  if (s.stride == 1) {
+    const int ht = conv_halo_stats_tiles(s.N, s.H, s.W, s.C, s.K, s.R, s.S, s.pad, s.P, s.Q);
+    if (ht > 0) {
+      *tile_rows = 0;
+      return ht;
+    }
+  }
+  if (!conv_tma_ok_fwd(s)) return 0;
   *tile_rows = kBM;
   return (s.N * s.P * s.Q + kBM - 1) / kBM;
 }

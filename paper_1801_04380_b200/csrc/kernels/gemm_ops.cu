@@ -414,6 +414,8 @@ void set_conv_tma(int on) { g_use_tma = on ? 1 : 0; }
 
 cudaError_t conv_fwd(const ConvShape& s, const float* x, const float* w, const float* bias, float* y,
                      cudaStream_t st, float* stats) {
+  if (use_tma() && s.stride == 1 && conv_halo_variant(s.N, s.H, s.W, s.C, s.K, s.R, s.S, s.pad, s.P, s.Q))
+    return conv_halo(s.N, s.H, s.W, s.C, s.K, s.R, s.S, s.pad, s.P, s.Q, x, w, bias, y, 0, stats, st);
   if (use_tma() && conv_tma_ok_fwd(s)) return conv_fwd_tma(s, x, w, bias, y, stats, st);
   if (stats) return cudaErrorInvalidValue;  // only the TMA kernels emit BN tile statistics
   switch (bn_for(s.K)) {
@@ -431,7 +433,13 @@ cudaError_t conv_dgrad(const ConvShape& s, const float* dy, const float* w, floa
   transpose_w_kernel<<<grid, block, 0, st>>>(w, wt, s.K, s.R * s.S, s.C, tma ? 1 : 0);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  if (tma) return conv_dgrad_tma(s, dy, wt, dx, accumulate, st);
+  if (tma) {
+    // stride-1 dgrad = stride-1 conv of dy with the flipped filter, padding R-1-pad
+    const int pd = s.R - 1 - s.pad;
+    if (s.R == s.S && conv_halo_variant(s.N, s.P, s.Q, s.K, s.C, s.R, s.S, pd, s.H, s.W))
+      return conv_halo(s.N, s.P, s.Q, s.K, s.C, s.R, s.S, pd, s.H, s.W, dy, wt, nullptr, dx, accumulate, nullptr, st);
+    return conv_dgrad_tma(s, dy, wt, dx, accumulate, st);
+  }
   switch (bn_for(s.C)) {
     case 64: return conv_dgrad_bn<64>(s, dy, wt, dx, accumulate, st);
     case 128: return conv_dgrad_bn<128>(s, dy, wt, dx, accumulate, st);

@@ -20,7 +20,9 @@ struct ConvShape {
 cudaError_t conv_fwd(const ConvShape& s, const float* x, const float* w, const float* bias, float* y,
                      cudaStream_t st, float* stats = nullptr);
 // Number of statistics tiles the forward (stem: conv_stem_fwd) emits, 0 if it
-// cannot; *tile_rows = output rows per tile (the last tile may hold fewer).
+// cannot; *tile_rows = output rows per tile (the last tile may hold fewer), or
+// 0 when each tile carries its own count (4 planes {shift, S1, S2, count}
+// instead of 3).  The partial buffer needs tiles * 4 * K floats.
 int conv_fwd_stats_tiles(const ConvShape& s, bool stem, int* tile_rows);
 // dx[N*H*W][C] (+)= conv_transpose(dy, w); wt = scratch of K*R*S*C floats.
 cudaError_t conv_dgrad(const ConvShape& s, const float* dy, const float* w, float* wt, float* dx,
@@ -60,6 +62,14 @@ cudaError_t conv_stem_wgrad(const ConvShape& s, const float* xp, const float* dy
 // Channel-pad raw NHWC images (C_raw -> Cs) for the generic path.
 cudaError_t pad_channels(const float* raw, int C_raw, float* out, int Cs, int64_t pixels, cudaStream_t st);
 
+// Halo-tiled stride-1 convolution (conv_halo.cu): one TMA box per 32-channel
+// chunk serves every filter tap.  Variant 0 = not applicable to the shape.
+int conv_halo_variant(int N, int H, int W, int C, int K, int R, int S, int pad, int P, int Q);
+int conv_halo_stats_tiles(int N, int H, int W, int C, int K, int R, int S, int pad, int P, int Q);
+cudaError_t conv_halo(int N, int H, int W, int C, int K, int R, int S, int pad, int P, int Q, const float* x,
+                      const float* w, const float* bias, float* y, int accumulate, float* stats, cudaStream_t st);
+void set_conv_halo(int mode);  // 0 off, 1 by shape (default; env SN_CONV_HALO=0), 2 whenever legal (tests)
+
 bool conv_tma_ok_dgrad_strided(const ConvShape& s);
 cudaError_t conv_dgrad_strided_tma(const ConvShape& s, const float* dy, const float* w, float* wt_scratch, float* dx,
                                    int accumulate, cudaStream_t st);
@@ -93,8 +103,9 @@ cudaError_t bn_fwd(const float* x, int64_t rows, int C, const float* gamma, cons
                    float* red_scratch, cudaStream_t st);
 // Statistics from the producing convolution's per-tile partials
 // ({shift, sum(y - shift), sum((y - shift)^2)} per tile and channel, tile t
-// holding min(tile_rows, rows - t*tile_rows) rows); x = the BN input (row 0
-// is the global shift).  Same outputs as bn_fwd(compute_stats=1, y=null).
+// holding min(tile_rows, rows - t*tile_rows) rows, or with tile_rows == 0 a
+// fourth plane holding each tile's row count); x = the BN input (row 0 is the
+// global shift).  Same outputs as bn_fwd(compute_stats=1, y=null).
 cudaError_t bn_stats_from_tiles(const float* tiles, int ntiles, int tile_rows, const float* x, int64_t rows, int C,
                                 float* stats, float* running, float eps, float momentum, float* red_scratch,
                                 cudaStream_t st);

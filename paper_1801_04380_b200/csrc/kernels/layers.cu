@@ -1157,10 +1157,13 @@ __global__ void tile_stats_stage1(const float* __restrict__ tiles, int ntiles, i
     double a = 0.0, b = 0.0;
     if (lane < lanes && c < C) {
       const double x0 = x[c];
+      const int planes = tile_rows > 0 ? 3 : 4;
       for (int t = t0 + lane; t < t1; t += lanes) {
-        const float* p = tiles + static_cast<size_t>(t) * 3 * C + c;
+        const float* p = tiles + static_cast<size_t>(t) * planes * C + c;
         const int64_t left = rows - static_cast<int64_t>(t) * tile_rows;
-        const double n = static_cast<double>(left < tile_rows ? left : tile_rows);
+        const double n = tile_rows > 0 ? static_cast<double>(left < tile_rows ? left : tile_rows)
+                                       : static_cast<double>(p[3 * C]);
+        if (n <= 0.0) continue;  // a tile past the last output row (its shift is not a value)
         const double d = static_cast<double>(p[0]) - x0;
         const double S1 = p[C], S2 = p[2 * C];
         a += S1 + n * d;

@@ -122,6 +122,20 @@ __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// One lane of a converged warp (elect.sync).  Single-thread tcgen05 / TMA
+// issue is written as "whole warp runs the loop, the elected lane issues", so
+// loop state and descriptors stay warp-uniform (uniform registers) and ptxas
+// emits no per-instruction waterfall (ELECT / R2UR.BROADCAST / BRA.U.ANY) loop.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 // ---- TMEM -----------------------------------------------------------------
 // Called by one full warp.  Writes the TMEM base address to *dst.
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst, uint32_t ncols) {

@@ -100,6 +100,10 @@ CONV_CASES = [
     (1, 64, 23, 23, 96, 5, 3, 2),    # stride 3, 5x5
     (2, 128, 8, 8, 512, 3, 1, 1),    # K = 512: two N tiles of 256
     (32, 64, 28, 28, 64, 3, 1, 1),   # several 256-row tiles per CTA pair (double-buffered TMEM)
+    (4, 64, 56, 56, 64, 3, 1, 1),    # ResNet stage 1 shape (halo, 3 sub-tiles of 2 rows)
+    (3, 128, 28, 28, 128, 3, 1, 1),  # stage 2 (halo, 2 sub-tiles of 4 rows)
+    (2, 256, 14, 14, 256, 3, 1, 1),  # stage 3 (halo, 8-row sub-tile, rows past P)
+    (2, 64, 10, 12, 96, 5, 1, 2),    # 5x5, non-square image, K % 64 != 0
 ]
 
 
@@ -119,15 +123,18 @@ def _shape_arr(N, C, H, W, K, k, s, p):
     return (ctypes.c_int * 11)(N, H, W, C, K, k, k, P, Q, s, p), P, Q
 
 
-@pytest.mark.parametrize("tma,pairs", [(1, 1), (1, 2), (0, 1)])
+@pytest.mark.parametrize("tma,pairs,halo", [(1, 1, 1), (1, 2, 0), (1, 1, 2), (0, 1, 0)])
 @pytest.mark.parametrize("case", CONV_CASES)
-def test_conv_fwd_dgrad_wgrad(cuda, case, tma, pairs):
+def test_conv_fwd_dgrad_wgrad(cuda, case, tma, pairs, halo):
     """pairs=2 forces the CTA-pair (cta_group::2, M = 256) TMA kernels on
-    every shape (odd tile counts, rows past M in the peer CTA)."""
+    every shape (odd tile counts, rows past M in the peer CTA); halo=2 the
+    halo-tiled stride-1 kernels wherever they apply (junk padded columns,
+    bands past the last output row)."""
     N, C, H, W, K, k, s, p = case
     lib = _conv_lib()
     lib.sn_test_set_conv_tma(tma)
     lib.sn_test_set_conv_pairs(pairs)
+    lib.sn_test_set_conv_halo(halo)
     shape, P, Q = _shape_arr(*case)
     g = torch.Generator().manual_seed(sum(case))
     x = torch.randn(N, C, H, W, generator=g)
@@ -168,6 +175,7 @@ def test_conv_fwd_dgrad_wgrad(cuda, case, tma, pairs):
         _check(db_d.cpu(), bd.grad, N * P * Q)
     lib.sn_test_set_conv_tma(1)
     lib.sn_test_set_conv_pairs(1)
+    lib.sn_test_set_conv_halo(1)
 
 
 def test_tma_overlapping_window_probe(cuda):

@@ -30,8 +30,10 @@ SHAPES = [
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--pairs", type=int, nargs="+", default=[0, 1, 2])
+    ap.add_argument("--halo", type=int, nargs="+", default=[1])
     ap.add_argument("--ops", nargs="+", default=["fwd", "dgrad", "wgrad"])
     ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--shapes", type=int, nargs="+", default=None, help="indices into SHAPES")
     args = ap.parse_args()
     import torch
     from paper_1801_04380_b200 import _native
@@ -42,7 +44,7 @@ def main() -> None:
     lib.sn_test_red_scratch_floats.restype = ctypes.c_longlong
     lib.sn_test_wgrad_splits.restype = ctypes.c_int
     dev = torch.device("cuda:0")
-    for shp in SHAPES:
+    for shp in [SHAPES[i] for i in (args.shapes if args.shapes is not None else range(len(SHAPES)))]:
         N, C, H, W, K, k, s, p = shp
         P = (H + 2 * p - k) // s + 1
         Q = (W + 2 * p - k) // s + 1
@@ -71,8 +73,9 @@ def main() -> None:
                                              part.data_ptr(), red.data_ptr())
                 call = lambda: lib.sn_test_conv(2, shape, ptrs, 0)
             line = f"{op:6s} N{N} C{C} {H}x{W} K{K} s{s}"
-            for pm in args.pairs:
+            for pm, hm in [(pm, hm) for hm in args.halo for pm in args.pairs]:
                 lib.sn_test_set_conv_pairs(pm)
+                lib.sn_test_set_conv_halo(hm)
                 lib.sn_test_set_sync(1)
                 for _ in range(2):
                     assert call() == 0
@@ -86,7 +89,7 @@ def main() -> None:
                 torch.cuda.synchronize()
                 ms = e0.elapsed_time(e1) / args.iters
                 lib.sn_test_set_sync(1)
-                line += f" | pairs{pm}: {ms * 1e3:8.1f} us {flops / ms / 1e9:7.1f} TF/s"
+                line += f" | p{pm}h{hm}: {ms * 1e3:7.1f} us {flops / ms / 1e9:6.1f} TF/s"
             print(line, flush=True)
     lib.sn_test_set_conv_pairs(1)
 
