@@ -286,15 +286,43 @@ def extras(args, net, cfg, ex, ms_per_step, local) -> dict:
         else:
             t_other += ms
     peaks = measured_peaks()
-    tf32 = tf32_gemm_peak(f"cuda:{local}")
+    cublas_tf32 = tf32_gemm_peak(f"cuda:{local}")
+    # tf32 tensor peak = half the dense bf16 peak: a kind::tf32 MMA covers K = 8
+    # per instruction where kind::f16 covers K = 16, at the same cycle count
+    # (profiles/r01_mma_probe.txt: 1190 vs 2380 TF/s at 1965 MHz)
+    if peaks.get("bf16_tflops_sustained"):  # kernels timed inside a long step: the sustained figure
+        bf16, src = float(peaks["bf16_tflops_sustained"]), "MEASURED_PEAKS.json bf16_tflops_sustained"
+    elif peaks.get("bf16_tflops"):
+        bf16, src = float(peaks["bf16_tflops"]), "MEASURED_PEAKS.json bf16_tflops (burst)"
+    else:
+        bf16, src = 1590.0, "B200_PROFILING.md fallback 1.59 PF bf16 (MEASURED_PEAKS.json absent)"
+    tf32 = bf16 / 2
     achieved = f_tensor / (t_tensor / 1e3) / 1e12 if t_tensor else 0.0
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_step_traffic.json")) as fh:
+            tr = json.load(fh)["per_step"]
+        traffic = {"dram_bytes_per_step": tr["conv_fc_gemm"]["dram_bytes_per_step"],
+                   "source": "profiles/r01_step_traffic.json (ncu dram__bytes_read+write, all CONV/FC launches)"}
+    except (OSError, KeyError, ValueError):
+        tr = None
     out["roofline"] = {"bound": "tensor", "kernel": "CONV/FC implicit-GEMM tcgen05 kind::tf32 (fwd+wgrad+dgrad)",
                        "achieved": round(achieved, 2), "peak": round(tf32, 2), "unit": "TFLOP/s",
                        "frac": round(achieved / tf32, 4) if tf32 else None,
-                       "peak_source": "cuBLAS tf32 GEMM 8192^3 measured in this run (MEASURED_PEAKS.json has bf16 "
-                                      f"only: {peaks.get('bf16_tflops')} TF/s burst)",
-                       "traffic": None, "algorithmic_tflop_per_step": round(f_tensor / 1e12, 4),
+                       "peak_source": f"tf32 = bf16 / 2, bf16 from {src}",
+                       "cublas_tf32_8192_tflops_this_run": round(cublas_tf32, 2),
+                       "traffic": traffic, "algorithmic_tflop_per_step": round(f_tensor / 1e12, 4),
                        "share_of_step": round(t_tensor / sum(p[0] for p in prof), 4)}
+    if tr and "hbm_layers" in tr:
+        hbm_peak = float(peaks.get("hbm_gbs") or 6650.0)
+        t_layers = t_other / 1e3
+        gbs = tr["hbm_layers"]["dram_bytes_per_step"] / t_layers / 1e9 if t_layers else 0.0
+        out["roofline_hbm_layers"] = {
+            "bound": "hbm", "kernel": "BN / ReLU / JOIN / POOL / softmax / split-K / SGD layer kernels",
+            "achieved": round(gbs, 1), "peak": hbm_peak, "unit": "GB/s", "frac": round(gbs / hbm_peak, 4),
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks.get("hbm_gbs") else "B200_PROFILING.md fallback",
+            "traffic": tr["hbm_layers"]["dram_bytes_per_step"],
+            "note": "achieved = ncu DRAM bytes of these launches per step / their summed event time this run"}
     out["time_by_layer_kind_ms"] = {k: round(v, 3) for k, v in sorted(by_kind.items(), key=lambda kv: -kv[1])}
     # unconstrained reference run: all features off, pool = whole-iteration residency
     try:

@@ -447,3 +447,230 @@ cudaError_t conv_halo(int N, int H, int W, int C, int K, int R, int S, int pad, 
 namespace sn {
 void set_conv_halo(int mode) { g_halo = mode; }
 }  // namespace sn
+
+// ---------------------------------------------------------------------------
+// Halo-tiled weight gradient for C = K = 64, R x S taps, stride 1:
+//   dW_tap[c][k] = sum over output positions p of x[p + shift(tap)][c] dy[p][k]
+// on the padded grid (dy is zero at the junk columns x' >= Q: TMA zero fill).
+// The GEMM K dimension is the position; per band of TR padded output rows one
+// x halo box per 32-channel chunk (MN-major, SWIZZLE_128B_ATOM_32B) and one dy
+// box per 32-channel chunk of k serve all R*S taps: the tap shift is a K-row
+// offset of the A descriptor.  One M = 64 MMA per (tap, 8 positions); the R*S
+// accumulators (64 lanes x 64 columns each, an M = 64 result occupying lanes
+// 16 x {0..3} + lane0, lane0 in {0, 16}) are packed two per 64-column TMEM
+// block.  Each persistent CTA accumulates a contiguous range of bands and
+// writes its partial [R*S*C][K] slice; splitk_reduce sums the CTAs' slices
+// in a fixed order into dw[K][R][S][C].
+namespace sn {
+namespace {
+
+struct HaloWgArgs {
+  int Wp, TR, R, S, pad, P, Q, bands, units;  // units = N * bands
+  uint32_t xbox_bytes, dybox_bytes;           // one TMA box (one 32-channel chunk)
+  uint32_t xslot, dyslot;                     // smem bytes per chunk buffer (with zeroed slack rows)
+  int ksteps;                                 // ceil(TR*Wp / 8)
+  float* partial;                             // [gridDim.x][R*S*64][64]
+};
+
+constexpr int kWgStages = 2;
+
+template <int RC, int SC>  // compile-time taps (0: runtime a.R x a.S)
+__global__ void __launch_bounds__(kHaloThreads, 1)
+    tc_conv_halo_wgrad64(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmDY,
+                         HaloWgArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t stage_bytes = 2 * a.xslot + 2 * a.dyslot;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kWgStages * stage_bytes);
+  uint64_t* empty = full + kWgStages;
+  uint64_t* done = empty + kWgStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int taps = a.R * a.S;
+
+  // zero every buffer once: the slack rows past each TMA box are read by the
+  // shifted descriptors (x) or the last partial k step (dy) and must be finite
+  for (uint32_t i = threadIdx.x * 16; i < kWgStages * stage_bytes; i += blockDim.x * 16)
+    *reinterpret_cast<float4*>(smem + i) = make_float4(0.f, 0.f, 0.f, 0.f);
+  fence_proxy_async();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kWgStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 5) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  // contiguous range of work units (image, band) for this CTA
+  const int per = (a.units + gridDim.x - 1) / gridDim.x;
+  const int u0 = min(a.units, blockIdx.x * per), u1 = min(a.units, u0 + per);
+
+  if (warp == 4) {
+    uint32_t s = 0, ph = 0;
+    bool wrap = false;
+    for (int u = u0; u < u1; ++u) {
+      const int n = u / a.bands, y0 = (u - n * a.bands) * a.TR;
+      if (wrap) mbar_wait(&empty[s], ph ^ 1);
+      if (elect_one()) {
+        uint8_t* st = smem + s * stage_bytes;
+        mbar_arrive_expect_tx(&full[s], 2 * a.xbox_bytes + 2 * a.dybox_bytes);
+        for (int c = 0; c < 2; ++c) {
+          tma_load_4d(smem_u32(st + c * a.xslot), &tmX, &full[s], c * 32, -a.pad, y0 - a.pad, n);
+          tma_load_4d(smem_u32(st + 2 * a.xslot + c * a.dyslot), &tmDY, &full[s], c * 32, 0, y0, n);
+        }
+      }
+      __syncwarp();
+      if (++s == kWgStages) {
+        s = 0;
+        ph ^= 1;
+        wrap = true;
+      }
+    }
+  } else if (warp == 5) {
+    // M = 64, N = 64, both operands MN-major (SW128_BASE32B): LBO = the other
+    // 32-channel chunk's buffer, SBO = 4 K rows (512 B); 8 positions = 1024 B
+    constexpr uint32_t idesc = idesc_tf32(64, 64, true, true);
+    const uint64_t xd0 = umma_desc(smem_u32(smem), a.xslot, 512, kLayoutSW128Base32);
+    const uint64_t dd0 = umma_desc(smem_u32(smem + 2 * a.xslot), a.dyslot, 512, kLayoutSW128Base32);
+    const uint32_t sstep = stage_bytes >> 4;
+    uint32_t s = 0, ph = 0;
+    bool first = true;
+    for (int u = u0; u < u1; ++u) {
+      mbar_wait(&full[s], ph);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint64_t xd = xd0 + s * sstep, dd = dd0 + s * sstep;
+        const uint32_t rowstep = static_cast<uint32_t>(a.Wp) * 8u;  // one padded row, 16-byte units
+        for (int kq = 0; kq < a.ksteps; ++kq) {
+          const uint64_t xk = xd + static_cast<uint32_t>(kq) * 64u, dk = dd + static_cast<uint32_t>(kq) * 64u;
+          const uint32_t acc = (first && kq == 0) ? 0u : 1u;
+          if constexpr (RC > 0) {
+#pragma unroll
+            for (int t = 0; t < RC * SC; ++t) {
+              const uint32_t d = tmem + static_cast<uint32_t>((t >> 1) * 64) + (static_cast<uint32_t>((t & 1) * 16) << 16);
+              umma_tf32(d, xk + (t / SC) * rowstep + (t % SC) * 8u, dk, idesc, acc);
+            }
+          } else {
+            int r = 0, sx = 0;
+            for (int t = 0; t < taps; ++t) {
+              const uint32_t d = tmem + static_cast<uint32_t>((t >> 1) * 64) + (static_cast<uint32_t>((t & 1) * 16) << 16);
+              umma_tf32(d, xk + r * rowstep + sx * 8u, dk, idesc, acc);
+              if (++sx == a.S) {
+                sx = 0;
+                ++r;
+              }
+            }
+          }
+        }
+        umma_commit(&empty[s]);
+      }
+      __syncwarp();
+      first = false;
+      if (++s == kWgStages) {
+        s = 0;
+        ph ^= 1;
+      }
+    }
+    if (elect_one()) umma_commit(done);
+    __syncwarp();
+  } else {
+    // epilogue: warp w, lane l -> tap 2b + (l >= 16), channel 16 w + (l & 15)
+    const int RSC = taps * 64;
+    float* out = a.partial + static_cast<size_t>(blockIdx.x) * RSC * 64;
+    if (u0 >= u1) {
+      // no work: this CTA's slice is zero
+      for (int i = threadIdx.x; i < RSC * 64; i += 128) out[i] = 0.f;
+    } else {
+      mbar_wait(done, 0);
+      tc_fence_after();
+      for (int b = 0; b < (taps + 1) / 2; ++b) {
+        const int tap = 2 * b + (lane >> 4);
+        const int c = 16 * warp + (lane & 15);
+        for (int k0 = 0; k0 < 64; k0 += 32) {
+          float v[32];
+          tmem_ld32(tmem + static_cast<uint32_t>(b * 64 + k0) + (static_cast<uint32_t>(warp * 32) << 16), v);
+          if (tap < taps) {
+            float4* dst = reinterpret_cast<float4*>(out + (static_cast<size_t>(tap) * 64 + c) * 64 + k0);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+}  // namespace
+
+// Applicable: C == K == 64, stride 1, padded width <= 128 rows per band.
+bool conv_halo_wgrad_ok(int N, int H, int W, int C, int K, int R, int S, int pad, int P, int Q) {
+  if (halo_mode() == 0 || C != 64 || K != 64 || R * S < 2 || R * S > 10 || !tma_encoders_ok()) return false;
+  if (P != H + 2 * pad - R + 1 || Q != W + 2 * pad - S + 1 || pad < 0) return false;
+  const int Wp = W + 2 * pad;
+  if (Wp > kBM) return false;
+  const int TR = std::min(kBM / Wp, P);
+  // by shape: the padded band must be mostly real positions
+  if (halo_mode() == 1 && TR * Q * 4 < 3 * kBM) return false;
+  const int xrows = (TR + R - 1) * Wp + 8 + (S - 1);
+  const int dyrows = (TR * Wp + 7) / 8 * 8;
+  const uint32_t stage = 2 * ((xrows * 128 + 1023) / 1024 * 1024) + 2 * ((dyrows * 128 + 1023) / 1024 * 1024);
+  return kWgStages * stage + 1024 + 256 <= 227 * 1024;
+}
+
+int conv_halo_wgrad_splits() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+  }
+  return n;
+}
+
+// partial: conv_halo_wgrad_splits() * R*S*64*64 floats; dw[64][R][S][64].
+cudaError_t conv_halo_wgrad(int N, int H, int W, int R, int S, int pad, int P, int Q, const float* x,
+                            const float* dy, float* partial, float* dw, cudaStream_t st) {
+  if (!conv_halo_wgrad_ok(N, H, W, 64, 64, R, S, pad, P, Q)) return cudaErrorInvalidValue;
+  HaloWgArgs a{};
+  a.Wp = W + 2 * pad;
+  a.TR = std::min(kBM / a.Wp, P);
+  a.R = R;
+  a.S = S;
+  a.pad = pad;
+  a.P = P;
+  a.Q = Q;
+  a.bands = (P + a.TR - 1) / a.TR;
+  a.units = N * a.bands;
+  const int xrows_box = (a.TR + R - 1) * a.Wp;
+  a.xbox_bytes = static_cast<uint32_t>(xrows_box) * 128;
+  a.dybox_bytes = static_cast<uint32_t>(a.TR * a.Wp) * 128;
+  a.xslot = ((xrows_box + 8 + (S - 1)) * 128 + 1023) / 1024 * 1024;
+  a.dyslot = (((a.TR * a.Wp + 7) / 8 * 8) * 128 + 1023) / 1024 * 1024;
+  a.ksteps = (a.TR * a.Wp + 7) / 8;
+  a.partial = partial;
+  CUtensorMap X, DY;
+  if (!tma_map_nhwc(&X, x, N, H, W, 64, a.Wp, a.TR + R - 1, 1)) return cudaErrorInvalidValue;
+  if (!tma_map_nhwc(&DY, dy, N, P, Q, 64, a.Wp, a.TR, 1)) return cudaErrorInvalidValue;
+  const int grid = conv_halo_wgrad_splits();
+  const int smem = kWgStages * (2 * a.xslot + 2 * a.dyslot) + 1024 + 256;
+  auto kern = (R == 3 && S == 3) ? tc_conv_halo_wgrad64<3, 3> : tc_conv_halo_wgrad64<0, 0>;
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (err != cudaSuccess) return err;
+  kern<<<grid, kHaloThreads, smem, st>>>(X, DY, a);
+  err = cudaGetLastError();
+  if (err != cudaSuccess) return err;
+  return splitk_reduce(partial, grid, R * S * 64, 64, dw, nullptr, 0, 1, st);
+}
+
+}  // namespace sn

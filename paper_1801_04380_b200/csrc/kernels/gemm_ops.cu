@@ -262,8 +262,34 @@ struct WgradA {
 
 // D[M][N] = sum_split P[split][M][N] (+bias[n]) (+D if accumulate); optionally
 // written transposed (D^T[N][M], for wgrad partials laid out [rsc][k]).
+// Stage 1 of a wide split-K reduction: group g of `per` consecutive splits is
+// summed (in split order) into its first split's slot, in place (each element
+// is read and written by one thread only).
+__global__ void splitk_group_kernel(float* P, int splits, int per, int64_t MN) {
+  const int g = blockIdx.y;
+  const int s0 = g * per, s1 = min(splits, s0 + per);
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < MN;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float* p = P + static_cast<size_t>(s0) * MN + e;
+    float acc = *p;
+    int s = s0 + 1;
+    for (; s + 3 < s1; s += 4) {
+      const float a0 = P[static_cast<size_t>(s) * MN + e], a1 = P[static_cast<size_t>(s + 1) * MN + e];
+      const float a2 = P[static_cast<size_t>(s + 2) * MN + e], a3 = P[static_cast<size_t>(s + 3) * MN + e];
+      acc += a0;
+      acc += a1;
+      acc += a2;
+      acc += a3;
+    }
+    for (; s < s1; ++s) acc += P[static_cast<size_t>(s) * MN + e];
+    *p = acc;
+  }
+}
+
+// sstride: distance between consecutive summed slices, in slices (1, or the
+// group size after splitk_group_kernel).
 __global__ void splitk_reduce_kernel(const float* __restrict__ P, int splits, int M, int N, float* D,
-                                     const float* bias, int accumulate, int transpose) {
+                                     const float* bias, int accumulate, int transpose, int sstride) {
   __shared__ float tile[32][33];
   const int m0 = blockIdx.y * 32, n0 = blockIdx.x * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
@@ -271,7 +297,7 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ P, int splits, in
     const int m = m0 + i, n = n0 + tx;
     float acc = 0.f;
     if (m < M && n < N) {
-      const size_t stride = static_cast<size_t>(M) * N;
+      const size_t stride = static_cast<size_t>(M) * N * sstride;
       const float* p = P + static_cast<size_t>(m) * N + n;
       for (int s = 0; s < splits; ++s) acc += p[s * stride];
       if (bias) acc += bias[n];
@@ -301,7 +327,21 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ P, int splits, in
 cudaError_t splitk_reduce_impl(const float* P, int splits, int M, int N, float* D, const float* bias, int accumulate,
                           int transpose, cudaStream_t st) {
   dim3 grid((N + 31) / 32, (M + 31) / 32), block(32, 8);
-  splitk_reduce_kernel<<<grid, block, 0, st>>>(P, splits, M, N, D, bias, accumulate, transpose);
+  // Few output tiles and many splits: first sum groups of splits with the whole
+  // GPU (in place), then reduce the group sums in order.
+  const int64_t MN = static_cast<int64_t>(M) * N;
+  const int64_t tiles = static_cast<int64_t>(grid.x) * grid.y;
+  if (splits >= 16 && tiles < 4 * 148) {
+    int groups = static_cast<int>(std::min<int64_t>(splits / 4, (4 * 148 + tiles - 1) / tiles));
+    groups = std::max(groups, 2);
+    const int per = (splits + groups - 1) / groups;
+    groups = (splits + per - 1) / per;
+    const int bx = static_cast<int>(std::min<int64_t>((MN + 255) / 256, 148 * 4 / groups + 1));
+    splitk_group_kernel<<<dim3(bx, groups), 256, 0, st>>>(const_cast<float*>(P), splits, per, MN);
+    splitk_reduce_kernel<<<grid, block, 0, st>>>(P, groups, M, N, D, bias, accumulate, transpose, per);
+    return cudaGetLastError();
+  }
+  splitk_reduce_kernel<<<grid, block, 0, st>>>(P, splits, M, N, D, bias, accumulate, transpose, 1);
   return cudaGetLastError();
 }
 
@@ -448,6 +488,9 @@ cudaError_t conv_dgrad(const ConvShape& s, const float* dy, const float* w, floa
 }
 
 int conv_wgrad_splits(const ConvShape& s, int64_t partial_floats_cap) {
+  // the halo weight-gradient kernel writes one partial slice per CTA
+  if (use_tma() && s.stride == 1 && conv_halo_wgrad_ok(s.N, s.H, s.W, s.C, s.K, s.R, s.S, s.pad, s.P, s.Q))
+    return conv_halo_wgrad_splits();
   const int64_t RSC = static_cast<int64_t>(s.R) * s.S * s.C;
   const int bn = bn_for(s.K);
   const int64_t tiles = ((RSC + kBM - 1) / kBM) * ((s.K + bn - 1) / bn);
@@ -466,6 +509,12 @@ cudaError_t conv_wgrad(const ConvShape& s, const float* x, const float* dy, floa
                        int splits, float* red_scratch, cudaStream_t st) {
   cudaError_t e;
   splits = effective_splits(s.N * s.P * s.Q, splits);  // the count the launch will really use
+  if (use_tma() && s.stride == 1 && conv_halo_wgrad_ok(s.N, s.H, s.W, s.C, s.K, s.R, s.S, s.pad, s.P, s.Q)) {
+    e = conv_halo_wgrad(s.N, s.H, s.W, s.R, s.S, s.pad, s.P, s.Q, x, dy, partial, dw, st);
+    if (e != cudaSuccess) return e;
+    if (!db) return cudaSuccess;
+    return bias_grad(dy, static_cast<int64_t>(s.N) * s.P * s.Q, s.K, db, red_scratch, st);
+  }
   if (use_tma() && conv_tma_ok_wgrad(s)) {
     e = conv_wgrad_tma(s, x, dy, partial, splits, st);
   } else {

@@ -617,6 +617,10 @@ __global__ void pool_fwd_kernel(PoolShape s, const float* __restrict__ x, float*
 }
 
 // float4 over channels (C % 4 == 0); 32-bit index math (tensors < 2^31 elements).
+// KC: compile-time window (0 = runtime s.K); with it the window's loads are
+// unrolled and in flight together (the max / sum order is the same row-major
+// order either way, so replays and both variants are bit-identical).
+template <int KC>
 __global__ void pool_fwd_v4_kernel(PoolShape s, const float4* __restrict__ x, float4* __restrict__ y, int total4) {
   const int C4 = s.C >> 2;
   const float inv = 1.0f / static_cast<float>(s.K * s.K);
@@ -628,30 +632,123 @@ __global__ void pool_fwd_v4_kernel(PoolShape s, const float4* __restrict__ x, fl
     const int p = t % s.P;
     const int n = t / s.P;
     const int h0 = p * s.stride - s.pad, w0 = q * s.stride - s.pad;
-    const int hb = h0 < 0 ? 0 : h0, he = min(h0 + s.K, s.H);
-    const int wb = w0 < 0 ? 0 : w0, we = min(w0 + s.K, s.W);
     const float4* xb = x + static_cast<size_t>(n) * s.H * s.W * C4 + c4;
     float4 acc;
-    if (s.mode == 0) {
-      acc = xb[(hb * s.W + wb) * C4];
-      for (int h = hb; h < he; ++h)
-        for (int w = wb; w < we; ++w) {
-          const float4 v = xb[(h * s.W + w) * C4];
+    if constexpr (KC > 0) {
+      float4 v[KC * KC];
+      bool in[KC * KC];
+#pragma unroll
+      for (int r = 0; r < KC; ++r)
+#pragma unroll
+        for (int u = 0; u < KC; ++u) {
+          const int h = h0 + r, w = w0 + u;
+          in[r * KC + u] = h >= 0 && h < s.H && w >= 0 && w < s.W;
+          v[r * KC + u] = in[r * KC + u] ? xb[(h * s.W + w) * C4] : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      if (s.mode == 0) {
+        bool have = false;
+#pragma unroll
+        for (int k = 0; k < KC * KC; ++k) {
+          if (!in[k]) continue;
+          if (!have) {
+            acc = v[k];
+            have = true;
+          } else {
+            acc.x = v[k].x > acc.x ? v[k].x : acc.x;
+            acc.y = v[k].y > acc.y ? v[k].y : acc.y;
+            acc.z = v[k].z > acc.z ? v[k].z : acc.z;
+            acc.w = v[k].w > acc.w ? v[k].w : acc.w;
+          }
+        }
+      } else {
+        acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int k = 0; k < KC * KC; ++k)
+          if (in[k]) {
+            acc.x += v[k].x; acc.y += v[k].y; acc.z += v[k].z; acc.w += v[k].w;
+          }
+        acc.x *= inv; acc.y *= inv; acc.z *= inv; acc.w *= inv;
+      }
+    } else {
+      const int hb = h0 < 0 ? 0 : h0, he = min(h0 + s.K, s.H);
+      const int wb = w0 < 0 ? 0 : w0, we = min(w0 + s.K, s.W);
+      if (s.mode == 0) {
+        acc = xb[(hb * s.W + wb) * C4];
+        for (int h = hb; h < he; ++h)
+          for (int w = wb; w < we; ++w) {
+            const float4 v = xb[(h * s.W + w) * C4];
+            acc.x = v.x > acc.x ? v.x : acc.x;
+            acc.y = v.y > acc.y ? v.y : acc.y;
+            acc.z = v.z > acc.z ? v.z : acc.z;
+            acc.w = v.w > acc.w ? v.w : acc.w;
+          }
+      } else {
+        acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int h = hb; h < he; ++h)
+          for (int w = wb; w < we; ++w) {
+            const float4 v = xb[(h * s.W + w) * C4];
+            acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+          }
+        acc.x *= inv; acc.y *= inv; acc.z *= inv; acc.w *= inv;
+      }
+    }
+    y[i] = acc;
+  }
+}
+
+// Global pool (one output pixel per image, window = the whole image, pad 0):
+// block = (image, 128 channels); 8 pixel lanes x 32 channel quads, each lane
+// reduces pixels lane, lane+8, ... and the lanes are combined in lane order.
+// Same row-major order per lane for max; avg sums in that fixed order.
+__global__ void __launch_bounds__(256) pool_global_kernel(PoolShape s, const float4* __restrict__ x,
+                                                          float4* __restrict__ y) {
+  __shared__ float4 part[8][32];
+  const int C4 = s.C >> 2;
+  const int cq = threadIdx.x & 31, pl = threadIdx.x >> 5;
+  const int c4 = blockIdx.x * 32 + cq;
+  const int n = blockIdx.y;
+  const int HW = s.H * s.W;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  bool have = false;
+  if (c4 < C4) {
+    const float4* xb = x + static_cast<size_t>(n) * HW * C4 + c4;
+    for (int i = pl; i < HW; i += 8) {
+      const float4 v = xb[static_cast<size_t>(i) * C4];
+      if (s.mode == 0) {
+        if (!have) {
+          acc = v;
+          have = true;
+        } else {
           acc.x = v.x > acc.x ? v.x : acc.x;
           acc.y = v.y > acc.y ? v.y : acc.y;
           acc.z = v.z > acc.z ? v.z : acc.z;
           acc.w = v.w > acc.w ? v.w : acc.w;
         }
-    } else {
-      acc = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int h = hb; h < he; ++h)
-        for (int w = wb; w < we; ++w) {
-          const float4 v = xb[(h * s.W + w) * C4];
-          acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
-        }
-      acc.x *= inv; acc.y *= inv; acc.z *= inv; acc.w *= inv;
+      } else {
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+      }
     }
-    y[i] = acc;
+  }
+  part[pl][cq] = acc;
+  __syncthreads();
+  if (pl == 0 && c4 < C4) {
+    float4 r = part[0][cq];
+    for (int l = 1; l < 8 && l < HW; ++l) {
+      const float4 v = part[l][cq];
+      if (s.mode == 0) {
+        r.x = v.x > r.x ? v.x : r.x;
+        r.y = v.y > r.y ? v.y : r.y;
+        r.z = v.z > r.z ? v.z : r.z;
+        r.w = v.w > r.w ? v.w : r.w;
+      } else {
+        r.x += v.x; r.y += v.y; r.z += v.z; r.w += v.w;
+      }
+    }
+    if (s.mode == 1) {
+      const float inv = 1.0f / static_cast<float>(s.K * s.K);
+      r.x *= inv; r.y *= inv; r.z *= inv; r.w *= inv;
+    }
+    y[static_cast<size_t>(n) * C4 + c4] = r;
   }
 }
 
@@ -1269,9 +1366,15 @@ cudaError_t relu_bwd_inplace(const float* y, float* g, int64_t n, cudaStream_t s
 cudaError_t pool_fwd(const PoolShape& s, const float* x, float* y, cudaStream_t st) {
   const int64_t total = static_cast<int64_t>(s.N) * s.P * s.Q * s.C;
   if (s.C % 4 == 0 && static_cast<int64_t>(s.N) * s.H * s.W * s.C < (1ll << 31)) {
+    if (s.P == 1 && s.Q == 1 && s.pad == 0 && s.K == s.H && s.K == s.W) {
+      dim3 grid((s.C / 4 + 31) / 32, s.N);
+      pool_global_kernel<<<grid, 256, 0, st>>>(s, reinterpret_cast<const float4*>(x), reinterpret_cast<float4*>(y));
+      return cudaGetLastError();
+    }
     const int total4 = static_cast<int>(total / 4);
-    pool_fwd_v4_kernel<<<blocks_for(total4), kThreads, 0, st>>>(s, reinterpret_cast<const float4*>(x),
-                                                                  reinterpret_cast<float4*>(y), total4);
+    auto k = s.K == 3 ? pool_fwd_v4_kernel<3> : (s.K == 2 ? pool_fwd_v4_kernel<2> : pool_fwd_v4_kernel<0>);
+    k<<<blocks_for(total4), kThreads, 0, st>>>(s, reinterpret_cast<const float4*>(x), reinterpret_cast<float4*>(y),
+                                               total4);
     return cudaGetLastError();
   }
   pool_fwd_kernel<<<blocks_for(total), kThreads, 0, st>>>(s, x, y, total);

@@ -87,3 +87,76 @@ extern "C" long long sn_probe_mma_rate(int n, int kind, int iters, int accs, int
   cudaFree(d);
   return h;
 }
+
+// TMEM layout of an M = 64 tf32 MMA (cta_group::1): A [64][32] and B [64][32]
+// K-major SW128 in smem (written by threads with the absolute-address swizzle),
+// D -> TMEM at lane offset `lane0` (0 or 64), column 0; all 128 lanes x 64
+// columns are read back into out[128][64] (NaN-initialised TMEM cells stay as
+// written by a previous tcgen05.st of NaN).
+namespace sn {
+namespace {
+__global__ void __launch_bounds__(128, 1) m64_layout_kernel(const float* A, const float* B, float* out, int lane0) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;          // 64 rows x 128 B
+  uint8_t* sB = smem + 8192;   // 64 rows x 128 B
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 16384);
+  uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < 64 * 32; i += blockDim.x) {
+    const int r = i / 32, k = i % 32;
+    const uint32_t off = sw128_off(r, k / 4) + (k % 4) * 4;
+    *reinterpret_cast<float*>(sA + off) = A[i];
+    *reinterpret_cast<float*>(sB + off) = B[i];
+  }
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc(slot, 64);
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *slot;
+  // fill TMEM with NaN so untouched cells are recognisable
+  {
+    uint32_t nanv = 0x7fc00000u;
+    for (int c = 0; c < 64; ++c)
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c),
+                   "r"(nanv)
+                   : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (threadIdx.x == 0) {
+    const uint32_t idesc = idesc_tf32(64, 64, false, false);
+    for (int kk = 0; kk < 4; ++kk)
+      umma_tf32(tmem + (static_cast<uint32_t>(lane0) << 16), umma_desc(smem_u32(sA) + kk * 32, 16, 1024, kLayoutSW128),
+                umma_desc(smem_u32(sB) + kk * 32, 16, 1024, kLayoutSW128), idesc, kk ? 1u : 0u);
+    umma_commit(bar);
+  }
+  __syncwarp();
+  mbar_wait(bar, 0);
+  tc_fence_after();
+  for (int c = 0; c < 64; c += 32) {
+    float v[32];
+    tmem_ld32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c, v);
+    for (int j = 0; j < 32; ++j) out[(warp * 32 + lane) * 64 + c + j] = v[j];
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, 64);
+}
+}  // namespace
+}  // namespace sn
+
+extern "C" int sn_probe_m64_layout(const float* A, const float* B, float* out, int lane0) {
+  const int smem = 16384 + 64 + 1024;
+  cudaFuncSetAttribute(sn::m64_layout_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  sn::m64_layout_kernel<<<1, 128, smem>>>(A, B, out, lane0);
+  if (cudaGetLastError() != cudaSuccess) return 3;
+  return cudaDeviceSynchronize() == cudaSuccess ? 0 : 4;
+}

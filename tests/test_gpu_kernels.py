@@ -260,6 +260,8 @@ POOL_CASES = [
     (2, 5, 9, 9, 2, 2, 0, 0),        # C % 4 != 0: scalar path
     (2, 64, 14, 14, 7, 1, 0, 1),     # global-ish average pool
     (2, 32, 20, 20, 3, 1, 1, 0),     # stride 1 (windows overlap by two)
+    (3, 512, 7, 7, 7, 1, 0, 1),      # ResNet global average pool (one window per image)
+    (2, 64, 5, 5, 5, 1, 0, 0),       # global max pool
 ]
 
 
