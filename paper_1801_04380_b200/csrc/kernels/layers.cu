@@ -696,6 +696,58 @@ __global__ void pool_fwd_v4_kernel(PoolShape s, const float4* __restrict__ x, fl
   }
 }
 
+// One block per output row (n, p) for the common small-window case: the only
+// per-element index math left is one division by C/4.
+template <int KC, int SC>
+__global__ void __launch_bounds__(256) pool_fwd_rows_kernel(PoolShape s, const float4* __restrict__ x,
+                                                            float4* __restrict__ y) {
+  const int C4 = s.C >> 2;
+  const int p = blockIdx.x, n = blockIdx.y;
+  const int h0 = p * SC - s.pad;
+  const float inv = 1.0f / static_cast<float>(KC * KC);
+  const float4* xb = x + static_cast<size_t>(n) * s.H * s.W * C4;
+  float4* yrow = y + (static_cast<size_t>(n) * s.P + p) * s.Q * C4;
+  for (int i = threadIdx.x; i < s.Q * C4; i += blockDim.x) {
+    const int q = i / C4, c4 = i - q * C4;
+    const int w0 = q * SC - s.pad;
+    float4 v[KC * KC];
+    bool in[KC * KC];
+#pragma unroll
+    for (int r = 0; r < KC; ++r)
+#pragma unroll
+      for (int u = 0; u < KC; ++u) {
+        const int h = h0 + r, w = w0 + u;
+        in[r * KC + u] = h >= 0 && h < s.H && w >= 0 && w < s.W;
+        v[r * KC + u] = in[r * KC + u] ? xb[(h * s.W + w) * C4 + c4] : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (s.mode == 0) {
+      bool have = false;
+#pragma unroll
+      for (int k = 0; k < KC * KC; ++k) {
+        if (!in[k]) continue;
+        if (!have) {
+          acc = v[k];
+          have = true;
+        } else {
+          acc.x = v[k].x > acc.x ? v[k].x : acc.x;
+          acc.y = v[k].y > acc.y ? v[k].y : acc.y;
+          acc.z = v[k].z > acc.z ? v[k].z : acc.z;
+          acc.w = v[k].w > acc.w ? v[k].w : acc.w;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < KC * KC; ++k)
+        if (in[k]) {
+          acc.x += v[k].x; acc.y += v[k].y; acc.z += v[k].z; acc.w += v[k].w;
+        }
+      acc.x *= inv; acc.y *= inv; acc.z *= inv; acc.w *= inv;
+    }
+    yrow[i] = acc;
+  }
+}
+
 // Global pool (one output pixel per image, window = the whole image, pad 0):
 // block = (image, 128 channels); 8 pixel lanes x 32 channel quads, each lane
 // reduces pixels lane, lane+8, ... and the lanes are combined in lane order.
@@ -893,111 +945,118 @@ __global__ void pool_gather_kernel(PoolShape s, const uchar4* __restrict__ arg, 
 // neighbouring blocks (cheap) so that no element has two writers.
 constexpr int kPoolCv = 4;  // float4s per pixel chunk (16 channels)
 
-// KC = compile-time window size (0: runtime s.K): with it the window's loads
-// are unrolled and all in flight at once.
-template <int KC>
+// KC / SC = compile-time window size and stride (0: runtime s.K / s.stride):
+// the window's loads are unrolled and all in flight at once, and the index
+// arithmetic is shifts.  Threads map to (column lane = tid / 4, 16-byte
+// channel quad = tid % 4) and walk rows / columns in nested loops, so no
+// per-element divisions remain (the kernel was issue-bound on them).
+template <int KC, int SC>
 __global__ void __launch_bounds__(256) pool_max_bwd_fused(PoolShape s, const float4* __restrict__ x,
                                                           const float4* __restrict__ y,
                                                           const float4* __restrict__ dy, float4* dx,
                                                           int accumulate, int PB, int WR) {
   extern __shared__ float4 psm[];
+  const int K = KC > 0 ? KC : s.K, ST = SC > 0 ? SC : s.stride;
   float4* sdy = psm;                                                  // [WR][Q][kPoolCv]
   uchar4* sarg = reinterpret_cast<uchar4*>(psm + WR * s.Q * kPoolCv);  // [WR][Q][kPoolCv]
   const int C4 = s.C / 4;
   const int c4 = blockIdx.x * kPoolCv;
   const int band = blockIdx.y, n = blockIdx.z;
-  int h_lo = band * PB * s.stride - s.pad;
-  int h_hi = (band + 1) * PB * s.stride - s.pad - 1;
+  int h_lo = band * PB * ST - s.pad;
+  int h_hi = (band + 1) * PB * ST - s.pad - 1;
   if (band == 0) h_lo = 0;
   if (band == gridDim.y - 1) h_hi = s.H - 1;
   if (h_lo < 0) h_lo = 0;
   if (h_hi > s.H - 1) h_hi = s.H - 1;
-  const int t = h_lo + s.pad - s.K + 1;
-  const int pl = t <= 0 ? 0 : (t + s.stride - 1) / s.stride;
-  int ph = (h_hi + s.pad) / s.stride;
+  const int t = h_lo + s.pad - K + 1;
+  const int pl = t <= 0 ? 0 : (t + ST - 1) / ST;
+  int ph = (h_hi + s.pad) / ST;
   if (ph > s.P - 1) ph = s.P - 1;
-  const int nwin = (ph - pl + 1) * s.Q * kPoolCv;
-  const float4* xn = x + static_cast<int64_t>(n) * s.H * s.W * C4 + c4;
-  for (int i = threadIdx.x; i < nwin; i += blockDim.x) {
-    const int cv = i % kPoolCv;
-    const int pq = i / kPoolCv;
-    const int q = pq % s.Q, pr = pq / s.Q;
-    const int p = pl + pr;
-    const int64_t o = ((static_cast<int64_t>(n) * s.P + p) * s.Q + q) * C4 + c4 + cv;
-    const float4 m = y[o];
-    const int h0 = p * s.stride - s.pad, w0 = q * s.stride - s.pad;
-    int a0 = 255, a1 = 255, a2 = 255, a3 = 255;
-    const float4 g = dy[o];
-    if constexpr (KC > 0) {
-      float4 v[KC * KC];
+  const int cv = threadIdx.x & 3, lane = threadIdx.x >> 2;
+  const float4* xn = x + static_cast<int64_t>(n) * s.H * s.W * C4 + c4 + cv;
+  // phase 1: argmax (first row-major match) and dy of every window touching the band
+  for (int p = pl; p <= ph; ++p) {
+    const int h0 = p * ST - s.pad;
+    const int64_t orow = (static_cast<int64_t>(n) * s.P + p) * s.Q;
+    for (int q = lane; q < s.Q; q += 64) {
+      const int64_t o = (orow + q) * C4 + c4 + cv;
+      const float4 m = y[o];
+      const float4 g = dy[o];
+      const int w0 = q * ST - s.pad;
+      int a0 = 255, a1 = 255, a2 = 255, a3 = 255;
+      if constexpr (KC > 0) {
+        float4 v[KC * KC];
 #pragma unroll
-      for (int r = 0; r < KC; ++r)
+        for (int r = 0; r < KC; ++r)
 #pragma unroll
-        for (int u = 0; u < KC; ++u) {
-          const int h = h0 + r, w = w0 + u;
-          const bool in = h >= 0 && h < s.H && w >= 0 && w < s.W;
-          // out-of-image taps can never equal the maximum: NaN
-          v[r * KC + u] = in ? xn[(static_cast<int64_t>(h) * s.W + w) * C4 + cv]
-                             : make_float4(NAN, NAN, NAN, NAN);
+          for (int u = 0; u < KC; ++u) {
+            const int h = h0 + r, w = w0 + u;
+            const bool in = h >= 0 && h < s.H && w >= 0 && w < s.W;
+            // out-of-image taps can never equal the maximum: NaN
+            v[r * KC + u] = in ? xn[(static_cast<int64_t>(h) * s.W + w) * C4] : make_float4(NAN, NAN, NAN, NAN);
+          }
+#pragma unroll
+        for (int k = KC * KC - 1; k >= 0; --k) {  // descending: the first (row-major) match wins
+          if (v[k].x == m.x) a0 = k;
+          if (v[k].y == m.y) a1 = k;
+          if (v[k].z == m.z) a2 = k;
+          if (v[k].w == m.w) a3 = k;
         }
-#pragma unroll
-      for (int k = KC * KC - 1; k >= 0; --k) {  // descending: the first (row-major) match wins
-        if (v[k].x == m.x) a0 = k;
-        if (v[k].y == m.y) a1 = k;
-        if (v[k].z == m.z) a2 = k;
-        if (v[k].w == m.w) a3 = k;
-      }
-    } else {
-      for (int r = 0; r < s.K; ++r) {
-        const int h = h0 + r;
-        if (h < 0 || h >= s.H) continue;
-        for (int u = 0; u < s.K; ++u) {
-          const int w = w0 + u;
-          if (w < 0 || w >= s.W) continue;
-          const float4 v = xn[(static_cast<int64_t>(h) * s.W + w) * C4 + cv];
-          const int off = r * s.K + u;
-          if (a0 == 255 && v.x == m.x) a0 = off;
-          if (a1 == 255 && v.y == m.y) a1 = off;
-          if (a2 == 255 && v.z == m.z) a2 = off;
-          if (a3 == 255 && v.w == m.w) a3 = off;
+      } else {
+        for (int r = 0; r < K; ++r) {
+          const int h = h0 + r;
+          if (h < 0 || h >= s.H) continue;
+          for (int u = 0; u < K; ++u) {
+            const int w = w0 + u;
+            if (w < 0 || w >= s.W) continue;
+            const float4 v = xn[(static_cast<int64_t>(h) * s.W + w) * C4];
+            const int off = r * K + u;
+            if (a0 == 255 && v.x == m.x) a0 = off;
+            if (a1 == 255 && v.y == m.y) a1 = off;
+            if (a2 == 255 && v.z == m.z) a2 = off;
+            if (a3 == 255 && v.w == m.w) a3 = off;
+          }
         }
       }
+      const int j = ((p - pl) * s.Q + q) * kPoolCv + cv;
+      sarg[j] = make_uchar4(a0, a1, a2, a3);
+      sdy[j] = g;
     }
-    sarg[i] = make_uchar4(a0, a1, a2, a3);
-    sdy[i] = g;
   }
   __syncthreads();
-  const int nin = (h_hi - h_lo + 1) * s.W * kPoolCv;
-  float4* dxn = dx + static_cast<int64_t>(n) * s.H * s.W * C4 + c4;
-  for (int i = threadIdx.x; i < nin; i += blockDim.x) {
-    const int cv = i % kPoolCv;
-    const int hw = i / kPoolCv;
-    const int w = hw % s.W, h = h_lo + hw / s.W;
-    int plo = h + s.pad - s.K + 1, qlo = w + s.pad - s.K + 1;
-    plo = plo <= 0 ? 0 : (plo + s.stride - 1) / s.stride;
-    qlo = qlo <= 0 ? 0 : (qlo + s.stride - 1) / s.stride;
-    int phi = (h + s.pad) / s.stride, qhi = (w + s.pad) / s.stride;
+  // phase 2: gather each input element of the band from the windows covering it
+  float4* dxn = dx + static_cast<int64_t>(n) * s.H * s.W * C4 + c4 + cv;
+  for (int h = h_lo; h <= h_hi; ++h) {
+    int plo = h + s.pad - K + 1;
+    plo = plo <= 0 ? 0 : (plo + ST - 1) / ST;
+    int phi = (h + s.pad) / ST;
     if (phi > s.P - 1) phi = s.P - 1;
-    if (qhi > s.Q - 1) qhi = s.Q - 1;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int p = plo; p <= phi; ++p) {
-      for (int q = qlo; q <= qhi; ++q) {
-        const int j = ((p - pl) * s.Q + q) * kPoolCv + cv;
-        const int off = (h - (p * s.stride - s.pad)) * s.K + (w - (q * s.stride - s.pad));
-        const uchar4 a = sarg[j];
-        const float4 g = sdy[j];
-        if (a.x == off) acc.x += g.x;
-        if (a.y == off) acc.y += g.y;
-        if (a.z == off) acc.z += g.z;
-        if (a.w == off) acc.w += g.w;
+    for (int w = lane; w < s.W; w += 64) {
+      int qlo = w + s.pad - K + 1;
+      qlo = qlo <= 0 ? 0 : (qlo + ST - 1) / ST;
+      int qhi = (w + s.pad) / ST;
+      if (qhi > s.Q - 1) qhi = s.Q - 1;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int p = plo; p <= phi; ++p) {
+        const int roff = (h - (p * ST - s.pad)) * K;
+        for (int q = qlo; q <= qhi; ++q) {
+          const int j = ((p - pl) * s.Q + q) * kPoolCv + cv;
+          const int off = roff + (w - (q * ST - s.pad));
+          const uchar4 a = sarg[j];
+          const float4 g = sdy[j];
+          if (a.x == off) acc.x += g.x;
+          if (a.y == off) acc.y += g.y;
+          if (a.z == off) acc.z += g.z;
+          if (a.w == off) acc.w += g.w;
+        }
       }
+      float4* d = dxn + (static_cast<int64_t>(h) * s.W + w) * C4;
+      if (accumulate) {
+        const float4 o = *d;
+        acc.x += o.x; acc.y += o.y; acc.z += o.z; acc.w += o.w;
+      }
+      *d = acc;
     }
-    float4* d = dxn + (static_cast<int64_t>(h) * s.W + w) * C4 + cv;
-    if (accumulate) {
-      const float4 o = *d;
-      acc.x += o.x; acc.y += o.y; acc.z += o.z; acc.w += o.w;
-    }
-    *d = acc;
   }
 }
 
@@ -1371,6 +1430,11 @@ cudaError_t pool_fwd(const PoolShape& s, const float* x, float* y, cudaStream_t 
       pool_global_kernel<<<grid, 256, 0, st>>>(s, reinterpret_cast<const float4*>(x), reinterpret_cast<float4*>(y));
       return cudaGetLastError();
     }
+    if (s.K == 3 && s.stride == 2) {
+      pool_fwd_rows_kernel<3, 2><<<dim3(s.P, s.N), 256, 0, st>>>(s, reinterpret_cast<const float4*>(x),
+                                                                 reinterpret_cast<float4*>(y));
+      return cudaGetLastError();
+    }
     const int total4 = static_cast<int>(total / 4);
     auto k = s.K == 3 ? pool_fwd_v4_kernel<3> : (s.K == 2 ? pool_fwd_v4_kernel<2> : pool_fwd_v4_kernel<0>);
     k<<<blocks_for(total4), kThreads, 0, st>>>(s, reinterpret_cast<const float4*>(x), reinterpret_cast<float4*>(y),
@@ -1408,7 +1472,10 @@ cudaError_t pool_bwd(const PoolShape& s, const float* x, const float* y, const f
   size_t smem;
   if (pool_fused_ok(s, &PB, &WR, &smem)) {
     dim3 grid(s.C / (4 * kPoolCv), (s.P + PB - 1) / PB, s.N);
-    auto k = s.K == 3 ? pool_max_bwd_fused<3> : (s.K == 2 ? pool_max_bwd_fused<2> : pool_max_bwd_fused<0>);
+    auto k = (s.K == 3 && s.stride == 2)   ? pool_max_bwd_fused<3, 2>
+             : (s.K == 2 && s.stride == 2) ? pool_max_bwd_fused<2, 2>
+             : s.K == 3                    ? pool_max_bwd_fused<3, 0>
+                                           : pool_max_bwd_fused<0, 0>;
     k<<<grid, 256, smem, st>>>(s, reinterpret_cast<const float4*>(x), reinterpret_cast<const float4*>(y),
                                reinterpret_cast<const float4*>(dy), reinterpret_cast<float4*>(dx), accumulate, PB,
                                WR);
