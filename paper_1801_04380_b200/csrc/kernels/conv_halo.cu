@@ -227,9 +227,18 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
           float v[32];
           tmem_ld32(tbase + static_cast<uint32_t>(c), v);
           if (a.bias) {
+            if (n0 + c + 32 <= a.N) {  // 16-byte loads (parameter slices are 256-byte aligned)
+              const float4* b4 = reinterpret_cast<const float4*>(a.bias + n0 + c);
 #pragma unroll
-            for (int q = 0; q < 32; ++q)
-              if (n0 + c + q < a.N) v[q] += __ldg(a.bias + n0 + c + q);
+              for (int q4 = 0; q4 < 8; ++q4) {
+                const float4 bq = __ldg(b4 + q4);
+                v[4 * q4] += bq.x; v[4 * q4 + 1] += bq.y; v[4 * q4 + 2] += bq.z; v[4 * q4 + 3] += bq.w;
+              }
+            } else {
+#pragma unroll
+              for (int q = 0; q < 32; ++q)
+                if (n0 + c + q < a.N) v[q] += __ldg(a.bias + n0 + c + q);
+            }
           }
           const uint32_t buf = smem_u32(sEpi) + (chunk_no & 1u) * (kBM * 128);
           if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
@@ -253,29 +262,20 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
             bulk_commit();
           }
           if (a.stats) {
-            // column `lane` of the staged chunk over this warp's rows; invalid
-            // (junk) rows are skipped; shift = the sub-tile's row 0 (always real
-            // unless the whole sub-tile lies past P, then count = 0)
+            // junk rows (padded columns x' >= Q, rows past P) are skipped; the
+            // shift is the sub-tile's row 0 (real unless the whole sub-tile lies
+            // past P, then its count is 0 and the reduction skips it)
             const uint8_t* sb = sEpi + (chunk_no & 1u) * (kBM * 128);
-            const uint32_t cq = static_cast<uint32_t>(lane) >> 2, cr = (static_cast<uint32_t>(lane) & 3u) * 4;
-            const float shift = *reinterpret_cast<const float*>(sb + sw128_off(0, cq) + cr);
-            float s1 = 0.f, s2 = 0.f;
-            for (int rr = 32 * warp; rr < 32 * warp + 32; ++rr) {
-              const int xx = rr % a.Wp, yy = rr / a.Wp;
-              if (yy >= a.TR || xx >= a.Q || ys + yy >= a.P) continue;
-              const float d = *reinterpret_cast<const float*>(sb + sw128_off(rr, cq) + cr) - shift;
-              s1 += d;
-              s2 = fmaf(d, d, s2);
-            }
-            sred[(warp * 32 + lane) * 2] = s1;
-            sred[(warp * 32 + lane) * 2 + 1] = s2;
-            named_bar(1, 128);
+            const int Wp = a.Wp, TR = a.TR, Q = a.Q, rows_left = a.P - ys;
+            float shift, t1, t2;
+            chunk_column_stats(
+                sb,
+                [=](int rr) {
+                  const int yy = rr / Wp, xx = rr - yy * Wp;
+                  return yy < TR && xx < Q && yy < rows_left;
+                },
+                sred, shift, t1, t2);
             if (warp == 0 && n0 + c + lane < a.N) {
-              float t1 = sred[lane * 2], t2 = sred[lane * 2 + 1];
-              for (int w = 1; w < 4; ++w) {
-                t1 += sred[(w * 32 + lane) * 2];
-                t2 += sred[(w * 32 + lane) * 2 + 1];
-              }
               const int rows_valid = max(0, min(a.TR, a.P - ys)) * a.Q;
               const size_t tile = (static_cast<size_t>(t / a.n_tiles) * MT + j);
               float* out = a.stats + tile * 4 * a.N + n0 + c + lane;

@@ -479,9 +479,18 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
           float v[32];
           tmem_ld32(tbase + static_cast<uint32_t>(c), v);
           if (e.bias) {
+            if (n0 + c + 32 <= e.N) {  // 16-byte loads (parameter slices are 256-byte aligned)
+              const float4* b4 = reinterpret_cast<const float4*>(e.bias + n0 + c);
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (n0 + c + j < e.N) v[j] += __ldg(e.bias + n0 + c + j);
+              for (int q4 = 0; q4 < 8; ++q4) {
+                const float4 bq = __ldg(b4 + q4);
+                v[4 * q4] += bq.x; v[4 * q4 + 1] += bq.y; v[4 * q4 + 2] += bq.z; v[4 * q4 + 3] += bq.w;
+              }
+            } else {
+#pragma unroll
+              for (int q = 0; q < 32; ++q)
+                if (n0 + c + q < e.N) v[q] += __ldg(e.bias + n0 + c + q);
+            }
           }
           const uint32_t buf = sEpi + (chunk_no & 1u) * (kBM * 128);
           // the store issued two chunks ago from this buffer must have read it
@@ -506,28 +515,12 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             bulk_commit();
           }
           if (e.stats) {
-            // column `lane` of the staged 128 x 32 chunk, rows 32*warp.. of this warp
             const int nv = MODE == 2 ? a.Q : min(kBM, e.M - m0);
             const uint8_t* sb = smem + L::EPI_OFF + (chunk_no & 1u) * (kBM * 128);
-            const uint32_t cq = static_cast<uint32_t>(lane) >> 2, cr = (static_cast<uint32_t>(lane) & 3u) * 4;
-            const float shift = *reinterpret_cast<const float*>(sb + sw128_off(0, cq) + cr);
-            float s1 = 0.f, s2 = 0.f;
-            const int r1 = min(nv, 32 * (warp + 1));
-            for (int r = 32 * warp; r < r1; ++r) {
-              const float d = *reinterpret_cast<const float*>(sb + sw128_off(r, cq) + cr) - shift;
-              s1 += d;
-              s2 = fmaf(d, d, s2);
-            }
-            float* sred = reinterpret_cast<float*>(smem + L::STATS_OFF);
-            sred[(warp * 32 + lane) * 2] = s1;
-            sred[(warp * 32 + lane) * 2 + 1] = s2;
-            named_bar(1, 128);
+            float shift, t1, t2;
+            chunk_column_stats(sb, [&](int r) { return r < nv; }, reinterpret_cast<float*>(smem + L::STATS_OFF),
+                               shift, t1, t2);
             if (warp == 0 && n0 + c + lane < e.N) {
-              float t1 = sred[lane * 2], t2 = sred[lane * 2 + 1];
-              for (int w = 1; w < 4; ++w) {
-                t1 += sred[(w * 32 + lane) * 2];
-                t2 += sred[(w * 32 + lane) * 2 + 1];
-              }
               float* out = e.stats + static_cast<size_t>(m0 / kBM) * 3 * e.N + n0 + c + lane;
               out[0] = shift;
               out[e.N] = t1;
@@ -976,6 +969,196 @@ cudaError_t stem_pad_input(const ConvShape& s, int H_raw, int W_raw, int C_raw, 
   return cudaGetLastError();
 }
 
+namespace {
+
+// Stem forward, RT output rows per tile (one 128-row accumulator each): the
+// whole filter (R k-blocks of 64 x 32, <= 64 output channels) is loaded into
+// SMEM once per CTA, and the sliding-window view of each padded input row
+// (one TMA box) is loaded once per tile and feeds every output row of the tile
+// that uses it -- (RT-1)*stride + R row loads per RT output rows instead of
+// R per row, and no per-tile weight traffic (the 1-row kernel was bound by
+// its L2 -> SMEM operand traffic).
+constexpr int kStemRT = 4;
+constexpr int kStemRing = 8;
+struct StemRowsArgs {
+  int N, P, Q, R, stride, K, rows_in;  // rows_in = (RT-1)*stride + R input rows per tile
+  int tiles;                           // N * ceil(P / RT)
+  const float* bias;
+  float* stats;                        // [N*P][3][K] tile statistics (tile = output row), or null
+};
+
+__global__ void __launch_bounds__(kTmaThreads, 1)
+    stem_rows_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW,
+                     const __grid_constant__ CUtensorMap tmD, StemRowsArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int A_BYTES = kBM * 128, W_BYTES = 64 * 128;
+  uint8_t* sA = smem;                                  // kStemRing input-row views
+  uint8_t* sW = sA + kStemRing * A_BYTES;              // R weight k-blocks (resident)
+  uint8_t* sEpi = sW + 8 * W_BYTES;                    // 2 x 16 KB store staging
+  uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + 2 * kBM * 128);
+  uint64_t* empty = full + kStemRing;
+  uint64_t* wbar = empty + kStemRing;
+  uint64_t* tfull = wbar + 1;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* sred = reinterpret_cast<float*>(tmem_slot + 4);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int bands = (a.P + kStemRT - 1) / kStemRT;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kStemRing; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(wbar, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 128);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 5) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 4) {
+    if (elect_one()) {
+      mbar_arrive_expect_tx(wbar, a.R * W_BYTES);
+      for (int r = 0; r < a.R; ++r) tma_load_2d(smem_u32(sW + r * W_BYTES), &tmW, wbar, r * 32, 0);
+    }
+    __syncwarp();
+    uint32_t s = 0, ph = 0;
+    bool wrap = false;
+    for (int t = blockIdx.x; t < a.tiles; t += gridDim.x) {
+      const int n = t / bands, p0 = (t - n * bands) * kStemRT;
+      for (int j = 0; j < a.rows_in; ++j) {
+        if (wrap) mbar_wait(&empty[s], ph ^ 1);
+        if (elect_one()) {
+          mbar_arrive_expect_tx(&full[s], A_BYTES);
+          tma_load_4d(smem_u32(sA + s * A_BYTES), &tmA, &full[s], 0, 0, p0 * a.stride + j, n);
+        }
+        __syncwarp();
+        if (++s == kStemRing) {
+          s = 0;
+          ph ^= 1;
+          wrap = true;
+        }
+      }
+    }
+  } else if (warp == 5) {
+    constexpr uint32_t idesc = idesc_tf32(kBM, 64, false, false);
+    const uint64_t ad0 = umma_desc(smem_u32(sA), 16, 1024, kLayoutSW128);
+    const uint64_t wd0 = umma_desc(smem_u32(sW), 16, 1024, kLayoutSW128);
+    mbar_wait(wbar, 0);
+    uint32_t s = 0, ph = 0;
+    int local = 0;
+    for (int t = blockIdx.x; t < a.tiles; t += gridDim.x, ++local) {
+      const int acc = local & 1;
+      if (local >= 2) mbar_wait(&tempty[acc], ((local >> 1) - 1) & 1);
+      tc_fence_after();
+      const uint32_t d0 = tmem + static_cast<uint32_t>(acc * kStemRT * 64);
+      for (int j = 0; j < a.rows_in; ++j) {
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint64_t ad = ad0 + s * (A_BYTES >> 4);
+#pragma unroll
+          for (int i = 0; i < kStemRT; ++i) {
+            const int r = j - i * a.stride;  // filter row this input row is for output row p0 + i
+            if (r < 0 || r >= a.R) continue;
+            const uint64_t wd = wd0 + static_cast<uint32_t>(r) * (W_BYTES >> 4);
+#pragma unroll
+            for (int kk = 0; kk < kBK / 8; ++kk)
+              umma_tf32(d0 + i * 64, ad + kk * 2, wd + kk * 2, idesc, (r | kk) != 0 ? 1u : 0u);
+          }
+          umma_commit(&empty[s]);
+        }
+        __syncwarp();
+        if (++s == kStemRing) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+      if (elect_one()) umma_commit(&tfull[acc]);
+      __syncwarp();
+    }
+  } else {
+    const uint32_t row = warp * 32 + lane;
+    int local = 0;
+    uint32_t chunk_no = 0;
+    for (int t = blockIdx.x; t < a.tiles; t += gridDim.x, ++local) {
+      const int n = t / bands, p0 = (t - n * bands) * kStemRT;
+      const int acc = local & 1;
+      mbar_wait(&tfull[acc], (local >> 1) & 1);
+      tc_fence_after();
+      for (int i = 0; i < kStemRT; ++i) {
+        const int p = p0 + i;
+        const uint32_t tbase = tmem + static_cast<uint32_t>((acc * kStemRT + i) * 64) +
+                               (static_cast<uint32_t>(warp * 32) << 16);
+#pragma unroll 1
+        for (int c = 0; c < 64; c += 32, ++chunk_no) {
+          if (c >= a.K) break;
+          float v[32];
+          tmem_ld32(tbase + static_cast<uint32_t>(c), v);
+          if (a.bias) {
+            if (c + 32 <= a.K) {  // 16-byte loads (parameter slices are 256-byte aligned)
+              const float4* b4 = reinterpret_cast<const float4*>(a.bias + c);
+#pragma unroll
+              for (int q4 = 0; q4 < 8; ++q4) {
+                const float4 bq = __ldg(b4 + q4);
+                v[4 * q4] += bq.x; v[4 * q4 + 1] += bq.y; v[4 * q4 + 2] += bq.z; v[4 * q4 + 3] += bq.w;
+              }
+            } else {
+#pragma unroll
+              for (int q = 0; q < 32; ++q)
+                if (c + q < a.K) v[q] += __ldg(a.bias + c + q);
+            }
+          }
+          const uint32_t buf = smem_u32(sEpi) + (chunk_no & 1u) * (kBM * 128);
+          if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          named_bar(1, 128);
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(buf + sw128_off(row, q)), "f"(v[4 * q]),
+                         "f"(v[4 * q + 1]), "f"(v[4 * q + 2]), "f"(v[4 * q + 3])
+                         : "memory");
+          fence_proxy_async();
+          named_bar(1, 128);
+          if (threadIdx.x == 0 && p < a.P) {
+            tma_store_4d(&tmD, buf, c, 0, p, n);
+            bulk_commit();
+          }
+          if (a.stats && p < a.P) {
+            const uint8_t* sb = sEpi + (chunk_no & 1u) * (kBM * 128);
+            float shift, t1, t2;
+            const int Q = a.Q;
+            chunk_column_stats(sb, [Q](int r) { return r < Q; }, sred, shift, t1, t2);
+            if (warp == 0 && c + lane < a.K) {
+              float* out = a.stats + (static_cast<size_t>(n) * a.P + p) * 3 * a.K + c + lane;
+              out[0] = shift;
+              out[a.K] = t1;
+              out[2 * static_cast<size_t>(a.K)] = t2;
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+    }
+    if (threadIdx.x == 0) bulk_wait_all();
+  }
+  __syncthreads();
+  if (warp == 5) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+}  // namespace
+
 cudaError_t conv_stem_fwd(const ConvShape& s, const float* xp, const float* w, float* wp_scratch, const float* bias,
                           float* y, float* stats, cudaStream_t st) {
   const StemGeom g = stem_geom(s);
@@ -983,6 +1166,32 @@ cudaError_t conv_stem_fwd(const ConvShape& s, const float* xp, const float* w, f
   stem_weights_kernel<<<148, 256, 0, st>>>(const_cast<float*>(w), wp_scratch, s.K, s.R, s.S, Sp, 1);
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return err;
+  if (s.K <= 64 && g.sblocks == 1 && s.R <= 8) {
+    CUtensorMap A, W, D;
+    if (!make_stem_view(&A, xp, g, kBM, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;
+    if (!make_tiled(&W, wp_scratch, s.K, s.R * Sp * 4, 64, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;
+    if (!make_nhwc4(&D, y, s.N, s.P, s.Q, s.K, kBM, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;
+    StemRowsArgs ra{};
+    ra.N = s.N;
+    ra.P = s.P;
+    ra.Q = s.Q;
+    ra.R = s.R;
+    ra.stride = s.stride;
+    ra.K = s.K;
+    ra.rows_in = (kStemRT - 1) * s.stride + s.R;
+    ra.tiles = s.N * ((s.P + kStemRT - 1) / kStemRT);
+    ra.bias = bias;
+    ra.stats = stats;
+    const int smem = kStemRing * kBM * 128 + 8 * 64 * 128 + 2 * kBM * 128 + 512 + 1024 + 1024;
+    static bool attr = false;
+    if (!attr) {
+      err = cudaFuncSetAttribute(stem_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (err != cudaSuccess) return err;
+      attr = true;
+    }
+    stem_rows_kernel<<<std::min(ra.tiles, num_sms()), kTmaThreads, smem, st>>>(A, W, D, ra);
+    return cudaGetLastError();
+  }
   const int BN = bn_for(s.K);
   CUtensorMap A, B, D;
   if (!make_stem_view(&A, xp, g, kBM, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;

@@ -226,4 +226,54 @@ __device__ __forceinline__ uint32_t sw128_off(uint32_t row, uint32_t chunk) {
   return (row << 7) + (((chunk ^ row) & 7u) << 4);
 }
 
+// Per-column statistics of one staged epilogue chunk (128 rows x 32 fp32 in
+// SWIZZLE_128B layout, 1024-aligned), over the rows valid(r) (row 0 must be
+// valid: it is the shift).  128 threads: thread t owns column quad t & 7 and
+// rows 8 * (t >> 3) .. +7 (16-byte shared loads), the four row groups of a
+// warp are combined with shuffles, the four warps in warp order by warp 0
+// through sred ([4][32][2] floats) -- a fixed order, so deterministic.
+// Warp 0 lane l returns column l's {shift, sum(y - shift), sum((y - shift)^2)}.
+template <class Valid>
+__device__ __forceinline__ void chunk_column_stats(const uint8_t* sb, Valid valid, float* sred, float& shift_out,
+                                                   float& s1_out, float& s2_out) {
+  const int t = threadIdx.x & 127, cq = t & 7, rg = t >> 3;
+  const float4 sh = *reinterpret_cast<const float4*>(sb + sw128_off(0, cq));
+  float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int r = rg * 8 + i;
+    if (!valid(r)) continue;
+    const float4 v = *reinterpret_cast<const float4*>(sb + sw128_off(r, cq));
+    const float d0 = v.x - sh.x, d1 = v.y - sh.y, d2 = v.z - sh.z, d3 = v.w - sh.w;
+    a.x += d0; a.y += d1; a.z += d2; a.w += d3;
+    b.x = fmaf(d0, d0, b.x); b.y = fmaf(d1, d1, b.y); b.z = fmaf(d2, d2, b.z); b.w = fmaf(d3, d3, b.w);
+  }
+  // row groups rg, rg^1, rg^2, rg^3 of a warp sit at lanes cq + 8k
+#pragma unroll
+  for (int off = 8; off <= 16; off <<= 1) {
+    a.x += __shfl_xor_sync(0xffffffffu, a.x, off); a.y += __shfl_xor_sync(0xffffffffu, a.y, off);
+    a.z += __shfl_xor_sync(0xffffffffu, a.z, off); a.w += __shfl_xor_sync(0xffffffffu, a.w, off);
+    b.x += __shfl_xor_sync(0xffffffffu, b.x, off); b.y += __shfl_xor_sync(0xffffffffu, b.y, off);
+    b.z += __shfl_xor_sync(0xffffffffu, b.z, off); b.w += __shfl_xor_sync(0xffffffffu, b.w, off);
+  }
+  const int warp = t >> 5, lane = t & 31;
+  if (lane < 8) {
+    float* o = sred + (warp * 32 + 4 * cq) * 2;
+    o[0] = a.x; o[1] = b.x; o[2] = a.y; o[3] = b.y; o[4] = a.z; o[5] = b.z; o[6] = a.w; o[7] = b.w;
+  }
+  named_bar(1, 128);
+  if (warp == 0) {
+    float t1 = sred[lane * 2], t2 = sred[lane * 2 + 1];
+    for (int w = 1; w < 4; ++w) {
+      t1 += sred[(w * 32 + lane) * 2];
+      t2 += sred[(w * 32 + lane) * 2 + 1];
+    }
+    const int q = lane >> 2, e = lane & 3;
+    const float4 sh0 = *reinterpret_cast<const float4*>(sb + sw128_off(0, q));
+    shift_out = e == 0 ? sh0.x : (e == 1 ? sh0.y : (e == 2 ? sh0.z : sh0.w));
+    s1_out = t1;
+    s2_out = t2;
+  }
+}
+
 }  // namespace sn
