@@ -469,7 +469,8 @@ struct HaloWgArgs {
   uint32_t xbox_bytes, dybox_bytes;           // one TMA box (one 32-channel chunk)
   uint32_t xslot, dyslot;                     // smem bytes per chunk buffer (with zeroed slack rows)
   int ksteps;                                 // ceil(TR*Wp / 8)
-  float* partial;                             // [gridDim.x][R*S*64][64]
+  float* partial;                             // [gridDim.x][R*S*Ct][Kt]
+  int c0, k0, Ct, Kt;                         // this 64 x 64 sub-problem's channel / k offsets, full C / K
 };
 
 constexpr int kWgStages = 2;
@@ -520,8 +521,8 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
         uint8_t* st = smem + s * stage_bytes;
         mbar_arrive_expect_tx(&full[s], 2 * a.xbox_bytes + 2 * a.dybox_bytes);
         for (int c = 0; c < 2; ++c) {
-          tma_load_4d(smem_u32(st + c * a.xslot), &tmX, &full[s], c * 32, -a.pad, y0 - a.pad, n);
-          tma_load_4d(smem_u32(st + 2 * a.xslot + c * a.dyslot), &tmDY, &full[s], c * 32, 0, y0, n);
+          tma_load_4d(smem_u32(st + c * a.xslot), &tmX, &full[s], a.c0 + c * 32, -a.pad, y0 - a.pad, n);
+          tma_load_4d(smem_u32(st + 2 * a.xslot + c * a.dyslot), &tmDY, &full[s], a.k0 + c * 32, 0, y0, n);
         }
       }
       __syncwarp();
@@ -580,11 +581,14 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
     __syncwarp();
   } else {
     // epilogue: warp w, lane l -> tap 2b + (l >= 16), channel 16 w + (l & 15)
-    const int RSC = taps * 64;
-    float* out = a.partial + static_cast<size_t>(blockIdx.x) * RSC * 64;
+    const int RSC = taps * a.Ct;
+    float* out = a.partial + static_cast<size_t>(blockIdx.x) * RSC * a.Kt;
     if (u0 >= u1) {
-      // no work: this CTA's slice is zero
-      for (int i = threadIdx.x; i < RSC * 64; i += 128) out[i] = 0.f;
+      // no work: this CTA's block of the slice is zero
+      for (int i = threadIdx.x; i < taps * 64 * 64; i += 128) {
+        const int tap = i / 4096, c = (i / 64) % 64, k = i % 64;
+        out[(static_cast<size_t>(tap) * a.Ct + a.c0 + c) * a.Kt + a.k0 + k] = 0.f;
+      }
     } else {
       mbar_wait(done, 0);
       tc_fence_after();
@@ -595,7 +599,8 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
           float v[32];
           tmem_ld32(tmem + static_cast<uint32_t>(b * 64 + k0) + (static_cast<uint32_t>(warp * 32) << 16), v);
           if (tap < taps) {
-            float4* dst = reinterpret_cast<float4*>(out + (static_cast<size_t>(tap) * 64 + c) * 64 + k0);
+            float4* dst =
+                reinterpret_cast<float4*>(out + (static_cast<size_t>(tap) * a.Ct + a.c0 + c) * a.Kt + a.k0 + k0);
 #pragma unroll
             for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
           }
@@ -613,9 +618,20 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
 
 }  // namespace
 
-// Applicable: C == K == 64, stride 1, padded width <= 128 rows per band.
+int conv_halo_wgrad_splits();
+
+// Applicable: C, K multiples of 64 (run as (C/64) x (K/64) sub-problems of
+// 64 x 64, each re-reading its x / dy chunks), stride 1, padded width <= 128
+// rows per band; by shape only up to C, K <= 128 (the sub-problems multiply
+// the operand traffic; at 256 channels the im2col kernel is as fast).
 bool conv_halo_wgrad_ok(int N, int H, int W, int C, int K, int R, int S, int pad, int P, int Q) {
-  if (halo_mode() == 0 || C != 64 || K != 64 || R * S < 2 || R * S > 10 || !tma_encoders_ok()) return false;
+  if (halo_mode() == 0 || C % 64 != 0 || K % 64 != 0 || R * S < 2 || R * S > 10 || !tma_encoders_ok()) return false;
+  // by shape only C = K = 64: the sub-problems re-read x / dy and each writes a
+  // full partial slice per CTA; at C = K = 128 the im2col kernel is faster
+  // (profiles/r01_conv_bench_wgrad_halo.txt: 222 vs 260 us on ResNet stage 2)
+  if (halo_mode() == 1 && (C > 64 || K > 64)) return false;
+  // one R*S*C*K partial slice per CTA must fit the executor's split-K scratch (64 Mi floats)
+  if (static_cast<int64_t>(conv_halo_wgrad_splits()) * R * S * C * K > (64ll << 20)) return false;
   if (P != H + 2 * pad - R + 1 || Q != W + 2 * pad - S + 1 || pad < 0) return false;
   const int Wp = W + 2 * pad;
   if (Wp > kBM) return false;
@@ -638,10 +654,10 @@ int conv_halo_wgrad_splits() {
   return n;
 }
 
-// partial: conv_halo_wgrad_splits() * R*S*64*64 floats; dw[64][R][S][64].
-cudaError_t conv_halo_wgrad(int N, int H, int W, int R, int S, int pad, int P, int Q, const float* x,
+// partial: conv_halo_wgrad_splits() * R*S*C*K floats; dw[K][R][S][C].
+cudaError_t conv_halo_wgrad(int N, int H, int W, int C, int K, int R, int S, int pad, int P, int Q, const float* x,
                             const float* dy, float* partial, float* dw, cudaStream_t st) {
-  if (!conv_halo_wgrad_ok(N, H, W, 64, 64, R, S, pad, P, Q)) return cudaErrorInvalidValue;
+  if (!conv_halo_wgrad_ok(N, H, W, C, K, R, S, pad, P, Q)) return cudaErrorInvalidValue;
   HaloWgArgs a{};
   a.Wp = W + 2 * pad;
   a.TR = std::min(kBM / a.Wp, P);
@@ -659,18 +675,25 @@ cudaError_t conv_halo_wgrad(int N, int H, int W, int R, int S, int pad, int P, i
   a.dyslot = (((a.TR * a.Wp + 7) / 8 * 8) * 128 + 1023) / 1024 * 1024;
   a.ksteps = (a.TR * a.Wp + 7) / 8;
   a.partial = partial;
+  a.Ct = C;
+  a.Kt = K;
   CUtensorMap X, DY;
-  if (!tma_map_nhwc(&X, x, N, H, W, 64, a.Wp, a.TR + R - 1, 1)) return cudaErrorInvalidValue;
-  if (!tma_map_nhwc(&DY, dy, N, P, Q, 64, a.Wp, a.TR, 1)) return cudaErrorInvalidValue;
+  if (!tma_map_nhwc(&X, x, N, H, W, C, a.Wp, a.TR + R - 1, 1)) return cudaErrorInvalidValue;
+  if (!tma_map_nhwc(&DY, dy, N, P, Q, K, a.Wp, a.TR, 1)) return cudaErrorInvalidValue;
   const int grid = conv_halo_wgrad_splits();
   const int smem = kWgStages * (2 * a.xslot + 2 * a.dyslot) + 1024 + 256;
   auto kern = (R == 3 && S == 3) ? tc_conv_halo_wgrad64<3, 3> : tc_conv_halo_wgrad64<0, 0>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (err != cudaSuccess) return err;
-  kern<<<grid, kHaloThreads, smem, st>>>(X, DY, a);
-  err = cudaGetLastError();
-  if (err != cudaSuccess) return err;
-  return splitk_reduce(partial, grid, R * S * 64, 64, dw, nullptr, 0, 1, st);
+  for (int c0 = 0; c0 < C; c0 += 64)
+    for (int k0 = 0; k0 < K; k0 += 64) {
+      a.c0 = c0;
+      a.k0 = k0;
+      kern<<<grid, kHaloThreads, smem, st>>>(X, DY, a);
+      err = cudaGetLastError();
+      if (err != cudaSuccess) return err;
+    }
+  return splitk_reduce(partial, grid, R * S * C, K, dw, nullptr, 0, 1, st);
 }
 
 }  // namespace sn

@@ -510,7 +510,7 @@ cudaError_t conv_wgrad(const ConvShape& s, const float* x, const float* dy, floa
   cudaError_t e;
   splits = effective_splits(s.N * s.P * s.Q, splits);  // the count the launch will really use
   if (use_tma() && s.stride == 1 && conv_halo_wgrad_ok(s.N, s.H, s.W, s.C, s.K, s.R, s.S, s.pad, s.P, s.Q)) {
-    e = conv_halo_wgrad(s.N, s.H, s.W, s.R, s.S, s.pad, s.P, s.Q, x, dy, partial, dw, st);
+    e = conv_halo_wgrad(s.N, s.H, s.W, s.C, s.K, s.R, s.S, s.pad, s.P, s.Q, x, dy, partial, dw, st);
     if (e != cudaSuccess) return e;
     if (!db) return cudaSuccess;
     return bias_grad(dy, static_cast<int64_t>(s.N) * s.P * s.Q, s.K, db, red_scratch, st);

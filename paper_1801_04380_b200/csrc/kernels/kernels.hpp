@@ -69,11 +69,12 @@ int conv_halo_stats_tiles(int N, int H, int W, int C, int K, int R, int S, int p
 cudaError_t conv_halo(int N, int H, int W, int C, int K, int R, int S, int pad, int P, int Q, const float* x,
                       const float* w, const float* bias, float* y, int accumulate, float* stats, cudaStream_t st);
 void set_conv_halo(int mode);  // 0 off, 1 by shape (default; env SN_CONV_HALO=0), 2 whenever legal (tests)
-// Halo-tiled weight gradient, C = K = 64 (M = 64 MMAs, all taps per CTA):
-// partial = conv_halo_wgrad_splits() * R*S*64*64 floats, dw[64][R][S][64].
+// Halo-tiled weight gradient, C, K multiples of 64 (64 x 64 sub-problems of
+// M = 64 MMAs, all taps per CTA): partial = conv_halo_wgrad_splits() * R*S*C*K
+// floats, dw[K][R][S][C].
 bool conv_halo_wgrad_ok(int N, int H, int W, int C, int K, int R, int S, int pad, int P, int Q);
 int conv_halo_wgrad_splits();
-cudaError_t conv_halo_wgrad(int N, int H, int W, int R, int S, int pad, int P, int Q, const float* x,
+cudaError_t conv_halo_wgrad(int N, int H, int W, int C, int K, int R, int S, int pad, int P, int Q, const float* x,
                             const float* dy, float* partial, float* dw, cudaStream_t st);
 
 bool conv_tma_ok_dgrad_strided(const ConvShape& s);

@@ -165,7 +165,8 @@ def test_conv_fwd_dgrad_wgrad(cuda, case, tma, pairs, halo):
     # wgrad + bias grad
     dw_d = torch.full((K, k, k, C), float("nan"), device=cuda)
     db_d = torch.full((K,), float("nan"), device=cuda)
-    part = torch.empty(8 << 20, device=cuda)
+    lib.sn_test_wgrad_splits.restype = ctypes.c_int
+    part = torch.empty(max(8 << 20, (lib.sn_test_wgrad_splits(shape) + 3) * k * k * C * K), device=cuda)
     red = torch.empty(int(lib.sn_test_red_scratch_floats(K)), device=cuda)
     ptrs = (ctypes.c_void_p * 6)(x_d.data_ptr(), dy_d.data_ptr(), dw_d.data_ptr(), db_d.data_ptr(),
                                  part.data_ptr(), red.data_ptr())
