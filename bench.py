@@ -34,18 +34,28 @@ ALL = "liveness,offload,cache,recompute=cost-aware,convselect"
 GiB = 1 << 30
 
 
+DEFAULT_BATCH = {"resnet50g": 256, "resnet152g": 256, "densenet121s": 256, "inception4s": 128, "alexnet": 200,
+                 "alex32": 16}
+
+
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--net", default="resnet50g", choices=["resnet50g", "resnet152g", "alexnet", "alex32"])
-    ap.add_argument("--batch", type=int, default=256)
+    ap.add_argument("--net", default="resnet50g",
+                    choices=["resnet50g", "resnet152g", "densenet121s", "inception4s", "alexnet", "alex32"],
+                    help="benchmark configs: alex32 (1), resnet50g (2, the headline), inception4s (3), "
+                         "densenet121s (4), resnet152g (5)")
+    ap.add_argument("--batch", type=int, default=None, help="per-GPU batch (default: the config's)")
     ap.add_argument("--pool-gib", type=float, default=24.0)
     ap.add_argument("--features", default=ALL)
     ap.add_argument("--no-extras", action="store_true", help="skip the unconstrained / profile / baseline legs")
-    return ap.parse_args()
+    args = ap.parse_args()
+    if args.batch is None:
+        args.batch = DEFAULT_BATCH[args.net]
+    return args
 
 
 def build_net(name: str):
@@ -55,6 +65,12 @@ def build_net(name: str):
         return gen_resnet(3, 4, 6, 3)
     if name == "resnet152g":
         return gen_resnet(3, 8, 36, 3)
+    if name == "densenet121s":
+        from paper_1801_04380_b200.netgen import gen_densenet
+        return gen_densenet()
+    if name == "inception4s":
+        from paper_1801_04380_b200.netgen import gen_inception
+        return gen_inception()
     return sn.load_network(os.path.join(ROOT, "paper_1801_04380_b200", "fixtures", f"{name}.net"))
 
 
@@ -98,6 +114,15 @@ class ClockSampler:
         reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": reasons, "samples": len(self.samples)}
+
+
+def baseline_metric() -> str:
+    """BASELINE.json's metric string (the workload itself is in config.workload)."""
+    try:
+        with open(os.path.join(ROOT, "BASELINE.json")) as fh:
+            return json.load(fh)["metric"]
+    except (OSError, KeyError, ValueError):
+        return "images/sec under memory budget at 1/2/4/8 B200; peak mem vs max_i(l_i)"
 
 
 def measured_peaks() -> dict:
@@ -229,7 +254,7 @@ def run_ours(args) -> None:
     e2e_dev_ms = sum(e_ms) / len(e_ms)
     h2d = img_host.numel() * 4 + lab_host.numel() * 4
     line = {
-        "metric": "images/sec under memory budget (ResNet-50g b256/GPU, 24 GiB pool, all SuperNeurons features)",
+        "metric": baseline_metric(),
         "value": round(value, 2), "unit": "images/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "fp32 storage, tf32 tensor-core math (fp32 accumulate)",
@@ -399,8 +424,7 @@ def run_reference(args) -> None:
     dt = time.perf_counter() - t0
     value = sample * args.steps / dt
     print(json.dumps({
-        "impl": "reference", "metric": "images/sec under memory budget (ResNet-50g b256/GPU, 24 GiB pool, "
-        "all SuperNeurons features)", "value": round(value, 3), "unit": "images/s", "n_gpus": args.gpus,
+        "impl": "reference", "metric": baseline_metric(), "value": round(value, 3), "unit": "images/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
         "data": "synthetic", "config": {"workload": f"{args.net} fwd+bwd+SGD, bounded sample of {sample} images "
@@ -410,7 +434,55 @@ def run_reference(args) -> None:
                          "sample": f"{sample} images/step, torch CPU restatement oracle/numerics.py; the reference "
                                    "memsched package is a simulator with no tensor numerics"},
         "e2e": {"value": round(value, 3), "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference_simulator": reference_simulator_time(args, net),
     }), flush=True)
+
+
+def reference_simulator_time(args, net) -> dict:
+    """The unmodified reference package (memsched 0.1.0, installed offline into
+    baseline/_ref with --no-deps: matplotlib is only for its PNG figures)
+    planning this config with its own run_simulation -- the reference's CPU
+    path for the schedule; our C++ planner produces the identical SimReport."""
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "memsched")):
+        return {"unavailable": "baseline/_ref not installed"}
+    sys.path.insert(0, ref_dir)
+    try:
+        import memsched
+        import paper_1801_04380_b200 as sn
+        rnet = memsched.parse_network(sn.network_text(net) if hasattr(sn, "network_text") else _net_text(net),
+                                      name=net.name)
+        cfg = memsched.SimConfig(pool_bytes=int(args.pool_gib * GiB), features=memsched.parse_features(args.features),
+                                 cost=memsched.CostConfig(batch=args.batch))
+        times = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            rep = memsched.run_simulation(rnet, cfg)
+            times.append(time.perf_counter() - t0)
+        t0 = time.perf_counter()
+        ours = sn.run_simulation(net, sn.SimConfig(pool_bytes=int(args.pool_gib * GiB),
+                                                   features=sn.parse_features(args.features),
+                                                   cost=sn.CostConfig(batch=args.batch)))
+        t_ours = time.perf_counter() - t0
+        return {"run_simulation_s": round(statistics.median(times), 4), "cores": 1,
+                "peak_bytes": rep.peak_bytes, "min_pool_bytes": rep.min_pool_bytes,
+                "ours_planner_s": round(t_ours, 4), "identical_peak": ours.peak_bytes == rep.peak_bytes}
+    except Exception as exc:  # report, never hide
+        return {"error": str(exc)[:200]}
+    finally:
+        sys.path.remove(ref_dir)
+
+
+def _net_text(net) -> str:
+    """.net text of a NetworkDef (layers in id order, then edges in next order)."""
+    lines = []
+    for l in net.layers:
+        kv = " ".join(f"{k}={v}" for k, v in l.params.items())
+        lines.append(f"layer {l.name} {l.kind.value} {kv}".rstrip())
+    for l in net.layers:
+        for n in l.next:
+            lines.append(f"edge {l.name} {net.layers[n].name}")
+    return "\n".join(lines) + "\n"
 
 
 def main() -> None:

@@ -404,5 +404,53 @@ def main() -> None:
     print(f"{len(results)} cases ({n_err} errors) in {time.time() - t0:.1f}s -> {OUT}")
 
 
+BRANCHY_OUT = HERE / "sched_golden_branchy.json.gz"
+
+
+def branchy_cases() -> list[dict]:
+    """Benchmark configs 3 and 4: the Inception-v4-style (branches, 4-way
+    JOIN-sum) and DenseNet-121-style (k-way JOIN-sum, dense recomputation)
+    graphs of paper_1801_04380_b200/netgen.py -- the reference ships no
+    generator for them, so their text is produced by ours and scheduled by the
+    reference."""
+    sys.path.insert(0, str(HERE.parent.parent))
+    from paper_1801_04380_b200 import netgen as ours
+    out: list[dict] = []
+    nets = [("densenet121s", ours.densenet_text(), 256), ("inception4s", ours.inception_text(), 128),
+            ("densenet_small", ours.densenet_text(blocks=(2, 3, 2, 2), widths=(32, 64, 64, 64)), 8),
+            ("inception_small", ours.inception_text(n_a=1, n_b=1, n_c=1), 4)]
+    for name, text, b in nets:
+        net = memsched.parse_network(text, name=name)
+        base = baseline_peak_bytes(build_costs(net, memsched.CostConfig(batch=b)))
+        for f in FEATURES + ["cache,recompute=speed,convselect", "cache,recompute=memory,convselect"]:
+            out.append({"id": f"{name}/b{b}/roomy/{f}", "text": text, "name": name, "batch": b,
+                        "pool": base + 256 * MiB, "features": f})
+        for frac in (2, 3):
+            for f in [ALL, "cache,recompute=memory,convselect"]:
+                out.append({"id": f"{name}/b{b}/tight{frac}/{f}", "text": text, "name": name, "batch": b,
+                            "pool": base // frac, "features": f, "cost": {"bandwidth_bytes_per_s": 2e9}})
+    return out
+
+
+def main_branchy() -> None:
+    t0 = time.time()
+    results, texts = [], {}
+    for case in branchy_cases():
+        res = run_case(case)
+        key = hashlib.sha256(res["text"].encode()).hexdigest()[:16]
+        texts[key] = res.pop("text")
+        res["net"] = key
+        results.append(res)
+    with gzip.open(BRANCHY_OUT, "wt") as fh:
+        json.dump({"generator": "tests/golden/make_golden.py --branchy",
+                   "reference": "memsched 0.1.0 (/root/reference/pkg)", "python": sys.version.split()[0],
+                   "nets": texts, "cases": results}, fh, separators=(",", ":"))
+    n_err = sum(1 for r in results if "error" in r)
+    print(f"{len(results)} cases ({n_err} errors) in {time.time() - t0:.1f}s -> {BRANCHY_OUT}")
+
+
 if __name__ == "__main__":
-    main()
+    if "--branchy" in sys.argv:
+        main_branchy()
+    else:
+        main()

@@ -301,3 +301,32 @@ def test_reassociating_fusions(cuda, monkeypatch):
             assert float((grads[l]["b"] - grads0[l]["b"]).abs().max()) <= 2e-3 * scale, net.layers[l].name
         else:
             assert relative_error(grads[l]["b"], grads0[l]["b"]) <= 2e-3, net.layers[l].name
+
+
+@pytest.mark.parametrize("kind", ["densenet", "inception"])
+def test_branchy_nets_match_oracle_and_are_schedule_invariant(cuda, kind):
+    """Benchmark configs 3-4 (reduced): the DenseNet-121-style (k-way JOIN-sum,
+    avg-pool transitions) and Inception-v4-style (4-branch modules, 3x3/s1 avg
+    pools, 8x8 global pool) graphs execute under every scheduling feature with
+    bit-identical gradients, and match the CPU oracle within the tf32
+    tolerance of the other nets."""
+    from paper_1801_04380_b200 import netgen
+    from paper_1801_04380_b200.training import init_parameters
+    from oracle.numerics import forward_backward, relative_error
+    if kind == "densenet":
+        net = netgen.gen_densenet(blocks=(2, 3, 2, 2), widths=(32, 64, 64, 64))
+        batch = 4
+    else:
+        net = netgen.gen_inception(n_a=1, n_b=1, n_c=1)
+        batch = 2
+    params = init_parameters(net, seed=4, head_scale=0.1)
+    images, labels = _inputs(net, batch, seed=7)
+    loss, grads, rep, _ = _run(net, batch, 8 << 30, ALL, params, images, labels)
+    for feats in ("none", "liveness,offload,recompute=memory"):
+        l2, g2, _, _ = _run(net, batch, 8 << 30, feats, params, images, labels)
+        assert l2 == loss and _bitwise(g2, grads), feats
+    ref_loss, _ = forward_backward(net, params, images, labels)
+    assert abs(loss - ref_loss) <= 5e-3 * abs(ref_loss), (loss, ref_loss)
+    ref, sens = _sensitivity(net, params, images, labels)
+    worst = max(relative_error(grads[l][k], ref[l][k]) for l in ref for k in ("w", "b"))
+    assert worst <= 3 * sens + 5e-3, (worst, sens)

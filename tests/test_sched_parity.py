@@ -1,7 +1,9 @@
 """Schedule parity: the C++ planner against golden vectors from the reference.
 
 tests/golden/sched_golden.json.gz was produced by tests/golden/make_golden.py
-running the reference simulator (memsched 0.1.0) itself.  For every case the
+running the reference simulator (memsched 0.1.0) itself;
+tests/golden/sched_golden_branchy.json.gz (make_golden.py --branchy) holds the
+Inception-v4-style and DenseNet-121-style graphs of benchmark configs 3-4.  For every case the
 planner must reproduce, bit for bit: every SimReport field (integers and IEEE
 doubles), every StepRow, every Selection, the recompute modes, and the full
 physical event tape (block offsets of every alloc, frees, copies, fetches,
@@ -23,16 +25,19 @@ import paper_1801_04380_b200 as sn
 from paper_1801_04380_b200 import simulator as snsim
 
 GOLDEN = Path(__file__).parent / "golden" / "sched_golden.json.gz"
+GOLDEN_BRANCHY = Path(__file__).parent / "golden" / "sched_golden_branchy.json.gz"
 
 
-def _load():
-    with gzip.open(GOLDEN, "rt") as fh:
+def _load(path):
+    with gzip.open(path, "rt") as fh:
         return json.load(fh)
 
 
-_DATA = _load()
-_NETS = _DATA["nets"]
+_DATA = _load(GOLDEN)
+_BRANCHY = _load(GOLDEN_BRANCHY)
+_NETS = {**_DATA["nets"], **_BRANCHY["nets"]}
 _CASES = _DATA["cases"]
+_BRANCHY_CASES = _BRANCHY["cases"]
 
 
 def canon(obj) -> str:
@@ -117,6 +122,14 @@ def test_schedule_matches_reference(case):
 
 @pytest.mark.parametrize("case", _DEEP, ids=_ids(_DEEP))
 def test_deep_resnet_schedule_matches_reference(case):
+    check_case(case)
+
+
+@pytest.mark.parametrize("case", _BRANCHY_CASES, ids=_ids(_BRANCHY_CASES))
+def test_branchy_schedule_matches_reference(case):
+    """Configs 3-4: Inception-v4-style branches and DenseNet-121-style k-way
+    JOIN-sums (liveness on branches, dense-segment recomputation, peak above
+    the floor), full tape parity."""
     check_case(case)
 
 
