@@ -206,8 +206,10 @@ def run_ours(args) -> None:
     def step():
         if world == 1:
             return ex.step(update=True)
-        loss, t = ex.step(update=False)
+        loss, t = ex.step(update=False)  # returns after the executor's stream has drained
         dist.all_reduce(grads)
+        # the SGD kernel runs on the executor's stream: it must see the reduced gradients
+        torch.cuda.current_stream(local).synchronize()
         ex.apply_update(0.01, 1.0 / world)
         return loss, t
 

@@ -67,6 +67,10 @@ def average_gradients(flat, ctx: DPContext, scale_in_update: bool = True):
     dist.all_reduce(flat, op=dist.ReduceOp.SUM)
     if not scale_in_update:
         flat.div_(ctx.world)
+    if flat.is_cuda:
+        # the executor's SGD kernel runs on its own stream, not torch's
+        import torch
+        torch.cuda.current_stream(flat.device).synchronize()
     return flat
 
 
