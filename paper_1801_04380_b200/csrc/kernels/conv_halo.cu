@@ -35,7 +35,8 @@
 namespace sn {
 namespace {
 
-constexpr int kHaloThreads = 192;
+constexpr int kHaloThreads = 192;   // weight-gradient kernel: 4 epilogue warps + producer + MMA
+constexpr int kHaloFwdThreads = 320;  // forward / dgrad: two epilogue groups (warps 0-3, 6-9)
 
 struct HaloArgs {
   int Wp, TR, MT, R, S, pad, P, Q, cchunks, bands, n_tiles, tiles;
@@ -48,19 +49,23 @@ struct HaloArgs {
   float* stats;        // BN statistics per sub-tile: [tile*MT + j][4][N] {shift, S1, S2, count}
 };
 
-template <int BN, int MT, int HST, int BST>
+template <int BN, int MT, int HST, int BST, int CG = 1>
 struct HaloSmem {
-  static constexpr int B_BYTES = BN * 128;
-  static constexpr int EPI_BYTES = 2 * kBM * 128;
-  // halo ring first (dynamic size), then the fixed tail
-  static constexpr int tail() { return BST * B_BYTES + EPI_BYTES + 512 + 1024; }
+  static constexpr int B_BYTES = (BN / CG) * 128;  // CTA pairs: each CTA stages half of the weight rows
+  static constexpr int EPI_BYTES = 2 * 2 * kBM * 128;  // two epilogue groups x double-buffered 16 KB chunks
+  // halo ring first (dynamic size), then the fixed tail (barriers, TMEM slot, 2 x 1 KB statistics scratch)
+  static constexpr int tail() { return BST * B_BYTES + EPI_BYTES + 512 + 2048 + 1024; }
 };
 
-template <int BN, int MT, int HST, int BST>
-__global__ void __launch_bounds__(kHaloThreads, 1)
+// CG = 2: CTA pair (cluster of 2): the pair's tile is 2 x TR*MT output rows,
+// rank r owns rows [r TR*MT, (r+1) TR*MT) of it (its own halo boxes, its own
+// TMEM accumulators) and stages half of every weight tile; the even CTA issues
+// tcgen05.mma.cta_group::2 with M = 256 (as conv_tma.cu CG = 2).
+template <int BN, int MT, int HST, int BST, int CG = 1>
+__global__ void __launch_bounds__(kHaloFwdThreads, 1)
     tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
                         const __grid_constant__ CUtensorMap tmY, HaloArgs a) {
-  using L = HaloSmem<BN, MT, HST, BST>;
+  using L = HaloSmem<BN, MT, HST, BST, CG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sH = smem;                                   // HST halo slots
@@ -73,7 +78,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
   uint64_t* tfull = bempty + BST;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  float* sred = reinterpret_cast<float*>(tmem_slot + 4);  // [4 warps][32][2]
+  float* sred0 = reinterpret_cast<float*>(tmem_slot + 4);  // per epilogue group [4 warps][32][2]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr uint32_t kCols = tmem_cols<2 * MT * BN>();
@@ -89,11 +94,20 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 128);
+      mbar_init(&tempty[b], 256 * CG);  // both epilogue groups of both CTAs drain the accumulator
     }
     fence_mbar_init();
   }
-  if (warp == 5) tmem_alloc(tmem_slot, kCols);
+  if (warp == 5) {
+    if constexpr (CG == 1) {
+      tmem_alloc(tmem_slot, kCols);
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(kCols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+  }
   if (warp == 4 && lane == 0) {
     tma_prefetch(&tmX);
     tma_prefetch(&tmW);
@@ -101,17 +115,21 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (CG == 2) cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int taps = a.R * a.S;
+  const int rank = CG == 2 ? static_cast<int>(cluster_rank()) : 0;
+  const int unit = blockIdx.x / CG, units = gridDim.x / CG;
 
-  // tile t -> (image n, band b, output-channel tile nt); band = TR*MT output rows
+  // tile t -> (image n, band b, output-channel tile nt); band = CG*TR*MT output
+  // rows, this CTA's part starts at y0
   auto coords = [&](int t, int& n, int& y0, int& n0) {
     const int nt = t % a.n_tiles;
     const int rest = t / a.n_tiles;
     const int b = rest % a.bands;
     n = rest / a.bands;
-    y0 = b * a.TR * MT;
+    y0 = (b * CG + rank) * a.TR * MT;
     n0 = nt * BN;
   };
 
@@ -120,14 +138,20 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
       // ---------------- TMA producer (whole warp; the elected lane issues) ----------------
       uint32_t hs = 0, hph = 0, bs = 0, bph = 0;
       bool hwrap = false, bwrap = false;  // ring slots reused: wait for their release
-      for (int t = blockIdx.x; t < a.tiles; t += gridDim.x) {
+      for (int t = unit; t < a.tiles; t += units) {
         int n, y0, n0;
         coords(t, n, y0, n0);
         for (int cc = 0; cc < a.cchunks; ++cc) {
           if (hwrap) mbar_wait(&hempty[hs], hph ^ 1);
           if (elect_one()) {
-            mbar_arrive_expect_tx(&hfull[hs], a.halo_bytes);
-            tma_load_4d(smem_u32(sH + hs * a.halo_slot), &tmX, &hfull[hs], cc * 32, -a.pad, y0 - a.pad, n);
+            if constexpr (CG == 1) {
+              mbar_arrive_expect_tx(&hfull[hs], a.halo_bytes);
+              tma_load_4d(smem_u32(sH + hs * a.halo_slot), &tmX, &hfull[hs], cc * 32, -a.pad, y0 - a.pad, n);
+            } else {
+              if (rank == 0) mbar_arrive_expect_tx(&hfull[hs], 2 * a.halo_bytes);
+              tma2_load_4d(smem_u32(sH + hs * a.halo_slot), &tmX, mapa_u32(&hfull[hs], 0), cc * 32, -a.pad,
+                           y0 - a.pad, n);
+            }
           }
           __syncwarp();
           if (++hs == HST) {
@@ -138,8 +162,14 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
           for (int tap = 0; tap < taps; ++tap) {
             if (bwrap) mbar_wait(&bempty[bs], bph ^ 1);
             if (elect_one()) {
-              mbar_arrive_expect_tx(&bfull[bs], L::B_BYTES);
-              tma_load_2d(smem_u32(sB + bs * L::B_BYTES), &tmW, &bfull[bs], (tap * a.cchunks + cc) * 32, n0);
+              if constexpr (CG == 1) {
+                mbar_arrive_expect_tx(&bfull[bs], L::B_BYTES);
+                tma_load_2d(smem_u32(sB + bs * L::B_BYTES), &tmW, &bfull[bs], (tap * a.cchunks + cc) * 32, n0);
+              } else {
+                if (rank == 0) mbar_arrive_expect_tx(&bfull[bs], 2 * L::B_BYTES);
+                tma2_load_2d(smem_u32(sB + bs * L::B_BYTES), &tmW, mapa_u32(&bfull[bs], 0),
+                             (tap * a.cchunks + cc) * 32, n0 + rank * (BN / CG));
+              }
             }
             __syncwarp();
             if (++bs == BST) {
@@ -152,16 +182,16 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
       }
     }
   } else if (warp == 5) {
-    {
-      // ---------------- MMA issuer (whole warp; the elected lane issues) ----------------
-      constexpr uint32_t idesc = idesc_tf32(kBM, BN, false, false);
+    if (rank == 0) {
+      // ---------------- MMA issuer (whole warp; the elected lane issues; pair leader for CG = 2) ----------------
+      constexpr uint32_t idesc = idesc_tf32(kBM * CG, BN, false, false);
       // lean issue loop (see conv_tma.cu): base descriptors + offsets in 16-byte units
       const uint64_t hdesc0 = umma_desc(smem_u32(sH), 16, 1024, kLayoutSW128);
       const uint64_t bdesc0 = umma_desc(smem_u32(sB), 16, 1024, kLayoutSW128);
       const uint32_t jstep = static_cast<uint32_t>(a.TR * a.Wp) * 8u;  // sub-tile rows * 128 B / 16
       uint32_t hs = 0, hph = 0, bs = 0, bph = 0;
       int local = 0;
-      for (int t = blockIdx.x; t < a.tiles; t += gridDim.x, ++local) {
+      for (int t = unit; t < a.tiles; t += units, ++local) {
         const int acc = local & 1;
         if (local >= 2) mbar_wait(&tempty[acc], ((local >> 1) - 1) & 1);
         tc_fence_after();
@@ -181,9 +211,16 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
 #pragma unroll
               for (int kk = 0; kk < kBK / 8; ++kk)
 #pragma unroll
-                for (int j = 0; j < MT; ++j)
-                  umma_tf32(d0 + j * BN, ad + j * jstep + kk * 2, bd + kk * 2, idesc, kk ? 1u : first);
-              umma_commit(&bempty[bs]);
+                for (int j = 0; j < MT; ++j) {
+                  if constexpr (CG == 1)
+                    umma_tf32(d0 + j * BN, ad + j * jstep + kk * 2, bd + kk * 2, idesc, kk ? 1u : first);
+                  else
+                    umma2_tf32(d0 + j * BN, ad + j * jstep + kk * 2, bd + kk * 2, idesc, kk ? 1u : first);
+                }
+              if constexpr (CG == 1)
+                umma_commit(&bempty[bs]);
+              else
+                umma2_commit(&bempty[bs]);
             }
             __syncwarp();
             if (++bs == BST) {
@@ -195,35 +232,55 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
               ++r;
             }
           }
-          if (elect_one()) umma_commit(&hempty[hs]);
+          if (elect_one()) {
+            if constexpr (CG == 1)
+              umma_commit(&hempty[hs]);
+            else
+              umma2_commit(&hempty[hs]);
+          }
           __syncwarp();
           if (++hs == HST) {
             hs = 0;
             hph ^= 1;
           }
         }
-        if (elect_one()) umma_commit(&tfull[acc]);
+        if (elect_one()) {
+          if constexpr (CG == 1)
+            umma_commit(&tfull[acc]);
+          else
+            umma2_commit(&tfull[acc]);
+        }
         __syncwarp();
       }
     }
   } else {
-    // ---------------- epilogue (warps 0-3 own TMEM lanes 32w..32w+31) ----------------
-    const uint32_t row = warp * 32 + lane;
+    // ---------------- epilogue: two groups of 4 warps (0-3, 6-9); warp w owns TMEM
+    // lanes 32 (w % 4) ..; group g drains the chunks (sub-tile, 32 columns) of
+    // parity g, with its own staging buffers, named barrier and leader thread
+    const int grp = warp >= 6 ? 1 : 0, q4 = warp & 3;
+    const uint32_t row = q4 * 32 + lane;
+    const bool leader = q4 == 0 && lane == 0;
+    const uint32_t bar_id = 1 + grp;
+    uint8_t* sEpiG = sEpi + grp * 2 * (kBM * 128);
+    float* sred = sred0 + grp * 256;
     int local = 0;
     uint32_t chunk_no = 0;
-    for (int t = blockIdx.x; t < a.tiles; t += gridDim.x, ++local) {
+    const uint32_t tempty_leader[2] = {CG == 2 ? mapa_u32(&tempty[0], 0) : 0u, CG == 2 ? mapa_u32(&tempty[1], 0) : 0u};
+    for (int t = unit; t < a.tiles; t += units, ++local) {
       int n, y0, n0;
       coords(t, n, y0, n0);
       const int acc = local & 1;
       mbar_wait(&tfull[acc], (local >> 1) & 1);
       tc_fence_after();
+      int ci = 0;  // chunk index within the tile (group = ci & 1)
       for (int j = 0; j < MT; ++j) {
         const int ys = y0 + j * a.TR;  // first output row of the sub-tile
         const uint32_t tbase = tmem + static_cast<uint32_t>(acc * MT * BN + j * BN) +
-                               (static_cast<uint32_t>(warp * 32) << 16);
+                               (static_cast<uint32_t>(q4 * 32) << 16);
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 32, ++chunk_no) {
+        for (int c = 0; c < BN; c += 32) {
           if (n0 + c >= a.N) break;
+          if ((ci++ & 1) != grp) continue;
           float v[32];
           tmem_ld32(tbase + static_cast<uint32_t>(c), v);
           if (a.bias) {
@@ -240,17 +297,17 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                 if (n0 + c + q < a.N) v[q] += __ldg(a.bias + n0 + c + q);
             }
           }
-          const uint32_t buf = smem_u32(sEpi) + (chunk_no & 1u) * (kBM * 128);
-          if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-          named_bar(1, 128);
+          const uint32_t buf = smem_u32(sEpiG) + (chunk_no & 1u) * (kBM * 128);
+          if (leader) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          named_bar(bar_id, 128);
 #pragma unroll
           for (int q = 0; q < 8; ++q)
             asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(buf + sw128_off(row, q)), "f"(v[4 * q]),
                          "f"(v[4 * q + 1]), "f"(v[4 * q + 2]), "f"(v[4 * q + 3])
                          : "memory");
           fence_proxy_async();
-          named_bar(1, 128);
-          if (threadIdx.x == 0) {
+          named_bar(bar_id, 128);
+          if (leader) {
             if (a.reduce)
               asm volatile(
                   "cp.reduce.async.bulk.tensor.4d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3, %4, %5}], "
@@ -265,7 +322,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
             // junk rows (padded columns x' >= Q, rows past P) are skipped; the
             // shift is the sub-tile's row 0 (real unless the whole sub-tile lies
             // past P, then its count is 0 and the reduction skips it)
-            const uint8_t* sb = sEpi + (chunk_no & 1u) * (kBM * 128);
+            const uint8_t* sb = sEpiG + (chunk_no & 1u) * (kBM * 128);
             const int Wp = a.Wp, TR = a.TR, Q = a.Q, rows_left = a.P - ys;
             float shift, t1, t2;
             chunk_column_stats(
@@ -274,10 +331,10 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                   const int yy = rr / Wp, xx = rr - yy * Wp;
                   return yy < TR && xx < Q && yy < rows_left;
                 },
-                sred, shift, t1, t2);
-            if (warp == 0 && n0 + c + lane < a.N) {
+                sred, shift, t1, t2, bar_id);
+            if (q4 == 0 && n0 + c + lane < a.N) {
               const int rows_valid = max(0, min(a.TR, a.P - ys)) * a.Q;
-              const size_t tile = (static_cast<size_t>(t / a.n_tiles) * MT + j);
+              const size_t tile = ((static_cast<size_t>(t / a.n_tiles) * CG + rank) * MT + j);
               float* out = a.stats + tile * 4 * a.N + n0 + c + lane;
               out[0] = shift;
               out[a.N] = t1;
@@ -285,17 +342,25 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
               out[3 * static_cast<size_t>(a.N)] = static_cast<float>(rows_valid);
             }
           }
+          ++chunk_no;
         }
       }
       tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      if constexpr (CG == 1)
+        mbar_arrive(&tempty[acc]);
+      else
+        mbar_arrive_cluster(tempty_leader[acc]);
     }
-    if (threadIdx.x == 0) bulk_wait_all();
+    if (leader) bulk_wait_all();
   }
   __syncthreads();
+  if constexpr (CG == 2) cluster_sync_all();
   if (warp == 5) {
     tc_fence_after();
-    tmem_dealloc(tmem, kCols);
+    if constexpr (CG == 1)
+      tmem_dealloc(tmem, kCols);
+    else
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols) : "memory");
   }
 }
 
@@ -333,25 +398,46 @@ bool halo_geom(int H, int W, int R, int S, int pad, int P, HaloGeom* g) {
   return true;
 }
 
-template <int BN, int MT, int HST, int BST>
+template <int BN, int MT, int HST, int BST, int CG>
 cudaError_t launch_halo(const CUtensorMap& X, const CUtensorMap& Wm, const CUtensorMap& Y, HaloArgs a,
                         const HaloGeom& g, cudaStream_t st) {
-  using L = HaloSmem<BN, MT, HST, BST>;
+  using L = HaloSmem<BN, MT, HST, BST, CG>;
   const int smem = static_cast<int>(HST * g.halo_slot) + L::tail();
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  auto kern = tc_conv_halo_kernel<BN, MT, HST, BST>;
+  auto kern = tc_conv_halo_kernel<BN, MT, HST, BST, CG>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (err != cudaSuccess) return err;
-  const int grid = std::min(a.tiles, num_sms_h());
-  kern<<<grid, kHaloThreads, smem, st>>>(X, Wm, Y, a);
-  return cudaGetLastError();
+  if constexpr (CG == 1) {
+    const int grid = std::min(a.tiles, num_sms_h());
+    kern<<<grid, kHaloFwdThreads, smem, st>>>(X, Wm, Y, a);
+    return cudaGetLastError();
+  } else {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * std::min(a.tiles, num_sms_h() / 2));
+    cfg.blockDim = dim3(kHaloFwdThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, X, Wm, Y, a);
+  }
 }
 
-// Variant table: (BN, MT, halo stages, weight stages) fitting 227 KB.
-template <int BN, int MT, int HST, int BST>
+// Variant table: (BN, MT, halo stages, weight stages, CTA group) fitting 227 KB.
+template <int BN, int MT, int HST, int BST, int CG = 1>
 bool halo_fits(const HaloGeom& g) {
-  return static_cast<int>(HST * g.halo_slot) + HaloSmem<BN, MT, HST, BST>::tail() <= 227 * 1024;
+  return static_cast<int>(HST * g.halo_slot) + HaloSmem<BN, MT, HST, BST, CG>::tail() <= 227 * 1024;
 }
+
+// variant id -> (BN, MT, CG): 1-3 single CTA BN 64/128/256, 4-6 the same as CTA pairs
+constexpr int kVarBN[7] = {0, 64, 128, 256, 64, 128, 256};
+constexpr int kVarMT[7] = {0, 3, 2, 1, 3, 2, 1};
+constexpr int kVarCG[7] = {0, 1, 1, 1, 2, 2, 2};
 
 }  // namespace
 
@@ -371,33 +457,44 @@ int conv_halo_variant(int N, int H, int W, int C, int K, int R, int S, int pad, 
   if (halo_mode() == 0 || C % 32 != 0 || K % 32 != 0 || R * S <= 1 || !tma_encoders_ok()) return 0;
   if (P != H + 2 * pad - R + 1 || Q != W + 2 * pad - S + 1 || pad < 0) return 0;
   // by shape: real output rows must fill >= 3/4 of each 128-row sub-tile, and
-  // the im2col kernel is L2-bound (K <= 64: its weight tile feeds one 64-wide
-  // MMA per k block; tools/conv_bench.py: 165 -> 149 us on ResNet stage 1,
-  // while at K >= 128 the im2col kernel is faster)
+  // K <= 128 (profiles/r01_conv_bench_halopair.txt, ResNet b256, CTA pairs:
+  // stage 1 161 -> 118 us, stage 2 102 -> 94 us; at K = 256 the im2col
+  // kernel's wider N amortises its operand traffic better: 80 vs 98 us)
   const int Wp = W + 2 * pad;
-  if (halo_mode() == 1 && (Wp > kBM || std::min(kBM / Wp, P) * Q * 4 < 3 * kBM || K > 64)) return 0;
+  if (halo_mode() == 1 && (Wp > kBM || std::min(kBM / Wp, P) * Q * 4 < 3 * kBM || K > 128)) return 0;
   HaloGeom g;
   const int bn = K <= 64 ? 64 : (K <= 128 ? 128 : 256);
+  // CTA pairs halve the per-SM weight traffic; they need >= 148 pair tiles
+  const int pm = conv_pairs_mode();
+  int v = 0;
   if (bn == 64) {
-    if (!halo_geom<64, 3>(H, W, R, S, pad, P, &g) || !halo_fits<64, 3, 2, 8>(g)) return 0;
-    return 1;
+    if (!halo_geom<64, 3>(H, W, R, S, pad, P, &g)) return 0;
+    v = halo_fits<64, 3, 2, 4>(g) ? 1 : 0;
+    if (pm != 0 && halo_fits<64, 3, 2, 8, 2>(g)) v = 4;
+  } else if (bn == 128) {
+    if (!halo_geom<128, 2>(H, W, R, S, pad, P, &g)) return 0;
+    v = halo_fits<128, 2, 2, 4>(g) ? 2 : 0;
+    if (pm != 0 && halo_fits<128, 2, 2, 8, 2>(g)) v = 5;
+  } else {
+    if (!halo_geom<256, 1>(H, W, R, S, pad, P, &g)) return 0;
+    v = halo_fits<256, 1, 2, 3>(g) ? 3 : 0;
+    if (pm != 0 && halo_fits<256, 1, 2, 6, 2>(g)) v = 6;
   }
-  if (bn == 128) {
-    if (!halo_geom<128, 2>(H, W, R, S, pad, P, &g) || !halo_fits<128, 2, 2, 6>(g)) return 0;
-    return 2;
+  if (v >= 4 && pm == 1) {
+    const int bands2 = (P + g.TR * g.MT * 2 - 1) / (g.TR * g.MT * 2);
+    if (static_cast<int64_t>(N) * bands2 * ((K + bn - 1) / bn) < num_sms_h() / 2) v -= 3;
   }
-  if (!halo_geom<256, 1>(H, W, R, S, pad, P, &g) || !halo_fits<256, 1, 2, 4>(g)) return 0;
-  return 3;
+  return v;
 }
 
 int conv_halo_stats_tiles(int N, int H, int W, int C, int K, int R, int S, int pad, int P, int Q) {
   const int v = conv_halo_variant(N, H, W, C, K, R, S, pad, P, Q);
   if (!v) return 0;
-  const int MT = v == 1 ? 3 : (v == 2 ? 2 : 1);
+  const int MT = kVarMT[v], CG = kVarCG[v];
   const int Wp = W + 2 * pad;
   const int TR = std::min(kBM / Wp, P);
-  const int bands = (P + TR * MT - 1) / (TR * MT);
-  return N * bands * MT;
+  const int bands = (P + TR * MT * CG - 1) / (TR * MT * CG);
+  return N * bands * CG * MT;
 }
 
 // y[N][P][Q][K] (+)= conv(x[N][H][W][C], w[K][R][S][C]) + bias, stride 1.
@@ -406,14 +503,13 @@ cudaError_t conv_halo(int N, int H, int W, int C, int K, int R, int S, int pad, 
   const int v = conv_halo_variant(N, H, W, C, K, R, S, pad, P, Q);
   if (!v) return cudaErrorInvalidValue;
   HaloGeom g;
-  const int BN = v == 1 ? 64 : (v == 2 ? 128 : 256);
-  const int MT = v == 1 ? 3 : (v == 2 ? 2 : 1);
-  if (v == 1) halo_geom<64, 3>(H, W, R, S, pad, P, &g);
-  else if (v == 2) halo_geom<128, 2>(H, W, R, S, pad, P, &g);
+  const int BN = kVarBN[v], MT = kVarMT[v], CG = kVarCG[v];
+  if (BN == 64) halo_geom<64, 3>(H, W, R, S, pad, P, &g);
+  else if (BN == 128) halo_geom<128, 2>(H, W, R, S, pad, P, &g);
   else halo_geom<256, 1>(H, W, R, S, pad, P, &g);
   CUtensorMap X, Wm, Y;
   if (!tma_map_nhwc(&X, x, N, H, W, C, g.Wp, g.halo_rows, 0)) return cudaErrorInvalidValue;
-  if (!tma_map_2d(&Wm, w, K, static_cast<int64_t>(R) * S * C, BN, 0)) return cudaErrorInvalidValue;
+  if (!tma_map_2d(&Wm, w, K, static_cast<int64_t>(R) * S * C, BN / CG, 0)) return cudaErrorInvalidValue;
   if (!tma_map_nhwc(&Y, y, N, P, Q, K, g.Wp, g.TR, 0)) return cudaErrorInvalidValue;
   HaloArgs a{};
   a.Wp = g.Wp;
@@ -425,7 +521,7 @@ cudaError_t conv_halo(int N, int H, int W, int C, int K, int R, int S, int pad, 
   a.P = P;
   a.Q = Q;
   a.cchunks = C / 32;
-  a.bands = (P + g.TR * MT - 1) / (g.TR * MT);
+  a.bands = (P + g.TR * MT * CG - 1) / (g.TR * MT * CG);
   a.n_tiles = (K + BN - 1) / BN;
   a.tiles = N * a.bands * a.n_tiles;
   a.halo_rows = g.halo_rows;
@@ -436,9 +532,12 @@ cudaError_t conv_halo(int N, int H, int W, int C, int K, int R, int S, int pad, 
   a.reduce = accumulate;
   a.stats = stats;
   switch (v) {
-    case 1: return launch_halo<64, 3, 2, 8>(X, Wm, Y, a, g, st);
-    case 2: return launch_halo<128, 2, 2, 6>(X, Wm, Y, a, g, st);
-    default: return launch_halo<256, 1, 2, 4>(X, Wm, Y, a, g, st);
+    case 1: return launch_halo<64, 3, 2, 4, 1>(X, Wm, Y, a, g, st);
+    case 2: return launch_halo<128, 2, 2, 4, 1>(X, Wm, Y, a, g, st);
+    case 3: return launch_halo<256, 1, 2, 3, 1>(X, Wm, Y, a, g, st);
+    case 4: return launch_halo<64, 3, 2, 8, 2>(X, Wm, Y, a, g, st);
+    case 5: return launch_halo<128, 2, 2, 8, 2>(X, Wm, Y, a, g, st);
+    default: return launch_halo<256, 1, 2, 6, 2>(X, Wm, Y, a, g, st);
   }
 }
 

@@ -103,57 +103,6 @@ struct TileGrid {
   int m_tiles, n_tiles, tiles;
 };
 
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-// shared::cluster address of the same smem variable in CTA `rank` of the cluster
-__device__ __forceinline__ uint32_t mapa_u32(const void* p, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cbar) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cbar) : "memory");
-}
-// TMA loads whose completion is signalled on the pair leader's mbarrier (cbar: cluster address)
-__device__ __forceinline__ void tma2_load_2d(uint32_t dst, const void* tmap, uint32_t cbar, int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
-      "%4}], [%2];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(cbar), "r"(c0), "r"(c1)
-      : "memory");
-}
-__device__ __forceinline__ void tma2_load_im2col_4d(uint32_t dst, const void* tmap, uint32_t cbar, int c, int w, int h,
-                                                    int n, uint16_t ws, uint16_t hr) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.im2col.mbarrier::complete_tx::bytes [%0], [%1, "
-      "{%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(cbar), "r"(c), "r"(w), "r"(h), "r"(n), "h"(ws), "h"(hr)
-      : "memory");
-}
-__device__ __forceinline__ void umma2_tf32(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                           uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-// commit the pair's MMAs to the same mbarrier in both CTAs
-__device__ __forceinline__ void umma2_commit(uint64_t* bar) {
-  asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-          smem_u32(bar)),
-      "h"(static_cast<uint16_t>(3))
-      : "memory");
-}
-
 template <int BN, int STAGES, int MODE, int CG = 1>
 __global__ void __launch_bounds__(kTmaThreads, 1)
     tc_conv_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -718,6 +667,7 @@ bool tma_map_2d(CUtensorMap* m, const float* base, int64_t rows, int64_t cols, i
 bool conv_tma_ok_fwd(const ConvShape& s) { return s.C % 32 == 0 && load_encoders(); }
 
 void set_conv_pairs(int mode) { g_pairs = mode; }
+int conv_pairs_mode() { return pairs_mode(); }
 
 int conv_fwd_stats_tiles(const ConvShape& s, bool stem, int* tile_rows) {
   if (stem) {
@@ -979,7 +929,8 @@ namespace {
 // R per row, and no per-tile weight traffic (the 1-row kernel was bound by
 // its L2 -> SMEM operand traffic).
 constexpr int kStemRT = 4;
-constexpr int kStemRing = 8;
+constexpr int kStemRing = 6;
+constexpr int kStemThreads = 320;  // producer (warp 4), MMA (warp 5), two epilogue groups (warps 0-3, 6-9)
 struct StemRowsArgs {
   int N, P, Q, R, stride, K, rows_in;  // rows_in = (RT-1)*stride + R input rows per tile
   int tiles;                           // N * ceil(P / RT)
@@ -987,7 +938,7 @@ struct StemRowsArgs {
   float* stats;                        // [N*P][3][K] tile statistics (tile = output row), or null
 };
 
-__global__ void __launch_bounds__(kTmaThreads, 1)
+__global__ void __launch_bounds__(kStemThreads, 1)
     stem_rows_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW,
                      const __grid_constant__ CUtensorMap tmD, StemRowsArgs a) {
   extern __shared__ uint8_t smem_raw[];
@@ -995,8 +946,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   constexpr int A_BYTES = kBM * 128, W_BYTES = 64 * 128;
   uint8_t* sA = smem;                                  // kStemRing input-row views
   uint8_t* sW = sA + kStemRing * A_BYTES;              // R weight k-blocks (resident)
-  uint8_t* sEpi = sW + 8 * W_BYTES;                    // 2 x 16 KB store staging
-  uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + 2 * kBM * 128);
+  uint8_t* sEpi = sW + a.R * W_BYTES;                  // 2 groups x 2 x 16 KB store staging
+  uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + 4 * kBM * 128);
   uint64_t* empty = full + kStemRing;
   uint64_t* wbar = empty + kStemRing;
   uint64_t* tfull = wbar + 1;
@@ -1014,7 +965,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     mbar_init(wbar, 1);
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 128);
+      mbar_init(&tempty[b], 256);
     }
     fence_mbar_init();
   }
@@ -1086,7 +1037,13 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
       __syncwarp();
     }
   } else {
-    const uint32_t row = warp * 32 + lane;
+    // two epilogue groups (warps 0-3, 6-9); group g drains the 32-column chunks of parity g
+    const int grp = warp >= 6 ? 1 : 0, q4 = warp & 3;
+    const uint32_t row = q4 * 32 + lane;
+    const bool leader = q4 == 0 && lane == 0;
+    const uint32_t bar_id = 1 + grp;
+    uint8_t* sEpiG = sEpi + grp * 2 * (kBM * 128);
+    float* sredG = sred + grp * 256;
     int local = 0;
     uint32_t chunk_no = 0;
     for (int t = blockIdx.x; t < a.tiles; t += gridDim.x, ++local) {
@@ -1094,22 +1051,24 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
       const int acc = local & 1;
       mbar_wait(&tfull[acc], (local >> 1) & 1);
       tc_fence_after();
+      int ci = 0;
       for (int i = 0; i < kStemRT; ++i) {
         const int p = p0 + i;
         const uint32_t tbase = tmem + static_cast<uint32_t>((acc * kStemRT + i) * 64) +
-                               (static_cast<uint32_t>(warp * 32) << 16);
+                               (static_cast<uint32_t>(q4 * 32) << 16);
 #pragma unroll 1
-        for (int c = 0; c < 64; c += 32, ++chunk_no) {
+        for (int c = 0; c < 64; c += 32) {
           if (c >= a.K) break;
+          if ((ci++ & 1) != grp) continue;
           float v[32];
           tmem_ld32(tbase + static_cast<uint32_t>(c), v);
           if (a.bias) {
-            if (c + 32 <= a.K) {  // 16-byte loads (parameter slices are 256-byte aligned)
+            if (c + 32 <= a.K) {
               const float4* b4 = reinterpret_cast<const float4*>(a.bias + c);
 #pragma unroll
-              for (int q4 = 0; q4 < 8; ++q4) {
-                const float4 bq = __ldg(b4 + q4);
-                v[4 * q4] += bq.x; v[4 * q4 + 1] += bq.y; v[4 * q4 + 2] += bq.z; v[4 * q4 + 3] += bq.w;
+              for (int q = 0; q < 8; ++q) {
+                const float4 bq = __ldg(b4 + q);
+                v[4 * q] += bq.x; v[4 * q + 1] += bq.y; v[4 * q + 2] += bq.z; v[4 * q + 3] += bq.w;
               }
             } else {
 #pragma unroll
@@ -1117,38 +1076,39 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
                 if (c + q < a.K) v[q] += __ldg(a.bias + c + q);
             }
           }
-          const uint32_t buf = smem_u32(sEpi) + (chunk_no & 1u) * (kBM * 128);
-          if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-          named_bar(1, 128);
+          const uint32_t buf = smem_u32(sEpiG) + (chunk_no & 1u) * (kBM * 128);
+          if (leader) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          named_bar(bar_id, 128);
 #pragma unroll
           for (int q = 0; q < 8; ++q)
             asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(buf + sw128_off(row, q)), "f"(v[4 * q]),
                          "f"(v[4 * q + 1]), "f"(v[4 * q + 2]), "f"(v[4 * q + 3])
                          : "memory");
           fence_proxy_async();
-          named_bar(1, 128);
-          if (threadIdx.x == 0 && p < a.P) {
+          named_bar(bar_id, 128);
+          if (leader && p < a.P) {
             tma_store_4d(&tmD, buf, c, 0, p, n);
             bulk_commit();
           }
           if (a.stats && p < a.P) {
-            const uint8_t* sb = sEpi + (chunk_no & 1u) * (kBM * 128);
+            const uint8_t* sb = sEpiG + (chunk_no & 1u) * (kBM * 128);
             float shift, t1, t2;
             const int Q = a.Q;
-            chunk_column_stats(sb, [Q](int r) { return r < Q; }, sred, shift, t1, t2);
-            if (warp == 0 && c + lane < a.K) {
+            chunk_column_stats(sb, [Q](int r) { return r < Q; }, sredG, shift, t1, t2, bar_id);
+            if (q4 == 0 && c + lane < a.K) {
               float* out = a.stats + (static_cast<size_t>(n) * a.P + p) * 3 * a.K + c + lane;
               out[0] = shift;
               out[a.K] = t1;
               out[2 * static_cast<size_t>(a.K)] = t2;
             }
           }
+          ++chunk_no;
         }
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
     }
-    if (threadIdx.x == 0) bulk_wait_all();
+    if (leader) bulk_wait_all();
   }
   __syncthreads();
   if (warp == 5) {
@@ -1182,14 +1142,14 @@ cudaError_t conv_stem_fwd(const ConvShape& s, const float* xp, const float* w, f
     ra.tiles = s.N * ((s.P + kStemRT - 1) / kStemRT);
     ra.bias = bias;
     ra.stats = stats;
-    const int smem = kStemRing * kBM * 128 + 8 * 64 * 128 + 2 * kBM * 128 + 512 + 1024 + 1024;
+    const int smem = kStemRing * kBM * 128 + s.R * 64 * 128 + 4 * kBM * 128 + 512 + 2048 + 1024;
     static bool attr = false;
     if (!attr) {
       err = cudaFuncSetAttribute(stem_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       if (err != cudaSuccess) return err;
       attr = true;
     }
-    stem_rows_kernel<<<std::min(ra.tiles, num_sms()), kTmaThreads, smem, st>>>(A, W, D, ra);
+    stem_rows_kernel<<<std::min(ra.tiles, num_sms()), kStemThreads, smem, st>>>(A, W, D, ra);
     return cudaGetLastError();
   }
   const int BN = bn_for(s.K);

@@ -84,6 +84,7 @@ void set_conv_tma(int on);
 // CTA-pair (cta_group::2) conv kernels: 0 off, 1 when the shape keeps the
 // pairs busy (default; env SN_CONV_PAIRS=0 turns them off), 2 always (tests).
 void set_conv_pairs(int mode);
+int conv_pairs_mode();
 bool use_tma();
 
 // FC: x[B][I], w[O][I], y[B][O]

@@ -122,6 +122,67 @@ __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// ---- CTA pairs (cta_group::2, cluster of 2) -----------------------------------
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of the same smem variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_u32(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cbar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cbar) : "memory");
+}
+// TMA loads whose completion is signalled on the pair leader's mbarrier (cbar: cluster address)
+__device__ __forceinline__ void tma2_load_2d(uint32_t dst, const void* tmap, uint32_t cbar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(cbar), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma2_load_im2col_4d(uint32_t dst, const void* tmap, uint32_t cbar, int c, int w, int h,
+                                                    int n, uint16_t ws, uint16_t hr) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.im2col.mbarrier::complete_tx::bytes [%0], [%1, "
+      "{%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(cbar), "r"(c), "r"(w), "r"(h), "r"(n), "h"(ws), "h"(hr)
+      : "memory");
+}
+__device__ __forceinline__ void umma2_tf32(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// commit the pair's MMAs to the same mbarrier in both CTAs
+__device__ __forceinline__ void umma2_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(static_cast<uint16_t>(3))
+      : "memory");
+}
+
+__device__ __forceinline__ void tma2_load_4d(uint32_t dst, const void* tmap, uint32_t cbar, int c0, int c1, int c2,
+                                             int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4, %5, %6}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(cbar), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
 // One lane of a converged warp (elect.sync).  Single-thread tcgen05 / TMA
 // issue is written as "whole warp runs the loop, the elected lane issues", so
 // loop state and descriptors stay warp-uniform (uniform registers) and ptxas
@@ -235,7 +296,7 @@ __device__ __forceinline__ uint32_t sw128_off(uint32_t row, uint32_t chunk) {
 // Warp 0 lane l returns column l's {shift, sum(y - shift), sum((y - shift)^2)}.
 template <class Valid>
 __device__ __forceinline__ void chunk_column_stats(const uint8_t* sb, Valid valid, float* sred, float& shift_out,
-                                                   float& s1_out, float& s2_out) {
+                                                   float& s1_out, float& s2_out, uint32_t bar_id = 1) {
   const int t = threadIdx.x & 127, cq = t & 7, rg = t >> 3;
   const float4 sh = *reinterpret_cast<const float4*>(sb + sw128_off(0, cq));
   float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
@@ -261,7 +322,7 @@ __device__ __forceinline__ void chunk_column_stats(const uint8_t* sb, Valid vali
     float* o = sred + (warp * 32 + 4 * cq) * 2;
     o[0] = a.x; o[1] = b.x; o[2] = a.y; o[3] = b.y; o[4] = a.z; o[5] = b.z; o[6] = a.w; o[7] = b.w;
   }
-  named_bar(1, 128);
+  named_bar(bar_id, 128);
   if (warp == 0) {
     float t1 = sred[lane * 2], t2 = sred[lane * 2 + 1];
     for (int w = 1; w < 4; ++w) {

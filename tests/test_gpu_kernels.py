@@ -123,7 +123,7 @@ def _shape_arr(N, C, H, W, K, k, s, p):
     return (ctypes.c_int * 11)(N, H, W, C, K, k, k, P, Q, s, p), P, Q
 
 
-@pytest.mark.parametrize("tma,pairs,halo", [(1, 1, 1), (1, 2, 0), (1, 1, 2), (0, 1, 0)])
+@pytest.mark.parametrize("tma,pairs,halo", [(1, 1, 1), (1, 2, 0), (1, 1, 2), (1, 2, 2), (0, 1, 0)])
 @pytest.mark.parametrize("case", CONV_CASES)
 def test_conv_fwd_dgrad_wgrad(cuda, case, tma, pairs, halo):
     """pairs=2 forces the CTA-pair (cta_group::2, M = 256) TMA kernels on
