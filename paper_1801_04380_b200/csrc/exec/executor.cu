@@ -652,12 +652,24 @@ struct Compiler {
         const int C = l.C;
         float* red = ex->red;
         const int relu = bwd_relu ? 1 : 0;
+        float* cpy = nullptr;
+        int cpy_acc = 0;
+        if (bn_from_join[cur_ti] >= 0) {
+          auto pj = pending_join.find(static_cast<int>(cur_ti));
+          if (pj == pending_join.end()) xfail(SN_EK_INTERNAL, "fused JOIN backward not recorded");
+          dy = const_cast<float*>(pj->second.dy);
+          cpy = pj->second.other;
+          cpy_acc = pj->second.other_acc;
+          pending_join.erase(pj);
+        }
         float* dcb = nullptr;
         if (bn_bias_now && dx) {
           dcb = ex->grads + ex->L[pid].b_off;
           conv_bias_done[pid] = 1;
         }
-        push([=] { ck(sn::bn_bwd(x, dy, rows, C, g, beta, stats, relu, dx, acc, dg, dbt, red, st, dcb), "bn_bwd"); },
+        push([=] {
+          ck(sn::bn_bwd(x, dy, rows, C, g, beta, stats, relu, dx, acc, dg, dbt, red, st, dcb, cpy, cpy_acc), "bn_bwd");
+        },
              dx ? (dcb ? 4 : 3) : 2);
         break;
       }
@@ -714,6 +726,16 @@ struct Compiler {
       }
       case snp::JOIN: {
         const auto& pv = net.prev[lid];
+        if (join_to_bn[cur_ti] >= 0) {
+          // deferred into the BN backward (see plan_fusions): record the pointers now
+          const int ra = join_relu[cur_ti];
+          const int other = pv[0] == ra ? pv[1] : pv[0];
+          int a_r = 0, a_o = 0;
+          dx_target(ra, &a_r);  // the BN's own gradient buffer: never written
+          float* d_o = dx_target(other, &a_o);
+          pending_join[join_to_bn[cur_ti]] = PendingJoin{dy, d_o, a_o};
+          break;
+        }
         if (pv.size() == 2 && n % 4 == 0) {
           const int o0 = net.grad_owner(pv[0]), o1 = net.grad_owner(pv[1]);
           if (o0 >= 0 && o1 >= 0 && o0 != o1) {  // one read of dy, two destinations
@@ -752,6 +774,16 @@ struct Compiler {
   // of a 2-input JOIN reading the ReLU: the whole chain runs at the JOIN.
   std::vector<int> join_fuse_at, join_from;
   std::vector<char> dead_at;  // forward / replay whose outputs are never read: not launched
+  // JOIN backward folded into the BN backward of the ReLU it feeds: join_to_bn[i]
+  // = tape index of that BN backward; the JOIN's gradient is read there
+  // directly and copied into the other input's buffer by the reduction pass.
+  std::vector<int> join_to_bn, bn_from_join, join_relu;
+  struct PendingJoin {
+    const float* dy = nullptr;
+    float* other = nullptr;
+    int other_acc = 0;
+  };
+  std::unordered_map<int, PendingJoin> pending_join;  // keyed by BN-backward tape index
   // CONV forward -> BN forward (next compute action, reading that output): the
   // CONV epilogue emits per-tile statistics, the BN only combines them.
   bool conv_stats_now = false, bn_tiles_now = false;
@@ -784,6 +816,9 @@ struct Compiler {
     join_fuse_at.assign(T, -1);
     join_from.assign(T, -1);
     dead_at.assign(T, 0);
+    join_to_bn.assign(T, -1);
+    bn_from_join.assign(T, -1);
+    join_relu.assign(T, -1);
     bn_bias_at.assign(T, 0);
     conv_bias_done.assign(net.n, 0);
     const char* env = std::getenv("SN_FUSE");  // SN_FUSE=0: one kernel per layer (A/B and bitwise tests)
@@ -920,6 +955,51 @@ struct Compiler {
         }
       }
       if (!read) dead_at[i] = 1;
+    }
+    // JOIN backward -> BN backward: safe when the JOIN's gradient buffer is not
+    // re-allocated (over its block range) before the BN backward reads it
+    for (size_t i = 0; i < T; ++i) {
+      const snp::Event& e = P.tape[i];
+      if (e.op != 'B' || net.kind[e.b] != snp::JOIN || net.prev[e.b].size() != 2) continue;
+      const int jn = e.b;
+      int ra = -1;
+      for (int p : net.prev[jn])
+        if (bn_relu_pair(p) && net.next[p].size() == 1) ra = p;
+      if (ra < 0) continue;
+      const int other = net.prev[jn][0] == ra ? net.prev[jn][1] : net.prev[jn][0];
+      if (other == ra || net.grad_owner(other) < 0 || ex->L[jn].C % 4 != 0) continue;
+      const int bn = net.prev[ra][0];
+      if (net.grad_owner(ra) != bn) continue;
+      int64_t joff = -1, jblk = 0;  // the JOIN gradient buffer's blocks
+      for (size_t j = i; j-- > 0;) {
+        const snp::Event& f = P.tape[j];
+        if (f.op == 'A' && f.a == snp::K_GRAD && f.b == jn) {
+          joff = f.c;
+          jblk = f.d;
+          break;
+        }
+      }
+      if (joff < 0) continue;
+      const int bn_dx_owner = net.grad_owner(net.prev[bn][0]);
+      for (size_t j = i + 1; j < T; ++j) {
+        const snp::Event& f = P.tape[j];
+        // a new buffer over the JOIN gradient's blocks breaks the fusion, except
+        // the BN's own dx target placed exactly there: it is freshly allocated
+        // (dx written, not accumulated) and dx = f(dy, x) is elementwise, so
+        // reading dy and writing dx at the same address is safe
+        if (f.op == 'A' && overlap(f.c, f.d, joff, jblk) &&
+            !(f.a == snp::K_GRAD && f.b == bn_dx_owner && f.c == joff && f.d == jblk))
+          break;
+        if (f.op == 'B' && f.b == bn) {
+          if (bn_bwd_relu[j]) {
+            join_to_bn[i] = static_cast<int>(j);
+            bn_from_join[j] = static_cast<int>(i);
+            join_relu[i] = ra;
+          }
+          break;
+        }
+        if (f.op == 'B' && f.b != ra) break;  // another backward in between: keep it simple
+      }
     }
     ex->elided = elide_out;
   }

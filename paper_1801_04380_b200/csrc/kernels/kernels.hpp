@@ -126,7 +126,11 @@ cudaError_t bn_stats_from_tiles(const float* tiles, int ntiles, int tile_rows, c
 bool bn_bwd_bias_ok(int C);
 cudaError_t bn_bwd(const float* x, const float* dy, int64_t rows, int C, const float* gamma, const float* beta,
                    const float* stats, int relu, float* dx, int accumulate, float* dgamma, float* dbeta,
-                   float* red_scratch, cudaStream_t st, float* dbias = nullptr);
+                   float* red_scratch, cudaStream_t st, float* dbias = nullptr, float* copy_dst = nullptr,
+                   int copy_acc = 0);
+// copy_dst (optional, C % 4 == 0): the fused backward of the 2-input JOIN
+// feeding the ReLU: its gradient dy is also written (copy_acc: added) into the
+// JOIN's other input's gradient buffer in the reduction pass.
 
 // Fused BN apply + ReLU (+ 2-input JOIN) (C % 4 == 0): y = bn(x), y_relu =
 // max(bn(x), 0), y_join = y_relu + join_other; null outputs are not written.

@@ -98,6 +98,7 @@ struct RedBiasOp {  // f1 = dy
     b = 0.f;
   }
   __device__ R load(int64_t off) const { return R{ld4(dy + off)}; }
+  __device__ void side(int64_t, const R&) const {}
   __device__ void comp(const P&, const R& r, float4& a, float4& b) const {
     a = r.g;
     b = zero4();
@@ -118,6 +119,7 @@ struct RedBnStatsOp {  // f1 = x - x[0][c], f2 = (x - x[0][c])^2
     b = d * d;
   }
   __device__ R load(int64_t off) const { return R{ld4(x + off)}; }
+  __device__ void side(int64_t, const R&) const {}
   __device__ void comp(const P& p, const R& r, float4& a, float4& b) const {
     a = make_float4(r.v.x - p.s.x, r.v.y - p.s.y, r.v.z - p.s.z, r.v.w - p.s.w);
     b = make_float4(a.x * a.x, a.y * a.y, a.z * a.z, a.w * a.w);
@@ -132,6 +134,10 @@ struct RedBnBwdOp {
   const float* gamma;
   const float* beta;
   int relu;
+  // fused JOIN backward: the raw dy (the JOIN's gradient) is also written
+  // (or added) into the JOIN's other input's gradient buffer
+  float* copy_dst;
+  int copy_acc;
   using P = Bn4;
   struct R {
     float4 g, v;
@@ -145,6 +151,16 @@ struct RedBnBwdOp {
     b = g * bn_xhat(v, stats[c], stats[C + c]);
   }
   __device__ R load(int64_t off) const { return R{ld4(dy + off), ld4(x + off)}; }
+  __device__ void side(int64_t off, const R& r) const {
+    if (!copy_dst) return;
+    float4* d = reinterpret_cast<float4*>(copy_dst + off);
+    if (copy_acc) {
+      const float4 o = *d;
+      *d = make_float4(o.x + r.g.x, o.y + r.g.y, o.z + r.g.z, o.w + r.g.w);
+    } else {
+      *d = r.g;
+    }
+  }
   __device__ void comp(const P& p, const R& r, float4& a, float4& b) const {
     float4 g = r.g;
     const float4 v = r.v;
@@ -189,6 +205,7 @@ __global__ void __launch_bounds__(kRedThreads) colred_stage1_v4(Op op, int64_t r
         for (int u = 0; u < kUnroll; ++u) raw[u] = op.load((r + u * lanes) * C + c4 * 4);
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
+          op.side((r + u * lanes) * C + c4 * 4, raw[u]);
           float4 fa, fb;
           op.comp(p, raw[u], fa, fb);
           add4(au[u], fa);
@@ -197,7 +214,9 @@ __global__ void __launch_bounds__(kRedThreads) colred_stage1_v4(Op op, int64_t r
       }
       for (; r < r1; r += lanes) {
         float4 fa, fb;
-        op.comp(p, op.load(r * C + c4 * 4), fa, fb);
+        const typename Op::R raw1 = op.load(r * C + c4 * 4);
+        op.side(r * C + c4 * 4, raw1);
+        op.comp(p, raw1, fa, fb);
         add4(au[0], fa);
         add4(bu[0], fb);
       }
@@ -1380,10 +1399,11 @@ bool bn_bwd_bias_ok(int C) { return C % 4 == 0 && kThreads % (C / 4) == 0; }
 
 cudaError_t bn_bwd(const float* x, const float* dy, int64_t rows, int C, const float* gamma, const float* beta,
                    const float* stats, int relu, float* dx, int accumulate, float* dgamma, float* dbeta,
-                   float* red_scratch, cudaStream_t st, float* dbias) {
+                   float* red_scratch, cudaStream_t st, float* dbias, float* copy_dst, int copy_acc) {
   float* coef = red_scratch + static_cast<int64_t>(kRedChunks) * 2 * C * 2;  // past the partials
-  cudaError_t e = colred(RedBnBwdOp{x, dy, stats, gamma, beta, relu}, BnBwdFin{C, dgamma, dbeta, coef}, rows, C,
-                         red_scratch, st);
+  if (copy_dst && C % 4 != 0) return cudaErrorInvalidValue;
+  cudaError_t e = colred(RedBnBwdOp{x, dy, stats, gamma, beta, relu, copy_dst, copy_acc},
+                         BnBwdFin{C, dgamma, dbeta, coef}, rows, C, red_scratch, st);
   if (e != cudaSuccess) return e;
   const int64_t n = rows * C;
   if (dbias && (!dx || !bn_bwd_bias_ok(C))) return cudaErrorInvalidValue;
