@@ -438,6 +438,7 @@ struct Compiler {
 
   // ---- layer kernels ----
   void forward(int lid, bool replay) {
+    if (replay && dead_at[cur_ti] && net.kind[lid] != snp::ACT) return;  // output never read (plan_fusions)
     const LayerRt& l = ex->L[lid];
     for (int p : net.prev[lid]) wait_fetch(p);
     float* y = ptr(snp::K_ACT, lid);
@@ -953,6 +954,57 @@ struct Compiler {
           if (k == snp::CONV || k == snp::BN || k == snp::POOL || k == snp::LRN || k == snp::FC)
             for (int p : net.prev[f.b]) read |= p == ra;
         }
+      }
+      if (!read) dead_at[i] = 1;
+    }
+    // Dead replays (general): a replay of an unfused layer whose output no later
+    // action reads before it is freed or rewritten -- under the kernels' actual
+    // reads, which are narrower than the reference's BACKWARD_NEEDS (the ReLU
+    // backward folded into the BN backward reads the BN input, not the BN
+    // output; average-pool backward reads neither x nor y).
+    auto reads_act = [&](size_t j, int L) -> bool {
+      const snp::Event& f = P.tape[j];
+      const int M = f.b;
+      if (f.op == 'O') return M == L;
+      if (f.op == 'C' || f.op == 'R') {
+        if (dead_at[j] || join_fuse_at[j] >= 0) return false;  // not launched here
+        if (fused_into[j] >= 0) return net.prev[fused_into[j]][0] == L;  // BN+ReLU: reads the BN input
+        if (join_from[j] >= 0) {
+          const int ra = P.tape[join_from[j]].b, bnj = net.prev[ra][0];
+          const int oth = net.prev[M][0] == ra ? net.prev[M][1] : net.prev[M][0];
+          return L == net.prev[bnj][0] || L == oth;
+        }
+        if (net.kind[M] == snp::BN && fuse_at[j] && f.op == 'R') return false;  // stats only on replay: none
+        for (int p : net.prev[M])
+          if (p == L) return true;
+        return false;
+      }
+      if (f.op == 'B') {
+        const int k = net.kind[M];
+        const bool x = !net.prev[M].empty() && net.prev[M][0] == L;
+        switch (k) {
+          case snp::CONV: case snp::FC: case snp::BN: return x;
+          case snp::POOL: return ex->L[M].pool.mode == 0 && (x || M == L);
+          case snp::LRN: return x || M == L;
+          case snp::SOFTMAX: return M == L;
+          case snp::ACT: return M == L && !act_bwd_skip[j];
+          default: return false;  // JOIN, DROPOUT read no activations
+        }
+      }
+      return false;
+    };
+    for (size_t i = 0; i < T; ++i) {
+      const snp::Event& e = P.tape[i];
+      if (e.op != 'R' || dead_at[i] || fused_into[i] >= 0 || join_from[i] >= 0 || join_fuse_at[i] >= 0) continue;
+      const int L = e.b;
+      if (net.kind[L] == snp::BN && fuse_at[i]) continue;  // launches nothing anyway
+      if (net.kind[L] == snp::SOFTMAX) continue;          // keeps its loss-row side effect simple
+      bool read = false;
+      for (size_t j = i + 1; j < T && !read; ++j) {
+        const snp::Event& f = P.tape[j];
+        if (f.op == 'F' && f.a == snp::K_ACT && f.b == L) break;
+        if ((f.op == 'C' || f.op == 'R') && f.b == L) break;
+        read = reads_act(j, L);
       }
       if (!read) dead_at[i] = 1;
     }
