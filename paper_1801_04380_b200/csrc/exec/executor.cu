@@ -67,6 +67,7 @@ struct LayerRt {
   sn::PoolShape pool{};
   int fc_in = 0, fc_splits = 1, wgrad_splits = 1;
   int stats_tiles = 0, stats_rows = 0;  // CONV: BN statistics tiles its forward can emit
+  uint8_t* argmax = nullptr;            // max POOL: per-output window argmax saved by the forward
 };
 
 struct Action {
@@ -291,6 +292,13 @@ void alloc_device(sn_exec* ex) {
   for (int i = 0; i < net.n; ++i)
     if (ex->L[i].kind == snp::POOL) pool_bytes = std::max(pool_bytes, sn::pool_scratch_bytes(ex->L[i].pool));
   ck(cudaMalloc(&ex->pool_scratch, static_cast<size_t>(pool_bytes)), "cudaMalloc(pool scratch)");
+  // saved max-pool argmaxes: layer state outside the pool accounting, like the
+  // BN saved statistics (one byte per output element)
+  for (int i = 0; i < net.n; ++i) {
+    LayerRt& l = ex->L[i];
+    if (l.kind == snp::POOL && sn::pool_saves_argmax(l.pool))
+      ck(cudaMalloc(&l.argmax, static_cast<size_t>(l.pool.N) * l.pool.P * l.pool.Q * l.pool.C), "cudaMalloc(argmax)");
+  }
   if (ex->data_id < 0) xfail(SN_EK_UNSUPPORTED, "numeric execution needs a DATA layer");
   const LayerRt& data = ex->L[ex->data_id];
   ex->image_floats = static_cast<int64_t>(ex->B) * data.H * data.W * data.C_raw;
@@ -520,7 +528,8 @@ struct Compiler {
         break;
       case snp::POOL: {
         const sn::PoolShape ps = l.pool;
-        push([=] { ck(sn::pool_fwd(ps, x, y, st), "pool_fwd"); }, 1);
+        uint8_t* am = l.argmax;
+        push([=] { ck(sn::pool_fwd(ps, x, y, st, am), "pool_fwd"); }, 1);
         break;
       }
       case snp::LRN: {
@@ -699,7 +708,8 @@ struct Compiler {
         const sn::PoolShape ps = l.pool;
         void* scratch = ex->pool_scratch;
         const int nk = sn::pool_bwd_kernels(ps);
-        if (dx) push([=] { ck(sn::pool_bwd(ps, x, y, dy, dx, acc, scratch, st), "pool_bwd"); }, nk);
+        const uint8_t* am = l.argmax;
+        if (dx) push([=] { ck(sn::pool_bwd(ps, x, y, dy, dx, acc, scratch, st, am), "pool_bwd"); }, nk);
         break;
       }
       case snp::LRN: {
@@ -1184,6 +1194,8 @@ void destroy(sn_exec* ex) {
                   const_cast<float**>(ex->ptr_table)};
   for (void* b : bufs)
     if (b) cudaFree(b);
+  for (auto& l : ex->L)
+    if (l.argmax) cudaFree(l.argmax);
   if (ex->s0) cudaStreamDestroy(ex->s0);
   if (ex->s1) cudaStreamDestroy(ex->s1);
   if (ex->s2) cudaStreamDestroy(ex->s2);

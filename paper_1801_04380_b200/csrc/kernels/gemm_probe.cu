@@ -130,6 +130,15 @@ extern "C" long long sn_test_pool(int op, const int* shape, void** p, int flag) 
   sn::PoolShape s{shape[0], shape[1], shape[2], shape[3], shape[4], shape[5], shape[6], shape[7], shape[8], shape[9]};
   if (op == 2) return sn::pool_scratch_bytes(s);
   if (op == 3) return sn::pool_bwd_kernels(s);
+  if (op == 4) return sn::pool_saves_argmax(s) ? 1 : 0;
+  if (op == 5) {  // forward recording the argmax, then the backward using it: p = {x, y, dy, dx, scratch, argmax}
+    cudaError_t e = sn::pool_fwd(s, (const float*)p[0], (float*)p[1], 0, (uint8_t*)p[5]);
+    if (e == cudaSuccess)
+      e = sn::pool_bwd(s, (const float*)p[0], (const float*)p[1], (const float*)p[2], (float*)p[3], flag, p[4], 0,
+                       (const uint8_t*)p[5]);
+    if (e != cudaSuccess) return 4;
+    return cudaDeviceSynchronize() == cudaSuccess ? 0 : 4;
+  }
   cudaError_t e;
   if (op == 0)
     e = sn::pool_fwd(s, (const float*)p[0], (float*)p[1], 0);

@@ -146,14 +146,18 @@ cudaError_t relu_bwd_inplace(const float* y, float* g, int64_t n, cudaStream_t s
 struct PoolShape {
   int N, H, W, C, P, Q, K, stride, pad, mode;  // mode 0 max, 1 avg
 };
-cudaError_t pool_fwd(const PoolShape& s, const float* x, float* y, cudaStream_t st);
+// argmax (optional, pool_saves_argmax(s)): the forward also records, per output
+// element, the first window position holding the maximum (one byte); the
+// backward then gathers with it instead of re-deriving it from x and y.
+bool pool_saves_argmax(const PoolShape& s);
+cudaError_t pool_fwd(const PoolShape& s, const float* x, float* y, cudaStream_t st, uint8_t* argmax = nullptr);
 // Max-pool backward recomputes each window's first argmax from x and y (the
 // reference's backward reads) into a byte per output (executor scratch of
 // pool_scratch_bytes), then gathers; avg-pool gathers directly.
 int64_t pool_scratch_bytes(const PoolShape& s);
 int pool_bwd_kernels(const PoolShape& s);  // launches one pool_bwd issues
 cudaError_t pool_bwd(const PoolShape& s, const float* x, const float* y, const float* dy, float* dx,
-                     int accumulate, void* scratch, cudaStream_t st);
+                     int accumulate, void* scratch, cudaStream_t st, const uint8_t* argmax = nullptr);
 
 cudaError_t lrn_fwd(const float* x, float* y, int64_t pixels, int C, int size, float alpha, float beta,
                     float k, cudaStream_t st);

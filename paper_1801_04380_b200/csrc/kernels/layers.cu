@@ -719,7 +719,7 @@ __global__ void pool_fwd_v4_kernel(PoolShape s, const float4* __restrict__ x, fl
 // per-element index math left is one division by C/4.
 template <int KC, int SC>
 __global__ void __launch_bounds__(256) pool_fwd_rows_kernel(PoolShape s, const float4* __restrict__ x,
-                                                            float4* __restrict__ y) {
+                                                            float4* __restrict__ y, uchar4* __restrict__ arg) {
   const int C4 = s.C >> 2;
   const int p = blockIdx.x, n = blockIdx.y;
   const int h0 = p * SC - s.pad;
@@ -741,20 +741,24 @@ __global__ void __launch_bounds__(256) pool_fwd_rows_kernel(PoolShape s, const f
       }
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     if (s.mode == 0) {
+      // max and the first (row-major) position holding it, for the backward
       bool have = false;
+      int a0 = 255, a1 = 255, a2 = 255, a3 = 255;
 #pragma unroll
       for (int k = 0; k < KC * KC; ++k) {
         if (!in[k]) continue;
         if (!have) {
           acc = v[k];
+          a0 = a1 = a2 = a3 = k;
           have = true;
         } else {
-          acc.x = v[k].x > acc.x ? v[k].x : acc.x;
-          acc.y = v[k].y > acc.y ? v[k].y : acc.y;
-          acc.z = v[k].z > acc.z ? v[k].z : acc.z;
-          acc.w = v[k].w > acc.w ? v[k].w : acc.w;
+          if (v[k].x > acc.x) { acc.x = v[k].x; a0 = k; }
+          if (v[k].y > acc.y) { acc.y = v[k].y; a1 = k; }
+          if (v[k].z > acc.z) { acc.z = v[k].z; a2 = k; }
+          if (v[k].w > acc.w) { acc.w = v[k].w; a3 = k; }
         }
       }
+      if (arg) arg[(static_cast<size_t>(n) * s.P + p) * s.Q * C4 + i] = make_uchar4(a0, a1, a2, a3);
     } else {
 #pragma unroll
       for (int k = 0; k < KC * KC; ++k)
@@ -973,7 +977,8 @@ template <int KC, int SC>
 __global__ void __launch_bounds__(256) pool_max_bwd_fused(PoolShape s, const float4* __restrict__ x,
                                                           const float4* __restrict__ y,
                                                           const float4* __restrict__ dy, float4* dx,
-                                                          int accumulate, int PB, int WR) {
+                                                          int accumulate, int PB, int WR,
+                                                          const uchar4* __restrict__ saved) {
   extern __shared__ float4 psm[];
   const int K = KC > 0 ? KC : s.K, ST = SC > 0 ? SC : s.stride;
   float4* sdy = psm;                                                  // [WR][Q][kPoolCv]
@@ -999,8 +1004,14 @@ __global__ void __launch_bounds__(256) pool_max_bwd_fused(PoolShape s, const flo
     const int64_t orow = (static_cast<int64_t>(n) * s.P + p) * s.Q;
     for (int q = lane; q < s.Q; q += 64) {
       const int64_t o = (orow + q) * C4 + c4 + cv;
-      const float4 m = y[o];
       const float4 g = dy[o];
+      if (saved) {  // argmax recorded by the forward: no x / y reads
+        const int j = ((p - pl) * s.Q + q) * kPoolCv + cv;
+        sarg[j] = saved[o];
+        sdy[j] = g;
+        continue;
+      }
+      const float4 m = y[o];
       const int w0 = q * ST - s.pad;
       int a0 = 255, a1 = 255, a2 = 255, a3 = 255;
       if constexpr (KC > 0) {
@@ -1075,6 +1086,64 @@ __global__ void __launch_bounds__(256) pool_max_bwd_fused(PoolShape s, const flo
         acc.x += o.x; acc.y += o.y; acc.z += o.z; acc.w += o.w;
       }
       *d = acc;
+    }
+  }
+}
+
+// Max-pool 3x3 / stride 2 / pad 1 backward with the forward's saved argmax, for
+// H = 2P, W = 2Q: one thread per 2 x 2 block of input pixels (rows 2m, 2m+1,
+// columns 2k, 2k+1) and channel quad.  The four windows (m|m+1, k|k+1) that can
+// cover the block are read once; input (2m+dh, 2k+dw) sits at window offset
+// (dh+1, dw+1) of window (m, k) and (dh-1, dw-1) of window (m+1, k+1), etc.
+// Contributions are summed in window order (m,k), (m,k+1), (m+1,k), (m+1,k+1)
+// -- the ascending (p, q) order of the general kernel, so the bits agree.
+__global__ void __launch_bounds__(256) pool_max_bwd_k3s2(PoolShape s, const uchar4* __restrict__ arg,
+                                                         const float4* __restrict__ dy, float4* dx, int accumulate,
+                                                         int64_t total) {
+  const int C4 = s.C >> 2;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c4 = static_cast<int>(i % C4);
+    int64_t t = i / C4;
+    const int k = static_cast<int>(t % s.Q);
+    t /= s.Q;
+    const int m = static_cast<int>(t % s.P);
+    const int n = static_cast<int>(t / s.P);
+    const int64_t wbase = (static_cast<int64_t>(n) * s.P + m) * s.Q + k;  // window (m, k)
+    const bool k1 = k + 1 < s.Q, m1 = m + 1 < s.P;
+    const uchar4 a00 = arg[wbase * C4 + c4];
+    const float4 g00 = dy[wbase * C4 + c4];
+    const uchar4 a01 = k1 ? arg[(wbase + 1) * C4 + c4] : make_uchar4(255, 255, 255, 255);
+    const float4 g01 = k1 ? dy[(wbase + 1) * C4 + c4] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const uchar4 a10 = m1 ? arg[(wbase + s.Q) * C4 + c4] : make_uchar4(255, 255, 255, 255);
+    const float4 g10 = m1 ? dy[(wbase + s.Q) * C4 + c4] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const uchar4 a11 = (k1 && m1) ? arg[(wbase + s.Q + 1) * C4 + c4] : make_uchar4(255, 255, 255, 255);
+    const float4 g11 = (k1 && m1) ? dy[(wbase + s.Q + 1) * C4 + c4] : make_float4(0.f, 0.f, 0.f, 0.f);
+    // out[dh][dw]: (window, offset) pairs in window order
+    float4 o[4];
+#define SN_PICK(A, G, OFF, ACC)                    \
+  ACC.x += (A.x == (OFF)) ? G.x : 0.f;             \
+  ACC.y += (A.y == (OFF)) ? G.y : 0.f;             \
+  ACC.z += (A.z == (OFF)) ? G.z : 0.f;             \
+  ACC.w += (A.w == (OFF)) ? G.w : 0.f;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) o[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    SN_PICK(a00, g00, 4, o[0]);                                          // (0,0)
+    SN_PICK(a00, g00, 5, o[1]); SN_PICK(a01, g01, 3, o[1]);              // (0,1)
+    SN_PICK(a00, g00, 7, o[2]); SN_PICK(a10, g10, 1, o[2]);              // (1,0)
+    SN_PICK(a00, g00, 8, o[3]); SN_PICK(a01, g01, 6, o[3]);              // (1,1)
+    SN_PICK(a10, g10, 2, o[3]); SN_PICK(a11, g11, 0, o[3]);
+#undef SN_PICK
+    const int64_t r0 = ((static_cast<int64_t>(n) * s.H + 2 * m) * s.W + 2 * k) * C4 + c4;
+    const int64_t r1 = r0 + static_cast<int64_t>(s.W) * C4;
+    float4* d[4] = {dx + r0, dx + r0 + C4, dx + r1, dx + r1 + C4};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (accumulate) {
+        const float4 old = *d[q];
+        o[q].x += old.x; o[q].y += old.y; o[q].z += old.z; o[q].w += old.w;
+      }
+      *d[q] = o[q];
     }
   }
 }
@@ -1442,7 +1511,7 @@ cudaError_t relu_bwd_inplace(const float* y, float* g, int64_t n, cudaStream_t s
   return cudaGetLastError();
 }
 
-cudaError_t pool_fwd(const PoolShape& s, const float* x, float* y, cudaStream_t st) {
+cudaError_t pool_fwd(const PoolShape& s, const float* x, float* y, cudaStream_t st, uint8_t* argmax) {
   const int64_t total = static_cast<int64_t>(s.N) * s.P * s.Q * s.C;
   if (s.C % 4 == 0 && static_cast<int64_t>(s.N) * s.H * s.W * s.C < (1ll << 31)) {
     if (s.P == 1 && s.Q == 1 && s.pad == 0 && s.K == s.H && s.K == s.W) {
@@ -1452,7 +1521,8 @@ cudaError_t pool_fwd(const PoolShape& s, const float* x, float* y, cudaStream_t 
     }
     if (s.K == 3 && s.stride == 2) {
       pool_fwd_rows_kernel<3, 2><<<dim3(s.P, s.N), 256, 0, st>>>(s, reinterpret_cast<const float4*>(x),
-                                                                 reinterpret_cast<float4*>(y));
+                                                                 reinterpret_cast<float4*>(y),
+                                                                 reinterpret_cast<uchar4*>(argmax));
       return cudaGetLastError();
     }
     const int total4 = static_cast<int>(total / 4);
@@ -1486,8 +1556,23 @@ int64_t pool_scratch_bytes(const PoolShape& s) {
   return (s.C % 4 == 0 && s.mode == 0 && s.K * s.K < 255) ? static_cast<int64_t>(s.N) * s.P * s.Q * s.C : 0;
 }
 
+bool pool_saves_argmax(const PoolShape& s) {
+  int PB, WR;
+  size_t smem;
+  return s.mode == 0 && s.K == 3 && s.stride == 2 && s.C % 4 == 0 && !(s.P == 1 && s.Q == 1) &&
+         static_cast<int64_t>(s.N) * s.H * s.W * s.C < (1ll << 31) && pool_fused_ok(s, &PB, &WR, &smem);
+}
+
 cudaError_t pool_bwd(const PoolShape& s, const float* x, const float* y, const float* dy, float* dx, int accumulate,
-                     void* scratch, cudaStream_t st) {
+                     void* scratch, cudaStream_t st, const uint8_t* argmax) {
+  if (argmax && s.mode == 0 && s.K == 3 && s.stride == 2 && s.pad == 1 && s.H == 2 * s.P && s.W == 2 * s.Q &&
+      s.C % 4 == 0) {
+    const int64_t total = static_cast<int64_t>(s.N) * s.P * s.Q * (s.C / 4);
+    pool_max_bwd_k3s2<<<blocks_for(total, kThreads, 148 * 32), kThreads, 0, st>>>(
+        s, reinterpret_cast<const uchar4*>(argmax), reinterpret_cast<const float4*>(dy), reinterpret_cast<float4*>(dx),
+        accumulate, total);
+    return cudaGetLastError();
+  }
   int PB, WR;
   size_t smem;
   if (pool_fused_ok(s, &PB, &WR, &smem)) {
@@ -1498,7 +1583,7 @@ cudaError_t pool_bwd(const PoolShape& s, const float* x, const float* y, const f
                                            : pool_max_bwd_fused<0, 0>;
     k<<<grid, 256, smem, st>>>(s, reinterpret_cast<const float4*>(x), reinterpret_cast<const float4*>(y),
                                reinterpret_cast<const float4*>(dy), reinterpret_cast<float4*>(dx), accumulate, PB,
-                               WR);
+                               WR, reinterpret_cast<const uchar4*>(argmax));
     return cudaGetLastError();
   }
   if (s.C % 4 == 0 && (s.mode == 1 || (scratch && s.K * s.K < 255))) {

@@ -319,3 +319,13 @@ def test_pool_fwd_bwd_exact(cuda, case, ties):
     assert lib.sn_test_pool(1, shape, ptrs, 1) == 0  # accumulate
     got2 = dx_d.permute(0, 3, 1, 2).cpu()
     assert torch.allclose(got2, 2 * got, rtol=0, atol=0) if mode == 0 else torch.allclose(got2, 2 * got)
+    if lib.sn_test_pool(4, shape, None, 0):
+        # the forward records the argmax, the backward gathers with it: same bits
+        am = torch.zeros(N * P * Q * C, dtype=torch.uint8, device=cuda)
+        y2 = torch.full((N, P, Q, C), float("nan"), device=cuda)
+        dx2 = torch.full((N, H, W, C), float("nan"), device=cuda)
+        ptrs = (ctypes.c_void_p * 6)(x_d.data_ptr(), y2.data_ptr(), dy_d.data_ptr(), dx2.data_ptr(),
+                                     scratch.data_ptr(), am.data_ptr())
+        assert lib.sn_test_pool(5, shape, ptrs, 0) == 0
+        assert torch.equal(y2, y_d)
+        assert torch.equal(dx2.permute(0, 3, 1, 2).cpu(), got)
