@@ -796,3 +796,224 @@ cudaError_t conv_halo_wgrad(int N, int H, int W, int C, int K, int R, int S, int
 }
 
 }  // namespace sn
+
+// ---------------------------------------------------------------------------
+// Halo weight gradient for C, K multiples of 128 (M = 128, N = 128 MMAs):
+//   dW[(r, s, c)][k] = sum_p x[p + r*Wp + s - pad*(Wp+1)][c] dy[p][k]
+// A CTA owns one job (filter row r, 128-channel group, 128-k group) and a
+// contiguous range of (image, band) work units; per unit it loads, for each of
+// its 4 channel chunks, the TR input rows of filter row r (one TMA box, zero
+// filled) and the TR rows of dy (one box per k chunk).  The S column taps of
+// the row are K-row shifts of the A descriptor; the A operand's four MN atoms
+// are the four channel-chunk buffers (uniform LBO).  S accumulators of 128
+// columns live in TMEM for the whole range; the CTA then writes its partial
+// slice [split][R*S*C][K] for its job's rows (every (split, row) written once:
+// the CTAs are split evenly across jobs).
+namespace sn {
+namespace {
+
+struct HaloWg128Args {
+  int Wp, TR, R, S, pad, P, bands, units;  // units = N * bands
+  int C, K, jobs_c, jobs_k, per_job;       // per_job = CTAs per job = splits
+  uint32_t box_bytes, slot;                // one chunk box; smem per chunk buffer
+  int ksteps;
+  float* partial;
+};
+
+constexpr int kWg128Stages = 2;
+
+__global__ void __launch_bounds__(kHaloThreads, 1)
+    tc_conv_halo_wgrad128(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmDY,
+                          HaloWg128Args a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t stage_bytes = 8 * a.slot;  // 4 x chunks, 4 dy chunks
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kWg128Stages * stage_bytes);
+  uint64_t* empty = full + kWg128Stages;
+  uint64_t* done = empty + kWg128Stages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  for (uint32_t i = threadIdx.x * 16; i < kWg128Stages * stage_bytes; i += blockDim.x * 16)
+    *reinterpret_cast<float4*>(smem + i) = make_float4(0.f, 0.f, 0.f, 0.f);
+  fence_proxy_async();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kWg128Stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 5) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const int jobs = a.R * a.jobs_c * a.jobs_k;
+  const int job = blockIdx.x / a.per_job, split = blockIdx.x % a.per_job;
+  const bool active = job < jobs;
+  const int r = active ? job / (a.jobs_c * a.jobs_k) : 0;
+  const int cg = active ? (job / a.jobs_k) % a.jobs_c : 0, kg = active ? job % a.jobs_k : 0;
+  const int per = (a.units + a.per_job - 1) / a.per_job;
+  const int u0 = active ? min(a.units, split * per) : 0, u1 = active ? min(a.units, u0 + per) : 0;
+
+  if (warp == 4) {
+    uint32_t s = 0, ph = 0;
+    bool wrap = false;
+    for (int u = u0; u < u1; ++u) {
+      const int n = u / a.bands, y0 = (u - n * a.bands) * a.TR;
+      if (wrap) mbar_wait(&empty[s], ph ^ 1);
+      if (elect_one()) {
+        uint8_t* st = smem + s * stage_bytes;
+        mbar_arrive_expect_tx(&full[s], 8 * a.box_bytes);
+        for (int c = 0; c < 4; ++c) {
+          tma_load_4d(smem_u32(st + c * a.slot), &tmX, &full[s], cg * 128 + c * 32, -a.pad, y0 + r - a.pad, n);
+          tma_load_4d(smem_u32(st + (4 + c) * a.slot), &tmDY, &full[s], kg * 128 + c * 32, 0, y0, n);
+        }
+      }
+      __syncwarp();
+      if (++s == kWg128Stages) {
+        s = 0;
+        ph ^= 1;
+        wrap = true;
+      }
+    }
+  } else if (warp == 5) {
+    constexpr uint32_t idesc = idesc_tf32(128, 128, true, true);
+    const uint64_t xd0 = umma_desc(smem_u32(smem), a.slot, 512, kLayoutSW128Base32);
+    const uint64_t dd0 = umma_desc(smem_u32(smem + 4 * a.slot), a.slot, 512, kLayoutSW128Base32);
+    const uint32_t sstep = stage_bytes >> 4;
+    uint32_t s = 0, ph = 0;
+    bool first = true;
+    for (int u = u0; u < u1; ++u) {
+      mbar_wait(&full[s], ph);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint64_t xd = xd0 + s * sstep, dd = dd0 + s * sstep;
+        for (int kq = 0; kq < a.ksteps; ++kq) {
+          const uint32_t acc = (first && kq == 0) ? 0u : 1u;
+          for (int sx = 0; sx < a.S; ++sx)
+            umma_tf32(tmem + static_cast<uint32_t>(sx * 128), xd + static_cast<uint32_t>(sx + 8 * kq) * 8u,
+                      dd + static_cast<uint32_t>(kq) * 64u, idesc, acc);
+        }
+        umma_commit(&empty[s]);
+      }
+      __syncwarp();
+      first = false;
+      if (++s == kWg128Stages) {
+        s = 0;
+        ph ^= 1;
+      }
+    }
+    if (elect_one()) umma_commit(done);
+    __syncwarp();
+  } else if (active) {
+    // epilogue: thread (warp w, lane l) = channel 32 w + l of the group, all 128 k of each tap
+    const int c = cg * 128 + warp * 32 + lane;
+    float* out = a.partial + static_cast<size_t>(split) * a.R * a.S * a.C * a.K;
+    if (u0 >= u1) {
+      for (int sx = 0; sx < a.S; ++sx) {
+        float4* dst = reinterpret_cast<float4*>(out + (static_cast<size_t>(r * a.S + sx) * a.C + c) * a.K + kg * 128);
+        for (int q = 0; q < 32; ++q) dst[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    } else {
+      mbar_wait(done, 0);
+      tc_fence_after();
+      for (int sx = 0; sx < a.S; ++sx) {
+        float4* dst = reinterpret_cast<float4*>(out + (static_cast<size_t>(r * a.S + sx) * a.C + c) * a.K + kg * 128);
+        for (int k0 = 0; k0 < 128; k0 += 32) {
+          float v[32];
+          tmem_ld32(tmem + static_cast<uint32_t>(sx * 128 + k0) + (static_cast<uint32_t>(warp * 32) << 16), v);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) dst[k0 / 4 + q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+}  // namespace
+
+// Rows per band: as many padded rows as keep two stages of 8 chunk buffers
+// (with their slack rows) in shared memory.
+int wg128_tr(int Wp, int S, int P, uint32_t* slot_out) {
+  int best = 0;
+  uint32_t best_slot = 0;
+  for (int t = 1; t <= P && t * Wp <= kBM; ++t) {
+    const int rows = (t * Wp + 7) / 8 * 8 + S + 8;
+    const uint32_t slot = (rows * 128 + 1023) / 1024 * 1024;
+    if (kWg128Stages * 8 * slot + 1024 + 256 <= 227 * 1024) {
+      best = t;
+      best_slot = slot;
+    }
+  }
+  if (slot_out) *slot_out = best_slot;
+  return best;
+}
+
+// C, K multiples of 128, stride 1, S <= 4 taps per row, padded width <= 128.
+bool conv_halo_wgrad128_ok(int N, int H, int W, int C, int K, int R, int S, int pad, int P, int Q) {
+  if (halo_mode() == 0 || C % 128 != 0 || K % 128 != 0 || S > 4 || R * S < 2 || !tma_encoders_ok()) return false;
+  if (P != H + 2 * pad - R + 1 || Q != W + 2 * pad - S + 1 || pad < 0) return false;
+  const int Wp = W + 2 * pad;
+  if (Wp > kBM) return false;
+  const int TR = wg128_tr(Wp, S, P, nullptr);
+  if (TR < 1) return false;
+  // by shape: most band positions real (junk columns cost MMA work), C = K = 128
+  if (halo_mode() == 1 && (TR * Q * 4 < 3 * TR * Wp || C > 128 || K > 128)) return false;
+  const int jobs = R * (C / 128) * (K / 128);
+  if (jobs > conv_halo_wgrad_splits()) return false;
+  const int per_job = conv_halo_wgrad_splits() / jobs;
+  return static_cast<int64_t>(per_job) * R * S * C * K <= (64ll << 20);
+}
+
+int conv_halo_wgrad128_splits(int C, int K, int R) {
+  const int jobs = R * (C / 128) * (K / 128);
+  return conv_halo_wgrad_splits() / jobs;
+}
+
+cudaError_t conv_halo_wgrad128(int N, int H, int W, int C, int K, int R, int S, int pad, int P, int Q,
+                               const float* x, const float* dy, float* partial, float* dw, cudaStream_t st) {
+  if (!conv_halo_wgrad128_ok(N, H, W, C, K, R, S, pad, P, Q)) return cudaErrorInvalidValue;
+  HaloWg128Args a{};
+  a.Wp = W + 2 * pad;
+  uint32_t slot = 0;
+  a.TR = wg128_tr(a.Wp, S, P, &slot);
+  a.R = R;
+  a.S = S;
+  a.pad = pad;
+  a.P = P;
+  a.bands = (P + a.TR - 1) / a.TR;
+  a.units = N * a.bands;
+  a.C = C;
+  a.K = K;
+  a.jobs_c = C / 128;
+  a.jobs_k = K / 128;
+  a.per_job = conv_halo_wgrad128_splits(C, K, R);
+  a.box_bytes = static_cast<uint32_t>(a.TR * a.Wp) * 128;
+  a.slot = slot;
+  a.ksteps = (a.TR * a.Wp + 7) / 8;
+  a.partial = partial;
+  CUtensorMap X, DY;
+  // x: TR rows of one filter row; dy: TR rows (columns >= Q read as zero)
+  if (!tma_map_nhwc(&X, x, N, H, W, C, a.Wp, a.TR, 1)) return cudaErrorInvalidValue;
+  if (!tma_map_nhwc(&DY, dy, N, P, Q, K, a.Wp, a.TR, 1)) return cudaErrorInvalidValue;
+  const int smem = kWg128Stages * 8 * a.slot + 1024 + 256;
+  cudaError_t err = cudaFuncSetAttribute(tc_conv_halo_wgrad128, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (err != cudaSuccess) return err;
+  const int grid = a.per_job * R * a.jobs_c * a.jobs_k;
+  tc_conv_halo_wgrad128<<<grid, kHaloThreads, smem, st>>>(X, DY, a);
+  err = cudaGetLastError();
+  if (err != cudaSuccess) return err;
+  return splitk_reduce(partial, a.per_job, R * S * C, K, dw, nullptr, 0, 1, st);
+}
+
+}  // namespace sn

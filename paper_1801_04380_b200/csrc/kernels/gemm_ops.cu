@@ -488,7 +488,9 @@ cudaError_t conv_dgrad(const ConvShape& s, const float* dy, const float* w, floa
 }
 
 int conv_wgrad_splits(const ConvShape& s, int64_t partial_floats_cap) {
-  // the halo weight-gradient kernel writes one partial slice per CTA
+  // the halo weight-gradient kernels write one partial slice per CTA (per job)
+  if (use_tma() && s.stride == 1 && conv_halo_wgrad128_ok(s.N, s.H, s.W, s.C, s.K, s.R, s.S, s.pad, s.P, s.Q))
+    return conv_halo_wgrad128_splits(s.C, s.K, s.R);
   if (use_tma() && s.stride == 1 && conv_halo_wgrad_ok(s.N, s.H, s.W, s.C, s.K, s.R, s.S, s.pad, s.P, s.Q))
     return conv_halo_wgrad_splits();
   const int64_t RSC = static_cast<int64_t>(s.R) * s.S * s.C;
@@ -509,6 +511,12 @@ cudaError_t conv_wgrad(const ConvShape& s, const float* x, const float* dy, floa
                        int splits, float* red_scratch, cudaStream_t st) {
   cudaError_t e;
   splits = effective_splits(s.N * s.P * s.Q, splits);  // the count the launch will really use
+  if (use_tma() && s.stride == 1 && conv_halo_wgrad128_ok(s.N, s.H, s.W, s.C, s.K, s.R, s.S, s.pad, s.P, s.Q)) {
+    e = conv_halo_wgrad128(s.N, s.H, s.W, s.C, s.K, s.R, s.S, s.pad, s.P, s.Q, x, dy, partial, dw, st);
+    if (e != cudaSuccess) return e;
+    if (!db) return cudaSuccess;
+    return bias_grad(dy, static_cast<int64_t>(s.N) * s.P * s.Q, s.K, db, red_scratch, st);
+  }
   if (use_tma() && s.stride == 1 && conv_halo_wgrad_ok(s.N, s.H, s.W, s.C, s.K, s.R, s.S, s.pad, s.P, s.Q)) {
     e = conv_halo_wgrad(s.N, s.H, s.W, s.C, s.K, s.R, s.S, s.pad, s.P, s.Q, x, dy, partial, dw, st);
     if (e != cudaSuccess) return e;

@@ -74,6 +74,12 @@ void set_conv_halo(int mode);  // 0 off, 1 by shape (default; env SN_CONV_HALO=0
 // floats, dw[K][R][S][C].
 bool conv_halo_wgrad_ok(int N, int H, int W, int C, int K, int R, int S, int pad, int P, int Q);
 int conv_halo_wgrad_splits();
+// C, K multiples of 128: one filter row x 128 channels x 128 k per CTA group,
+// M = N = 128 MMAs; partial = conv_halo_wgrad128_splits(C, K, R) * R*S*C*K floats.
+bool conv_halo_wgrad128_ok(int N, int H, int W, int C, int K, int R, int S, int pad, int P, int Q);
+int conv_halo_wgrad128_splits(int C, int K, int R);
+cudaError_t conv_halo_wgrad128(int N, int H, int W, int C, int K, int R, int S, int pad, int P, int Q,
+                               const float* x, const float* dy, float* partial, float* dw, cudaStream_t st);
 cudaError_t conv_halo_wgrad(int N, int H, int W, int C, int K, int R, int S, int pad, int P, int Q, const float* x,
                             const float* dy, float* partial, float* dw, cudaStream_t st);
 
