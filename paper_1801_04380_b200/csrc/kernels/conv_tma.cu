@@ -1191,14 +1191,189 @@ int conv_stem_wgrad_splits(const ConvShape& s) {
 
 int64_t stem_wgrad_partial_floats(const ConvShape& s) {
   const StemGeom g = stem_geom(s);
-  return static_cast<int64_t>(conv_stem_wgrad_splits(s)) * s.R * g.sblocks * 32 * s.K;
+  const int64_t rows = static_cast<int64_t>(s.R) * g.sblocks * 32 * s.K;
+  return std::max<int64_t>(conv_stem_wgrad_splits(s), num_sms()) * rows;
 }
+
+namespace {
+
+// Stem weight gradient, 4 output rows per k block: the sliding-window views of
+// input rows 2p .. 2p+13 (14 boxes of 32 windows) serve output rows p .. p+3 --
+// row p+g's filter-row atoms r = 0..7 are boxes 2g .. 2g+7, consecutive, so the
+// A operand of either 128-row M tile is a uniform-stride run of boxes -- and
+// both M tiles (filter rows 0-3, 4-7; row 7 is padding) share every dy box.
+// 22 boxes per 4 x 32 output pixels instead of 48: the 1-row kernel was bound
+// by this operand traffic.  Each CTA accumulates a contiguous range of units
+// (image, 4-row group, 32-column block) and writes one [256][64] partial slice.
+constexpr int kSwG = 4;  // output rows per k block
+constexpr int kSwStages = 2;
+struct StemWgArgs {
+  int N, P, Q, groups, qblocks, units, stride;
+  int M;           // valid rows R * 32 (the rest of the second M tile is the padding atom)
+  float* partial;  // [gridDim.x][M][64]
+};
+
+__global__ void __launch_bounds__(kTmaThreads, 1)
+    stem_wgrad_rows_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                           StemWgArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int NA = 2 * kSwG + 6, NB = 2 * kSwG;  // box slots per stage (stride <= 2)
+  const int na = a.stride * (kSwG - 1) + 8;         // input rows the 4 output rows need (8 = R padded)
+  constexpr uint32_t STAGE = (NA + NB) * 4096;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSwStages * STAGE);
+  uint64_t* empty = full + kSwStages;
+  uint64_t* done = empty + kSwStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kSwStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 5) tmem_alloc(tmem_slot, 128);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int per = (a.units + gridDim.x - 1) / gridDim.x;
+  const int u0 = min(a.units, static_cast<int>(blockIdx.x) * per), u1 = min(a.units, u0 + per);
+  auto unit = [&](int u, int& n, int& p0, int& qb) {
+    qb = u % a.qblocks;
+    const int r = u / a.qblocks;
+    p0 = (r % a.groups) * kSwG;
+    n = r / a.groups;
+  };
+  if (warp == 4) {
+    uint32_t s = 0, ph = 0;
+    bool wrap = false;
+    for (int u = u0; u < u1; ++u) {
+      int n, p0, qb;
+      unit(u, n, p0, qb);
+      if (wrap) mbar_wait(&empty[s], ph ^ 1);
+      if (elect_one()) {
+        uint8_t* st = smem + s * STAGE;
+        mbar_arrive_expect_tx(&full[s], (na + NB) * 4096);
+        for (int j = 0; j < na; ++j)
+          tma_load_4d(smem_u32(st + j * 4096), &tmA, &full[s], 0, qb * 32, p0 * a.stride + j, n);
+        for (int g = 0; g < kSwG; ++g)
+          for (int kc = 0; kc < 2; ++kc)
+            tma_load_4d(smem_u32(st + (NA + 2 * g + kc) * 4096), &tmB, &full[s], kc * 32, qb * 32, p0 + g, n);
+      }
+      __syncwarp();
+      if (++s == kSwStages) {
+        s = 0;
+        ph ^= 1;
+        wrap = true;
+      }
+    }
+  } else if (warp == 5) {
+    constexpr uint32_t idesc = idesc_tf32(kBM, 64, true, true);
+    const uint64_t a0 = umma_desc(smem_u32(smem), 4096, 512, kLayoutSW128Base32);
+    const uint64_t b0 = umma_desc(smem_u32(smem + NA * 4096), 4096, 512, kLayoutSW128Base32);
+    uint32_t s = 0, ph = 0;
+    bool first = true;
+    for (int u = u0; u < u1; ++u) {
+      mbar_wait(&full[s], ph);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint64_t ad = a0 + s * (STAGE >> 4), bd = b0 + s * (STAGE >> 4);
+#pragma unroll
+        for (int g = 0; g < kSwG; ++g)
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              umma_tf32(tmem + mt * 64, ad + (a.stride * g + 4 * mt) * 256 + kk * 64, bd + g * 512 + kk * 64, idesc,
+                        (first && g == 0 && kk == 0) ? 0u : 1u);
+        umma_commit(&empty[s]);
+      }
+      __syncwarp();
+      first = false;
+      if (++s == kSwStages) {
+        s = 0;
+        ph ^= 1;
+      }
+    }
+    if (elect_one()) umma_commit(done);
+    __syncwarp();
+  } else {
+    const int lane = threadIdx.x & 31;
+    float* out = a.partial + static_cast<size_t>(blockIdx.x) * a.M * 64;
+    if (u0 >= u1) {
+      for (int mt = 0; mt < 2; ++mt) {
+        const int row = mt * 128 + warp * 32 + lane;
+        if (row >= a.M) continue;
+        float4* dst = reinterpret_cast<float4*>(out + row * 64);
+        for (int q = 0; q < 16; ++q) dst[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    } else {
+      mbar_wait(done, 0);
+      tc_fence_after();
+      for (int mt = 0; mt < 2; ++mt) {
+        const int row = mt * 128 + warp * 32 + lane;
+        float4* dst = reinterpret_cast<float4*>(out + row * 64);
+        for (int c = 0; c < 64; c += 32) {
+          float v[32];
+          tmem_ld32(tmem + static_cast<uint32_t>(mt * 64 + c) + (static_cast<uint32_t>(warp * 32) << 16), v);
+          if (row < a.M) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              dst[c / 4 + q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 128);
+  }
+}
+
+}  // namespace
 
 cudaError_t conv_stem_wgrad(const ConvShape& s, const float* xp, const float* dy, float* partial, float* wp_scratch,
                             float* dw, float* db, float* red, cudaStream_t st) {
   const StemGeom g = stem_geom(s);
   const int Sp = g.sblocks * 8;
   const int M = s.R * g.sblocks * 32;
+  cudaError_t err;
+  if (s.K == 64 && g.sblocks == 1 && s.R <= 8 && s.P % kSwG == 0 && s.stride <= 2) {
+    CUtensorMap A, B;
+    if (!make_stem_view(&A, xp, g, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) return cudaErrorInvalidValue;
+    if (!make_nhwc4(&B, dy, s.N, s.P, s.Q, s.K, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) return cudaErrorInvalidValue;
+    StemWgArgs wa{};
+    wa.N = s.N;
+    wa.P = s.P;
+    wa.Q = s.Q;
+    wa.groups = s.P / kSwG;
+    wa.qblocks = g.qblocks;
+    wa.units = s.N * wa.groups * wa.qblocks;
+    wa.stride = s.stride;
+    wa.M = M;
+    wa.partial = partial;
+    const int grid = num_sms();
+    const int smem = kSwStages * (2 * kSwG + 6 + 2 * kSwG) * 4096 + 256 + 1024;
+    err = cudaFuncSetAttribute(stem_wgrad_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (err != cudaSuccess) return err;
+    stem_wgrad_rows_kernel<<<grid, kTmaThreads, smem, st>>>(A, B, wa);
+    err = cudaGetLastError();
+    if (err != cudaSuccess) return err;
+    // rows (r, s', c) of the [256][64] slices; rows >= R*32 are the padding atom
+    err = splitk_reduce(partial, grid, M, s.K, wp_scratch, nullptr, 0, 1, st);
+    if (err != cudaSuccess) return err;
+    stem_weights_kernel<<<148, 256, 0, st>>>(dw, wp_scratch, s.K, s.R, s.S, Sp, 0);
+    err = cudaGetLastError();
+    if (err != cudaSuccess) return err;
+    if (!db) return cudaSuccess;
+    return bias_grad(dy, static_cast<int64_t>(s.N) * s.P * s.Q, s.K, db, red, st);
+  }
   const int splits = conv_stem_wgrad_splits(s);
   const int BN = bn_for(s.K);
   CUtensorMap A, B, D;
@@ -1218,7 +1393,6 @@ cudaError_t conv_stem_wgrad(const ConvShape& s, const float* xp, const float* dy
   a.fqb = FastDivT(g.qblocks);
   a.fP = FastDivT(s.P);
   const EpiArgs e{nullptr, s.K, 0, 1};
-  cudaError_t err;
   switch (BN) {
     case 64: err = launch<64, 3>(A, B, D, a, e, M, s.K, splits, st); break;
     case 128: err = launch<128, 3>(A, B, D, a, e, M, s.K, splits, st); break;

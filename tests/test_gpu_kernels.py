@@ -196,6 +196,9 @@ STEM_CASES = [  # (N, C_raw, H, W, K, k, stride, pad)
     (3, 3, 32, 32, 32, 3, 1, 1),     # CIFAR-style 3x3 stride 1
     (2, 1, 28, 28, 128, 5, 1, 2),    # grayscale, 5x5, BN=128
     (2, 4, 40, 36, 256, 3, 2, 1),    # 4 real channels, BN=256, ragged rows
+    (3, 3, 64, 60, 64, 5, 2, 2),     # K=64, P % 4 == 0: multi-row forward and weight-gradient kernels
+    (2, 3, 32, 32, 64, 5, 1, 2),     # the same at stride 1
+    (2, 3, 30, 30, 32, 7, 2, 3),     # K=32, P % 4 != 0 (last row group partial)
 ]
 
 
