@@ -117,6 +117,12 @@ struct sn_exec {
   std::unordered_map<int, char*> stash;
   // streams / events
   cudaStream_t s0 = nullptr, s1 = nullptr, s2 = nullptr;
+  // s3: weight gradients (off the backward critical path) run on a side
+  // stream, overlapping the next layers' backward; their own scratch buffers
+  cudaStream_t s3 = nullptr;
+  float* partial_w = nullptr;
+  float* red_w = nullptr;
+  float* wt_w = nullptr;
   std::vector<cudaEvent_t> events;
   cudaEvent_t t_begin = nullptr, t_end = nullptr;
   // compiled program
@@ -288,6 +294,9 @@ void alloc_device(sn_exec* ex) {
   ck(cudaMalloc(&ex->partial, ex->partial_cap * sizeof(float)), "cudaMalloc(partial)");
   ck(cudaMalloc(&ex->wt_scratch, std::max<int64_t>(wt, 64) * sizeof(float)), "cudaMalloc(wt)");
   ck(cudaMalloc(&ex->red, red * sizeof(float)), "cudaMalloc(red)");
+  ck(cudaMalloc(&ex->partial_w, ex->partial_cap * sizeof(float)), "cudaMalloc(partial_w)");
+  ck(cudaMalloc(&ex->wt_w, std::max<int64_t>(wt, 64) * sizeof(float)), "cudaMalloc(wt_w)");
+  ck(cudaMalloc(&ex->red_w, red * sizeof(float)), "cudaMalloc(red_w)");
   int64_t pool_bytes = 256;
   for (int i = 0; i < net.n; ++i)
     if (ex->L[i].kind == snp::POOL) pool_bytes = std::max(pool_bytes, sn::pool_scratch_bytes(ex->L[i].pool));
@@ -333,7 +342,10 @@ struct Compiler {
   std::vector<std::pair<std::pair<int64_t, int64_t>, cudaEvent_t>> freed_reading;  // region being read by D2H
   std::unordered_map<int, cudaEvent_t> h2d_live;                   // act lid -> fetch event (not yet waited)
   std::vector<char> fetched;                                       // lids fetched anywhere in the tape
-  bool used_s1 = false, used_s2 = false;
+  bool used_s1 = false, used_s2 = false, used_s3 = false;
+  // activation / gradient keys a side-stream weight gradient still reads: when
+  // the tape frees one, later allocations over its blocks wait for that event
+  std::unordered_map<int64_t, cudaEvent_t> side_reads;
   int data_id = -1;
 
   Compiler(sn_exec* e) : ex(e), P(e->plan->plan), net(e->plan->plan.net) {
@@ -391,6 +403,11 @@ struct Compiler {
     const int64_t key = key_code(e.a, e.b);
     auto it = where.find(key);
     if (it == where.end()) xfail(SN_EK_INTERNAL, "tape frees an unknown key");
+    auto sr = side_reads.find(key);
+    if (sr != side_reads.end()) {
+      freed_reading.push_back({it->second, sr->second});
+      side_reads.erase(sr);
+    }
     if (e.a == snp::K_ACT) {
       auto d = d2h_live.find(e.b);
       if (d != d2h_live.end()) {
@@ -621,16 +638,35 @@ struct Compiler {
         const int sp = l.wgrad_splits;
         if (conv_bias_done[lid]) db = nullptr;  // summed by the BN backward's dx pass
         const int nbias = db ? 2 : 0;
+        // weight gradient on the side stream s3 (after everything s0 has issued so
+        // far: x and dy are ready), dgrad on s0 right away
+        cudaStream_t s3 = ex->s3;
+        float* part_w = ex->partial_w;
+        float* red_w = ex->red_w;
+        float* wt_w = ex->wt_w;
+        cudaEvent_t ready = ex->new_event(), wdone = ex->new_event();
+        used_s3 = true;
+        side_reads[snp::key_code(snp::K_ACT, pid)] = wdone;
+        side_reads[snp::key_code(snp::K_GRAD, owner)] = wdone;
         if (lid == ex->stem_layer) {  // DATA has no gradient
-          push([=] { ck(sn::conv_stem_wgrad(cs, x, dy, part, wt, dw, db, red, st), "conv_stem_wgrad"); },
-               3 + nbias);
+          push([=] {
+            ck(cudaEventRecord(ready, st), "record");
+            ck(cudaStreamWaitEvent(s3, ready, 0), "wait");
+            ck(sn::conv_stem_wgrad(cs, x, dy, part_w, wt_w, dw, db, red_w, s3), "conv_stem_wgrad");
+            ck(cudaEventRecord(wdone, s3), "record");
+          }, 3 + nbias);
           break;
         }
         const int ndgrad = !dx ? 0 : (cs.stride > 1 ? 2 * cs.stride * cs.stride : 2);
         push([=] {
-          ck(sn::conv_wgrad(cs, x, dy, dw, db, part, sp, red, st), "conv_wgrad");
+          ck(cudaEventRecord(ready, st), "record");
+          ck(cudaStreamWaitEvent(s3, ready, 0), "wait");
+          ck(sn::conv_wgrad(cs, x, dy, dw, db, part_w, sp, red_w, s3), "conv_wgrad");
+          ck(cudaEventRecord(wdone, s3), "record");
           if (dx) ck(sn::conv_dgrad(cs, dy, w, wt, dx, acc, st), "conv_dgrad");
         }, 2 + nbias + ndgrad);
+        (void)part;
+        (void)red;
         break;
       }
       case snp::FC: {
@@ -1137,6 +1173,14 @@ struct Compiler {
         ck(cudaStreamWaitEvent(s0, j, 0), "wait");
       }, 0);
     }
+    if (used_s3) {
+      cudaEvent_t j = ex->new_event();
+      cudaStream_t s3 = ex->s3;
+      push([=] {
+        ck(cudaEventRecord(j, s3), "record");
+        ck(cudaStreamWaitEvent(s0, j, 0), "wait");
+      }, 0);
+    }
     uint32_t* it = ex->iteration;
     push([=] { ck(sn::bump_iteration(it, s0), "bump"); }, 1);
     ex->final_keys = where;
@@ -1191,6 +1235,7 @@ void destroy(sn_exec* ex) {
   if (ex->data_buf && ex->data_buf != ex->images) cudaFree(ex->data_buf);
   void* bufs[] = {ex->arena, ex->params, ex->grads, ex->state, ex->images, ex->labels, ex->loss_rows, ex->loss,
                   ex->iteration, ex->wt_scratch, ex->partial, ex->red, ex->tstats, ex->pool_scratch,
+                  ex->partial_w, ex->red_w, ex->wt_w,
                   const_cast<float**>(ex->ptr_table)};
   for (void* b : bufs)
     if (b) cudaFree(b);
@@ -1199,6 +1244,7 @@ void destroy(sn_exec* ex) {
   if (ex->s0) cudaStreamDestroy(ex->s0);
   if (ex->s1) cudaStreamDestroy(ex->s1);
   if (ex->s2) cudaStreamDestroy(ex->s2);
+  if (ex->s3) cudaStreamDestroy(ex->s3);
   delete ex;
 }
 
@@ -1226,6 +1272,7 @@ int sn_exec_create(const sn_plan* plan, const sn_net_desc* /*net*/, const sn_lay
     ck(cudaStreamCreateWithFlags(&ex->s0, cudaStreamNonBlocking), "stream");
     ck(cudaStreamCreateWithFlags(&ex->s1, cudaStreamNonBlocking), "stream");
     ck(cudaStreamCreateWithFlags(&ex->s2, cudaStreamNonBlocking), "stream");
+    ck(cudaStreamCreateWithFlags(&ex->s3, cudaStreamNonBlocking), "stream");
     ck(cudaEventCreate(&ex->t_begin), "event");
     ck(cudaEventCreate(&ex->t_end), "event");
     setup_layers(ex, numerics);
