@@ -250,6 +250,15 @@ int sn_exec_step(sn_exec* ex, int32_t update, float* loss_host, sn_step_timing* 
 /* End-to-end: copy host images/labels in, run the step, read the loss back. */
 int sn_exec_step_host(sn_exec* ex, const float* images_host, const int32_t* labels_host,
                       int32_t update, float* loss_host, sn_step_timing* timing);
+/* End-to-end with a one-batch input pipeline (the data layer's prefetch):
+ * runs the step on images_host/labels_host and, while it computes, copies
+ * next_images_host/next_labels_host (may be NULL) into a device staging
+ * buffer.  A call whose images_host is the batch staged by the previous call
+ * only waits for what is left of that copy; otherwise it stages it first.  The
+ * next_* host buffers must stay unchanged until the following call returns. */
+int sn_exec_step_host_pipelined(sn_exec* ex, const float* images_host, const int32_t* labels_host,
+                                const float* next_images_host, const int32_t* next_labels_host, int32_t update,
+                                float* loss_host, sn_step_timing* timing);
 /* Copy a layer's current forward output (if resident in the arena) or its
  * gradient buffer to device memory `dst`; used by parity tests. */
 int sn_exec_read_tensor(sn_exec* ex, int32_t kind, int32_t layer, float* dst, int64_t n_floats);

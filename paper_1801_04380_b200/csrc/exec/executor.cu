@@ -125,6 +125,13 @@ struct sn_exec {
   float* wt_w = nullptr;
   std::vector<cudaEvent_t> events;
   cudaEvent_t t_begin = nullptr, t_end = nullptr;
+  // pipelined host input (sn_exec_step_host_pipelined): the next batch is
+  // copied into a staging buffer on s4 while the current step computes
+  cudaStream_t s4 = nullptr;
+  float* images_stage = nullptr;
+  int32_t* labels_stage = nullptr;
+  cudaEvent_t staged_ev = nullptr, consumed_ev = nullptr;
+  const void* staged_src = nullptr;
   // compiled program
   std::vector<Action> prog;
   int64_t kernels_per_step = 0;
@@ -1230,12 +1237,15 @@ void destroy(sn_exec* ex) {
   for (cudaEvent_t e : ex->events) cudaEventDestroy(e);
   if (ex->t_begin) cudaEventDestroy(ex->t_begin);
   if (ex->t_end) cudaEventDestroy(ex->t_end);
+  if (ex->staged_ev) cudaEventDestroy(ex->staged_ev);
+  if (ex->consumed_ev) cudaEventDestroy(ex->consumed_ev);
+  if (ex->s4) cudaStreamDestroy(ex->s4);
   for (auto& kv : ex->stash)
     if (kv.second) cudaFreeHost(kv.second);
   if (ex->data_buf && ex->data_buf != ex->images) cudaFree(ex->data_buf);
   void* bufs[] = {ex->arena, ex->params, ex->grads, ex->state, ex->images, ex->labels, ex->loss_rows, ex->loss,
                   ex->iteration, ex->wt_scratch, ex->partial, ex->red, ex->tstats, ex->pool_scratch,
-                  ex->partial_w, ex->red_w, ex->wt_w,
+                  ex->partial_w, ex->red_w, ex->wt_w, ex->images_stage, ex->labels_stage,
                   const_cast<float**>(ex->ptr_table)};
   for (void* b : bufs)
     if (b) cudaFree(b);
@@ -1362,6 +1372,60 @@ int sn_exec_step_host(sn_exec* ex, const float* images_host, const int32_t* labe
        "images H2D");
     ck(cudaMemcpyAsync(ex->labels, labels_host, ex->B * sizeof(int32_t), cudaMemcpyHostToDevice, ex->s0),
        "labels H2D");
+    if (ex->opt.use_graph)
+      ck(cudaGraphLaunch(ex->gexec, ex->s0), "GraphLaunch");
+    else
+      run_program(ex);
+    if (update) ck(sn::sgd_update(ex->params, ex->grads, ex->n_params, ex->opt.lr, ex->opt.grad_scale, ex->s0), "sgd");
+    ck(cudaMemcpyAsync(loss_host, ex->loss, sizeof(float), cudaMemcpyDeviceToHost, ex->s0), "loss D2H");
+    ck(cudaEventRecord(ex->t_end, ex->s0), "record");
+    ck(cudaStreamSynchronize(ex->s0), "sync");
+    if (timing) {
+      float ms = 0.f;
+      ck(cudaEventElapsedTime(&ms, ex->t_begin, ex->t_end), "elapsed");
+      timing->step_ms = ms;
+      timing->kernels = ex->kernels_per_step + (update ? 1 : 0);
+      timing->d2h_bytes = ex->d2h_bytes;
+      timing->h2d_bytes = ex->h2d_bytes;
+      timing->arena_high_water = ex->plan->plan.report.pool_high_water_bytes;
+    }
+  });
+  return rc;
+}
+
+int sn_exec_step_host_pipelined(sn_exec* ex, const float* images_host, const int32_t* labels_host,
+                                const float* next_images_host, const int32_t* next_labels_host, int32_t update,
+                                float* loss_host, sn_step_timing* timing) {
+  if (!ex || !images_host || !labels_host) return xset(SN_EK_INTERNAL, "null argument");
+  const int rc = xguard([&] {
+    ck(cudaSetDevice(ex->device), "cudaSetDevice");
+    if (ex->opt.use_graph) ensure_graph(ex);
+    const size_t ibytes = ex->image_floats * sizeof(float), lbytes = ex->B * sizeof(int32_t);
+    if (!ex->s4) {
+      ck(cudaStreamCreateWithFlags(&ex->s4, cudaStreamNonBlocking), "stream");
+      ck(cudaMalloc(&ex->images_stage, ibytes), "cudaMalloc(images_stage)");
+      ck(cudaMalloc(&ex->labels_stage, lbytes), "cudaMalloc(labels_stage)");
+      ck(cudaEventCreateWithFlags(&ex->staged_ev, cudaEventDisableTiming), "event");
+      ck(cudaEventCreateWithFlags(&ex->consumed_ev, cudaEventDisableTiming), "event");
+      ck(cudaEventRecord(ex->consumed_ev, ex->s0), "record");
+    }
+    auto stage = [&](const float* img, const int32_t* lab) {
+      ck(cudaStreamWaitEvent(ex->s4, ex->consumed_ev, 0), "wait");
+      ck(cudaMemcpyAsync(ex->images_stage, img, ibytes, cudaMemcpyHostToDevice, ex->s4), "images H2D");
+      ck(cudaMemcpyAsync(ex->labels_stage, lab, lbytes, cudaMemcpyHostToDevice, ex->s4), "labels H2D");
+      ck(cudaEventRecord(ex->staged_ev, ex->s4), "record");
+      ex->staged_src = img;
+    };
+    ck(cudaEventRecord(ex->t_begin, ex->s0), "record");
+    if (ex->staged_src != images_host) stage(images_host, labels_host);  // first call of a run
+    ck(cudaStreamWaitEvent(ex->s0, ex->staged_ev, 0), "wait");
+    ck(cudaMemcpyAsync(ex->images, ex->images_stage, ibytes, cudaMemcpyDeviceToDevice, ex->s0), "images D2D");
+    ck(cudaMemcpyAsync(ex->labels, ex->labels_stage, lbytes, cudaMemcpyDeviceToDevice, ex->s0), "labels D2D");
+    ck(cudaEventRecord(ex->consumed_ev, ex->s0), "record");
+    ex->staged_src = nullptr;
+    // stage the next batch now: the loss read below is a pageable copy that
+    // blocks the host until the step is done
+    if (next_images_host && next_labels_host) stage(next_images_host, next_labels_host);
     if (ex->opt.use_graph)
       ck(cudaGraphLaunch(ex->gexec, ex->s0), "GraphLaunch");
     else

@@ -146,6 +146,8 @@ def _xlib():
         L.sn_exec_inputs.argtypes = [C.c_void_p, P(C.c_void_p), P(C.c_void_p), P(C.c_int64)]
         L.sn_exec_step.argtypes = [C.c_void_p, C.c_int32, P(C.c_float), P(TimingC)]
         L.sn_exec_step_host.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, P(C.c_float), P(TimingC)]
+        L.sn_exec_step_host_pipelined.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                                  C.c_int32, P(C.c_float), P(TimingC)]
         L.sn_exec_read_tensor.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int64]
         L.sn_exec_apply_update.argtypes = [C.c_void_p, C.c_float, C.c_float]
         L.sn_exec_profile.argtypes = [C.c_void_p, P(C.c_float), P(C.c_int32), P(C.c_int32), C.c_size_t,
@@ -274,6 +276,32 @@ class Executor:
                                     C.byref(loss), C.byref(t)) != 0:
             _raise_exec(self.L)
         return loss.value, t
+
+    def step_host_pipelined(self, images_host, labels_host, next_images_host=None, next_labels_host=None,
+                            update: bool = True) -> tuple[float, TimingC]:
+        """One end-to-end step on pinned host buffers that also stages the next
+        batch's host->device copy behind this step's compute."""
+        loss = C.c_float()
+        t = TimingC()
+        rc = self.L.sn_exec_step_host_pipelined(
+            self.ptr, images_host.data_ptr(), labels_host.data_ptr(),
+            None if next_images_host is None else next_images_host.data_ptr(),
+            None if next_labels_host is None else next_labels_host.data_ptr(), int(update),
+            C.byref(loss), C.byref(t))
+        if rc != 0:
+            _raise_exec(self.L)
+        return loss.value, t
+
+    def train_host(self, batches, update: bool = True) -> list[tuple[float, TimingC]]:
+        """End to end over a sequence of pinned host (images NHWC, labels int32)
+        batches: batch i+1 is copied to the device while step i computes (the
+        data layer's one-batch prefetch); returns [(loss, timing)] per step."""
+        batches = list(batches)
+        out = []
+        for i, (img, lab) in enumerate(batches):
+            nxt = batches[i + 1] if i + 1 < len(batches) else (None, None)
+            out.append(self.step_host_pipelined(img, lab, nxt[0], nxt[1], update))
+        return out
 
     def read_activation(self, lid: int):
         """Layer output still resident at the end of the iteration, as (B, C, H, W)

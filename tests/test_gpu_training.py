@@ -330,3 +330,28 @@ def test_branchy_nets_match_oracle_and_are_schedule_invariant(cuda, kind):
     ref, sens = _sensitivity(net, params, images, labels)
     worst = max(relative_error(grads[l][k], ref[l][k]) for l in ref for k in ("w", "b"))
     assert worst <= 3 * sens + 5e-3, (worst, sens)
+
+
+def test_pipelined_host_steps_match_serial_host_steps(cuda, alex32_case):
+    """The prefetching end-to-end call (sn_exec_step_host_pipelined) trains
+    exactly like one synchronous sn_exec_step_host per batch."""
+    sn = _sn()
+    from paper_1801_04380_b200.training import Executor
+    net, params, _, _ = alex32_case
+    batches = []
+    for s in range(4):
+        img, lab = _inputs(net, 16, seed=10 + 2 * s)
+        batches.append((img.permute(0, 2, 3, 1).contiguous().pin_memory(), lab.to(torch.int32).pin_memory()))
+    batches = batches + batches[:2]  # revisit buffers, like a loader's ring
+    cfg = sn.SimConfig(pool_bytes=1 << 30, features=sn.parse_features(ALL), cost=sn.CostConfig(batch=16))
+    runs = []
+    for pipelined in (False, True):
+        ex = Executor(net, cfg, params=params, lr=0.005)
+        if pipelined:
+            losses = [l for l, _ in ex.train_host(batches)]
+        else:
+            losses = [ex.step_host(img, lab)[0] for img, lab in batches]
+        runs.append((losses, ex.get("params")))
+        ex.close()
+    assert runs[0][0] == runs[1][0]
+    assert _bitwise(runs[0][1], runs[1][1])
