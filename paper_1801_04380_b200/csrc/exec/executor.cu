@@ -1004,7 +1004,8 @@ struct Compiler {
         if (f.op == 'B') {
           if (f.b == ra) read |= !act_bwd_skip[j];
           const int k = net.kind[f.b];
-          if (k == snp::CONV || k == snp::BN || k == snp::POOL || k == snp::LRN || k == snp::FC)
+          const bool pool_am = k == snp::POOL && ex->L[f.b].argmax && sn::pool_bwd_argmax_only(ex->L[f.b].pool);
+          if (k == snp::CONV || k == snp::BN || (k == snp::POOL && !pool_am) || k == snp::LRN || k == snp::FC)
             for (int p : net.prev[f.b]) read |= p == ra;
         }
       }
@@ -1037,7 +1038,9 @@ struct Compiler {
         const bool x = !net.prev[M].empty() && net.prev[M][0] == L;
         switch (k) {
           case snp::CONV: case snp::FC: case snp::BN: return x;
-          case snp::POOL: return ex->L[M].pool.mode == 0 && (x || M == L);
+          case snp::POOL:
+            if (ex->L[M].argmax && sn::pool_bwd_argmax_only(ex->L[M].pool)) return false;
+            return ex->L[M].pool.mode == 0 && (x || M == L);
           case snp::LRN: return x || M == L;
           case snp::SOFTMAX: return M == L;
           case snp::ACT: return M == L && !act_bwd_skip[j];

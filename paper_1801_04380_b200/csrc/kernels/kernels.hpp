@@ -162,6 +162,8 @@ cudaError_t pool_fwd(const PoolShape& s, const float* x, float* y, cudaStream_t 
 // pool_scratch_bytes), then gathers; avg-pool gathers directly.
 int64_t pool_scratch_bytes(const PoolShape& s);
 int pool_bwd_kernels(const PoolShape& s);  // launches one pool_bwd issues
+// pool_bwd with a saved argmax reads neither x nor y (the gather kernel path)
+bool pool_bwd_argmax_only(const PoolShape& s);
 cudaError_t pool_bwd(const PoolShape& s, const float* x, const float* y, const float* dy, float* dx,
                      int accumulate, void* scratch, cudaStream_t st, const uint8_t* argmax = nullptr);
 

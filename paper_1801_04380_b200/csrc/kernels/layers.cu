@@ -1563,10 +1563,13 @@ bool pool_saves_argmax(const PoolShape& s) {
          static_cast<int64_t>(s.N) * s.H * s.W * s.C < (1ll << 31) && pool_fused_ok(s, &PB, &WR, &smem);
 }
 
+bool pool_bwd_argmax_only(const PoolShape& s) {
+  return pool_saves_argmax(s) && s.pad == 1 && s.H == 2 * s.P && s.W == 2 * s.Q;
+}
+
 cudaError_t pool_bwd(const PoolShape& s, const float* x, const float* y, const float* dy, float* dx, int accumulate,
                      void* scratch, cudaStream_t st, const uint8_t* argmax) {
-  if (argmax && s.mode == 0 && s.K == 3 && s.stride == 2 && s.pad == 1 && s.H == 2 * s.P && s.W == 2 * s.Q &&
-      s.C % 4 == 0) {
+  if (argmax && pool_bwd_argmax_only(s)) {
     const int64_t total = static_cast<int64_t>(s.N) * s.P * s.Q * (s.C / 4);
     pool_max_bwd_k3s2<<<blocks_for(total, kThreads, 148 * 32), kThreads, 0, st>>>(
         s, reinterpret_cast<const uchar4*>(argmax), reinterpret_cast<const float4*>(dy), reinterpret_cast<float4*>(dx),

@@ -22,6 +22,7 @@ def main() -> None:
     ap.add_argument("--features", default="liveness,offload,cache,recompute=cost-aware,convselect")
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--graph", action="store_true")
+    ap.add_argument("--order", action="store_true", help="print every action in tape order")
     args = ap.parse_args()
     import torch
     import paper_1801_04380_b200 as sn
@@ -36,6 +37,12 @@ def main() -> None:
         loss, t = ex.step()
         print(f"loss {loss:.4f} step {t.step_ms:.2f} ms kernels {t.kernels}", flush=True)
     prof = ex.profile()
+    if args.order:
+        tot = 0.0
+        for i, (ms, lid, typ) in enumerate(prof):
+            tot += ms
+            name = net.layers[lid].name if lid >= 0 else "-"
+            print(f"{i:4d} {name:>14} {['fwd', 'replay', 'bwd', 'copy'][typ]:>6} {ms:8.3f} {tot:8.3f}")
     agg: dict = {}
     for ms, lid, typ in prof:
         if lid >= 0:
