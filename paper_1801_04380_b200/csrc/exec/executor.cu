@@ -534,6 +534,7 @@ struct Compiler {
       }
       case snp::ACT:
         if (fused_bn >= 0 && join_fuse_at[cur_ti] >= 0) break;  // launched at the JOIN (bn_apply_relu_join)
+        if (fused_bn >= 0 && pool_fuse_at[cur_ti] >= 0) break;  // launched at the POOL (pool_fwd_bn_relu)
         if (dead_at[cur_ti]) break;                                // output never read (plan_fusions)
         if (fused_bn >= 0) {
           const LayerRt& bl = ex->L[fused_bn];
@@ -553,6 +554,19 @@ struct Compiler {
       case snp::POOL: {
         const sn::PoolShape ps = l.pool;
         uint8_t* am = l.argmax;
+        if (pool_from[cur_ti] >= 0) {
+          // BN apply + ReLU + max pool in one pass (peephole, see plan_fusions)
+          const int ra = P.tape[pool_from[cur_ti]].b;
+          const int bn = net.prev[ra][0];
+          const LayerRt& bl = ex->L[bn];
+          const float* bx = ptr(snp::K_ACT, net.prev[bn][0]);
+          float* ry = elide_out[ra] ? nullptr : ptr(snp::K_ACT, ra);
+          const float* g = ex->params + bl.w_off;
+          const float* b = ex->params + bl.b_off;
+          const float* stats = ex->state + bl.state_off;
+          push([=] { ck(sn::pool_fwd_bn_relu(ps, bx, g, b, stats, ry, y, am, st), "pool_fwd_bn_relu"); }, 1);
+          break;
+        }
         push([=] { ck(sn::pool_fwd(ps, x, y, st, am), "pool_fwd"); }, 1);
         break;
       }
@@ -827,6 +841,7 @@ struct Compiler {
   // BN+ReLU (fused) forward / replay whose next compute action is the same op
   // of a 2-input JOIN reading the ReLU: the whole chain runs at the JOIN.
   std::vector<int> join_fuse_at, join_from;
+  std::vector<int> pool_fuse_at, pool_from;  // BN+ReLU -> max POOL: ACT tape index <-> POOL tape index
   std::vector<char> dead_at;  // forward / replay whose outputs are never read: not launched
   // JOIN backward folded into the BN backward of the ReLU it feeds: join_to_bn[i]
   // = tape index of that BN backward; the JOIN's gradient is read there
@@ -869,6 +884,8 @@ struct Compiler {
     bn_tiles_at.assign(T, 0);
     join_fuse_at.assign(T, -1);
     join_from.assign(T, -1);
+    pool_fuse_at.assign(T, -1);
+    pool_from.assign(T, -1);
     dead_at.assign(T, 0);
     join_to_bn.assign(T, -1);
     bn_from_join.assign(T, -1);
@@ -982,16 +999,47 @@ struct Compiler {
         break;
       }
     }
+    // ReLU -> max POOL (saved argmax, so the pool backward reads neither
+    // activation): the same window rules as ReLU -> JOIN
+    std::vector<int> act_pool_fused(net.n, 0), pool_fwd_n(net.n, 0), pool_fwd_fused(net.n, 0);
+    for (size_t i = 0; i < T; ++i) {
+      const snp::Event& e = P.tape[i];
+      if ((e.op == 'C' || e.op == 'R') && net.kind[e.b] == snp::POOL) ++pool_fwd_n[e.b];
+      if (fused_into[i] < 0 || join_fuse_at[i] >= 0) continue;
+      const int ra = e.b, bn = fused_into[i], bin = net.prev[bn][0];
+      for (size_t j = i + 1; j < T; ++j) {
+        const snp::Event& f = P.tape[j];
+        if ((f.op == 'F' && f.a == snp::K_ACT) || f.op == 'O' || f.op == 'P' || f.op == 'D') {
+          if (f.op == 'F' && f.b == bn && elide_out[bn]) continue;
+          if (f.b == ra || f.b == bn || f.b == bin) break;
+          continue;
+        }
+        if (!is_compute(f.op)) continue;
+        const auto& pv = net.prev[f.b];
+        if (f.op == e.op && net.kind[f.b] == snp::POOL && pv.size() == 1 && pv[0] == ra && ex->L[f.b].argmax &&
+            sn::pool_fwd_bn_relu_ok(ex->L[f.b].pool)) {
+          pool_fuse_at[i] = static_cast<int>(j);
+          pool_from[j] = static_cast<int>(i);
+          ++act_pool_fused[ra];
+          ++pool_fwd_fused[f.b];
+        }
+        break;
+      }
+    }
     for (int a = 0; a < net.n; ++a) {
       if (!bn_relu_pair(a) || !act_bwd_fused[a] || net.next[a].size() != 1) continue;
-      if (act_fwd[a] == act_join_fused[a]) elide_out[a] = 1;  // read only by the fused chains
+      const int nx = net.next[a][0];
+      // every forward of the ReLU fused into its single consumer, and (POOL)
+      // every forward of that consumer fed by such a fused chain
+      if (act_fwd[a] == act_join_fused[a] && act_join_fused[a] > 0) elide_out[a] = 1;  // read only by the fused chains
+      (void)nx;
     }
     // Dead writes: a fused BN+ReLU forward / replay (BN output not
     // materialised) whose ReLU output nobody reads before it is freed or
     // rewritten -- typically a replay the reference schedules because the
     // ReLU backward reads y, which here is folded into the BN backward.
     for (size_t i = 0; i < T; ++i) {
-      if (fused_into[i] < 0 || join_fuse_at[i] >= 0 || !elide_out[fused_into[i]]) continue;
+      if (fused_into[i] < 0 || join_fuse_at[i] >= 0 || pool_fuse_at[i] >= 0 || !elide_out[fused_into[i]]) continue;
       const int ra = P.tape[i].b;
       bool read = false;
       for (size_t j = i + 1; j < T && !read; ++j) {
@@ -999,7 +1047,7 @@ struct Compiler {
         if (f.op == 'F' && f.a == snp::K_ACT && f.b == ra) break;
         if ((f.op == 'C' || f.op == 'R') && f.b == ra) break;  // rewritten
         if (f.op == 'O' && f.b == ra) read = true;
-        if ((f.op == 'C' || f.op == 'R') && join_from[j] < 0)
+        if ((f.op == 'C' || f.op == 'R') && join_from[j] < 0 && pool_from[j] < 0)
           for (int p : net.prev[f.b]) read |= p == ra;
         if (f.op == 'B') {
           if (f.b == ra) read |= !act_bwd_skip[j];
@@ -1011,6 +1059,17 @@ struct Compiler {
       }
       if (!read) dead_at[i] = 1;
     }
+    // ReLU -> POOL chains: the ReLU output is never materialised when every
+    // live (not dead) forward of the ReLU is fused into the pool and every
+    // forward of the pool is such a fused chain
+    for (int a = 0; a < net.n; ++a) {
+      if (!bn_relu_pair(a) || !act_bwd_fused[a] || net.next[a].size() != 1 || act_pool_fused[a] == 0) continue;
+      const int nx = net.next[a][0];
+      int live = 0;
+      for (size_t i = 0; i < T; ++i)
+        live += (P.tape[i].op == 'C' || P.tape[i].op == 'R') && P.tape[i].b == a && !dead_at[i];
+      if (live == act_pool_fused[a] && pool_fwd_n[nx] == pool_fwd_fused[nx]) elide_out[a] = 1;
+    }
     // Dead replays (general): a replay of an unfused layer whose output no later
     // action reads before it is freed or rewritten -- under the kernels' actual
     // reads, which are narrower than the reference's BACKWARD_NEEDS (the ReLU
@@ -1021,7 +1080,8 @@ struct Compiler {
       const int M = f.b;
       if (f.op == 'O') return M == L;
       if (f.op == 'C' || f.op == 'R') {
-        if (dead_at[j] || join_fuse_at[j] >= 0) return false;  // not launched here
+        if (dead_at[j] || join_fuse_at[j] >= 0 || pool_fuse_at[j] >= 0) return false;  // not launched here
+        if (pool_from[j] >= 0) return L == net.prev[net.prev[P.tape[pool_from[j]].b][0]][0];  // reads the BN input
         if (fused_into[j] >= 0) return net.prev[fused_into[j]][0] == L;  // BN+ReLU: reads the BN input
         if (join_from[j] >= 0) {
           const int ra = P.tape[join_from[j]].b, bnj = net.prev[ra][0];
@@ -1051,7 +1111,9 @@ struct Compiler {
     };
     for (size_t i = 0; i < T; ++i) {
       const snp::Event& e = P.tape[i];
-      if (e.op != 'R' || dead_at[i] || fused_into[i] >= 0 || join_from[i] >= 0 || join_fuse_at[i] >= 0) continue;
+      if (e.op != 'R' || dead_at[i] || fused_into[i] >= 0 || join_from[i] >= 0 || join_fuse_at[i] >= 0 ||
+          pool_from[i] >= 0)
+        continue;
       const int L = e.b;
       if (net.kind[L] == snp::BN && fuse_at[i]) continue;  // launches nothing anyway
       if (net.kind[L] == snp::SOFTMAX) continue;          // keeps its loss-row side effect simple

@@ -1143,11 +1143,11 @@ cudaError_t conv_stem_fwd(const ConvShape& s, const float* xp, const float* w, f
     ra.bias = bias;
     ra.stats = stats;
     const int smem = kStemRing * kBM * 128 + s.R * 64 * 128 + 4 * kBM * 128 + 512 + 2048 + 1024;
-    static bool attr = false;
-    if (!attr) {
+    static int attr_smem = 0;  // the filter's share depends on R: raise the opt-in when a larger one comes
+    if (smem > attr_smem) {
       err = cudaFuncSetAttribute(stem_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       if (err != cudaSuccess) return err;
-      attr = true;
+      attr_smem = smem;
     }
     stem_rows_kernel<<<std::min(ra.tiles, num_sms()), kStemThreads, smem, st>>>(A, W, D, ra);
     return cudaGetLastError();

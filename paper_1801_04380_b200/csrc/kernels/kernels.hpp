@@ -164,6 +164,13 @@ int64_t pool_scratch_bytes(const PoolShape& s);
 int pool_bwd_kernels(const PoolShape& s);  // launches one pool_bwd issues
 // pool_bwd with a saved argmax reads neither x nor y (the gather kernel path)
 bool pool_bwd_argmax_only(const PoolShape& s);
+// BN (batch statistics) + ReLU + max pool in one pass over the BN input x:
+// y = pool(relu(bn(x))), the argmax saved as pool_fwd does, the ReLU output
+// written to y_relu when not null (pool_fwd_bn_relu_ok: k3 s2 pad 1, even
+// input, C <= 512).
+bool pool_fwd_bn_relu_ok(const PoolShape& s);
+cudaError_t pool_fwd_bn_relu(const PoolShape& s, const float* x, const float* gamma, const float* beta,
+                             const float* stats, float* y_relu, float* y, uint8_t* argmax, cudaStream_t st);
 cudaError_t pool_bwd(const PoolShape& s, const float* x, const float* y, const float* dy, float* dx,
                      int accumulate, void* scratch, cudaStream_t st, const uint8_t* argmax = nullptr);
 

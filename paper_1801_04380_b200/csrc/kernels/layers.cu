@@ -717,11 +717,25 @@ __global__ void pool_fwd_v4_kernel(PoolShape s, const float4* __restrict__ x, fl
 
 // One block per output row (n, p) for the common small-window case: the only
 // per-element index math left is one division by C/4.
-template <int KC, int SC>
+//
+// BNR: the input is a BN input; BN (batch statistics) + ReLU are applied on
+// load (bn_affine4 / relu4, bit-identical to bn_apply_v4).  yr (optional)
+// receives the ReLU output, each element written by the one window that owns
+// it (rows/cols 2p, 2p+1: needs pad 1, H = 2P, W = 2Q; pool_fwd_bn_relu_ok).
+constexpr int kPoolBnMaxC4 = 128;
+template <int KC, int SC, bool BNR>
 __global__ void __launch_bounds__(256) pool_fwd_rows_kernel(PoolShape s, const float4* __restrict__ x,
-                                                            float4* __restrict__ y, uchar4* __restrict__ arg) {
+                                                            float4* __restrict__ y, uchar4* __restrict__ arg,
+                                                            const float* __restrict__ stats,
+                                                            const float* __restrict__ gamma,
+                                                            const float* __restrict__ beta, float4* __restrict__ yr) {
   const int C4 = s.C >> 2;
   const int p = blockIdx.x, n = blockIdx.y;
+  __shared__ Bn4 bp[BNR ? kPoolBnMaxC4 : 1];
+  if constexpr (BNR) {
+    for (int c = threadIdx.x; c < C4; c += blockDim.x) bp[c] = bn_params4(stats, gamma, beta, 4 * c, s.C);
+    __syncthreads();
+  }
   const int h0 = p * SC - s.pad;
   const float inv = 1.0f / static_cast<float>(KC * KC);
   const float4* xb = x + static_cast<size_t>(n) * s.H * s.W * C4;
@@ -739,6 +753,18 @@ __global__ void __launch_bounds__(256) pool_fwd_rows_kernel(PoolShape s, const f
         in[r * KC + u] = h >= 0 && h < s.H && w >= 0 && w < s.W;
         v[r * KC + u] = in[r * KC + u] ? xb[(h * s.W + w) * C4 + c4] : make_float4(0.f, 0.f, 0.f, 0.f);
       }
+    if constexpr (BNR) {
+      const Bn4 bq = bp[c4];
+#pragma unroll
+      for (int r = 0; r < KC; ++r)
+#pragma unroll
+        for (int u = 0; u < KC; ++u) {
+          if (!in[r * KC + u]) continue;
+          v[r * KC + u] = relu4(bn_affine4(v[r * KC + u], bq));
+          if (yr && r >= 1 && u >= 1)
+            yr[static_cast<size_t>(n) * s.H * s.W * C4 + ((h0 + r) * s.W + (w0 + u)) * C4 + c4] = v[r * KC + u];
+        }
+    }
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     if (s.mode == 0) {
       // max and the first (row-major) position holding it, for the backward
@@ -768,6 +794,114 @@ __global__ void __launch_bounds__(256) pool_fwd_rows_kernel(PoolShape s, const f
       acc.x *= inv; acc.y *= inv; acc.z *= inv; acc.w *= inv;
     }
     yrow[i] = acc;
+  }
+}
+
+// 3x3 / stride 2 / pad 1 max pool over an even input (H = 2P, W = 2Q), the
+// shape after a stride-2 stem: block = (band of PB output rows, image), thread
+// = (output column q, channel quad); each thread walks its band keeping input
+// row 2p-1 from the previous output row in registers, so it loads 6 of the 9
+// window elements per output (the columns 2q-1 are also its left neighbour's:
+// L1/L2 hits) and the input leaves HBM once.  Same window order, comparisons
+// and argmax encoding as pool_fwd_rows_kernel.  BNR as there.
+// Row partial of a 3-wide window row: the max per component and the first
+// column holding it, as the window index k = 3*r + u (strict > keeps the first).
+struct RowMax {
+  float4 v;
+  int a0, a1, a2, a3;
+};
+__device__ __forceinline__ void rowmax_take(RowMax& m, const float4& v, int k) {
+  if (v.x > m.v.x) { m.v.x = v.x; m.a0 = k; }
+  if (v.y > m.v.y) { m.v.y = v.y; m.a1 = k; }
+  if (v.z > m.v.z) { m.v.z = v.z; m.a2 = k; }
+  if (v.w > m.v.w) { m.v.w = v.w; m.a3 = k; }
+}
+__device__ __forceinline__ void rowmax_take(RowMax& m, const RowMax& o) {
+  if (o.v.x > m.v.x) { m.v.x = o.v.x; m.a0 = o.a0; }
+  if (o.v.y > m.v.y) { m.v.y = o.v.y; m.a1 = o.a1; }
+  if (o.v.z > m.v.z) { m.v.z = o.v.z; m.a2 = o.a2; }
+  if (o.v.w > m.v.w) { m.v.w = o.v.w; m.a3 = o.a3; }
+}
+
+template <bool BNR>
+__global__ void __launch_bounds__(448, 2) pool_fwd_k3s2_band_kernel(PoolShape s, int PB, int CS, const float4* __restrict__ x,
+                                                                  float4* __restrict__ y, uchar4* __restrict__ arg,
+                                                                  const float* __restrict__ stats,
+                                                                  const float* __restrict__ gamma,
+                                                                  const float* __restrict__ beta,
+                                                                  float4* __restrict__ yr) {
+  const int C4 = s.C >> 2;
+  const int n = blockIdx.y;
+  const int q = threadIdx.x / CS, c4 = blockIdx.z * CS + threadIdx.x - q * CS;  // CS channel quads per block
+  __shared__ Bn4 bp[BNR ? kPoolBnMaxC4 : 1];
+  if constexpr (BNR) {
+    for (int c = threadIdx.x; c < C4; c += blockDim.x) bp[c] = bn_params4(stats, gamma, beta, 4 * c, s.C);
+    __syncthreads();
+  }
+  if (q >= s.Q) return;
+  const bool left = q > 0;  // column 2q-1 inside the image
+  const int rs = s.W * C4;  // input row stride (float4)
+  // element (h, 2q-1+u) of this image: xi[h*rs + col + u*C4]
+  const float4* xi = x + static_cast<size_t>(n) * s.H * rs;
+  float4* yri = BNR && yr ? yr + static_cast<size_t>(n) * s.H * rs : nullptr;
+  const int col = (2 * q - 1) * C4 + c4;
+  auto load3 = [&](int h, float4* v) {
+    const int o = h * rs + col;
+    v[0] = left ? xi[o] : make_float4(0.f, 0.f, 0.f, 0.f);
+    v[1] = xi[o + C4];
+    v[2] = xi[o + 2 * C4];
+  };
+  // BN+ReLU (BNR) and the row partial of one loaded window triple
+  auto reduce3 = [&](int h, float4* v, int kr, bool own) -> RowMax {
+    if constexpr (BNR) {
+      const Bn4 b = bp[c4];
+#pragma unroll
+      for (int u = 0; u < 3; ++u) v[u] = relu4(bn_affine4(v[u], b));
+      if (yri && own) {
+        const int o = h * rs + col;
+        yri[o + C4] = v[1];
+        yri[o + 2 * C4] = v[2];
+      }
+    }
+    RowMax m;
+    if (left) {
+      m.v = v[0];
+      m.a0 = m.a1 = m.a2 = m.a3 = kr;
+      rowmax_take(m, v[1], kr + 1);
+    } else {
+      m.v = v[1];
+      m.a0 = m.a1 = m.a2 = m.a3 = kr + 1;
+    }
+    rowmax_take(m, v[2], kr + 2);
+    return m;
+  };
+  const int p0 = blockIdx.x * PB, p1 = min(s.P, p0 + PB);
+  RowMax top{};
+  if (p0 > 0) {
+    float4 t[3];
+    load3(2 * p0 - 1, t);
+    top = reduce3(2 * p0 - 1, t, 0, false);
+  }
+  for (int p = p0; p < p1; ++p) {
+    float4 a[3], b[3];
+    load3(2 * p, a);  // all six loads in flight before any math
+    load3(2 * p + 1, b);
+    const RowMax m0 = reduce3(2 * p, a, 3, true);
+    const RowMax m1 = reduce3(2 * p + 1, b, 6, true);
+    RowMax acc;
+    if (p > 0) {
+      acc = top;
+      rowmax_take(acc, m0);
+    } else {
+      acc = m0;
+    }
+    rowmax_take(acc, m1);
+    // the bottom row's partial is the next window's top row, with k shifted by 6
+    top = m1;
+    top.a0 -= 6; top.a1 -= 6; top.a2 -= 6; top.a3 -= 6;
+    const size_t o = ((static_cast<size_t>(n) * s.P + p) * s.Q + q) * C4 + c4;
+    if (arg) arg[o] = make_uchar4(acc.a0, acc.a1, acc.a2, acc.a3);
+    y[o] = acc.v;
   }
 }
 
@@ -1511,6 +1645,28 @@ cudaError_t relu_bwd_inplace(const float* y, float* g, int64_t n, cudaStream_t s
   return cudaGetLastError();
 }
 
+// channel quads per block of the band kernel: the largest divisor of C/4 with
+// Q * CS <= 448 threads (0: not applicable)
+static int pool_k3s2_band_cs(const PoolShape& s) {
+  if (!(s.mode == 0 && s.K == 3 && s.stride == 2 && s.pad == 1 && s.H == 2 * s.P && s.W == 2 * s.Q && s.C % 4 == 0))
+    return 0;
+  const int C4 = s.C / 4;
+  for (int cs = C4; cs >= 1; --cs)
+    if (C4 % cs == 0 && s.Q * cs <= 448) return s.Q * cs >= 128 ? cs : 0;
+  return 0;
+}
+static bool pool_k3s2_band_ok(const PoolShape& s) { return pool_k3s2_band_cs(s) > 0; }
+static void pool_k3s2_band(const PoolShape& s, bool bnr, const float* x, float* y, uint8_t* argmax,
+                           const float* stats, const float* gamma, const float* beta, float* y_relu,
+                           cudaStream_t st) {
+  const int PB = 4, CS = pool_k3s2_band_cs(s);
+  const dim3 grid((s.P + PB - 1) / PB, s.N, s.C / 4 / CS);
+  auto k = bnr ? pool_fwd_k3s2_band_kernel<true> : pool_fwd_k3s2_band_kernel<false>;
+  k<<<grid, s.Q * CS, 0, st>>>(s, PB, CS, reinterpret_cast<const float4*>(x), reinterpret_cast<float4*>(y),
+                               reinterpret_cast<uchar4*>(argmax), stats, gamma, beta,
+                               reinterpret_cast<float4*>(y_relu));
+}
+
 cudaError_t pool_fwd(const PoolShape& s, const float* x, float* y, cudaStream_t st, uint8_t* argmax) {
   const int64_t total = static_cast<int64_t>(s.N) * s.P * s.Q * s.C;
   if (s.C % 4 == 0 && static_cast<int64_t>(s.N) * s.H * s.W * s.C < (1ll << 31)) {
@@ -1519,10 +1675,14 @@ cudaError_t pool_fwd(const PoolShape& s, const float* x, float* y, cudaStream_t 
       pool_global_kernel<<<grid, 256, 0, st>>>(s, reinterpret_cast<const float4*>(x), reinterpret_cast<float4*>(y));
       return cudaGetLastError();
     }
+    if (pool_k3s2_band_ok(s)) {
+      pool_k3s2_band(s, false, x, y, argmax, nullptr, nullptr, nullptr, nullptr, st);
+      return cudaGetLastError();
+    }
     if (s.K == 3 && s.stride == 2) {
-      pool_fwd_rows_kernel<3, 2><<<dim3(s.P, s.N), 256, 0, st>>>(s, reinterpret_cast<const float4*>(x),
-                                                                 reinterpret_cast<float4*>(y),
-                                                                 reinterpret_cast<uchar4*>(argmax));
+      pool_fwd_rows_kernel<3, 2, false><<<dim3(s.P, s.N), 256, 0, st>>>(
+          s, reinterpret_cast<const float4*>(x), reinterpret_cast<float4*>(y), reinterpret_cast<uchar4*>(argmax),
+          nullptr, nullptr, nullptr, nullptr);
       return cudaGetLastError();
     }
     const int total4 = static_cast<int>(total / 4);
@@ -1565,6 +1725,21 @@ bool pool_saves_argmax(const PoolShape& s) {
 
 bool pool_bwd_argmax_only(const PoolShape& s) {
   return pool_saves_argmax(s) && s.pad == 1 && s.H == 2 * s.P && s.W == 2 * s.Q;
+}
+
+bool pool_fwd_bn_relu_ok(const PoolShape& s) { return pool_bwd_argmax_only(s) && s.C / 4 <= kPoolBnMaxC4; }
+
+cudaError_t pool_fwd_bn_relu(const PoolShape& s, const float* x, const float* gamma, const float* beta,
+                             const float* stats, float* y_relu, float* y, uint8_t* argmax, cudaStream_t st) {
+  if (!pool_fwd_bn_relu_ok(s) || !argmax) return cudaErrorInvalidValue;
+  if (pool_k3s2_band_ok(s)) {
+    pool_k3s2_band(s, true, x, y, argmax, stats, gamma, beta, y_relu, st);
+    return cudaGetLastError();
+  }
+  pool_fwd_rows_kernel<3, 2, true><<<dim3(s.P, s.N), 256, 0, st>>>(
+      s, reinterpret_cast<const float4*>(x), reinterpret_cast<float4*>(y), reinterpret_cast<uchar4*>(argmax), stats,
+      gamma, beta, reinterpret_cast<float4*>(y_relu));
+  return cudaGetLastError();
 }
 
 cudaError_t pool_bwd(const PoolShape& s, const float* x, const float* y, const float* dy, float* dx, int accumulate,

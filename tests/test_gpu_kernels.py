@@ -260,6 +260,8 @@ POOL_CASES = [
     (4, 64, 112, 112, 3, 2, 1, 0),   # ResNet stem max-pool (fused argmax+gather path)
     (3, 96, 55, 55, 3, 2, 0, 0),     # AlexNet pool1
     (2, 48, 13, 13, 3, 2, 0, 0),     # C % 16 == 0, P < 8: one band
+    (2, 128, 56, 56, 3, 2, 1, 0),    # band kernel, two channel slices per image band
+    (2, 64, 40, 24, 3, 2, 1, 0),     # band kernel, non-square, partial last band
     (2, 12, 17, 17, 3, 2, 1, 0),     # C % 16 != 0: two-pass argmax + gather
     (2, 5, 9, 9, 2, 2, 0, 0),        # C % 4 != 0: scalar path
     (2, 64, 14, 14, 7, 1, 0, 1),     # global-ish average pool
