@@ -269,7 +269,7 @@ void alloc_device(sn_exec* ex) {
     }
     if (l.kind == snp::BN || l.kind == snp::CONV || l.kind == snp::FC)
       red = std::max(red, sn::red_scratch_floats(l.C));
-    if (l.kind == snp::CONV) wt = std::max(wt, l.w_n);
+    if (l.kind == snp::CONV) wt = std::max(wt, std::max<int64_t>(l.w_n, sn::conv_dgrad_scratch_floats(l.conv)));
   }
   ck(cudaMemcpy(ex->state, st.data(), st.size() * sizeof(float), cudaMemcpyHostToDevice), "memcpy(state)");
   // split-K partial scratch (outside the arena, like cuDNN's internal buffers):
@@ -678,7 +678,7 @@ struct Compiler {
           }, 3 + nbias);
           break;
         }
-        const int ndgrad = !dx ? 0 : (cs.stride > 1 ? 2 * cs.stride * cs.stride : 2);
+        const int ndgrad = !dx ? 0 : sn::conv_dgrad_launches(cs);
         push([=] {
           ck(cudaEventRecord(ready, st), "record");
           ck(cudaStreamWaitEvent(s3, ready, 0), "wait");

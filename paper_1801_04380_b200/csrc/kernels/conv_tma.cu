@@ -93,6 +93,9 @@ struct EpiArgs {
   float* scatter;     // null: TMA store path
   int M, Uhw, Uw, t0, v0, st, ph, pw, pad, H, W;
   FastDivT fUhw, fUw;
+  // Sub-pixel strided dgrad (subpix = C): GEMM row m = (n, u, v) of dy's grid,
+  // column (a*2 + b)*C + c lands at dx[n][2u+a][2v+b][c].
+  int subpix;
   // BatchNorm statistics of the output (forward; the consumer is a BN):
   // per M tile and column, {shift = tile row 0, sum(y - shift), sum((y - shift)^2)}
   // over the tile's valid rows, into stats[tile][3][N] (see bn_stats_from_tiles).
@@ -399,20 +402,48 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
           const int uv = m - n * e.Uhw;
           const int u = static_cast<int>(e.fUw.div(static_cast<uint32_t>(uv)));
           const int v = uv - u * e.Uw;
-          const int h = (u + e.t0) * e.st + e.ph - e.pad;
-          const int w = (v + e.v0) * e.st + e.pw - e.pad;
-          dst = e.scatter + (static_cast<size_t>(n * e.H + h) * e.W + w) * e.N;
+          if (e.subpix) {  // the 2x2 block (2u, 2v) of dx; columns pick the phase below
+            dst = e.scatter + (static_cast<size_t>(n * e.H + 2 * u) * e.W + 2 * v) * e.subpix;
+          } else {
+            const int h = (u + e.t0) * e.st + e.ph - e.pad;
+            const int w = (v + e.v0) * e.st + e.pw - e.pad;
+            dst = e.scatter + (static_cast<size_t>(n * e.H + h) * e.W + w) * e.N;
+          }
         }
+        // Each row's 32-column chunk is 128 contiguous bytes of dx: stage the
+        // warp's 32 rows in shared memory (16-byte units XOR-swizzled by row)
+        // and write them back 4 rows x 128 B per warp instruction (coalesced),
+        // each lane taking its row's base pointer from the owning lane.
+        const uint32_t wbuf = sEpi + static_cast<uint32_t>(warp) * 4096u;
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
           float v[32];
           tmem_ld32(tbase + static_cast<uint32_t>(c), v);
-          if (dst) {
+          float* dchunk = dst ? dst + n0 + c : nullptr;
+          if (dst && e.subpix) {
+            const int col = n0 + c, ab = col / e.subpix;
+            dchunk = dst + ((ab >> 1) * e.W + (ab & 1)) * e.subpix + (col - ab * e.subpix);
+          }
 #pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-              if (n0 + c + j >= e.N) break;
-              float4* p = reinterpret_cast<float4*>(dst + n0 + c + j);
-              float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+          for (int j = 0; j < 8; ++j)
+            asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(wbuf + lane * 128u + ((j ^ (lane & 7)) << 4)),
+                         "f"(v[4 * j]), "f"(v[4 * j + 1]), "f"(v[4 * j + 2]), "f"(v[4 * j + 3])
+                         : "memory");
+          __syncwarp();
+          const unsigned long long mine = reinterpret_cast<unsigned long long>(dchunk);
+          const int q = lane & 7;
+          const bool col_ok = n0 + c + 4 * q < e.N;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int r = 4 * i + (lane >> 3);
+            float* rp = reinterpret_cast<float*>(__shfl_sync(0xffffffffu, mine, r));
+            float4 o;
+            asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                         : "=f"(o.x), "=f"(o.y), "=f"(o.z), "=f"(o.w)
+                         : "r"(wbuf + static_cast<uint32_t>(r) * 128u + ((q ^ (r & 7)) << 4))
+                         : "memory");
+            if (rp && col_ok) {
+              float4* p = reinterpret_cast<float4*>(rp + 4 * q);
               if (e.reduce) {
                 const float4 old = *p;
                 o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
@@ -420,6 +451,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
               *p = o;
             }
           }
+          __syncwarp();
         }
       } else {
 #pragma unroll 1
@@ -640,6 +672,32 @@ bool use_pairs(int64_t rows) { return pairs_mode() == 2 || (pairs_mode() == 1 &&
 
 int bn_for(int n) { return n <= 64 ? 64 : (n <= 128 ? 128 : 256); }
 
+// Single-CTA tile width by wave fill: 128-wide tiles run the tensor pipe at the
+// same rate as 256-wide ones (64 vs 128 cycles per k step, tools/mma_probe.py),
+// so when the 256-wide tile count leaves the last wave of the persistent grid
+// much emptier (ResNet stage 4: 196 tiles = 1.32 waves), halve the width.
+// Tile shape (CTA group, tile width) of the im2col kernels.  Large M: pairs of
+// 256-wide tiles (use_pairs).  Small M with >= 256 output columns (ResNet stage
+// 4, M = 12544): 256-wide tiles fill 1.32 waves; pairs of 128-wide tiles fill
+// 2.65 and share the B tile across the pair (conv_bench: 101 -> 90 us fwd).
+struct TileCfg {
+  int cg, bn;
+};
+TileCfg tile_cfg(int64_t M, int n);
+int g_bn_force = 0;  // A/B knob (conv_bench --bn): 0 = policy, else the tile width when it fits
+int bn_for_waves(int64_t M, int n) {
+  const int bn = bn_for(n);
+  if (g_bn_force > 0) return g_bn_force < bn ? g_bn_force : bn;
+  if (bn != 256) return bn;
+  const int64_t mt = (M + kBM - 1) / kBM;
+  auto fill = [](int64_t tiles) {
+    const int64_t waves = (tiles + 147) / 148;
+    return static_cast<double>(tiles) / static_cast<double>(waves * 148);
+  };
+  const double f256 = fill(mt * ((n + 255) / 256)), f128 = fill(mt * ((n + 127) / 128));
+  return f128 > f256 + 0.1 ? 128 : 256;
+}
+
 }  // namespace
 
 bool tma_encoders_ok() { return load_encoders(); }
@@ -666,7 +724,16 @@ bool tma_map_2d(CUtensorMap* m, const float* base, int64_t rows, int64_t cols, i
 
 bool conv_tma_ok_fwd(const ConvShape& s) { return s.C % 32 == 0 && load_encoders(); }
 
+namespace {
+TileCfg tile_cfg(int64_t M, int n) {
+  if (use_pairs(M)) return {2, g_bn_force ? bn_for_waves(M, n) : bn_for(n)};
+  if (pairs_mode() == 1 && !g_bn_force && bn_for(n) == 256) return {2, 128};
+  return {1, bn_for_waves(M, n)};
+}
+}  // namespace
+
 void set_conv_pairs(int mode) { g_pairs = mode; }
+void set_conv_bn(int bn) { g_bn_force = bn; }
 int conv_pairs_mode() { return pairs_mode(); }
 
 int conv_fwd_stats_tiles(const ConvShape& s, bool stem, int* tile_rows) {
@@ -707,14 +774,14 @@ bool conv_tma_ok_wgrad(const ConvShape& s) { return s.C % 32 == 0 && s.K % 32 ==
 
 cudaError_t conv_fwd_tma(const ConvShape& s, const float* x, const float* w, const float* bias, float* y,
                          float* stats, cudaStream_t st) {
-  const int BN = bn_for(s.K);
   CUtensorMap A, B;
   if (!make_im2col(&A, x, s.N, s.H, s.W, s.C, -s.pad, -s.pad, s.pad - (s.R - 1), s.pad - (s.S - 1), s.stride, kBM,
                    CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
   const int Ktot = s.R * s.S * s.C;
   const int M = s.N * s.P * s.Q;
-  const int CG = use_pairs(M) ? 2 : 1;
+  const TileCfg tc = tile_cfg(M, s.K);
+  const int CG = tc.cg, BN = tc.bn;
   if (!make_tiled(&B, w, s.K, Ktot, BN / CG, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;
   TmaArgs a{};
   a.num_kb = Ktot / kBK;
@@ -752,7 +819,6 @@ cudaError_t conv_fwd_tma(const ConvShape& s, const float* x, const float* w, con
 // wt_flip[c][r][s][k] = w[k][R-1-r][S-1-s][c], written by the caller.
 cudaError_t conv_dgrad_tma(const ConvShape& s, const float* dy, const float* wt_flip, float* dx, int accumulate,
                            cudaStream_t st) {
-  const int BN = bn_for(s.C);
   CUtensorMap A, B;
   const int padh = s.R - 1 - s.pad, padw = s.S - 1 - s.pad;
   if (!make_im2col(&A, dy, s.N, s.P, s.Q, s.K, -padh, -padw, padh - (s.R - 1), padw - (s.S - 1), 1, kBM,
@@ -760,7 +826,8 @@ cudaError_t conv_dgrad_tma(const ConvShape& s, const float* dy, const float* wt_
     return cudaErrorInvalidValue;
   const int Ktot = s.R * s.S * s.K;
   const int M = s.N * s.H * s.W;
-  const int CG = use_pairs(M) ? 2 : 1;
+  const TileCfg tc = tile_cfg(M, s.C);
+  const int CG = tc.cg, BN = tc.bn;
   if (!make_tiled(&B, wt_flip, s.C, Ktot, BN / CG, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;
   TmaArgs a{};
   a.num_kb = Ktot / kBK;
@@ -1534,6 +1601,92 @@ cudaError_t conv_dgrad_strided_tma(const ConvShape& s, const float* dy, const fl
     }
   }
   return cudaSuccess;
+}
+
+// Sub-pixel form of the 3x3 / stride-2 / pad-1 dgrad over an even input: dx
+// pixel (2u+a, 2v+b) only sees dy pixels (u+dr, v+ds), dr, ds in {0, 1}, through
+// filter tap (a - 2dr + 1, b - 2ds + 1) -- one GEMM over dy's grid with a 2x2
+// window and 4C output columns (a, b, c), instead of four phase GEMMs that each
+// re-read dy with 64..256-wide tiles and 4..16 k blocks.  7 of the 16 (tap,
+// phase) weight blocks are zero (56% useful MMA work, at the full 256-wide rate).
+// wsub[(a*2+b)*C + c][(dr*2+ds)*K + k] = w[k][a-2dr+1][b-2ds+1][c] or 0.
+__global__ void subpix_weights_kernel(const float* __restrict__ w, float* __restrict__ wsub, int K, int C) {
+  const int64_t total = static_cast<int64_t>(16) * C * K;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int k = static_cast<int>(i % K);
+    int64_t t = i / K;
+    const int tap = static_cast<int>(t % 4);
+    t /= 4;
+    const int c = static_cast<int>(t % C);
+    const int ab = static_cast<int>(t / C);
+    const int r = (ab >> 1) - 2 * (tap >> 1) + 1, q = (ab & 1) - 2 * (tap & 1) + 1;
+    wsub[i] = (r >= 0 && q >= 0) ? w[((static_cast<int64_t>(k) * 3 + r) * 3 + q) * C + c] : 0.f;
+  }
+}
+
+bool conv_dgrad_subpix_ok(const ConvShape& s) {
+  return s.R == 3 && s.S == 3 && s.stride == 2 && s.pad == 1 && s.H == 2 * s.P && s.W == 2 * s.Q &&
+         s.C % 32 == 0 && s.K % 32 == 0 && load_encoders();
+}
+
+cudaError_t conv_dgrad_subpix_tma(const ConvShape& s, const float* dy, const float* w, float* wt_scratch, float* dx,
+                                  int accumulate, cudaStream_t st) {
+  if (!conv_dgrad_subpix_ok(s)) return cudaErrorInvalidValue;
+  const int64_t wn = static_cast<int64_t>(16) * s.C * s.K;
+  subpix_weights_kernel<<<std::min<int64_t>(1184, (wn + 255) / 256), 256, 0, st>>>(w, wt_scratch, s.K, s.C);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  // im2col over dy (P x Q grid), window 2x2 at (u, v); row/col P, Q read as 0
+  CUtensorMap A, B, D;
+  if (!make_im2col(&A, dy, s.N, s.P, s.Q, s.K, 0, 0, 0, 0, 1, kBM, CU_TENSOR_MAP_SWIZZLE_128B))
+    return cudaErrorInvalidValue;
+  const int Ncols = 4 * s.C, Ktot = 4 * s.K;
+  const int M = s.N * s.P * s.Q;
+  // pairs halve each CTA's share of the (large, 16CK) weight tile stream; small
+  // M keeps single CTAs (conv_bench, stage 4: 84 us single vs 93 us pairs of 128)
+  const TileCfg tc = use_pairs(M) ? tile_cfg(M, Ncols) : TileCfg{1, bn_for_waves(M, Ncols)};
+  const int CG = tc.cg, BN = tc.bn;
+  if (!make_tiled(&B, wt_scratch, Ncols, Ktot, BN / CG, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;
+  std::memset(&D, 0, sizeof D);
+  TmaArgs a{};
+  a.num_kb = Ktot / kBK;
+  a.cchunks = s.K / 32;
+  a.S = 2;
+  a.P = s.P;
+  a.Q = s.Q;
+  a.PQ = s.P * s.Q;
+  a.stride = 1;
+  a.pad = 0;
+  a.pad_w = 0;
+  a.fcc = FastDivT(a.cchunks);
+  a.fS = FastDivT(2);
+  a.fPQ = FastDivT(a.PQ);
+  a.fQ = FastDivT(s.Q);
+  EpiArgs ep{};
+  ep.N = Ncols;
+  ep.reduce = accumulate;
+  ep.scatter = dx;
+  ep.M = M;
+  ep.Uhw = s.P * s.Q;
+  ep.Uw = s.Q;
+  ep.H = s.H;
+  ep.W = s.W;
+  ep.fUhw = FastDivT(s.P * s.Q);
+  ep.fUw = FastDivT(s.Q);
+  ep.subpix = s.C;
+  if (CG == 2) {
+    switch (BN) {
+      case 64: return launch<64, 0, 2>(A, B, D, a, ep, M, Ncols, 1, st);
+      case 128: return launch<128, 0, 2>(A, B, D, a, ep, M, Ncols, 1, st);
+      default: return launch<256, 0, 2>(A, B, D, a, ep, M, Ncols, 1, st);
+    }
+  }
+  switch (BN) {
+    case 64: return launch<64, 0>(A, B, D, a, ep, M, Ncols, 1, st);
+    case 128: return launch<128, 0>(A, B, D, a, ep, M, Ncols, 1, st);
+    default: return launch<256, 0>(A, B, D, a, ep, M, Ncols, 1, st);
+  }
 }
 
 cudaError_t conv_wgrad_tma(const ConvShape& s, const float* x, const float* dy, float* partial, int splits,

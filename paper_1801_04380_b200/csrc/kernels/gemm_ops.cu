@@ -465,8 +465,27 @@ cudaError_t conv_fwd(const ConvShape& s, const float* x, const float* w, const f
   }
 }
 
+namespace {
+int g_subpix = 1;
+bool use_subpix(const ConvShape& s) { return g_subpix && use_tma() && conv_dgrad_subpix_ok(s); }
+}  // namespace
+
+void set_conv_subpix(int on) { g_subpix = on; }
+
+int conv_dgrad_launches(const ConvShape& s) {
+  if (use_subpix(s)) return 2;
+  if (use_tma() && conv_tma_ok_dgrad_strided(s)) return 2 * s.stride * s.stride;
+  return 2;
+}
+
+int64_t conv_dgrad_scratch_floats(const ConvShape& s) {
+  const int64_t base = static_cast<int64_t>(s.K) * s.R * s.S * s.C;
+  return conv_dgrad_subpix_ok(s) ? std::max<int64_t>(base, 16ll * s.C * s.K) : base;
+}
+
 cudaError_t conv_dgrad(const ConvShape& s, const float* dy, const float* w, float* wt, float* dx, int accumulate,
                        cudaStream_t st) {
+  if (use_subpix(s)) return conv_dgrad_subpix_tma(s, dy, w, wt, dx, accumulate, st);
   if (use_tma() && conv_tma_ok_dgrad_strided(s)) return conv_dgrad_strided_tma(s, dy, w, wt, dx, accumulate, st);
   dim3 grid((s.C + 31) / 32, (s.K + 31) / 32, s.R * s.S), block(32, 8);
   const bool tma = use_tma() && conv_tma_ok_dgrad(s);

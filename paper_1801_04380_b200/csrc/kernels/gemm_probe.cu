@@ -120,6 +120,8 @@ extern "C" int sn_test_tma_overlap(const float* base) { return sn::tma_probe_ove
 // 1: TMA-fed conv kernels where the shape allows (default), 0: cp.async gathers.
 extern "C" void sn_test_set_conv_tma(int on) { sn::set_conv_tma(on); }
 extern "C" void sn_test_set_conv_pairs(int mode) { sn::set_conv_pairs(mode); }
+extern "C" void sn_test_set_conv_bn(int bn) { sn::set_conv_bn(bn); }
+extern "C" void sn_test_set_conv_subpix(int on) { sn::set_conv_subpix(on); }
 extern "C" void sn_test_set_conv_halo(int mode) { sn::set_conv_halo(mode); }
 
 // Pool layer kernels on caller buffers.  shape = {N,H,W,C,P,Q,K,stride,pad,mode}.

@@ -84,12 +84,21 @@ cudaError_t conv_halo_wgrad(int N, int H, int W, int C, int K, int R, int S, int
                             const float* dy, float* partial, float* dw, cudaStream_t st);
 
 bool conv_tma_ok_dgrad_strided(const ConvShape& s);
+// 3x3 / stride 2 / pad 1 dgrad as one sub-pixel GEMM (conv_tma.cu); wt_scratch
+// must hold 16*C*K floats (conv_dgrad_scratch_floats)
+bool conv_dgrad_subpix_ok(const ConvShape& s);
+cudaError_t conv_dgrad_subpix_tma(const ConvShape& s, const float* dy, const float* w, float* wt_scratch, float* dx,
+                                  int accumulate, cudaStream_t st);
+void set_conv_subpix(int on);          // 0: phase-decomposed strided dgrad (A/B, tests)
+int conv_dgrad_launches(const ConvShape& s);          // kernels one conv_dgrad issues
+int64_t conv_dgrad_scratch_floats(const ConvShape& s);  // wt scratch conv_dgrad needs
 cudaError_t conv_dgrad_strided_tma(const ConvShape& s, const float* dy, const float* w, float* wt_scratch, float* dx,
                                    int accumulate, cudaStream_t st);
 void set_conv_tma(int on);
 // CTA-pair (cta_group::2) conv kernels: 0 off, 1 when the shape keeps the
 // pairs busy (default; env SN_CONV_PAIRS=0 turns them off), 2 always (tests).
 void set_conv_pairs(int mode);
+void set_conv_bn(int bn);  // im2col conv tile width override (0 = policy), for A/B timing
 int conv_pairs_mode();
 bool use_tma();
 

@@ -96,6 +96,9 @@ CONV_CASES = [
     (4, 128, 7, 7, 256, 3, 1, 1),    # 7x7 tiles straddle images
     (2, 256, 14, 14, 64, 1, 1, 0),   # 1x1, K = 64
     (2, 64, 15, 15, 128, 3, 2, 1),   # odd extent, stride 2 (uneven phases)
+    (2, 64, 16, 16, 128, 3, 2, 1),   # even extent, stride 2: sub-pixel dgrad (one 256-wide tile)
+    (3, 32, 28, 20, 64, 3, 2, 1),    # sub-pixel dgrad, non-square, 128 output columns
+    (2, 128, 14, 14, 96, 3, 2, 1),   # sub-pixel dgrad, two 256-wide tiles, K % 64 != 0
     (2, 32, 16, 16, 64, 1, 2, 0),    # 1x1 stride 2: phases without taps
     (1, 64, 23, 23, 96, 5, 3, 2),    # stride 3, 5x5
     (2, 128, 8, 8, 512, 3, 1, 1),    # K = 512: two N tiles of 256
@@ -123,15 +126,20 @@ def _shape_arr(N, C, H, W, K, k, s, p):
     return (ctypes.c_int * 11)(N, H, W, C, K, k, k, P, Q, s, p), P, Q
 
 
-@pytest.mark.parametrize("tma,pairs,halo", [(1, 1, 1), (1, 2, 0), (1, 1, 2), (1, 2, 2), (0, 1, 0)])
+@pytest.mark.parametrize("tma,pairs,halo,subpix", [(1, 1, 1, 1), (1, 2, 0, 1), (1, 1, 2, 1), (1, 2, 2, 1), (0, 1, 0, 1),
+                                                   (1, 1, 1, 0)])
 @pytest.mark.parametrize("case", CONV_CASES)
-def test_conv_fwd_dgrad_wgrad(cuda, case, tma, pairs, halo):
+def test_conv_fwd_dgrad_wgrad(cuda, case, tma, pairs, halo, subpix):
     """pairs=2 forces the CTA-pair (cta_group::2, M = 256) TMA kernels on
     every shape (odd tile counts, rows past M in the peer CTA); halo=2 the
     halo-tiled stride-1 kernels wherever they apply (junk padded columns,
-    bands past the last output row)."""
+    bands past the last output row); subpix=0 the phase-decomposed strided
+    dgrad instead of the sub-pixel GEMM."""
     N, C, H, W, K, k, s, p = case
+    if not subpix and s == 1:
+        pytest.skip("sub-pixel toggle only affects strided dgrad")
     lib = _conv_lib()
+    lib.sn_test_set_conv_subpix(subpix)
     lib.sn_test_set_conv_tma(tma)
     lib.sn_test_set_conv_pairs(pairs)
     lib.sn_test_set_conv_halo(halo)
@@ -155,7 +163,7 @@ def test_conv_fwd_dgrad_wgrad(cuda, case, tma, pairs, halo):
     assert lib.sn_test_conv(0, shape, ptrs, 0) == 0
     _check(y_d.permute(0, 3, 1, 2).cpu(), y.detach(), C * k * k)
     # dgrad, overwrite then accumulate
-    wt = torch.empty(K * k * k * C, device=cuda)
+    wt = torch.empty(max(K * k * k * C, 16 * C * K), device=cuda)
     dx_d = torch.full((N, H, W, C), float("nan"), device=cuda)
     ptrs = (ctypes.c_void_p * 4)(dy_d.data_ptr(), w_d.data_ptr(), wt.data_ptr(), dx_d.data_ptr())
     assert lib.sn_test_conv(1, shape, ptrs, 0) == 0
@@ -177,6 +185,7 @@ def test_conv_fwd_dgrad_wgrad(cuda, case, tma, pairs, halo):
     lib.sn_test_set_conv_tma(1)
     lib.sn_test_set_conv_pairs(1)
     lib.sn_test_set_conv_halo(1)
+    lib.sn_test_set_conv_subpix(1)
 
 
 def test_tma_overlapping_window_probe(cuda):

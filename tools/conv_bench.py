@@ -31,6 +31,7 @@ def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--pairs", type=int, nargs="+", default=[0, 1, 2])
     ap.add_argument("--halo", type=int, nargs="+", default=[1])
+    ap.add_argument("--bn", type=int, nargs="+", default=[0], help="im2col tile width override (0 = policy)")
     ap.add_argument("--ops", nargs="+", default=["fwd", "dgrad", "wgrad"])
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--shapes", type=int, nargs="+", default=None, help="indices into SHAPES")
@@ -73,7 +74,8 @@ def main() -> None:
                                              part.data_ptr(), red.data_ptr())
                 call = lambda: lib.sn_test_conv(2, shape, ptrs, 0)
             line = f"{op:6s} N{N} C{C} {H}x{W} K{K} s{s}"
-            for pm, hm in [(pm, hm) for hm in args.halo for pm in args.pairs]:
+            for pm, hm, bn in [(pm, hm, bn) for hm in args.halo for pm in args.pairs for bn in args.bn]:
+                lib.sn_test_set_conv_bn(bn)
                 lib.sn_test_set_conv_pairs(pm)
                 lib.sn_test_set_conv_halo(hm)
                 lib.sn_test_set_sync(1)
@@ -89,9 +91,11 @@ def main() -> None:
                 torch.cuda.synchronize()
                 ms = e0.elapsed_time(e1) / args.iters
                 lib.sn_test_set_sync(1)
-                line += f" | p{pm}h{hm}: {ms * 1e3:7.1f} us {flops / ms / 1e9:6.1f} TF/s"
+                tag = f"p{pm}h{hm}" + (f"b{bn}" if bn else "")
+                line += f" | {tag}: {ms * 1e3:7.1f} us {flops / ms / 1e9:6.1f} TF/s"
             print(line, flush=True)
     lib.sn_test_set_conv_pairs(1)
+    lib.sn_test_set_conv_bn(0)
 
 
 if __name__ == "__main__":
