@@ -721,12 +721,14 @@ struct Compiler {
         const int relu = bwd_relu ? 1 : 0;
         float* cpy = nullptr;
         int cpy_acc = 0;
+        float* own = nullptr;
         if (bn_from_join[cur_ti] >= 0) {
           auto pj = pending_join.find(static_cast<int>(cur_ti));
           if (pj == pending_join.end()) xfail(SN_EK_INTERNAL, "fused JOIN backward not recorded");
           dy = const_cast<float*>(pj->second.dy);
           cpy = pj->second.other;
           cpy_acc = pj->second.other_acc;
+          own = pj->second.own;
           pending_join.erase(pj);
         }
         float* dcb = nullptr;
@@ -735,7 +737,8 @@ struct Compiler {
           conv_bias_done[pid] = 1;
         }
         push([=] {
-          ck(sn::bn_bwd(x, dy, rows, C, g, beta, stats, relu, dx, acc, dg, dbt, red, st, dcb, cpy, cpy_acc), "bn_bwd");
+          ck(sn::bn_bwd(x, dy, rows, C, g, beta, stats, relu, dx, acc, dg, dbt, red, st, dcb, cpy, cpy_acc, own),
+             "bn_bwd");
         },
              dx ? (dcb ? 4 : 3) : 2);
         break;
@@ -799,9 +802,10 @@ struct Compiler {
           const int ra = join_relu[cur_ti];
           const int other = pv[0] == ra ? pv[1] : pv[0];
           int a_r = 0, a_o = 0;
-          dx_target(ra, &a_r);  // the BN's own gradient buffer: never written
+          float* own = dx_target(ra, &a_r);  // the BN's own gradient buffer: written only with copy_own
+          if (join_copy_own[cur_ti] && a_r) xfail(SN_EK_INTERNAL, "JOIN fold: the BN's dy buffer is not fresh");
           float* d_o = dx_target(other, &a_o);
-          pending_join[join_to_bn[cur_ti]] = PendingJoin{dy, d_o, a_o};
+          pending_join[join_to_bn[cur_ti]] = PendingJoin{dy, d_o, a_o, join_copy_own[cur_ti] ? own : nullptr};
           break;
         }
         if (pv.size() == 2 && n % 4 == 0) {
@@ -851,7 +855,9 @@ struct Compiler {
     const float* dy = nullptr;
     float* other = nullptr;
     int other_acc = 0;
+    float* own = nullptr;  // join_copy_own: the BN's own dy buffer, written by the first pass
   };
+  std::vector<char> join_copy_own;
   std::unordered_map<int, PendingJoin> pending_join;  // keyed by BN-backward tape index
   // CONV forward -> BN forward (next compute action, reading that output): the
   // CONV epilogue emits per-tile statistics, the BN only combines them.
@@ -890,6 +896,7 @@ struct Compiler {
     join_to_bn.assign(T, -1);
     bn_from_join.assign(T, -1);
     join_relu.assign(T, -1);
+    join_copy_own.assign(T, 0);
     bn_bias_at.assign(T, 0);
     conv_bias_done.assign(net.n, 0);
     const char* env = std::getenv("SN_FUSE");  // SN_FUSE=0: one kernel per layer (A/B and bitwise tests)
@@ -1151,20 +1158,40 @@ struct Compiler {
       }
       if (joff < 0) continue;
       const int bn_dx_owner = net.grad_owner(net.prev[bn][0]);
+      // the BN's own dy buffer (the ReLU's gradient, in place), allocated before
+      int64_t ooff = -1, oblk = 0, xoff = -1, xblk = 0;
+      for (size_t j = i; j-- > 0;) {
+        const snp::Event& f = P.tape[j];
+        if (f.op == 'A' && f.a == snp::K_GRAD && f.b == bn) {
+          ooff = f.c;
+          oblk = f.d;
+          break;
+        }
+      }
+      bool copy_own = false;
       for (size_t j = i + 1; j < T; ++j) {
         const snp::Event& f = P.tape[j];
         // a new buffer over the JOIN gradient's blocks breaks the fusion, except
-        // the BN's own dx target placed exactly there: it is freshly allocated
-        // (dx written, not accumulated) and dx = f(dy, x) is elementwise, so
-        // reading dy and writing dx at the same address is safe
-        if (f.op == 'A' && overlap(f.c, f.d, joff, jblk) &&
-            !(f.a == snp::K_GRAD && f.b == bn_dx_owner && f.c == joff && f.d == jblk))
-          break;
+        // the BN's own dx target: placed exactly there, dx = f(dy, x) is
+        // elementwise, so reading dy and writing dx at the same address is safe;
+        // placed partly over it, the first (statistics) pass also copies dy into
+        // the BN's own dy buffer and the dx pass reads that copy (copy_own)
+        if (f.op == 'A' && overlap(f.c, f.d, joff, jblk)) {
+          if (!(f.a == snp::K_GRAD && f.b == bn_dx_owner)) break;
+          if (!(f.c == joff && f.d == jblk)) {
+            copy_own = true;
+            xoff = f.c;
+            xblk = f.d;
+          }
+        }
         if (f.op == 'B' && f.b == bn) {
-          if (bn_bwd_relu[j]) {
+          const bool own_ok = !copy_own || (ooff >= 0 && !overlap(ooff, oblk, joff, jblk) &&
+                                            !overlap(ooff, oblk, xoff, xblk));
+          if (bn_bwd_relu[j] && own_ok) {
             join_to_bn[i] = static_cast<int>(j);
             bn_from_join[j] = static_cast<int>(i);
             join_relu[i] = ra;
+            join_copy_own[i] = copy_own ? 1 : 0;
           }
           break;
         }

@@ -142,7 +142,9 @@ bool bn_bwd_bias_ok(int C);
 cudaError_t bn_bwd(const float* x, const float* dy, int64_t rows, int C, const float* gamma, const float* beta,
                    const float* stats, int relu, float* dx, int accumulate, float* dgamma, float* dbeta,
                    float* red_scratch, cudaStream_t st, float* dbias = nullptr, float* copy_dst = nullptr,
-                   int copy_acc = 0);
+                   int copy_acc = 0, float* copy2 = nullptr);
+// copy2 (optional, C % 4 == 0): the statistics pass also writes dy there and
+// the dx pass reads dy from it (dx may then overlap the original dy).
 // copy_dst (optional, C % 4 == 0): the fused backward of the 2-input JOIN
 // feeding the ReLU: its gradient dy is also written (copy_acc: added) into the
 // JOIN's other input's gradient buffer in the reduction pass.

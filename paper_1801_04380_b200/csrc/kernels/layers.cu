@@ -138,6 +138,7 @@ struct RedBnBwdOp {
   // (or added) into the JOIN's other input's gradient buffer
   float* copy_dst;
   int copy_acc;
+  float* copy2;  // optional second (plain) copy of dy: the dx pass reads it
   using P = Bn4;
   struct R {
     float4 g, v;
@@ -152,6 +153,7 @@ struct RedBnBwdOp {
   }
   __device__ R load(int64_t off) const { return R{ld4(dy + off), ld4(x + off)}; }
   __device__ void side(int64_t off, const R& r) const {
+    if (copy2) *reinterpret_cast<float4*>(copy2 + off) = r.g;
     if (!copy_dst) return;
     float4* d = reinterpret_cast<float4*>(copy_dst + off);
     if (copy_acc) {
@@ -1602,12 +1604,14 @@ bool bn_bwd_bias_ok(int C) { return C % 4 == 0 && kThreads % (C / 4) == 0; }
 
 cudaError_t bn_bwd(const float* x, const float* dy, int64_t rows, int C, const float* gamma, const float* beta,
                    const float* stats, int relu, float* dx, int accumulate, float* dgamma, float* dbeta,
-                   float* red_scratch, cudaStream_t st, float* dbias, float* copy_dst, int copy_acc) {
+                   float* red_scratch, cudaStream_t st, float* dbias, float* copy_dst, int copy_acc,
+                   float* copy2) {
   float* coef = red_scratch + static_cast<int64_t>(kRedChunks) * 2 * C * 2;  // past the partials
-  if (copy_dst && C % 4 != 0) return cudaErrorInvalidValue;
-  cudaError_t e = colred(RedBnBwdOp{x, dy, stats, gamma, beta, relu, copy_dst, copy_acc},
+  if ((copy_dst || copy2) && C % 4 != 0) return cudaErrorInvalidValue;
+  cudaError_t e = colred(RedBnBwdOp{x, dy, stats, gamma, beta, relu, copy_dst, copy_acc, copy2},
                          BnBwdFin{C, dgamma, dbeta, coef}, rows, C, red_scratch, st);
   if (e != cudaSuccess) return e;
+  if (copy2) dy = copy2;  // the dx pass reads the copy (the original may be overwritten by dx)
   const int64_t n = rows * C;
   if (dbias && (!dx || !bn_bwd_bias_ok(C))) return cudaErrorInvalidValue;
   if (dx) {
