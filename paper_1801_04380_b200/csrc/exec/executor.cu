@@ -25,6 +25,7 @@
 #include <map>
 #include <string>
 #include <unordered_map>
+#include <unordered_set>
 #include <vector>
 
 #include "../kernels/kernels.hpp"
@@ -347,6 +348,9 @@ struct Compiler {
   std::unordered_map<int, bool> fresh;                             // grad owner -> not yet written
   std::unordered_map<int, cudaEvent_t> d2h_live;                   // act lid -> copy-out event
   std::vector<std::pair<std::pair<int64_t, int64_t>, cudaEvent_t>> freed_reading;  // region being read by D2H
+  // buffers allocated over such regions: the events their first use must wait for
+  std::unordered_map<int64_t, std::vector<cudaEvent_t>> pending_wait;
+  std::unordered_set<cudaEvent_t> waited;
   std::unordered_map<int, cudaEvent_t> h2d_live;                   // act lid -> fetch event (not yet waited)
   std::vector<char> fetched;                                       // lids fetched anywhere in the tape
   bool used_s1 = false, used_s2 = false, used_s3 = false;
@@ -370,11 +374,35 @@ struct Compiler {
 
   float* ptr(int kind, int id) {
     if (kind == snp::K_ACT && id == data_id) return ex->data_buf;
-    auto it = where.find(key_code(kind, id));
+    const int64_t key = key_code(kind, id);
+    auto it = where.find(key);
     if (it == where.end())
       xfail(SN_EK_INTERNAL, std::string("tape references non-resident ") + (kind == 0 ? "act " : kind == 1 ? "grad " : "ws ") +
                                 std::to_string(id));
+    // first use of a buffer allocated over blocks another stream may still be
+    // reading: the compute stream waits here, not at the allocation
+    if (!pending_wait.empty()) {
+      auto pw = pending_wait.find(key);
+      if (pw != pending_wait.end()) {
+        const std::vector<cudaEvent_t> evs = std::move(pw->second);
+        pending_wait.erase(pw);
+        for (cudaEvent_t ev : evs) flush_hazard(ev);
+      }
+    }
     return reinterpret_cast<float*>(ex->arena + it->second.first * snp::kBlockBytes);
+  }
+
+  // s0 waits for a reader event once; every hazard it covers is then retired
+  void flush_hazard(cudaEvent_t ev) {
+    if (waited.count(ev)) return;
+    waited.insert(ev);
+    s0_wait(ev);
+    for (size_t i = 0; i < freed_reading.size();) {
+      if (freed_reading[i].second == ev)
+        freed_reading.erase(freed_reading.begin() + i);
+      else
+        ++i;
+    }
   }
 
   void s0_wait(cudaEvent_t e) {
@@ -396,20 +424,17 @@ struct Compiler {
     const int64_t key = key_code(e.a, e.b);
     where[key] = {e.c, e.d};
     if (e.a == snp::K_GRAD) fresh[e.b] = true;
-    for (size_t i = 0; i < freed_reading.size();) {
-      if (overlap(e.c, e.d, freed_reading[i].first.first, freed_reading[i].first.second)) {
-        s0_wait(freed_reading[i].second);
-        freed_reading.erase(freed_reading.begin() + i);
-      } else {
-        ++i;
-      }
-    }
+    // regions another stream may still be reading: waited at this buffer's
+    // first use (ptr), not here
+    for (const auto& h : freed_reading)
+      if (overlap(e.c, e.d, h.first.first, h.first.second)) pending_wait[key].push_back(h.second);
   }
 
   void on_free(const snp::Event& e) {
     const int64_t key = key_code(e.a, e.b);
     auto it = where.find(key);
     if (it == where.end()) xfail(SN_EK_INTERNAL, "tape frees an unknown key");
+    pending_wait.erase(key);  // never used: its hazards stay registered for the next occupant
     auto sr = side_reads.find(key);
     if (sr != side_reads.end()) {
       freed_reading.push_back({it->second, sr->second});
