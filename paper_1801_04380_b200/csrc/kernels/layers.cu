@@ -3,6 +3,7 @@
 // NHWC fp32; float4 paths whenever the channel count allows.  Every reduction
 // is two-stage with a fixed combination order, so a replayed (recomputed)
 // forward and every feature set produce bit-identical values.
+#include <algorithm>
 #include <cfloat>
 #include <cmath>
 
@@ -1524,45 +1525,61 @@ namespace {
 // global shift x0 = x[0][c]:  with d = shift_t - x0,
 //   sum(y - x0)     = S1_t + n_t d
 //   sum((y - x0)^2) = S2_t + 2 d S1_t + n_t d^2.
-__global__ void tile_stats_stage1(const float* __restrict__ tiles, int ntiles, int tile_rows, int64_t rows, int C,
-                                  const float* __restrict__ x, int chunk, double* part) {
+// Block = (chunk of tiles, 64 channels); 4 tile lanes x 64 channels per block,
+// each lane walks its tiles with 4 independent accumulator pairs (loads in
+// flight), lanes and accumulators merged in a fixed order.  ~2 blocks per SM
+// (a 25-block grid for stage 3 took 13 us of pure latency).
+constexpr int kTsChan = 64, kTsLanes = kThreads / kTsChan;
+__global__ void __launch_bounds__(kThreads) tile_stats_stage1(const float* __restrict__ tiles, int ntiles,
+                                                              int tile_rows, int64_t rows, int C,
+                                                              const float* __restrict__ x, int chunk, double* part) {
   __shared__ double s1[kThreads], s2[kThreads];
   const int t0 = blockIdx.x * chunk;
   const int t1 = min(ntiles, t0 + chunk);
-  const int cb = C < kThreads ? C : kThreads;
-  const int lanes = kThreads / cb;
-  const int lane = threadIdx.x / cb, cc = threadIdx.x % cb;
-  for (int c0 = 0; c0 < C; c0 += cb) {
-    const int c = c0 + cc;
-    double a = 0.0, b = 0.0;
-    if (lane < lanes && c < C) {
-      const double x0 = x[c];
-      const int planes = tile_rows > 0 ? 3 : 4;
-      for (int t = t0 + lane; t < t1; t += lanes) {
-        const float* p = tiles + static_cast<size_t>(t) * planes * C + c;
-        const int64_t left = rows - static_cast<int64_t>(t) * tile_rows;
+  const int lane = threadIdx.x / kTsChan;
+  const int c = blockIdx.y * kTsChan + threadIdx.x % kTsChan;
+  const int planes = tile_rows > 0 ? 3 : 4;
+  double a[4] = {0, 0, 0, 0}, b[4] = {0, 0, 0, 0};
+  if (c < C) {
+    const double x0 = x[c];
+    int t = t0 + lane;
+    for (; t < t1; t += 4 * kTsLanes) {
+      float sh[4], f1[4], f2[4], cnt[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int tu = t + u * kTsLanes;
+        const float* p = tiles + static_cast<size_t>(tu < t1 ? tu : t0) * planes * C + c;
+        sh[u] = p[0];
+        f1[u] = p[C];
+        f2[u] = p[2 * C];
+        cnt[u] = tile_rows > 0 ? 0.f : p[3 * C];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int tu = t + u * kTsLanes;
+        if (tu >= t1) continue;
+        const int64_t left = rows - static_cast<int64_t>(tu) * tile_rows;
         const double n = tile_rows > 0 ? static_cast<double>(left < tile_rows ? left : tile_rows)
-                                       : static_cast<double>(p[3 * C]);
+                                       : static_cast<double>(cnt[u]);
         if (n <= 0.0) continue;  // a tile past the last output row (its shift is not a value)
-        const double d = static_cast<double>(p[0]) - x0;
-        const double S1 = p[C], S2 = p[2 * C];
-        a += S1 + n * d;
-        b += S2 + 2.0 * d * S1 + n * d * d;
+        const double d = static_cast<double>(sh[u]) - x0;
+        const double S1 = f1[u], S2 = f2[u];
+        a[u] += S1 + n * d;
+        b[u] += S2 + 2.0 * d * S1 + n * d * d;
       }
     }
-    s1[threadIdx.x] = a;
-    s2[threadIdx.x] = b;
-    __syncthreads();
-    if (lane == 0 && c < C) {
-      double A = 0.0, B = 0.0;
-      for (int l = 0; l < lanes; ++l) {
-        A += s1[l * cb + cc];
-        B += s2[l * cb + cc];
-      }
-      part[(static_cast<size_t>(blockIdx.x) * 2) * C + c] = A;
-      part[(static_cast<size_t>(blockIdx.x) * 2 + 1) * C + c] = B;
+  }
+  s1[threadIdx.x] = (a[0] + a[1]) + (a[2] + a[3]);
+  s2[threadIdx.x] = (b[0] + b[1]) + (b[2] + b[3]);
+  __syncthreads();
+  if (lane == 0 && c < C) {
+    double A = 0.0, B = 0.0;
+    for (int l = 0; l < kTsLanes; ++l) {
+      A += s1[l * kTsChan + threadIdx.x];
+      B += s2[l * kTsChan + threadIdx.x];
     }
-    __syncthreads();
+    part[(static_cast<size_t>(blockIdx.x) * 2) * C + c] = A;
+    part[(static_cast<size_t>(blockIdx.x) * 2 + 1) * C + c] = B;
   }
 }
 
@@ -1572,11 +1589,12 @@ cudaError_t bn_stats_from_tiles(const float* tiles, int ntiles, int tile_rows, c
                                 float* stats, float* running, float eps, float momentum, float* red_scratch,
                                 cudaStream_t st) {
   double* part = reinterpret_cast<double*>(red_scratch);
-  int nb = (ntiles + 15) / 16;
-  nb = nb < 1 ? 1 : (nb > kRedChunks ? kRedChunks : nb);
+  const int cgroups = (C + kTsChan - 1) / kTsChan;
+  int nb = (2 * 148 + cgroups - 1) / cgroups;  // ~2 blocks per SM in total
+  nb = std::max(1, std::min({nb, (ntiles + 3) / 4, kRedChunks}));
   const int chunk = (ntiles + nb - 1) / nb;
   nb = (ntiles + chunk - 1) / chunk;
-  tile_stats_stage1<<<nb, kThreads, 0, st>>>(tiles, ntiles, tile_rows, rows, C, x, chunk, part);
+  tile_stats_stage1<<<dim3(nb, cgroups), kThreads, 0, st>>>(tiles, ntiles, tile_rows, rows, C, x, chunk, part);
   colred_stage2<<<(C + 31) / 32, kStage2Threads, 0, st>>>(part, nb, C,
                                                           BnStatsFin{x, rows, C, eps, momentum, stats, running});
   return cudaGetLastError();
