@@ -1060,11 +1060,7 @@ struct Compiler {
     }
     for (int a = 0; a < net.n; ++a) {
       if (!bn_relu_pair(a) || !act_bwd_fused[a] || net.next[a].size() != 1) continue;
-      const int nx = net.next[a][0];
-      // every forward of the ReLU fused into its single consumer, and (POOL)
-      // every forward of that consumer fed by such a fused chain
-      if (act_fwd[a] == act_join_fused[a] && act_join_fused[a] > 0) elide_out[a] = 1;  // read only by the fused chains
-      (void)nx;
+      // (ReLU output elision: after the dead-write analysis below)
     }
     // Dead writes: a fused BN+ReLU forward / replay (BN output not
     // materialised) whose ReLU output nobody reads before it is freed or
@@ -1091,16 +1087,28 @@ struct Compiler {
       }
       if (!read) dead_at[i] = 1;
     }
-    // ReLU -> POOL chains: the ReLU output is never materialised when every
-    // live (not dead) forward of the ReLU is fused into the pool and every
-    // forward of the pool is such a fused chain
+    // ReLU -> JOIN / POOL chains: the ReLU output is never materialised when
+    // every live (not dead) forward of the ReLU is fused into its single
+    // consumer and every forward of that consumer is such a fused chain (the
+    // reference replays ReLU outputs for the ReLU backward, which is folded
+    // into the BN backward here: those replays are dead)
+    std::vector<int> join_fwd_n(net.n, 0), join_fwd_fused(net.n, 0);
+    for (size_t i = 0; i < T; ++i) {
+      const snp::Event& e = P.tape[i];
+      if ((e.op != 'C' && e.op != 'R') || net.kind[e.b] != snp::JOIN) continue;
+      ++join_fwd_n[e.b];
+      join_fwd_fused[e.b] += join_from[i] >= 0;
+    }
     for (int a = 0; a < net.n; ++a) {
-      if (!bn_relu_pair(a) || !act_bwd_fused[a] || net.next[a].size() != 1 || act_pool_fused[a] == 0) continue;
+      if (!bn_relu_pair(a) || !act_bwd_fused[a] || net.next[a].size() != 1) continue;
       const int nx = net.next[a][0];
       int live = 0;
       for (size_t i = 0; i < T; ++i)
         live += (P.tape[i].op == 'C' || P.tape[i].op == 'R') && P.tape[i].b == a && !dead_at[i];
-      if (live == act_pool_fused[a] && pool_fwd_n[nx] == pool_fwd_fused[nx]) elide_out[a] = 1;
+      if (act_join_fused[a] > 0 && live == act_join_fused[a] && join_fwd_n[nx] == join_fwd_fused[nx])
+        elide_out[a] = 1;
+      if (act_pool_fused[a] > 0 && live == act_pool_fused[a] && pool_fwd_n[nx] == pool_fwd_fused[nx])
+        elide_out[a] = 1;
     }
     // Dead replays (general): a replay of an unfused layer whose output no later
     // action reads before it is freed or rewritten -- under the kernels' actual
