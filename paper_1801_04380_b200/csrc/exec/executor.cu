@@ -271,6 +271,7 @@ void alloc_device(sn_exec* ex) {
     if (l.kind == snp::BN || l.kind == snp::CONV || l.kind == snp::FC)
       red = std::max(red, sn::red_scratch_floats(l.C));
     if (l.kind == snp::CONV) wt = std::max(wt, std::max<int64_t>(l.w_n, sn::conv_dgrad_scratch_floats(l.conv)));
+    if (l.kind == snp::FC) wt = std::max(wt, l.w_n);  // fc_dgrad's transposed weights
   }
   ck(cudaMemcpy(ex->state, st.data(), st.size() * sizeof(float), cudaMemcpyHostToDevice), "memcpy(state)");
   // split-K partial scratch (outside the arena, like cuDNN's internal buffers):
@@ -522,7 +523,7 @@ struct Compiler {
         const float* b = ex->params + l.b_off;
         const int B = ex->B, I = l.fc_in, O = l.C, sp = l.fc_splits;
         float* part = ex->partial;
-        push([=] { ck(sn::fc_fwd(B, I, O, x, w, b, y, part, sp, st), "fc_fwd"); }, 2);
+        push([=] { ck(sn::fc_fwd(B, I, O, x, w, b, y, part, sp, st), "fc_fwd"); }, sn::fc_fwd_launches(B, I, O));
         break;
       }
       case snp::BN: {
@@ -725,9 +726,10 @@ struct Compiler {
         float* db = ex->grads + l.b_off;
         float* part = ex->partial;
         float* red = ex->red;
+        float* wt = ex->wt_scratch;
         push([=] {
           ck(sn::fc_wgrad(B, I, O, x, dy, dw, db, red, st), "fc_wgrad");
-          if (dx) ck(sn::fc_dgrad(B, I, O, dy, w, dx, acc, part, sp, st), "fc_dgrad");
+          if (dx) ck(sn::fc_dgrad(B, I, O, dy, w, dx, acc, part, sp, st, wt), "fc_dgrad");
         }, dx ? 6 : 4);
         break;
       }

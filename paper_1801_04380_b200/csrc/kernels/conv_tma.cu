@@ -768,7 +768,10 @@ int tma_probe_overlap(const float* base) {
                                          CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE));
 }
 bool conv_tma_ok_dgrad(const ConvShape& s) {
-  return s.stride == 1 && s.K % 32 == 0 && s.H == s.P && s.W == s.Q && load_encoders();
+  // a 1x1 filter may have K % 32 != 0 (the FC dgrad): the last channel chunk
+  // reads past K, which both tensor maps zero-fill (one tap: no neighbour to hit)
+  const bool kok = s.K % 32 == 0 || (s.R == 1 && s.S == 1 && s.K % 4 == 0);
+  return s.stride == 1 && kok && s.H == s.P && s.W == s.Q && load_encoders();
 }
 bool conv_tma_ok_wgrad(const ConvShape& s) { return s.C % 32 == 0 && s.K % 32 == 0 && load_encoders(); }
 
@@ -830,8 +833,8 @@ cudaError_t conv_dgrad_tma(const ConvShape& s, const float* dy, const float* wt_
   const int CG = tc.cg, BN = tc.bn;
   if (!make_tiled(&B, wt_flip, s.C, Ktot, BN / CG, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;
   TmaArgs a{};
-  a.num_kb = Ktot / kBK;
-  a.cchunks = s.K / 32;
+  a.num_kb = (Ktot + kBK - 1) / kBK;
+  a.cchunks = (s.K + 31) / 32;
   a.S = s.S;
   a.P = s.H;
   a.Q = s.W;

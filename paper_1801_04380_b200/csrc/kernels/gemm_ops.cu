@@ -569,8 +569,23 @@ int fc_splits(int B, int I, int O, int64_t partial_floats_cap) {
   return static_cast<int>(std::max<int64_t>(1, want));
 }
 
+namespace {
+// FC forward as a 1x1 convolution over B "images" of one pixel: the TMA
+// im2col kernel (K-major x and w straight from HBM, bias in the epilogue, no
+// split-K partials); 32 us + a 7 us reduction -> one ~8 us launch for 512->1000
+ConvShape fc_as_conv(int B, int I, int O) {
+  ConvShape cs{};
+  cs.N = B; cs.H = 1; cs.W = 1; cs.C = I; cs.K = O; cs.R = 1; cs.S = 1; cs.P = 1; cs.Q = 1; cs.stride = 1; cs.pad = 0;
+  return cs;
+}
+bool fc_fwd_tma_ok(int B, int I, int O) { return use_tma() && conv_tma_ok_fwd(fc_as_conv(B, I, O)) && O % 4 == 0; }
+}  // namespace
+
+int fc_fwd_launches(int B, int I, int O) { return fc_fwd_tma_ok(B, I, O) ? 1 : 2; }
+
 cudaError_t fc_fwd(int B, int I, int O, const float* x, const float* w, const float* bias, float* y, float* partial,
                    int splits, cudaStream_t st) {
+  if (fc_fwd_tma_ok(B, I, O)) return conv_fwd_tma(fc_as_conv(B, I, O), x, w, bias, y, nullptr, st);
   const int eff = effective_splits(I, splits);
   cudaError_t e = fc_gemm(0, 0, x, I, w, I, B, O, I, partial, eff, st);
   if (e != cudaSuccess) return e;
@@ -578,7 +593,10 @@ cudaError_t fc_fwd(int B, int I, int O, const float* x, const float* w, const fl
 }
 
 cudaError_t fc_dgrad(int B, int I, int O, const float* dy, const float* w, float* dx, int accumulate, float* partial,
-                     int splits, cudaStream_t st) {
+                     int splits, cudaStream_t st, float* wt_scratch) {
+  // as the dgrad of the 1x1 convolution (w transposed once, TMA kernel, no split-K)
+  const ConvShape cs = fc_as_conv(B, I, O);
+  if (wt_scratch && use_tma() && conv_tma_ok_dgrad(cs)) return conv_dgrad(cs, dy, w, wt_scratch, dx, accumulate, st);
   // dx[b][i] = sum_o dy[b][o] w[o][i]: A = dy (K-major, ld O), B[i][o] = w[o][i] (MN-major, ld I)
   const int eff = effective_splits(O, splits);
   cudaError_t e = fc_gemm(0, 1, dy, O, w, I, B, I, O, partial, eff, st);

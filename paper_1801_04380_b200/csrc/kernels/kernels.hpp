@@ -104,10 +104,11 @@ bool use_tma();
 
 // FC: x[B][I], w[O][I], y[B][O]
 int fc_splits(int B, int I, int O, int64_t partial_floats_cap);
+int fc_fwd_launches(int B, int I, int O);  // kernels one fc_fwd issues
 cudaError_t fc_fwd(int B, int I, int O, const float* x, const float* w, const float* bias, float* y,
                    float* partial, int splits, cudaStream_t st);
 cudaError_t fc_dgrad(int B, int I, int O, const float* dy, const float* w, float* dx, int accumulate,
-                     float* partial, int splits, cudaStream_t st);
+                     float* partial, int splits, cudaStream_t st, float* wt_scratch = nullptr);
 cudaError_t fc_wgrad(int B, int I, int O, const float* x, const float* dy, float* dw, float* db,
                      float* red_scratch, cudaStream_t st);
 
