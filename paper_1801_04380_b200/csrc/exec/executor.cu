@@ -285,6 +285,8 @@ void alloc_device(sn_exec* ex) {
     } else if (l.kind == snp::FC) {
       l.fc_splits = sn::fc_splits(ex->B, l.fc_in, l.C, cap);
       partial = std::max(partial, static_cast<int64_t>(l.fc_splits) * ex->B * std::max(l.fc_in, l.C));
+      l.wgrad_splits = sn::fc_wgrad_splits(ex->B, l.fc_in, l.C, cap);
+      partial = std::max(partial, static_cast<int64_t>(l.wgrad_splits) * l.fc_in * l.C);
     }
   }
   if (ex->stem_layer >= 0) {
@@ -727,10 +729,11 @@ struct Compiler {
         float* part = ex->partial;
         float* red = ex->red;
         float* wt = ex->wt_scratch;
+        const int wsp = l.wgrad_splits;
         push([=] {
-          ck(sn::fc_wgrad(B, I, O, x, dy, dw, db, red, st), "fc_wgrad");
+          ck(sn::fc_wgrad(B, I, O, x, dy, dw, db, red, st, part, wsp), "fc_wgrad");
           if (dx) ck(sn::fc_dgrad(B, I, O, dy, w, dx, acc, part, sp, st, wt), "fc_dgrad");
-        }, dx ? 6 : 4);
+        }, sn::fc_bwd_launches(B, I, O, wsp, dx != nullptr));
         break;
       }
       case snp::BN: {

@@ -773,7 +773,12 @@ bool conv_tma_ok_dgrad(const ConvShape& s) {
   const bool kok = s.K % 32 == 0 || (s.R == 1 && s.S == 1 && s.K % 4 == 0);
   return s.stride == 1 && kok && s.H == s.P && s.W == s.Q && load_encoders();
 }
-bool conv_tma_ok_wgrad(const ConvShape& s) { return s.C % 32 == 0 && s.K % 32 == 0 && load_encoders(); }
+bool conv_tma_ok_wgrad(const ConvShape& s) {
+  // 1x1 with K % 32 != 0 (the FC): dy's last column box and the partial store
+  // run past K (zero fill / clipped)
+  const bool kok = s.K % 32 == 0 || (s.R == 1 && s.S == 1 && s.K % 4 == 0);
+  return s.C % 32 == 0 && kok && load_encoders();
+}
 
 cudaError_t conv_fwd_tma(const ConvShape& s, const float* x, const float* w, const float* bias, float* y,
                          float* stats, cudaStream_t st) {

@@ -604,8 +604,31 @@ cudaError_t fc_dgrad(int B, int I, int O, const float* dy, const float* w, float
   return splitk_reduce_impl(partial, eff, B, I, dx, nullptr, accumulate, 0, st);
 }
 
+int fc_bwd_launches(int B, int I, int O, int wsplits, bool dgrad) {
+  int n = 0;
+  const ConvShape cs = fc_as_conv(B, I, O);
+  if (wsplits > 0 && use_tma() && conv_tma_ok_wgrad(cs)) {
+    const int sp = effective_splits(B, wsplits);
+    const int64_t tiles = static_cast<int64_t>((O + 31) / 32) * ((I + 31) / 32);
+    n += 1 + ((sp >= 16 && tiles < 4 * 148) ? 2 : 1) + 2;  // wgrad, split-K reduction, bias (colred)
+  } else {
+    n += 1 + 2;  // tc_gemm wgrad, bias (colred)
+  }
+  if (dgrad) n += 2;  // transpose + TMA dgrad, or tc_gemm + reduction
+  return n;
+}
+
+int fc_wgrad_splits(int B, int I, int O, int64_t partial_floats_cap) {
+  const ConvShape cs = fc_as_conv(B, I, O);
+  return (use_tma() && conv_tma_ok_wgrad(cs)) ? conv_wgrad_splits(cs, partial_floats_cap) : 0;
+}
+
 cudaError_t fc_wgrad(int B, int I, int O, const float* x, const float* dy, float* dw, float* db, float* red_scratch,
-                     cudaStream_t st) {
+                     cudaStream_t st, float* partial, int splits) {
+  // as the weight gradient of the 1x1 convolution (TMA kernel, split-K over the batch)
+  const ConvShape cs = fc_as_conv(B, I, O);
+  if (partial && splits > 0 && use_tma() && conv_tma_ok_wgrad(cs))
+    return conv_wgrad(cs, x, dy, dw, db, partial, splits, red_scratch, st);
   // dw[o][i] = sum_b dy[b][o] x[b][i]: A[o][b] = dy (MN-major, ld O), B[i][b] = x (MN-major, ld I)
   EpiStore e{dw, nullptr, O, I, I, 0};
   MatMNLoader<kBM> la{};

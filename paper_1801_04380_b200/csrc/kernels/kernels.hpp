@@ -109,8 +109,12 @@ cudaError_t fc_fwd(int B, int I, int O, const float* x, const float* w, const fl
                    float* partial, int splits, cudaStream_t st);
 cudaError_t fc_dgrad(int B, int I, int O, const float* dy, const float* w, float* dx, int accumulate,
                      float* partial, int splits, cudaStream_t st, float* wt_scratch = nullptr);
+// fc_wgrad_splits: split count for fc_wgrad's TMA path (0: not applicable)
+int fc_wgrad_splits(int B, int I, int O, int64_t partial_floats_cap);
+int fc_bwd_launches(int B, int I, int O, int wsplits, bool dgrad);  // kernels fc_wgrad (+ fc_dgrad) issue
 cudaError_t fc_wgrad(int B, int I, int O, const float* x, const float* dy, float* dw, float* db,
-                     float* red_scratch, cudaStream_t st);
+                     float* red_scratch, cudaStream_t st, float* partial = nullptr,
+                     int splits = 0);
 
 // ---- memory-bound layer kernels (layers.cu) ------------------------------------
 // Per-channel column reductions over a [rows][C] matrix need a scratch of
