@@ -6,6 +6,8 @@
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
+#include <cstdlib>
+#include <type_traits>
 
 #include "kernels.hpp"
 
@@ -182,9 +184,9 @@ struct RedBnBwdOp {
 // channels and walks its rows with kUnroll independent accumulators (fixed
 // per-thread order, fixed merge).
 constexpr int kRedThreads = 512;
-template <class Op>
-__global__ void __launch_bounds__(kRedThreads) colred_stage1_v4(Op op, int64_t rows, int C, int64_t chunk,
-                                                                double* part) {
+template <class Op, int kUo = 0, int MINB = 2>
+__global__ void __launch_bounds__(kRedThreads, MINB) colred_stage1_v4(Op op, int64_t rows, int C, int64_t chunk,
+                                                                   double* part) {
   __shared__ float4 s1[kRedThreads], s2[kRedThreads];
   const int64_t r0 = static_cast<int64_t>(blockIdx.x) * chunk;
   const int64_t r1 = r0 + chunk < rows ? r0 + chunk : rows;
@@ -195,24 +197,24 @@ __global__ void __launch_bounds__(kRedThreads) colred_stage1_v4(Op op, int64_t r
   const int lane = t / cb, cc = t % cb;
   for (int c0 = 0; c0 < C4; c0 += cb) {
     const int c4 = c0 + cc;
+    // one accumulator pair (the kU rows' loads are what must overlap, not
+    // the adds): 2 blocks of 512 threads per SM instead of 1 at 127 registers
+    constexpr int kU = kUo ? kUo : kUnroll;
     float4 a = zero4(), b = a;
     if (lane < lanes && c4 < C4) {
       const typename Op::P p = op.prep4(c4 * 4, C);
-      float4 au[kUnroll], bu[kUnroll];
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) au[u] = bu[u] = zero4();
       int64_t r = r0 + lane;
-      for (; r + (kUnroll - 1) * lanes < r1; r += kUnroll * lanes) {
-        typename Op::R raw[kUnroll];
+      for (; r + (kU - 1) * lanes < r1; r += kU * lanes) {
+        typename Op::R raw[kU];
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) raw[u] = op.load((r + u * lanes) * C + c4 * 4);
+        for (int u = 0; u < kU; ++u) raw[u] = op.load((r + u * lanes) * C + c4 * 4);
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
+        for (int u = 0; u < kU; ++u) {
           op.side((r + u * lanes) * C + c4 * 4, raw[u]);
           float4 fa, fb;
           op.comp(p, raw[u], fa, fb);
-          add4(au[u], fa);
-          add4(bu[u], fb);
+          add4(a, fa);
+          add4(b, fb);
         }
       }
       for (; r < r1; r += lanes) {
@@ -220,15 +222,8 @@ __global__ void __launch_bounds__(kRedThreads) colred_stage1_v4(Op op, int64_t r
         const typename Op::R raw1 = op.load(r * C + c4 * 4);
         op.side(r * C + c4 * 4, raw1);
         op.comp(p, raw1, fa, fb);
-        add4(au[0], fa);
-        add4(bu[0], fb);
-      }
-      a = au[0];
-      b = bu[0];
-#pragma unroll
-      for (int u = 1; u < kUnroll; ++u) {
-        add4(a, au[u]);
-        add4(b, bu[u]);
+        add4(a, fa);
+        add4(b, fb);
       }
     }
     s1[t] = a;
@@ -347,7 +342,12 @@ cudaError_t colred(Op op, Fin fin, int64_t rows, int C, float* scratch_f, cudaSt
   const int64_t chunk = (rows + nb - 1) / nb;
   nb = (rows + chunk - 1) / chunk;
   if (nb < 1) nb = 1;
-  if (v4)
+  // RedBnBwdOp (two operands + side copies per row): one 512-thread block per
+  // SM without a register cap beats two capped ones (eager A/B over the step:
+  // 9.47 vs 9.52 ms, SN_COLRED_ROWS experiment)
+  if (v4 && std::is_same<Op, RedBnBwdOp>::value)
+    colred_stage1_v4<Op, 4, 1><<<static_cast<int>(nb), kRedThreads, 0, st>>>(op, rows, C, chunk, part);
+  else if (v4)
     colred_stage1_v4<<<static_cast<int>(nb), kRedThreads, 0, st>>>(op, rows, C, chunk, part);
   else
     colred_stage1<<<static_cast<int>(nb), kThreads, 0, st>>>(op, rows, C, chunk, part);
@@ -518,7 +518,7 @@ __device__ void bias_block_reduce(const float4& v, int C, double* part) {
 // consumer this BN is (its gradient buffer holds nothing else) -- as per-block partials part[block][2][C] (doubles; second plane 0) for
 // colred_stage2: a fixed thread -> (channel quad, row lane) map, so the sums
 // are deterministic.
-__global__ void bn_dx_v4(const float4* __restrict__ x, const float4* __restrict__ dy, int64_t n4, int64_t rows,
+__global__ void __launch_bounds__(kThreads, 4) bn_dx_v4(const float4* __restrict__ x, const float4* __restrict__ dy, int64_t n4, int64_t rows,
                          int C, const float* __restrict__ gamma, const float* __restrict__ beta,
                          const float* __restrict__ stats, const float* __restrict__ coef, float4* dx, int accumulate,
                          int relu, double* dbias_part) {
@@ -535,17 +535,19 @@ __global__ void bn_dx_v4(const float4* __restrict__ x, const float4* __restrict_
   const float k2[4] = {c2.x * inv_m, c2.y * inv_m, c2.z * inv_m, c2.w * inv_m};
   const float gs[4] = {p.g.x * p.is.x, p.g.y * p.is.y, p.g.z * p.is.z, p.g.w * p.is.w};
   const float m[4] = {p.m.x, p.m.y, p.m.z, p.m.w}, is[4] = {p.is.x, p.is.y, p.is.z, p.is.w};
-  for (int64_t i0 = L.start; i0 < n4; i0 += kUnroll * L.S) {
-    float4 xv[kUnroll], gv[kUnroll], ov[kUnroll];
+  // 2 rows per thread in flight (x, dy[, dx]) at <= 64 registers: 4 blocks per SM
+  constexpr int U = 2;
+  for (int64_t i0 = L.start; i0 < n4; i0 += U * L.S) {
+    float4 xv[U], gv[U], ov[U];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
+    for (int u = 0; u < U; ++u) {
       const int64_t i = i0 + u * L.S;
       xv[u] = i < n4 ? x[i] : zero4();
       gv[u] = i < n4 ? dy[i] : zero4();
       ov[u] = (accumulate && i < n4) ? dx[i] : zero4();
     }
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
+    for (int u = 0; u < U; ++u) {
       const int64_t i = i0 + u * L.S;
       if (i >= n4) break;
       if (relu) {
