@@ -283,26 +283,31 @@ __global__ void colred_stage1(Op op, int64_t rows, int C, int64_t chunk, double*
   }
 }
 
-// Stage 2: 32 channels per block (lane = channel); the 32 warps take
-// interleaved stage-1 blocks (4 loads in flight per operand), then the warp
-// sums are combined in warp order -- a fixed order, so the result is
-// deterministic -- and handed to the finaliser (no extra launch).
+// Stage 2: 8 channels per block x 128 partial lanes (thread = channel + 8 *
+// lane, so a warp reads 4 stage-1 rows x 8 adjacent channels); each lane sums
+// stage-1 blocks lane, lane + 128, ... (4 loads in flight per operand), then
+// the lanes are combined 8 at a time and the 16 group sums in order -- a fixed
+// order, so the result is deterministic -- and handed to the finaliser.  More
+// blocks and shorter chains than one block per 32 channels (C = 64 ran on 2 SMs).
 constexpr int kStage2Threads = 1024;
+constexpr int kStage2Chan = 8, kStage2Lanes = kStage2Threads / kStage2Chan;
+inline int stage2_blocks(int C) { return (C + kStage2Chan - 1) / kStage2Chan; }
 template <class Fin>
 __global__ void __launch_bounds__(kStage2Threads) colred_stage2(const double* __restrict__ part, int nblocks, int C,
                                                                 Fin fin) {
-  __shared__ double sa[32][33], sb[32][33];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int c = blockIdx.x * 32 + lane;
+  __shared__ double sa[kStage2Lanes][kStage2Chan], sb[kStage2Lanes][kStage2Chan];
+  __shared__ double ga[16][kStage2Chan], gb[16][kStage2Chan];
+  const int cl = threadIdx.x % kStage2Chan, pl = threadIdx.x / kStage2Chan;
+  const int c = blockIdx.x * kStage2Chan + cl;
   double A = 0.0, B = 0.0;
   if (c < C) {
-    int b = w;
-    for (; b + 3 * 32 < nblocks; b += 4 * 32) {
+    int b = pl;
+    for (; b + 3 * kStage2Lanes < nblocks; b += 4 * kStage2Lanes) {
       double va[4], vb[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        va[u] = part[(static_cast<size_t>(b + 32 * u) * 2) * C + c];
-        vb[u] = part[(static_cast<size_t>(b + 32 * u) * 2 + 1) * C + c];
+        va[u] = part[(static_cast<size_t>(b + kStage2Lanes * u) * 2) * C + c];
+        vb[u] = part[(static_cast<size_t>(b + kStage2Lanes * u) * 2 + 1) * C + c];
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
@@ -310,19 +315,29 @@ __global__ void __launch_bounds__(kStage2Threads) colred_stage2(const double* __
         B += vb[u];
       }
     }
-    for (; b < nblocks; b += 32) {
+    for (; b < nblocks; b += kStage2Lanes) {
       A += part[(static_cast<size_t>(b) * 2) * C + c];
       B += part[(static_cast<size_t>(b) * 2 + 1) * C + c];
     }
   }
-  sa[w][lane] = A;
-  sb[w][lane] = B;
+  sa[pl][cl] = A;
+  sb[pl][cl] = B;
   __syncthreads();
-  if (w == 0 && c < C) {
+  if (pl < 16) {
     double a = 0.0, b = 0.0;
-    for (int i = 0; i < 32; ++i) {
-      a += sa[i][lane];
-      b += sb[i][lane];
+    for (int i = 0; i < kStage2Lanes / 16; ++i) {
+      a += sa[pl * (kStage2Lanes / 16) + i][cl];
+      b += sb[pl * (kStage2Lanes / 16) + i][cl];
+    }
+    ga[pl][cl] = a;
+    gb[pl][cl] = b;
+  }
+  __syncthreads();
+  if (pl == 0 && c < C) {
+    double a = 0.0, b = 0.0;
+    for (int i = 0; i < 16; ++i) {
+      a += ga[i][cl];
+      b += gb[i][cl];
     }
     fin(c, a, b);
   }
@@ -351,7 +366,7 @@ cudaError_t colred(Op op, Fin fin, int64_t rows, int C, float* scratch_f, cudaSt
     colred_stage1_v4<<<static_cast<int>(nb), kRedThreads, 0, st>>>(op, rows, C, chunk, part);
   else
     colred_stage1<<<static_cast<int>(nb), kThreads, 0, st>>>(op, rows, C, chunk, part);
-  colred_stage2<<<(C + 31) / 32, kStage2Threads, 0, st>>>(part, static_cast<int>(nb), C, fin);
+  colred_stage2<<<stage2_blocks(C), kStage2Threads, 0, st>>>(part, static_cast<int>(nb), C, fin);
   return cudaGetLastError();
 }
 
@@ -1597,7 +1612,7 @@ cudaError_t bn_stats_from_tiles(const float* tiles, int ntiles, int tile_rows, c
   const int chunk = (ntiles + nb - 1) / nb;
   nb = (ntiles + chunk - 1) / chunk;
   tile_stats_stage1<<<dim3(nb, cgroups), kThreads, 0, st>>>(tiles, ntiles, tile_rows, rows, C, x, chunk, part);
-  colred_stage2<<<(C + 31) / 32, kStage2Threads, 0, st>>>(part, nb, C,
+  colred_stage2<<<stage2_blocks(C), kStage2Threads, 0, st>>>(part, nb, C,
                                                           BnStatsFin{x, rows, C, eps, momentum, stats, running});
   return cudaGetLastError();
 }
@@ -1644,7 +1659,7 @@ cudaError_t bn_bwd(const float* x, const float* dy, int64_t rows, int C, const f
       bn_dx_v4<<<nb, kThreads, 0, st>>>(reinterpret_cast<const float4*>(x), reinterpret_cast<const float4*>(dy),
                                         n / 4, rows, C, gamma, beta, stats, coef, reinterpret_cast<float4*>(dx),
                                         accumulate, relu, part);
-      if (dbias) colred_stage2<<<(C + 31) / 32, kStage2Threads, 0, st>>>(part, nb, C, BiasFin{dbias});
+      if (dbias) colred_stage2<<<stage2_blocks(C), kStage2Threads, 0, st>>>(part, nb, C, BiasFin{dbias});
     } else {
       bn_dx_scalar<<<blocks_for(n), kThreads, 0, st>>>(x, dy, n, rows, C, gamma, beta, stats, coef, dx, accumulate,
                                                        relu);
