@@ -310,7 +310,9 @@ def run_ours(args) -> None:
                    "baseline_peak_bytes_features_none": rep.baseline_peak_bytes,
                    "offload_d2h_bytes_per_step_issued": int(t.d2h_bytes),
                    "offload_scheduled_bytes_per_step_planned": rep.scheduled_transfer_bytes,
-                   "replays_per_step": rep.extra_forward_steps},
+                   "replays_per_step": rep.extra_forward_steps,
+                   "conv_wgrad_partials_in_planned_workspace": "%d of %d" % (
+                       ex.workspace_use()[0], sum(ex.workspace_use()))},
         "clocks": clocks.summary(),
         "losses": [round(l, 5) for l in losses[:3]] + [round(losses[-1], 5)],
     }

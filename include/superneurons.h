@@ -269,6 +269,10 @@ int sn_exec_profile(sn_exec* ex, float* action_ms, int32_t* action_layer, int32_
                     size_t* n);
 /* Launch the SGD update alone (after an external gradient all-reduce). */
 int sn_exec_apply_update(sn_exec* ex, float lr, float grad_scale);
+/* CONV weight gradients whose split-K partials live in the conv workspace the
+ * plan granted their step (reference simulator.py:624-654, the dynamic
+ * workspace) vs in executor scratch outside the pool (workspace too small). */
+int sn_exec_workspace_use(const sn_exec* ex, int32_t* wgrad_in_pool, int32_t* wgrad_outside);
 /* Stream the executor launches on (for cross-library ordering). */
 void* sn_exec_stream(sn_exec* ex);
 

@@ -121,6 +121,7 @@ struct sn_exec {
   // s3: weight gradients (off the backward critical path) run on a side
   // stream, overlapping the next layers' backward; their own scratch buffers
   cudaStream_t s3 = nullptr;
+  int wgrad_ws_in_pool = 0, wgrad_ws_outside = 0;  // CONV weight gradients: partials in the granted workspace or not
   float* partial_w = nullptr;
   float* red_w = nullptr;
   float* wt_w = nullptr;
@@ -684,7 +685,6 @@ struct Compiler {
         float* wt = ex->wt_scratch;
         float* part = ex->partial;
         float* red = ex->red;
-        const int sp = l.wgrad_splits;
         if (conv_bias_done[lid]) db = nullptr;  // summed by the BN backward's dx pass
         const int nbias = db ? 2 : 0;
         // weight gradient on the side stream s3 (after everything s0 has issued so
@@ -697,6 +697,32 @@ struct Compiler {
         used_s3 = true;
         side_reads[snp::key_code(snp::K_ACT, pid)] = wdone;
         side_reads[snp::key_code(snp::K_GRAD, owner)] = wdone;
+        // The split-K partials go to the conv workspace the planner granted this
+        // step (the selected algorithm's factor x output bytes, sized from the
+        // free pool) when they fit; else to the executor's scratch outside the
+        // pool.  The split count itself stays fixed per layer: it sets the
+        // summation order, and the gradients must be bit-identical under every
+        // feature set / schedule.
+        const int sp = l.wgrad_splits;
+        {
+          const snp::Event& bev = P.tape[cur_ti];
+          float* ws = nullptr;
+          int64_t ws_floats = 0;
+          const int64_t wkey = snp::key_code(snp::K_WS, bev.d);
+          if (bev.d >= 0 && where.count(wkey)) {
+            ws = ptr(snp::K_WS, static_cast<int>(bev.d));
+            ws_floats = where[wkey].second * snp::kBlockBytes / static_cast<int64_t>(sizeof(float));
+          }
+          const int64_t slice = static_cast<int64_t>(cs.R) * cs.S * cs.C * cs.K;
+          const int64_t need = lid == ex->stem_layer ? sn::stem_wgrad_partial_floats(cs) : sp * slice;
+          if (ws && ws_floats >= need) {
+            part_w = ws;
+            side_reads[wkey] = wdone;  // written on s3 after the tape frees it
+            ++ex->wgrad_ws_in_pool;
+          } else {
+            ++ex->wgrad_ws_outside;
+          }
+        }
         if (lid == ex->stem_layer) {  // DATA has no gradient
           push([=] {
             ck(cudaEventRecord(ready, st), "record");
@@ -1602,6 +1628,13 @@ int sn_exec_profile(sn_exec* ex, float* action_ms, int32_t* action_layer, int32_
     }
     for (auto& e : ev) cudaEventDestroy(e);
   });
+}
+
+int sn_exec_workspace_use(const sn_exec* ex, int32_t* wgrad_in_pool, int32_t* wgrad_outside) {
+  if (!ex) return xset(SN_EK_INTERNAL, "null argument");
+  if (wgrad_in_pool) *wgrad_in_pool = ex->wgrad_ws_in_pool;
+  if (wgrad_outside) *wgrad_outside = ex->wgrad_ws_outside;
+  return SN_OK;
 }
 
 int sn_exec_apply_update(sn_exec* ex, float lr, float grad_scale) {

@@ -506,6 +506,12 @@ cudaError_t conv_dgrad(const ConvShape& s, const float* dy, const float* w, floa
   }
 }
 
+bool conv_wgrad_splits_fixed(const ConvShape& s) {
+  return use_tma() && s.stride == 1 &&
+         (conv_halo_wgrad128_ok(s.N, s.H, s.W, s.C, s.K, s.R, s.S, s.pad, s.P, s.Q) ||
+          conv_halo_wgrad_ok(s.N, s.H, s.W, s.C, s.K, s.R, s.S, s.pad, s.P, s.Q));
+}
+
 int conv_wgrad_splits(const ConvShape& s, int64_t partial_floats_cap) {
   // the halo weight-gradient kernels write one partial slice per CTA (per job)
   if (use_tma() && s.stride == 1 && conv_halo_wgrad128_ok(s.N, s.H, s.W, s.C, s.K, s.R, s.S, s.pad, s.P, s.Q))

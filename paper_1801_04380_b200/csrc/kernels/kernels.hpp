@@ -29,6 +29,9 @@ cudaError_t conv_dgrad(const ConvShape& s, const float* dy, const float* w, floa
                        int accumulate, cudaStream_t st);
 // dw[K][R*S*C] = sum_pixels im2col(x)^T dy ; db[K] = column sums of dy (skipped if db is null).
 // partial: scratch of splits*R*S*C*K floats (see conv_wgrad_splits).
+// the halo weight-gradient kernels: their partial-slice count is fixed by the
+// kernel (one per CTA or job), the im2col kernel's split count is free
+bool conv_wgrad_splits_fixed(const ConvShape& s);
 int conv_wgrad_splits(const ConvShape& s, int64_t partial_floats_cap);
 cudaError_t conv_wgrad(const ConvShape& s, const float* x, const float* dy, float* dw, float* db,
                        float* partial, int splits, float* red_scratch, cudaStream_t st);

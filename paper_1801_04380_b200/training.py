@@ -150,6 +150,7 @@ def _xlib():
                                                   C.c_int32, P(C.c_float), P(TimingC)]
         L.sn_exec_read_tensor.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int64]
         L.sn_exec_apply_update.argtypes = [C.c_void_p, C.c_float, C.c_float]
+        L.sn_exec_workspace_use.argtypes = [C.c_void_p, P(C.c_int32), P(C.c_int32)]
         L.sn_exec_profile.argtypes = [C.c_void_p, P(C.c_float), P(C.c_int32), P(C.c_int32), C.c_size_t,
                                       P(C.c_size_t)]
         L.sn_exec_stream.argtypes = [C.c_void_p]
@@ -302,6 +303,14 @@ class Executor:
             nxt = batches[i + 1] if i + 1 < len(batches) else (None, None)
             out.append(self.step_host_pipelined(img, lab, nxt[0], nxt[1], update))
         return out
+
+    def workspace_use(self) -> tuple[int, int]:
+        """(CONV weight gradients with their split-K partials in the planned conv
+        workspace, ones that needed scratch outside the pool)."""
+        a, b = C.c_int32(), C.c_int32()
+        if self.L.sn_exec_workspace_use(self.ptr, C.byref(a), C.byref(b)) != 0:
+            _raise_exec(self.L)
+        return a.value, b.value
 
     def read_activation(self, lid: int):
         """Layer output still resident at the end of the iteration, as (B, C, H, W)

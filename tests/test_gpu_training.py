@@ -355,3 +355,25 @@ def test_pipelined_host_steps_match_serial_host_steps(cuda, alex32_case):
         ex.close()
     assert runs[0][0] == runs[1][0]
     assert _bitwise(runs[0][1], runs[1][1])
+
+
+def test_wgrad_partials_use_the_planned_workspace(cuda, alex32_case):
+    """With convselect the planner grants each CONV step a workspace (factor x
+    output bytes from the free pool); the weight-gradient split-K partials live
+    there, inside the pool, whenever they fit -- and the gradients stay
+    bit-identical to a run without workspaces (the split count is per layer)."""
+    sn = _sn()
+    from paper_1801_04380_b200.training import Executor
+    net, params, images, labels = alex32_case
+    uses, grads = [], []
+    for feats in ("liveness", "liveness,convselect"):
+        cfg = sn.SimConfig(pool_bytes=1 << 30, features=sn.parse_features(feats), cost=sn.CostConfig(batch=16))
+        ex = Executor(net, cfg, params=params)
+        ex.set_inputs(images, labels)
+        ex.step(update=False)
+        uses.append(ex.workspace_use())
+        grads.append(ex.get("grads"))
+        ex.close()
+    n_conv = sum(1 for l in net.layers if l.kind.name == "CONV")
+    assert sum(uses[1]) == n_conv and uses[1][0] >= 1, uses
+    assert _bitwise(grads[0], grads[1])
