@@ -304,6 +304,9 @@ def run_ours(args) -> None:
                 "serial_step_host_images_per_s": round(B * world / (serial_ms / 1e3), 2),
                 "serial_wall_images_per_s": round(B * world * e_steps / serial_wall, 2)},
         "gpu_launches": int(kernels),
+        "transfers": dict(ex.transfer_stats(),
+                          note="last iteration: offload copy-outs / fetches the tape issued (elided backups "
+                               "excluded), copy-engine GB/s, compute-stream time blocked on fetches"),
         "memory": {"peak_bytes": rep.peak_bytes, "min_pool_bytes_max_i_l_i": rep.min_pool_bytes,
                    "peak_over_floor": round(rep.peak_bytes / rep.min_pool_bytes, 4),
                    "pool_high_water_bytes": rep.pool_high_water_bytes,

@@ -273,6 +273,12 @@ int sn_exec_apply_update(sn_exec* ex, float lr, float grad_scale);
  * plan granted their step (reference simulator.py:624-654, the dynamic
  * workspace) vs in executor scratch outside the pool (workspace too small). */
 int sn_exec_workspace_use(const sn_exec* ex, int32_t* wgrad_in_pool, int32_t* wgrad_outside);
+/* Transfers of the last iteration (offload copy-outs and fetches the tape
+ * issued, reference simulator.py:378-413): bytes and copy-engine busy time per
+ * direction, and the time the compute stream stood blocked on fetches (the
+ * exposed, non-overlapped transfer time).  Synchronises the compute stream. */
+int sn_exec_transfer_stats(sn_exec* ex, int64_t* d2h_bytes, double* d2h_ms, int64_t* h2d_bytes, double* h2d_ms,
+                           double* exposed_ms);
 /* Stream the executor launches on (for cross-library ordering). */
 void* sn_exec_stream(sn_exec* ex);
 

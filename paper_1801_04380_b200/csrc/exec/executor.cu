@@ -149,6 +149,24 @@ struct sn_exec {
     events.push_back(e);
     return e;
   }
+  // Transfer evidence (sn_exec_transfer_stats): timing events around every
+  // issued copy on its copy stream, and around every compute-stream wait for
+  // a fetch (the exposed, non-overlapped part of a transfer).
+  struct Timer {
+    cudaEvent_t a, b;
+    int64_t bytes;
+    int kind;  // 0 D2H copy-out, 1 H2D fetch, 2 compute stream blocked on a fetch
+  };
+  std::vector<Timer> timers;
+  Timer& new_timer(int kind, int64_t bytes) {
+    Timer t{nullptr, nullptr, bytes, kind};
+    ck(cudaEventCreate(&t.a), "cudaEventCreate");
+    ck(cudaEventCreate(&t.b), "cudaEventCreate");
+    events.push_back(t.a);
+    events.push_back(t.b);
+    timers.push_back(t);
+    return timers.back();
+  }
 };
 
 namespace {
@@ -417,7 +435,13 @@ struct Compiler {
   void wait_fetch(int lid) {
     auto it = h2d_live.find(lid);
     if (it != h2d_live.end()) {
+      // exposed transfer time: from when the compute stream reaches the wait
+      // to when the fetch has landed
+      const sn_exec::Timer tm = ex->new_timer(2, P.costs[lid].device_bytes);
+      cudaStream_t s0 = ex->s0;
+      push([=] { ck(cudaEventRecordWithFlags(tm.a, s0, cudaEventRecordExternal), "record"); }, 0);
       s0_wait(it->second);
+      push([=] { ck(cudaEventRecordWithFlags(tm.b, s0, cudaEventRecordExternal), "record"); }, 0);
       h2d_live.erase(it);
     }
   }
@@ -466,10 +490,13 @@ struct Compiler {
     const float* src = ptr(snp::K_ACT, lid);
     cudaEvent_t prod = ex->new_event(), done = ex->new_event();
     cudaStream_t s0 = ex->s0, s1 = ex->s1;
+    const sn_exec::Timer tm = ex->new_timer(0, nbytes);
     push([=] {
       ck(cudaEventRecord(prod, s0), "record");
       ck(cudaStreamWaitEvent(s1, prod, 0), "wait");
+      ck(cudaEventRecordWithFlags(tm.a, s1, cudaEventRecordExternal), "record");
       ck(cudaMemcpyAsync(host, src, static_cast<size_t>(nbytes), cudaMemcpyDeviceToHost, s1), "D2H");
+      ck(cudaEventRecordWithFlags(tm.b, s1, cudaEventRecordExternal), "record");
       ck(cudaEventRecord(done, s1), "record");
     }, 0);
     d2h_live[lid] = done;
@@ -485,11 +512,14 @@ struct Compiler {
     float* dst = ptr(snp::K_ACT, lid);
     cudaEvent_t before = ex->new_event(), done = ex->new_event(), out = d->second;
     cudaStream_t s0 = ex->s0, s2 = ex->s2;
+    const sn_exec::Timer tm = ex->new_timer(1, nbytes);
     push([=] {
       ck(cudaEventRecord(before, s0), "record");
       ck(cudaStreamWaitEvent(s2, before, 0), "wait");
       ck(cudaStreamWaitEvent(s2, out, 0), "wait");
+      ck(cudaEventRecordWithFlags(tm.a, s2, cudaEventRecordExternal), "record");
       ck(cudaMemcpyAsync(dst, host, static_cast<size_t>(nbytes), cudaMemcpyHostToDevice, s2), "H2D");
+      ck(cudaEventRecordWithFlags(tm.b, s2, cudaEventRecordExternal), "record");
       ck(cudaEventRecord(done, s2), "record");
     }, 0);
     h2d_live[lid] = done;
@@ -1627,6 +1657,28 @@ int sn_exec_profile(sn_exec* ex, float* action_ms, int32_t* action_layer, int32_
       if (action_type) action_type[i] = ex->prog[i].type;
     }
     for (auto& e : ev) cudaEventDestroy(e);
+  });
+}
+
+int sn_exec_transfer_stats(sn_exec* ex, int64_t* d2h_bytes, double* d2h_ms, int64_t* h2d_bytes, double* h2d_ms,
+                           double* exposed_ms) {
+  if (!ex) return xset(SN_EK_INTERNAL, "null argument");
+  return xguard([&] {
+    ck(cudaSetDevice(ex->device), "cudaSetDevice");
+    ck(cudaStreamSynchronize(ex->s0), "sync");
+    int64_t bytes[3] = {0, 0, 0};
+    double ms[3] = {0, 0, 0};
+    for (const auto& t : ex->timers) {
+      float m = 0.f;
+      ck(cudaEventElapsedTime(&m, t.a, t.b), "elapsed");
+      bytes[t.kind] += t.bytes;
+      ms[t.kind] += m;
+    }
+    if (d2h_bytes) *d2h_bytes = bytes[0];
+    if (d2h_ms) *d2h_ms = ms[0];
+    if (h2d_bytes) *h2d_bytes = bytes[1];
+    if (h2d_ms) *h2d_ms = ms[1];
+    if (exposed_ms) *exposed_ms = ms[2];
   });
 }
 

@@ -151,6 +151,8 @@ def _xlib():
         L.sn_exec_read_tensor.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int64]
         L.sn_exec_apply_update.argtypes = [C.c_void_p, C.c_float, C.c_float]
         L.sn_exec_workspace_use.argtypes = [C.c_void_p, P(C.c_int32), P(C.c_int32)]
+        L.sn_exec_transfer_stats.argtypes = [C.c_void_p, P(C.c_int64), P(C.c_double), P(C.c_int64),
+                                             P(C.c_double), P(C.c_double)]
         L.sn_exec_profile.argtypes = [C.c_void_p, P(C.c_float), P(C.c_int32), P(C.c_int32), C.c_size_t,
                                       P(C.c_size_t)]
         L.sn_exec_stream.argtypes = [C.c_void_p]
@@ -311,6 +313,19 @@ class Executor:
         if self.L.sn_exec_workspace_use(self.ptr, C.byref(a), C.byref(b)) != 0:
             _raise_exec(self.L)
         return a.value, b.value
+
+    def transfer_stats(self) -> dict:
+        """PCIe evidence of the last iteration: bytes, copy-engine ms and GB/s per
+        direction, and the ms the compute stream was blocked on fetches."""
+        db, hb = C.c_int64(), C.c_int64()
+        dm, hm, xm = C.c_double(), C.c_double(), C.c_double()
+        if self.L.sn_exec_transfer_stats(self.ptr, C.byref(db), C.byref(dm), C.byref(hb), C.byref(hm),
+                                         C.byref(xm)) != 0:
+            _raise_exec(self.L)
+        gbs = lambda b, m: round(b / (m * 1e6), 2) if m > 0 else None  # noqa: E731
+        return {"d2h_bytes": db.value, "d2h_ms": round(dm.value, 4), "d2h_GBps": gbs(db.value, dm.value),
+                "h2d_bytes": hb.value, "h2d_ms": round(hm.value, 4), "h2d_GBps": gbs(hb.value, hm.value),
+                "exposed_ms": round(xm.value, 4)}
 
     def read_activation(self, lid: int):
         """Layer output still resident at the end of the iteration, as (B, C, H, W)
