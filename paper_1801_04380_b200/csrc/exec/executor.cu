@@ -904,6 +904,27 @@ struct Compiler {
             break;
           }
         }
+        if (pv.size() > 2 && n % 4 == 0) {
+          std::vector<int> owners;
+          for (int p : pv) owners.push_back(net.grad_owner(p));
+          std::vector<int> sorted = owners;
+          std::sort(sorted.begin(), sorted.end());
+          if (std::adjacent_find(sorted.begin(), sorted.end()) == sorted.end()) {  // distinct buffers
+            std::vector<float*> dsts;
+            std::vector<int> accs;
+            for (int p : pv) {
+              int acc = 0;
+              float* dx = dx_target(p, &acc);
+              if (!dx) continue;
+              dsts.push_back(dx);
+              accs.push_back(acc);
+            }
+            const int k = static_cast<int>(dsts.size());
+            if (k) push([=] { ck(sn::grad_copy_multi(dy, dsts.data(), accs.data(), k, n, st), "join_bwd_k"); },
+                        sn::grad_copy_multi_launches(k));
+            break;
+          }
+        }
         for (int p : pv) {
           int acc = 0;
           float* dx = dx_target(p, &acc);

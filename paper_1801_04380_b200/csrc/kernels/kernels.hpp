@@ -215,6 +215,9 @@ cudaError_t loss_reduce(const float* loss_rows, int B, float* loss, cudaStream_t
 cudaError_t join_fwd(const float* const* inputs, int n_in, float* y, int64_t n, cudaStream_t st);
 // dst (+)= src
 cudaError_t grad_copy(const float* src, float* dst, int64_t n, int accumulate, cudaStream_t st);
+// k-way JOIN backward in ceil(k/8) passes over dy (n % 4 == 0; destinations distinct)
+int grad_copy_multi_launches(int k);
+cudaError_t grad_copy_multi(const float* src, float* const* dsts, const int* accs, int k, int64_t n, cudaStream_t st);
 
 cudaError_t sgd_update(float* params, const float* grads, int64_t n, float lr, float grad_scale,
                        cudaStream_t st);

@@ -1874,6 +1874,56 @@ cudaError_t join_fwd(const float* const* inputs, int n_in, float* y, int64_t n, 
   return cudaGetLastError();
 }
 
+namespace {
+// k-way JOIN backward: one read of dy, every destination written (or added,
+// old + dy as grad_copy does) in the same pass
+constexpr int kMultiDst = 8;
+struct MultiDst {
+  float4* d[kMultiDst];
+  int acc[kMultiDst];
+  int k;
+};
+__global__ void grad_copy_multi_kernel(const float4* __restrict__ src, MultiDst md, int64_t n4) {
+  const int64_t T = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i0 < n4; i0 += 2 * T) {
+    float4 v[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) v[u] = i0 + u * T < n4 ? src[i0 + u * T] : zero4();
+    for (int t = 0; t < md.k; ++t) {
+      float4* d = md.d[t];
+      float4 o[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) o[u] = (md.acc[t] && i0 + u * T < n4) ? d[i0 + u * T] : zero4();
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (i0 + u * T >= n4) continue;
+        float4 w = v[u];
+        if (md.acc[t]) add4(w, o[u]);
+        d[i0 + u * T] = w;
+      }
+    }
+  }
+}
+}  // namespace
+
+int grad_copy_multi_launches(int k) { return (k + kMultiDst - 1) / kMultiDst; }
+
+cudaError_t grad_copy_multi(const float* src, float* const* dsts, const int* accs, int k, int64_t n, cudaStream_t st) {
+  if (n % 4 != 0) return cudaErrorInvalidValue;
+  for (int t0 = 0; t0 < k; t0 += kMultiDst) {
+    MultiDst md{};
+    md.k = std::min(kMultiDst, k - t0);
+    for (int t = 0; t < md.k; ++t) {
+      md.d[t] = reinterpret_cast<float4*>(dsts[t0 + t]);
+      md.acc[t] = accs[t0 + t];
+    }
+    grad_copy_multi_kernel<<<elt_blocks(n / 4), kThreads, 0, st>>>(reinterpret_cast<const float4*>(src), md, n / 4);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 cudaError_t grad_copy(const float* src, float* dst, int64_t n, int accumulate, cudaStream_t st) {
   grad_copy_kernel<<<elt_blocks(n / 4 + 1), kThreads, 0, st>>>(src, dst, n, accumulate);
   return cudaGetLastError();
