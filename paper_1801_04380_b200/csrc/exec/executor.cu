@@ -1057,25 +1057,38 @@ struct Compiler {
     }
     std::vector<int> act_fwd(net.n, 0), act_fwd_fused(net.n, 0), bn_fwd(net.n, 0), bn_fwd_fused(net.n, 0);
     std::vector<char> act_bwd_fused(net.n, 0);
+    // BN replays the reference schedules between the ReLU backward and the BN
+    // backward (for BACKWARD_NEEDS the fused backward does not have): dead
+    std::vector<char> pre_bwd_replay(T, 0);
     for (size_t i = 0; i < T; ++i) {
       const snp::Event& e = P.tape[i];
       if (e.op == 'C' || e.op == 'R') {
         if (net.kind[e.b] == snp::ACT) {
           ++act_fwd[e.b];
           act_fwd_fused[e.b] += fused_into[i] >= 0;
-        } else if (net.kind[e.b] == snp::BN) {
+        } else if (net.kind[e.b] == snp::BN && !pre_bwd_replay[i]) {
           ++bn_fwd[e.b];
           bn_fwd_fused[e.b] += fuse_at[i];
         }
       }
       if (e.op != 'B' || !bn_relu_pair(e.b)) continue;
       const int bn = net.prev[e.b][0];
+      std::vector<size_t> bn_replays;
       for (size_t j = i + 1; j < T; ++j) {
-        if (!is_compute(P.tape[j].op)) continue;
-        if (P.tape[j].op == 'B' && P.tape[j].b == bn) {
+        const snp::Event& f = P.tape[j];
+        if (!is_compute(f.op)) continue;
+        if (f.op == 'R' && f.b == bn && !fuse_at[j]) {  // recomputes the BN output nobody reads now
+          bn_replays.push_back(j);
+          continue;
+        }
+        if (f.op == 'B' && f.b == bn) {
           act_bwd_skip[i] = 1;
           bn_bwd_relu[j] = 1;
           act_bwd_fused[e.b] = 1;
+          for (size_t k : bn_replays) {
+            pre_bwd_replay[k] = 1;
+            dead_at[k] = 1;
+          }
         }
         break;
       }
