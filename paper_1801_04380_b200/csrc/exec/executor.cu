@@ -173,6 +173,16 @@ namespace {
 
 int64_t key_code(int kind, int64_t id) { return snp::key_code(kind, id); }
 
+// A timing event readable after the step: inside a graph capture the record
+// must be an external node (an internal one only orders the graph)
+cudaError_t record_timer(cudaEvent_t e, cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaError_t err = cudaStreamIsCapturing(st, &cs);
+  if (err != cudaSuccess) return err;
+  return cs == cudaStreamCaptureStatusActive ? cudaEventRecordWithFlags(e, st, cudaEventRecordExternal)
+                                             : cudaEventRecord(e, st);
+}
+
 void setup_layers(sn_exec* ex, const sn_layer_numerics* numerics) {
   const snp::Plan& P = ex->plan->plan;
   const Net& net = P.net;
@@ -439,9 +449,9 @@ struct Compiler {
       // to when the fetch has landed
       const sn_exec::Timer tm = ex->new_timer(2, P.costs[lid].device_bytes);
       cudaStream_t s0 = ex->s0;
-      push([=] { ck(cudaEventRecordWithFlags(tm.a, s0, cudaEventRecordExternal), "record"); }, 0);
+      push([=] { ck(record_timer(tm.a, s0), "record"); }, 0);
       s0_wait(it->second);
-      push([=] { ck(cudaEventRecordWithFlags(tm.b, s0, cudaEventRecordExternal), "record"); }, 0);
+      push([=] { ck(record_timer(tm.b, s0), "record"); }, 0);
       h2d_live.erase(it);
     }
   }
@@ -494,9 +504,9 @@ struct Compiler {
     push([=] {
       ck(cudaEventRecord(prod, s0), "record");
       ck(cudaStreamWaitEvent(s1, prod, 0), "wait");
-      ck(cudaEventRecordWithFlags(tm.a, s1, cudaEventRecordExternal), "record");
+      ck(record_timer(tm.a, s1), "record");
       ck(cudaMemcpyAsync(host, src, static_cast<size_t>(nbytes), cudaMemcpyDeviceToHost, s1), "D2H");
-      ck(cudaEventRecordWithFlags(tm.b, s1, cudaEventRecordExternal), "record");
+      ck(record_timer(tm.b, s1), "record");
       ck(cudaEventRecord(done, s1), "record");
     }, 0);
     d2h_live[lid] = done;
@@ -517,9 +527,9 @@ struct Compiler {
       ck(cudaEventRecord(before, s0), "record");
       ck(cudaStreamWaitEvent(s2, before, 0), "wait");
       ck(cudaStreamWaitEvent(s2, out, 0), "wait");
-      ck(cudaEventRecordWithFlags(tm.a, s2, cudaEventRecordExternal), "record");
+      ck(record_timer(tm.a, s2), "record");
       ck(cudaMemcpyAsync(dst, host, static_cast<size_t>(nbytes), cudaMemcpyHostToDevice, s2), "H2D");
-      ck(cudaEventRecordWithFlags(tm.b, s2, cudaEventRecordExternal), "record");
+      ck(record_timer(tm.b, s2), "record");
       ck(cudaEventRecord(done, s2), "record");
     }, 0);
     h2d_live[lid] = done;

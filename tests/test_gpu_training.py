@@ -377,3 +377,24 @@ def test_wgrad_partials_use_the_planned_workspace(cuda, alex32_case):
     n_conv = sum(1 for l in net.layers if l.kind.name == "CONV")
     assert sum(uses[1]) == n_conv and uses[1][0] >= 1, uses
     assert _bitwise(grads[0], grads[1])
+
+
+@pytest.mark.parametrize("graph", [True, False])
+def test_transfer_stats_eager_and_graph(cuda, graph):
+    """The copy-engine / exposed-fetch timers work in both execution modes
+    (graph: external event-record nodes; eager: plain records): AlexNet b250 in
+    a 1536 MiB cache pool fetches 477,024,000 bytes back on demand."""
+    sn = _sn()
+    from paper_1801_04380_b200.training import Executor, init_parameters
+    net = _fixture("alexnet")
+    params = init_parameters(net, seed=3, head_scale=0.1)
+    images, labels = _inputs(net, 250, seed=5)
+    cfg = sn.SimConfig(pool_bytes=1536 << 20, features=sn.parse_features("cache"), cost=sn.CostConfig(batch=250))
+    ex = Executor(net, cfg, params=params, use_graph=graph)
+    ex.set_inputs(images, labels)
+    ex.step(update=False)
+    ts = ex.transfer_stats()
+    ex.close()
+    assert ts["h2d_bytes"] >= 477024000 and ts["h2d_ms"] > 0 and ts["h2d_GBps"] > 1
+    assert ts["d2h_bytes"] > 0 and ts["d2h_ms"] > 0
+    assert ts["exposed_ms"] >= 0
