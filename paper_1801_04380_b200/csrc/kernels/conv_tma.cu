@@ -771,7 +771,11 @@ bool conv_tma_ok_dgrad(const ConvShape& s) {
   // a 1x1 filter may have K % 32 != 0 (the FC dgrad): the last channel chunk
   // reads past K, which both tensor maps zero-fill (one tap: no neighbour to hit)
   const bool kok = s.K % 32 == 0 || (s.R == 1 && s.S == 1 && s.K % 4 == 0);
-  return s.stride == 1 && kok && s.H == s.P && s.W == s.Q && load_encoders();
+  // any stride-1 geometry (the dgrad is the full correlation of dy padded by
+  // R-1-pad: "valid" convolutions too), as long as that padding is >= 0
+  const bool geom = s.H == s.P + s.R - 1 - 2 * s.pad && s.W == s.Q + s.S - 1 - 2 * s.pad && s.pad <= s.R - 1 &&
+                    s.pad <= s.S - 1;
+  return s.stride == 1 && kok && geom && load_encoders();
 }
 bool conv_tma_ok_wgrad(const ConvShape& s) {
   // 1x1 with K % 32 != 0 (the FC): dy's last column box and the partial store

@@ -108,6 +108,8 @@ CONV_CASES = [
     (2, 256, 14, 14, 256, 3, 1, 1),  # stage 3 (halo, 8-row sub-tile, rows past P)
     (2, 64, 10, 12, 96, 5, 1, 2),    # 5x5, non-square image, K % 64 != 0
     (4, 64, 1, 1, 1000, 1, 1, 0),    # the FC as a 1x1 conv: K % 32 != 0 (dgrad's last chunk zero-filled)
+    (2, 96, 13, 13, 64, 3, 1, 0),    # "valid" 3x3 (pad 0, H != P): TMA dgrad over dy padded by 2
+    (3, 32, 15, 11, 64, 3, 1, 0),    # valid, non-square
     (3, 96, 5, 5, 100, 1, 1, 0),     # 1x1, K % 32 != 0 with spatial extent
 ]
 
