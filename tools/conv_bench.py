@@ -35,6 +35,8 @@ def main() -> None:
     ap.add_argument("--ops", nargs="+", default=["fwd", "dgrad", "wgrad"])
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--shapes", type=int, nargs="+", default=None, help="indices into SHAPES")
+    ap.add_argument("--shape", type=int, nargs=8, action="append", default=None,
+                    metavar=("N", "C", "H", "W", "K", "k", "s", "p"), help="extra shape (repeatable)")
     args = ap.parse_args()
     import torch
     from paper_1801_04380_b200 import _native
@@ -45,7 +47,10 @@ def main() -> None:
     lib.sn_test_red_scratch_floats.restype = ctypes.c_longlong
     lib.sn_test_wgrad_splits.restype = ctypes.c_int
     dev = torch.device("cuda:0")
-    for shp in [SHAPES[i] for i in (args.shapes if args.shapes is not None else range(len(SHAPES)))]:
+    shapes = [SHAPES[i] for i in (args.shapes if args.shapes is not None else range(len(SHAPES)))]
+    if args.shape:
+        shapes = ([SHAPES[i] for i in args.shapes] if args.shapes is not None else []) + [tuple(x) for x in args.shape]
+    for shp in shapes:
         N, C, H, W, K, k, s, p = shp
         P = (H + 2 * p - k) // s + 1
         Q = (W + 2 * p - k) // s + 1
