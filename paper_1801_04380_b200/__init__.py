@@ -20,7 +20,7 @@ from .simulator import (POLICIES, Features, SimConfig, SimReport, StepRow, Sweep
 from .analysis import (GradBuffer, LruCache, OffloadPlan, RecomputePlan, Segment, TensorLife,
                        build_offload_plan, demand_peak, grad_buffers, liveness_peak, liveness_table,
                        min_pool_bytes, plan, resident_curve, step_demands, working_set_bytes)
-from .netgen import gen_resnet, make_uniform_chain
+from .netgen import gen_resnet, make_uniform_chain, random_fanjoin
 from .poolalloc import BLOCK_BYTES, BlockPool
 
 __version__ = "0.1.0"
@@ -33,7 +33,7 @@ __all__ = [
     "Selection", "SimConfig", "SimReport", "StepRow", "SweepPoint", "TensorLife", "baseline_peak_bytes",
     "build_costs", "build_offload_plan", "build_schedule", "demand_peak", "forward_order", "gen_resnet",
     "grad_buffers", "grad_owner", "liveness_peak", "liveness_table", "load_network", "make_uniform_chain", "mib",
-    "min_pool_bytes", "parse_features", "parse_network", "plan", "propagate_shapes", "resident_curve",
+    "min_pool_bytes", "parse_features", "parse_network", "plan", "propagate_shapes", "random_fanjoin", "resident_curve",
     "run_simulation", "run_sweep", "select_algorithm", "step_demands", "working_set_bytes", "run_training",
     "__version__",
 ]

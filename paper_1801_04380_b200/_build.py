@@ -4,6 +4,9 @@
   block pool, LRU cache, event tape).  Host only, built with g++.
 * ``_lib/libsnexec.so``  -- CUDA executor + sm_100a kernels, built with nvcc
   ``-gencode arch=compute_100a,code=sm_100a``; links libsnplan.so.
+* ``_lib/libsntest.so``  -- test-only hooks and hardware probes (``csrc/testing``:
+  kernel-level parity entry points, tcgen05 rate / layout probes); links
+  libsnexec.so and is never loaded by the training path.
 
 Both are plain C-ABI libraries loaded with ctypes (see ``_native.py``); the
 declarations live in ``include/superneurons.h``.
@@ -100,9 +103,32 @@ def build_exec(force: bool = False) -> Path:
     return out
 
 
+def build_testing(force: bool = False) -> Path:
+    exe = build_exec(force)
+    out = LIB / "libsntest.so"
+    srcs = _sources("testing", (".cu",))
+    headers = _sources("kernels", (".cuh", ".h", ".hpp")) + sorted(INCLUDE.glob("*.h"))
+    flags = ["-O3", "-std=c++17", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr"]
+    digest = _digest(srcs + headers + [exe], flags)
+    if not force and _up_to_date(out, digest):
+        return out
+    objdir = LIB / "obj"
+    objdir.mkdir(exist_ok=True)
+    objs = [str(objdir / ("test_" + src.stem + ".o")) for src in srcs]
+    import concurrent.futures as cf
+    with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as pool:
+        list(pool.map(lambda so: _run([NVCC, *flags, f"-I{INCLUDE}", f"-I{CSRC}", "-c", str(so[0]), "-o", so[1]]),
+                      zip(srcs, objs)))
+    _run([NVCC, *ARCH, "-shared", *objs, "-o", str(out), f"-L{LIB}", "-lsnexec", "-lsnplan",
+          "-Xlinker", "-rpath,$ORIGIN"])
+    _stamp(out, digest)
+    return out
+
+
 def build_all(force: bool = False) -> None:
     build_planner(force)
     build_exec(force)
+    build_testing(force)
 
 
 if __name__ == "__main__":

@@ -43,3 +43,9 @@ def planner() -> ctypes.CDLL:
 def executor() -> ctypes.CDLL:
     planner()
     return load("snexec")
+
+
+def testing() -> ctypes.CDLL:
+    """Test-only hooks and probes (libsntest.so); never used by the product path."""
+    executor()
+    return load("sntest")

@@ -773,13 +773,15 @@ struct Compiler {
           break;
         }
         const int ndgrad = !dx ? 0 : sn::conv_dgrad_launches(cs);
+        const int nwgrad = sn::conv_wgrad_launches(cs, sp, db != nullptr);
         push([=] {
           ck(cudaEventRecord(ready, st), "record");
           ck(cudaStreamWaitEvent(s3, ready, 0), "wait");
           ck(sn::conv_wgrad(cs, x, dy, dw, db, part_w, sp, red_w, s3), "conv_wgrad");
           ck(cudaEventRecord(wdone, s3), "record");
           if (dx) ck(sn::conv_dgrad(cs, dy, w, wt, dx, acc, st), "conv_dgrad");
-        }, 2 + nbias + ndgrad);
+        }, nwgrad + ndgrad);
+        (void)nbias;
         (void)part;
         (void)red;
         break;
@@ -1392,7 +1394,9 @@ struct Compiler {
         default: break;  // cache bookkeeping and step markers need no device work
       }
     }
-    // Join the copy streams back into the compute stream.
+    // Join the copy streams back into the compute stream (no layer: the
+    // trailing actions must not inherit the last tape event's layer / type).
+    cur_layer = -1, cur_type = 3;
     cudaStream_t s0 = ex->s0;
     if (used_s1) {
       cudaEvent_t j = ex->new_event();
@@ -1442,6 +1446,18 @@ void ensure_graph(sn_exec* ex) {
   }
   ck(cudaStreamEndCapture(ex->s0, &ex->graph), "EndCapture");
   ck(cudaGraphInstantiate(&ex->gexec, ex->graph, 0), "GraphInstantiate");
+  // exact launch count of one iteration: the kernel nodes of the graph
+  size_t nn = 0;
+  ck(cudaGraphGetNodes(ex->graph, nullptr, &nn), "GraphGetNodes");
+  std::vector<cudaGraphNode_t> nodes(nn);
+  ck(cudaGraphGetNodes(ex->graph, nodes.data(), &nn), "GraphGetNodes");
+  int64_t kern = 0;
+  for (cudaGraphNode_t nd : nodes) {
+    cudaGraphNodeType t;
+    ck(cudaGraphNodeGetType(nd, &t), "GraphNodeGetType");
+    kern += t == cudaGraphNodeTypeKernel;
+  }
+  ex->kernels_per_step = kern;
   ex->graph_ready = true;
 }
 

@@ -543,6 +543,21 @@ int conv_wgrad_splits(const ConvShape& s, int64_t partial_floats_cap) {
   return effective_splits(static_cast<int>(NPQ), static_cast<int>(want));
 }
 
+int splitk_reduce_launches(int splits, int M, int N) {
+  const int64_t tiles = static_cast<int64_t>((N + 31) / 32) * ((M + 31) / 32);
+  return (splits >= 16 && tiles < 4 * 148) ? 2 : 1;  // mirrors splitk_reduce_impl
+}
+
+int conv_wgrad_launches(const ConvShape& s, int splits, bool bias) {
+  const int nb = bias ? 2 : 0;  // bias_grad: column-reduction stage 1 + finish
+  const int RSC = s.R * s.S * s.C;
+  if (use_tma() && s.stride == 1 && conv_halo_wgrad128_ok(s.N, s.H, s.W, s.C, s.K, s.R, s.S, s.pad, s.P, s.Q))
+    return 1 + splitk_reduce_launches(conv_halo_wgrad128_splits(s.C, s.K, s.R), RSC, s.K) + nb;
+  if (use_tma() && s.stride == 1 && conv_halo_wgrad_ok(s.N, s.H, s.W, s.C, s.K, s.R, s.S, s.pad, s.P, s.Q))
+    return (s.C / 64) * (s.K / 64) + splitk_reduce_launches(conv_halo_wgrad_splits(), RSC, s.K) + nb;
+  return 1 + splitk_reduce_launches(effective_splits(s.N * s.P * s.Q, splits), RSC, s.K) + nb;
+}
+
 cudaError_t conv_wgrad(const ConvShape& s, const float* x, const float* dy, float* dw, float* db, float* partial,
                        int splits, float* red_scratch, cudaStream_t st) {
   cudaError_t e;

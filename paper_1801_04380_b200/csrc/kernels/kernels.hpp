@@ -35,6 +35,9 @@ bool conv_wgrad_splits_fixed(const ConvShape& s);
 int conv_wgrad_splits(const ConvShape& s, int64_t partial_floats_cap);
 cudaError_t conv_wgrad(const ConvShape& s, const float* x, const float* dy, float* dw, float* db,
                        float* partial, int splits, float* red_scratch, cudaStream_t st);
+// kernels one conv_wgrad issues (bias: db not null); splitk_reduce's own count
+int conv_wgrad_launches(const ConvShape& s, int splits, bool bias);
+int splitk_reduce_launches(int splits, int M, int N);
 
 // TMA-fed variants (conv_tma.cu); conv_fwd/conv_dgrad/conv_wgrad dispatch to
 // them when the shapes allow (C % 32 == 0; dgrad stride 1) unless SN_CONV_TMA=0.

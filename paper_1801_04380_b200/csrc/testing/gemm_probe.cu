@@ -1,8 +1,8 @@
 // Test hook: the tcgen05 GEMM core on plain strided matrices, for the
 // kernel-level parity tests (tests/test_gpu_kernels.py).  Not on the training
 // path; the executor calls the same template through its conv/FC wrappers.
-#include "gemm_tc.cuh"
-#include "kernels.hpp"
+#include "../kernels/gemm_tc.cuh"
+#include "../kernels/kernels.hpp"
 
 namespace {
 

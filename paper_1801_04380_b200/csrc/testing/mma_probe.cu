@@ -4,7 +4,7 @@
 // accumulators.  Reports clock64 cycles per MMA (max over CTAs).
 #include <cstdint>
 
-#include "tc_common.cuh"
+#include "../kernels/tc_common.cuh"
 
 namespace sn {
 namespace {

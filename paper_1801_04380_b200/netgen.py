@@ -8,7 +8,10 @@ their schedules are the reference's.  The classifier pooling carries
 unchanged) because the executor needs a pooling mode and global average
 pooling is what a ResNet uses.
 
-``make_uniform_chain`` is the reference's closed-form test chain.
+``make_uniform_chain`` is the reference's closed-form test chain and
+``random_fanjoin`` its seeded fan-out/fan-in property-test generator
+(memsched netgen.py:112-171): the same ``random.Random(seed)`` draws in the
+same order, so a seed gives the reference's network text exactly.
 ``densenet_text`` / ``inception_text`` build the JOIN-sum DenseNet-121- and
 Inception-v4-style graphs of benchmark configs 3-4 (the reference ships no
 generator for them; the reference parser accepts their text unchanged).
@@ -16,10 +19,13 @@ generator for them; the reference parser accepts their text unchanged).
 
 from __future__ import annotations
 
+import random
+
 from .errors import ConfigError
 from .netgraph import NetworkDef, parse_network
 
 __all__ = ["resnet_text", "gen_resnet", "uniform_chain_text", "make_uniform_chain",
+           "fanjoin_text", "random_fanjoin",
            "densenet_text", "gen_densenet", "inception_text", "gen_inception"]
 
 
@@ -117,6 +123,65 @@ def uniform_chain_text(n_layers: int, cp_positions: tuple[int, ...] = (), c: int
 def make_uniform_chain(n_layers: int, cp_positions: tuple[int, ...] = (), c: int = 4, h: int = 16,
                        w: int = 16) -> NetworkDef:
     return parse_network(uniform_chain_text(n_layers, cp_positions, c, h, w), name=f"chain{n_layers}")
+
+
+# Layer kinds a fan-join branch draws from (reference netgen.py:112).
+FANJOIN_BRANCH_KINDS = ("ACT", "LRN", "BN", "CONV")
+
+
+def fanjoin_text(seed: int, min_blocks: int = 2, max_blocks: int = 5) -> str:
+    """Text of the seeded fan-out/fan-in net: a spine of blocks, each 2-3
+    shape-preserving branches of 1-2 layers summed by a JOIN, a 2x2 POOL after
+    a block with probability 0.4 while h >= 4, then FC + SOFTMAX.  Every layer
+    line precedes every edge line, as in the reference."""
+    rng = random.Random(seed)
+    c = rng.choice((2, 3, 4))
+    hw = rng.choice((8, 16))
+    layers = [f"layer data DATA c={c} h={hw} w={hw}"]
+    edges: list[str] = []
+    counter = [0]
+
+    def name(prefix: str) -> str:
+        counter[0] += 1
+        return f"{prefix}{counter[0]}"
+
+    spine = "data"
+    for _ in range(rng.randint(min_blocks, max_blocks)):
+        tails = []
+        for _ in range(rng.randint(2, 3)):
+            at = spine
+            for _ in range(rng.randint(1, 2)):
+                kind = rng.choice(FANJOIN_BRANCH_KINDS)
+                lname = name(kind.lower())
+                if kind == "CONV":
+                    k = rng.choice((1, 3))
+                    layers.append(f"layer {lname} CONV out={c} k={k} p={1 if k == 3 else 0}")
+                else:
+                    layers.append(f"layer {lname} {kind}")
+                edges.append(f"edge {at} {lname}")
+                at = lname
+            tails.append(at)
+        join = name("join")
+        layers.append(f"layer {join} JOIN")
+        edges.extend(f"edge {t} {join}" for t in tails)
+        spine = join
+        if hw >= 4 and rng.random() < 0.4:
+            pool = name("pool")
+            layers.append(f"layer {pool} POOL k=2 s=2")
+            edges.append(f"edge {spine} {pool}")
+            spine = pool
+            hw //= 2
+    fc = name("fc")
+    layers.append(f"layer {fc} FC out={rng.choice((10, 16, 32))}")
+    edges.append(f"edge {spine} {fc}")
+    sm = name("softmax")
+    layers.append(f"layer {sm} SOFTMAX")
+    edges.append(f"edge {fc} {sm}")
+    return "\n".join(layers + edges) + "\n"
+
+
+def random_fanjoin(seed: int, min_blocks: int = 2, max_blocks: int = 5) -> NetworkDef:
+    return parse_network(fanjoin_text(seed, min_blocks, max_blocks), name=f"fanjoin_{seed}")
 
 
 # ---------------------------------------------------------------------------

@@ -78,7 +78,7 @@ def test_measured_columns_render(capsys):
 
 
 @pytest.mark.gpu
-def test_cli_execute_on_gpu(capsys):
+def test_cli_execute_on_gpu(cuda, capsys):
     """``memsched run --execute`` plans, runs the schedule on the B200 and adds
     the measured object; the plan part equals the non-executing run."""
     from paper_1801_04380_b200 import cli

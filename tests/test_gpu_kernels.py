@@ -16,7 +16,7 @@ pytestmark = pytest.mark.gpu
 
 def _lib():
     from paper_1801_04380_b200 import _native
-    lib = _native.executor()
+    lib = _native.testing()
     lib.sn_test_gemm.restype = ctypes.c_int
     lib.sn_test_gemm.argtypes = [ctypes.c_int] * 3 + [ctypes.c_void_p] * 3 + [ctypes.c_int] * 6
     return lib
@@ -116,7 +116,7 @@ CONV_CASES = [
 
 def _conv_lib():
     from paper_1801_04380_b200 import _native
-    lib = _native.executor()
+    lib = _native.testing()
     lib.sn_test_conv.restype = ctypes.c_int
     lib.sn_test_conv.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_void_p),
                                  ctypes.c_int]
@@ -196,7 +196,7 @@ def test_tma_overlapping_window_probe(cuda):
     """Records whether the driver accepts overlapping-row tensor maps (used to
     decide the stem-convolution design); informational, always passes."""
     from paper_1801_04380_b200 import _native
-    lib = _native.executor()
+    lib = _native.testing()
     lib.sn_test_tma_overlap.restype = ctypes.c_int
     lib.sn_test_tma_overlap.argtypes = [ctypes.c_void_p]
     buf = torch.zeros(2 * 224 * 224 * 4, device=cuda)
@@ -286,7 +286,7 @@ POOL_CASES = [
 
 def _pool_lib():
     from paper_1801_04380_b200 import _native
-    lib = _native.executor()
+    lib = _native.testing()
     lib.sn_test_pool.restype = ctypes.c_longlong
     lib.sn_test_pool.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_void_p),
                                  ctypes.c_int]

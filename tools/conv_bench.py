@@ -40,7 +40,7 @@ def main() -> None:
     args = ap.parse_args()
     import torch
     from paper_1801_04380_b200 import _native
-    lib = _native.executor()
+    lib = _native.testing()
     lib.sn_test_conv.restype = ctypes.c_int
     lib.sn_test_conv.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_void_p),
                                  ctypes.c_int]

@@ -4,7 +4,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import torch
 from paper_1801_04380_b200 import _native
-lib = _native.executor()
+lib = _native.testing()
 lib.sn_probe_m64_layout.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_int]
 g = torch.Generator().manual_seed(0)
 # A row r = e_r-ish so D[r][c] is identifiable: A[r][k] = (k == 0) * (r + 1), B[c][k] = (k == 0) * 1000 * (c + 1)... exact in tf32

@@ -4,7 +4,7 @@ import ctypes, os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_1801_04380_b200 import _native
-lib = _native.executor()
+lib = _native.testing()
 lib.sn_probe_mma_rate.restype = ctypes.c_longlong
 lib.sn_probe_mma_rate.argtypes = [ctypes.c_int] * 5
 iters = 4096

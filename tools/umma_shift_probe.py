@@ -5,7 +5,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import torch
 from paper_1801_04380_b200 import _native
-lib = _native.executor()
+lib = _native.testing()
 lib.sn_test_umma_shift.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_int] * 3
 g = torch.Generator().manual_seed(0)
 B = torch.randn(64, 32, generator=g)
