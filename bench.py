@@ -34,8 +34,12 @@ ALL = "liveness,offload,cache,recompute=cost-aware,convselect"
 GiB = 1 << 30
 
 
-DEFAULT_BATCH = {"resnet50g": 256, "resnet152g": 256, "densenet121s": 256, "inception4s": 128, "alexnet": 200,
-                 "alex32": 16}
+DEFAULT_BATCH = {"resnet50g": 256, "resnet152g": 256, "resnet2534g": 16, "densenet121s": 256, "inception4s": 128,
+                 "alexnet": 200, "alex32": 16}
+# pool budgets: 24 GiB (BASELINE.json config 2); the depth run uses the
+# reference's own 12e9 B at batch 16 (pkg/tests/test_acceptance.py:467-497)
+DEFAULT_POOL = {"resnet2534g": 12 * 10 ** 9}
+NETS = ["resnet50g", "resnet152g", "resnet2534g", "densenet121s", "inception4s", "alexnet", "alex32"]
 
 
 def parse_args():
@@ -44,17 +48,18 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--net", default="resnet50g",
-                    choices=["resnet50g", "resnet152g", "densenet121s", "inception4s", "alexnet", "alex32"],
+    ap.add_argument("--net", default="resnet50g", choices=NETS,
                     help="benchmark configs: alex32 (1), resnet50g (2, the headline), inception4s (3), "
-                         "densenet121s (4), resnet152g (5)")
+                         "densenet121s (4), resnet152g / resnet2534g (5)")
     ap.add_argument("--batch", type=int, default=None, help="per-GPU batch (default: the config's)")
-    ap.add_argument("--pool-gib", type=float, default=24.0)
+    ap.add_argument("--pool-gib", type=float, default=None, help="pool budget in GiB (default: the config's)")
     ap.add_argument("--features", default=ALL)
     ap.add_argument("--no-extras", action="store_true", help="skip the unconstrained / profile / baseline legs")
     args = ap.parse_args()
     if args.batch is None:
         args.batch = DEFAULT_BATCH[args.net]
+    if args.pool_gib is None:
+        args.pool_gib = DEFAULT_POOL.get(args.net, 24 * GiB) / GiB
     return args
 
 
@@ -65,6 +70,8 @@ def build_net(name: str):
         return gen_resnet(3, 4, 6, 3)
     if name == "resnet152g":
         return gen_resnet(3, 8, 36, 3)
+    if name == "resnet2534g":
+        return gen_resnet(211, 211, 211, 211)
     if name == "densenet121s":
         from paper_1801_04380_b200.netgen import gen_densenet
         return gen_densenet()
@@ -408,123 +415,144 @@ def extras(args, net, cfg, ex, ms_per_step, local) -> dict:
                                 "overhead_of_memory_schedule": round(ms_per_step / u - 1.0, 4)}
     except Exception as exc:  # report, never hide
         out["unconstrained"] = {"error": str(exc)[:200]}
-    out["cpu_baseline"] = cpu_baseline(net, sample=4)
+    out["cpu_baseline"] = cpu_baseline(args.net, sample=min(args.batch, 16))
     return out
 
 
 def _inputs(net, B):
     import torch
-    import paper_1801_04380_b200 as sn
-    c, h, w = sn.propagate_shapes(net)[net.data_id]
-    n_cls = math.prod(sn.propagate_shapes(net)[net.terminal_id])
+    from oracle import netdef
+    onet = netdef.as_onet(net)
+    shp = netdef.shapes(onet)
+    c, h, w = shp[onet.data_id]
+    n_cls = math.prod(shp[onet.terminal_id])
     g = torch.Generator().manual_seed(1000)
     return torch.randn(B, c, h, w, generator=g), torch.randint(0, n_cls, (B,), generator=g)
 
 
-def cpu_baseline(net, sample: int) -> dict:
-    """The CPU restatement (oracle/numerics.py) timed on the host cores."""
+def net_text(name: str) -> str:
+    """The config's ``.net`` text without the product package: the oracle's
+    restated generator for the residual nets, the bundled text files otherwise."""
+    from oracle import netdef
+    blocks = {"resnet50g": (3, 4, 6, 3), "resnet152g": (3, 8, 36, 3), "resnet2534g": (211, 211, 211, 211)}
+    if name in blocks:
+        return netdef.resnet_text(*blocks[name])
+    with open(os.path.join(ROOT, "paper_1801_04380_b200", "fixtures", f"{name}.net")) as fh:
+        return fh.read()
+
+
+def cpu_model() -> str:
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def cpu_baseline(name: str, sample: int) -> dict:
+    """The CPU restatement (oracle/numerics.py, no product code) timed on the
+    host cores on a bounded sample of the workload."""
     import torch
-    from paper_1801_04380_b200.training import init_parameters
+    from oracle import netdef
     from oracle.numerics import forward_backward
     threads = len(os.sched_getaffinity(0))
     torch.set_num_threads(threads)
-    params = init_parameters(net, seed=2)
-    images, labels = _inputs(net, sample)
-    forward_backward(net, params, images, labels)  # warm
+    onet = netdef.parse_net(net_text(name), name)
+    params = netdef.init_parameters(onet, seed=2)
+    images, labels = _inputs(onet, sample)
+    forward_backward(onet, params, images, labels)  # warm
     t0 = time.perf_counter()
     reps = 0
     while reps < 2 or time.perf_counter() - t0 < 5.0:
-        forward_backward(net, params, images, labels)
+        forward_backward(onet, params, images, labels)
         reps += 1
         if time.perf_counter() - t0 > 25.0:
             break
     dt = (time.perf_counter() - t0) / reps
     return {"value": round(sample / dt, 3), "unit": "images/s", "cores": threads, "kind": "port",
-            "sample": f"{reps} fp32 fwd+bwd passes of {sample} images ({net.name}), torch CPU restatement "
+            "cpu": cpu_model(),
+            "sample": f"{reps} fp32 fwd+bwd passes of {sample} images ({name}), torch CPU restatement "
                       "(oracle/numerics.py)"}
 
 
 def run_reference(args) -> None:
+    """The reference's CPU path for this workload, on the host cores, with no
+    product code: (1) the training step the reference describes but cannot
+    execute (it has no tensors), as the oracle's torch CPU fp32
+    restatement, full per-GPU batch per step; (2) the unmodified reference
+    package's own schedule computation (memsched.run_simulation from
+    baseline/_ref) for the same config."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     import torch
-    from paper_1801_04380_b200.training import init_parameters
+    from oracle import netdef
     from oracle.numerics import forward_backward, sgd_step
-    net = build_net(args.net)
     threads = len(os.sched_getaffinity(0))
     torch.set_num_threads(threads)
-    sample = 4
-    params = init_parameters(net, seed=2)
-    images, labels = _inputs(net, sample)
-    for _ in range(max(1, min(args.warmup, 2))):
-        forward_backward(net, params, images, labels)
+    text = net_text(args.net)
+    onet = netdef.parse_net(text, args.net)
+    B = args.batch
+    params = netdef.init_parameters(onet, seed=2)
+    images, labels = _inputs(onet, B)
+    for _ in range(max(1, args.warmup)):
+        forward_backward(onet, params, images, labels)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        _, grads = forward_backward(net, params, images, labels)
+        _, grads = forward_backward(onet, params, images, labels)
         params = sgd_step(params, grads, 0.01)
     dt = time.perf_counter() - t0
-    value = sample * args.steps / dt
+    value = B * args.steps / dt
+    pool = int(args.pool_gib * GiB)
     print(json.dumps({
-        "impl": "reference", "metric": baseline_metric(), "value": round(value, 3), "unit": "images/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3),
+        "impl": "reference", "metric": baseline_metric(), "value": round(value, 3), "unit": "images/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": max(1, args.warmup),
+        "ms_per_step": round(dt / args.steps * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
-        "data": "synthetic", "config": {"workload": f"{args.net} fwd+bwd+SGD, bounded sample of {sample} images "
-                                                    "per step (the b256 workload at CPU scale)",
-                                        "model": args.net, "parallelism": "cpu"},
+        "data": "synthetic N(0,1) images, uniform labels; He-uniform weights (seed 2)",
+        "config": {"workload": f"{args.net}_b{B}_pool{args.pool_gib:g}GiB_{args.features.replace(',', '+')}",
+                   "model": args.net, "global_batch": B, "per_gpu_batch": B, "parallelism": "cpu",
+                   "pool_bytes": pool, "features": args.features},
         "cpu_baseline": {"value": round(value, 3), "unit": "images/s", "cores": threads, "kind": "port",
-                         "sample": f"{sample} images/step, torch CPU restatement oracle/numerics.py; the reference "
-                                   "memsched package is a simulator with no tensor numerics"},
+                         "cpu": cpu_model(),
+                         "sample": f"full {args.net} batch of {B} per step, fwd+bwd+SGD, torch CPU fp32 "
+                                   "restatement oracle/numerics.py (the reference memsched package is a simulator "
+                                   "with no tensor numerics)"},
         "e2e": {"value": round(value, 3), "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "reference_simulator": reference_simulator_time(args, net),
+        "reference_simulator": reference_simulator_time(args, text, pool),
     }), flush=True)
 
 
-def reference_simulator_time(args, net) -> dict:
+def reference_simulator_time(args, text: str, pool: int) -> dict:
     """The unmodified reference package (memsched 0.1.0, installed offline into
     baseline/_ref with --no-deps: matplotlib is only for its PNG figures)
     planning this config with its own run_simulation -- the reference's CPU
-    path for the schedule; our C++ planner produces the identical SimReport."""
+    path for the schedule (1 core, CPython)."""
     ref_dir = os.path.join(ROOT, "baseline", "_ref")
     if not os.path.isdir(os.path.join(ref_dir, "memsched")):
         return {"unavailable": "baseline/_ref not installed"}
     sys.path.insert(0, ref_dir)
     try:
         import memsched
-        import paper_1801_04380_b200 as sn
-        rnet = memsched.parse_network(sn.network_text(net) if hasattr(sn, "network_text") else _net_text(net),
-                                      name=net.name)
-        cfg = memsched.SimConfig(pool_bytes=int(args.pool_gib * GiB), features=memsched.parse_features(args.features),
+        rnet = memsched.parse_network(text, name=args.net)
+        cfg = memsched.SimConfig(pool_bytes=pool, features=memsched.parse_features(args.features),
                                  cost=memsched.CostConfig(batch=args.batch))
         times = []
-        for _ in range(3):
+        for _ in range(1 if len(rnet.layers) > 1000 else 3):
             t0 = time.perf_counter()
             rep = memsched.run_simulation(rnet, cfg)
             times.append(time.perf_counter() - t0)
-        t0 = time.perf_counter()
-        ours = sn.run_simulation(net, sn.SimConfig(pool_bytes=int(args.pool_gib * GiB),
-                                                   features=sn.parse_features(args.features),
-                                                   cost=sn.CostConfig(batch=args.batch)))
-        t_ours = time.perf_counter() - t0
-        return {"run_simulation_s": round(statistics.median(times), 4), "cores": 1,
+        return {"run_simulation_s": round(statistics.median(times), 4), "cores": 1, "cpu": cpu_model(),
+                "module": os.path.relpath(memsched.__file__, ROOT),
                 "peak_bytes": rep.peak_bytes, "min_pool_bytes": rep.min_pool_bytes,
-                "ours_planner_s": round(t_ours, 4), "identical_peak": ours.peak_bytes == rep.peak_bytes}
+                "pool_high_water_bytes": rep.pool_high_water_bytes}
     except Exception as exc:  # report, never hide
         return {"error": str(exc)[:200]}
     finally:
         sys.path.remove(ref_dir)
-
-
-def _net_text(net) -> str:
-    """.net text of a NetworkDef (layers in id order, then edges in next order)."""
-    lines = []
-    for l in net.layers:
-        kv = " ".join(f"{k}={v}" for k, v in l.params.items())
-        lines.append(f"layer {l.name} {l.kind.value} {kv}".rstrip())
-    for l in net.layers:
-        for n in l.next:
-            lines.append(f"edge {l.name} {net.layers[n].name}")
-    return "\n".join(lines) + "\n"
 
 
 def main() -> None:
