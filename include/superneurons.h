@@ -218,6 +218,13 @@ typedef struct sn_exec_options {
   uint64_t seed;          /* dropout mask seed */
   float lr;               /* SGD learning rate */
   float grad_scale;       /* multiply gradients before the update (1/world) */
+  int32_t precision;      /* CONV / FC math: 0 tf32 tensor cores (fp32 accumulate),
+                             1 fp32-faithful 3xTF32 split operands (~3x the MMA work) */
+  int32_t stash;          /* where copied-out tensors live: 0 pinned host memory (PCIe),
+                             1 device memory of stash_device (an NVLink peer's spare HBM;
+                             the executor's own device = same-device loopback) */
+  int32_t stash_device;
+  int32_t reserved_;
 } sn_exec_options;
 
 typedef struct sn_step_timing {

@@ -1429,6 +1429,14 @@ struct Compiler {
   }
 };
 
+// The kernels' numeric mode is process-wide (sn::set_precision); every entry
+// point that launches or captures this executor's work sets its own.
+struct PrecisionScope {
+  int saved;
+  explicit PrecisionScope(const sn_exec* ex) : saved(sn::precision()) { sn::set_precision(ex->opt.precision); }
+  ~PrecisionScope() { sn::set_precision(saved); }
+};
+
 void run_program(sn_exec* ex) {
   for (const Action& a : ex->prog) a.fn();
 }
@@ -1520,6 +1528,8 @@ int sn_exec_create(const sn_plan* plan, const sn_net_desc* /*net*/, const sn_lay
     ex->plan = plan;
     ex->net = &plan->plan.net;
     ex->opt = *opts;
+    if (ex->opt.precision != 0 && ex->opt.precision != 1) xfail(SN_EK_CONFIG, "precision must be 0 (tf32) or 1 (fp32)");
+    PrecisionScope prec(ex);
     ex->device = opts->device;
     ex->B = static_cast<int>(plan->plan.cost_cfg.batch);
     if (plan->plan.cost_cfg.dtype_bytes != 4)
@@ -1584,6 +1594,7 @@ int sn_exec_step(sn_exec* ex, int32_t update, float* loss_host, sn_step_timing* 
   if (!ex) return xset(SN_EK_INTERNAL, "null argument");
   return xguard([&] {
     ck(cudaSetDevice(ex->device), "cudaSetDevice");
+    PrecisionScope prec(ex);
     if (ex->opt.use_graph) ensure_graph(ex);
     ck(cudaEventRecord(ex->t_begin, ex->s0), "record");
     if (ex->opt.use_graph)
@@ -1612,6 +1623,7 @@ int sn_exec_step_host(sn_exec* ex, const float* images_host, const int32_t* labe
   if (!ex) return xset(SN_EK_INTERNAL, "null argument");
   const int rc = xguard([&] {
     ck(cudaSetDevice(ex->device), "cudaSetDevice");
+    PrecisionScope prec(ex);
     if (ex->opt.use_graph) ensure_graph(ex);
     ck(cudaEventRecord(ex->t_begin, ex->s0), "record");
     ck(cudaMemcpyAsync(ex->images, images_host, ex->image_floats * sizeof(float), cudaMemcpyHostToDevice, ex->s0),
@@ -1645,6 +1657,7 @@ int sn_exec_step_host_pipelined(sn_exec* ex, const float* images_host, const int
   if (!ex || !images_host || !labels_host) return xset(SN_EK_INTERNAL, "null argument");
   const int rc = xguard([&] {
     ck(cudaSetDevice(ex->device), "cudaSetDevice");
+    PrecisionScope prec(ex);
     if (ex->opt.use_graph) ensure_graph(ex);
     const size_t ibytes = ex->image_floats * sizeof(float), lbytes = ex->B * sizeof(int32_t);
     if (!ex->s4) {
@@ -1701,6 +1714,7 @@ int sn_exec_profile(sn_exec* ex, float* action_ms, int32_t* action_layer, int32_
   if (cap < ex->prog.size()) return xset(SN_EK_INTERNAL, "output buffer too small");
   return xguard([&] {
     ck(cudaSetDevice(ex->device), "cudaSetDevice");
+    PrecisionScope prec(ex);
     std::vector<cudaEvent_t> ev(ex->prog.size() + 1);
     for (auto& e : ev) ck(cudaEventCreate(&e), "event");
     ck(cudaEventRecord(ev[0], ex->s0), "record");

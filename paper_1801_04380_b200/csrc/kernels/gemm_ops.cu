@@ -443,12 +443,18 @@ cudaError_t splitk_reduce(const float* P, int splits, int M, int N, float* D, co
 }
 
 static int g_use_tma = -1;  // SN_CONV_TMA=0 forces the cp.async gather path (tests, A/B)
+static int g_precision = 0;  // 0 tf32, 1 fp32-faithful 3xTF32 (gather kernels only)
+int gemm_precision() { return g_precision; }
+void set_precision(int p) { g_precision = p ? 1 : 0; }
+int precision() { return g_precision; }
 bool use_tma() {
   if (g_use_tma < 0) {
     const char* v = std::getenv("SN_CONV_TMA");
     g_use_tma = (v && v[0] == '0') ? 0 : 1;
   }
-  return g_use_tma == 1;
+  // the 3xTF32 split lives in the generic gather kernel (gemm_tc.cuh): the
+  // fp32-faithful mode routes every CONV / FC through it
+  return g_use_tma == 1 && g_precision == 0;
 }
 void set_conv_tma(int on) { g_use_tma = on ? 1 : 0; }
 

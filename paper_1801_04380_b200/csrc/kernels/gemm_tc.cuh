@@ -13,6 +13,14 @@
 // hold 32 consecutive rows of one k), so transposed operands (dgrad/wgrad) are
 // fed directly from their NHWC layout without a transpose pass.
 //
+// fp32-faithful mode (SPLIT3, "3xTF32"): after a stage lands, the producers
+// split every operand element in place into hi = tf32_rn(x) and a residual
+// lo = x - hi (exact in fp32) written to a twin buffer of the same swizzled
+// layout, and the issuer accumulates hi.hi + hi.lo + lo.hi per K = 8 step.
+// The dropped lo.lo term and the tf32 rounding of lo are ~2^-22 relative:
+// fp32-level products with fp32 accumulation, at 3x the MMA work and half
+// the pipeline depth (the twins double the smem per stage).
+//
 // The operand gathers are policy objects (see conv loaders in conv_tc.cu):
 //   struct Loader { __device__ void tile_init(int r0, void* scratch, int tid);
 //                   __device__ void load(uint32_t smem_tile, int kb, int tid); };
@@ -27,11 +35,12 @@ constexpr int kProducers = 128;
 constexpr int kGemmThreads = 160;
 constexpr int kScratchBytes = 4096;  // per-operand tile_init scratch (row tables)
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, bool SPLIT3 = false>
 struct GemmSmem {
   static constexpr int A_BYTES = kBM * 128;
   static constexpr int B_BYTES = BN * 128;
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGE_BYTES = (A_BYTES + B_BYTES) * (SPLIT3 ? 2 : 1);
+  static constexpr int LO_OFF = STAGES * (A_BYTES + B_BYTES);  // SPLIT3: lo twins of every stage
   static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
   static constexpr int SCRATCH_OFF = BAR_OFF + 256;
   static constexpr int TOTAL = SCRATCH_OFF + 2 * kScratchBytes + 1024;  // +1024 alignment slack
@@ -58,15 +67,35 @@ __device__ __forceinline__ uint32_t mn_tile_off(uint32_t krow, uint32_t mchunk) 
          ((((c16 >> 1) ^ r4) & 3u) << 5) + ((c16 & 1u) << 4);
 }
 
-template <int BN, int STAGES, bool A_MN, bool B_MN, class LA, class LB, class EPI>
+// hi = x rounded to tf32 (low 13 mantissa bits zero), lo = x - hi (exact).
+__device__ __forceinline__ float tf32_hi(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+// Split a tile of `bytes` (a multiple of 128 * 16) in place: tile -> hi, twin -> lo.
+template <int BYTES>
+__device__ __forceinline__ void split3_tile(uint8_t* tile, uint8_t* twin, int tid) {
+#pragma unroll 4
+  for (int off = tid * 16; off < BYTES; off += kProducers * 16) {
+    float4 v = *reinterpret_cast<const float4*>(tile + off);
+    const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+    *reinterpret_cast<float4*>(tile + off) = h;
+    *reinterpret_cast<float4*>(twin + off) = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+  }
+}
+
+template <int BN, int STAGES, bool A_MN, bool B_MN, class LA, class LB, class EPI, bool SPLIT3 = false>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     tc_gemm_kernel(LA la, LB lb, EPI epi, int num_kb, int kb_per_split) {
-  using L = GemmSmem<BN, STAGES>;
+  using L = GemmSmem<BN, STAGES, SPLIT3>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * L::A_BYTES;
+  uint8_t* sA_lo = smem + L::LO_OFF;  // SPLIT3 only
+  uint8_t* sB_lo = sA_lo + STAGES * L::A_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
   uint64_t* empty = full + STAGES;
   uint64_t* done = empty + STAGES;
@@ -104,6 +133,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp < 4) {
     // ---------------- producers ----------------
     constexpr int LAG = STAGES - 1;
+    // a landed stage: (SPLIT3) every producer's copies are in, split it, then
+    // publish it to the tensor core
+    auto publish = [&](int j) {
+      const int s = j % STAGES;
+      if constexpr (SPLIT3) {
+        named_bar(1, kProducers);
+        split3_tile<L::A_BYTES>(sA + s * L::A_BYTES, sA_lo + s * L::A_BYTES, tid);
+        split3_tile<L::B_BYTES>(sB + s * L::B_BYTES, sB_lo + s * L::B_BYTES, tid);
+      }
+      fence_proxy_async();
+      mbar_arrive(&full[s]);
+    };
     for (int i = 0; i < nkb; ++i) {
       const int s = i % STAGES;
       if (i >= STAGES) mbar_wait(&empty[s], ((i / STAGES) - 1) & 1);
@@ -112,13 +153,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       cp_async_commit();
       if (i >= LAG) {
         cp_async_wait<LAG>();
-        fence_proxy_async();
-        mbar_arrive(&full[(i - LAG) % STAGES]);
+        publish(i - LAG);
       }
     }
     cp_async_wait<0>();
-    fence_proxy_async();
-    for (int j = (nkb > LAG ? nkb - LAG : 0); j < nkb; ++j) mbar_arrive(&full[j % STAGES]);
+    for (int j = (nkb > LAG ? nkb - LAG : 0); j < nkb; ++j) publish(j);
 
     // ---------------- epilogue ----------------
     mbar_wait(done, 0);
@@ -153,6 +192,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                              kLayoutSW128Base32)
                  : umma_desc(b0 + kk * 32, 16, 1024, kLayoutSW128);
         umma_tf32(tmem, ad, bd, idesc, (i | kk) != 0 ? 1u : 0u);
+        if constexpr (SPLIT3) {
+          // the twins sit at a fixed offset with the same 1024-aligned swizzle
+          // phase: the descriptors differ only in their start address (16 B units)
+          constexpr uint64_t kLoA = static_cast<uint64_t>(L::LO_OFF) >> 4;
+          umma_tf32(tmem, ad, bd + kLoA, idesc, 1u);
+          umma_tf32(tmem, ad + kLoA, bd, idesc, 1u);
+        }
       }
       umma_commit(&empty[s]);
     }
@@ -165,11 +211,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
 }
 
-template <int BN, int STAGES, bool A_MN, bool B_MN, class LA, class LB, class EPI>
-inline cudaError_t launch_tc_gemm(const LA& la, const LB& lb, const EPI& epi, int M, int N, int K,
-                                  int splits, cudaStream_t stream) {
-  using L = GemmSmem<BN, STAGES>;
-  auto kern = tc_gemm_kernel<BN, STAGES, A_MN, B_MN, LA, LB, EPI>;
+// Numeric mode of the gather GEMMs (set_precision in kernels.hpp): 0 tf32,
+// 1 fp32-faithful 3xTF32 (SPLIT3).
+int gemm_precision();
+
+template <int BN, int STAGES, bool A_MN, bool B_MN, bool SPLIT3, class LA, class LB, class EPI>
+inline cudaError_t launch_tc_gemm_impl(const LA& la, const LB& lb, const EPI& epi, int M, int N, int K,
+                                       int splits, cudaStream_t stream) {
+  using L = GemmSmem<BN, STAGES, SPLIT3>;
+  auto kern = tc_gemm_kernel<BN, STAGES, A_MN, B_MN, LA, LB, EPI, SPLIT3>;
   static bool attr_set = false;  // per template instantiation
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
@@ -184,6 +234,20 @@ inline cudaError_t launch_tc_gemm(const LA& la, const LB& lb, const EPI& epi, in
   dim3 grid((M + kBM - 1) / kBM, (N + BN - 1) / BN, splits);
   kern<<<grid, kGemmThreads, L::TOTAL, stream>>>(la, lb, epi, num_kb, kps);
   return cudaGetLastError();
+}
+
+// 3xTF32 stage depth: the lo twins double the smem of a stage
+template <int BN>
+constexpr int split3_stages() {
+  return BN >= 256 ? 2 : (BN >= 128 ? 3 : 4);
+}
+
+template <int BN, int STAGES, bool A_MN, bool B_MN, class LA, class LB, class EPI>
+inline cudaError_t launch_tc_gemm(const LA& la, const LB& lb, const EPI& epi, int M, int N, int K,
+                                  int splits, cudaStream_t stream) {
+  if (gemm_precision() == 1)
+    return launch_tc_gemm_impl<BN, split3_stages<BN>(), A_MN, B_MN, true>(la, lb, epi, M, N, K, splits, stream);
+  return launch_tc_gemm_impl<BN, STAGES, A_MN, B_MN, false>(la, lb, epi, M, N, K, splits, stream);
 }
 
 // Split count actually used by launch_tc_gemm for a requested count.

@@ -101,6 +101,12 @@ int64_t conv_dgrad_scratch_floats(const ConvShape& s);  // wt scratch conv_dgrad
 cudaError_t conv_dgrad_strided_tma(const ConvShape& s, const float* dy, const float* w, float* wt_scratch, float* dx,
                                    int accumulate, cudaStream_t st);
 void set_conv_tma(int on);
+// Numeric mode of every CONV / FC contraction: 0 = tf32 tensor-core math (the
+// TMA / halo / pair kernels), 1 = fp32-faithful 3xTF32 split operands in the
+// generic gather kernel (gemm_tc.cuh).  Process-wide; the executor sets it
+// around its own launches (sn_exec_options.precision).
+void set_precision(int p);
+int precision();
 // CTA-pair (cta_group::2) conv kernels: 0 off, 1 when the shape keeps the
 // pairs busy (default; env SN_CONV_PAIRS=0 turns them off), 2 always (tests).
 void set_conv_pairs(int mode);

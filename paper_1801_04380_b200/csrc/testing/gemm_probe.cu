@@ -156,3 +156,6 @@ int umma_shift_probe_run(const float* A, const float* B, float* D, int mn, int s
 extern "C" int sn_test_umma_shift(const float* A, const float* B, float* D, int mn, int shift, int base_off) {
   return sn::umma_shift_probe_run(A, B, D, mn, shift, base_off);
 }
+
+// Numeric mode of the gather GEMMs for the kernel-level tests (0 tf32, 1 3xTF32).
+extern "C" void sn_test_set_precision(int p) { sn::set_precision(p); }

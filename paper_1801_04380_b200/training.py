@@ -15,7 +15,10 @@ in ``oracle/numerics.py`` identically:
   * BN    batch statistics, eps 1e-5, momentum 0.1 (running stats updated once per iteration)
   * SOFTMAX (terminal) + cross-entropy, mean over the batch
   * ACT   ReLU; JOIN = elementwise sum; FC flattens NHWC (h, w, c) order
-Tensors are fp32 NHWC; CONV/FC contract on tcgen05 in tf32 with fp32 accumulation.
+Tensors are fp32 NHWC; CONV/FC contract on tcgen05 in tf32 with fp32 accumulation
+(``precision="tf32"``, the default) or, with ``precision="fp32"``, as 3xTF32
+split operands (hi.hi + hi.lo + lo.hi, fp32-level products) in the generic
+gather kernel -- the fp32-faithful mode the numeric parity tests pin at 1e-4.
 """
 
 from __future__ import annotations
@@ -43,7 +46,11 @@ class NumericsC(C.Structure):
 class ExecOptionsC(C.Structure):
     _fields_ = [("device", C.c_int32), ("elide_backups", C.c_int32), ("use_graph", C.c_int32),
                 ("num_classes", C.c_int32), ("seed", C.c_uint64), ("lr", C.c_float),
-                ("grad_scale", C.c_float)]
+                ("grad_scale", C.c_float), ("precision", C.c_int32), ("stash", C.c_int32),
+                ("stash_device", C.c_int32), ("reserved_", C.c_int32)]
+
+
+PRECISIONS = {"tf32": 0, "fp32": 1}
 
 
 class TimingC(C.Structure):
@@ -172,7 +179,8 @@ class Executor:
 
     def __init__(self, net: NetworkDef, config: SimConfig, device: int = 0, *, seed: int = 2,
                  dropout_seed: int = 1234, lr: float = 0.01, grad_scale: float = 1.0,
-                 elide_backups: bool = True, use_graph: bool = True, params: dict | None = None) -> None:
+                 elide_backups: bool = True, use_graph: bool = True, params: dict | None = None,
+                 precision: str = "tf32") -> None:
         import torch
         if not torch.cuda.is_available():
             raise DeviceError("run_training needs a CUDA device (B200); there is no CPU fallback")
@@ -184,7 +192,11 @@ class Executor:
         nums = (NumericsC * len(net.layers))(*[
             NumericsC(n.pool_mode, n.lrn_size, n.lrn_alpha, n.lrn_beta, n.lrn_k, n.dropout_rate,
                       n.bn_eps, n.bn_momentum) for n in layer_numerics(net)])
-        opts = ExecOptionsC(device, int(elide_backups), int(use_graph), 0, dropout_seed, lr, grad_scale)
+        if precision not in PRECISIONS:
+            raise MemschedError(f"precision must be one of {sorted(PRECISIONS)}, got {precision!r}")
+        self.precision = precision
+        opts = ExecOptionsC(device, int(elide_backups), int(use_graph), 0, dropout_seed, lr, grad_scale,
+                            PRECISIONS[precision], 0, device, 0)
         self.ptr = C.c_void_p()
         torch.cuda.set_device(device)
         torch.cuda.synchronize()

@@ -47,6 +47,32 @@ def test_tc_gemm_majors(cuda, bn, a_mn, b_mn, M, N, K):
     _check(D.cpu(), ref, K)
 
 
+@pytest.mark.parametrize("bn", [64, 128, 256])
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 1)])
+@pytest.mark.parametrize("M,N,K", [(128, 64, 32), (300, 200, 200), (257, 96, 1000)])
+def test_tc_gemm_3xtf32_is_fp32_faithful(cuda, bn, a_mn, b_mn, M, N, K):
+    """precision 1 (3xTF32 split operands): within 2e-6 relative Frobenius of
+    the fp64 product -- fp32-level (dropped lo.lo term and tf32 rounding of lo
+    ~2^-22 per product), about 1000x tighter than the tf32 bound."""
+    lib = _lib()
+    g = torch.Generator(device="cpu").manual_seed(M * 5 + N + K)
+    A = torch.randn(M, K, generator=g)
+    B = torch.randn(N, K, generator=g)
+    ref = A.double() @ B.double().T
+    Ad = (A.T.contiguous() if a_mn else A).to(cuda)
+    Bd = (B.T.contiguous() if b_mn else B).to(cuda)
+    D = torch.full((M, N), float("nan"), device=cuda)
+    lib.sn_test_set_precision(1)
+    try:
+        rc = lib.sn_test_gemm(a_mn, b_mn, bn, Ad.data_ptr(), Bd.data_ptr(), D.data_ptr(),
+                              M, N, K, M if a_mn else K, N if b_mn else K, 1)
+    finally:
+        lib.sn_test_set_precision(0)
+    assert rc == 0
+    err = ((D.cpu().double() - ref).norm() / ref.norm()).item()
+    assert err < 2e-6, err
+
+
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (1, 1)])
 def test_tc_gemm_split_k(cuda, a_mn, b_mn):
     lib = _lib()

@@ -398,3 +398,68 @@ def test_transfer_stats_eager_and_graph(cuda, graph):
     assert ts["h2d_bytes"] >= 477024000 and ts["h2d_ms"] > 0 and ts["h2d_GBps"] > 1
     assert ts["d2h_bytes"] > 0 and ts["d2h_ms"] > 0
     assert ts["exposed_ms"] >= 0
+
+
+# ---- fp32-faithful mode (precision="fp32": 3xTF32 split operands) ----------
+# Stated tolerance: loss rel. err <= 1e-5 and every parameter gradient within
+# 1e-4 relative Frobenius of the CPU fp32 oracle, masks included (fp32-level
+# products leave only ~1e-6 activation differences, so ReLU / max-pool flips
+# are rare single elements).  A CONV bias feeding a training-mode BN has an
+# exactly-zero true gradient; it is compared absolutely against the layer's
+# weight-gradient norm.
+FP32_TOL = 1e-4
+
+
+def _fp32_errors(net, grads, ref):
+    sn = _sn()
+    from oracle.numerics import relative_error
+    errs = {}
+    for l in ref:
+        lay = net.layers[l]
+        bn_fed = lay.kind is sn.LayerKind.CONV and any(net.layers[n].kind is sn.LayerKind.BN for n in lay.next)
+        errs[(lay.name, "w")] = relative_error(grads[l]["w"], ref[l]["w"])
+        if bn_fed:
+            errs[(lay.name, "b")] = (grads[l]["b"] - ref[l]["b"]).norm().item() / ref[l]["w"].norm().item()
+        else:
+            errs[(lay.name, "b")] = relative_error(grads[l]["b"], ref[l]["b"])
+    return errs
+
+
+def _fp32_case(net, batch, pool, params, images, labels):
+    from oracle.numerics import forward_backward
+    loss, grads, rep, _ = _run(net, batch, pool, ALL, params, images, labels, precision="fp32")
+    ref_loss, ref = forward_backward(net, params, images, labels)
+    assert abs(loss - ref_loss) <= 1e-5 * abs(ref_loss), (loss, ref_loss)
+    errs = _fp32_errors(net, grads, ref)
+    assert max(errs.values()) <= FP32_TOL, sorted(errs.items(), key=lambda kv: -kv[1])[:4]
+    return rep
+
+
+def test_fp32_mode_smooth32_matches_oracle(cuda):
+    from paper_1801_04380_b200.training import init_parameters
+    net = _sn().parse_network(SMOOTH32, name="smooth32")
+    params = init_parameters(net, seed=4, head_scale=0.1)
+    images, labels = _inputs(net, 16)
+    _fp32_case(net, 16, 1 << 30, params, images, labels)
+
+
+def test_fp32_mode_alex32_matches_oracle(cuda, alex32_case):
+    net, params, images, labels = alex32_case
+    rep = _fp32_case(net, 16, 1 << 30, params, images, labels)
+    assert rep.peak_bytes == 16777216
+
+
+def test_fp32_mode_resnet50g_b8_matches_oracle(cuda):
+    from paper_1801_04380_b200.netgen import gen_resnet
+    from paper_1801_04380_b200.training import init_parameters
+    net = gen_resnet(3, 4, 6, 3)
+    params = init_parameters(net, seed=2, head_scale=0.1)
+    images, labels = _inputs(net, 8)
+    _fp32_case(net, 8, 4 << 30, params, images, labels)
+
+
+def test_fp32_mode_feature_sets_are_bit_identical(cuda, alex32_case):
+    net, params, images, labels = alex32_case
+    base_loss, base, _, _ = _run(net, 16, 1 << 30, "none", params, images, labels, precision="fp32")
+    loss, grads, _, _ = _run(net, 16, 17 << 20, ALL, params, images, labels, precision="fp32")
+    assert loss == base_loss and _bitwise(grads, base)
