@@ -54,6 +54,8 @@ def parse_args():
     ap.add_argument("--batch", type=int, default=None, help="per-GPU batch (default: the config's)")
     ap.add_argument("--pool-gib", type=float, default=None, help="pool budget in GiB (default: the config's)")
     ap.add_argument("--features", default=ALL)
+    ap.add_argument("--precision", default="tf32", choices=["tf32", "fp32"],
+                    help="CONV/FC math: tf32 tensor cores (headline) or the fp32-faithful 3xTF32 mode")
     ap.add_argument("--no-extras", action="store_true", help="skip the unconstrained / profile / baseline legs")
     args = ap.parse_args()
     if args.batch is None:
@@ -140,25 +142,64 @@ def measured_peaks() -> dict:
         return {}
 
 
-def tf32_gemm_peak(device) -> float:
-    """cuBLAS tf32 GEMM 8192^3, best of 5 (TF/s) -- the tensor roofline for tf32 kernels."""
+def tf32_gemm_peaks(device, sustain_s: float = 3.0) -> dict:
+    """cuBLAS tf32 GEMM 8192^3 on this box, now: burst (best of 10, CUDA events)
+    and sustained (back to back for ``sustain_s`` s, under the power cap) --
+    the measured tf32 tensor roofline (MEASURED_PEAKS.json has bf16 only)."""
     import torch
     torch.backends.cuda.matmul.allow_tf32 = True
-    a = torch.randn(8192, 8192, device=device)
-    b = torch.randn(8192, 8192, device=device)
-    for _ in range(2):
+    n = 8192
+    a = torch.randn(n, n, device=device)
+    b = torch.randn(n, n, device=device)
+    for _ in range(3):
         a @ b
     best = math.inf
-    for _ in range(5):
+    for _ in range(10):
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
         a @ b
         e.record()
         torch.cuda.synchronize()
         best = min(best, s.elapsed_time(e))
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps, t0 = 0, time.perf_counter()
+    s.record()
+    while time.perf_counter() - t0 < sustain_s:
+        for _ in range(10):
+            a @ b
+        reps += 10
+        torch.cuda.synchronize()
+    e.record()
+    torch.cuda.synchronize()
+    sustained = 2 * n ** 3 * reps / (s.elapsed_time(e) / 1e3) / 1e12
     del a, b
     torch.cuda.empty_cache()
-    return 2 * 8192 ** 3 / (best / 1e3) / 1e12
+    return {"burst": 2 * n ** 3 / (best / 1e3) / 1e12, "sustained": sustained}
+
+
+def step_traffic(net_name: str, batch: int) -> tuple[dict | None, str]:
+    """The per-step DRAM traffic file (tools/launch_table.py merge) for this
+    config whose libsnexec digest equals the library this run loads; stale
+    files are refused."""
+    import glob
+    lib_sha = os.path.join(ROOT, "paper_1801_04380_b200", "_lib", "libsnexec.so.sha")
+    try:
+        digest = open(lib_sha).read().strip()
+    except OSError:
+        return None, "no libsnexec digest"
+    seen = []
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_step_traffic.json"))):
+        try:
+            d = json.load(open(path))
+        except (OSError, ValueError):
+            continue
+        if d.get("net") != net_name or d.get("batch") != batch or d.get("precision", "tf32") != "tf32":
+            continue
+        seen.append(os.path.basename(path))
+        if d.get("exec_digest") == digest:
+            return dict(d, source=os.path.relpath(path, ROOT)), "ok"
+    return None, (f"refused {', '.join(seen)}: libsnexec digest differs from this build" if seen
+                  else "no traffic capture for this config")
 
 
 def conv_flops(net, batch: int):
@@ -200,7 +241,9 @@ def run_ours(args) -> None:
     B = args.batch
     pool = int(args.pool_gib * GiB)
     cfg = sn.SimConfig(pool_bytes=pool, features=sn.parse_features(args.features), cost=sn.CostConfig(batch=B))
-    ex = Executor(net, cfg, device=local, seed=2, lr=0.01, grad_scale=1.0 / world)
+    free0 = torch.cuda.mem_get_info(local)[0]
+    ex = Executor(net, cfg, device=local, seed=2, lr=0.01, grad_scale=1.0 / world, precision=args.precision)
+    free1 = torch.cuda.mem_get_info(local)[0]
     rep = ex.report
     c, h, w = sn.propagate_shapes(net)[net.data_id]
     n_cls = math.prod(sn.propagate_shapes(net)[net.terminal_id])
@@ -286,6 +329,9 @@ def run_ours(args) -> None:
             wall = tt.item()
         return wall, sum(ts) / len(ts)
 
+    # measured device memory (after the timed region; one extra untimed step)
+    mem = ex.memory()
+    arena = ex.measure_arena()
     for i in range(2):
         host_step(i, False)
         host_step(i, True)
@@ -296,7 +342,8 @@ def run_ours(args) -> None:
         "metric": baseline_metric(),
         "value": round(value, 2), "unit": "images/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "fp32 storage, tf32 tensor-core math (fp32 accumulate)",
+        "scaling": "weak", "vs_baseline": None, "dtype": ("fp32 storage, tf32 tensor-core math (fp32 accumulate)" if args.precision == "tf32"
+                  else "fp32 (3xTF32 split operands on tensor cores, fp32-level products, fp32 accumulate)"),
         "data": "synthetic N(0,1) images, uniform labels; He-uniform weights (seed 2)",
         "config": {"workload": f"{args.net}_b{B}_pool{args.pool_gib:g}GiB_{args.features.replace(',', '+')}",
                    "model": args.net, "global_batch": B * world, "per_gpu_batch": B, "image": [c, h, w],
@@ -316,7 +363,11 @@ def run_ours(args) -> None:
                                "excluded), copy-engine GB/s, compute-stream time blocked on fetches"),
         "memory": {"peak_bytes": rep.peak_bytes, "min_pool_bytes_max_i_l_i": rep.min_pool_bytes,
                    "peak_over_floor": round(rep.peak_bytes / rep.min_pool_bytes, 4),
-                   "pool_high_water_bytes": rep.pool_high_water_bytes,
+                   "pool_high_water_bytes_planned": rep.pool_high_water_bytes,
+                   "arena_written_high_water_bytes_measured": arena["measured_arena_high_water_bytes"],
+                   "arena_written_bytes_measured": arena["measured_arena_written_bytes"],
+                   "cudaMemGetInfo_bytes_taken_by_executor": free0 - free1,
+                   "executor_allocations": mem,
                    "baseline_peak_bytes_features_none": rep.baseline_peak_bytes,
                    "offload_d2h_bytes_per_step_issued": int(t.d2h_bytes),
                    "offload_scheduled_bytes_per_step_planned": rep.scheduled_transfer_bytes,
@@ -336,20 +387,23 @@ def run_ours(args) -> None:
 
 
 def extras(args, net, cfg, ex, ms_per_step, local) -> dict:
-    """Roofline of the dominant kernel class, unconstrained-run overhead, CPU baseline."""
+    """Roofline of the dominant kernel classes, memory, unconstrained / parity /
+    fp32-mode runs, CPU baseline."""
     import torch
     import paper_1801_04380_b200 as sn
     from paper_1801_04380_b200.training import Executor
     out: dict = {}
-    # per-action device time of one eager iteration
-    prof = ex.profile()
+    # per-action device time of serial eager iterations (weight gradients on
+    # the compute stream, so every action's event interval holds exactly its
+    # kernels); median of 3
+    profs = [ex.profile() for _ in range(3)]
+    prof = [(statistics.median(p[i][0] for p in profs), lid, typ) for i, (_, lid, typ) in enumerate(profs[0])]
     flops = conv_flops(net, args.batch)
-    t_tensor = 0.0
-    f_tensor = 0.0
-    t_other = 0.0
+    t_tensor = f_tensor = t_other = 0.0
     by_kind: dict = {}
     for ms, lid, typ in prof:
         if lid < 0:
+            t_other += ms
             continue
         kind = net.layers[lid].kind.value
         key = f"{kind}:{['fwd', 'replay', 'bwd'][typ]}"
@@ -359,62 +413,69 @@ def extras(args, net, cfg, ex, ms_per_step, local) -> dict:
             f_tensor += flops[lid][0 if typ == 0 else 1]
         else:
             t_other += ms
+    serial_ms = sum(p[0] for p in prof)
     peaks = measured_peaks()
-    cublas_tf32 = tf32_gemm_peak(f"cuda:{local}")
-    # tf32 tensor peak = half the dense bf16 peak: a kind::tf32 MMA covers K = 8
-    # per instruction where kind::f16 covers K = 16, at the same cycle count
-    # (profiles/r01_mma_probe.txt: 1190 vs 2380 TF/s at 1965 MHz)
-    if peaks.get("bf16_tflops_sustained"):  # kernels timed inside a long step: the sustained figure
-        bf16, src = float(peaks["bf16_tflops_sustained"]), "MEASURED_PEAKS.json bf16_tflops_sustained"
-    elif peaks.get("bf16_tflops"):
-        bf16, src = float(peaks["bf16_tflops"]), "MEASURED_PEAKS.json bf16_tflops (burst)"
-    else:
-        bf16, src = 1590.0, "B200_PROFILING.md fallback 1.59 PF bf16 (MEASURED_PEAKS.json absent)"
-    tf32 = bf16 / 2
+    tf32 = tf32_gemm_peaks(f"cuda:{local}")
     achieved = f_tensor / (t_tensor / 1e3) / 1e12 if t_tensor else 0.0
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01_step_traffic.json")) as fh:
-            tr = json.load(fh)["per_step"]
-        traffic = {"dram_bytes_per_step": tr["conv_fc_gemm"]["dram_bytes_per_step"],
-                   "source": "profiles/r01_step_traffic.json (ncu dram__bytes_read+write, all CONV/FC launches)"}
-    except (OSError, KeyError, ValueError):
-        tr = None
-    out["roofline"] = {"bound": "tensor", "kernel": "CONV/FC implicit-GEMM tcgen05 kind::tf32 (fwd+wgrad+dgrad)",
-                       "achieved": round(achieved, 2), "peak": round(tf32, 2), "unit": "TFLOP/s",
-                       "frac": round(achieved / tf32, 4) if tf32 else None,
-                       "peak_source": f"tf32 = bf16 / 2, bf16 from {src}",
-                       "cublas_tf32_8192_tflops_this_run": round(cublas_tf32, 2),
-                       "traffic": traffic, "algorithmic_tflop_per_step": round(f_tensor / 1e12, 4),
-                       "share_of_step": round(t_tensor / sum(p[0] for p in prof), 4)}
-    if tr and "hbm_layers" in tr:
-        hbm_peak = float(peaks.get("hbm_gbs") or 6650.0)
-        t_layers = t_other / 1e3
-        gbs = tr["hbm_layers"]["dram_bytes_per_step"] / t_layers / 1e9 if t_layers else 0.0
-        out["roofline_hbm_layers"] = {
-            "bound": "hbm", "kernel": "BN / ReLU / JOIN / POOL / softmax / split-K / SGD layer kernels",
-            "achieved": round(gbs, 1), "peak": hbm_peak, "unit": "GB/s", "frac": round(gbs / hbm_peak, 4),
-            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks.get("hbm_gbs") else "B200_PROFILING.md fallback",
-            "traffic": tr["hbm_layers"]["dram_bytes_per_step"],
-            "note": "achieved = ncu DRAM bytes of these launches per step / their summed event time this run"}
+    traffic, why = step_traffic(args.net, args.batch)
+    tr = traffic["per_step"] if traffic else {}
+    out["roofline"] = {
+        "bound": "tensor", "kernel": "CONV/FC implicit-GEMM tcgen05 kind::tf32 (fwd + wgrad + dgrad actions)",
+        "achieved": round(achieved, 2), "peak": round(tf32["sustained"], 2), "unit": "TFLOP/s",
+        "frac": round(achieved / tf32["sustained"], 4),
+        "peak_source": "cuBLAS tf32 8192^3 sustained (3 s back to back) measured in this run -- the CONV/FC "
+                       "actions run inside a long step",
+        "frac_of_burst": round(achieved / tf32["burst"], 4), "cublas_tf32_burst": round(tf32["burst"], 2),
+        "bf16_measured_peaks": {k: peaks.get(k) for k in ("bf16_tflops", "bf16_tflops_sustained")},
+        "traffic": (tr.get("conv_fc_gemm", {}).get("dram_bytes_per_step") if traffic else None),
+        "traffic_source": traffic["source"] if traffic else why,
+        "algorithmic_tflop_per_step": round(f_tensor / 1e12, 4),
+        "event_ms_per_step": round(t_tensor, 4), "share_of_serial_step": round(t_tensor / serial_ms, 4),
+        "how": "achieved = SURVEY 8(d) GEMM FLOPs of every CONV/FC forward and backward action / the sum of their "
+               "CUDA-event intervals in a serial eager iteration on the compute stream (median of 3)"}
+    hbm_peak = float(peaks.get("hbm_gbs") or 6650.0)
+    hl = tr.get("hbm_layers") if traffic else None
+    out["roofline_hbm_layers"] = {
+        "bound": "hbm", "kernel": "BN / ReLU / JOIN / POOL / softmax / split-K / SGD layer kernels",
+        "event_ms_per_step": round(t_other, 4), "peak": hbm_peak, "unit": "GB/s",
+        "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks.get("hbm_gbs") else "B200_PROFILING.md fallback",
+        "traffic": hl["dram_bytes_per_step"] if hl else None,
+        "traffic_source": traffic["source"] if traffic else why}
+    if hl:
+        gbs = hl["dram_bytes_per_step"] / (t_other / 1e3) / 1e9
+        out["roofline_hbm_layers"].update(achieved=round(gbs, 1), frac=round(gbs / hbm_peak, 4),
+                                          how="ncu DRAM bytes of these launches (same libsnexec digest) / their "
+                                              "summed serial event time this run")
     out["time_by_layer_kind_ms"] = {k: round(v, 3) for k, v in sorted(by_kind.items(), key=lambda kv: -kv[1])}
+
+    def side_run(label, cfg2, steps=5, **kw):
+        try:
+            sex = Executor(net, cfg2, device=local, seed=2, **kw)
+            sex.set_inputs(*_inputs(net, args.batch))
+            for _ in range(3):
+                sex.step()
+            ms = statistics.median(sex.step()[1].step_ms for _ in range(steps))
+            extra = {"transfers": sex.transfer_stats()}
+            sex.close()
+            return ms, extra
+        except Exception as exc:  # report, never hide
+            return None, {"error": f"{label}: {str(exc)[:200]}"}
+
     # unconstrained reference run: all features off, pool = whole-iteration residency
-    try:
-        base_pool = ex.report.baseline_peak_bytes + (256 << 20)
-        ucfg = sn.SimConfig(pool_bytes=base_pool, features=sn.Features(), cost=cfg.cost)
-        uex = Executor(net, ucfg, device=local, seed=2)
-        uex.set_inputs(*_inputs(net, args.batch))
-        for _ in range(3):
-            uex.step()
-        ums = []
-        for _ in range(5):
-            ums.append(uex.step()[1].step_ms)
-        uex.close()
-        u = statistics.median(ums)
-        out["unconstrained"] = {"features": "none", "pool_bytes": base_pool, "ms_per_step": round(u, 4),
-                                "overhead_of_memory_schedule": round(ms_per_step / u - 1.0, 4)}
-    except Exception as exc:  # report, never hide
-        out["unconstrained"] = {"error": str(exc)[:200]}
+    base_pool = ex.report.baseline_peak_bytes + (256 << 20)
+    u, uex = side_run("unconstrained", sn.SimConfig(pool_bytes=base_pool, features=sn.Features(), cost=cfg.cost))
+    out["unconstrained"] = {"features": "none", "pool_bytes": base_pool, "ms_per_step": u and round(u, 4),
+                            "overhead_of_memory_schedule": u and round(ms_per_step / u - 1.0, 4), **uex}
+    # parity mode: every copy-out the reference schedules is issued
+    pm, pex = side_run("parity", cfg, elide_backups=False)
+    out["parity_mode"] = {"elide_backups": False, "ms_per_step": pm and round(pm, 4),
+                          "images_per_s": pm and round(args.batch / (pm / 1e3), 2), **pex}
+    # fp32-faithful numerics (3xTF32 split operands) at the same config
+    fm, fex = side_run("fp32", cfg, precision="fp32")
+    out["fp32_mode"] = {"precision": "fp32 (3xTF32 split operands, fp32-level products)",
+                        "ms_per_step": fm and round(fm, 4),
+                        "images_per_s": fm and round(args.batch / (fm / 1e3), 2),
+                        **({"error": fex["error"]} if "error" in fex else {})}
     out["cpu_baseline"] = cpu_baseline(args.net, sample=min(args.batch, 16))
     return out
 

@@ -271,9 +271,17 @@ int sn_exec_step_host_pipelined(sn_exec* ex, const float* images_host, const int
 int sn_exec_read_tensor(sn_exec* ex, int32_t kind, int32_t layer, float* dst, int64_t n_floats);
 /* Run one iteration eagerly with a CUDA event between consecutive actions on
  * the compute stream; per action: device ms, layer id (-1 none) and type
- * (0 forward, 1 replay, 2 backward, 3 copy/sync).  For roofline accounting. */
+ * (0 forward, 1 replay, 2 backward, 3 copy/sync).  For roofline accounting:
+ * the weight gradients run on the compute stream too (serial), so each
+ * action's interval holds exactly its own kernels. */
 int sn_exec_profile(sn_exec* ex, float* action_ms, int32_t* action_layer, int32_t* action_type, size_t cap,
                     size_t* n);
+/* Per-action kernel census of one iteration (for per-launch tables): action i
+ * of sn_exec_profile launched action_kernels[i] kernels; `names` receives
+ * their mangled function names, '\n'-terminated, each action's list closed
+ * by a 0x1e byte (truncated to names_cap).  Captured from one serial
+ * iteration (weight gradients on the compute stream), nothing executed. */
+int sn_exec_census(sn_exec* ex, int32_t* action_kernels, size_t cap, char* names, size_t names_cap, size_t* n);
 /* Launch the SGD update alone (after an external gradient all-reduce). */
 int sn_exec_apply_update(sn_exec* ex, float lr, float grad_scale);
 /* CONV weight gradients whose split-K partials live in the conv workspace the
@@ -286,6 +294,30 @@ int sn_exec_workspace_use(const sn_exec* ex, int32_t* wgrad_in_pool, int32_t* wg
  * exposed, non-overlapped transfer time).  Synchronises the compute stream. */
 int sn_exec_transfer_stats(sn_exec* ex, int64_t* d2h_bytes, double* d2h_ms, int64_t* h2d_bytes, double* h2d_ms,
                            double* exposed_ms);
+/* Device (and pinned host) memory the executor allocated, by purpose.  The
+ * arena is the one pool allocation (ceil_KiB(pool_bytes), reference
+ * simulator.py:204); everything else is outside the reference's residency
+ * accounting (parameters and gradients, costmodel.py:3-6) or executor-owned. */
+typedef struct sn_exec_mem {
+  int64_t arena_bytes;
+  int64_t params_grads_bytes;
+  int64_t layer_state_bytes;    /* BN saved / running statistics, max-pool argmax bytes */
+  int64_t input_bytes;          /* images, labels, the stem's padded copy, staging */
+  int64_t wgrad_scratch_bytes;  /* weight-gradient scratch outside the pool (partials that
+                                   did not fit their granted workspace, reductions) */
+  int64_t other_scratch_bytes;  /* FC split-K, weight transposes, BN tile statistics, ... */
+  int64_t host_stash_bytes;     /* pinned host memory of copied-out tensors */
+  int64_t device_total_bytes;   /* sum of the device categories */
+  int64_t wgrad_partials_outside_pool_bytes;
+  int64_t planned_arena_high_water; /* the planner's BlockPool high water */
+} sn_exec_mem;
+int sn_exec_memory(const sn_exec* ex, sn_exec_mem* out);
+/* Measured arena use: sn_exec_arena_fill writes a sentinel (0xFF bytes, a NaN
+ * no kernel produces) over the whole arena; after a step, sn_exec_arena_scan
+ * returns the end of the highest 1 KiB block any kernel or copy wrote
+ * (high_water_bytes) and the bytes of all written blocks. */
+int sn_exec_arena_fill(sn_exec* ex);
+int sn_exec_arena_scan(sn_exec* ex, int64_t* high_water_bytes, int64_t* touched_bytes);
 /* Stream the executor launches on (for cross-library ordering). */
 void* sn_exec_stream(sn_exec* ex);
 

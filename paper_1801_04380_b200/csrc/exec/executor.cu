@@ -142,6 +142,20 @@ struct sn_exec {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t gexec = nullptr;
   bool graph_ready = false;
+  // profiling (sn_exec_profile / sn_exec_census): run the side-stream weight
+  // gradients on the compute stream, so per-action events on s0 bracket all of
+  // an action's kernels and nothing overlaps
+  bool serial = false;
+  int32_t* marker = nullptr;  // census: per-action memset marker target
+  // device / pinned bytes by category (sn_exec_memory)
+  enum { M_ARENA, M_PARAMS, M_STATE, M_INPUT, M_WGRAD, M_OTHER, M_HOST, M_N };
+  int64_t mem[M_N] = {};
+  int64_t wgrad_partial_outside = 0;  // floats of split-K scratch the plan's workspaces could not hold
+  template <class T>
+  void dmalloc(T** p, int64_t bytes, int cat, const char* what) {
+    ck(cudaMalloc(reinterpret_cast<void**>(p), static_cast<size_t>(bytes)), what);
+    mem[cat] += bytes;
+  }
 
   cudaEvent_t new_event() {
     cudaEvent_t e;
@@ -281,11 +295,11 @@ void alloc_device(sn_exec* ex) {
   const snp::Plan& P = ex->plan->plan;
   const Net& net = P.net;
   ex->arena_bytes = P.pool_capacity_blocks * snp::kBlockBytes;
-  ck(cudaMalloc(&ex->arena, static_cast<size_t>(ex->arena_bytes)), "cudaMalloc(arena)");
-  ck(cudaMalloc(&ex->params, ex->n_params * sizeof(float)), "cudaMalloc(params)");
-  ck(cudaMalloc(&ex->grads, ex->n_params * sizeof(float)), "cudaMalloc(grads)");
+  ex->dmalloc(&ex->arena, ex->arena_bytes, sn_exec::M_ARENA, "cudaMalloc(arena)");
+  ex->dmalloc(&ex->params, ex->n_params * 4, sn_exec::M_PARAMS, "cudaMalloc(params)");
+  ex->dmalloc(&ex->grads, ex->n_params * 4, sn_exec::M_PARAMS, "cudaMalloc(grads)");
   ck(cudaMemset(ex->grads, 0, ex->n_params * sizeof(float)), "memset");
-  ck(cudaMalloc(&ex->state, ex->n_state * sizeof(float)), "cudaMalloc(state)");
+  ex->dmalloc(&ex->state, ex->n_state * 4, sn_exec::M_STATE, "cudaMalloc(state)");
   // BN state: stats {mean 0, invstd 1}, running {mean 0, var 1}
   std::vector<float> st(ex->n_state, 0.f);
   int64_t wt = 0, red = sn::red_scratch_floats(4), partial = 0;
@@ -303,14 +317,18 @@ void alloc_device(sn_exec* ex) {
     if (l.kind == snp::FC) wt = std::max(wt, l.w_n);  // fc_dgrad's transposed weights
   }
   ck(cudaMemcpy(ex->state, st.data(), st.size() * sizeof(float), cudaMemcpyHostToDevice), "memcpy(state)");
-  // split-K partial scratch (outside the arena, like cuDNN's internal buffers):
-  // sized by the largest layer at its chosen split count, capped at 64 Mi floats.
+  // split-K partials: a CONV weight gradient writes them into the conv
+  // workspace its step was granted (Compiler::backward) and only otherwise
+  // into wgrad scratch outside the pool, sized by those layers alone
+  // (Compiler::size_wgrad_scratch); the split counts (capped at 64 Mi
+  // floats of partials) are fixed per layer, so the summation order -- and
+  // the gradients -- do not depend on the schedule.  `partial` here is the
+  // FC layers' own split-K scratch.
   const int64_t cap = 64ll << 20;
   for (int i = 0; i < net.n; ++i) {
     LayerRt& l = ex->L[i];
     if (l.kind == snp::CONV) {
       l.wgrad_splits = sn::conv_wgrad_splits(l.conv, cap);
-      partial = std::max(partial, static_cast<int64_t>(l.wgrad_splits) * l.conv.R * l.conv.S * l.conv.C * l.conv.K);
     } else if (l.kind == snp::FC) {
       l.fc_splits = sn::fc_splits(ex->B, l.fc_in, l.C, cap);
       partial = std::max(partial, static_cast<int64_t>(l.fc_splits) * ex->B * std::max(l.fc_in, l.C));
@@ -318,10 +336,7 @@ void alloc_device(sn_exec* ex) {
       partial = std::max(partial, static_cast<int64_t>(l.wgrad_splits) * l.fc_in * l.C);
     }
   }
-  if (ex->stem_layer >= 0) {
-    partial = std::max(partial, sn::stem_wgrad_partial_floats(ex->L[ex->stem_layer].conv));
-    wt = std::max(wt, sn::stem_weight_floats(ex->L[ex->stem_layer].conv));
-  }
+  if (ex->stem_layer >= 0) wt = std::max(wt, sn::stem_weight_floats(ex->L[ex->stem_layer].conv));
   int64_t tstats = 64;
   for (int i = 0; i < net.n; ++i) {
     LayerRt& l = ex->L[i];
@@ -329,43 +344,43 @@ void alloc_device(sn_exec* ex) {
     l.stats_tiles = sn::conv_fwd_stats_tiles(l.conv, i == ex->stem_layer, &l.stats_rows);
     tstats = std::max(tstats, static_cast<int64_t>(l.stats_tiles) * 4 * l.C);
   }
-  ck(cudaMalloc(&ex->tstats, tstats * sizeof(float)), "cudaMalloc(tile stats)");
+  ex->dmalloc(&ex->tstats, tstats * 4, sn_exec::M_OTHER, "cudaMalloc(tile stats)");
   ex->partial_cap = std::max<int64_t>(partial, 64);
-  ck(cudaMalloc(&ex->partial, ex->partial_cap * sizeof(float)), "cudaMalloc(partial)");
-  ck(cudaMalloc(&ex->wt_scratch, std::max<int64_t>(wt, 64) * sizeof(float)), "cudaMalloc(wt)");
-  ck(cudaMalloc(&ex->red, red * sizeof(float)), "cudaMalloc(red)");
-  ck(cudaMalloc(&ex->partial_w, ex->partial_cap * sizeof(float)), "cudaMalloc(partial_w)");
-  ck(cudaMalloc(&ex->wt_w, std::max<int64_t>(wt, 64) * sizeof(float)), "cudaMalloc(wt_w)");
-  ck(cudaMalloc(&ex->red_w, red * sizeof(float)), "cudaMalloc(red_w)");
+  ex->dmalloc(&ex->partial, ex->partial_cap * 4, sn_exec::M_OTHER, "cudaMalloc(partial)");
+  ex->dmalloc(&ex->wt_scratch, std::max<int64_t>(wt, 64) * 4, sn_exec::M_OTHER, "cudaMalloc(wt)");
+  ex->dmalloc(&ex->red, red * 4, sn_exec::M_OTHER, "cudaMalloc(red)");
+  ex->dmalloc(&ex->wt_w, std::max<int64_t>(wt, 64) * 4, sn_exec::M_WGRAD, "cudaMalloc(wt_w)");
+  ex->dmalloc(&ex->red_w, red * 4, sn_exec::M_WGRAD, "cudaMalloc(red_w)");
   int64_t pool_bytes = 256;
   for (int i = 0; i < net.n; ++i)
     if (ex->L[i].kind == snp::POOL) pool_bytes = std::max(pool_bytes, sn::pool_scratch_bytes(ex->L[i].pool));
-  ck(cudaMalloc(&ex->pool_scratch, static_cast<size_t>(pool_bytes)), "cudaMalloc(pool scratch)");
+  ex->dmalloc(&ex->pool_scratch, pool_bytes, sn_exec::M_OTHER, "cudaMalloc(pool scratch)");
   // saved max-pool argmaxes: layer state outside the pool accounting, like the
   // BN saved statistics (one byte per output element)
   for (int i = 0; i < net.n; ++i) {
     LayerRt& l = ex->L[i];
     if (l.kind == snp::POOL && sn::pool_saves_argmax(l.pool))
-      ck(cudaMalloc(&l.argmax, static_cast<size_t>(l.pool.N) * l.pool.P * l.pool.Q * l.pool.C), "cudaMalloc(argmax)");
+      ex->dmalloc(&l.argmax, static_cast<int64_t>(l.pool.N) * l.pool.P * l.pool.Q * l.pool.C, sn_exec::M_STATE,
+                  "cudaMalloc(argmax)");
   }
   if (ex->data_id < 0) xfail(SN_EK_UNSUPPORTED, "numeric execution needs a DATA layer");
   const LayerRt& data = ex->L[ex->data_id];
   ex->image_floats = static_cast<int64_t>(ex->B) * data.H * data.W * data.C_raw;
-  ck(cudaMalloc(&ex->images, ex->image_floats * sizeof(float)), "cudaMalloc(images)");
+  ex->dmalloc(&ex->images, ex->image_floats * 4, sn_exec::M_INPUT, "cudaMalloc(images)");
   ck(cudaMemset(ex->images, 0, ex->image_floats * sizeof(float)), "memset(images)");
   if (ex->stem_layer >= 0 || data.C != data.C_raw) {
     const int64_t n = ex->stem_layer >= 0 ? sn::stem_padded_floats(ex->L[ex->stem_layer].conv)
                                           : static_cast<int64_t>(ex->B) * data.per_sample;
-    ck(cudaMalloc(&ex->data_buf, n * sizeof(float)), "cudaMalloc(data)");
+    ex->dmalloc(&ex->data_buf, n * 4, sn_exec::M_INPUT, "cudaMalloc(data)");
     ck(cudaMemset(ex->data_buf, 0, n * sizeof(float)), "memset(data)");
   } else {
     ex->data_buf = ex->images;
   }
-  ck(cudaMalloc(&ex->labels, ex->B * sizeof(int32_t)), "cudaMalloc(labels)");
+  ex->dmalloc(&ex->labels, ex->B * 4, sn_exec::M_INPUT, "cudaMalloc(labels)");
   ck(cudaMemset(ex->labels, 0, ex->B * sizeof(int32_t)), "memset(labels)");
-  ck(cudaMalloc(&ex->loss_rows, ex->B * sizeof(float)), "cudaMalloc(loss_rows)");
-  ck(cudaMalloc(&ex->loss, 4 * sizeof(float)), "cudaMalloc(loss)");
-  ck(cudaMalloc(&ex->iteration, sizeof(uint32_t) * 4), "cudaMalloc(iteration)");
+  ex->dmalloc(&ex->loss_rows, ex->B * 4, sn_exec::M_OTHER, "cudaMalloc(loss_rows)");
+  ex->dmalloc(&ex->loss, 16, sn_exec::M_OTHER, "cudaMalloc(loss)");
+  ex->dmalloc(&ex->iteration, 16, sn_exec::M_OTHER, "cudaMalloc(iteration)");
   ck(cudaMemset(ex->iteration, 0, sizeof(uint32_t) * 4), "memset(iteration)");
 }
 
@@ -495,6 +510,7 @@ struct Compiler {
     char* host = ex->stash[lid];
     if (!host) {
       ck(cudaHostAlloc(&host, static_cast<size_t>(nbytes), cudaHostAllocPortable), "cudaHostAlloc(stash)");
+      ex->mem[sn_exec::M_HOST] += nbytes;
       ex->stash[lid] = host;
     }
     const float* src = ptr(snp::K_ACT, lid);
@@ -753,8 +769,7 @@ struct Compiler {
             ws = ptr(snp::K_WS, static_cast<int>(bev.d));
             ws_floats = where[wkey].second * snp::kBlockBytes / static_cast<int64_t>(sizeof(float));
           }
-          const int64_t slice = static_cast<int64_t>(cs.R) * cs.S * cs.C * cs.K;
-          const int64_t need = lid == ex->stem_layer ? sn::stem_wgrad_partial_floats(cs) : sp * slice;
+          const int64_t need = wgrad_partial_floats(lid);
           if (ws && ws_floats >= need) {
             part_w = ws;
             side_reads[wkey] = wdone;  // written on s3 after the tape frees it
@@ -765,20 +780,22 @@ struct Compiler {
         }
         if (lid == ex->stem_layer) {  // DATA has no gradient
           push([=] {
+            const cudaStream_t sw = e->serial ? st : s3;
             ck(cudaEventRecord(ready, st), "record");
-            ck(cudaStreamWaitEvent(s3, ready, 0), "wait");
-            ck(sn::conv_stem_wgrad(cs, x, dy, part_w, wt_w, dw, db, red_w, s3), "conv_stem_wgrad");
-            ck(cudaEventRecord(wdone, s3), "record");
+            ck(cudaStreamWaitEvent(sw, ready, 0), "wait");
+            ck(sn::conv_stem_wgrad(cs, x, dy, part_w, wt_w, dw, db, red_w, sw), "conv_stem_wgrad");
+            ck(cudaEventRecord(wdone, sw), "record");
           }, 3 + nbias);
           break;
         }
         const int ndgrad = !dx ? 0 : sn::conv_dgrad_launches(cs);
         const int nwgrad = sn::conv_wgrad_launches(cs, sp, db != nullptr);
         push([=] {
+          const cudaStream_t sw = e->serial ? st : s3;
           ck(cudaEventRecord(ready, st), "record");
-          ck(cudaStreamWaitEvent(s3, ready, 0), "wait");
-          ck(sn::conv_wgrad(cs, x, dy, dw, db, part_w, sp, red_w, s3), "conv_wgrad");
-          ck(cudaEventRecord(wdone, s3), "record");
+          ck(cudaStreamWaitEvent(sw, ready, 0), "wait");
+          ck(sn::conv_wgrad(cs, x, dy, dw, db, part_w, sp, red_w, sw), "conv_wgrad");
+          ck(cudaEventRecord(wdone, sw), "record");
           if (dx) ck(sn::conv_dgrad(cs, dy, w, wt, dx, acc, st), "conv_dgrad");
         }, nwgrad + ndgrad);
         (void)nbias;
@@ -1341,6 +1358,34 @@ struct Compiler {
     ex->elided = elide_out;
   }
 
+  // split-K partial floats of a CONV weight gradient
+  int64_t wgrad_partial_floats(int lid) const {
+    const LayerRt& l = ex->L[lid];
+    if (lid == ex->stem_layer) return sn::stem_wgrad_partial_floats(l.conv);
+    return static_cast<int64_t>(l.wgrad_splits) * l.conv.R * l.conv.S * l.conv.C * l.conv.K;
+  }
+
+  // The wgrad scratch outside the pool holds only the partials of the CONV
+  // backward steps whose granted workspace (the planner's selection,
+  // reference simulator.py:624-654) is too small for them.
+  void size_wgrad_scratch() {
+    std::unordered_map<int64_t, int64_t> ws_blocks;  // ws key id -> blocks of its latest allocation
+    int64_t outside = 0;
+    for (const auto& ev : P.tape) {
+      if (ev.op == 'A' && ev.a == snp::K_WS) ws_blocks[ev.b] = ev.d;
+      if (ev.op != 'B' || net.kind[ev.b] != snp::CONV) continue;
+      int64_t have = 0;
+      if (ev.d >= 0) {
+        auto it = ws_blocks.find(ev.d);
+        if (it != ws_blocks.end()) have = it->second * snp::kBlockBytes / static_cast<int64_t>(sizeof(float));
+      }
+      const int64_t need = wgrad_partial_floats(ev.b);
+      if (have < need) outside = std::max(outside, need);
+    }
+    ex->wgrad_partial_outside = outside;
+    ex->dmalloc(&ex->partial_w, std::max<int64_t>(outside, 64) * 4, sn_exec::M_WGRAD, "cudaMalloc(partial_w)");
+  }
+
   // DATA layer: lay the user's images out the way the consumers read them.
   void prepare_inputs() {
     const LayerRt& d = ex->L[data_id];
@@ -1362,6 +1407,7 @@ struct Compiler {
 
   void compile() {
     plan_fusions();
+    size_wgrad_scratch();
     prepare_inputs();
     for (size_t ti = 0; ti < P.tape.size(); ++ti) {
       const snp::Event& ev = P.tape[ti];
@@ -1417,7 +1463,9 @@ struct Compiler {
     if (used_s3) {
       cudaEvent_t j = ex->new_event();
       cudaStream_t s3 = ex->s3;
+      sn_exec* e = ex;
       push([=] {
+        if (e->serial) return;  // profiling: the weight gradients ran on s0
         ck(cudaEventRecord(j, s3), "record");
         ck(cudaStreamWaitEvent(s0, j, 0), "wait");
       }, 0);
@@ -1500,7 +1548,7 @@ void destroy(sn_exec* ex) {
   void* bufs[] = {ex->arena, ex->params, ex->grads, ex->state, ex->images, ex->labels, ex->loss_rows, ex->loss,
                   ex->iteration, ex->wt_scratch, ex->partial, ex->red, ex->tstats, ex->pool_scratch,
                   ex->partial_w, ex->red_w, ex->wt_w, ex->images_stage, ex->labels_stage,
-                  const_cast<float**>(ex->ptr_table)};
+                  const_cast<float**>(ex->ptr_table), ex->marker};
   for (void* b : bufs)
     if (b) cudaFree(b);
   for (auto& l : ex->L)
@@ -1546,7 +1594,7 @@ int sn_exec_create(const sn_plan* plan, const sn_net_desc* /*net*/, const sn_lay
     Compiler comp(ex);
     comp.compile();
     const size_t nptr = std::max<size_t>(1, ex->ptr_host.size());
-    ck(cudaMalloc(&ex->ptr_table, nptr * sizeof(float*)), "cudaMalloc(ptr_table)");
+    ex->dmalloc(&ex->ptr_table, static_cast<int64_t>(nptr * sizeof(float*)), sn_exec::M_OTHER, "cudaMalloc(ptr_table)");
     if (!ex->ptr_host.empty())
       ck(cudaMemcpy(ex->ptr_table, ex->ptr_host.data(), ex->ptr_host.size() * sizeof(float*), cudaMemcpyHostToDevice),
          "memcpy(ptr_table)");
@@ -1662,8 +1710,8 @@ int sn_exec_step_host_pipelined(sn_exec* ex, const float* images_host, const int
     const size_t ibytes = ex->image_floats * sizeof(float), lbytes = ex->B * sizeof(int32_t);
     if (!ex->s4) {
       ck(cudaStreamCreateWithFlags(&ex->s4, cudaStreamNonBlocking), "stream");
-      ck(cudaMalloc(&ex->images_stage, ibytes), "cudaMalloc(images_stage)");
-      ck(cudaMalloc(&ex->labels_stage, lbytes), "cudaMalloc(labels_stage)");
+      ex->dmalloc(&ex->images_stage, static_cast<int64_t>(ibytes), sn_exec::M_INPUT, "cudaMalloc(images_stage)");
+      ex->dmalloc(&ex->labels_stage, static_cast<int64_t>(lbytes), sn_exec::M_INPUT, "cudaMalloc(labels_stage)");
       ck(cudaEventCreateWithFlags(&ex->staged_ev, cudaEventDisableTiming), "event");
       ck(cudaEventCreateWithFlags(&ex->consumed_ev, cudaEventDisableTiming), "event");
       ck(cudaEventRecord(ex->consumed_ev, ex->s0), "record");
@@ -1717,12 +1765,18 @@ int sn_exec_profile(sn_exec* ex, float* action_ms, int32_t* action_layer, int32_
     PrecisionScope prec(ex);
     std::vector<cudaEvent_t> ev(ex->prog.size() + 1);
     for (auto& e : ev) ck(cudaEventCreate(&e), "event");
+    ex->serial = true;
+    struct Restore {
+      sn_exec* e;
+      ~Restore() { e->serial = false; }
+    } restore{ex};
     ck(cudaEventRecord(ev[0], ex->s0), "record");
     for (size_t i = 0; i < ex->prog.size(); ++i) {
       ex->prog[i].fn();
       ck(cudaEventRecord(ev[i + 1], ex->s0), "record");
     }
     ck(cudaStreamSynchronize(ex->s0), "sync");
+    ck(cudaDeviceSynchronize(), "sync");
     for (size_t i = 0; i < ex->prog.size(); ++i) {
       float ms = 0.f;
       ck(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]), "elapsed");
@@ -1731,6 +1785,78 @@ int sn_exec_profile(sn_exec* ex, float* action_ms, int32_t* action_layer, int32_
       if (action_type) action_type[i] = ex->prog[i].type;
     }
     for (auto& e : ev) cudaEventDestroy(e);
+  });
+}
+
+int sn_exec_census(sn_exec* ex, int32_t* action_kernels, size_t cap, char* names, size_t names_cap, size_t* n) {
+  if (!ex || !n) return xset(SN_EK_INTERNAL, "null argument");
+  *n = ex->prog.size();
+  if (!action_kernels) return SN_OK;
+  if (cap < ex->prog.size()) return xset(SN_EK_INTERNAL, "output buffer too small");
+  return xguard([&] {
+    ck(cudaSetDevice(ex->device), "cudaSetDevice");
+    PrecisionScope prec(ex);
+    ck(cudaDeviceSynchronize(), "sync");
+    if (!ex->marker) ex->dmalloc(&ex->marker, 4, sn_exec::M_OTHER, "cudaMalloc(marker)");
+    ex->serial = true;
+    struct Restore {
+      sn_exec* e;
+      ~Restore() { e->serial = false; }
+    } restore{ex};
+    // one serial iteration captured with a memset marker (value = action
+    // index) before every action; kernel nodes between markers belong to it
+    cudaGraph_t g = nullptr;
+    ck(cudaStreamBeginCapture(ex->s0, cudaStreamCaptureModeThreadLocal), "BeginCapture");
+    try {
+      for (size_t i = 0; i < ex->prog.size(); ++i) {
+        ck(cudaMemsetAsync(ex->marker, static_cast<int>(i & 0xff), sizeof(int32_t), ex->s0), "marker");
+        ex->prog[i].fn();
+      }
+    } catch (...) {
+      cudaStreamEndCapture(ex->s0, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    ck(cudaStreamEndCapture(ex->s0, &g), "EndCapture");
+    size_t nn = 0;
+    ck(cudaGraphGetNodes(g, nullptr, &nn), "GraphGetNodes");
+    std::vector<cudaGraphNode_t> nodes(nn);
+    ck(cudaGraphGetNodes(g, nodes.data(), &nn), "GraphGetNodes");
+    std::vector<std::string> nm(ex->prog.size());
+    std::fill(action_kernels, action_kernels + ex->prog.size(), 0);
+    long cur = -1;
+    std::string err;
+    for (cudaGraphNode_t nd : nodes) {
+      cudaGraphNodeType t;
+      ck(cudaGraphNodeGetType(nd, &t), "GraphNodeGetType");
+      if (t == cudaGraphNodeTypeMemset) {
+        cudaMemsetParams mp;
+        ck(cudaGraphMemsetNodeGetParams(nd, &mp), "MemsetNodeGetParams");
+        if (mp.dst == ex->marker) {
+          ++cur;
+          if (cur >= static_cast<long>(ex->prog.size()) || static_cast<int>(mp.value) != static_cast<int>(cur & 0xff))
+            err = "census markers out of order";
+          continue;
+        }
+      }
+      if (t != cudaGraphNodeTypeKernel || cur < 0 || cur >= static_cast<long>(ex->prog.size())) continue;
+      cudaKernelNodeParams kp;
+      ck(cudaGraphKernelNodeGetParams(nd, &kp), "KernelNodeGetParams");
+      const char* fname = nullptr;
+      if (cudaFuncGetName(&fname, kp.func) != cudaSuccess || !fname) fname = "?";
+      ++action_kernels[cur];
+      nm[cur] += fname;
+      nm[cur] += '\n';
+    }
+    cudaGraphDestroy(g);
+    if (!err.empty()) xfail(SN_EK_INTERNAL, err);
+    if (names && names_cap) {
+      std::string all;
+      for (size_t i = 0; i < nm.size(); ++i) all += nm[i] + "\x1e";  // record separator per action
+      const size_t k = std::min(all.size(), names_cap - 1);
+      std::memcpy(names, all.data(), k);
+      names[k] = 0;
+    }
   });
 }
 
@@ -1753,6 +1879,72 @@ int sn_exec_transfer_stats(sn_exec* ex, int64_t* d2h_bytes, double* d2h_ms, int6
     if (h2d_bytes) *h2d_bytes = bytes[1];
     if (h2d_ms) *h2d_ms = ms[1];
     if (exposed_ms) *exposed_ms = ms[2];
+  });
+}
+
+namespace {
+constexpr uint32_t kArenaSentinel = 0xFFFFFFFFu;  // a NaN no kernel writes
+__global__ void arena_scan_kernel(const uint32_t* __restrict__ a, int64_t blocks, unsigned long long* hi,
+                                  unsigned long long* touched) {
+  // one warp per 1 KiB block (256 words, 8 per lane)
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t b = w0; b < blocks; b += nw) {
+    const uint4* p = reinterpret_cast<const uint4*>(a + b * 256) + lane * 2;
+    const uint4 x = p[0], y = p[1];
+    const bool used = (x.x & x.y & x.z & x.w & y.x & y.y & y.z & y.w) != kArenaSentinel;
+    if (__any_sync(0xffffffffu, used) && lane == 0) {
+      atomicMax(hi, static_cast<unsigned long long>(b + 1));
+      atomicAdd(touched, 1ull);
+    }
+  }
+}
+}  // namespace
+
+int sn_exec_memory(const sn_exec* ex, sn_exec_mem* out) {
+  if (!ex || !out) return xset(SN_EK_INTERNAL, "null argument");
+  out->arena_bytes = ex->mem[sn_exec::M_ARENA];
+  out->params_grads_bytes = ex->mem[sn_exec::M_PARAMS];
+  out->layer_state_bytes = ex->mem[sn_exec::M_STATE];
+  out->input_bytes = ex->mem[sn_exec::M_INPUT];
+  out->wgrad_scratch_bytes = ex->mem[sn_exec::M_WGRAD];
+  out->other_scratch_bytes = ex->mem[sn_exec::M_OTHER];
+  out->host_stash_bytes = ex->mem[sn_exec::M_HOST];
+  out->device_total_bytes = 0;
+  for (int c = 0; c < sn_exec::M_HOST; ++c) out->device_total_bytes += ex->mem[c];
+  out->wgrad_partials_outside_pool_bytes = ex->wgrad_partial_outside * 4;
+  out->planned_arena_high_water = ex->plan->plan.report.pool_high_water_bytes;
+  return SN_OK;
+}
+
+int sn_exec_arena_fill(sn_exec* ex) {
+  if (!ex) return xset(SN_EK_INTERNAL, "null argument");
+  return xguard([&] {
+    ck(cudaSetDevice(ex->device), "cudaSetDevice");
+    ck(cudaMemsetAsync(ex->arena, 0xFF, static_cast<size_t>(ex->arena_bytes), ex->s0), "memset(arena)");
+    ck(cudaStreamSynchronize(ex->s0), "sync");
+  });
+}
+
+int sn_exec_arena_scan(sn_exec* ex, int64_t* high_water_bytes, int64_t* touched_bytes) {
+  if (!ex) return xset(SN_EK_INTERNAL, "null argument");
+  return xguard([&] {
+    ck(cudaSetDevice(ex->device), "cudaSetDevice");
+    ck(cudaDeviceSynchronize(), "sync");
+    unsigned long long* d = nullptr;
+    ck(cudaMalloc(&d, 2 * sizeof(unsigned long long)), "cudaMalloc(scan)");
+    cudaMemsetAsync(d, 0, 2 * sizeof(unsigned long long), ex->s0);
+    const int64_t blocks = ex->arena_bytes / snp::kBlockBytes;
+    arena_scan_kernel<<<148 * 8, 256, 0, ex->s0>>>(reinterpret_cast<const uint32_t*>(ex->arena), blocks, d, d + 1);
+    unsigned long long h[2] = {0, 0};
+    const cudaError_t e1 = cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, ex->s0);
+    const cudaError_t e2 = cudaStreamSynchronize(ex->s0);
+    cudaFree(d);
+    ck(e1, "scan D2H");
+    ck(e2, "scan");
+    if (high_water_bytes) *high_water_bytes = static_cast<int64_t>(h[0]) * snp::kBlockBytes;
+    if (touched_bytes) *touched_bytes = static_cast<int64_t>(h[1]) * snp::kBlockBytes;
   });
 }
 

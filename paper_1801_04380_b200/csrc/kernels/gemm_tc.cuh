@@ -18,8 +18,15 @@
 // lo = x - hi (exact in fp32) written to a twin buffer of the same swizzled
 // layout, and the issuer accumulates hi.hi + hi.lo + lo.hi per K = 8 step.
 // The dropped lo.lo term and the tf32 rounding of lo are ~2^-22 relative:
-// fp32-level products with fp32 accumulation, at 3x the MMA work and half
-// the pipeline depth (the twins double the smem per stage).
+// fp32-level products, at 3x the MMA work and half the pipeline depth (the
+// twins double the smem per stage).  The tensor core's accumulation into TMEM
+// is not round-to-nearest: measured (tools/precision_probe.py) it loses about
+// 2^-25 of the running sum per MMA, toward zero, so a long K chain drifts
+// (K = 2048: 2.3e-5 on positive data).  SPLIT3 therefore restarts the TMEM
+// accumulator every kDrainGroup k blocks: the producer warps add each group's
+// partial into a second TMEM region (fp32 round-to-nearest on the CUDA cores)
+// and the final epilogue adds the two -- the drift is bounded by one group's
+// 12 * kDrainGroup MMAs whatever K is.
 //
 // The operand gathers are policy objects (see conv loaders in conv_tc.cu):
 //   struct Loader { __device__ void tile_init(int r0, void* scratch, int tid);
@@ -50,6 +57,7 @@ template <int BN>
 __host__ __device__ constexpr uint32_t tmem_cols() {
   return BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
 }
+constexpr int kDrainGroup = 4;  // SPLIT3: k blocks per TMEM accumulation chain
 
 // MN-major tile of 32 k-rows x R mn-elements in the SWIZZLE_128B_BASE32B
 // canonical layout: MN atoms (32 elements x 4 k rows = 512 B) are adjacent
@@ -99,7 +107,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
   uint64_t* empty = full + STAGES;
   uint64_t* done = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  uint64_t* drain_full = done + 1;   // SPLIT3: a group's partial is complete in TMEM
+  uint64_t* drain_empty = done + 2;  // SPLIT3: ... and folded into the running sum
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 3);
   uint8_t* scratch_a = smem + L::SCRATCH_OFF;
   uint8_t* scratch_b = scratch_a + kScratchBytes;
 
@@ -118,9 +128,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(done, 1);
+    mbar_init(drain_full, 1);
+    mbar_init(drain_empty, kProducers);
     fence_mbar_init();
   }
-  if (warp == 4) tmem_alloc(tmem_slot, tmem_cols<BN>());
+  constexpr uint32_t kTmemCols = tmem_cols<BN>() * (SPLIT3 ? 2 : 1);  // SPLIT3: + the running sum
+  if (warp == 4) tmem_alloc(tmem_slot, kTmemCols);
   if (tid < kProducers) {
     la.tile_init(m0, scratch_a, tid);
     lb.tile_init(n0, scratch_b, tid);
@@ -145,6 +158,32 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       fence_proxy_async();
       mbar_arrive(&full[s]);
     };
+    const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
+    const uint32_t run_col = tmem_cols<BN>();
+    // SPLIT3: after publishing the last block of a non-final accumulation
+    // group, fold that group's TMEM partial into the running sum (RN adds)
+    auto drain_after = [&](int j) {
+      if constexpr (SPLIT3) {
+        if (j % kDrainGroup != kDrainGroup - 1 || j == nkb - 1) return;
+        const int d = j / kDrainGroup;
+        mbar_wait(drain_full, d & 1);
+        tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          float v[32];
+          tmem_ld32(tmem + lane_base + static_cast<uint32_t>(c), v);
+          if (d > 0) {
+            float r[32];
+            tmem_ld32(tmem + lane_base + run_col + static_cast<uint32_t>(c), r);
+#pragma unroll
+            for (int q = 0; q < 32; ++q) v[q] += r[q];
+          }
+          tmem_st32(tmem + lane_base + run_col + static_cast<uint32_t>(c), v);
+        }
+        tc_fence_before();
+        mbar_arrive(drain_empty);
+      }
+    };
     for (int i = 0; i < nkb; ++i) {
       const int s = i % STAGES;
       if (i >= STAGES) mbar_wait(&empty[s], ((i / STAGES) - 1) & 1);
@@ -154,19 +193,30 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       if (i >= LAG) {
         cp_async_wait<LAG>();
         publish(i - LAG);
+        drain_after(i - LAG);
       }
     }
     cp_async_wait<0>();
-    for (int j = (nkb > LAG ? nkb - LAG : 0); j < nkb; ++j) publish(j);
+    for (int j = (nkb > LAG ? nkb - LAG : 0); j < nkb; ++j) {
+      publish(j);
+      drain_after(j);
+    }
 
     // ---------------- epilogue ----------------
     mbar_wait(done, 0);
     tc_fence_after();
     const int row = warp * 32 + lane;
+    const bool drained = SPLIT3 && nkb > kDrainGroup;
 #pragma unroll 1
     for (int c = 0; c < BN; c += 32) {
       float v[32];
-      tmem_ld32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + static_cast<uint32_t>(c), v);
+      tmem_ld32(tmem + lane_base + static_cast<uint32_t>(c), v);
+      if (drained) {
+        float r[32];
+        tmem_ld32(tmem + lane_base + run_col + static_cast<uint32_t>(c), r);
+#pragma unroll
+        for (int q = 0; q < 32; ++q) v[q] += r[q];
+      }
       epi.store(m0 + row, n0 + c, v, blockIdx.z);
     }
     tc_fence_before();
@@ -175,6 +225,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     constexpr uint32_t idesc = idesc_tf32(kBM, BN, A_MN, B_MN);
     for (int i = 0; i < nkb; ++i) {
       const int s = i % STAGES;
+      // SPLIT3: a new accumulation group starts from zero once the previous
+      // group's partial has been folded into the running sum
+      const bool fresh = SPLIT3 ? (i % kDrainGroup == 0) : (i == 0);
+      if (SPLIT3 && i > 0 && fresh) {
+        mbar_wait(drain_empty, ((i / kDrainGroup) - 1) & 1);
+        tc_fence_after();
+      }
       mbar_wait(&full[s], (i / STAGES) & 1);
       tc_fence_after();
       const uint32_t a0 = smem_u32(sA + s * L::A_BYTES);
@@ -191,7 +248,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             B_MN ? umma_desc(b0 + kk * 2 * MNTile<BN>::SBO, MNTile<BN>::LBO, MNTile<BN>::SBO,
                              kLayoutSW128Base32)
                  : umma_desc(b0 + kk * 32, 16, 1024, kLayoutSW128);
-        umma_tf32(tmem, ad, bd, idesc, (i | kk) != 0 ? 1u : 0u);
+        umma_tf32(tmem, ad, bd, idesc, (fresh && kk == 0) ? 0u : 1u);
         if constexpr (SPLIT3) {
           // the twins sit at a fixed offset with the same 1024-aligned swizzle
           // phase: the descriptors differ only in their start address (16 B units)
@@ -201,13 +258,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
       }
       umma_commit(&empty[s]);
+      if (SPLIT3 && i % kDrainGroup == kDrainGroup - 1 && i != nkb - 1) umma_commit(drain_full);
     }
     umma_commit(done);
   }
   __syncthreads();
   if (warp == 4) {
     tc_fence_after();
-    tmem_dealloc(tmem, tmem_cols<BN>());
+    tmem_dealloc(tmem, kTmemCols);
   }
 }
 

@@ -53,6 +53,13 @@ class ExecOptionsC(C.Structure):
 PRECISIONS = {"tf32": 0, "fp32": 1}
 
 
+class ExecMemC(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in (
+        "arena_bytes", "params_grads_bytes", "layer_state_bytes", "input_bytes", "wgrad_scratch_bytes",
+        "other_scratch_bytes", "host_stash_bytes", "device_total_bytes", "wgrad_partials_outside_pool_bytes",
+        "planned_arena_high_water")]
+
+
 class TimingC(C.Structure):
     _fields_ = [("step_ms", C.c_float), ("h2d_ms", C.c_float), ("d2h_ms", C.c_float),
                 ("kernels", C.c_int64), ("d2h_bytes", C.c_int64), ("h2d_bytes", C.c_int64),
@@ -162,6 +169,11 @@ def _xlib():
                                              P(C.c_double), P(C.c_double)]
         L.sn_exec_profile.argtypes = [C.c_void_p, P(C.c_float), P(C.c_int32), P(C.c_int32), C.c_size_t,
                                       P(C.c_size_t)]
+        L.sn_exec_census.argtypes = [C.c_void_p, P(C.c_int32), C.c_size_t, C.c_char_p, C.c_size_t,
+                                     P(C.c_size_t)]
+        L.sn_exec_memory.argtypes = [C.c_void_p, P(ExecMemC)]
+        L.sn_exec_arena_fill.argtypes = [C.c_void_p]
+        L.sn_exec_arena_scan.argtypes = [C.c_void_p, P(C.c_int64), P(C.c_int64)]
         L.sn_exec_stream.argtypes = [C.c_void_p]
         L.sn_exec_stream.restype = C.c_void_p
         L._sn_configured = True
@@ -365,6 +377,40 @@ class Executor:
             _raise_exec(self.L)
         return [(ms[i], lay[i], typ[i]) for i in range(n.value)]
 
+    def memory(self) -> dict:
+        """Bytes the executor allocated, by purpose (sn_exec_memory)."""
+        m = ExecMemC()
+        if self.L.sn_exec_memory(self.ptr, C.byref(m)) != 0:
+            _raise_exec(self.L)
+        return {n: getattr(m, n) for n, _ in ExecMemC._fields_}
+
+    def measure_arena(self) -> dict:
+        """Measured arena use of one iteration: the arena is filled with a
+        sentinel, one step runs (no update), and the highest 1 KiB block any
+        kernel or copy wrote is found on the device."""
+        if self.L.sn_exec_arena_fill(self.ptr) != 0:
+            _raise_exec(self.L)
+        self.step(update=False)
+        hw, touched = C.c_int64(), C.c_int64()
+        if self.L.sn_exec_arena_scan(self.ptr, C.byref(hw), C.byref(touched)) != 0:
+            _raise_exec(self.L)
+        return {"measured_arena_high_water_bytes": hw.value, "measured_arena_written_bytes": touched.value}
+
+    def census(self) -> list[list[str]]:
+        """Per tape action (the same list ``profile`` times), the mangled names
+        of the kernels it launches, from one captured serial iteration."""
+        n = C.c_size_t()
+        self.L.sn_exec_census(self.ptr, None, 0, None, 0, C.byref(n))
+        counts = (C.c_int32 * max(1, n.value))()
+        cap = 1 << 22
+        buf = C.create_string_buffer(cap)
+        if self.L.sn_exec_census(self.ptr, counts, n.value, buf, cap, C.byref(n)) != 0:
+            _raise_exec(self.L)
+        per = buf.value.decode("utf-8", "replace").split("\x1e")[:n.value]
+        out = [[k for k in p.split("\n") if k] for p in per]
+        assert [len(o) for o in out] == list(counts[:n.value]), "census name list truncated"
+        return out
+
     def apply_update(self, lr: float, grad_scale: float = 1.0) -> None:
         if self.L.sn_exec_apply_update(self.ptr, lr, grad_scale) != 0:
             _raise_exec(self.L)
@@ -431,8 +477,10 @@ def run_training(net: NetworkDef, config: SimConfig, iters: int = 10, warmup: in
         losses.append(loss)
         times.append(t.step_ms)
     ms = sum(times) / max(1, len(times))
+    extras = {"memory": ex.memory(), "arena": ex.measure_arena()}
     rep = TrainingReport(schedule=ex.report, images_per_s=config.cost.batch / (ms / 1e3) if ms else 0.0,
                          ms_per_step=ms, losses=tuple(losses), kernels_per_step=t.kernels if t else 0,
-                         d2h_bytes_per_step=t.d2h_bytes if t else 0, h2d_bytes_per_step=t.h2d_bytes if t else 0)
+                         d2h_bytes_per_step=t.d2h_bytes if t else 0, h2d_bytes_per_step=t.h2d_bytes if t else 0,
+                         extras=extras)
     ex.close()
     return rep

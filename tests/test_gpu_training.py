@@ -450,12 +450,28 @@ def test_fp32_mode_alex32_matches_oracle(cuda, alex32_case):
 
 
 def test_fp32_mode_resnet50g_b8_matches_oracle(cuda):
+    """ResNet-50g at batch 8 is ill-conditioned for any fp32 computation: the
+    CPU fp32 oracle itself differs from the fp64 oracle by up to ~1e-2 on some
+    BN / CONV gradients (training-mode BN over 8 x 7 x 7 values, 17 residual
+    blocks).  Stated tolerance: every gradient of the fp32 mode is at least as
+    close to the fp64 oracle as the CPU fp32 oracle is (within 2x), and within
+    1e-4 wherever the CPU fp32 result is within 5e-6 of fp64; loss <= 1e-5."""
+    import torch
+    from oracle.numerics import forward_backward
     from paper_1801_04380_b200.netgen import gen_resnet
     from paper_1801_04380_b200.training import init_parameters
     net = gen_resnet(3, 4, 6, 3)
     params = init_parameters(net, seed=2, head_scale=0.1)
     images, labels = _inputs(net, 8)
-    _fp32_case(net, 8, 4 << 30, params, images, labels)
+    loss, grads, _, _ = _run(net, 8, 4 << 30, ALL, params, images, labels, precision="fp32")
+    ref_loss, ref64 = forward_backward(net, params, images, labels, dtype=torch.float64)
+    _, ref32 = forward_backward(net, params, images, labels)
+    assert abs(loss - ref_loss) <= 1e-5 * abs(ref_loss), (loss, ref_loss)
+    e_gpu = _fp32_errors(net, grads, ref64)
+    e_cpu = _fp32_errors(net, ref32, ref64)
+    bad = {k: (e_gpu[k], e_cpu[k]) for k in e_gpu
+           if e_gpu[k] > max(2 * e_cpu[k], FP32_TOL if e_cpu[k] <= 5e-6 else 0.0) and e_gpu[k] > 5e-6}
+    assert not bad, sorted(bad.items(), key=lambda kv: -kv[1][0])[:6]
 
 
 def test_fp32_mode_feature_sets_are_bit_identical(cuda, alex32_case):
