@@ -53,6 +53,8 @@ def parse_args():
                          "densenet121s (4), resnet152g / resnet2534g (5)")
     ap.add_argument("--batch", type=int, default=None, help="per-GPU batch (default: the config's)")
     ap.add_argument("--pool-gib", type=float, default=None, help="pool budget in GiB (default: the config's)")
+    ap.add_argument("--pool-bytes", type=int, default=None, help="pool budget in bytes (overrides --pool-gib), "
+                    "e.g. the schedulable floor max_i(l_i) = 3288334336 for resnet50g b256")
     ap.add_argument("--features", default=ALL)
     ap.add_argument("--precision", default="tf32", choices=["tf32", "fp32"],
                     help="CONV/FC math: tf32 tensor cores (headline) or the fp32-faithful 3xTF32 mode")
@@ -60,6 +62,8 @@ def parse_args():
     args = ap.parse_args()
     if args.batch is None:
         args.batch = DEFAULT_BATCH[args.net]
+    if args.pool_bytes is not None:
+        args.pool_gib = args.pool_bytes / GiB
     if args.pool_gib is None:
         args.pool_gib = DEFAULT_POOL.get(args.net, 24 * GiB) / GiB
     return args
@@ -239,7 +243,7 @@ def run_ours(args) -> None:
 
     net = build_net(args.net)
     B = args.batch
-    pool = int(args.pool_gib * GiB)
+    pool = args.pool_bytes or int(args.pool_gib * GiB)
     cfg = sn.SimConfig(pool_bytes=pool, features=sn.parse_features(args.features), cost=sn.CostConfig(batch=B))
     free0 = torch.cuda.mem_get_info(local)[0]
     ex = Executor(net, cfg, device=local, seed=2, lr=0.01, grad_scale=1.0 / world, precision=args.precision)
@@ -364,9 +368,10 @@ def run_ours(args) -> None:
         "memory": {"peak_bytes": rep.peak_bytes, "min_pool_bytes_max_i_l_i": rep.min_pool_bytes,
                    "peak_over_floor": round(rep.peak_bytes / rep.min_pool_bytes, 4),
                    "pool_high_water_bytes_planned": rep.pool_high_water_bytes,
-                   "arena_written_high_water_bytes_measured": arena["measured_arena_high_water_bytes"],
+                   "arena_bytes": mem["arena_bytes"],
                    "arena_written_bytes_measured": arena["measured_arena_written_bytes"],
                    "cudaMemGetInfo_bytes_taken_by_executor": free0 - free1,
+                   "device_bytes_over_floor": round((free0 - free1) / rep.min_pool_bytes, 4),
                    "executor_allocations": mem,
                    "baseline_peak_bytes_features_none": rep.baseline_peak_bytes,
                    "offload_d2h_bytes_per_step_issued": int(t.d2h_bytes),

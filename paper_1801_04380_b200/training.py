@@ -386,15 +386,18 @@ class Executor:
 
     def measure_arena(self) -> dict:
         """Measured arena use of one iteration: the arena is filled with a
-        sentinel, one step runs (no update), and the highest 1 KiB block any
-        kernel or copy wrote is found on the device."""
+        sentinel, one step runs (no update), and the 1 KiB blocks any kernel or
+        copy wrote are counted on the device (the union of every placement in
+        the iteration; gradient buffers are placed from the top of the pool,
+        as the reference's BlockPool(high=True) does, so the highest written
+        block is the arena's end whenever a gradient buffer was allocated)."""
         if self.L.sn_exec_arena_fill(self.ptr) != 0:
             _raise_exec(self.L)
         self.step(update=False)
         hw, touched = C.c_int64(), C.c_int64()
         if self.L.sn_exec_arena_scan(self.ptr, C.byref(hw), C.byref(touched)) != 0:
             _raise_exec(self.L)
-        return {"measured_arena_high_water_bytes": hw.value, "measured_arena_written_bytes": touched.value}
+        return {"measured_arena_written_bytes": touched.value, "measured_arena_highest_written_byte": hw.value}
 
     def census(self) -> list[list[str]]:
         """Per tape action (the same list ``profile`` times), the mangled names

@@ -156,6 +156,13 @@ def merge(args) -> None:
     flat = [(a, k) for a in lt["actions"] for k in a["kernels"]]
     if len(flat) != len(launches):
         sys.exit(f"census has {len(flat)} kernels, ncu region {len(launches)}: not the same iteration")
+    def short(ncu_name: str) -> str:
+        n = ncu_name.replace("void ", "").replace("unnamed>::", "").replace("(anonymous namespace)::", "")
+        m = re.match(r"(?:\w+::)*(\w+)\s*[<(]", n)
+        return m.group(1) if m else n
+    bad = [(i, short(L["name"]), k) for i, ((a, k), L) in enumerate(zip(flat, launches)) if short(L["name"]) not in k]
+    if bad:
+        sys.exit(f"census / ncu launch names differ at {len(bad)} launches, first {bad[0]}")
     rows = []
     cls = collections.defaultdict(lambda: {"launches": 0, "s": 0.0, "dram": 0.0, "flops": 0.0})
     for (a, kname), L in zip(flat, launches):
