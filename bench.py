@@ -9,7 +9,8 @@ selection).  One step = forward + backward + SGD update of one batch.
     python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
 
 Under torchrun each rank is one replica (weak scaling, fixed per-GPU batch)
-and the weight gradients are all-reduced over NCCL.  Rank 0 prints ONE JSON
+and the executor sums the weight gradients over NCCL itself, in buckets
+overlapped with the backward (dp.py).  Rank 0 prints ONE JSON
 line.  ``--impl reference`` times the CPU restatement of the same training
 step (oracle/numerics.py; the reference itself has no numerics and cannot
 run here) on a bounded sample, with all host threads.
@@ -232,21 +233,23 @@ def run_ours(args) -> None:
     import paper_1801_04380_b200 as sn
     from paper_1801_04380_b200.training import Executor
 
+    from paper_1801_04380_b200 import dp as dpmod
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dist = None
+    ctx = dpmod.init("nccl")  # torch.distributed: rendezvous, barriers, max-over-ranks timing only
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
 
     net = build_net(args.net)
     B = args.batch
     pool = args.pool_bytes or int(args.pool_gib * GiB)
     cfg = sn.SimConfig(pool_bytes=pool, features=sn.parse_features(args.features), cost=sn.CostConfig(batch=B))
     free0 = torch.cuda.mem_get_info(local)[0]
-    ex = Executor(net, cfg, device=local, seed=2, lr=0.01, grad_scale=1.0 / world, precision=args.precision)
+    # weight-gradient all-reduce: NCCL buckets inside the executor's step (dp=ctx)
+    ex = Executor(net, cfg, device=local, seed=2, lr=0.01, precision=args.precision, dp=ctx if world > 1 else None)
     free1 = torch.cuda.mem_get_info(local)[0]
     rep = ex.report
     c, h, w = sn.propagate_shapes(net)[net.data_id]
@@ -258,14 +261,7 @@ def run_ours(args) -> None:
     grads = ex.grads_tensor()
 
     def step():
-        if world == 1:
-            return ex.step(update=True)
-        loss, t = ex.step(update=False)  # returns after the executor's stream has drained
-        dist.all_reduce(grads)
-        # the SGD kernel runs on the executor's stream: it must see the reduced gradients
-        torch.cuda.current_stream(local).synchronize()
-        ex.apply_update(0.01, 1.0 / world)
-        return loss, t
+        return ex.step(update=True)
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -312,13 +308,7 @@ def run_ours(args) -> None:
             call = lambda upd: ex.step_host(cur[0], cur[1], update=upd)  # noqa: E731
         else:
             call = lambda upd: ex.step_host_pipelined(cur[0], cur[1], nxt[0], nxt[1], update=upd)  # noqa: E731
-        if world == 1:
-            return call(True)
-        loss, t = call(False)
-        dist.all_reduce(grads)
-        torch.cuda.current_stream(local).synchronize()
-        ex.apply_update(0.01, 1.0 / world)
-        return loss, t
+        return call(True)
 
     def host_run(pipelined):
         if dist:
@@ -385,6 +375,7 @@ def run_ours(args) -> None:
     if not args.no_extras and rank == 0:
         line.update(extras(args, net, cfg, ex, ms_per_step, local))
     ex.close()
+    ctx.close()
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:

@@ -225,6 +225,15 @@ typedef struct sn_exec_options {
                              the executor's own device = same-device loopback) */
   int32_t stash_device;
   int32_t reserved_;
+  /* Data-parallel replica; dp_comm NULL = single replica.  The
+   * weight gradients are summed over the dp_world ranks by ncclAllReduce in
+   * buckets of about dp_bucket_bytes, each issued on a communication stream
+   * as soon as the backward steps of its layers are done (overlapping the
+   * rest of the backward), and each bucket's SGD update (grad_scale applied,
+   * normally 1/world) follows its all-reduce on that stream. */
+  void* dp_comm;          /* ncclComm_t from sn_dp_comm_create, owned by the caller */
+  int32_t dp_world, dp_rank;
+  int64_t dp_bucket_bytes; /* 0: default (8 MiB) */
 } sn_exec_options;
 
 typedef struct sn_step_timing {
@@ -320,6 +329,25 @@ int sn_exec_arena_fill(sn_exec* ex);
 int sn_exec_arena_scan(sn_exec* ex, int64_t* high_water_bytes, int64_t* touched_bytes);
 /* Stream the executor launches on (for cross-library ordering). */
 void* sn_exec_stream(sn_exec* ex);
+
+/* ======================================================================
+ * Data-parallel replicas: one process per GPU, NCCL (libnccl.so.2 loaded at
+ * run time) for the one collective of the path, the weight-gradient sum.
+ * ====================================================================== */
+typedef struct sn_dp_id {
+  char bytes[128]; /* ncclUniqueId: made by rank 0, broadcast by the caller */
+} sn_dp_id;
+const char* sn_dp_last_error(void);
+int sn_dp_nccl_version(int32_t* version);
+int sn_dp_unique_id(sn_dp_id* out);
+int sn_dp_comm_create(const sn_dp_id* id, int32_t world, int32_t rank, int32_t device, void** comm_out);
+void sn_dp_comm_destroy(void* comm);
+/* The all-reduce buckets of a plan (host only, no device needed): bucket i
+ * covers floats [lo[i], hi[i]) of the flat gradient block and is issued right
+ * after the backward step of layer after_layer[i]; buckets are in issue
+ * (backward) order and cover every parameter float exactly once. */
+int sn_dp_buckets(const sn_plan* plan, int64_t bucket_bytes, int64_t* lo, int64_t* hi, int32_t* after_layer,
+                  size_t cap, size_t* n);
 
 #ifdef __cplusplus
 }

@@ -97,7 +97,7 @@ def build_exec(force: bool = False) -> Path:
     with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as pool:
         list(pool.map(lambda so: _run([NVCC, *flags, f"-I{INCLUDE}", f"-I{CSRC}", "-c", str(so[0]), "-o", so[1]]),
                       zip(srcs, objs)))
-    _run([NVCC, *ARCH, "-shared", *objs, "-o", str(out), f"-L{LIB}", "-lsnplan",
+    _run([NVCC, *ARCH, "-shared", *objs, "-o", str(out), f"-L{LIB}", "-lsnplan", "-ldl",
           "-Xlinker", "-rpath,$ORIGIN"])
     _stamp(out, digest)
     return out

@@ -30,6 +30,7 @@
 
 #include "../kernels/kernels.hpp"
 #include "../planner/handle.hpp"
+#include "nccl_dl.hpp"
 #include "superneurons.h"
 
 namespace {
@@ -147,6 +148,17 @@ struct sn_exec {
   // an action's kernels and nothing overlaps
   bool serial = false;
   int32_t* marker = nullptr;  // census: per-action memset marker target
+  // data-parallel replica: buckets of the weight-gradient all-reduce, issued on
+  // s5 after the backward steps of their layers
+  struct Bucket {
+    int64_t lo = 0, hi = 0;  // floats of the flat gradient block
+    int after_layer = -1;    // issued right after this layer's backward action
+    std::vector<int> layers;
+  };
+  std::vector<Bucket> buckets;
+  cudaStream_t s5 = nullptr;
+  int32_t* update_flag = nullptr;
+  bool dp() const { return opt.dp_comm != nullptr; }
   // device / pinned bytes by category (sn_exec_memory)
   enum { M_ARENA, M_PARAMS, M_STATE, M_INPUT, M_WGRAD, M_OTHER, M_HOST, M_N };
   int64_t mem[M_N] = {};
@@ -291,6 +303,67 @@ void setup_layers(sn_exec* ex, const sn_layer_numerics* numerics) {
   }
 }
 
+// Buckets in backward (issue) order: a bucket is a contiguous float range of
+// the parameter block holding whole layers; it grows with each parameter
+// layer whose backward step completes, as long as the range it would span
+// holds no layer still waiting for its backward step or already in a closed
+// bucket, and up to `cap_bytes`.
+void plan_buckets(sn_exec* ex, int64_t cap_bytes) {
+  const snp::Plan& P = ex->plan->plan;
+  const Net& net = P.net;
+  struct Iv {
+    int64_t lo, hi;
+    int lid;
+  };
+  std::vector<Iv> ivs;
+  for (int i = 0; i < net.n; ++i) {
+    const LayerRt& l = ex->L[i];
+    if (l.w_off < 0) continue;
+    ivs.push_back({std::min(l.w_off, l.b_off), std::max(l.w_off + l.w_n, l.b_off + l.b_n), i});
+  }
+  std::sort(ivs.begin(), ivs.end(), [](const Iv& a, const Iv& b) { return a.lo < b.lo; });
+  std::vector<int> state(net.n, 0);  // 0 pending, 1 in the open bucket, 2 in a closed bucket
+  ex->buckets.clear();
+  sn_exec::Bucket cur;
+  auto close = [&] {
+    if (cur.layers.empty()) return;
+    for (int l : cur.layers) state[l] = 2;
+    ex->buckets.push_back(cur);
+    cur = sn_exec::Bucket{};
+  };
+  auto fits = [&](int64_t lo, int64_t hi) {
+    for (const Iv& v : ivs)
+      if (v.lo < hi && lo < v.hi && state[v.lid] != 1) return false;
+    return true;
+  };
+  std::vector<char> seen(net.n, 0);
+  for (const auto& ev : P.tape) {
+    if (ev.op != 'B' || ex->L[ev.b].w_off < 0 || seen[ev.b]) continue;
+    seen[ev.b] = 1;
+    const LayerRt& l = ex->L[ev.b];
+    const int64_t lo = std::min(l.w_off, l.b_off), hi = std::max(l.w_off + l.w_n, l.b_off + l.b_n);
+    state[ev.b] = 1;
+    if (!cur.layers.empty()) {
+      const int64_t nlo = std::min(cur.lo, lo), nhi = std::max(cur.hi, hi);
+      if ((nhi - nlo) * 4 > cap_bytes || !fits(nlo, nhi)) {
+        state[ev.b] = 0;
+        close();
+        state[ev.b] = 1;
+      }
+    }
+    if (cur.layers.empty()) {
+      cur.lo = lo;
+      cur.hi = hi;
+    } else {
+      cur.lo = std::min(cur.lo, lo);
+      cur.hi = std::max(cur.hi, hi);
+    }
+    cur.layers.push_back(ev.b);
+    cur.after_layer = ev.b;
+  }
+  close();
+}
+
 void alloc_device(sn_exec* ex) {
   const snp::Plan& P = ex->plan->plan;
   const Net& net = P.net;
@@ -404,6 +477,9 @@ struct Compiler {
   // activation / gradient keys a side-stream weight gradient still reads: when
   // the tape frees one, later allocations over its blocks wait for that event
   std::unordered_map<int64_t, cudaEvent_t> side_reads;
+  std::unordered_map<int, cudaEvent_t> wgrad_done;  // CONV layer -> its s3 weight-gradient completion
+  bool used_s5 = false;
+  size_t next_bucket = 0;
   int data_id = -1;
 
   Compiler(sn_exec* e) : ex(e), P(e->plan->plan), net(e->plan->plan.net) {
@@ -751,6 +827,7 @@ struct Compiler {
         float* wt_w = ex->wt_w;
         cudaEvent_t ready = ex->new_event(), wdone = ex->new_event();
         used_s3 = true;
+        wgrad_done[lid] = wdone;
         side_reads[snp::key_code(snp::K_ACT, pid)] = wdone;
         side_reads[snp::key_code(snp::K_GRAD, owner)] = wdone;
         // The split-K partials go to the conv workspace the planner granted this
@@ -1358,6 +1435,40 @@ struct Compiler {
     ex->elided = elide_out;
   }
 
+  // Data-parallel bucket all-reduce + update on s5, right after the backward
+  // step that completes the bucket: s5 waits for everything s0 issued (BN /
+  // FC / bias gradients) and for the side-stream weight gradients of the
+  // bucket's CONV layers.  Each layer's parameters are not read again in
+  // this iteration after its backward step (its replays precede it), so the
+  // bucket's update can run while the backward continues.
+  void dp_after_backward(int lid) {
+    while (next_bucket < ex->buckets.size() && ex->buckets[next_bucket].after_layer == lid) {
+      const sn_exec::Bucket& b = ex->buckets[next_bucket++];
+      std::vector<cudaEvent_t> waits;
+      for (int l : b.layers) {
+        auto it = wgrad_done.find(l);
+        if (it != wgrad_done.end()) waits.push_back(it->second);
+      }
+      cudaEvent_t e0 = ex->new_event();
+      sn_exec* e = ex;
+      const int64_t lo = b.lo, n = b.hi - b.lo;
+      const float lr = ex->opt.lr, scale = ex->opt.grad_scale;
+      push([=] {
+        std::string err;
+        const sndp::Nccl* nc = sndp::nccl(&err);
+        if (!nc) xfail(SN_EK_CUDA, err);
+        ck(cudaEventRecord(e0, e->s0), "record");
+        ck(cudaStreamWaitEvent(e->s5, e0, 0), "wait");
+        for (cudaEvent_t w : waits) ck(cudaStreamWaitEvent(e->s5, w, 0), "wait");
+        const ncclResult_t r = nc->AllReduce(e->grads + lo, e->grads + lo, static_cast<size_t>(n), ncclFloat32,
+                                             ncclSum, static_cast<ncclComm_t>(e->opt.dp_comm), e->s5);
+        if (r != ncclSuccess) xfail(SN_EK_CUDA, std::string("ncclAllReduce: ") + nc->GetErrorString(r));
+        ck(sn::sgd_update_flagged(e->params + lo, e->grads + lo, n, lr, scale, e->update_flag, e->s5), "sgd");
+      }, 2);
+      used_s5 = true;
+    }
+  }
+
   // split-K partial floats of a CONV weight gradient
   int64_t wgrad_partial_floats(int lid) const {
     const LayerRt& l = ex->L[lid];
@@ -1433,6 +1544,10 @@ struct Compiler {
         case 'B':
           cur_layer = ev.b, cur_type = 2;
           backward(ev.b);
+          if (ex->dp()) {
+            cur_layer = -1, cur_type = 3;
+            dp_after_backward(ev.b);
+          }
           break;
         case 'O': on_copy_out(ev.b); break;
         case 'P':
@@ -1470,6 +1585,15 @@ struct Compiler {
         ck(cudaStreamWaitEvent(s0, j, 0), "wait");
       }, 0);
     }
+    if (used_s5) {
+      cudaEvent_t j = ex->new_event();
+      cudaStream_t s5 = ex->s5;
+      push([=] {
+        ck(cudaEventRecord(j, s5), "record");
+        ck(cudaStreamWaitEvent(s0, j, 0), "wait");
+      }, 0);
+    }
+    if (ex->dp() && next_bucket != ex->buckets.size()) xfail(SN_EK_INTERNAL, "data-parallel buckets not all issued");
     uint32_t* it = ex->iteration;
     push([=] { ck(sn::bump_iteration(it, s0), "bump"); }, 1);
     ex->final_keys = where;
@@ -1548,7 +1672,7 @@ void destroy(sn_exec* ex) {
   void* bufs[] = {ex->arena, ex->params, ex->grads, ex->state, ex->images, ex->labels, ex->loss_rows, ex->loss,
                   ex->iteration, ex->wt_scratch, ex->partial, ex->red, ex->tstats, ex->pool_scratch,
                   ex->partial_w, ex->red_w, ex->wt_w, ex->images_stage, ex->labels_stage,
-                  const_cast<float**>(ex->ptr_table), ex->marker};
+                  const_cast<float**>(ex->ptr_table), ex->marker, ex->update_flag};
   for (void* b : bufs)
     if (b) cudaFree(b);
   for (auto& l : ex->L)
@@ -1557,6 +1681,7 @@ void destroy(sn_exec* ex) {
   if (ex->s1) cudaStreamDestroy(ex->s1);
   if (ex->s2) cudaStreamDestroy(ex->s2);
   if (ex->s3) cudaStreamDestroy(ex->s3);
+  if (ex->s5) cudaStreamDestroy(ex->s5);
   delete ex;
 }
 
@@ -1591,6 +1716,14 @@ int sn_exec_create(const sn_plan* plan, const sn_net_desc* /*net*/, const sn_lay
     ck(cudaEventCreate(&ex->t_end), "event");
     setup_layers(ex, numerics);
     alloc_device(ex);
+    if (ex->dp()) {
+      if (ex->opt.dp_world < 1 || ex->opt.dp_rank < 0 || ex->opt.dp_rank >= ex->opt.dp_world)
+        xfail(SN_EK_CONFIG, "bad data-parallel world / rank");
+      plan_buckets(ex, ex->opt.dp_bucket_bytes > 0 ? ex->opt.dp_bucket_bytes : (8ll << 20));
+      ck(cudaStreamCreateWithFlags(&ex->s5, cudaStreamNonBlocking), "stream");
+      ex->dmalloc(&ex->update_flag, 4, sn_exec::M_OTHER, "cudaMalloc(update flag)");
+      ck(cudaMemset(ex->update_flag, 0, 4), "memset(flag)");
+    }
     Compiler comp(ex);
     comp.compile();
     const size_t nptr = std::max<size_t>(1, ex->ptr_host.size());
@@ -1645,11 +1778,13 @@ int sn_exec_step(sn_exec* ex, int32_t update, float* loss_host, sn_step_timing* 
     PrecisionScope prec(ex);
     if (ex->opt.use_graph) ensure_graph(ex);
     ck(cudaEventRecord(ex->t_begin, ex->s0), "record");
+    if (ex->dp()) ck(cudaMemsetAsync(ex->update_flag, update ? 1 : 0, 4, ex->s0), "update flag");
     if (ex->opt.use_graph)
       ck(cudaGraphLaunch(ex->gexec, ex->s0), "GraphLaunch");
     else
       run_program(ex);
-    if (update) ck(sn::sgd_update(ex->params, ex->grads, ex->n_params, ex->opt.lr, ex->opt.grad_scale, ex->s0), "sgd");
+    if (update && !ex->dp())
+      ck(sn::sgd_update(ex->params, ex->grads, ex->n_params, ex->opt.lr, ex->opt.grad_scale, ex->s0), "sgd");
     ck(cudaEventRecord(ex->t_end, ex->s0), "record");
     if (loss_host) ck(cudaMemcpyAsync(loss_host, ex->loss, sizeof(float), cudaMemcpyDeviceToHost, ex->s0), "loss D2H");
     ck(cudaStreamSynchronize(ex->s0), "sync");
@@ -1678,11 +1813,13 @@ int sn_exec_step_host(sn_exec* ex, const float* images_host, const int32_t* labe
        "images H2D");
     ck(cudaMemcpyAsync(ex->labels, labels_host, ex->B * sizeof(int32_t), cudaMemcpyHostToDevice, ex->s0),
        "labels H2D");
+    if (ex->dp()) ck(cudaMemsetAsync(ex->update_flag, update ? 1 : 0, 4, ex->s0), "update flag");
     if (ex->opt.use_graph)
       ck(cudaGraphLaunch(ex->gexec, ex->s0), "GraphLaunch");
     else
       run_program(ex);
-    if (update) ck(sn::sgd_update(ex->params, ex->grads, ex->n_params, ex->opt.lr, ex->opt.grad_scale, ex->s0), "sgd");
+    if (update && !ex->dp())
+      ck(sn::sgd_update(ex->params, ex->grads, ex->n_params, ex->opt.lr, ex->opt.grad_scale, ex->s0), "sgd");
     ck(cudaMemcpyAsync(loss_host, ex->loss, sizeof(float), cudaMemcpyDeviceToHost, ex->s0), "loss D2H");
     ck(cudaEventRecord(ex->t_end, ex->s0), "record");
     ck(cudaStreamSynchronize(ex->s0), "sync");
@@ -1733,11 +1870,13 @@ int sn_exec_step_host_pipelined(sn_exec* ex, const float* images_host, const int
     // stage the next batch now: the loss read below is a pageable copy that
     // blocks the host until the step is done
     if (next_images_host && next_labels_host) stage(next_images_host, next_labels_host);
+    if (ex->dp()) ck(cudaMemsetAsync(ex->update_flag, update ? 1 : 0, 4, ex->s0), "update flag");
     if (ex->opt.use_graph)
       ck(cudaGraphLaunch(ex->gexec, ex->s0), "GraphLaunch");
     else
       run_program(ex);
-    if (update) ck(sn::sgd_update(ex->params, ex->grads, ex->n_params, ex->opt.lr, ex->opt.grad_scale, ex->s0), "sgd");
+    if (update && !ex->dp())
+      ck(sn::sgd_update(ex->params, ex->grads, ex->n_params, ex->opt.lr, ex->opt.grad_scale, ex->s0), "sgd");
     ck(cudaMemcpyAsync(loss_host, ex->loss, sizeof(float), cudaMemcpyDeviceToHost, ex->s0), "loss D2H");
     ck(cudaEventRecord(ex->t_end, ex->s0), "record");
     ck(cudaStreamSynchronize(ex->s0), "sync");
@@ -1770,6 +1909,7 @@ int sn_exec_profile(sn_exec* ex, float* action_ms, int32_t* action_layer, int32_
       sn_exec* e;
       ~Restore() { e->serial = false; }
     } restore{ex};
+    if (ex->dp()) ck(cudaMemsetAsync(ex->update_flag, 0, 4, ex->s0), "update flag");
     ck(cudaEventRecord(ev[0], ex->s0), "record");
     for (size_t i = 0; i < ex->prog.size(); ++i) {
       ex->prog[i].fn();
@@ -1945,6 +2085,27 @@ int sn_exec_arena_scan(sn_exec* ex, int64_t* high_water_bytes, int64_t* touched_
     ck(e2, "scan");
     if (high_water_bytes) *high_water_bytes = static_cast<int64_t>(h[0]) * snp::kBlockBytes;
     if (touched_bytes) *touched_bytes = static_cast<int64_t>(h[1]) * snp::kBlockBytes;
+  });
+}
+
+int sn_dp_buckets(const sn_plan* plan, int64_t bucket_bytes, int64_t* lo, int64_t* hi, int32_t* after_layer,
+                  size_t cap, size_t* n) {
+  if (!plan || !n) return xset(SN_EK_INTERNAL, "null argument");
+  sn_exec tmp;  // host-side layout only: no device resources are created
+  tmp.plan = plan;
+  tmp.net = &plan->plan.net;
+  tmp.B = static_cast<int>(plan->plan.cost_cfg.batch);
+  return xguard([&] {
+    setup_layers(&tmp, nullptr);
+    plan_buckets(&tmp, bucket_bytes > 0 ? bucket_bytes : (8ll << 20));
+    *n = tmp.buckets.size();
+    if (!lo) return;
+    if (cap < tmp.buckets.size()) xfail(SN_EK_INTERNAL, "output buffer too small");
+    for (size_t i = 0; i < tmp.buckets.size(); ++i) {
+      lo[i] = tmp.buckets[i].lo;
+      hi[i] = tmp.buckets[i].hi;
+      if (after_layer) after_layer[i] = tmp.buckets[i].after_layer;
+    }
   });
 }
 

@@ -230,6 +230,9 @@ cudaError_t grad_copy_multi(const float* src, float* const* dsts, const int* acc
 
 cudaError_t sgd_update(float* params, const float* grads, int64_t n, float lr, float grad_scale,
                        cudaStream_t st);
+// Same update, skipped on the device when *flag == 0 (graph-captured DP buckets).
+cudaError_t sgd_update_flagged(float* params, const float* grads, int64_t n, float lr, float grad_scale,
+                               const int* flag, cudaStream_t st);
 cudaError_t bump_iteration(uint32_t* iteration, cudaStream_t st);
 cudaError_t fill_zero(float* p, int64_t n, cudaStream_t st);
 

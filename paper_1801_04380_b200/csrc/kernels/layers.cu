@@ -1498,6 +1498,16 @@ __global__ void sgd_kernel(float* p, const float* __restrict__ g, int64_t n, flo
     p[i] -= lr * (g[i] * scale);
 }
 
+// The data-parallel per-bucket update: skipped when *flag == 0 (a step
+// without update); same arithmetic as sgd_kernel.
+__global__ void sgd_flagged_kernel(float* p, const float* __restrict__ g, int64_t n, float lr, float scale,
+                                   const int* flag) {
+  if (*flag == 0) return;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride)
+    p[i] -= lr * (g[i] * scale);
+}
+
 __global__ void bump_kernel(uint32_t* it) { *it += 1; }
 
 __global__ void zero_kernel(float* p, int64_t n) {
@@ -1945,6 +1955,12 @@ __global__ void pad_channels_kernel(const float* __restrict__ raw, int C_raw, fl
 
 cudaError_t pad_channels(const float* raw, int C_raw, float* out, int Cs, int64_t pixels, cudaStream_t st) {
   pad_channels_kernel<<<blocks_for(pixels * Cs), kThreads, 0, st>>>(raw, C_raw, out, Cs, pixels * Cs);
+  return cudaGetLastError();
+}
+
+cudaError_t sgd_update_flagged(float* params, const float* grads, int64_t n, float lr, float grad_scale,
+                               const int* flag, cudaStream_t st) {
+  sgd_flagged_kernel<<<blocks_for(n), kThreads, 0, st>>>(params, grads, n, lr, grad_scale, flag);
   return cudaGetLastError();
 }
 

@@ -47,7 +47,8 @@ class ExecOptionsC(C.Structure):
     _fields_ = [("device", C.c_int32), ("elide_backups", C.c_int32), ("use_graph", C.c_int32),
                 ("num_classes", C.c_int32), ("seed", C.c_uint64), ("lr", C.c_float),
                 ("grad_scale", C.c_float), ("precision", C.c_int32), ("stash", C.c_int32),
-                ("stash_device", C.c_int32), ("reserved_", C.c_int32)]
+                ("stash_device", C.c_int32), ("reserved_", C.c_int32), ("dp_comm", C.c_void_p),
+                ("dp_world", C.c_int32), ("dp_rank", C.c_int32), ("dp_bucket_bytes", C.c_int64)]
 
 
 PRECISIONS = {"tf32": 0, "fp32": 1}
@@ -192,7 +193,7 @@ class Executor:
     def __init__(self, net: NetworkDef, config: SimConfig, device: int = 0, *, seed: int = 2,
                  dropout_seed: int = 1234, lr: float = 0.01, grad_scale: float = 1.0,
                  elide_backups: bool = True, use_graph: bool = True, params: dict | None = None,
-                 precision: str = "tf32") -> None:
+                 precision: str = "tf32", dp=None, dp_bucket_bytes: int = 0) -> None:
         import torch
         if not torch.cuda.is_available():
             raise DeviceError("run_training needs a CUDA device (B200); there is no CPU fallback")
@@ -207,8 +208,20 @@ class Executor:
         if precision not in PRECISIONS:
             raise MemschedError(f"precision must be one of {sorted(PRECISIONS)}, got {precision!r}")
         self.precision = precision
+        # data-parallel replica (dp.DPContext): NCCL communicator for the bucketed
+        # gradient all-reduce; each rank draws its own dropout masks, and the
+        # update applies lr * sum_ranks(grad) / world unless grad_scale is given
+        self.dp = dp if (dp is not None and dp.world > 1) or (dp is not None and dp.force_comm) else None
+        comm = None
+        if self.dp is not None:
+            from .dp import rank_seed
+            comm = self.dp.comm(device)
+            dropout_seed = rank_seed(dropout_seed, self.dp)
+            if grad_scale == 1.0:
+                grad_scale = 1.0 / self.dp.world
         opts = ExecOptionsC(device, int(elide_backups), int(use_graph), 0, dropout_seed, lr, grad_scale,
-                            PRECISIONS[precision], 0, device, 0)
+                            PRECISIONS[precision], 0, device, 0, comm,
+                            self.dp.world if self.dp else 1, self.dp.rank if self.dp else 0, dp_bucket_bytes)
         self.ptr = C.c_void_p()
         torch.cuda.set_device(device)
         torch.cuda.synchronize()

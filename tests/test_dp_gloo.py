@@ -94,3 +94,65 @@ def test_two_replicas_equal_full_batch_gradient():
     ref = torch.cat([full[l][k].reshape(-1) for l in sorted(full) for k in ("w", "b")])
     err = (g0.double() - ref.double()).norm() / ref.double().norm()
     assert err < 1e-5, err
+
+
+def _bucket_worker(rank: int, world: int, port: int, out_q) -> None:
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    torch.set_num_threads(1)
+    import paper_1801_04380_b200 as sn
+    from paper_1801_04380_b200 import dp
+    from paper_1801_04380_b200.netgen import gen_resnet
+    ctx = dp.init("gloo")
+    uid = dp.share_unique_id(ctx)  # rank 0's NCCL id, broadcast over gloo
+    net = gen_resnet(3, 4, 6, 3)
+    cfg = sn.SimConfig(pool_bytes=24 << 30, features=sn.parse_features(
+        "liveness,offload,cache,recompute=cost-aware,convselect"), cost=sn.CostConfig(batch=256))
+    buckets = dp.bucket_plan(net, cfg, bucket_bytes=4 << 20)
+    n = max(hi for _, hi, _ in buckets)
+    # stub gradient / parameter blocks standing in for the executor's device blocks
+    grads = torch.randn(n, generator=torch.Generator().manual_seed(100 + rank))
+    params = torch.randn(n, generator=torch.Generator().manual_seed(7))
+    full = grads.clone()
+    torch.distributed.all_reduce(full)
+    ref = params - 0.01 * (full * (1.0 / world))
+    # the executor's order: one all-reduce + update per bucket, in issue order
+    for lo, hi, _ in buckets:
+        g = grads[lo:hi].clone()
+        torch.distributed.all_reduce(g)
+        params[lo:hi] -= 0.01 * (g * (1.0 / world))
+    out_q.put((rank, uid, buckets, bool(torch.equal(params, ref)), dp.rank_seed(1234, ctx)))
+    torch.distributed.barrier()
+    torch.distributed.destroy_process_group()
+
+
+def test_bucketed_allreduce_plumbing_two_ranks():
+    """The product's DP host logic at world 2 on gloo: rank 0's NCCL unique id
+    reaches every rank; every rank computes the same bucket plan (host only,
+    sn_dp_buckets); the buckets are disjoint and cover the parameter block;
+    the per-bucket all-reduce + update in issue order equals one global
+    all-reduce + SGD bit for bit; ranks draw different dropout seeds."""
+    import sys
+    sys.path.insert(0, ROOT)
+    from oracle.numerics import dropout_keep
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bucket_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in range(2)], key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    (_, uid0, b0, ok0, seed0), (_, uid1, b1, ok1, seed1) = res
+    assert uid0 == uid1 and len(uid0) == 128
+    assert b0 == b1 and len(b0) > 1
+    spans = sorted((lo, hi) for lo, hi, _ in b0)
+    assert spans[0][0] == 0 and all(a[1] <= b[0] for a, b in zip(spans, spans[1:]))
+    assert all(b[0] - a[1] < 64 for a, b in zip(spans, spans[1:]))  # only alignment padding between
+    assert ok0 and ok1
+    assert seed0 != seed1
+    assert not (dropout_keep(4096, 0.5, seed0, 3, 0) == dropout_keep(4096, 0.5, seed1, 3, 0)).all()

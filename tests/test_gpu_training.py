@@ -479,3 +479,41 @@ def test_fp32_mode_feature_sets_are_bit_identical(cuda, alex32_case):
     base_loss, base, _, _ = _run(net, 16, 1 << 30, "none", params, images, labels, precision="fp32")
     loss, grads, _, _ = _run(net, 16, 17 << 20, ALL, params, images, labels, precision="fp32")
     assert loss == base_loss and _bitwise(grads, base)
+
+
+# ---- data-parallel program path (NCCL communicator inside the executor) ----
+
+@pytest.mark.parametrize("which", ["alex32", "resnet50g_b8"])
+def test_dp_world1_nccl_path_is_bit_identical(cuda, alex32_case, which):
+    """A world-size-1 NCCL communicator exercises the whole DP program path
+    (bucketed ncclAllReduce on the communication stream after each bucket's
+    backward steps, per-bucket fused SGD, stream joins, graph capture): after
+    two update steps the parameters and gradients equal the single-replica
+    executor's bit for bit."""
+    sn = _sn()
+    from paper_1801_04380_b200 import dp
+    from paper_1801_04380_b200.training import Executor, init_parameters
+    if which == "alex32":
+        net, params, images, labels = alex32_case
+        batch, pool = 16, 1 << 30
+    else:
+        from paper_1801_04380_b200.netgen import gen_resnet
+        net = gen_resnet(3, 4, 6, 3)
+        params = init_parameters(net, seed=2, head_scale=0.1)
+        images, labels = _inputs(net, 8)
+        batch, pool = 8, 4 << 30
+    cfg = sn.SimConfig(pool_bytes=pool, features=sn.parse_features(ALL), cost=sn.CostConfig(batch=batch))
+    out = []
+    for use_dp in (False, True):
+        ctx = dp.DPContext(force_comm=True) if use_dp else None
+        ex = Executor(net, cfg, params=params, lr=0.01, dp=ctx, dp_bucket_bytes=1 << 20)
+        ex.set_inputs(images, labels)
+        losses = [ex.step(update=True)[0] for _ in range(2)]
+        out.append((losses, ex.get("params"), ex.get("grads")))
+        ex.close()
+        if ctx:
+            ctx.close()
+    (l0, p0, g0), (l1, p1, g1) = out
+    assert l0 == l1
+    assert _bitwise(p0, p1) and _bitwise(g0, g1)
+    assert any(not torch.equal(p0[l]['w'], params[l]['w']) for l in params)  # the updates ran
