@@ -58,7 +58,7 @@ def test_c_abi_exports_every_declared_symbol():
     exe = _native.executor()
     missing = []
     for sym in _header_symbols():
-        lib = exe if sym.startswith("sn_exec") else plan
+        lib = exe if sym.startswith(("sn_exec", "sn_dp")) else plan
         if not hasattr(lib, sym):
             missing.append(sym)
     assert not missing, missing
