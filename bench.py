@@ -466,6 +466,19 @@ def extras(args, net, cfg, ex, ms_per_step, local) -> dict:
     pm, pex = side_run("parity", cfg, elide_backups=False)
     out["parity_mode"] = {"elide_backups": False, "ms_per_step": pm and round(pm, 4),
                           "images_per_s": pm and round(args.batch / (pm / 1e3), 2), **pex}
+    # the Unified Tensor Pool's copy-out store in HBM (f2: an NVLink peer's spare
+    # memory; on one GPU the same device as a loopback) vs pinned host memory,
+    # at a pool tight enough that the schedule fetches tensors back (4 GiB)
+    tight = sn.SimConfig(pool_bytes=4 * GiB, features=cfg.features, cost=cfg.cost)
+    th, thx = side_run("host stash", tight)
+    td, tdx = side_run("device stash", tight, stash="device")
+    out["utp_stash"] = {"pool_bytes": 4 * GiB,
+                        "host_pinned": {"ms_per_step": th and round(th, 4),
+                                        "images_per_s": th and round(args.batch / (th / 1e3), 2), **thx},
+                        "device_loopback": {"ms_per_step": td and round(td, 4),
+                                            "images_per_s": td and round(args.batch / (td / 1e3), 2), **tdx},
+                        "note": "stash=device on this GPU stands in for a peer's HBM over NVLink (unmeasured at "
+                                "N>1: one GPU per run here)"}
     # fp32-faithful numerics (3xTF32 split operands) at the same config
     fm, fex = side_run("fp32", cfg, precision="fp32")
     out["fp32_mode"] = {"precision": "fp32 (3xTF32 split operands, fp32-level products)",

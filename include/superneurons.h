@@ -315,8 +315,10 @@ typedef struct sn_exec_mem {
   int64_t wgrad_scratch_bytes;  /* weight-gradient scratch outside the pool (partials that
                                    did not fit their granted workspace, reductions) */
   int64_t other_scratch_bytes;  /* FC split-K, weight transposes, BN tile statistics, ... */
-  int64_t host_stash_bytes;     /* pinned host memory of copied-out tensors */
-  int64_t device_total_bytes;   /* sum of the device categories */
+  int64_t host_stash_bytes;     /* pinned host memory of copied-out tensors (stash 0) */
+  int64_t device_stash_bytes;   /* stash 1 on this device (loopback) */
+  int64_t peer_stash_bytes;     /* stash 1 on a peer device's HBM */
+  int64_t device_total_bytes;   /* sum of this device's categories (arena .. device stash) */
   int64_t wgrad_partials_outside_pool_bytes;
   int64_t planned_arena_high_water; /* the planner's BlockPool high water */
 } sn_exec_mem;

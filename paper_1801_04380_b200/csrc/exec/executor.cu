@@ -160,7 +160,8 @@ struct sn_exec {
   int32_t* update_flag = nullptr;
   bool dp() const { return opt.dp_comm != nullptr; }
   // device / pinned bytes by category (sn_exec_memory)
-  enum { M_ARENA, M_PARAMS, M_STATE, M_INPUT, M_WGRAD, M_OTHER, M_HOST, M_N };
+  enum { M_ARENA, M_PARAMS, M_STATE, M_INPUT, M_WGRAD, M_OTHER, M_STASH, M_HOST, M_PEER, M_N };
+  std::vector<std::pair<char*, int>> peer_stash;  // device stash allocations (pointer, device)
   int64_t mem[M_N] = {};
   int64_t wgrad_partial_outside = 0;  // floats of split-K scratch the plan's workspaces could not hold
   template <class T>
@@ -584,26 +585,54 @@ struct Compiler {
     if (ex->opt.elide_backups && !fetched[lid]) return;
     const int64_t nbytes = P.costs[lid].device_bytes;
     char* host = ex->stash[lid];
-    if (!host) {
-      ck(cudaHostAlloc(&host, static_cast<size_t>(nbytes), cudaHostAllocPortable), "cudaHostAlloc(stash)");
-      ex->mem[sn_exec::M_HOST] += nbytes;
-      ex->stash[lid] = host;
-    }
+    if (!host) host = ex->stash[lid] = stash_alloc(nbytes);
     const float* src = ptr(snp::K_ACT, lid);
     cudaEvent_t prod = ex->new_event(), done = ex->new_event();
     cudaStream_t s0 = ex->s0, s1 = ex->s1;
     const sn_exec::Timer tm = ex->new_timer(0, nbytes);
+    const cudaMemcpyKind kind = ex->opt.stash ? cudaMemcpyDefault : cudaMemcpyDeviceToHost;
     push([=] {
       ck(cudaEventRecord(prod, s0), "record");
       ck(cudaStreamWaitEvent(s1, prod, 0), "wait");
       ck(record_timer(tm.a, s1), "record");
-      ck(cudaMemcpyAsync(host, src, static_cast<size_t>(nbytes), cudaMemcpyDeviceToHost, s1), "D2H");
+      ck(cudaMemcpyAsync(host, src, static_cast<size_t>(nbytes), kind, s1), "copy-out");
       ck(record_timer(tm.b, s1), "record");
       ck(cudaEventRecord(done, s1), "record");
     }, 0);
     d2h_live[lid] = done;
     ex->d2h_bytes += nbytes;
     used_s1 = true;
+  }
+
+  // Where a copied-out tensor lives (reference UTP: host
+  // DRAM or "DRAM of other GPUs"): pinned host memory over PCIe, or HBM of
+  // opt.stash_device -- an NVLink peer's spare memory, or this device itself
+  // (loopback) -- addressed through UVA with peer access enabled.
+  char* stash_alloc(int64_t nbytes) {
+    char* p = nullptr;
+    if (!ex->opt.stash) {
+      ck(cudaHostAlloc(&p, static_cast<size_t>(nbytes), cudaHostAllocPortable), "cudaHostAlloc(stash)");
+      ex->mem[sn_exec::M_HOST] += nbytes;
+      return p;
+    }
+    const int dev = ex->opt.stash_device;
+    if (dev != ex->device) {
+      int can = 0;
+      ck(cudaDeviceCanAccessPeer(&can, ex->device, dev), "cudaDeviceCanAccessPeer");
+      if (!can)
+        xfail(SN_EK_CONFIG, "stash device " + std::to_string(dev) + " is not a peer of device " +
+                                std::to_string(ex->device));
+      const cudaError_t e = cudaDeviceEnablePeerAccess(dev, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) ck(e, "cudaDeviceEnablePeerAccess");
+      cudaGetLastError();
+      ck(cudaSetDevice(dev), "cudaSetDevice(stash)");
+    }
+    const cudaError_t e = cudaMalloc(&p, static_cast<size_t>(nbytes));
+    if (dev != ex->device) ck(cudaSetDevice(ex->device), "cudaSetDevice");
+    ck(e, "cudaMalloc(device stash)");
+    ex->mem[dev == ex->device ? sn_exec::M_STASH : sn_exec::M_PEER] += nbytes;
+    ex->peer_stash.push_back({p, dev});
+    return p;
   }
 
   void on_fetch(int lid) {
@@ -615,12 +644,13 @@ struct Compiler {
     cudaEvent_t before = ex->new_event(), done = ex->new_event(), out = d->second;
     cudaStream_t s0 = ex->s0, s2 = ex->s2;
     const sn_exec::Timer tm = ex->new_timer(1, nbytes);
+    const cudaMemcpyKind kind = ex->opt.stash ? cudaMemcpyDefault : cudaMemcpyHostToDevice;
     push([=] {
       ck(cudaEventRecord(before, s0), "record");
       ck(cudaStreamWaitEvent(s2, before, 0), "wait");
       ck(cudaStreamWaitEvent(s2, out, 0), "wait");
       ck(record_timer(tm.a, s2), "record");
-      ck(cudaMemcpyAsync(dst, host, static_cast<size_t>(nbytes), cudaMemcpyHostToDevice, s2), "H2D");
+      ck(cudaMemcpyAsync(dst, host, static_cast<size_t>(nbytes), kind, s2), "fetch");
       ck(record_timer(tm.b, s2), "record");
       ck(cudaEventRecord(done, s2), "record");
     }, 0);
@@ -1666,8 +1696,14 @@ void destroy(sn_exec* ex) {
   if (ex->staged_ev) cudaEventDestroy(ex->staged_ev);
   if (ex->consumed_ev) cudaEventDestroy(ex->consumed_ev);
   if (ex->s4) cudaStreamDestroy(ex->s4);
-  for (auto& kv : ex->stash)
-    if (kv.second) cudaFreeHost(kv.second);
+  if (!ex->opt.stash)
+    for (auto& kv : ex->stash)
+      if (kv.second) cudaFreeHost(kv.second);
+  for (auto& pd : ex->peer_stash) {
+    cudaSetDevice(pd.second);
+    cudaFree(pd.first);
+  }
+  if (!ex->peer_stash.empty()) cudaSetDevice(ex->device);
   if (ex->data_buf && ex->data_buf != ex->images) cudaFree(ex->data_buf);
   void* bufs[] = {ex->arena, ex->params, ex->grads, ex->state, ex->images, ex->labels, ex->loss_rows, ex->loss,
                   ex->iteration, ex->wt_scratch, ex->partial, ex->red, ex->tstats, ex->pool_scratch,
@@ -1702,6 +1738,7 @@ int sn_exec_create(const sn_plan* plan, const sn_net_desc* /*net*/, const sn_lay
     ex->net = &plan->plan.net;
     ex->opt = *opts;
     if (ex->opt.precision != 0 && ex->opt.precision != 1) xfail(SN_EK_CONFIG, "precision must be 0 (tf32) or 1 (fp32)");
+    if (ex->opt.stash != 0 && ex->opt.stash != 1) xfail(SN_EK_CONFIG, "stash must be 0 (pinned host) or 1 (device)");
     PrecisionScope prec(ex);
     ex->device = opts->device;
     ex->B = static_cast<int>(plan->plan.cost_cfg.batch);
@@ -2051,8 +2088,10 @@ int sn_exec_memory(const sn_exec* ex, sn_exec_mem* out) {
   out->wgrad_scratch_bytes = ex->mem[sn_exec::M_WGRAD];
   out->other_scratch_bytes = ex->mem[sn_exec::M_OTHER];
   out->host_stash_bytes = ex->mem[sn_exec::M_HOST];
+  out->device_stash_bytes = ex->mem[sn_exec::M_STASH];
+  out->peer_stash_bytes = ex->mem[sn_exec::M_PEER];
   out->device_total_bytes = 0;
-  for (int c = 0; c < sn_exec::M_HOST; ++c) out->device_total_bytes += ex->mem[c];
+  for (int c = 0; c <= sn_exec::M_STASH; ++c) out->device_total_bytes += ex->mem[c];
   out->wgrad_partials_outside_pool_bytes = ex->wgrad_partial_outside * 4;
   out->planned_arena_high_water = ex->plan->plan.report.pool_high_water_bytes;
   return SN_OK;

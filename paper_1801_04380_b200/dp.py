@@ -25,7 +25,7 @@ __all__ = ["DPContext", "init", "rank_seed", "unique_id", "share_unique_id", "bu
 
 
 class DPIdC(C.Structure):
-    _fields_ = [("bytes", C.c_char * 128)]
+    _fields_ = [("bytes", C.c_ubyte * 128)]  # c_ubyte: a c_char field would stop at the first NUL
 
 
 def _lib():
@@ -68,7 +68,7 @@ class DPContext:
             L = _lib()
             uid = self._uid if self._uid is not None else share_unique_id(self)
             cid = DPIdC()
-            C.memmove(cid.bytes, uid, 128)
+            C.memmove(C.addressof(cid), uid, 128)
             out = C.c_void_p()
             if L.sn_dp_comm_create(C.byref(cid), self.world, self.rank, device, C.byref(out)) != 0:
                 from .errors import DeviceError
@@ -124,7 +124,7 @@ def unique_id() -> bytes:
     if L.sn_dp_unique_id(C.byref(out)) != 0:
         from .errors import DeviceError
         raise DeviceError(_err(L))
-    return bytes(out.bytes) + b"\0" * (128 - len(bytes(out.bytes)))
+    return C.string_at(C.addressof(out), 128)
 
 
 def share_unique_id(ctx: DPContext) -> bytes:

@@ -57,7 +57,8 @@ PRECISIONS = {"tf32": 0, "fp32": 1}
 class ExecMemC(C.Structure):
     _fields_ = [(n, C.c_int64) for n in (
         "arena_bytes", "params_grads_bytes", "layer_state_bytes", "input_bytes", "wgrad_scratch_bytes",
-        "other_scratch_bytes", "host_stash_bytes", "device_total_bytes", "wgrad_partials_outside_pool_bytes",
+        "other_scratch_bytes", "host_stash_bytes", "device_stash_bytes", "peer_stash_bytes", "device_total_bytes",
+        "wgrad_partials_outside_pool_bytes",
         "planned_arena_high_water")]
 
 
@@ -193,7 +194,8 @@ class Executor:
     def __init__(self, net: NetworkDef, config: SimConfig, device: int = 0, *, seed: int = 2,
                  dropout_seed: int = 1234, lr: float = 0.01, grad_scale: float = 1.0,
                  elide_backups: bool = True, use_graph: bool = True, params: dict | None = None,
-                 precision: str = "tf32", dp=None, dp_bucket_bytes: int = 0) -> None:
+                 precision: str = "tf32", dp=None, dp_bucket_bytes: int = 0, stash: str = "host",
+                 stash_device: int | None = None) -> None:
         import torch
         if not torch.cuda.is_available():
             raise DeviceError("run_training needs a CUDA device (B200); there is no CPU fallback")
@@ -219,8 +221,14 @@ class Executor:
             dropout_seed = rank_seed(dropout_seed, self.dp)
             if grad_scale == 1.0:
                 grad_scale = 1.0 / self.dp.world
+        # Unified Tensor Pool backing store of copied-out tensors: pinned host
+        # memory ("host", PCIe) or HBM of a device ("device": stash_device, an
+        # NVLink peer, or this GPU itself as a loopback)
+        if stash not in ("host", "device"):
+            raise MemschedError(f"stash must be 'host' or 'device', got {stash!r}")
         opts = ExecOptionsC(device, int(elide_backups), int(use_graph), 0, dropout_seed, lr, grad_scale,
-                            PRECISIONS[precision], 0, device, 0, comm,
+                            PRECISIONS[precision], int(stash == "device"),
+                            device if stash_device is None else stash_device, 0, comm,
                             self.dp.world if self.dp else 1, self.dp.rank if self.dp else 0, dp_bucket_bytes)
         self.ptr = C.c_void_p()
         torch.cuda.set_device(device)

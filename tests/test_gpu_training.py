@@ -517,3 +517,38 @@ def test_dp_world1_nccl_path_is_bit_identical(cuda, alex32_case, which):
     assert l0 == l1
     assert _bitwise(p0, p1) and _bitwise(g0, g1)
     assert any(not torch.equal(p0[l]['w'], params[l]['w']) for l in params)  # the updates ran
+
+
+# ---- UTP backing store in device memory (peer HBM; loopback on one GPU) ----
+
+def test_device_stash_loopback_is_bit_identical(cuda):
+    """The Unified Tensor Pool's copy-out store in HBM (stash="device": an
+    NVLink peer's memory, here the same GPU as a loopback) instead of pinned
+    host memory: the AlexNet b250 cache-knee schedule (evictions and demand
+    fetches of 477,024,000 bytes) gives bit-identical gradients, and the
+    copies run device-to-device."""
+    from paper_1801_04380_b200.training import init_parameters
+    net = _fixture("alexnet")
+    params = init_parameters(net, seed=3, head_scale=0.1)
+    images, labels = _inputs(net, 250, seed=5)
+    _, base, _, _ = _run(net, 250, 8 << 30, "none", params, images, labels)
+    sn = _sn()
+    from paper_1801_04380_b200.training import Executor
+    cfg = sn.SimConfig(pool_bytes=1536 << 20, features=sn.parse_features("cache"), cost=sn.CostConfig(batch=250))
+    ex = Executor(net, cfg, params=params, stash="device")
+    ex.set_inputs(images, labels)
+    _, t = ex.step(update=False)
+    grads = ex.get("grads")
+    mem = ex.memory()
+    xfer = ex.transfer_stats()
+    ex.close()
+    assert _bitwise(grads, base)
+    assert t.h2d_bytes > 0 and mem["device_stash_bytes"] > 0 and mem["host_stash_bytes"] == 0
+    assert xfer["h2d_GBps"] and xfer["h2d_GBps"] > 100  # not PCIe-bound
+
+
+def test_device_stash_parity_copies_bit_identical(cuda, alex32_case):
+    net, params, images, labels = alex32_case
+    _, base, _, _ = _run(net, 16, 1 << 30, ALL, params, images, labels)
+    _, dev, _, t = _run(net, 16, 1 << 30, ALL, params, images, labels, elide_backups=False, stash="device")
+    assert t.d2h_bytes == 10822272 and _bitwise(dev, base)
