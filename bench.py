@@ -57,6 +57,8 @@ def parse_args():
     ap.add_argument("--pool-bytes", type=int, default=None, help="pool budget in bytes (overrides --pool-gib), "
                     "e.g. the schedulable floor max_i(l_i) = 3288334336 for resnet50g b256")
     ap.add_argument("--features", default=ALL)
+    ap.add_argument("--stash", default="host", choices=["host", "device"],
+                    help="UTP copy-out store: pinned host memory (PCIe) or device HBM (peer / loopback)")
     ap.add_argument("--precision", default="tf32", choices=["tf32", "fp32"],
                     help="CONV/FC math: tf32 tensor cores (headline) or the fp32-faithful 3xTF32 mode")
     ap.add_argument("--no-extras", action="store_true", help="skip the unconstrained / profile / baseline legs")
@@ -249,7 +251,8 @@ def run_ours(args) -> None:
     cfg = sn.SimConfig(pool_bytes=pool, features=sn.parse_features(args.features), cost=sn.CostConfig(batch=B))
     free0 = torch.cuda.mem_get_info(local)[0]
     # weight-gradient all-reduce: NCCL buckets inside the executor's step (dp=ctx)
-    ex = Executor(net, cfg, device=local, seed=2, lr=0.01, precision=args.precision, dp=ctx if world > 1 else None)
+    ex = Executor(net, cfg, device=local, seed=2, lr=0.01, precision=args.precision, dp=ctx if world > 1 else None,
+                  stash=args.stash)
     free1 = torch.cuda.mem_get_info(local)[0]
     rep = ex.report
     c, h, w = sn.propagate_shapes(net)[net.data_id]
@@ -339,8 +342,9 @@ def run_ours(args) -> None:
         "scaling": "weak", "vs_baseline": None, "dtype": ("fp32 storage, tf32 tensor-core math (fp32 accumulate)" if args.precision == "tf32"
                   else "fp32 (3xTF32 split operands on tensor cores, fp32-level products, fp32 accumulate)"),
         "data": "synthetic N(0,1) images, uniform labels; He-uniform weights (seed 2)",
-        "config": {"workload": f"{args.net}_b{B}_pool{args.pool_gib:g}GiB_{args.features.replace(',', '+')}",
-                   "model": args.net, "global_batch": B * world, "per_gpu_batch": B, "image": [c, h, w],
+        "config": {"workload": f"{args.net}_b{B}_pool{args.pool_gib:g}GiB_{args.features.replace(',', '+')}"
+                               + ("" if args.stash == "host" else "_stash-device"),
+                   "model": args.net, "global_batch": B * world, "stash": args.stash, "per_gpu_batch": B, "image": [c, h, w],
                    "parallelism": f"dp{world}", "pool_bytes": pool, "features": args.features,
                    "l2": "no flush needed: per-step working set (~3.3 GB arena) >> 126 MB L2"},
         "e2e": {"value": round(B * world * e_steps / e2e_wall, 2), "unit": "images/s",

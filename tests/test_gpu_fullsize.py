@@ -1,0 +1,116 @@
+"""Every BASELINE.json config pinned numerically on the GPU, one training step
+each, at full (or the largest CPU-oracle-tractable) size, in both numeric modes,
+against the CPU oracle (oracle/numerics.py) on identical inputs and weights.
+
+Stated tolerances (per parameter tensor, relative Frobenius; a CONV bias that
+feeds a training-mode BN has a zero true gradient and is compared absolutely
+against the layer's weight-gradient norm):
+  * precision="fp32" (3xTF32): at least as close to the fp64 oracle as the CPU
+    fp32 oracle is (<= 2x its error), and <= 1e-4 wherever the CPU fp32 error
+    is <= 5e-6 -- deep nets with training-mode BN are ill-conditioned for any
+    fp32 computation (the CPU fp32 oracle itself is up to ~1e-2 off fp64 on
+    ResNet-50g b8 BN gradients), so a fixed 1e-4 would test the oracle, not
+    the kernels; loss <= 1e-5 relative to fp64.
+  * precision="tf32": within 3x (+5e-3) of how far tf32 rounding alone moves
+    the fp32 gradients (the oracle's tf32 emulation), loss <= 5e-3.
+Batches: the config's own where the CPU oracle (fp32 + fp64 + tf32 emulation)
+runs in about a minute, else the largest that does (DenseNet-style 64,
+Inception-style 16, ResNet-2534g 4); override with SN_FULLSIZE_BATCH=<n>.
+A summary per config is written to gpurun_out/fullsize_<config>.json when
+that directory exists.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ALL = "liveness,offload,cache,recompute=cost-aware,convselect"
+GiB = 1 << 30
+CONFIGS = {  # name: (batch, pool bytes)
+    "alex32": (16, 1 << 30),
+    "resnet50g": (256, 24 * GiB),
+    "resnet152g": (64, 24 * GiB),
+    "densenet121s": (64, 24 * GiB),
+    "inception4s": (16, 24 * GiB),
+    "resnet2534g": (4, 12 * 10 ** 9),
+}
+
+
+def _net(name):
+    import paper_1801_04380_b200 as sn
+    from paper_1801_04380_b200 import netgen
+    blocks = {"resnet50g": (3, 4, 6, 3), "resnet152g": (3, 8, 36, 3), "resnet2534g": (211, 211, 211, 211)}
+    if name in blocks:
+        return netgen.gen_resnet(*blocks[name])
+    return sn.load_network(os.path.join(ROOT, "paper_1801_04380_b200", "fixtures", f"{name}.net"))
+
+
+def _errs(net, grads, ref):
+    from oracle.numerics import relative_error
+    out = {}
+    for l in ref:
+        lay = net.layers[l]
+        bn_fed = lay.kind.value == "CONV" and any(net.layers[n].kind.value == "BN" for n in lay.next)
+        out[(lay.name, "w")] = relative_error(grads[l]["w"], ref[l]["w"])
+        out[(lay.name, "b")] = ((grads[l]["b"] - ref[l]["b"]).double().norm().item() / ref[l]["w"].double().norm().item()
+                                if bn_fed else relative_error(grads[l]["b"], ref[l]["b"]))
+    return out
+
+
+@pytest.mark.parametrize("name", list(CONFIGS))
+def test_config_matches_oracle_both_modes(cuda, name):
+    import paper_1801_04380_b200 as sn
+    from paper_1801_04380_b200.training import Executor, init_parameters
+    from oracle.numerics import forward_backward
+    batch, pool = CONFIGS[name]
+    batch = int(os.environ.get("SN_FULLSIZE_BATCH", batch))
+    net = _net(name)
+    params = init_parameters(net, seed=2, head_scale=0.1)
+    c, h, w = sn.propagate_shapes(net)[net.data_id]
+    import math
+    ncls = math.prod(sn.propagate_shapes(net)[net.terminal_id])
+    images = torch.randn(batch, c, h, w, generator=torch.Generator().manual_seed(0))
+    labels = torch.randint(0, ncls, (batch,), generator=torch.Generator().manual_seed(1))
+    cfg = sn.SimConfig(pool_bytes=pool, features=sn.parse_features(ALL), cost=sn.CostConfig(batch=batch))
+    gpu = {}
+    for prec in ("tf32", "fp32"):
+        ex = Executor(net, cfg, params=params, precision=prec)
+        ex.set_inputs(images, labels)
+        loss, _ = ex.step(update=False)
+        gpu[prec] = (loss, ex.get("grads"))
+        peak, floor = ex.report.peak_bytes, ex.report.min_pool_bytes
+        ex.close()
+    torch.set_num_threads(len(os.sched_getaffinity(0)))
+    l32, r32 = forward_backward(net, params, images, labels)
+    l64, r64 = forward_backward(net, params, images, labels, dtype=torch.float64)
+    _, remu = forward_backward(net, params, images, labels, tf32=True)
+    # fp32 mode vs fp64, relative to the CPU fp32 oracle's own distance
+    e_gpu, e_cpu = _errs(net, gpu["fp32"][1], r64), _errs(net, r32, r64)
+    bad32 = {k: (e_gpu[k], e_cpu[k]) for k in e_gpu
+             if e_gpu[k] > max(2 * e_cpu[k], 1e-4 if e_cpu[k] <= 5e-6 else 0.0) and e_gpu[k] > 5e-6}
+    # tf32 mode vs fp32, relative to tf32 rounding's own effect
+    sens = max(_errs(net, remu, r32).values())
+    e_tf = _errs(net, gpu["tf32"][1], r32)
+    worst_tf = max(e_tf.values())
+    summary = {"config": name, "batch": batch, "peak_bytes": peak, "min_pool_bytes": floor,
+               "loss": {"fp64_oracle": l64, "fp32_oracle": l32, "gpu_fp32_mode": gpu["fp32"][0],
+                        "gpu_tf32_mode": gpu["tf32"][0]},
+               "fp32_mode_worst_vs_fp64": max(e_gpu.values()), "cpu_fp32_worst_vs_fp64": max(e_cpu.values()),
+               "fp32_mode_median_vs_fp64": sorted(e_gpu.values())[len(e_gpu) // 2],
+               "tf32_mode_worst_vs_fp32": worst_tf, "tf32_emulation_sensitivity": sens,
+               "fp32_violations": {f"{k[0]}.{k[1]}": v for k, v in bad32.items()}}
+    if os.path.isdir(os.path.join(ROOT, "gpurun_out")):
+        with open(os.path.join(ROOT, "gpurun_out", f"fullsize_{name}.json"), "w") as fh:
+            json.dump(summary, fh, indent=1)
+    assert abs(gpu["fp32"][0] - l64) <= 1e-5 * abs(l64), summary["loss"]
+    assert not bad32, sorted(bad32.items(), key=lambda kv: -kv[1][0])[:6]
+    assert abs(gpu["tf32"][0] - l32) <= 5e-3 * abs(l32), summary["loss"]
+    assert worst_tf <= 3 * sens + 5e-3, (worst_tf, sens)
