@@ -429,11 +429,13 @@ cudaError_t fc_gemm_bn(int a_mn, int b_mn, const float* A, int lda, const float*
 cudaError_t fc_gemm(int a_mn, int b_mn, const float* A, int lda, const float* B, int ldb, int M, int N, int K,
                     float* partial, int splits, cudaStream_t st) {
   if (N <= 64) return fc_gemm_bn<64>(a_mn, b_mn, A, lda, B, ldb, M, N, K, partial, splits, st);
-  if (N <= 128) return fc_gemm_bn<128>(a_mn, b_mn, A, lda, B, ldb, M, N, K, partial, splits, st);
+  if (N <= 128 || gemm_precision() == 1) return fc_gemm_bn<128>(a_mn, b_mn, A, lda, B, ldb, M, N, K, partial, splits, st);
   return fc_gemm_bn<256>(a_mn, b_mn, A, lda, B, ldb, M, N, K, partial, splits, st);
 }
 
-int bn_for(int n) { return n <= 64 ? 64 : (n <= 128 ? 128 : 256); }
+// tile width of the gather GEMMs; the fp32-faithful mode stays at <= 128, where
+// two TMEM partial accumulators fit beside the running sum (gemm_tc.cuh)
+int bn_for(int n) { return n <= 64 ? 64 : ((n <= 128 || gemm_precision() == 1) ? 128 : 256); }
 
 }  // namespace
 
@@ -677,7 +679,7 @@ cudaError_t fc_wgrad(int B, int I, int O, const float* x, const float* dy, float
     MatMNLoader<64> lb{};
     lb.base = x; lb.rows = I; lb.K = B; lb.ld = I; lb.fast = (reinterpret_cast<uintptr_t>(x) % 16 == 0) && I % 4 == 0;
     err = launch_tc_gemm<64, 4, true, true>(la, lb, e, O, I, B, 1, st);
-  } else if (I <= 128) {
+  } else if (I <= 128 || gemm_precision() == 1) {
     MatMNLoader<128> lb{};
     lb.base = x; lb.rows = I; lb.K = B; lb.ld = I; lb.fast = (reinterpret_cast<uintptr_t>(x) % 16 == 0) && I % 4 == 0;
     err = launch_tc_gemm<128, 4, true, true>(la, lb, e, O, I, B, 1, st);

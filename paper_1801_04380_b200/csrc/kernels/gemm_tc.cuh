@@ -22,11 +22,16 @@
 // twins double the smem per stage).  The tensor core's accumulation into TMEM
 // is not round-to-nearest: measured (tools/precision_probe.py) it loses about
 // 2^-25 of the running sum per MMA, toward zero, so a long K chain drifts
-// (K = 2048: 2.3e-5 on positive data).  SPLIT3 therefore restarts the TMEM
-// accumulator every kDrainGroup k blocks: the producer warps add each group's
-// partial into a second TMEM region (fp32 round-to-nearest on the CUDA cores)
-// and the final epilogue adds the two -- the drift is bounded by one group's
-// 12 * kDrainGroup MMAs whatever K is.
+// (K = 2048: 2.3e-5 on positive data), and that drift is biased, so it
+// compounds through a deep network.  SPLIT3 therefore restarts the TMEM
+// accumulator every split3_group() k blocks: the producer warps add each
+// group's partial into a running sum in TMEM (fp32 round-to-nearest on the
+// CUDA cores) and the epilogue adds the last group -- the drift is bounded by
+// one group's 12 * group MMAs whatever K is.  With BN <= 128 two partial
+// accumulators alternate (one k block per group, drained while the tensor
+// core fills the other); BN = 256 has room for one (4 blocks per group, the
+// MMA waits for each drain).  lo is rounded to tf32 explicitly, so the
+// hardware's own operand conversion drops nothing (unbiased).
 //
 // The operand gathers are policy objects (see conv loaders in conv_tc.cu):
 //   struct Loader { __device__ void tile_init(int r0, void* scratch, int tid);
@@ -57,7 +62,15 @@ template <int BN>
 __host__ __device__ constexpr uint32_t tmem_cols() {
   return BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
 }
-constexpr int kDrainGroup = 4;  // SPLIT3: k blocks per TMEM accumulation chain
+// SPLIT3 accumulation: partial accumulators in TMEM and k blocks per group
+template <int BN>
+constexpr int split3_accs() {
+  return BN <= 128 ? 2 : 1;
+}
+template <int BN>
+constexpr int split3_group() {
+  return split3_accs<BN>() == 2 ? 1 : 4;
+}
 
 // MN-major tile of 32 k-rows x R mn-elements in the SWIZZLE_128B_BASE32B
 // canonical layout: MN atoms (32 elements x 4 k rows = 512 B) are adjacent
@@ -89,7 +102,8 @@ __device__ __forceinline__ void split3_tile(uint8_t* tile, uint8_t* twin, int ti
     float4 v = *reinterpret_cast<const float4*>(tile + off);
     const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
     *reinterpret_cast<float4*>(tile + off) = h;
-    *reinterpret_cast<float4*>(twin + off) = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+    *reinterpret_cast<float4*>(twin + off) =
+        make_float4(tf32_hi(v.x - h.x), tf32_hi(v.y - h.y), tf32_hi(v.z - h.z), tf32_hi(v.w - h.w));
   }
 }
 
@@ -107,9 +121,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
   uint64_t* empty = full + STAGES;
   uint64_t* done = empty + STAGES;
-  uint64_t* drain_full = done + 1;   // SPLIT3: a group's partial is complete in TMEM
-  uint64_t* drain_empty = done + 2;  // SPLIT3: ... and folded into the running sum
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 3);
+  uint64_t* drain_full = done + 1;   // SPLIT3 [2]: a group's partial is complete in TMEM
+  uint64_t* drain_empty = done + 3;  // SPLIT3 [2]: ... and folded into the running sum
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 5);
   uint8_t* scratch_a = smem + L::SCRATCH_OFF;
   uint8_t* scratch_b = scratch_a + kScratchBytes;
 
@@ -128,11 +142,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(done, 1);
-    mbar_init(drain_full, 1);
-    mbar_init(drain_empty, kProducers);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&drain_full[a], 1);
+      mbar_init(&drain_empty[a], kProducers);
+    }
     fence_mbar_init();
   }
-  constexpr uint32_t kTmemCols = tmem_cols<BN>() * (SPLIT3 ? 2 : 1);  // SPLIT3: + the running sum
+  constexpr int kAcc = SPLIT3 ? split3_accs<BN>() : 1;
+  constexpr int kG = split3_group<BN>();
+  // SPLIT3: kAcc partial accumulators + the running sum (a power of two of columns)
+  constexpr uint32_t kTmemCols = tmem_cols<BN>() * (SPLIT3 ? (kAcc == 2 ? 4 : 2) : 1);
   if (warp == 4) tmem_alloc(tmem_slot, kTmemCols);
   if (tid < kProducers) {
     la.tile_init(m0, scratch_a, tid);
@@ -143,6 +162,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  const int last_group = (nkb - 1) / kG;  // SPLIT3 accumulation groups 0 .. last_group
   if (warp < 4) {
     // ---------------- producers ----------------
     constexpr int LAG = STAGES - 1;
@@ -159,19 +179,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_arrive(&full[s]);
     };
     const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
-    const uint32_t run_col = tmem_cols<BN>();
-    // SPLIT3: after publishing the last block of a non-final accumulation
-    // group, fold that group's TMEM partial into the running sum (RN adds)
+    const uint32_t run_col = tmem_cols<BN>() * kAcc;
+    // SPLIT3: fold group d's TMEM partial into the running sum (RN adds).  With
+    // two accumulators this runs after the first block of group d + 1 is
+    // published, so the tensor core fills the other one meanwhile.
     auto drain_after = [&](int j) {
       if constexpr (SPLIT3) {
-        if (j % kDrainGroup != kDrainGroup - 1 || j == nkb - 1) return;
-        const int d = j / kDrainGroup;
-        mbar_wait(drain_full, d & 1);
+        const int d = (j + 1 - kAcc) / kG;  // candidate group finished by publishing j
+        if (j + 1 - kAcc < 0 || (j + 1 - kAcc) % kG != kG - 1 || d >= last_group) return;
+        const int a = d % kAcc;
+        mbar_wait(&drain_full[a], (d / kAcc) & 1);
         tc_fence_after();
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
           float v[32];
-          tmem_ld32(tmem + lane_base + static_cast<uint32_t>(c), v);
+          tmem_ld32(tmem + lane_base + static_cast<uint32_t>(a * tmem_cols<BN>() + c), v);
           if (d > 0) {
             float r[32];
             tmem_ld32(tmem + lane_base + run_col + static_cast<uint32_t>(c), r);
@@ -181,7 +203,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           tmem_st32(tmem + lane_base + run_col + static_cast<uint32_t>(c), v);
         }
         tc_fence_before();
-        mbar_arrive(drain_empty);
+        mbar_arrive(&drain_empty[a]);
       }
     };
     for (int i = 0; i < nkb; ++i) {
@@ -206,11 +228,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     mbar_wait(done, 0);
     tc_fence_after();
     const int row = warp * 32 + lane;
-    const bool drained = SPLIT3 && nkb > kDrainGroup;
+    const bool drained = SPLIT3 && last_group > 0;
+    const uint32_t acc_col = SPLIT3 ? static_cast<uint32_t>((last_group % kAcc) * tmem_cols<BN>()) : 0u;
 #pragma unroll 1
     for (int c = 0; c < BN; c += 32) {
       float v[32];
-      tmem_ld32(tmem + lane_base + static_cast<uint32_t>(c), v);
+      tmem_ld32(tmem + lane_base + acc_col + static_cast<uint32_t>(c), v);
       if (drained) {
         float r[32];
         tmem_ld32(tmem + lane_base + run_col + static_cast<uint32_t>(c), r);
@@ -225,11 +248,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     constexpr uint32_t idesc = idesc_tf32(kBM, BN, A_MN, B_MN);
     for (int i = 0; i < nkb; ++i) {
       const int s = i % STAGES;
-      // SPLIT3: a new accumulation group starts from zero once the previous
-      // group's partial has been folded into the running sum
-      const bool fresh = SPLIT3 ? (i % kDrainGroup == 0) : (i == 0);
-      if (SPLIT3 && i > 0 && fresh) {
-        mbar_wait(drain_empty, ((i / kDrainGroup) - 1) & 1);
+      // SPLIT3: group g accumulates from zero into accumulator g % kAcc once
+      // that accumulator's previous group has been folded into the running sum
+      const int g = i / kG;
+      const bool fresh = SPLIT3 ? (i % kG == 0) : (i == 0);
+      const uint32_t dtm = tmem + (SPLIT3 ? static_cast<uint32_t>((g % kAcc) * tmem_cols<BN>()) : 0u);
+      if (SPLIT3 && fresh && g >= kAcc) {
+        mbar_wait(&drain_empty[g % kAcc], ((g - kAcc) / kAcc) & 1);
         tc_fence_after();
       }
       mbar_wait(&full[s], (i / STAGES) & 1);
@@ -248,17 +273,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             B_MN ? umma_desc(b0 + kk * 2 * MNTile<BN>::SBO, MNTile<BN>::LBO, MNTile<BN>::SBO,
                              kLayoutSW128Base32)
                  : umma_desc(b0 + kk * 32, 16, 1024, kLayoutSW128);
-        umma_tf32(tmem, ad, bd, idesc, (fresh && kk == 0) ? 0u : 1u);
+        umma_tf32(dtm, ad, bd, idesc, (fresh && kk == 0) ? 0u : 1u);
         if constexpr (SPLIT3) {
           // the twins sit at a fixed offset with the same 1024-aligned swizzle
           // phase: the descriptors differ only in their start address (16 B units)
           constexpr uint64_t kLoA = static_cast<uint64_t>(L::LO_OFF) >> 4;
-          umma_tf32(tmem, ad, bd + kLoA, idesc, 1u);
-          umma_tf32(tmem, ad + kLoA, bd, idesc, 1u);
+          umma_tf32(dtm, ad, bd + kLoA, idesc, 1u);
+          umma_tf32(dtm, ad + kLoA, bd, idesc, 1u);
         }
       }
       umma_commit(&empty[s]);
-      if (SPLIT3 && i % kDrainGroup == kDrainGroup - 1 && i != nkb - 1) umma_commit(drain_full);
+      if (SPLIT3 && (i % kG == kG - 1) && g < last_group) umma_commit(&drain_full[g % kAcc]);
     }
     umma_commit(done);
   }
