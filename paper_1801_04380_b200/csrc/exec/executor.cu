@@ -958,20 +958,6 @@ struct Compiler {
           dcb = ex->grads + ex->L[pid].b_off;
           conv_bias_done[pid] = 1;
         }
-        auto pp = pending_pool.find(static_cast<int>(cur_ti));
-        if (pp != pending_pool.end()) {
-          const LayerRt& lp = ex->L[pp->second.pool];
-          const sn::PoolShape ps = lp.pool;
-          const uint8_t* am = lp.argmax;
-          const float* dyp = pp->second.dy_pool;
-          pending_pool.erase(pp);
-          push([=] {
-            ck(sn::bn_bwd_pool(ps, am, dyp, x, rows, C, g, beta, stats, relu, dx, acc, dg, dbt, red, st, dcb),
-               "bn_bwd_pool");
-          },
-               dx ? (dcb ? 4 : 3) : 2);
-          break;
-        }
         push([=] {
           ck(sn::bn_bwd(x, dy, rows, C, g, beta, stats, relu, dx, acc, dg, dbt, red, st, dcb, cpy, cpy_acc, own),
              "bn_bwd");
@@ -1005,10 +991,6 @@ struct Compiler {
         void* scratch = ex->pool_scratch;
         const int nk = sn::pool_bwd_kernels(ps);
         const uint8_t* am = l.argmax;
-        if (dx && !acc && pool_to_bn[cur_ti] >= 0) {  // launched by the BN backward it feeds
-          pending_pool[pool_to_bn[cur_ti]] = PendingPool{dy, lid};
-          break;
-        }
         if (dx) push([=] { ck(sn::pool_bwd(ps, x, y, dy, dx, acc, scratch, st, am), "pool_bwd"); }, nk);
         break;
       }
@@ -1120,16 +1102,6 @@ struct Compiler {
   };
   std::vector<char> join_copy_own;
   std::unordered_map<int, PendingJoin> pending_join;  // keyed by BN-backward tape index
-  // max POOL backward (saved argmax) -> folded ReLU backward -> BN backward:
-  // the BN's two passes gather their dy from the pool output's gradient
-  // (sn::bn_bwd_pool), the pool backward launches nothing.  Bit-identical to
-  // the unfused kernels, so the fusion may depend on the schedule.
-  std::vector<int> pool_to_bn, bn_from_pool;
-  struct PendingPool {
-    const float* dy_pool = nullptr;
-    int pool = -1;
-  };
-  std::unordered_map<int, PendingPool> pending_pool;  // keyed by BN-backward tape index
   // CONV forward -> BN forward (next compute action, reading that output): the
   // CONV epilogue emits per-tile statistics, the BN only combines them.
   bool conv_stats_now = false, bn_tiles_now = false;
@@ -1168,8 +1140,6 @@ struct Compiler {
     bn_from_join.assign(T, -1);
     join_relu.assign(T, -1);
     join_copy_own.assign(T, 0);
-    pool_to_bn.assign(T, -1);
-    bn_from_pool.assign(T, -1);
     bn_bias_at.assign(T, 0);
     conv_bias_done.assign(net.n, 0);
     const char* env = std::getenv("SN_FUSE");  // SN_FUSE=0: one kernel per layer (A/B and bitwise tests)
@@ -1490,47 +1460,6 @@ struct Compiler {
           break;
         }
         if (f.op == 'B' && f.b != ra) break;  // another backward in between: keep it simple
-      }
-    }
-    // POOL backward -> BN backward: safe when the pool output's gradient (read
-    // by both BN passes) is not re-allocated over before the BN backward, and
-    // nothing but the folded ReLU backward and non-kernel events lie between.
-    // SN_FUSE_POOL_BN=0 turns it off alone (the bitwise A/B test).
-    const char* env_pb = std::getenv("SN_FUSE_POOL_BN");
-    for (size_t i = 0; i < T && !(env_pb && env_pb[0] == '0'); ++i) {
-      const snp::Event& e = P.tape[i];
-      if (e.op != 'B' || net.kind[e.b] != snp::POOL) continue;
-      const int pl = e.b;
-      const LayerRt& lp = ex->L[pl];
-      const int ra = net.prev[pl][0];
-      if (!lp.argmax || !bn_relu_pair(ra) || net.next[ra].size() != 1) continue;
-      const int bn = net.prev[ra][0];
-      if (net.grad_owner(ra) != bn || !sn::pool_bn_bwd_ok(lp.pool, ex->L[bn].C) || net.grad_owner(pl) != pl) continue;
-      int64_t joff = -1, jblk = 0;
-      for (size_t j = i; j-- > 0;) {
-        const snp::Event& f = P.tape[j];
-        if (f.op == 'A' && f.a == snp::K_GRAD && f.b == pl) {
-          joff = f.c;
-          jblk = f.d;
-          break;
-        }
-      }
-      if (joff < 0) continue;
-      for (size_t j = i + 1; j < T; ++j) {
-        const snp::Event& f = P.tape[j];
-        if (f.op == 'A' && overlap(f.c, f.d, joff, jblk)) break;
-        if (f.op == 'B' && f.b == ra) {
-          if (!act_bwd_skip[j]) break;
-          continue;
-        }
-        if (f.op == 'B' && f.b == bn) {
-          if (bn_bwd_relu[j] && bn_from_join[j] < 0) {
-            pool_to_bn[i] = static_cast<int>(j);
-            bn_from_pool[j] = static_cast<int>(i);
-          }
-          break;
-        }
-        if (is_compute(f.op) && !(f.op == 'R' && dead_at[j])) break;
       }
     }
     ex->elided = elide_out;

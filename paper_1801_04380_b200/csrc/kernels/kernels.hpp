@@ -160,17 +160,6 @@ cudaError_t bn_bwd(const float* x, const float* dy, int64_t rows, int C, const f
                    const float* stats, int relu, float* dx, int accumulate, float* dgamma, float* dbeta,
                    float* red_scratch, cudaStream_t st, float* dbias = nullptr, float* copy_dst = nullptr,
                    int copy_acc = 0, float* copy2 = nullptr);
-// The backward of max POOL (3x3 / s2 / p1 with saved argmax) -> [ReLU] -> BN
-// in the BN's two passes: dy (the pool input's gradient) is gathered from
-// the pool output's gradient and the argmax where each pass needs it, never
-// materialised; bit-identical to pool_bwd + bn_bwd (same picks, same sums).
-// x = the BN input (rows = N*H*W of the pool input); other arguments as bn_bwd.
-struct PoolShape;
-bool pool_bn_bwd_ok(const PoolShape& ps, int bn_C);
-cudaError_t bn_bwd_pool(const PoolShape& ps, const uint8_t* argmax, const float* dy_pool, const float* x, int64_t rows,
-                        int C, const float* gamma, const float* beta, const float* stats, int relu, float* dx,
-                        int accumulate, float* dgamma, float* dbeta, float* red_scratch, cudaStream_t st,
-                        float* dbias = nullptr);
 // copy2 (optional, C % 4 == 0): the statistics pass also writes dy there and
 // the dx pass reads dy from it (dx may then overlap the original dy).
 // copy_dst (optional, C % 4 == 0): the fused backward of the 2-input JOIN

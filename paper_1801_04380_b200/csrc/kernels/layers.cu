@@ -179,65 +179,6 @@ struct RedBnBwdOp {
   }
 };
 
-// The gradient a 3x3 / stride 2 / pad 1 max pool (H = 2P, W = 2Q, saved
-// argmax) sends to input element quad i4 of [N][H][W][C/4], computed where it
-// is needed instead of materialised: the same picks, in the same order, from
-// +0 as pool_max_bwd_k3s2 -- so the value is bit-identical to the one that
-// kernel stores.  Input (2m+dh, 2k+dw) is window offset (dh+1, dw+1) of
-// window (m, k), (dh+1, dw-1) of (m, k+1), (dh-1, dw+1) of (m+1, k), (dh-1,
-// dw-1) of (m+1, k+1).
-struct PoolGatherDy {
-  PoolShape s;
-  const uchar4* arg;
-  const float4* dyp;  // the pool output's gradient [N][P][Q][C/4]
-  __device__ float4 operator()(int64_t i4) const {
-    const int C4 = s.C >> 2;
-    const int c4 = static_cast<int>(i4 % C4);
-    int64_t t = i4 / C4;
-    const int w = static_cast<int>(t % s.W);
-    t /= s.W;
-    const int h = static_cast<int>(t % s.H);
-    const int n = static_cast<int>(t / s.H);
-    const int m = h >> 1, k = w >> 1, dh = h & 1, dw = w & 1;
-    const int64_t wb = (static_cast<int64_t>(n) * s.P + m) * s.Q + k;
-    float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
-    auto pick = [&](int64_t win, int off) {
-      const uchar4 a = arg[win * C4 + c4];
-      const float4 g = dyp[win * C4 + c4];
-      o.x += (a.x == off) ? g.x : 0.f;
-      o.y += (a.y == off) ? g.y : 0.f;
-      o.z += (a.z == off) ? g.z : 0.f;
-      o.w += (a.w == off) ? g.w : 0.f;
-    };
-    const bool k1 = k + 1 < s.Q, m1 = m + 1 < s.P;
-    pick(wb, (dh + 1) * 3 + dw + 1);
-    if (dw && k1) pick(wb + 1, (dh + 1) * 3 + dw - 1);
-    if (dh && m1) pick(wb + s.Q, (dh - 1) * 3 + dw + 1);
-    if (dh && dw && k1 && m1) pick(wb + s.Q + 1, (dh - 1) * 3 + dw - 1);
-    return o;
-  }
-};
-
-// RedBnBwdOp with dy gathered from a max pool's output gradient (the fused
-// pool -> ReLU -> BN backward): identical summands, so identical sums.
-struct RedBnBwdPoolOp {
-  const float* x;
-  PoolGatherDy dy;
-  const float* stats;
-  const float* gamma;
-  const float* beta;
-  int relu;
-  using P = Bn4;
-  using R = RedBnBwdOp::R;
-  __device__ P prep4(int c, int C) const { return bn_params4(stats, gamma, beta, c, C); }
-  __device__ R load(int64_t off) const { return R{dy(off >> 2), ld4(x + off)}; }
-  __device__ void side(int64_t, const R&) const {}
-  __device__ void comp(const P& p, const R& r, float4& a, float4& b) const {
-    RedBnBwdOp{x, nullptr, stats, gamma, beta, relu, nullptr, 0, nullptr}.comp(p, r, a, b);
-  }
-  __device__ void eval(int64_t, int, int, float&, float&) const {}  // float4 path only
-};
-
 // Stage 1, float4 variant for C % 4 == 0: block b reduces rows [b*chunk,
 // (b+1)*chunk) into part[b][2][C] (doubles).  A thread owns 4 adjacent
 // channels and walks its rows with kUnroll independent accumulators (fixed
@@ -419,7 +360,7 @@ cudaError_t colred(Op op, Fin fin, int64_t rows, int C, float* scratch_f, cudaSt
   // RedBnBwdOp (two operands + side copies per row): one 512-thread block per
   // SM without a register cap beats two capped ones (eager A/B over the step:
   // 9.47 vs 9.52 ms, SN_COLRED_ROWS experiment)
-  if (v4 && (std::is_same<Op, RedBnBwdOp>::value || std::is_same<Op, RedBnBwdPoolOp>::value))
+  if (v4 && std::is_same<Op, RedBnBwdOp>::value)
     colred_stage1_v4<Op, 4, 1><<<static_cast<int>(nb), kRedThreads, 0, st>>>(op, rows, C, chunk, part);
   else if (v4)
     colred_stage1_v4<<<static_cast<int>(nb), kRedThreads, 0, st>>>(op, rows, C, chunk, part);
@@ -592,12 +533,7 @@ __device__ void bias_block_reduce(const float4& v, int C, double* part) {
 // consumer this BN is (its gradient buffer holds nothing else) -- as per-block partials part[block][2][C] (doubles; second plane 0) for
 // colred_stage2: a fixed thread -> (channel quad, row lane) map, so the sums
 // are deterministic.
-struct PlainDy {
-  const float4* p;
-  __device__ float4 operator()(int64_t i4) const { return p[i4]; }
-};
-template <class DY>
-__global__ void __launch_bounds__(kThreads, 4) bn_dx_v4(const float4* __restrict__ x, DY dy, int64_t n4, int64_t rows,
+__global__ void __launch_bounds__(kThreads, 4) bn_dx_v4(const float4* __restrict__ x, const float4* __restrict__ dy, int64_t n4, int64_t rows,
                          int C, const float* __restrict__ gamma, const float* __restrict__ beta,
                          const float* __restrict__ stats, const float* __restrict__ coef, float4* dx, int accumulate,
                          int relu, double* dbias_part) {
@@ -622,7 +558,7 @@ __global__ void __launch_bounds__(kThreads, 4) bn_dx_v4(const float4* __restrict
     for (int u = 0; u < U; ++u) {
       const int64_t i = i0 + u * L.S;
       xv[u] = i < n4 ? x[i] : zero4();
-      gv[u] = i < n4 ? dy(i) : zero4();
+      gv[u] = i < n4 ? dy[i] : zero4();
       ov[u] = (accumulate && i < n4) ? dx[i] : zero4();
     }
 #pragma unroll
@@ -1730,41 +1666,15 @@ cudaError_t bn_bwd(const float* x, const float* dy, int64_t rows, int C, const f
       double* part = dbias ? reinterpret_cast<double*>(red_scratch + static_cast<int64_t>(kRedChunks) * 2 * C * 2 +
                                                        ((2 * C + 63) / 64) * 64)
                            : nullptr;
-      bn_dx_v4<<<nb, kThreads, 0, st>>>(reinterpret_cast<const float4*>(x),
-                                        PlainDy{reinterpret_cast<const float4*>(dy)}, n / 4, rows, C, gamma, beta,
-                                        stats, coef, reinterpret_cast<float4*>(dx), accumulate, relu, part);
+      bn_dx_v4<<<nb, kThreads, 0, st>>>(reinterpret_cast<const float4*>(x), reinterpret_cast<const float4*>(dy),
+                                        n / 4, rows, C, gamma, beta, stats, coef, reinterpret_cast<float4*>(dx),
+                                        accumulate, relu, part);
       if (dbias) colred_stage2<<<stage2_blocks(C), kStage2Threads, 0, st>>>(part, nb, C, BiasFin{dbias});
     } else {
       bn_dx_scalar<<<blocks_for(n), kThreads, 0, st>>>(x, dy, n, rows, C, gamma, beta, stats, coef, dx, accumulate,
                                                        relu);
     }
   }
-  return cudaGetLastError();
-}
-
-bool pool_bn_bwd_ok(const PoolShape& ps, int bn_C) {
-  return pool_bwd_argmax_only(ps) && ps.C == bn_C && ps.C % 4 == 0;
-}
-
-cudaError_t bn_bwd_pool(const PoolShape& ps, const uint8_t* argmax, const float* dy_pool, const float* x, int64_t rows,
-                        int C, const float* gamma, const float* beta, const float* stats, int relu, float* dx,
-                        int accumulate, float* dgamma, float* dbeta, float* red_scratch, cudaStream_t st,
-                        float* dbias) {
-  if (!pool_bn_bwd_ok(ps, C) || !argmax || rows != static_cast<int64_t>(ps.N) * ps.H * ps.W) return cudaErrorInvalidValue;
-  if (dbias && (!dx || !bn_bwd_bias_ok(C))) return cudaErrorInvalidValue;
-  const PoolGatherDy g{ps, reinterpret_cast<const uchar4*>(argmax), reinterpret_cast<const float4*>(dy_pool)};
-  float* coef = red_scratch + static_cast<int64_t>(kRedChunks) * 2 * C * 2;
-  cudaError_t e = colred(RedBnBwdPoolOp{x, g, stats, gamma, beta, relu}, BnBwdFin{C, dgamma, dbeta, coef}, rows, C,
-                         red_scratch, st);
-  if (e != cudaSuccess || !dx) return e;
-  const int64_t n = rows * C;
-  const int nb = elt_blocks(n / 4, C / 4);
-  double* part = dbias ? reinterpret_cast<double*>(red_scratch + static_cast<int64_t>(kRedChunks) * 2 * C * 2 +
-                                                   ((2 * C + 63) / 64) * 64)
-                       : nullptr;
-  bn_dx_v4<<<nb, kThreads, 0, st>>>(reinterpret_cast<const float4*>(x), g, n / 4, rows, C, gamma, beta, stats, coef,
-                                    reinterpret_cast<float4*>(dx), accumulate, relu, part);
-  if (dbias) colred_stage2<<<stage2_blocks(C), kStage2Threads, 0, st>>>(part, nb, C, BiasFin{dbias});
   return cudaGetLastError();
 }
 

@@ -552,20 +552,3 @@ def test_device_stash_parity_copies_bit_identical(cuda, alex32_case):
     _, base, _, _ = _run(net, 16, 1 << 30, ALL, params, images, labels)
     _, dev, _, t = _run(net, 16, 1 << 30, ALL, params, images, labels, elide_backups=False, stash="device")
     assert t.d2h_bytes == 10822272 and _bitwise(dev, base)
-
-
-def test_pool_bn_backward_fusion_is_bit_identical(cuda, monkeypatch):
-    """The stem's max-pool backward folded into the BN backward that follows
-    (dy gathered from the pooled gradient and the argmax in both BN passes,
-    never written) equals pool_bwd + bn_bwd bit for bit, in the production
-    configuration (every other fusion on), and saves the pool kernel."""
-    from paper_1801_04380_b200.netgen import gen_resnet
-    from paper_1801_04380_b200.training import init_parameters
-    net = gen_resnet(3, 4, 6, 3)
-    params = init_parameters(net, seed=2, head_scale=0.1)
-    images, labels = _inputs(net, 8)
-    loss, grads, _, t = _run(net, 8, 4 << 30, ALL, params, images, labels)
-    monkeypatch.setenv("SN_FUSE_POOL_BN", "0")
-    loss0, grads0, _, t0 = _run(net, 8, 4 << 30, ALL, params, images, labels)
-    assert t.kernels == t0.kernels - 1
-    assert loss == loss0 and _bitwise(grads, grads0)
