@@ -224,7 +224,9 @@ typedef struct sn_exec_options {
                              1 device memory of stash_device (an NVLink peer's spare HBM;
                              the executor's own device = same-device loopback) */
   int32_t stash_device;
-  int32_t reserved_;
+  int32_t autotune;       /* 1: benchmark the CONV kernel variants per layer shape at create time
+                             and run the fastest (non-parity mode: summation orders differ);
+                             sn_exec_catalog reports the measurements */
   /* Data-parallel replica; dp_comm NULL = single replica.  The
    * weight gradients are summed over the dp_world ranks by ncclAllReduce in
    * buckets of about dp_bucket_bytes, each issued on a communication stream
@@ -329,6 +331,18 @@ int sn_exec_memory(const sn_exec* ex, sn_exec_mem* out);
  * (high_water_bytes) and the bytes of all written blocks. */
 int sn_exec_arena_fill(sn_exec* ex);
 int sn_exec_arena_scan(sn_exec* ex, int64_t* high_water_bytes, int64_t* touched_bytes);
+/* The measured CONV kernel-variant catalog (autotune): one entry per (layer
+ * shape, op, variant): the representative layer, op 0 forward / 1 dgrad /
+ * 2 wgrad, the dispatch knobs (halo 0 off / 1 by shape, pairs 0 off / 1 by
+ * size, bn 0 policy / forced im2col tile width, subpix 0 off / 1 on), the
+ * median event time in microseconds, and whether it was chosen. */
+typedef struct sn_catalog_entry {
+  int32_t layer, op;
+  int32_t halo, pairs, bn, subpix;
+  float us;
+  int32_t chosen;
+} sn_catalog_entry;
+int sn_exec_catalog(const sn_exec* ex, sn_catalog_entry* out, size_t cap, size_t* n);
 /* Stream the executor launches on (for cross-library ordering). */
 void* sn_exec_stream(sn_exec* ex);
 

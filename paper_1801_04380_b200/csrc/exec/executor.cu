@@ -68,6 +68,9 @@ struct LayerRt {
   sn::ConvShape conv{};
   sn::PoolShape pool{};
   int fc_in = 0, fc_splits = 1, wgrad_splits = 1;
+  // CONV kernel variants (forward, dgrad, wgrad): the process defaults, or the
+  // fastest measured one when the executor benchmarks them (opt.autotune)
+  sn::ConvKnobs kf{}, kd{}, kw{};
   int stats_tiles = 0, stats_rows = 0;  // CONV: BN statistics tiles its forward can emit
   uint8_t* argmax = nullptr;            // max POOL: per-output window argmax saved by the forward
 };
@@ -148,6 +151,15 @@ struct sn_exec {
   // an action's kernels and nothing overlaps
   bool serial = false;
   int32_t* marker = nullptr;  // census: per-action memset marker target
+  // measured CONV kernel-variant catalog (opt.autotune): every variant timed per
+  // layer shape and op, the fastest applied
+  struct CatEntry {
+    int layer, op;  // representative layer of the shape; 0 fwd, 1 dgrad, 2 wgrad
+    sn::ConvKnobs k;
+    float us;
+    int chosen;
+  };
+  std::vector<CatEntry> catalog;
   // data-parallel replica: buckets of the weight-gradient all-reduce, issued on
   // s5 after the backward steps of their layers
   struct Bucket {
@@ -295,6 +307,8 @@ void setup_layers(sn_exec* ex, const sn_layer_numerics* numerics) {
   }
   ex->n_params = std::max<int64_t>(poff, kAlignFloats);
   ex->n_state = std::max<int64_t>(soff, kAlignFloats);
+  const sn::ConvKnobs defaults = sn::conv_knobs();
+  for (LayerRt& l : ex->L) l.kf = l.kd = l.kw = defaults;
   // A lone CONV on a 4-channel DATA layer reads a spatially padded copy of the
   // images through the sliding-window TMA stem kernels (conv_tma.cu).
   if (ex->data_id >= 0 && net.next[ex->data_id].size() == 1) {
@@ -302,6 +316,123 @@ void setup_layers(sn_exec* ex, const sn_layer_numerics* numerics) {
     if (ex->L[c].kind == snp::CONV && ex->L[ex->data_id].C == 4 && sn::use_tma() && sn::conv_stem_ok(ex->L[c].conv))
       ex->stem_layer = c;
   }
+}
+
+// Measured kernel-variant catalog (the reference's convselect benchmarks the
+// memory-feasible algorithms; here the algorithms are this
+// executor's kernel variants): for every distinct CONV shape and op, time each
+// variant of the dispatch knobs on scratch buffers (1 warm-up + median of 3,
+// CUDA events) and give the layers of that shape the fastest.  Weight-gradient
+// variants whose split-K partials exceed the 64 Mi-float scratch cap are not
+// memory-feasible and are skipped.  Summation orders differ between
+// variants, so this is a non-parity mode (off by default).
+void autotune(sn_exec* ex) {
+  const Net& net = ex->plan->plan.net;
+  std::map<std::vector<int>, std::vector<int>> shapes;  // shape key -> CONV layers
+  for (int i = 0; i < net.n; ++i) {
+    const LayerRt& l = ex->L[i];
+    if (l.kind != snp::CONV || i == ex->stem_layer) continue;
+    const sn::ConvShape& c = l.conv;
+    const bool dgrad = net.kind[net.prev[i][0]] != snp::DATA;
+    shapes[{c.N, c.H, c.W, c.C, c.K, c.R, c.S, c.P, c.Q, c.stride, c.pad, dgrad ? 1 : 0}].push_back(i);
+  }
+  if (shapes.empty()) return;
+  int64_t nx = 64, nw = 64, ny = 64, nwt = 64, nred = 64;
+  const int64_t cap = 64ll << 20;
+  for (const auto& kv : shapes) {
+    const sn::ConvShape& c = ex->L[kv.second[0]].conv;
+    nx = std::max<int64_t>(nx, static_cast<int64_t>(c.N) * c.H * c.W * c.C);
+    ny = std::max<int64_t>(ny, static_cast<int64_t>(c.N) * c.P * c.Q * c.K);
+    nw = std::max<int64_t>(nw, static_cast<int64_t>(c.K) * c.R * c.S * c.C);
+    nwt = std::max<int64_t>(nwt, std::max<int64_t>(nw, sn::conv_dgrad_scratch_floats(c)));
+    nred = std::max<int64_t>(nred, sn::red_scratch_floats(std::max(c.C, c.K)));
+  }
+  std::vector<void*> bufs;
+  auto dal = [&](int64_t floats) {
+    void* p = nullptr;
+    ck(cudaMalloc(&p, static_cast<size_t>(floats) * 4), "cudaMalloc(autotune)");
+    ck(cudaMemset(p, 0, static_cast<size_t>(floats) * 4), "memset(autotune)");
+    bufs.push_back(p);
+    return static_cast<float*>(p);
+  };
+  struct Free {
+    std::vector<void*>* b;
+    ~Free() {
+      for (void* p : *b) cudaFree(p);
+    }
+  } free_bufs{&bufs};
+  float *x = dal(nx), *y = dal(ny), *dy = dal(ny), *dx = dal(nx), *w = dal(nw), *bias = dal(4096), *dw = dal(nw);
+  float *wt = dal(nwt), *red = dal(nred), *part = dal(cap);
+  cudaEvent_t e0, e1;
+  ck(cudaEventCreate(&e0), "event");
+  ck(cudaEventCreate(&e1), "event");
+  cudaStream_t st = ex->s0;
+  auto time_us = [&](const std::function<cudaError_t()>& f) -> float {
+    ck(f(), "autotune warm-up");
+    float t[3];
+    for (int r = 0; r < 3; ++r) {
+      ck(cudaEventRecord(e0, st), "record");
+      ck(f(), "autotune launch");
+      ck(cudaEventRecord(e1, st), "record");
+      ck(cudaEventSynchronize(e1), "sync");
+      ck(cudaEventElapsedTime(&t[r], e0, e1), "elapsed");
+    }
+    std::sort(t, t + 3);
+    return t[1] * 1000.f;
+  };
+  const sn::ConvKnobs base = sn::conv_knobs();
+  auto with = [&](int halo, int pairs, int bn, int subpix) {
+    sn::ConvKnobs k = base;
+    if (halo >= 0) k.halo = halo;
+    if (pairs >= 0) k.pairs = pairs;
+    if (bn >= 0) k.bn = bn;
+    if (subpix >= 0) k.subpix = subpix;
+    return k;
+  };
+  const std::vector<sn::ConvKnobs> fwd_v = {base, with(0, -1, -1, -1), with(-1, 0, -1, -1), with(0, 0, -1, -1),
+                                           with(0, -1, 128, -1), with(0, -1, 64, -1)};
+  const std::vector<sn::ConvKnobs> dgrad_v = {base, with(0, -1, -1, -1), with(-1, 0, -1, -1), with(-1, -1, -1, 0),
+                                             with(0, 0, -1, -1)};
+  const std::vector<sn::ConvKnobs> wgrad_v = {base, with(0, -1, -1, -1), with(-1, 0, -1, -1), with(0, 0, -1, -1)};
+  for (const auto& kv : shapes) {
+    const int rep = kv.second[0];
+    const sn::ConvShape cs = ex->L[rep].conv;
+    const bool has_dgrad = kv.first.back() != 0;
+    for (int op = 0; op < 3; ++op) {
+      if (op == 1 && !has_dgrad) continue;
+      const auto& vs = op == 0 ? fwd_v : (op == 1 ? dgrad_v : wgrad_v);
+      float best = 0.f;
+      sn::ConvKnobs pick = base;
+      const size_t first = ex->catalog.size();
+      std::vector<sn::ConvKnobs> seen;
+      for (const sn::ConvKnobs& k : vs) {
+        if (std::find(seen.begin(), seen.end(), k) != seen.end()) continue;
+        seen.push_back(k);
+        sn::KnobScope ks(k);
+        float us = 0.f;
+        if (op == 0) {
+          us = time_us([&] { return sn::conv_fwd(cs, x, w, bias, y, st, nullptr); });
+        } else if (op == 1) {
+          if (sn::conv_dgrad_scratch_floats(cs) > nwt) continue;
+          us = time_us([&] { return sn::conv_dgrad(cs, dy, w, wt, dx, 0, st); });
+        } else {
+          const int sp = sn::conv_wgrad_splits(cs, cap);
+          if (static_cast<int64_t>(sp) * cs.R * cs.S * cs.C * cs.K > cap) continue;  // not memory-feasible
+          us = time_us([&] { return sn::conv_wgrad(cs, x, dy, dw, nullptr, part, sp, red, st); });
+        }
+        ex->catalog.push_back({rep, op, k, us, 0});
+        if (ex->catalog.size() == first + 1 || us < best) {
+          best = us;
+          pick = k;
+        }
+      }
+      for (size_t j = first; j < ex->catalog.size(); ++j) ex->catalog[j].chosen = ex->catalog[j].k == pick;
+      for (int lid : kv.second) (op == 0 ? ex->L[lid].kf : (op == 1 ? ex->L[lid].kd : ex->L[lid].kw)) = pick;
+    }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  ck(cudaDeviceSynchronize(), "autotune");
 }
 
 // Buckets in backward (issue) order: a bucket is a contiguous float range of
@@ -387,7 +518,10 @@ void alloc_device(sn_exec* ex) {
     }
     if (l.kind == snp::BN || l.kind == snp::CONV || l.kind == snp::FC)
       red = std::max(red, sn::red_scratch_floats(l.C));
-    if (l.kind == snp::CONV) wt = std::max(wt, std::max<int64_t>(l.w_n, sn::conv_dgrad_scratch_floats(l.conv)));
+    if (l.kind == snp::CONV) {
+      sn::KnobScope ks(l.kd);
+      wt = std::max(wt, std::max<int64_t>(l.w_n, sn::conv_dgrad_scratch_floats(l.conv)));
+    }
     if (l.kind == snp::FC) wt = std::max(wt, l.w_n);  // fc_dgrad's transposed weights
   }
   ck(cudaMemcpy(ex->state, st.data(), st.size() * sizeof(float), cudaMemcpyHostToDevice), "memcpy(state)");
@@ -402,6 +536,7 @@ void alloc_device(sn_exec* ex) {
   for (int i = 0; i < net.n; ++i) {
     LayerRt& l = ex->L[i];
     if (l.kind == snp::CONV) {
+      sn::KnobScope ks(l.kw);
       l.wgrad_splits = sn::conv_wgrad_splits(l.conv, cap);
     } else if (l.kind == snp::FC) {
       l.fc_splits = sn::fc_splits(ex->B, l.fc_in, l.C, cap);
@@ -415,6 +550,7 @@ void alloc_device(sn_exec* ex) {
   for (int i = 0; i < net.n; ++i) {
     LayerRt& l = ex->L[i];
     if (l.kind != snp::CONV) continue;
+    sn::KnobScope ks(l.kf);
     l.stats_tiles = sn::conv_fwd_stats_tiles(l.conv, i == ex->stem_layer, &l.stats_rows);
     tstats = std::max(tstats, static_cast<int64_t>(l.stats_tiles) * 4 * l.C);
   }
@@ -680,7 +816,11 @@ struct Compiler {
           push([=] { ck(sn::conv_stem_fwd(cs, x, w, wp, b, y, ts, st), "conv_stem_fwd"); }, 2);
           break;
         }
-        push([=] { ck(sn::conv_fwd(cs, x, w, b, y, st, ts), "conv_fwd"); }, 1);
+        const sn::ConvKnobs kf = l.kf;
+        push([=] {
+          sn::KnobScope ks(kf);
+          ck(sn::conv_fwd(cs, x, w, b, y, st, ts), "conv_fwd");
+        }, 1);
         break;
       }
       case snp::FC: {
@@ -895,15 +1035,29 @@ struct Compiler {
           }, 3 + nbias);
           break;
         }
-        const int ndgrad = !dx ? 0 : sn::conv_dgrad_launches(cs);
-        const int nwgrad = sn::conv_wgrad_launches(cs, sp, db != nullptr);
+        const sn::ConvKnobs kd = l.kd, kw = l.kw;
+        int ndgrad = 0, nwgrad = 0;
+        {
+          sn::KnobScope ks(kd);
+          ndgrad = !dx ? 0 : sn::conv_dgrad_launches(cs);
+        }
+        {
+          sn::KnobScope ks(kw);
+          nwgrad = sn::conv_wgrad_launches(cs, sp, db != nullptr);
+        }
         push([=] {
           const cudaStream_t sw = e->serial ? st : s3;
           ck(cudaEventRecord(ready, st), "record");
           ck(cudaStreamWaitEvent(sw, ready, 0), "wait");
-          ck(sn::conv_wgrad(cs, x, dy, dw, db, part_w, sp, red_w, sw), "conv_wgrad");
+          {
+            sn::KnobScope ks(kw);
+            ck(sn::conv_wgrad(cs, x, dy, dw, db, part_w, sp, red_w, sw), "conv_wgrad");
+          }
           ck(cudaEventRecord(wdone, sw), "record");
-          if (dx) ck(sn::conv_dgrad(cs, dy, w, wt, dx, acc, st), "conv_dgrad");
+          if (dx) {
+            sn::KnobScope ks(kd);
+            ck(sn::conv_dgrad(cs, dy, w, wt, dx, acc, st), "conv_dgrad");
+          }
         }, nwgrad + ndgrad);
         (void)nbias;
         (void)part;
@@ -1752,6 +1906,7 @@ int sn_exec_create(const sn_plan* plan, const sn_net_desc* /*net*/, const sn_lay
     ck(cudaEventCreate(&ex->t_begin), "event");
     ck(cudaEventCreate(&ex->t_end), "event");
     setup_layers(ex, numerics);
+    if (ex->opt.autotune) autotune(ex);
     alloc_device(ex);
     if (ex->dp()) {
       if (ex->opt.dp_world < 1 || ex->opt.dp_rank < 0 || ex->opt.dp_rank >= ex->opt.dp_world)
@@ -2146,6 +2301,18 @@ int sn_dp_buckets(const sn_plan* plan, int64_t bucket_bytes, int64_t* lo, int64_
       if (after_layer) after_layer[i] = tmp.buckets[i].after_layer;
     }
   });
+}
+
+int sn_exec_catalog(const sn_exec* ex, sn_catalog_entry* out, size_t cap, size_t* n) {
+  if (!ex || !n) return xset(SN_EK_INTERNAL, "null argument");
+  *n = ex->catalog.size();
+  if (!out) return SN_OK;
+  if (cap < ex->catalog.size()) return xset(SN_EK_INTERNAL, "output buffer too small");
+  for (size_t i = 0; i < ex->catalog.size(); ++i) {
+    const auto& c = ex->catalog[i];
+    out[i] = sn_catalog_entry{c.layer, c.op, c.k.halo, c.k.pairs, c.k.bn, c.k.subpix, c.us, c.chosen};
+  }
+  return SN_OK;
 }
 
 int sn_exec_workspace_use(const sn_exec* ex, int32_t* wgrad_in_pool, int32_t* wgrad_outside) {

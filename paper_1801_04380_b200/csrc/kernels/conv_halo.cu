@@ -453,6 +453,8 @@ int halo_mode() {
   return g_halo;
 }
 
+int conv_halo_mode() { return halo_mode(); }
+
 int conv_halo_variant(int N, int H, int W, int C, int K, int R, int S, int pad, int P, int Q) {
   if (halo_mode() == 0 || C % 32 != 0 || K % 32 != 0 || R * S <= 1 || !tma_encoders_ok()) return 0;
   if (P != H + 2 * pad - R + 1 || Q != W + 2 * pad - S + 1 || pad < 0) return 0;

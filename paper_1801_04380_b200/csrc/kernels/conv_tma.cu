@@ -734,6 +734,7 @@ TileCfg tile_cfg(int64_t M, int n) {
 
 void set_conv_pairs(int mode) { g_pairs = mode; }
 void set_conv_bn(int bn) { g_bn_force = bn; }
+int conv_bn_force() { return g_bn_force; }
 int conv_pairs_mode() { return pairs_mode(); }
 
 int conv_fwd_stats_tiles(const ConvShape& s, bool stem, int* tile_rows) {

@@ -479,6 +479,15 @@ bool use_subpix(const ConvShape& s) { return g_subpix && use_tma() && conv_dgrad
 }  // namespace
 
 void set_conv_subpix(int on) { g_subpix = on; }
+int conv_subpix_mode() { return g_subpix; }
+
+ConvKnobs conv_knobs() { return ConvKnobs{conv_halo_mode(), conv_pairs_mode(), conv_bn_force(), conv_subpix_mode()}; }
+void set_conv_knobs(const ConvKnobs& k) {
+  set_conv_halo(k.halo);
+  set_conv_pairs(k.pairs);
+  set_conv_bn(k.bn);
+  set_conv_subpix(k.subpix);
+}
 
 int conv_dgrad_launches(const ConvShape& s) {
   if (use_subpix(s)) return 2;

@@ -113,6 +113,24 @@ void set_conv_pairs(int mode);
 void set_conv_bn(int bn);  // im2col conv tile width override (0 = policy), for A/B timing
 int conv_pairs_mode();
 bool use_tma();
+int conv_halo_mode();
+int conv_bn_force();
+int conv_subpix_mode();
+// The kernel-variant knobs of the CONV dispatch above, as one value (read at
+// launch; the executor applies a layer's measured choice around its launches).
+struct ConvKnobs {
+  int halo, pairs, bn, subpix;  // set_conv_halo / set_conv_pairs / set_conv_bn / set_conv_subpix
+  bool operator==(const ConvKnobs& o) const {
+    return halo == o.halo && pairs == o.pairs && bn == o.bn && subpix == o.subpix;
+  }
+};
+ConvKnobs conv_knobs();
+void set_conv_knobs(const ConvKnobs& k);
+struct KnobScope {
+  ConvKnobs saved;
+  explicit KnobScope(const ConvKnobs& k) : saved(conv_knobs()) { set_conv_knobs(k); }
+  ~KnobScope() { set_conv_knobs(saved); }
+};
 
 // FC: x[B][I], w[O][I], y[B][O]
 int fc_splits(int B, int I, int O, int64_t partial_floats_cap);

@@ -47,7 +47,7 @@ class ExecOptionsC(C.Structure):
     _fields_ = [("device", C.c_int32), ("elide_backups", C.c_int32), ("use_graph", C.c_int32),
                 ("num_classes", C.c_int32), ("seed", C.c_uint64), ("lr", C.c_float),
                 ("grad_scale", C.c_float), ("precision", C.c_int32), ("stash", C.c_int32),
-                ("stash_device", C.c_int32), ("reserved_", C.c_int32), ("dp_comm", C.c_void_p),
+                ("stash_device", C.c_int32), ("autotune", C.c_int32), ("dp_comm", C.c_void_p),
                 ("dp_world", C.c_int32), ("dp_rank", C.c_int32), ("dp_bucket_bytes", C.c_int64)]
 
 
@@ -60,6 +60,11 @@ class ExecMemC(C.Structure):
         "other_scratch_bytes", "host_stash_bytes", "device_stash_bytes", "peer_stash_bytes", "device_total_bytes",
         "wgrad_partials_outside_pool_bytes",
         "planned_arena_high_water")]
+
+
+class CatalogC(C.Structure):
+    _fields_ = [("layer", C.c_int32), ("op", C.c_int32), ("halo", C.c_int32), ("pairs", C.c_int32),
+                ("bn", C.c_int32), ("subpix", C.c_int32), ("us", C.c_float), ("chosen", C.c_int32)]
 
 
 class TimingC(C.Structure):
@@ -176,6 +181,7 @@ def _xlib():
         L.sn_exec_memory.argtypes = [C.c_void_p, P(ExecMemC)]
         L.sn_exec_arena_fill.argtypes = [C.c_void_p]
         L.sn_exec_arena_scan.argtypes = [C.c_void_p, P(C.c_int64), P(C.c_int64)]
+        L.sn_exec_catalog.argtypes = [C.c_void_p, P(CatalogC), C.c_size_t, P(C.c_size_t)]
         L.sn_exec_stream.argtypes = [C.c_void_p]
         L.sn_exec_stream.restype = C.c_void_p
         L._sn_configured = True
@@ -195,7 +201,7 @@ class Executor:
                  dropout_seed: int = 1234, lr: float = 0.01, grad_scale: float = 1.0,
                  elide_backups: bool = True, use_graph: bool = True, params: dict | None = None,
                  precision: str = "tf32", dp=None, dp_bucket_bytes: int = 0, stash: str = "host",
-                 stash_device: int | None = None) -> None:
+                 stash_device: int | None = None, autotune: bool = False) -> None:
         import torch
         if not torch.cuda.is_available():
             raise DeviceError("run_training needs a CUDA device (B200); there is no CPU fallback")
@@ -228,7 +234,7 @@ class Executor:
             raise MemschedError(f"stash must be 'host' or 'device', got {stash!r}")
         opts = ExecOptionsC(device, int(elide_backups), int(use_graph), 0, dropout_seed, lr, grad_scale,
                             PRECISIONS[precision], int(stash == "device"),
-                            device if stash_device is None else stash_device, 0, comm,
+                            device if stash_device is None else stash_device, int(autotune), comm,
                             self.dp.world if self.dp else 1, self.dp.rank if self.dp else 0, dp_bucket_bytes)
         self.ptr = C.c_void_p()
         torch.cuda.set_device(device)
@@ -419,6 +425,20 @@ class Executor:
         if self.L.sn_exec_arena_scan(self.ptr, C.byref(hw), C.byref(touched)) != 0:
             _raise_exec(self.L)
         return {"measured_arena_written_bytes": touched.value, "measured_arena_highest_written_byte": hw.value}
+
+    def catalog(self) -> list[dict]:
+        """The measured CONV kernel-variant catalog (``autotune=True``): every
+        variant timed per layer shape and op, and which one the layers of that
+        shape run (empty without autotune)."""
+        n = C.c_size_t()
+        self.L.sn_exec_catalog(self.ptr, None, 0, C.byref(n))
+        buf = (CatalogC * max(1, n.value))()
+        if self.L.sn_exec_catalog(self.ptr, buf, n.value, C.byref(n)) != 0:
+            _raise_exec(self.L)
+        ops = ("fwd", "dgrad", "wgrad")
+        return [{"layer": self.net.layers[e.layer].name, "op": ops[e.op],
+                 "variant": {"halo": e.halo, "pairs": e.pairs, "bn": e.bn, "subpix": e.subpix},
+                 "us": round(e.us, 2), "chosen": bool(e.chosen)} for e in buf[:n.value]]
 
     def census(self) -> list[list[str]]:
         """Per tape action (the same list ``profile`` times), the mangled names

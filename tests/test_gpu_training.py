@@ -552,3 +552,43 @@ def test_device_stash_parity_copies_bit_identical(cuda, alex32_case):
     _, base, _, _ = _run(net, 16, 1 << 30, ALL, params, images, labels)
     _, dev, _, t = _run(net, 16, 1 << 30, ALL, params, images, labels, elide_backups=False, stash="device")
     assert t.d2h_bytes == 10822272 and _bitwise(dev, base)
+
+
+# ---- measured kernel-variant catalog (non-parity mode) ----------------------
+
+def test_autotune_catalog_measures_and_trains(cuda):
+    """autotune=True benchmarks every CONV kernel variant per layer shape and op
+    at create time and runs the fastest (a non-parity mode: summation orders
+    differ from the default variants).  The catalog covers every distinct
+    shape x op with exactly one chosen variant, the chosen one is the fastest
+    measured, and the step still matches the CPU oracle at the tf32
+    tolerance."""
+    from oracle.numerics import forward_backward, relative_error
+    from paper_1801_04380_b200.netgen import gen_resnet
+    from paper_1801_04380_b200.training import init_parameters
+    net = gen_resnet(1, 1, 2, 1)
+    params = init_parameters(net, seed=6, head_scale=0.1)
+    images, labels = _inputs(net, 8, seed=3)
+    sn = _sn()
+    from paper_1801_04380_b200.training import Executor
+    cfg = sn.SimConfig(pool_bytes=4 << 30, features=sn.parse_features(ALL), cost=sn.CostConfig(batch=8))
+    ex = Executor(net, cfg, params=params, autotune=True)
+    cat = ex.catalog()
+    ex.set_inputs(images, labels)
+    loss, _ = ex.step(update=False)
+    grads = ex.get("grads")
+    ex.close()
+    assert cat and all(c["us"] > 0 for c in cat)
+    groups = {}
+    for c in cat:
+        groups.setdefault((c["layer"], c["op"]), []).append(c)
+    assert {op for _, op in groups} == {"fwd", "dgrad", "wgrad"}
+    for g in groups.values():
+        assert sum(c["chosen"] for c in g) == 1
+        assert min(g, key=lambda c: c["us"])["chosen"]
+    ref_loss, ref = forward_backward(net, params, images, labels)
+    _, emu = forward_backward(net, params, images, labels, tf32=True)
+    sens = max(relative_error(emu[l][k], ref[l][k]) for l in ref for k in ("w", "b"))
+    worst = max(relative_error(grads[l][k], ref[l][k]) for l in ref for k in ("w", "b"))
+    assert abs(loss - ref_loss) <= 5e-3 * abs(ref_loss)
+    assert worst <= 3 * sens + 5e-3, (worst, sens)
