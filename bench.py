@@ -59,6 +59,9 @@ def parse_args():
     ap.add_argument("--features", default=ALL)
     ap.add_argument("--stash", default="host", choices=["host", "device"],
                     help="UTP copy-out store: pinned host memory (PCIe) or device HBM (peer / loopback)")
+    ap.add_argument("--autotune", action="store_true",
+                    help="benchmark the CONV kernel variants per layer shape at create time and run the fastest "
+                         "(measured catalog, non-parity mode)")
     ap.add_argument("--precision", default="tf32", choices=["tf32", "fp32"],
                     help="CONV/FC math: tf32 tensor cores (headline) or the fp32-faithful 3xTF32 mode")
     ap.add_argument("--no-extras", action="store_true", help="skip the unconstrained / profile / baseline legs")
@@ -252,7 +255,7 @@ def run_ours(args) -> None:
     free0 = torch.cuda.mem_get_info(local)[0]
     # weight-gradient all-reduce: NCCL buckets inside the executor's step (dp=ctx)
     ex = Executor(net, cfg, device=local, seed=2, lr=0.01, precision=args.precision, dp=ctx if world > 1 else None,
-                  stash=args.stash)
+                  stash=args.stash, autotune=args.autotune)
     free1 = torch.cuda.mem_get_info(local)[0]
     rep = ex.report
     c, h, w = sn.propagate_shapes(net)[net.data_id]
@@ -374,6 +377,10 @@ def run_ours(args) -> None:
                    "conv_wgrad_partials_in_planned_workspace": "%d of %d" % (
                        ex.workspace_use()[0], sum(ex.workspace_use()))},
         "clocks": clocks.summary(),
+        **({"autotune_catalog": {"entries": len(ex.catalog()),
+                                 "changed_from_default": [f"{c['layer']}:{c['op']}:{c['variant']}" for c in ex.catalog()
+                                                          if c["chosen"] and c["variant"] != ex.catalog()[0]["variant"]]}}
+           if args.autotune else {}),
         "losses": [round(l, 5) for l in losses[:3]] + [round(losses[-1], 5)],
     }
     if not args.no_extras and rank == 0:
