@@ -106,6 +106,9 @@ struct sn_exec {
   int data_id = -1;
   int stem_layer = -1;        // CONV reading a spatially padded C=4 copy of the images (TMA stem path)
   std::vector<char> elided;   // per layer: output fused away (never written)
+  std::vector<int> eff_owner;  // per layer: the buffer holding its output gradient (see setup_layers)
+  std::vector<char> side_root;
+  std::unordered_map<int, float*> side;  // side root -> its output-gradient buffer (outside the pool)
   int32_t* labels = nullptr;
   float* loss_rows = nullptr;
   float* loss = nullptr;
@@ -257,15 +260,36 @@ void setup_layers(sn_exec* ex, const sn_layer_numerics* numerics) {
     if (static_cast<int64_t>(ex->B) * l.per_sample >= (1ll << 31))
       xfail(SN_EK_UNSUPPORTED, "tensor of layer '" + net.names[i] + "' exceeds 2^31 elements");
   }
+  // Gradient buffers.  The reference aliases an ACT / DROPOUT gradient with
+  // its producer's (GRAD_INPLACE_KINDS, costmodel.py:207-221).  When that
+  // producer forks, its other consumers' gradients would mix with the in-place
+  // layer's own incoming gradient in the one buffer; the first in-place layer
+  // after such a fork (a "side root") gets its own output-gradient buffer
+  // outside the pool, and its backward adds its masked gradient into the
+  // producer's.  eff_owner[i]: the buffer holding d(output of i) -- a pool
+  // gradient key, a side root's id, or -1 (no gradient).
+  ex->eff_owner.assign(n, -2);
+  ex->side_root.assign(n, 0);
+  std::function<int(int)> eo = [&](int i) -> int {
+    if (ex->eff_owner[i] != -2) return ex->eff_owner[i];
+    int r;
+    if (snp::is_inplace(net.kind[i])) {
+      const int p = net.prev[i][0];
+      if (net.next[p].size() != 1 && net.grad_owner(p) >= 0) {
+        ex->side_root[i] = 1;
+        r = i;
+      } else {
+        r = eo(p);
+      }
+    } else {
+      r = net.grad_owner(i);
+    }
+    return ex->eff_owner[i] = r;
+  };
+  for (int i = 0; i < n; ++i) eo(i);
   for (int i = 0; i < n; ++i) {
     LayerRt& l = ex->L[i];
     const int k = l.kind;
-    if (snp::is_inplace(k)) {
-      const int p = net.prev[i][0];
-      if (net.next[p].size() != 1)
-        xfail(SN_EK_UNSUPPORTED, "in-place gradient of '" + net.names[i] + "' aliases a fork at '" + net.names[p] +
-                                     "' (other consumers' gradients would be overwritten)");
-    }
     if (k == snp::SOFTMAX && i != ex->terminal)
       xfail(SN_EK_UNSUPPORTED, "SOFTMAX is only supported as the terminal layer");
     if (k == snp::CONV || k == snp::POOL) {
@@ -591,6 +615,12 @@ void alloc_device(sn_exec* ex) {
   ex->dmalloc(&ex->loss_rows, ex->B * 4, sn_exec::M_OTHER, "cudaMalloc(loss_rows)");
   ex->dmalloc(&ex->loss, 16, sn_exec::M_OTHER, "cudaMalloc(loss)");
   ex->dmalloc(&ex->iteration, 16, sn_exec::M_OTHER, "cudaMalloc(iteration)");
+  for (int i = 0; i < net.n; ++i)
+    if (ex->side_root[i]) {
+      float* p = nullptr;
+      ex->dmalloc(&p, static_cast<int64_t>(ex->B) * ex->L[i].per_sample * 4, sn_exec::M_OTHER, "cudaMalloc(fork grad)");
+      ex->side[i] = p;
+    }
   ck(cudaMemset(ex->iteration, 0, sizeof(uint32_t) * 4), "memset(iteration)");
 }
 
@@ -956,10 +986,13 @@ struct Compiler {
   }
 
   // Destination for d(input pid) and whether it is the first write.
+  // the buffer of gradient owner `owner` (eff_owner numbering)
+  float* grad_ptr(int owner) { return ex->side_root[owner] ? ex->side.at(owner) : ptr(snp::K_GRAD, owner); }
+
   float* dx_target(int pid, int* accumulate) {
-    const int owner = net.grad_owner(pid);
+    const int owner = ex->eff_owner[pid];
     if (owner < 0) return nullptr;
-    float* p = ptr(snp::K_GRAD, owner);
+    float* p = grad_ptr(owner);
     auto it = fresh.find(owner);
     *accumulate = (it != fresh.end() && it->second) ? 0 : 1;
     fresh[owner] = false;
@@ -972,8 +1005,8 @@ struct Compiler {
     cudaStream_t st = ex->s0;
     sn_exec* e = ex;
     const int64_t n = static_cast<int64_t>(ex->B) * l.per_sample;
-    const int owner = net.grad_owner(lid);
-    float* dy = (owner >= 0 && lid != ex->terminal) ? ptr(snp::K_GRAD, owner) : nullptr;
+    const int owner = ex->eff_owner[lid];
+    float* dy = (owner >= 0 && lid != ex->terminal) ? grad_ptr(owner) : nullptr;
     const int pid = net.prev[lid].empty() ? -1 : net.prev[lid][0];
     switch (l.kind) {
       case snp::CONV: {
@@ -999,7 +1032,7 @@ struct Compiler {
         used_s3 = true;
         wgrad_done[lid] = wdone;
         side_reads[snp::key_code(snp::K_ACT, pid)] = wdone;
-        side_reads[snp::key_code(snp::K_GRAD, owner)] = wdone;
+        if (owner >= 0 && !ex->side_root[owner]) side_reads[snp::key_code(snp::K_GRAD, owner)] = wdone;
         // The split-K partials go to the conv workspace the planner granted this
         // step (the selected algorithm's factor x output bytes, sized from the
         // free pool) when they fit; else to the executor's scratch outside the
@@ -1120,6 +1153,14 @@ struct Compiler {
         break;
       }
       case snp::ACT: {
+        if (ex->side_root[lid]) {  // own gradient buffer: add the masked gradient into the producer's
+          const bool written = !(fresh.count(lid) && fresh[lid]);
+          int acc = 0;
+          float* g = dx_target(pid, &acc);
+          const float* y = ptr(snp::K_ACT, lid);
+          if (g && written) push([=] { ck(sn::relu_bwd_to(y, dy, g, n, acc, st), "relu_bwd_to"); }, 1);
+          break;
+        }
         int acc = 0;
         float* g = dx_target(pid, &acc);
         if (g && dy && g != dy) xfail(SN_EK_INTERNAL, "in-place gradient buffer mismatch");
@@ -1129,10 +1170,19 @@ struct Compiler {
         break;
       }
       case snp::DROPOUT: {
-        int acc = 0;
-        float* g = dx_target(pid, &acc);
         const float rate = l.num.dropout_rate;
         const uint64_t seed = ex->opt.seed;
+        if (ex->side_root[lid]) {
+          const bool written = !(fresh.count(lid) && fresh[lid]);
+          int acc = 0;
+          float* g = dx_target(pid, &acc);
+          if (g && written)
+            push([=] { ck(sn::dropout_bwd_to(dy, g, n, rate, seed, lid, e->iteration, acc, st), "dropout_bwd_to"); },
+                 1);
+          break;
+        }
+        int acc = 0;
+        float* g = dx_target(pid, &acc);
         if (g) push([=] { ck(sn::dropout_bwd_inplace(g, n, rate, seed, lid, e->iteration, st), "dropout_bwd"); }, 1);
         break;
       }
@@ -1185,7 +1235,7 @@ struct Compiler {
           break;
         }
         if (pv.size() == 2 && n % 4 == 0) {
-          const int o0 = net.grad_owner(pv[0]), o1 = net.grad_owner(pv[1]);
+          const int o0 = ex->eff_owner[pv[0]], o1 = ex->eff_owner[pv[1]];
           if (o0 >= 0 && o1 >= 0 && o0 != o1) {  // one read of dy, two destinations
             int a0 = 0, a1 = 0;
             float* d0 = dx_target(pv[0], &a0);
@@ -1196,7 +1246,7 @@ struct Compiler {
         }
         if (pv.size() > 2 && n % 4 == 0) {
           std::vector<int> owners;
-          for (int p : pv) owners.push_back(net.grad_owner(p));
+          for (int p : pv) owners.push_back(ex->eff_owner[p]);
           std::vector<int> sorted = owners;
           std::sort(sorted.begin(), sorted.end());
           if (std::adjacent_find(sorted.begin(), sorted.end()) == sorted.end()) {  // distinct buffers
@@ -1701,6 +1751,8 @@ struct Compiler {
   }
 
   void compile() {
+    for (int i = 0; i < net.n; ++i)
+      if (ex->side_root[i]) fresh[i] = true;  // side gradient buffers: the first write overwrites
     plan_fusions();
     size_wgrad_scratch();
     prepare_inputs();
@@ -1867,6 +1919,7 @@ void destroy(sn_exec* ex) {
     if (b) cudaFree(b);
   for (auto& l : ex->L)
     if (l.argmax) cudaFree(l.argmax);
+  for (auto& kv : ex->side) cudaFree(kv.second);
   if (ex->s0) cudaStreamDestroy(ex->s0);
   if (ex->s1) cudaStreamDestroy(ex->s1);
   if (ex->s2) cudaStreamDestroy(ex->s2);

@@ -194,6 +194,9 @@ cudaError_t grad_copy2(const float* src, float* d1, int acc1, float* d2, int acc
 
 cudaError_t relu_fwd(const float* x, float* y, int64_t n, cudaStream_t st);
 cudaError_t relu_bwd_inplace(const float* y, float* g, int64_t n, cudaStream_t st);
+// dx (+)= (y > 0) * dy: the backward of an ACT with its own gradient buffer
+// (its producer forks; see the executor's side roots)
+cudaError_t relu_bwd_to(const float* y, const float* dy, float* dx, int64_t n, int accumulate, cudaStream_t st);
 
 struct PoolShape {
   int N, H, W, C, P, Q, K, stride, pad, mode;  // mode 0 max, 1 avg
@@ -230,6 +233,8 @@ cudaError_t dropout_fwd(const float* x, float* y, int64_t n, float rate, uint64_
                         const uint32_t* iteration, cudaStream_t st);
 cudaError_t dropout_bwd_inplace(float* g, int64_t n, float rate, uint64_t seed, int layer,
                                 const uint32_t* iteration, cudaStream_t st);
+cudaError_t dropout_bwd_to(const float* dy, float* dx, int64_t n, float rate, uint64_t seed, int layer,
+                           const uint32_t* iteration, int accumulate, cudaStream_t st);
 
 // Softmax over F features per row + cross entropy vs labels; loss_rows[B].
 cudaError_t softmax_fwd(const float* x, float* y, int B, int F, const int32_t* labels, float* loss_rows,

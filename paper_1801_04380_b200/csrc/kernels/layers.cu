@@ -1686,6 +1686,20 @@ cudaError_t relu_fwd(const float* x, float* y, int64_t n, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+__global__ void relu_bwd_to_kernel(const float* __restrict__ y, const float* __restrict__ dy, float* dx, int64_t n,
+                                   int accumulate) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride) {
+    const float v = y[i] > 0.f ? dy[i] : 0.f;
+    dx[i] = accumulate ? dx[i] + v : v;
+  }
+}
+
+cudaError_t relu_bwd_to(const float* y, const float* dy, float* dx, int64_t n, int accumulate, cudaStream_t st) {
+  relu_bwd_to_kernel<<<blocks_for(n), kThreads, 0, st>>>(y, dy, dx, n, accumulate);
+  return cudaGetLastError();
+}
+
 cudaError_t relu_bwd_inplace(const float* y, float* g, int64_t n, cudaStream_t st) {
   const int64_t n4 = n / 4;
   if (n4) relu_bwd_kernel<<<elt_blocks(n4), kThreads, 0, st>>>(reinterpret_cast<const float4*>(y),
@@ -1851,6 +1865,23 @@ cudaError_t dropout_fwd(const float* x, float* y, int64_t n, float rate, uint64_
                         const uint32_t* iteration, cudaStream_t st) {
   dropout_fwd_kernel<<<blocks_for(n), kThreads, 0, st>>>(x, y, n, drop_thresh(rate), 1.0f / (1.0f - rate), seed, layer,
                                                          iteration);
+  return cudaGetLastError();
+}
+
+__global__ void dropout_bwd_to_kernel(const float* __restrict__ dy, float* dx, int64_t n, uint32_t thresh, float scale,
+                                      uint64_t seed, int layer, const uint32_t* iteration, int accumulate) {
+  const uint32_t it = *iteration;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride) {
+    const float v = drop_keep(seed, layer, it, static_cast<uint32_t>(i), thresh) ? dy[i] * scale : 0.f;
+    dx[i] = accumulate ? dx[i] + v : v;
+  }
+}
+
+cudaError_t dropout_bwd_to(const float* dy, float* dx, int64_t n, float rate, uint64_t seed, int layer,
+                           const uint32_t* iteration, int accumulate, cudaStream_t st) {
+  dropout_bwd_to_kernel<<<blocks_for(n), kThreads, 0, st>>>(dy, dx, n, drop_thresh(rate), 1.0f / (1.0f - rate), seed,
+                                                            layer, iteration, accumulate);
   return cudaGetLastError();
 }
 
