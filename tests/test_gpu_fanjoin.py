@@ -20,7 +20,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 ALL = "liveness,offload,cache,recompute=cost-aware,convselect"
-SEEDS = list(range(12))
+SEEDS = list(range(40))
 
 
 def _case(net, batch=4, seed=0):
