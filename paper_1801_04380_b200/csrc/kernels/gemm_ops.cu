@@ -545,18 +545,27 @@ int conv_wgrad_splits(const ConvShape& s, int64_t partial_floats_cap) {
   // left 40 of 148 SMs idle (Inception-style 384->384 wgrad, 73 % fill).
   const int64_t slots = 148 * (bn <= 128 ? 2 : 1);
   const int64_t per = RSC * s.K;
-  const int64_t smax = std::max<int64_t>(
-      1, std::min<int64_t>({16, std::max<int64_t>(1, nkb / 8), std::max<int64_t>(1, partial_floats_cap / per)}));
+  auto search = [&](int64_t limit, int64_t& want, double& best) {
+    const int64_t smax = std::max<int64_t>(
+        1, std::min<int64_t>({limit, std::max<int64_t>(1, nkb / 8), std::max<int64_t>(1, partial_floats_cap / per)}));
+    want = 1;
+    best = 0.0;
+    for (int64_t sp = 1; sp <= smax; ++sp) {
+      const int64_t items = tiles * sp, waves = (items + slots - 1) / slots;
+      const double fill = static_cast<double>(items) / static_cast<double>(waves * slots);
+      if (fill > best + 0.02) {
+        best = fill;
+        want = sp;
+      }
+    }
+  };
   int64_t want = 1;
   double best = 0.0;
-  for (int64_t sp = 1; sp <= smax; ++sp) {
-    const int64_t items = tiles * sp, waves = (items + slots - 1) / slots;
-    const double fill = static_cast<double>(items) / static_cast<double>(waves * slots);
-    if (fill > best + 0.02) {
-      best = fill;
-      want = sp;
-    }
-  }
+  search(16, want, best);
+  // few output tiles (a stride-2 3x3 wgrad of 64 -> 128 channels has 5): up to
+  // 16 splits leave most slots idle (80 of 296 CTAs, 34 % tensor pipe) -- go
+  // to 64 splits there (the partials stay a few MB)
+  if (best < 0.6) search(64, want, best);
   return effective_splits(static_cast<int>(NPQ), static_cast<int>(want));
 }
 

@@ -71,3 +71,14 @@ def _check(net):
             # 1e-5) no worse than twice the CPU fp32 oracle's own distance from fp64
             e_gpu, e_cpu = err(g32, l, k), err(ref32, l, k)
             assert e_gpu <= max(1e-4, 2 * e_cpu), (net.layers[l].name, k, e_gpu, e_cpu)
+
+
+def test_nested_fan10(cuda):
+    from paper_1801_04380_b200.cli import resolve_network
+    _check(resolve_network("nested_fan10"))
+
+
+@pytest.mark.parametrize("seed", SEEDS)
+def test_random_fanjoin(cuda, seed):
+    from paper_1801_04380_b200 import random_fanjoin
+    _check(random_fanjoin(seed))
