@@ -1059,13 +1059,23 @@ struct Compiler {
           }
         }
         if (lid == ex->stem_layer) {  // DATA has no gradient
+          const bool fused = stem_fuse_pending;
+          const sn::StemBnFuse fz = stem_fuse;
+          if (fused) {  // the BN input and dy are read on s3 after the tape frees them
+            side_reads[stem_fuse_keys[0]] = wdone;
+            side_reads[stem_fuse_keys[1]] = wdone;
+            stem_fuse_pending = false;
+          }
+          const bool rows = sn::conv_stem_wgrad_rows_ok(cs);
+          const int nk = rows ? 2 + sn::splitk_reduce_launches(148, cs.R * 32, cs.K) + (db ? 1 : 0) : 3 + nbias;
           push([=] {
             const cudaStream_t sw = e->serial ? st : s3;
             ck(cudaEventRecord(ready, st), "record");
             ck(cudaStreamWaitEvent(sw, ready, 0), "wait");
-            ck(sn::conv_stem_wgrad(cs, x, dy, part_w, wt_w, dw, db, red_w, sw), "conv_stem_wgrad");
+            ck(sn::conv_stem_wgrad(cs, x, dy, part_w, wt_w, dw, db, red_w, sw, fused ? &fz : nullptr),
+               "conv_stem_wgrad");
             ck(cudaEventRecord(wdone, sw), "record");
-          }, 3 + nbias);
+          }, nk);
           break;
         }
         const sn::ConvKnobs kd = l.kd, kw = l.kw;
@@ -1144,6 +1154,16 @@ struct Compiler {
         if (bn_bias_now && dx) {
           dcb = ex->grads + ex->L[pid].b_off;
           conv_bias_done[pid] = 1;
+        }
+        if (stem_bn_fuse_at[cur_ti] && dx && !acc) {  // dx formed inside the stem weight gradient
+          stem_fuse = sn::StemBnFuse{x, dy, stats, g, beta, sn::bn_coef_ptr(red, C), rows, relu};
+          stem_fuse_pending = true;
+          stem_fuse_keys[0] = snp::key_code(snp::K_ACT, pid);
+          stem_fuse_keys[1] = snp::key_code(snp::K_GRAD, lid);
+          push([=] {
+            ck(sn::bn_bwd(x, dy, rows, C, g, beta, stats, relu, nullptr, 0, dg, dbt, red, st), "bn_bwd_stats");
+          }, 2);
+          break;
         }
         push([=] {
           ck(sn::bn_bwd(x, dy, rows, C, g, beta, stats, relu, dx, acc, dg, dbt, red, st, dcb, cpy, cpy_acc, own),
@@ -1306,6 +1326,12 @@ struct Compiler {
   };
   std::vector<char> join_copy_own;
   std::unordered_map<int, PendingJoin> pending_join;  // keyed by BN-backward tape index
+  // stem BN backward -> stem CONV backward: the BN's dx pass runs inside the
+  // stem weight gradient (sn::StemBnFuse), dx is never written
+  std::vector<char> stem_bn_fuse_at;
+  bool stem_fuse_pending = false;
+  sn::StemBnFuse stem_fuse{};
+  int64_t stem_fuse_keys[2] = {0, 0};
   // CONV forward -> BN forward (next compute action, reading that output): the
   // CONV epilogue emits per-tile statistics, the BN only combines them.
   bool conv_stats_now = false, bn_tiles_now = false;
@@ -1344,6 +1370,7 @@ struct Compiler {
     bn_from_join.assign(T, -1);
     join_relu.assign(T, -1);
     join_copy_own.assign(T, 0);
+    stem_bn_fuse_at.assign(T, 0);
     bn_bias_at.assign(T, 0);
     conv_bias_done.assign(net.n, 0);
     const char* env = std::getenv("SN_FUSE");  // SN_FUSE=0: one kernel per layer (A/B and bitwise tests)
@@ -1376,6 +1403,8 @@ struct Compiler {
       if (e.op != 'B' || net.kind[e.b] != snp::BN || net.prev[e.b].size() != 1) continue;
       const int cv = net.prev[e.b][0];
       if (net.kind[cv] != snp::CONV || net.next[cv].size() != 1 || !sn::bn_bwd_bias_ok(ex->L[e.b].C)) continue;
+      // the stem's weight-gradient kernel sums its bias gradient itself (fused or not, same order)
+      if (cv == ex->stem_layer && sn::conv_stem_wgrad_rows_ok(ex->L[cv].conv)) continue;
       bn_bias_at[i] = 1;
     }
     for (size_t i = 0; i < T; ++i) {
@@ -1664,6 +1693,37 @@ struct Compiler {
           break;
         }
         if (f.op == 'B' && f.b != ra) break;  // another backward in between: keep it simple
+      }
+    }
+    // stem BN backward -> stem CONV backward (next compute action): the stem
+    // weight gradient reads the BN input and the BN's dy and forms dx itself,
+    // provided nothing is allocated over those two tensors' blocks before it
+    // has read them (they are freed at the end of the BN's backward step)
+    const int stem = ex->stem_layer;
+    const char* env_sb = std::getenv("SN_FUSE_STEM_BN");  // =0: materialise the stem BN's dx (A/B test)
+    for (size_t i = 0; i < T && stem >= 0 && !(env_sb && env_sb[0] == '0'); ++i) {
+      const snp::Event& e = P.tape[i];
+      if (e.op != 'B' || net.kind[e.b] != snp::BN || net.prev[e.b].size() != 1 || net.prev[e.b][0] != stem) continue;
+      const int bn = e.b;
+      if (net.next[stem].size() != 1 || bn_from_join[i] >= 0 || !sn::conv_stem_wgrad_rows_ok(ex->L[stem].conv) ||
+          ex->eff_owner[bn] != bn)
+        continue;
+      int64_t xo = -1, xb = 0, go = -1, gb = 0;
+      for (size_t j = i; j-- > 0 && (xo < 0 || go < 0);) {
+        const snp::Event& f = P.tape[j];
+        if (f.op != 'A') continue;
+        if (xo < 0 && f.a == snp::K_ACT && f.b == stem) xo = f.c, xb = f.d;
+        if (go < 0 && f.a == snp::K_GRAD && f.b == bn) go = f.c, gb = f.d;
+      }
+      if (xo < 0 || go < 0) continue;
+      for (size_t j = i + 1; j < T; ++j) {
+        const snp::Event& f = P.tape[j];
+        if (f.op == 'A' && (overlap(f.c, f.d, xo, xb) || overlap(f.c, f.d, go, gb))) break;
+        if (f.op == 'B' && f.b == stem) {
+          stem_bn_fuse_at[i] = 1;
+          break;
+        }
+        if (is_compute(f.op)) break;
       }
     }
     ex->elided = elide_out;

@@ -24,6 +24,7 @@
 #include <mutex>
 
 #include "gemm_tc.cuh"
+#include "bn_math.cuh"
 #include "kernels.hpp"
 #include "tma_host.hpp"
 
@@ -1264,38 +1265,58 @@ int64_t stem_wgrad_partial_floats(const ConvShape& s) {
 
 namespace {
 
-// Stem weight gradient, 4 output rows per k block: the sliding-window views of
-// input rows 2p .. 2p+13 (14 boxes of 32 windows) serve output rows p .. p+3 --
+// Stem weight gradient, 2 output rows per k block: the sliding-window views of
+// input rows 2p .. 2p+9 (10 boxes of 32 windows) serve output rows p, p+1 --
 // row p+g's filter-row atoms r = 0..7 are boxes 2g .. 2g+7, consecutive, so the
 // A operand of either 128-row M tile is a uniform-stride run of boxes -- and
 // both M tiles (filter rows 0-3, 4-7; row 7 is padding) share every dy box.
-// 22 boxes per 4 x 32 output pixels instead of 48: the 1-row kernel was bound
-// by this operand traffic.  Each CTA accumulates a contiguous range of units
-// (image, 4-row group, 32-column block) and writes one [256][64] partial slice.
-constexpr int kSwG = 4;  // output rows per k block
-constexpr int kSwStages = 2;
+// Each CTA accumulates a contiguous range of units (image, 2-row group,
+// 32-column block) and writes one [256][64] partial slice.
+//
+// Warps 0-3 see every dy tile before the tensor core does: they sum the conv
+// bias gradient from it (fixed order: thread = channel quad x k-row group),
+// and with FUSED the tile is not dy at all but the stem BN's own dy g, which
+// they turn into the BN's dx in place from the BN input x (loaded beside it)
+// and the BN statistics -- the BN backward's dx pass fused into its only
+// consumer, dx never written to HBM.  Both paths compute dx with the same
+// element function (bn_dx_elem) and sum in the same order, so they are
+// bit-identical.
+constexpr int kSwG = 2;  // output rows per k block
+constexpr int kSwStages = 3;
 struct StemWgArgs {
   int N, P, Q, groups, qblocks, units, stride;
   int M;           // valid rows R * 32 (the rest of the second M tile is the padding atom)
   float* partial;  // [gridDim.x][M][64]
+  double* dbias_part;  // [gridDim.x][2][64] conv bias gradient partials (plane 1 zero), or null
+  // FUSED: the stem BN's backward (its statistics pass has run)
+  const float* stats;  // BN mean[64], invstd[64]
+  const float* gamma;
+  const float* beta;
+  const float* coef;   // sum(g), sum(g xhat) [2][64]
+  float inv_m;
+  int relu;
 };
 
+template <bool FUSED>
 __global__ void __launch_bounds__(kTmaThreads, 1)
     stem_wgrad_rows_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                           StemWgArgs a) {
+                           const __grid_constant__ CUtensorMap tmX, StemWgArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  constexpr int NA = 2 * kSwG + 6, NB = 2 * kSwG;  // box slots per stage (stride <= 2)
-  const int na = a.stride * (kSwG - 1) + 8;         // input rows the 4 output rows need (8 = R padded)
-  constexpr uint32_t STAGE = (NA + NB) * 4096;
+  constexpr int NA = 2 * kSwG + 6, NB = 2 * kSwG, NX = FUSED ? 2 * kSwG : 0;  // box slots per stage (stride <= 2)
+  const int na = a.stride * (kSwG - 1) + 8;  // input rows the output rows need (8 = R padded)
+  constexpr uint32_t STAGE = (NA + NB + NX) * 4096;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSwStages * STAGE);
-  uint64_t* empty = full + kSwStages;
+  uint64_t* conv = full + kSwStages;   // warps 0-3 are done with the dy tile
+  uint64_t* empty = conv + kSwStages;
   uint64_t* done = empty + kSwStages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  float4* sred = reinterpret_cast<float4*>(smem + kSwStages * STAGE + 128);  // 128 float4 (2 KB)
   const int warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
     for (int i = 0; i < kSwStages; ++i) {
       mbar_init(&full[i], 1);
+      mbar_init(&conv[i], 128);
       mbar_init(&empty[i], 1);
     }
     mbar_init(done, 1);
@@ -1323,12 +1344,15 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
       if (wrap) mbar_wait(&empty[s], ph ^ 1);
       if (elect_one()) {
         uint8_t* st = smem + s * STAGE;
-        mbar_arrive_expect_tx(&full[s], (na + NB) * 4096);
+        mbar_arrive_expect_tx(&full[s], (na + NB + NX) * 4096);
         for (int j = 0; j < na; ++j)
           tma_load_4d(smem_u32(st + j * 4096), &tmA, &full[s], 0, qb * 32, p0 * a.stride + j, n);
         for (int g = 0; g < kSwG; ++g)
-          for (int kc = 0; kc < 2; ++kc)
+          for (int kc = 0; kc < 2; ++kc) {
             tma_load_4d(smem_u32(st + (NA + 2 * g + kc) * 4096), &tmB, &full[s], kc * 32, qb * 32, p0 + g, n);
+            if (FUSED)
+              tma_load_4d(smem_u32(st + (NA + NB + 2 * g + kc) * 4096), &tmX, &full[s], kc * 32, qb * 32, p0 + g, n);
+          }
       }
       __syncwarp();
       if (++s == kSwStages) {
@@ -1344,7 +1368,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     uint32_t s = 0, ph = 0;
     bool first = true;
     for (int u = u0; u < u1; ++u) {
-      mbar_wait(&full[s], ph);
+      mbar_wait(&conv[s], ph);
       tc_fence_after();
       if (elect_one()) {
         const uint64_t ad = a0 + s * (STAGE >> 4), bd = b0 + s * (STAGE >> 4);
@@ -1368,6 +1392,88 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     if (elect_one()) umma_commit(done);
     __syncwarp();
   } else {
+    // ---- dy tiles: bias-gradient sums, FUSED: g -> dx in place ----
+    // thread = channel quad cq (kc = cq / 8, 16-byte chunk cq % 8 of the
+    // 128-byte k-rows) x k-row group kg (rows kg, kg+8, kg+16, kg+24)
+    const int t = threadIdx.x, cq = t & 15, kg = t >> 4, kc = cq >> 3, mc = cq & 7;
+    const int c0 = cq * 4;
+    float4 bsum = make_float4(0.f, 0.f, 0.f, 0.f);
+    float gm[4] = {0, 0, 0, 0}, gi[4] = {0, 0, 0, 0}, gga[4] = {0, 0, 0, 0}, gbe[4] = {0, 0, 0, 0};
+    float gs[4] = {0, 0, 0, 0}, k1[4] = {0, 0, 0, 0}, k2[4] = {0, 0, 0, 0};
+    if (FUSED) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        gm[e] = a.stats[c0 + e];
+        gi[e] = a.stats[64 + c0 + e];
+        gga[e] = a.gamma[c0 + e];
+        gbe[e] = a.beta[c0 + e];
+        gs[e] = gga[e] * gi[e];
+        k1[e] = a.coef[c0 + e] * a.inv_m;
+        k2[e] = a.coef[64 + c0 + e] * a.inv_m;
+      }
+    }
+    uint32_t s = 0, ph = 0;
+    for (int u = u0; u < u1; ++u) {
+      int n, p0, qb;
+      unit(u, n, p0, qb);
+      (void)n;
+      (void)p0;
+      const int qvalid = a.Q - qb * 32;  // k-rows (output columns) beyond Q are zero-filled padding
+      mbar_wait(&full[s], ph);
+      uint8_t* st = smem + s * STAGE;
+#pragma unroll
+      for (int g = 0; g < kSwG; ++g) {
+        uint8_t* bbox = st + (NA + 2 * g + kc) * 4096;
+        const uint8_t* xbox = st + (NA + NB + 2 * g + kc) * 4096;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint32_t krow = static_cast<uint32_t>(kg + 8 * i);
+          const uint32_t off = mn_tile_off<32>(krow, static_cast<uint32_t>(mc));
+          float4 v = *reinterpret_cast<const float4*>(bbox + off);
+          if (FUSED) {
+            const float4 xv = *reinterpret_cast<const float4*>(xbox + off);
+            const float xs[4] = {xv.x, xv.y, xv.z, xv.w};
+            float gg[4] = {v.x, v.y, v.z, v.w}, r[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              if (a.relu && !(bn_affine(xs[e], gm[e], gi[e], gga[e], gbe[e]) > 0.f)) gg[e] = 0.f;
+              r[e] = static_cast<int>(krow) < qvalid ? bn_dx_elem(gg[e], xs[e], gm[e], gi[e], gs[e], k1[e], k2[e])
+                                                     : 0.f;
+            }
+            v = make_float4(r[0], r[1], r[2], r[3]);
+            *reinterpret_cast<float4*>(bbox + off) = v;
+          }
+          bsum.x += v.x;
+          bsum.y += v.y;
+          bsum.z += v.z;
+          bsum.w += v.w;
+        }
+      }
+      if (FUSED) fence_proxy_async();
+      mbar_arrive(&conv[s]);
+      if (++s == kSwStages) {
+        s = 0;
+        ph ^= 1;
+      }
+    }
+    // conv bias gradient partial of this CTA: the 8 k-row groups of each
+    // channel quad in order, in double
+    if (a.dbias_part) {
+      sred[t] = bsum;
+      named_bar(1, 128);
+      if (t < 16) {
+        double acc[4] = {0, 0, 0, 0};
+        for (int j = 0; j < 8; ++j) {
+          const float4 w = sred[j * 16 + t];
+          acc[0] += w.x; acc[1] += w.y; acc[2] += w.z; acc[3] += w.w;
+        }
+        double* p = a.dbias_part + static_cast<size_t>(blockIdx.x) * 128 + t * 4;
+        for (int e = 0; e < 4; ++e) {
+          p[e] = acc[e];
+          p[64 + e] = 0.0;
+        }
+      }
+    }
     const int lane = threadIdx.x & 31;
     float* out = a.partial + static_cast<size_t>(blockIdx.x) * a.M * 64;
     if (u0 >= u1) {
@@ -1405,16 +1511,24 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
 
 }  // namespace
 
+bool conv_stem_wgrad_rows_ok(const ConvShape& s) {
+  const StemGeom g = stem_geom(s);
+  return s.K == 64 && g.sblocks == 1 && s.R <= 8 && s.P % kSwG == 0 && s.stride <= 2;
+}
+
 cudaError_t conv_stem_wgrad(const ConvShape& s, const float* xp, const float* dy, float* partial, float* wp_scratch,
-                            float* dw, float* db, float* red, cudaStream_t st) {
+                            float* dw, float* db, float* red, cudaStream_t st, const StemBnFuse* fuse) {
   const StemGeom g = stem_geom(s);
   const int Sp = g.sblocks * 8;
   const int M = s.R * g.sblocks * 32;
   cudaError_t err;
-  if (s.K == 64 && g.sblocks == 1 && s.R <= 8 && s.P % kSwG == 0 && s.stride <= 2) {
-    CUtensorMap A, B;
+  if (conv_stem_wgrad_rows_ok(s)) {
+    CUtensorMap A, B, X;
+    const float* bsrc = fuse ? fuse->g : dy;
     if (!make_stem_view(&A, xp, g, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) return cudaErrorInvalidValue;
-    if (!make_nhwc4(&B, dy, s.N, s.P, s.Q, s.K, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) return cudaErrorInvalidValue;
+    if (!make_nhwc4(&B, bsrc, s.N, s.P, s.Q, s.K, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) return cudaErrorInvalidValue;
+    if (!make_nhwc4(&X, fuse ? fuse->x : bsrc, s.N, s.P, s.Q, s.K, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
+      return cudaErrorInvalidValue;
     StemWgArgs wa{};
     wa.N = s.N;
     wa.P = s.P;
@@ -1425,11 +1539,22 @@ cudaError_t conv_stem_wgrad(const ConvShape& s, const float* xp, const float* dy
     wa.stride = s.stride;
     wa.M = M;
     wa.partial = partial;
+    wa.dbias_part = db ? reinterpret_cast<double*>(red) : nullptr;
+    if (fuse) {
+      wa.stats = fuse->stats;
+      wa.gamma = fuse->gamma;
+      wa.beta = fuse->beta;
+      wa.coef = fuse->coef;
+      wa.inv_m = 1.0f / static_cast<float>(fuse->rows);
+      wa.relu = fuse->relu;
+    }
     const int grid = num_sms();
-    const int smem = kSwStages * (2 * kSwG + 6 + 2 * kSwG) * 4096 + 256 + 1024;
-    err = cudaFuncSetAttribute(stem_wgrad_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const int nbox = 2 * kSwG + 6 + 2 * kSwG + (fuse ? 2 * kSwG : 0);
+    const int smem = kSwStages * nbox * 4096 + 128 + 2048 + 1024;
+    auto kern = fuse ? stem_wgrad_rows_kernel<true> : stem_wgrad_rows_kernel<false>;
+    err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (err != cudaSuccess) return err;
-    stem_wgrad_rows_kernel<<<grid, kTmaThreads, smem, st>>>(A, B, wa);
+    kern<<<grid, kTmaThreads, smem, st>>>(A, B, X, wa);
     err = cudaGetLastError();
     if (err != cudaSuccess) return err;
     // rows (r, s', c) of the [256][64] slices; rows >= R*32 are the padding atom
@@ -1439,8 +1564,9 @@ cudaError_t conv_stem_wgrad(const ConvShape& s, const float* xp, const float* dy
     err = cudaGetLastError();
     if (err != cudaSuccess) return err;
     if (!db) return cudaSuccess;
-    return bias_grad(dy, static_cast<int64_t>(s.N) * s.P * s.Q, s.K, db, red, st);
+    return bias_grad_from_partials(reinterpret_cast<const double*>(red), grid, s.K, db, st);
   }
+  if (fuse) return cudaErrorInvalidValue;  // the fused BN dx exists only in the rows kernel
   const int splits = conv_stem_wgrad_splits(s);
   const int BN = bn_for(s.K);
   CUtensorMap A, B, D;

@@ -63,8 +63,23 @@ cudaError_t stem_pad_input(const ConvShape& s, int H_raw, int W_raw, int C_raw, 
                            cudaStream_t st);
 cudaError_t conv_stem_fwd(const ConvShape& s, const float* xp, const float* w, float* wp_scratch, const float* bias,
                           float* y, float* stats, cudaStream_t st);
+// The stem BN's backward fused into the stem weight gradient: instead of the
+// materialised BN dx, the kernel reads the BN input x and the BN's own dy g
+// and forms dx on the fly (statistics / coefficients from bn_bwd's
+// statistics pass); bit-identical to running bn_bwd's dx pass first.
+struct StemBnFuse {
+  const float* x;      // BN input (the stem CONV's output) [N][P][Q][K]
+  const float* g;      // BN output gradient [N][P][Q][K] (ReLU mask applied here when relu)
+  const float* stats;  // BN mean[K], invstd[K]
+  const float* gamma;
+  const float* beta;
+  const float* coef;   // bn_bwd's {sum g, sum g xhat} (bn_coef_ptr)
+  int64_t rows;
+  int relu;
+};
+bool conv_stem_wgrad_rows_ok(const ConvShape& s);
 cudaError_t conv_stem_wgrad(const ConvShape& s, const float* xp, const float* dy, float* partial, float* wp_scratch,
-                            float* dw, float* db, float* red, cudaStream_t st);
+                            float* dw, float* db, float* red, cudaStream_t st, const StemBnFuse* fuse = nullptr);
 // Channel-pad raw NHWC images (C_raw -> Cs) for the generic path.
 cudaError_t pad_channels(const float* raw, int C_raw, float* out, int Cs, int64_t pixels, cudaStream_t st);
 
@@ -153,6 +168,10 @@ constexpr int kRedChunks = 592;
 int64_t red_scratch_floats(int C);
 
 cudaError_t bias_grad(const float* dy, int64_t rows, int C, float* db, float* red_scratch, cudaStream_t st);
+// db[c] = sum over blocks of part[block][0][c] (fixed order; part [nblocks][2][C] doubles)
+cudaError_t bias_grad_from_partials(const double* part, int nblocks, int C, float* db, cudaStream_t st);
+// where bn_bwd leaves its {sum g, sum g xhat} coefficients inside red_scratch
+float* bn_coef_ptr(float* red_scratch, int C);
 
 // BatchNorm (training statistics).  stats = {mean[C], invstd[C]} saved outside
 // the arena; running = {mean[C], var[C]} updated only when update_running.

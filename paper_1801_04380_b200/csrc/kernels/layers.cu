@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <type_traits>
 
+#include "bn_math.cuh"
 #include "kernels.hpp"
 
 namespace sn {
@@ -41,10 +42,7 @@ __device__ __forceinline__ float4 relu4(const float4& v) {
 // BN normalisation, written with explicit-rounding intrinsics so that the
 // forward, its replays and the ReLU mask recomputed in the fused backward are
 // bit-identical (no compiler FMA contraction choices).
-__device__ __forceinline__ float bn_xhat(float x, float m, float is) { return __fmul_rn(__fsub_rn(x, m), is); }
-__device__ __forceinline__ float bn_affine(float x, float m, float is, float g, float b) {
-  return __fmaf_rn(bn_xhat(x, m, is), g, b);
-}
+
 struct Bn4 {
   float4 m, is, g, b;
 };
@@ -497,7 +495,9 @@ __global__ void bn_dx_scalar(const float* __restrict__ x, const float* __restric
     float g = dy[j];
     if (relu && !(bn_affine(x[j], stats[c], stats[C + c], gamma[c], beta[c]) > 0.f)) g = 0.f;
     const float xh = bn_xhat(x[j], stats[c], stats[C + c]);
-    const float v = gamma[c] * stats[C + c] * (g - coef[c] * inv_m - xh * (coef[C + c] * inv_m));
+    (void)xh;
+    const float v = bn_dx_elem(g, x[j], stats[c], stats[C + c], gamma[c] * stats[C + c], coef[c] * inv_m,
+                               coef[C + c] * inv_m);
     dx[j] = accumulate ? dx[j] + v : v;
   }
 }
@@ -573,7 +573,7 @@ __global__ void __launch_bounds__(kThreads, 4) bn_dx_v4(const float4* __restrict
       const float xs[4] = {xv[u].x, xv[u].y, xv[u].z, xv[u].w}, gg[4] = {gv[u].x, gv[u].y, gv[u].z, gv[u].w};
       float r[4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) r[e] = gs[e] * (gg[e] - k1[e] - bn_xhat(xs[e], m[e], is[e]) * k2[e]);
+      for (int e = 0; e < 4; ++e) r[e] = bn_dx_elem(gg[e], xs[e], m[e], is[e], gs[e], k1[e], k2[e]);
       float4 o = make_float4(r[0], r[1], r[2], r[3]);
       if (dbias_part) add4(bsum, o);
       if (accumulate) add4(o, ov[u]);
@@ -1522,6 +1522,13 @@ int64_t red_scratch_floats(int C) {
   // fused bias-gradient partials of bn_bwd: kEltBlocks*2*C doubles
   return static_cast<int64_t>(kRedChunks) * 2 * C * 2 + 2 * C + 64 + static_cast<int64_t>(kEltBlocks) * 2 * C * 2;
 }
+
+cudaError_t bias_grad_from_partials(const double* part, int nblocks, int C, float* db, cudaStream_t st) {
+  colred_stage2<<<stage2_blocks(C), kStage2Threads, 0, st>>>(part, nblocks, C, BiasFin{db});
+  return cudaGetLastError();
+}
+
+float* bn_coef_ptr(float* red_scratch, int C) { return red_scratch + static_cast<int64_t>(kRedChunks) * 2 * C * 2; }
 
 cudaError_t bias_grad(const float* dy, int64_t rows, int C, float* db, float* red_scratch, cudaStream_t st) {
   return colred(RedBiasOp{dy}, BiasFin{db}, rows, C, red_scratch, st);

@@ -592,3 +592,20 @@ def test_autotune_catalog_measures_and_trains(cuda):
     worst = max(relative_error(grads[l][k], ref[l][k]) for l in ref for k in ("w", "b"))
     assert abs(loss - ref_loss) <= 5e-3 * abs(ref_loss)
     assert worst <= 3 * sens + 5e-3, (worst, sens)
+
+
+def test_stem_bn_dx_fused_into_stem_wgrad_is_bit_identical(cuda, monkeypatch):
+    """The stem BN's dx pass folded into the stem weight gradient (dx formed
+    from the BN input and dy inside the kernel, never written) equals the
+    materialised path bit for bit, with every other fusion on, and launches
+    one kernel fewer."""
+    from paper_1801_04380_b200.netgen import gen_resnet
+    from paper_1801_04380_b200.training import init_parameters
+    net = gen_resnet(3, 4, 6, 3)
+    params = init_parameters(net, seed=2, head_scale=0.1)
+    images, labels = _inputs(net, 8)
+    loss, grads, _, t = _run(net, 8, 4 << 30, ALL, params, images, labels)
+    monkeypatch.setenv("SN_FUSE_STEM_BN", "0")
+    loss0, grads0, _, t0 = _run(net, 8, 4 << 30, ALL, params, images, labels)
+    assert t.kernels == t0.kernels - 1
+    assert loss == loss0 and _bitwise(grads, grads0)
