@@ -383,7 +383,10 @@ def run_ours(args) -> None:
            if args.autotune else {}),
         "losses": [round(l, 5) for l in losses[:3]] + [round(losses[-1], 5)],
     }
-    if not args.no_extras and rank == 0:
+    # the extras time eager iterations of this executor, whose weight-gradient
+    # all-reduce needs every rank: single-replica runs only (the contract asks
+    # for roofline / CPU baseline at N = 1)
+    if not args.no_extras and world == 1:
         line.update(extras(args, net, cfg, ex, ms_per_step, local))
     ex.close()
     ctx.close()

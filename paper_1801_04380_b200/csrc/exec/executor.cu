@@ -2028,6 +2028,17 @@ int sn_exec_create(const sn_plan* plan, const sn_net_desc* /*net*/, const sn_lay
       ck(cudaStreamCreateWithFlags(&ex->s5, cudaStreamNonBlocking), "stream");
       ex->dmalloc(&ex->update_flag, 4, sn_exec::M_OTHER, "cudaMalloc(update flag)");
       ck(cudaMemset(ex->update_flag, 0, 4), "memset(flag)");
+      // one eager all-reduce of every bucket (the gradients are still zero) so
+      // NCCL sets up its connections outside the CUDA-graph capture
+      std::string nerr;
+      const sndp::Nccl* nc = sndp::nccl(&nerr);
+      if (!nc) xfail(SN_EK_CUDA, nerr);
+      for (const auto& b : ex->buckets) {
+        const ncclResult_t r = nc->AllReduce(ex->grads + b.lo, ex->grads + b.lo, static_cast<size_t>(b.hi - b.lo),
+                                             ncclFloat32, ncclSum, static_cast<ncclComm_t>(ex->opt.dp_comm), ex->s5);
+        if (r != ncclSuccess) xfail(SN_EK_CUDA, std::string("ncclAllReduce (warm-up): ") + nc->GetErrorString(r));
+      }
+      ck(cudaStreamSynchronize(ex->s5), "sync(warm-up)");
     }
     Compiler comp(ex);
     comp.compile();
