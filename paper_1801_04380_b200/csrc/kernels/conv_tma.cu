@@ -997,11 +997,7 @@ namespace {
 // R per row, and no per-tile weight traffic (the 1-row kernel was bound by
 // its L2 -> SMEM operand traffic).
 constexpr int kStemRT = 4;
-constexpr int kStemRing = 4;
-// store staging buffers per epilogue group: the output write is TMA-store
-// latency bound (each group may only reuse a buffer once its previous store
-// has been read), so more buffers = more stores in flight per SM
-constexpr int kStemEpiBufs = 3;
+constexpr int kStemRing = 6;
 constexpr int kStemThreads = 320;  // producer (warp 4), MMA (warp 5), two epilogue groups (warps 0-3, 6-9)
 struct StemRowsArgs {
   int N, P, Q, R, stride, K, rows_in;  // rows_in = (RT-1)*stride + R input rows per tile
@@ -1018,8 +1014,8 @@ __global__ void __launch_bounds__(kStemThreads, 1)
   constexpr int A_BYTES = kBM * 128, W_BYTES = 64 * 128;
   uint8_t* sA = smem;                                  // kStemRing input-row views
   uint8_t* sW = sA + kStemRing * A_BYTES;              // R weight k-blocks (resident)
-  uint8_t* sEpi = sW + a.R * W_BYTES;                  // 2 groups x kStemEpiBufs x 16 KB store staging
-  uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + 2 * kStemEpiBufs * kBM * 128);
+  uint8_t* sEpi = sW + a.R * W_BYTES;                  // 2 groups x 2 x 16 KB store staging
+  uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + 4 * kBM * 128);
   uint64_t* empty = full + kStemRing;
   uint64_t* wbar = empty + kStemRing;
   uint64_t* tfull = wbar + 1;
@@ -1114,7 +1110,7 @@ __global__ void __launch_bounds__(kStemThreads, 1)
     const uint32_t row = q4 * 32 + lane;
     const bool leader = q4 == 0 && lane == 0;
     const uint32_t bar_id = 1 + grp;
-    uint8_t* sEpiG = sEpi + grp * kStemEpiBufs * (kBM * 128);
+    uint8_t* sEpiG = sEpi + grp * 2 * (kBM * 128);
     float* sredG = sred + grp * 256;
     int local = 0;
     uint32_t chunk_no = 0;
@@ -1148,9 +1144,8 @@ __global__ void __launch_bounds__(kStemThreads, 1)
                 if (c + q < a.K) v[q] += __ldg(a.bias + c + q);
             }
           }
-          const uint32_t bi = chunk_no % kStemEpiBufs;
-          const uint32_t buf = smem_u32(sEpiG) + bi * (kBM * 128);
-          if (leader) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kStemEpiBufs - 1) : "memory");
+          const uint32_t buf = smem_u32(sEpiG) + (chunk_no & 1u) * (kBM * 128);
+          if (leader) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
           named_bar(bar_id, 128);
 #pragma unroll
           for (int q = 0; q < 8; ++q)
@@ -1164,7 +1159,7 @@ __global__ void __launch_bounds__(kStemThreads, 1)
             bulk_commit();
           }
           if (a.stats && p < a.P) {
-            const uint8_t* sb = sEpiG + bi * (kBM * 128);
+            const uint8_t* sb = sEpiG + (chunk_no & 1u) * (kBM * 128);
             float shift, t1, t2;
             const int Q = a.Q;
             chunk_column_stats(sb, [Q](int r) { return r < Q; }, sredG, shift, t1, t2, bar_id);
@@ -1215,7 +1210,7 @@ cudaError_t conv_stem_fwd(const ConvShape& s, const float* xp, const float* w, f
     ra.tiles = s.N * ((s.P + kStemRT - 1) / kStemRT);
     ra.bias = bias;
     ra.stats = stats;
-    const int smem = kStemRing * kBM * 128 + s.R * 64 * 128 + 2 * kStemEpiBufs * kBM * 128 + 512 + 2048 + 1024;
+    const int smem = kStemRing * kBM * 128 + s.R * 64 * 128 + 4 * kBM * 128 + 512 + 2048 + 1024;
     static int attr_smem = 0;  // the filter's share depends on R: raise the opt-in when a larger one comes
     if (smem > attr_smem) {
       err = cudaFuncSetAttribute(stem_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
