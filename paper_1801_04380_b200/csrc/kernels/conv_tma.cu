@@ -636,14 +636,7 @@ cudaError_t launch(const CUtensorMap& A, const CUtensorMap& B, const CUtensorMap
   tg.m_tiles = (M + kBM * CG - 1) / (kBM * CG);
   tg.n_tiles = (N + BN - 1) / BN;
   tg.tiles = tg.m_tiles * tg.n_tiles * ((a.num_kb + kps - 1) / kps);
-  // experiment knob: SN_WGRAD_SMS caps the persistent grid of the weight
-  // gradients (MODE 1), which run on the side stream beside the backward chain
-  static int wg_cap = -1;
-  if (wg_cap < 0) {
-    const char* v = std::getenv("SN_WGRAD_SMS");
-    wg_cap = v ? std::atoi(v) : 0;
-  }
-  const int sms = (MODE == 1 && wg_cap > 0) ? std::min(wg_cap, num_sms()) : num_sms();
+  const int sms = num_sms();
   if constexpr (CG == 1) {
     const int grid = std::min(tg.tiles, sms);
     kern<<<grid, kTmaThreads, L::TOTAL, st>>>(A, B, D, args, e, tg);
