@@ -293,6 +293,12 @@ int sn_exec_profile(sn_exec* ex, float* action_ms, int32_t* action_layer, int32_
  * by a 0x1e byte (truncated to names_cap).  Captured from one serial
  * iteration (weight gradients on the compute stream), nothing executed. */
 int sn_exec_census(sn_exec* ex, int32_t* action_kernels, size_t cap, char* names, size_t names_cap, size_t* n);
+/* Per-kernel CUDA-event time of one iteration: the serial iteration of
+ * sn_exec_census replayed node by node on the compute stream (copies and
+ * memsets too), an event pair around every kernel, median of `reps` replays.
+ * us[k] / action[k] for the k-th kernel in issue order (n = count; call with
+ * us = NULL first to size the buffers). */
+int sn_exec_kernel_times(sn_exec* ex, int32_t reps, float* us, int32_t* action, size_t cap, size_t* n);
 /* Launch the SGD update alone (after an external gradient all-reduce). */
 int sn_exec_apply_update(sn_exec* ex, float lr, float grad_scale);
 /* CONV weight gradients whose split-K partials live in the conv workspace the

@@ -2244,6 +2244,63 @@ int sn_exec_profile(sn_exec* ex, float* action_ms, int32_t* action_layer, int32_
   });
 }
 
+namespace {
+// One serial iteration captured with a memset marker (value = action index)
+// before every action: the graph's nodes in issue order, each tagged with the
+// action that issued it (markers and external timer events excluded).
+struct Census {
+  cudaGraph_t graph = nullptr;
+  std::vector<std::pair<cudaGraphNode_t, int>> nodes;  // (node, action)
+  ~Census() {
+    if (graph) cudaGraphDestroy(graph);
+  }
+};
+
+void capture_census(sn_exec* ex, Census& c) {
+  if (!ex->marker) ex->dmalloc(&ex->marker, 4, sn_exec::M_OTHER, "cudaMalloc(marker)");
+  ex->serial = true;
+  struct Restore {
+    sn_exec* e;
+    ~Restore() { e->serial = false; }
+  } restore{ex};
+  ck(cudaStreamBeginCapture(ex->s0, cudaStreamCaptureModeThreadLocal), "BeginCapture");
+  try {
+    for (size_t i = 0; i < ex->prog.size(); ++i) {
+      ck(cudaMemsetAsync(ex->marker, static_cast<int>(i & 0xff), sizeof(int32_t), ex->s0), "marker");
+      ex->prog[i].fn();
+    }
+  } catch (...) {
+    cudaGraph_t g = nullptr;
+    cudaStreamEndCapture(ex->s0, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  ck(cudaStreamEndCapture(ex->s0, &c.graph), "EndCapture");
+  size_t nn = 0;
+  ck(cudaGraphGetNodes(c.graph, nullptr, &nn), "GraphGetNodes");
+  std::vector<cudaGraphNode_t> nodes(nn);
+  ck(cudaGraphGetNodes(c.graph, nodes.data(), &nn), "GraphGetNodes");
+  long cur = -1;
+  for (cudaGraphNode_t nd : nodes) {
+    cudaGraphNodeType t;
+    ck(cudaGraphNodeGetType(nd, &t), "GraphNodeGetType");
+    if (t == cudaGraphNodeTypeMemset) {
+      cudaMemsetParams mp;
+      ck(cudaGraphMemsetNodeGetParams(nd, &mp), "MemsetNodeGetParams");
+      if (mp.dst == ex->marker) {
+        ++cur;
+        if (cur >= static_cast<long>(ex->prog.size()) || static_cast<int>(mp.value) != static_cast<int>(cur & 0xff))
+          xfail(SN_EK_INTERNAL, "census markers out of order");
+        continue;
+      }
+    }
+    if (cur < 0 || (t != cudaGraphNodeTypeKernel && t != cudaGraphNodeTypeMemcpy && t != cudaGraphNodeTypeMemset))
+      continue;
+    c.nodes.push_back({nd, static_cast<int>(cur)});
+  }
+}
+}  // namespace
+
 int sn_exec_census(sn_exec* ex, int32_t* action_kernels, size_t cap, char* names, size_t names_cap, size_t* n) {
   if (!ex || !n) return xset(SN_EK_INTERNAL, "null argument");
   *n = ex->prog.size();
@@ -2253,59 +2310,22 @@ int sn_exec_census(sn_exec* ex, int32_t* action_kernels, size_t cap, char* names
     ck(cudaSetDevice(ex->device), "cudaSetDevice");
     PrecisionScope prec(ex);
     ck(cudaDeviceSynchronize(), "sync");
-    if (!ex->marker) ex->dmalloc(&ex->marker, 4, sn_exec::M_OTHER, "cudaMalloc(marker)");
-    ex->serial = true;
-    struct Restore {
-      sn_exec* e;
-      ~Restore() { e->serial = false; }
-    } restore{ex};
-    // one serial iteration captured with a memset marker (value = action
-    // index) before every action; kernel nodes between markers belong to it
-    cudaGraph_t g = nullptr;
-    ck(cudaStreamBeginCapture(ex->s0, cudaStreamCaptureModeThreadLocal), "BeginCapture");
-    try {
-      for (size_t i = 0; i < ex->prog.size(); ++i) {
-        ck(cudaMemsetAsync(ex->marker, static_cast<int>(i & 0xff), sizeof(int32_t), ex->s0), "marker");
-        ex->prog[i].fn();
-      }
-    } catch (...) {
-      cudaStreamEndCapture(ex->s0, &g);
-      if (g) cudaGraphDestroy(g);
-      throw;
-    }
-    ck(cudaStreamEndCapture(ex->s0, &g), "EndCapture");
-    size_t nn = 0;
-    ck(cudaGraphGetNodes(g, nullptr, &nn), "GraphGetNodes");
-    std::vector<cudaGraphNode_t> nodes(nn);
-    ck(cudaGraphGetNodes(g, nodes.data(), &nn), "GraphGetNodes");
+    Census c;
+    capture_census(ex, c);
     std::vector<std::string> nm(ex->prog.size());
     std::fill(action_kernels, action_kernels + ex->prog.size(), 0);
-    long cur = -1;
-    std::string err;
-    for (cudaGraphNode_t nd : nodes) {
+    for (const auto& na : c.nodes) {
       cudaGraphNodeType t;
-      ck(cudaGraphNodeGetType(nd, &t), "GraphNodeGetType");
-      if (t == cudaGraphNodeTypeMemset) {
-        cudaMemsetParams mp;
-        ck(cudaGraphMemsetNodeGetParams(nd, &mp), "MemsetNodeGetParams");
-        if (mp.dst == ex->marker) {
-          ++cur;
-          if (cur >= static_cast<long>(ex->prog.size()) || static_cast<int>(mp.value) != static_cast<int>(cur & 0xff))
-            err = "census markers out of order";
-          continue;
-        }
-      }
-      if (t != cudaGraphNodeTypeKernel || cur < 0 || cur >= static_cast<long>(ex->prog.size())) continue;
+      ck(cudaGraphNodeGetType(na.first, &t), "GraphNodeGetType");
+      if (t != cudaGraphNodeTypeKernel) continue;
       cudaKernelNodeParams kp;
-      ck(cudaGraphKernelNodeGetParams(nd, &kp), "KernelNodeGetParams");
+      ck(cudaGraphKernelNodeGetParams(na.first, &kp), "KernelNodeGetParams");
       const char* fname = nullptr;
       if (cudaFuncGetName(&fname, kp.func) != cudaSuccess || !fname) fname = "?";
-      ++action_kernels[cur];
-      nm[cur] += fname;
-      nm[cur] += '\n';
+      ++action_kernels[na.second];
+      nm[na.second] += fname;
+      nm[na.second] += '\n';
     }
-    cudaGraphDestroy(g);
-    if (!err.empty()) xfail(SN_EK_INTERNAL, err);
     if (names && names_cap) {
       std::string all;
       for (size_t i = 0; i < nm.size(); ++i) all += nm[i] + "\x1e";  // record separator per action
@@ -2313,6 +2333,90 @@ int sn_exec_census(sn_exec* ex, int32_t* action_kernels, size_t cap, char* names
       std::memcpy(names, all.data(), k);
       names[k] = 0;
     }
+  });
+}
+
+int sn_exec_kernel_times(sn_exec* ex, int32_t reps, float* us, int32_t* action, size_t cap, size_t* n) {
+  if (!ex || !n) return xset(SN_EK_INTERNAL, "null argument");
+  return xguard([&] {
+    ck(cudaSetDevice(ex->device), "cudaSetDevice");
+    PrecisionScope prec(ex);
+    ck(cudaDeviceSynchronize(), "sync");
+    Census c;
+    capture_census(ex, c);
+    size_t nk = 0;
+    for (const auto& na : c.nodes) {
+      cudaGraphNodeType t;
+      ck(cudaGraphNodeGetType(na.first, &t), "GraphNodeGetType");
+      nk += t == cudaGraphNodeTypeKernel;
+    }
+    *n = nk;
+    if (!us) return;
+    if (cap < nk) xfail(SN_EK_INTERNAL, "output buffer too small");
+    // replay the iteration node by node on s0 (copies and memsets too, so the
+    // data each kernel sees is the real one), an event pair around every kernel
+    std::vector<cudaEvent_t> ev(2 * nk);
+    for (auto& e : ev) ck(cudaEventCreate(&e), "event");
+    std::vector<std::vector<float>> t(nk);
+    cudaStream_t st = ex->s0;
+    for (int r = 0; r < std::max(1, static_cast<int>(reps)); ++r) {
+      size_t k = 0;
+      for (const auto& na : c.nodes) {
+        cudaGraphNodeType ty;
+        ck(cudaGraphNodeGetType(na.first, &ty), "GraphNodeGetType");
+        if (ty == cudaGraphNodeTypeMemcpy) {
+          cudaMemcpy3DParms mp;
+          ck(cudaGraphMemcpyNodeGetParams(na.first, &mp), "MemcpyNodeGetParams");
+          ck(cudaMemcpy3DAsync(&mp, st), "replay copy");
+          continue;
+        }
+        if (ty == cudaGraphNodeTypeMemset) {
+          cudaMemsetParams mp;
+          ck(cudaGraphMemsetNodeGetParams(na.first, &mp), "MemsetNodeGetParams");
+          if (mp.height <= 1)
+            ck(cudaMemsetAsync(mp.dst, static_cast<int>(mp.value), mp.width * mp.elementSize, st), "replay memset");
+          else
+            ck(cudaMemset2DAsync(mp.dst, mp.pitch, static_cast<int>(mp.value), mp.width * mp.elementSize, mp.height,
+                                 st),
+               "replay memset");
+          continue;
+        }
+        cudaKernelNodeParams kp;
+        ck(cudaGraphKernelNodeGetParams(na.first, &kp), "KernelNodeGetParams");
+        cudaLaunchAttributeValue cl{};
+        const bool has_cl =
+            cudaGraphKernelNodeGetAttribute(na.first, cudaLaunchAttributeClusterDimension, &cl) == cudaSuccess &&
+            cl.clusterDim.x * cl.clusterDim.y * cl.clusterDim.z > 1;
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = kp.gridDim;
+        cfg.blockDim = kp.blockDim;
+        cfg.dynamicSmemBytes = kp.sharedMemBytes;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        if (has_cl) {
+          at[0].id = cudaLaunchAttributeClusterDimension;
+          at[0].val = cl;
+          cfg.attrs = at;
+          cfg.numAttrs = 1;
+        }
+        ck(cudaEventRecord(ev[2 * k], st), "record");
+        ck(cudaLaunchKernelExC(&cfg, kp.func, kp.kernelParams), "replay launch");
+        ck(cudaEventRecord(ev[2 * k + 1], st), "record");
+        if (r == 0) action[k] = na.second;
+        ++k;
+      }
+      ck(cudaStreamSynchronize(st), "sync");
+      for (size_t i = 0; i < nk; ++i) {
+        float ms = 0.f;
+        ck(cudaEventElapsedTime(&ms, ev[2 * i], ev[2 * i + 1]), "elapsed");
+        t[i].push_back(ms * 1000.f);
+      }
+    }
+    for (size_t i = 0; i < nk; ++i) {
+      std::sort(t[i].begin(), t[i].end());
+      us[i] = t[i][t[i].size() / 2];
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
   });
 }
 

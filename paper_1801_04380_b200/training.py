@@ -182,6 +182,8 @@ def _xlib():
         L.sn_exec_arena_fill.argtypes = [C.c_void_p]
         L.sn_exec_arena_scan.argtypes = [C.c_void_p, P(C.c_int64), P(C.c_int64)]
         L.sn_exec_catalog.argtypes = [C.c_void_p, P(CatalogC), C.c_size_t, P(C.c_size_t)]
+        L.sn_exec_kernel_times.argtypes = [C.c_void_p, C.c_int32, P(C.c_float), P(C.c_int32), C.c_size_t,
+                                           P(C.c_size_t)]
         L.sn_exec_stream.argtypes = [C.c_void_p]
         L.sn_exec_stream.restype = C.c_void_p
         L._sn_configured = True
@@ -439,6 +441,19 @@ class Executor:
         return [{"layer": self.net.layers[e.layer].name, "op": ops[e.op],
                  "variant": {"halo": e.halo, "pairs": e.pairs, "bn": e.bn, "subpix": e.subpix},
                  "us": round(e.us, 2), "chosen": bool(e.chosen)} for e in buf[:n.value]]
+
+    def kernel_times(self, reps: int = 3) -> list[tuple[int, float]]:
+        """(action index, microseconds) of every kernel of one serial iteration
+        in issue order: the iteration replayed node by node with a CUDA event
+        pair around each kernel, median of ``reps`` replays."""
+        n = C.c_size_t()
+        if self.L.sn_exec_kernel_times(self.ptr, reps, None, None, 0, C.byref(n)) != 0:
+            _raise_exec(self.L)
+        us = (C.c_float * max(1, n.value))()
+        act = (C.c_int32 * max(1, n.value))()
+        if self.L.sn_exec_kernel_times(self.ptr, reps, us, act, n.value, C.byref(n)) != 0:
+            _raise_exec(self.L)
+        return [(act[i], us[i]) for i in range(n.value)]
 
     def census(self) -> list[list[str]]:
         """Per tape action (the same list ``profile`` times), the mangled names

@@ -32,6 +32,8 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
+from paper_1801_04380_b200.profiling import is_tensor, is_wgrad  # noqa: E402
+
 METRICS = ("gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,"
            "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active,"
            "dram__throughput.avg.pct_of_peak_sustained_elapsed")
@@ -56,38 +58,6 @@ def git_sha() -> str:
         return "unknown"
 
 
-def gemm_dims(net, shapes, lid: int, batch: int) -> dict:
-    """Implicit-GEMM view of a CONV / FC layer: forward M x N x K, wgrad and dgrad."""
-    lay = net.layers[lid]
-    o, i = shapes[lid], shapes[lay.prev[0]]
-    if lay.kind.value == "CONV":
-        k = lay.params["k"]
-        M, N, K = batch * o[1] * o[2], o[0], k * k * i[0]
-        return {"fwd": (M, N, K), "wgrad": (K, N, M), "dgrad": (batch * i[1] * i[2], i[0], k * k * o[0])}
-    fan = math.prod(i)
-    return {"fwd": (batch, o[0], fan), "wgrad": (fan, o[0], batch), "dgrad": (batch, fan, o[0])}
-
-
-def is_tensor(name: str) -> bool:
-    return any(t in name for t in ("tc_conv", "tc_gemm", "stem_rows_kernel", "stem_wgrad_rows"))
-
-
-def is_wgrad(name: str) -> bool:
-    """Mangled census names: the halo / stem weight-gradient kernels say so;
-    tc_conv_tma_kernel<BN, STAGES, MODE, CG> is a weight gradient at MODE 1 or 3;
-    tc_gemm_kernel<BN, STAGES, A_MN, B_MN, ...> with both operands MN-major."""
-    if "wgrad" in name:
-        return True
-    if "tc_conv_tma_kernel" in name:
-        ints = re.findall(r"Li(\d+)E", name.split("tc_conv_tma_kernel", 1)[1])
-        return len(ints) >= 3 and ints[2] in ("1", "3")
-    if "tc_gemm_kernel" in name:
-        tail = name.split("tc_gemm_kernel", 1)[1]
-        flags = re.findall(r"Lb([01])E", tail)
-        return len(flags) >= 2 and flags[0] == "1" and flags[1] == "1"
-    return False
-
-
 def collect(args) -> None:
     import torch
     import paper_1801_04380_b200 as sn
@@ -101,7 +71,8 @@ def collect(args) -> None:
     ex.set_inputs(*_inputs(net, B))
     for _ in range(3):
         ex.step(update=False)
-    census = ex.census()
+    from paper_1801_04380_b200.profiling import kernel_table
+    actions = kernel_table(ex, reps=5)  # census + per-kernel event times + FLOP attribution
     runs = [ex.profile() for _ in range(5)]
     if args.ncu_region:
         torch.cuda.synchronize()
@@ -109,21 +80,13 @@ def collect(args) -> None:
         ex.profile()
         torch.cuda.synchronize()
         torch.cuda.profiler.stop()
-    shapes = sn.propagate_shapes(net)
-    actions = []
-    for i, (names, (ms0, lid, typ)) in enumerate(zip(census, runs[0])):
-        a = {"i": i, "layer": lid, "type": TYPES[typ], "kernels": names,
-             "ms": statistics.median(r[i][0] for r in runs)}
-        if lid >= 0:
-            lay = net.layers[lid]
-            a["name"], a["kind"] = lay.name, lay.kind.value
-            if lay.kind.value in ("CONV", "FC"):
-                a["gemm"] = gemm_dims(net, shapes, lid, B)
-                a["has_dgrad"] = net.layers[lay.prev[0]].kind.value != "DATA"
-        actions.append(a)
+    for a, r in zip(actions, zip(*runs)):
+        a["ms"] = statistics.median(x[0] for x in r)
+        a["kernel_names"] = [k["name"] for k in a["kernels"]]
     out = {"net": args.net, "batch": B, "pool_bytes": pool, "features": args.features, "precision": args.precision,
            "git_sha": git_sha(), "exec_digest": exec_digest(), "device": torch.cuda.get_device_name(0),
            "kernels_per_step": sum(len(a["kernels"]) for a in actions), "actions": actions,
+           "kernel_event_us_per_step": sum(k["us"] for a in actions for k in a["kernels"]),
            "serial_step_ms": statistics.median(sum(x[0] for x in r) for r in runs)}
     ex.close()
     with open(args.out, "w") as fh:
@@ -153,9 +116,14 @@ def read_ncu(path: str) -> list[dict]:
 def merge(args) -> None:
     lt = json.load(open(args.json))
     launches = read_ncu(args.csv)
-    flat = [(a, k) for a in lt["actions"] for k in a["kernels"]]
+    flat = [(a, k["name"]) for a in lt["actions"] for k in a["kernels"]]
+    kinfo = [k for a in lt["actions"] for k in a["kernels"]]
     if len(flat) != len(launches):
         sys.exit(f"census has {len(flat)} kernels, ncu region {len(launches)}: not the same iteration")
+    ev_cls = collections.defaultdict(float)
+    for a in lt["actions"]:
+        for k in a["kernels"]:
+            ev_cls["tensor" if is_tensor(k["name"]) else "hbm"] += k["us"]
     def short(ncu_name: str) -> str:
         n = ncu_name.replace("void ", "").replace("unnamed>::", "").replace("(anonymous namespace)::", "")
         m = re.match(r"(?:\w+::)*(\w+)\s*[<(]", n)
@@ -165,24 +133,16 @@ def merge(args) -> None:
         sys.exit(f"census / ncu launch names differ at {len(bad)} launches, first {bad[0]}")
     rows = []
     cls = collections.defaultdict(lambda: {"launches": 0, "s": 0.0, "dram": 0.0, "flops": 0.0})
-    for (a, kname), L in zip(flat, launches):
+    for ((a, kname), L), ki in zip(zip(flat, launches), kinfo):
         m = L["m"]
         t = m.get("gpu__time_duration.sum", 0.0)
         dram = m.get("dram__bytes_read.sum", 0.0) + m.get("dram__bytes_write.sum", 0.0)
-        flops, dims = 0.0, ""
-        tensor = is_tensor(kname)
-        if tensor and "gemm" in a:
-            same = [k for k in a["kernels"] if is_tensor(k)]
-            if a["type"] == "bwd":
-                wg = [k for k in same if is_wgrad(k)]
-                dg = [k for k in same if not is_wgrad(k)]
-                part = "wgrad" if is_wgrad(kname) else "dgrad"
-                group = wg if part == "wgrad" else dg
-            else:
-                part, group = "fwd", same
-            M, N, K = a["gemm"][part]
-            flops = 2.0 * M * N * K / max(1, len(group))
-            dims = f"{part} {M}x{N}x{K}" + (f" /{len(group)}" if len(group) > 1 else "")
+        flops, tensor = ki["flops"], is_tensor(kname)
+        dims = ""
+        if flops:
+            M, N, K = a["gemm"][ki["part"]]
+            nk = sum(1 for k in a["kernels"] if k.get("part") == ki["part"])
+            dims = f"{ki['part']} {M}x{N}x{K}" + (f" /{nk}" if nk > 1 else "")
         key = "tensor (CONV/FC GEMM)" if tensor else "hbm (layer / reduction kernels)"
         c = cls[key]
         c["launches"] += 1
@@ -190,7 +150,7 @@ def merge(args) -> None:
         c["dram"] += dram
         c["flops"] += flops
         rows.append({"i": a["i"], "layer": a.get("name", "-"), "type": a["type"], "kernel": L["name"][:70],
-                     "dims": dims, "us": t * 1e6, "flops": flops, "dram": dram,
+                     "dims": dims, "us": t * 1e6, "ev_us": ki["us"], "flops": flops, "dram": dram,
                      "tflops": flops / t / 1e12 if t and flops else None, "gbs": dram / t / 1e9 if t else None,
                      "tensor_pct": m.get("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active"),
                      "dram_pct": m.get("dram__throughput.avg.pct_of_peak_sustained_elapsed")})
@@ -206,10 +166,13 @@ def merge(args) -> None:
         md.append(f"| {k} | {c['launches']} | {c['s'] * 1e3:.3f} | {c['s'] / tot:.3f} | {c['dram'] / 1e9:.3f} | "
                   f"{c['dram'] / c['s'] / 1e9:.0f} | {c['flops'] / 1e12:.4f} | "
                   f"{(c['flops'] / c['s'] / 1e12) if c['flops'] else 0:.1f} |")
-    md += ["", "| # | layer | phase | kernel | GEMM | us | TF/s | tensor % | DRAM MB | GB/s | DRAM % |",
-           "|---|---|---|---|---|---|---|---|---|---|---|"]
+    md += ["", "`us` = ncu gpu__time_duration (cold); `ev us` = CUDA-event time of the same kernel in a node-by-node "
+           "replay of the iteration (warm, `sn_exec_kernel_times`, median of 5); TF/s from the ncu time.", "",
+           "| # | layer | phase | kernel | GEMM | us | ev us | TF/s | tensor % | DRAM MB | GB/s | DRAM % |",
+           "|---|---|---|---|---|---|---|---|---|---|---|---|"]
     for r in rows:
         md.append(f"| {r['i']} | {r['layer']} | {r['type']} | `{r['kernel']}` | {r['dims']} | {r['us']:.1f} | "
+                  f"{r['ev_us']:.1f} | "
                   f"{'' if r['tflops'] is None else f'{r['tflops']:.0f}'} | "
                   f"{'' if r['tensor_pct'] is None else f'{r['tensor_pct']:.0f}'} | {r['dram'] / 1e6:.1f} | "
                   f"{'' if r['gbs'] is None else f'{r['gbs']:.0f}'} | "
