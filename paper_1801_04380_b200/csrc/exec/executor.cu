@@ -2245,6 +2245,17 @@ int sn_exec_profile(sn_exec* ex, float* action_ms, int32_t* action_layer, int32_
 }
 
 namespace {
+// Holds the stream for `ns` nanoseconds of GPU time: queued behind it, the
+// replayed launches and their events run back to back instead of at the pace
+// the host issues them.
+__global__ void hold_stream_kernel(uint64_t ns) {
+  uint64_t t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
+
 // One serial iteration captured with a memset marker (value = action index)
 // before every action: the graph's nodes in issue order, each tagged with the
 // action that issued it (markers and external timer events excluded).
@@ -2361,6 +2372,7 @@ int sn_exec_kernel_times(sn_exec* ex, int32_t reps, float* us, int32_t* action, 
     cudaStream_t st = ex->s0;
     for (int r = 0; r < std::max(1, static_cast<int>(reps)); ++r) {
       size_t k = 0;
+      hold_stream_kernel<<<1, 1, 0, st>>>(static_cast<uint64_t>(nk) * 40000ull);  // ~40 us of host time per kernel
       for (const auto& na : c.nodes) {
         cudaGraphNodeType ty;
         ck(cudaGraphNodeGetType(na.first, &ty), "GraphNodeGetType");
