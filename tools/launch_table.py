@@ -51,10 +51,18 @@ def exec_digest() -> str:
 
 
 def git_sha() -> str:
+    """HEAD of the tree this runs from; on the GPU box (a snapshot without .git)
+    the .graft_head file written next to the sources before the call."""
     try:
-        return subprocess.run(["git", "rev-parse", "--short=12", "HEAD"], cwd=ROOT, capture_output=True,
-                              text=True, timeout=10).stdout.strip() or "unknown"
+        out = subprocess.run(["git", "rev-parse", "--short=12", "HEAD"], cwd=ROOT, capture_output=True,
+                             text=True, timeout=10).stdout.strip()
+        if out:
+            return out
     except Exception:
+        pass
+    try:
+        return open(os.path.join(ROOT, ".graft_head")).read().strip()[:12] + " (+ working tree)"
+    except OSError:
         return "unknown"
 
 
