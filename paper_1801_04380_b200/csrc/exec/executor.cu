@@ -1061,9 +1061,9 @@ struct Compiler {
         if (lid == ex->stem_layer) {  // DATA has no gradient
           const bool fused = stem_fuse_pending;
           const sn::StemBnFuse fz = stem_fuse;
-          if (fused) {  // the BN input and dy are read on s3 after the tape frees them
+          if (fused) {  // the BN input and dy (or the pool gradient) are read on s3 after the tape frees them
             side_reads[stem_fuse_keys[0]] = wdone;
-            side_reads[stem_fuse_keys[1]] = wdone;
+            if (stem_fuse_keys[1] >= 0) side_reads[stem_fuse_keys[1]] = wdone;
             stem_fuse_pending = false;
           }
           const bool rows = sn::conv_stem_wgrad_rows_ok(cs);
@@ -1155,6 +1155,44 @@ struct Compiler {
           dcb = ex->grads + ex->L[pid].b_off;
           conv_bias_done[pid] = 1;
         }
+        const int pool = bn_pool_at[cur_ti];
+        if (pool >= 0) {  // statistics in the following max pool's block order
+          const sn::PoolShape ps = ex->L[pool].pool;
+          const uint8_t* am = ex->L[pool].argmax;
+          auto pg = pending_gather.find(static_cast<int>(cur_ti));
+          const bool gather = pool_gather_at[cur_ti] && pg != pending_gather.end() && dx && !acc;
+          if (pool_gather_at[cur_ti] && !gather) xfail(SN_EK_INTERNAL, "pool gather planned but not possible");
+          if (gather) {
+            const float* dyp = pg->second.dy_pool;
+            stem_fuse = sn::StemBnFuse{x, nullptr, stats, g, beta, sn::bn_coef_ptr(red, C), rows, relu,
+                                       dyp, am, ps.P, ps.Q};
+            stem_fuse_pending = true;
+            stem_fuse_keys[0] = snp::key_code(snp::K_ACT, pid);
+            stem_fuse_keys[1] = pg->second.key;
+            pending_gather.erase(pg);
+            push([=] {
+              ck(sn::bn_bwd_pool_stats(ps, am, dyp, nullptr, x, C, g, beta, stats, relu, dg, dbt, red, st),
+                 "bn_bwd_pool_stats");
+            }, 2);
+            break;
+          }
+          const float* dym = dy;
+          push([=] {
+            ck(sn::bn_bwd_pool_stats(ps, am, nullptr, dym, x, C, g, beta, stats, relu, dg, dbt, red, st),
+               "bn_bwd_pool_stats");
+          }, 2);
+          if (stem_bn_fuse_at[cur_ti] && dx && !acc) {
+            stem_fuse = sn::StemBnFuse{x, dy, stats, g, beta, sn::bn_coef_ptr(red, C), rows, relu};
+            stem_fuse_pending = true;
+            stem_fuse_keys[0] = snp::key_code(snp::K_ACT, pid);
+            stem_fuse_keys[1] = snp::key_code(snp::K_GRAD, lid);
+            break;
+          }
+          if (dx)
+            push([=] { ck(sn::bn_bwd_dx(x, dy, rows, C, g, beta, stats, relu, dx, acc, red, st, dcb), "bn_bwd_dx"); },
+                 dcb ? 2 : 1);
+          break;
+        }
         if (stem_bn_fuse_at[cur_ti] && dx && !acc) {  // dx formed inside the stem weight gradient
           stem_fuse = sn::StemBnFuse{x, dy, stats, g, beta, sn::bn_coef_ptr(red, C), rows, relu};
           stem_fuse_pending = true;
@@ -1215,6 +1253,16 @@ struct Compiler {
         void* scratch = ex->pool_scratch;
         const int nk = sn::pool_bwd_kernels(ps);
         const uint8_t* am = l.argmax;
+        const int bi = pool_skip_at[cur_ti];
+        if (bi >= 0) {
+          if (dx && !acc) {  // gathered by the BN backward and the stem weight gradient
+            const int po = ex->eff_owner[lid];
+            pending_gather[bi] =
+                PendingGather{dy, ex->side_root[po] ? int64_t(-1) : snp::key_code(snp::K_GRAD, po)};
+            break;
+          }
+          pool_gather_at[bi] = 0;
+        }
         if (dx) push([=] { ck(sn::pool_bwd(ps, x, y, dy, dx, acc, scratch, st, am), "pool_bwd"); }, nk);
         break;
       }
@@ -1332,6 +1380,20 @@ struct Compiler {
   bool stem_fuse_pending = false;
   sn::StemBnFuse stem_fuse{};
   int64_t stem_fuse_keys[2] = {0, 0};
+  // BN -> ReLU -> 3x3/s2 max pool (saved argmax): the BN backward statistics
+  // run in the pool's 2 x 2 block order (bn_bwd_pool_stats; a reassociating
+  // fusion, same bits whether dy is gathered or read).  bn_pool_at: BN
+  // backward index -> the pool layer.  pool_gather_at: BN backward index whose
+  // statistics and (stem weight gradient) dx gather dy from the pool's
+  // gradient and argmax; pool_skip_at: that pool's backward index -> the BN
+  // backward index (its dx is never written).
+  std::vector<int> bn_pool_at, pool_skip_at;
+  std::vector<char> pool_gather_at;
+  struct PendingGather {
+    const float* dy_pool = nullptr;
+    int64_t key = -1;  // the pool gradient's arena key (-1: outside the arena)
+  };
+  std::unordered_map<int, PendingGather> pending_gather;  // keyed by BN-backward tape index
   // CONV forward -> BN forward (next compute action, reading that output): the
   // CONV epilogue emits per-tile statistics, the BN only combines them.
   bool conv_stats_now = false, bn_tiles_now = false;
@@ -1371,6 +1433,9 @@ struct Compiler {
     join_relu.assign(T, -1);
     join_copy_own.assign(T, 0);
     stem_bn_fuse_at.assign(T, 0);
+    bn_pool_at.assign(T, -1);
+    pool_skip_at.assign(T, -1);
+    pool_gather_at.assign(T, 0);
     bn_bias_at.assign(T, 0);
     conv_bias_done.assign(net.n, 0);
     const char* env = std::getenv("SN_FUSE");  // SN_FUSE=0: one kernel per layer (A/B and bitwise tests)
@@ -1726,7 +1791,73 @@ struct Compiler {
         if (is_compute(f.op)) break;
       }
     }
+    plan_pool_stats(reassoc);
     ex->elided = elide_out;
+  }
+
+  // BN -> ReLU -> max POOL (k3 s2 p1, saved argmax, H = 2P): pool-order BN
+  // backward statistics always (with the reassociating fusions); when the BN's
+  // dx goes into the stem weight gradient (stem_bn_fuse_at), the ReLU backward
+  // is folded into the BN and the pool backward is the compute action right
+  // before them, the pool backward is dropped and both consumers gather dy --
+  // provided nothing is allocated over the pool gradient's blocks until the
+  // stem weight gradient has read them.
+  void plan_pool_stats(bool reassoc) {
+    const size_t T = P.tape.size();
+    const char* env_pg = std::getenv("SN_FUSE_POOL_GATHER");  // =0: run the pool backward (A/B test)
+    const bool gather_ok = !(env_pg && env_pg[0] == '0');
+    for (size_t i = 0; i < T && reassoc; ++i) {
+      const snp::Event& e = P.tape[i];
+      if (e.op != 'B' || net.kind[e.b] != snp::BN || bn_from_join[i] >= 0 || net.next[e.b].size() != 1) continue;
+      const int bn = e.b, act = net.next[bn][0];
+      if (!bn_relu_pair(act) || net.next[act].size() != 1) continue;
+      const int pool = net.next[act][0];
+      if (net.kind[pool] != snp::POOL || !ex->L[pool].argmax || !sn::pool_bn_stats_ok(ex->L[pool].pool, ex->L[bn].C))
+        continue;
+      if (ex->eff_owner[bn] != bn && ex->eff_owner[bn] != act) continue;
+      bn_pool_at[i] = pool;
+      if (!gather_ok || !stem_bn_fuse_at[i] || !bn_bwd_relu[i]) continue;
+      const sn::ConvShape& cs = ex->L[ex->stem_layer].conv;
+      if (!sn::stem_pool_gather_ok(cs, ex->L[pool].pool.P, ex->L[pool].pool.Q)) continue;
+      // the compute actions right before: [ReLU backward (folded)], pool backward
+      size_t ip = SIZE_MAX;
+      for (size_t j = i; j-- > 0;) {
+        const snp::Event& f = P.tape[j];
+        if (!is_compute(f.op)) continue;
+        if (f.op == 'B' && f.b == act && act_bwd_skip[j]) continue;
+        if (f.op == 'B' && f.b == pool) ip = j;
+        break;
+      }
+      if (ip == SIZE_MAX) continue;
+      const int po = ex->eff_owner[pool];
+      if (po < 0) continue;
+      size_t is = SIZE_MAX;  // the stem backward
+      for (size_t j = i + 1; j < T; ++j)
+        if (P.tape[j].op == 'B') {
+          if (P.tape[j].b == ex->stem_layer) is = j;
+          break;
+        }
+      if (is == SIZE_MAX) continue;
+      bool ok = true;
+      if (!ex->side_root[po]) {
+        int64_t go = -1, gb = 0;
+        for (size_t j = ip; j-- > 0;) {
+          const snp::Event& f = P.tape[j];
+          if (f.op == 'A' && f.a == snp::K_GRAD && f.b == po) {
+            go = f.c, gb = f.d;
+            break;
+          }
+        }
+        if (go < 0) continue;
+        for (size_t j = ip + 1; j < is && ok; ++j) {
+          const snp::Event& f = P.tape[j];
+          if (f.op == 'A' && overlap(f.c, f.d, go, gb)) ok = false;
+        }
+      }
+      if (!ok) continue;
+      pool_gather_at[i] = 1;
+      pool_skip_at[ip] = static_cast<int>(i);
+    }
   }
 
   // Data-parallel bucket all-reduce + update on s5, right after the backward

@@ -1274,16 +1274,31 @@ namespace {
 // Each CTA accumulates a contiguous range of units (image, 2-row group,
 // 32-column block) and writes one [256][64] partial slice.
 //
-// Warps 0-3 see every dy tile before the tensor core does: they sum the conv
-// bias gradient from it (fixed order: thread = channel quad x k-row group),
+// Warps 0-7 see every dy tile before the tensor core does: they sum the conv
+// bias gradient from it (fixed order: thread = channel quad x 2 x 2 pixel blocks),
 // and with FUSED the tile is not dy at all but the stem BN's own dy g, which
 // they turn into the BN's dx in place from the BN input x (loaded beside it)
 // and the BN statistics -- the BN backward's dx pass fused into its only
 // consumer, dx never written to HBM.  Both paths compute dx with the same
 // element function (bn_dx_elem) and sum in the same order, so they are
 // bit-identical.
+//
+// MODE 2 (the BN's output feeds a ReLU and a 3x3 / s2 / p1 max pool with
+// saved argmax) goes one step further back: g is not read either but gathered
+// from the pool output's gradient and the argmax -- for the k block's 2 x 32
+// pixels, the pool windows (rows p0/2, p0/2 + 1; columns qb*16 .. qb*16+16)
+// arrive as one TMA box each (out-of-range windows zero-filled: a zero pick),
+// and each pixel sums its picks from +0 in pool_max_bwd_k3s2's order -- so the
+// pool backward never runs and neither g nor dx is written.  The x tiles land
+// in the B slots and are overwritten by dx in place.
 constexpr int kSwG = 2;  // output rows per k block
 constexpr int kSwStages = 3;
+constexpr int kSwConv = 8;                                   // converter / epilogue warps
+constexpr int kSwThreads = (kSwConv + 2) * 32;               // + TMA producer + MMA issuer
+constexpr int kSwWin = 17;                                   // pool windows per k block row (32 pixels + 1)
+constexpr int kSwGatherDy = 2 * kSwWin * 64 * 4;             // [2][17][64] fp32
+constexpr int kSwGatherAm = 2 * kSwWin * 64;                 // [2][17][64] u8
+constexpr int kSwGather = ((kSwGatherDy + kSwGatherAm + 1023) / 1024) * 1024;
 struct StemWgArgs {
   int N, P, Q, groups, qblocks, units, stride;
   int M;           // valid rows R * 32 (the rest of the second M tile is the padding atom)
@@ -1298,32 +1313,36 @@ struct StemWgArgs {
   int relu;
 };
 
-template <bool FUSED>
-__global__ void __launch_bounds__(kTmaThreads, 1)
+template <int MODE>
+__global__ void __launch_bounds__(kSwThreads, 1)
     stem_wgrad_rows_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                           const __grid_constant__ CUtensorMap tmX, StemWgArgs a) {
+                           const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmG,
+                           const __grid_constant__ CUtensorMap tmM, StemWgArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  constexpr int NA = 2 * kSwG + 6, NB = 2 * kSwG, NX = FUSED ? 2 * kSwG : 0;  // box slots per stage (stride <= 2)
+  constexpr bool FUSED = MODE >= 1, GATHER = MODE == 2;
+  static_assert(kSwG == 2, "warps 0-3 walk the k block's 2 rows as 2 x 2 pixel blocks");
+  // box slots per stage (stride <= 2); GATHER: x in the B slots, then the pool windows
+  constexpr int NA = 2 * kSwG + 6, NB = 2 * kSwG, NX = MODE == 1 ? 2 * kSwG : 0;
   const int na = a.stride * (kSwG - 1) + 8;  // input rows the output rows need (8 = R padded)
-  constexpr uint32_t STAGE = (NA + NB + NX) * 4096;
+  constexpr uint32_t STAGE = (NA + NB + NX) * 4096 + (GATHER ? kSwGather : 0);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSwStages * STAGE);
   uint64_t* conv = full + kSwStages;   // warps 0-3 are done with the dy tile
   uint64_t* empty = conv + kSwStages;
   uint64_t* done = empty + kSwStages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
-  float4* sred = reinterpret_cast<float4*>(smem + kSwStages * STAGE + 128);  // 128 float4 (2 KB)
+  float4* sred = reinterpret_cast<float4*>(smem + kSwStages * STAGE + 128);  // kSwConv * 32 float4
   const int warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
     for (int i = 0; i < kSwStages; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&conv[i], 128);
+      mbar_init(&conv[i], kSwConv * 32);
       mbar_init(&empty[i], 1);
     }
     mbar_init(done, 1);
     fence_mbar_init();
   }
-  if (warp == 5) tmem_alloc(tmem_slot, 128);
+  if (warp == kSwConv + 1) tmem_alloc(tmem_slot, 128);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -1336,7 +1355,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     p0 = (r % a.groups) * kSwG;
     n = r / a.groups;
   };
-  if (warp == 4) {
+  if (warp == kSwConv) {
     uint32_t s = 0, ph = 0;
     bool wrap = false;
     for (int u = u0; u < u1; ++u) {
@@ -1345,15 +1364,21 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
       if (wrap) mbar_wait(&empty[s], ph ^ 1);
       if (elect_one()) {
         uint8_t* st = smem + s * STAGE;
-        mbar_arrive_expect_tx(&full[s], (na + NB + NX) * 4096);
+        mbar_arrive_expect_tx(&full[s], (na + NB + NX) * 4096 + (GATHER ? kSwGatherDy + kSwGatherAm : 0));
         for (int j = 0; j < na; ++j)
           tma_load_4d(smem_u32(st + j * 4096), &tmA, &full[s], 0, qb * 32, p0 * a.stride + j, n);
         for (int g = 0; g < kSwG; ++g)
           for (int kc = 0; kc < 2; ++kc) {
-            tma_load_4d(smem_u32(st + (NA + 2 * g + kc) * 4096), &tmB, &full[s], kc * 32, qb * 32, p0 + g, n);
-            if (FUSED)
+            tma_load_4d(smem_u32(st + (NA + 2 * g + kc) * 4096), GATHER ? &tmX : &tmB, &full[s], kc * 32, qb * 32,
+                        p0 + g, n);
+            if (MODE == 1)
               tma_load_4d(smem_u32(st + (NA + NB + 2 * g + kc) * 4096), &tmX, &full[s], kc * 32, qb * 32, p0 + g, n);
           }
+        if (GATHER) {
+          uint8_t* gw = st + (NA + NB) * 4096;
+          tma_load_4d(smem_u32(gw), &tmG, &full[s], 0, qb * 16, p0 >> 1, n);
+          tma_load_4d(smem_u32(gw + kSwGatherDy), &tmM, &full[s], 0, qb * 16, p0 >> 1, n);
+        }
       }
       __syncwarp();
       if (++s == kSwStages) {
@@ -1362,7 +1387,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         wrap = true;
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == kSwConv + 1) {
     constexpr uint32_t idesc = idesc_tf32(kBM, 64, true, true);
     const uint64_t a0 = umma_desc(smem_u32(smem), 4096, 512, kLayoutSW128Base32);
     const uint64_t b0 = umma_desc(smem_u32(smem + NA * 4096), 4096, 512, kLayoutSW128Base32);
@@ -1395,8 +1420,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   } else {
     // ---- dy tiles: bias-gradient sums, FUSED: g -> dx in place ----
     // thread = channel quad cq (kc = cq / 8, 16-byte chunk cq % 8 of the
-    // 128-byte k-rows) x k-row group kg (rows kg, kg+8, kg+16, kg+24)
-    const int t = threadIdx.x, cq = t & 15, kg = t >> 4, kc = cq >> 3, mc = cq & 7;
+    // 128-byte k-rows) x 2 x 2 pixel block cb (k-rows 2cb, 2cb+1 of both
+    // output rows)
+    static_assert(kSwConv == 8, "16 channel quads x 16 pixel blocks");
+    const int t = threadIdx.x, cq = t & 15, cb = t >> 4, kc = cq >> 3, mc = cq & 7;
     const int c0 = cq * 4;
     float4 bsum = make_float4(0.f, 0.f, 0.f, 0.f);
     float gm[4] = {0, 0, 0, 0}, gi[4] = {0, 0, 0, 0}, gga[4] = {0, 0, 0, 0}, gbe[4] = {0, 0, 0, 0};
@@ -1422,15 +1449,38 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
       const int qvalid = a.Q - qb * 32;  // k-rows (output columns) beyond Q are zero-filled padding
       mbar_wait(&full[s], ph);
       uint8_t* st = smem + s * STAGE;
+      {
+        const int c = cb;
+        float4 o[4];
+        if (GATHER) {
+          // the block's pixels (dh, dw) from windows (r, c), (r, c + 1) of the
+          // box, picks in pool_max_bwd_k3s2's order
+          const float4* gd = reinterpret_cast<const float4*>(st + (NA + NB) * 4096);
+          const uchar4* gm4 = reinterpret_cast<const uchar4*>(st + (NA + NB) * 4096 + kSwGatherDy);
+          const int w00 = c * 16 + cq, w01 = w00 + 16, w10 = w00 + kSwWin * 16, w11 = w10 + 16;
+          const uchar4 a00 = gm4[w00], a01 = gm4[w01], a10 = gm4[w10], a11 = gm4[w11];
+          const float4 g00 = gd[w00], g01 = gd[w01], g10 = gd[w10], g11 = gd[w11];
 #pragma unroll
-      for (int g = 0; g < kSwG; ++g) {
-        uint8_t* bbox = st + (NA + 2 * g + kc) * 4096;
-        const uint8_t* xbox = st + (NA + NB + 2 * g + kc) * 4096;
+          for (int q = 0; q < 4; ++q) o[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+#define SN_PICK(A, G, OFF, ACC)        \
+  ACC.x += (A.x == (OFF)) ? G.x : 0.f; \
+  ACC.y += (A.y == (OFF)) ? G.y : 0.f; \
+  ACC.z += (A.z == (OFF)) ? G.z : 0.f; \
+  ACC.w += (A.w == (OFF)) ? G.w : 0.f;
+          SN_PICK(a00, g00, 4, o[0]);
+          SN_PICK(a00, g00, 5, o[1]); SN_PICK(a01, g01, 3, o[1]);
+          SN_PICK(a00, g00, 7, o[2]); SN_PICK(a10, g10, 1, o[2]);
+          SN_PICK(a00, g00, 8, o[3]); SN_PICK(a01, g01, 6, o[3]);
+          SN_PICK(a10, g10, 2, o[3]); SN_PICK(a11, g11, 0, o[3]);
+#undef SN_PICK
+        }
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const uint32_t krow = static_cast<uint32_t>(kg + 8 * i);
-          const uint32_t off = mn_tile_off<32>(krow, static_cast<uint32_t>(mc));
-          float4 v = *reinterpret_cast<const float4*>(bbox + off);
+        for (int q = 0; q < 4; ++q) {
+          const int dh = q >> 1, krow = 2 * c + (q & 1);
+          uint8_t* bbox = st + (NA + 2 * dh + kc) * 4096;
+          const uint8_t* xbox = GATHER ? bbox : st + (NA + NB + 2 * dh + kc) * 4096;
+          const uint32_t off = mn_tile_off<32>(static_cast<uint32_t>(krow), static_cast<uint32_t>(mc));
+          float4 v = GATHER ? o[q] : *reinterpret_cast<const float4*>(bbox + off);
           if (FUSED) {
             const float4 xv = *reinterpret_cast<const float4*>(xbox + off);
             const float xs[4] = {xv.x, xv.y, xv.z, xv.w};
@@ -1438,8 +1488,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               if (a.relu && !(bn_affine(xs[e], gm[e], gi[e], gga[e], gbe[e]) > 0.f)) gg[e] = 0.f;
-              r[e] = static_cast<int>(krow) < qvalid ? bn_dx_elem(gg[e], xs[e], gm[e], gi[e], gs[e], k1[e], k2[e])
-                                                     : 0.f;
+              r[e] = krow < qvalid ? bn_dx_elem(gg[e], xs[e], gm[e], gi[e], gs[e], k1[e], k2[e]) : 0.f;
             }
             v = make_float4(r[0], r[1], r[2], r[3]);
             *reinterpret_cast<float4*>(bbox + off) = v;
@@ -1457,14 +1506,14 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         ph ^= 1;
       }
     }
-    // conv bias gradient partial of this CTA: the 8 k-row groups of each
-    // channel quad in order, in double
+    // conv bias gradient partial of this CTA: the 16 pixel-block columns of
+    // each channel quad in order, in double
     if (a.dbias_part) {
       sred[t] = bsum;
-      named_bar(1, 128);
+      named_bar(1, kSwConv * 32);
       if (t < 16) {
         double acc[4] = {0, 0, 0, 0};
-        for (int j = 0; j < 8; ++j) {
+        for (int j = 0; j < 16; ++j) {
           const float4 w = sred[j * 16 + t];
           acc[0] += w.x; acc[1] += w.y; acc[2] += w.z; acc[3] += w.w;
         }
@@ -1475,36 +1524,31 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         }
       }
     }
-    const int lane = threadIdx.x & 31;
+    // epilogue: warp w drains M tile w / 4, TMEM lanes 32 (w % 4) ..
+    const int lane = threadIdx.x & 31, mt = warp >> 2, wl = warp & 3;
     float* out = a.partial + static_cast<size_t>(blockIdx.x) * a.M * 64;
+    const int row = mt * 128 + wl * 32 + lane;
+    float4* dst = reinterpret_cast<float4*>(out + row * 64);
     if (u0 >= u1) {
-      for (int mt = 0; mt < 2; ++mt) {
-        const int row = mt * 128 + warp * 32 + lane;
-        if (row >= a.M) continue;
-        float4* dst = reinterpret_cast<float4*>(out + row * 64);
+      if (row < a.M)
         for (int q = 0; q < 16; ++q) dst[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-      }
     } else {
       mbar_wait(done, 0);
       tc_fence_after();
-      for (int mt = 0; mt < 2; ++mt) {
-        const int row = mt * 128 + warp * 32 + lane;
-        float4* dst = reinterpret_cast<float4*>(out + row * 64);
-        for (int c = 0; c < 64; c += 32) {
-          float v[32];
-          tmem_ld32(tmem + static_cast<uint32_t>(mt * 64 + c) + (static_cast<uint32_t>(warp * 32) << 16), v);
-          if (row < a.M) {
+      for (int c = 0; c < 64; c += 32) {
+        float v[32];
+        tmem_ld32(tmem + static_cast<uint32_t>(mt * 64 + c) + (static_cast<uint32_t>(wl * 32) << 16), v);
+        if (row < a.M) {
 #pragma unroll
-            for (int q = 0; q < 8; ++q)
-              dst[c / 4 + q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-          }
+          for (int q = 0; q < 8; ++q)
+            dst[c / 4 + q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
         }
       }
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 5) {
+  if (warp == kSwConv + 1) {
     tc_fence_after();
     tmem_dealloc(tmem, 128);
   }
@@ -1517,6 +1561,10 @@ bool conv_stem_wgrad_rows_ok(const ConvShape& s) {
   return s.K == 64 && g.sblocks == 1 && s.R <= 8 && s.P % kSwG == 0 && s.stride <= 2;
 }
 
+bool stem_pool_gather_ok(const ConvShape& s, int pool_P, int pool_Q) {
+  return conv_stem_wgrad_rows_ok(s) && s.P == 2 * pool_P && s.Q == 2 * pool_Q;
+}
+
 cudaError_t conv_stem_wgrad(const ConvShape& s, const float* xp, const float* dy, float* partial, float* wp_scratch,
                             float* dw, float* db, float* red, cudaStream_t st, const StemBnFuse* fuse) {
   const StemGeom g = stem_geom(s);
@@ -1524,12 +1572,31 @@ cudaError_t conv_stem_wgrad(const ConvShape& s, const float* xp, const float* dy
   const int M = s.R * g.sblocks * 32;
   cudaError_t err;
   if (conv_stem_wgrad_rows_ok(s)) {
-    CUtensorMap A, B, X;
-    const float* bsrc = fuse ? fuse->g : dy;
+    CUtensorMap A, B, X, G, Am;
+    const int mode = !fuse ? 0 : fuse->dy_pool ? 2 : 1;
+    if (mode == 2 && !stem_pool_gather_ok(s, fuse->pool_P, fuse->pool_Q)) return cudaErrorInvalidValue;
+    const float* bsrc = mode == 0 ? dy : mode == 1 ? fuse->g : fuse->x;
     if (!make_stem_view(&A, xp, g, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) return cudaErrorInvalidValue;
     if (!make_nhwc4(&B, bsrc, s.N, s.P, s.Q, s.K, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) return cudaErrorInvalidValue;
     if (!make_nhwc4(&X, fuse ? fuse->x : bsrc, s.N, s.P, s.Q, s.K, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
       return cudaErrorInvalidValue;
+    G = X;
+    Am = X;
+    if (mode == 2) {  // pool windows [N][P/2][Q/2][64]: boxes {64, 17, 2, 1}, zero-filled past the edges
+      const cuuint64_t P2 = static_cast<cuuint64_t>(fuse->pool_P), Q2 = static_cast<cuuint64_t>(fuse->pool_Q);
+      cuuint64_t dims[4] = {64, Q2, P2, static_cast<cuuint64_t>(s.N)};
+      cuuint32_t box[4] = {64, kSwWin, 2, 1};
+      cuuint32_t estr[4] = {1, 1, 1, 1};
+      cuuint64_t sf[3] = {64 * 4, Q2 * 64 * 4, P2 * Q2 * 64 * 4};
+      cuuint64_t sb[3] = {64, Q2 * 64, P2 * Q2 * 64};
+      if (g_encode_tiled(&G, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(fuse->dy_pool), dims, sf, box,
+                         estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS ||
+          g_encode_tiled(&Am, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<uint8_t*>(fuse->argmax), dims, sb, box,
+                         estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return cudaErrorInvalidValue;
+    }
     StemWgArgs wa{};
     wa.N = s.N;
     wa.P = s.P;
@@ -1550,12 +1617,14 @@ cudaError_t conv_stem_wgrad(const ConvShape& s, const float* xp, const float* dy
       wa.relu = fuse->relu;
     }
     const int grid = num_sms();
-    const int nbox = 2 * kSwG + 6 + 2 * kSwG + (fuse ? 2 * kSwG : 0);
-    const int smem = kSwStages * nbox * 4096 + 128 + 2048 + 1024;
-    auto kern = fuse ? stem_wgrad_rows_kernel<true> : stem_wgrad_rows_kernel<false>;
+    const int nbox = 2 * kSwG + 6 + 2 * kSwG + (mode == 1 ? 2 * kSwG : 0);
+    const int smem = kSwStages * (nbox * 4096 + (mode == 2 ? kSwGather : 0)) + 128 + kSwConv * 32 * 16 + 1024;
+    auto kern = mode == 2   ? stem_wgrad_rows_kernel<2>
+                : mode == 1 ? stem_wgrad_rows_kernel<1>
+                            : stem_wgrad_rows_kernel<0>;
     err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (err != cudaSuccess) return err;
-    kern<<<grid, kTmaThreads, smem, st>>>(A, B, X, wa);
+    kern<<<grid, kSwThreads, smem, st>>>(A, B, X, G, Am, wa);
     err = cudaGetLastError();
     if (err != cudaSuccess) return err;
     // rows (r, s', c) of the [256][64] slices; rows >= R*32 are the padding atom

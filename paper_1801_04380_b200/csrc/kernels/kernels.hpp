@@ -76,8 +76,15 @@ struct StemBnFuse {
   const float* coef;   // bn_bwd's {sum g, sum g xhat} (bn_coef_ptr)
   int64_t rows;
   int relu;
+  // optional: g gathered instead from a following 3x3 / s2 / p1 max pool's
+  // output gradient [N][pool_P][pool_Q][K] and saved argmax (g unused; the
+  // pool backward need not run; coef from bn_bwd_pool_stats)
+  const float* dy_pool = nullptr;
+  const uint8_t* argmax = nullptr;
+  int pool_P = 0, pool_Q = 0;
 };
 bool conv_stem_wgrad_rows_ok(const ConvShape& s);
+bool stem_pool_gather_ok(const ConvShape& s, int pool_P, int pool_Q);
 cudaError_t conv_stem_wgrad(const ConvShape& s, const float* xp, const float* dy, float* partial, float* wp_scratch,
                             float* dw, float* db, float* red, cudaStream_t st, const StemBnFuse* fuse = nullptr);
 // Channel-pad raw NHWC images (C_raw -> Cs) for the generic path.
@@ -197,6 +204,20 @@ cudaError_t bn_bwd(const float* x, const float* dy, int64_t rows, int C, const f
                    const float* stats, int relu, float* dx, int accumulate, float* dgamma, float* dbeta,
                    float* red_scratch, cudaStream_t st, float* dbias = nullptr, float* copy_dst = nullptr,
                    int copy_acc = 0, float* copy2 = nullptr);
+// Statistics pass of bn_bwd (dgamma, dbeta, and the coefficients at
+// bn_coef_ptr) for a BN whose [ReLU'd] output feeds a 3x3 / s2 / p1 max pool
+// with saved argmax, in 2 x 2 pixel-block order: dy gathered from the pool
+// output's gradient and argmax (dy_mat null: the pool backward need not run)
+// or read from the materialised pool-input gradient dy_mat -- same bits.
+struct PoolShape;
+// bn_bwd's dx pass alone, from coefficients a statistics pass left at bn_coef_ptr
+cudaError_t bn_bwd_dx(const float* x, const float* dy, int64_t rows, int C, const float* gamma, const float* beta,
+                      const float* stats, int relu, float* dx, int accumulate, float* red_scratch, cudaStream_t st,
+                      float* dbias = nullptr);
+bool pool_bn_stats_ok(const PoolShape& ps, int bn_C);
+cudaError_t bn_bwd_pool_stats(const PoolShape& ps, const uint8_t* argmax, const float* dy_pool, const float* dy_mat,
+                              const float* x, int C, const float* gamma, const float* beta, const float* stats,
+                              int relu, float* dgamma, float* dbeta, float* red_scratch, cudaStream_t st);
 // copy2 (optional, C % 4 == 0): the statistics pass also writes dy there and
 // the dx pass reads dy from it (dx may then overlap the original dy).
 // copy_dst (optional, C % 4 == 0): the fused backward of the 2-input JOIN

@@ -1654,34 +1654,186 @@ cudaError_t grad_copy2(const float* src, float* d1, int acc1, float* d2, int acc
 
 bool bn_bwd_bias_ok(int C) { return C % 4 == 0 && kThreads % (C / 4) == 0; }
 
+cudaError_t bn_bwd_dx(const float* x, const float* dy, int64_t rows, int C, const float* gamma, const float* beta,
+                      const float* stats, int relu, float* dx, int accumulate, float* red_scratch, cudaStream_t st,
+                      float* dbias) {
+  const float* coef = bn_coef_ptr(red_scratch, C);
+  const int64_t n = rows * C;
+  if (dbias && (!dx || !bn_bwd_bias_ok(C))) return cudaErrorInvalidValue;
+  if (!dx) return cudaSuccess;
+  if (C % 4 == 0) {
+    const int nb = elt_blocks(n / 4, C / 4);
+    // bias partials past the colred partials and coef (see red_scratch_floats)
+    double* part = dbias ? reinterpret_cast<double*>(red_scratch + static_cast<int64_t>(kRedChunks) * 2 * C * 2 +
+                                                     ((2 * C + 63) / 64) * 64)
+                         : nullptr;
+    bn_dx_v4<<<nb, kThreads, 0, st>>>(reinterpret_cast<const float4*>(x), reinterpret_cast<const float4*>(dy), n / 4,
+                                      rows, C, gamma, beta, stats, coef, reinterpret_cast<float4*>(dx), accumulate,
+                                      relu, part);
+    if (dbias) colred_stage2<<<stage2_blocks(C), kStage2Threads, 0, st>>>(part, nb, C, BiasFin{dbias});
+  } else {
+    bn_dx_scalar<<<blocks_for(n), kThreads, 0, st>>>(x, dy, n, rows, C, gamma, beta, stats, coef, dx, accumulate,
+                                                     relu);
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t bn_bwd(const float* x, const float* dy, int64_t rows, int C, const float* gamma, const float* beta,
                    const float* stats, int relu, float* dx, int accumulate, float* dgamma, float* dbeta,
                    float* red_scratch, cudaStream_t st, float* dbias, float* copy_dst, int copy_acc,
                    float* copy2) {
-  float* coef = red_scratch + static_cast<int64_t>(kRedChunks) * 2 * C * 2;  // past the partials
+  float* coef = bn_coef_ptr(red_scratch, C);
   if ((copy_dst || copy2) && C % 4 != 0) return cudaErrorInvalidValue;
+  if (dbias && (!dx || !bn_bwd_bias_ok(C))) return cudaErrorInvalidValue;
   cudaError_t e = colred(RedBnBwdOp{x, dy, stats, gamma, beta, relu, copy_dst, copy_acc, copy2},
                          BnBwdFin{C, dgamma, dbeta, coef}, rows, C, red_scratch, st);
   if (e != cudaSuccess) return e;
   if (copy2) dy = copy2;  // the dx pass reads the copy (the original may be overwritten by dx)
-  const int64_t n = rows * C;
-  if (dbias && (!dx || !bn_bwd_bias_ok(C))) return cudaErrorInvalidValue;
-  if (dx) {
-    if (C % 4 == 0) {
-      const int nb = elt_blocks(n / 4, C / 4);
-      // bias partials past the colred partials and coef (see red_scratch_floats)
-      double* part = dbias ? reinterpret_cast<double*>(red_scratch + static_cast<int64_t>(kRedChunks) * 2 * C * 2 +
-                                                       ((2 * C + 63) / 64) * 64)
-                           : nullptr;
-      bn_dx_v4<<<nb, kThreads, 0, st>>>(reinterpret_cast<const float4*>(x), reinterpret_cast<const float4*>(dy),
-                                        n / 4, rows, C, gamma, beta, stats, coef, reinterpret_cast<float4*>(dx),
-                                        accumulate, relu, part);
-      if (dbias) colred_stage2<<<stage2_blocks(C), kStage2Threads, 0, st>>>(part, nb, C, BiasFin{dbias});
-    } else {
-      bn_dx_scalar<<<blocks_for(n), kThreads, 0, st>>>(x, dy, n, rows, C, gamma, beta, stats, coef, dx, accumulate,
-                                                       relu);
+  return bn_bwd_dx(x, dy, rows, C, gamma, beta, stats, relu, dx, accumulate, red_scratch, st, dbias);
+}
+
+// ---------------------------------------------------------------------------
+// BN backward statistics of a BN whose ReLU output feeds a 3x3 / stride 2 /
+// pad 1 max pool with saved argmax (H = 2P, W = 2Q) -- the stem's: one pass
+// over 2 x 2 pixel blocks (thread item = a run of kPbRun blocks along a pool
+// row x channel quad; windows two neighbouring blocks share load once) taking dy either gathered from the pool output's
+// gradient and the argmax (GATHER: the pool backward fused in, its output
+// never written) or read from the materialised pool-input gradient.  The
+// gathered values are the same picks, summed from +0 in the same order, as
+// pool_max_bwd_k3s2 writes, so both variants give the same bits.  Per-thread
+// sums (a fixed channel quad: the grid stride is a multiple of C/4) are
+// combined per block in thread order into part[block][2][C] doubles, then by
+// colred_stage2 in block order (deterministic).
+constexpr int kPbThreads = 256;
+
+constexpr int kPbRun = 8;  // 2 x 2 blocks per thread item (a run along the pool row)
+constexpr int kPbBlocks = 2 * 148;  // one wave on a B200 at 2 blocks / SM (fixed: it sets the summation order)
+static_assert(kPbBlocks <= kRedChunks, "partials fit the reduction scratch");
+
+template <bool GATHER>
+__global__ void __launch_bounds__(kPbThreads, 2) pool_bn_stats_kernel(  // kPbBlocks: one wave
+    PoolShape s, const uchar4* __restrict__ arg, const float4* __restrict__ dyp, const float4* __restrict__ dym,
+    const float4* __restrict__ x, const float* __restrict__ stats, const float* __restrict__ gamma,
+    const float* __restrict__ beta, int relu, int items, double* part) {
+  __shared__ float4 sh[kPbThreads];
+  const int C4 = s.C >> 2;
+  const int runs = (s.Q + kPbRun - 1) / kPbRun;
+  const int stride = gridDim.x * blockDim.x;  // a multiple of C4
+  const int i0 = blockIdx.x * blockDim.x + threadIdx.x;
+  const int c4 = i0 % C4;
+  const RedBnBwdOp op{nullptr, nullptr, stats, gamma, beta, relu, nullptr, 0, nullptr};
+  const Bn4 p = op.prep4(c4 * 4, s.C);
+  float4 a = zero4(), b = zero4();
+  const uchar4 none = make_uchar4(255, 255, 255, 255);
+  for (int i = i0; i < items; i += stride) {
+    int t = i / C4;
+    const int run = t % runs;
+    t /= runs;
+    const int m = t % s.P;
+    const int n = t / s.P;
+    const int k0 = run * kPbRun, k1e = min(s.Q, k0 + kPbRun);
+    const bool m1 = m + 1 < s.P;
+    const int64_t wrow = (static_cast<int64_t>(n) * s.P + m) * s.Q;  // window (m, 0)
+    // windows (m, k), (m + 1, k) carried from the previous block's right-hand pair
+    uchar4 a00 = none, a10 = none;
+    float4 g00 = zero4(), g10 = zero4();
+    if (GATHER) {
+      a00 = arg[(wrow + k0) * C4 + c4];
+      g00 = dyp[(wrow + k0) * C4 + c4];
+      if (m1) {
+        a10 = arg[(wrow + s.Q + k0) * C4 + c4];
+        g10 = dyp[(wrow + s.Q + k0) * C4 + c4];
+      }
+    }
+    for (int k = k0; k < k1e; ++k) {
+      float4 o[4];
+      const int64_t r0 = ((static_cast<int64_t>(n) * s.H + 2 * m) * s.W + 2 * k) * C4 + c4;
+      const int64_t r1 = r0 + static_cast<int64_t>(s.W) * C4;
+      if (GATHER) {
+        const bool k1 = k + 1 < s.Q;
+        uchar4 a01 = none, a11 = none;
+        float4 g01 = zero4(), g11 = zero4();
+        if (k1) {
+          a01 = arg[(wrow + k + 1) * C4 + c4];
+          g01 = dyp[(wrow + k + 1) * C4 + c4];
+          if (m1) {
+            a11 = arg[(wrow + s.Q + k + 1) * C4 + c4];
+            g11 = dyp[(wrow + s.Q + k + 1) * C4 + c4];
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) o[q] = zero4();
+#define SN_PICK(A, G, OFF, ACC)        \
+  ACC.x += (A.x == (OFF)) ? G.x : 0.f; \
+  ACC.y += (A.y == (OFF)) ? G.y : 0.f; \
+  ACC.z += (A.z == (OFF)) ? G.z : 0.f; \
+  ACC.w += (A.w == (OFF)) ? G.w : 0.f;
+        SN_PICK(a00, g00, 4, o[0]);
+        SN_PICK(a00, g00, 5, o[1]); SN_PICK(a01, g01, 3, o[1]);
+        SN_PICK(a00, g00, 7, o[2]); SN_PICK(a10, g10, 1, o[2]);
+        SN_PICK(a00, g00, 8, o[3]); SN_PICK(a01, g01, 6, o[3]);
+        SN_PICK(a10, g10, 2, o[3]); SN_PICK(a11, g11, 0, o[3]);
+#undef SN_PICK
+        a00 = a01, g00 = g01, a10 = a11, g10 = g11;
+      } else {
+        o[0] = dym[r0];
+        o[1] = dym[r0 + C4];
+        o[2] = dym[r1];
+        o[3] = dym[r1 + C4];
+      }
+      const float4 xv[4] = {x[r0], x[r0 + C4], x[r1], x[r1 + C4]};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float4 fa, fb;
+        op.comp(p, RedBnBwdOp::R{o[q], xv[q]}, fa, fb);
+        add4(a, fa);
+        add4(b, fb);
+      }
     }
   }
+  // block combination: thread t holds quad t % C4 (kPbThreads % C4 == 0)
+  for (int plane = 0; plane < 2; ++plane) {
+    sh[threadIdx.x] = plane ? b : a;
+    __syncthreads();
+    for (int q = threadIdx.x; q < C4; q += blockDim.x) {
+      double acc[4] = {0, 0, 0, 0};
+      for (int tt = q; tt < static_cast<int>(blockDim.x); tt += C4) {
+        const float4 w = sh[tt];
+        acc[0] += w.x; acc[1] += w.y; acc[2] += w.z; acc[3] += w.w;
+      }
+      double* dst = part + (static_cast<size_t>(blockIdx.x) * 2 + plane) * s.C + q * 4;
+      for (int e = 0; e < 4; ++e) dst[e] = acc[e];
+    }
+    __syncthreads();
+  }
+}
+
+bool pool_bn_stats_ok(const PoolShape& ps, int bn_C) {
+  return pool_bwd_argmax_only(ps) && ps.C == bn_C && ps.C % 4 == 0 && kPbThreads % (ps.C / 4) == 0 &&
+         static_cast<int64_t>(ps.N) * ps.P * ((ps.Q + kPbRun - 1) / kPbRun) * (ps.C / 4) < (int64_t(1) << 31);
+}
+
+cudaError_t bn_bwd_pool_stats(const PoolShape& ps, const uint8_t* argmax, const float* dy_pool, const float* dy_mat,
+                              const float* x, int C, const float* gamma, const float* beta, const float* stats,
+                              int relu, float* dgamma, float* dbeta, float* red_scratch, cudaStream_t st) {
+  if (!pool_bn_stats_ok(ps, C)) return cudaErrorInvalidValue;
+  const int items = ps.N * ps.P * ((ps.Q + kPbRun - 1) / kPbRun) * (C / 4);
+  const int nb = (items + kPbThreads - 1) / kPbThreads;
+  const int grid = nb < 1 ? 1 : (nb > kPbBlocks ? kPbBlocks : nb);
+  double* part = reinterpret_cast<double*>(red_scratch);
+  float* coef = bn_coef_ptr(red_scratch, C);
+  const uchar4* arg = reinterpret_cast<const uchar4*>(argmax);
+  if (dy_mat) {
+    pool_bn_stats_kernel<false><<<grid, kPbThreads, 0, st>>>(ps, arg, nullptr, reinterpret_cast<const float4*>(dy_mat),
+                                                             reinterpret_cast<const float4*>(x), stats, gamma, beta,
+                                                             relu, items, part);
+  } else {
+    if (!argmax || !dy_pool) return cudaErrorInvalidValue;
+    pool_bn_stats_kernel<true><<<grid, kPbThreads, 0, st>>>(ps, arg, reinterpret_cast<const float4*>(dy_pool), nullptr,
+                                                            reinterpret_cast<const float4*>(x), stats, gamma, beta,
+                                                            relu, items, part);
+  }
+  colred_stage2<<<stage2_blocks(C), kStage2Threads, 0, st>>>(part, grid, C, BnBwdFin{C, dgamma, dbeta, coef});
   return cudaGetLastError();
 }
 

@@ -600,14 +600,36 @@ def test_stem_bn_dx_fused_into_stem_wgrad_is_bit_identical(cuda, monkeypatch):
     """The stem BN's dx pass folded into the stem weight gradient (dx formed
     from the BN input and dy inside the kernel, never written) equals the
     materialised path bit for bit, with every other fusion on, and launches
-    one kernel fewer."""
+    one kernel fewer; gathering dy from the stem max pool's gradient and
+    argmax (the pool backward dropped) saves one more, same bits."""
     from paper_1801_04380_b200.netgen import gen_resnet
     from paper_1801_04380_b200.training import init_parameters
     net = gen_resnet(3, 4, 6, 3)
     params = init_parameters(net, seed=2, head_scale=0.1)
     images, labels = _inputs(net, 8)
     loss, grads, _, t = _run(net, 8, 4 << 30, ALL, params, images, labels)
+    monkeypatch.setenv("SN_FUSE_POOL_GATHER", "0")
+    loss1, grads1, _, t1 = _run(net, 8, 4 << 30, ALL, params, images, labels)
     monkeypatch.setenv("SN_FUSE_STEM_BN", "0")
     loss0, grads0, _, t0 = _run(net, 8, 4 << 30, ALL, params, images, labels)
-    assert t.kernels == t0.kernels - 1
+    assert t1.kernels == t0.kernels - 1
+    assert loss1 == loss0 and _bitwise(grads1, grads0)
+    # and the stem pool backward gathered into both (the pool's dx never written)
+    assert t.kernels == t1.kernels - 1
+    assert loss == loss1 and _bitwise(grads, grads1)
+
+
+@pytest.mark.parametrize("feats", ["liveness", "liveness,recompute=memory", "liveness,offload,cache"])
+def test_stem_pool_gather_bit_identical_across_schedules(cuda, monkeypatch, feats):
+    """The pool-ordered stem BN statistics give the same bits whether dy is
+    gathered (pool backward dropped) or read from the materialised pool dx,
+    under schedules that allow the gather and schedules that do not."""
+    from paper_1801_04380_b200.netgen import gen_resnet
+    from paper_1801_04380_b200.training import init_parameters
+    net = gen_resnet(3, 4, 6, 3)
+    params = init_parameters(net, seed=5, head_scale=0.1)
+    images, labels = _inputs(net, 8)
+    loss, grads, _, _ = _run(net, 8, 4 << 30, feats, params, images, labels)
+    monkeypatch.setenv("SN_FUSE_POOL_GATHER", "0")
+    loss0, grads0, _, _ = _run(net, 8, 4 << 30, feats, params, images, labels)
     assert loss == loss0 and _bitwise(grads, grads0)
