@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(kHaloFwdThreads, 1)
                         const __grid_constant__ CUtensorMap tmY, HaloArgs a) {
   using L = HaloSmem<BN, MT, HST, BST, CG>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   uint8_t* sH = smem;                                   // HST halo slots
   uint8_t* sB = smem + HST * a.halo_slot;               // BST weight tiles
   uint8_t* sEpi = sB + BST * L::B_BYTES;                // 2 x 16 KB store staging
@@ -581,7 +581,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
     tc_conv_halo_wgrad64(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmDY,
                          HaloWgArgs a) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   const uint32_t stage_bytes = 2 * a.xslot + 2 * a.dyslot;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kWgStages * stage_bytes);
   uint64_t* empty = full + kWgStages;
@@ -828,7 +828,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
     tc_conv_halo_wgrad128(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmDY,
                           HaloWg128Args a) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   const uint32_t stage_bytes = 8 * a.slot;  // 4 x chunks, 4 dy chunks
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kWg128Stages * stage_bytes);
   uint64_t* empty = full + kWg128Stages;

@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   static_assert(CG == 1 || MODE <= 1, "CTA pairs: forward / dgrad (MODE 0) and wgrad (MODE 1) only");
   using L = TmaSmem<BN, STAGES, CG>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * L::A_BYTES;
   const uint32_t sEpi = smem_u32(smem + L::EPI_OFF);
@@ -739,9 +739,18 @@ void set_conv_bn(int bn) { g_bn_force = bn; }
 int conv_bn_force() { return g_bn_force; }
 int conv_pairs_mode() { return pairs_mode(); }
 
+constexpr int kStemRT = 4;  // stem forward: output rows per tile
+// the stem forward's rows kernel: <= 64 channels, one 8-tap block per filter row, R <= 8
+bool stem_rows_fwd_ok(const ConvShape& s) { return s.K <= 64 && (s.S + 7) / 8 == 1 && s.R <= 8; }
+
 int conv_fwd_stats_tiles(const ConvShape& s, bool stem, int* tile_rows) {
   if (stem) {
-    *tile_rows = s.Q;
+    if (stem_rows_fwd_ok(s)) {  // one tile per kStemRT output rows (contiguous: P % kStemRT == 0)
+      if (s.P % kStemRT != 0) return 0;
+      *tile_rows = kStemRT * s.Q;
+      return s.N * s.P / kStemRT;
+    }
+    *tile_rows = s.Q;  // generic path: one 128-row tile per output row
     return s.N * s.P;
   }
   if (!use_tma()) return 0;
@@ -997,21 +1006,21 @@ namespace {
 // that uses it -- (RT-1)*stride + R row loads per RT output rows instead of
 // R per row, and no per-tile weight traffic (the 1-row kernel was bound by
 // its L2 -> SMEM operand traffic).
-constexpr int kStemRT = 4;
 constexpr int kStemRing = 6;
 constexpr int kStemThreads = 320;  // producer (warp 4), MMA (warp 5), two epilogue groups (warps 0-3, 6-9)
 struct StemRowsArgs {
   int N, P, Q, R, stride, K, rows_in;  // rows_in = (RT-1)*stride + R input rows per tile
   int tiles;                           // N * ceil(P / RT)
   const float* bias;
-  float* stats;                        // [N*P][3][K] tile statistics (tile = output row), or null
+  float* stats;                        // [N*P/RT][3][K] tile statistics (tile = RT output rows), or null
+  float* y;                            // output [N][P][Q][K]
 };
 
 __global__ void __launch_bounds__(kStemThreads, 1)
     stem_rows_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW,
                      const __grid_constant__ CUtensorMap tmD, StemRowsArgs a) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   constexpr int A_BYTES = kBM * 128, W_BYTES = 64 * 128;
   uint8_t* sA = smem;                                  // kStemRing input-row views
   uint8_t* sW = sA + kStemRing * A_BYTES;              // R weight k-blocks (resident)
@@ -1023,8 +1032,11 @@ __global__ void __launch_bounds__(kStemThreads, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   float* sred = reinterpret_cast<float*>(tmem_slot + 4);
+  sred += (4u - ((smem_u32(sred) >> 2) & 3u)) & 3u;  // 16-byte aligned (float4 shift stores)
+  float* sbias = sred + 1152 + ((4u - ((smem_u32(sred + 1152) >> 2) & 3u)) & 3u);  // [64], 16-byte aligned
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int bands = (a.P + kStemRT - 1) / kStemRT;
+  if (a.bias && threadIdx.x < 64) sbias[threadIdx.x] = threadIdx.x < a.K ? a.bias[threadIdx.x] : 0.f;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStemRing; ++i) {
@@ -1106,78 +1118,122 @@ __global__ void __launch_bounds__(kStemThreads, 1)
       __syncwarp();
     }
   } else {
-    // two epilogue groups (warps 0-3, 6-9); group g drains the 32-column chunks of parity g
+    // two epilogue groups (warps 0-3, 6-9); group g drains output channels
+    // 32g .. 32g+31 of every row of the tile.  Per row: TMEM -> registers ->
+    // swizzled staging (one barrier), then thread (cq = t & 7, rg = t >> 3)
+    // reads back column quad cq of rows 8rg .. 8rg+7 and uses each value twice:
+    // a coalesced global store (a warp instruction writes 4 whole 128-byte
+    // rows) and the BN statistics, accumulated in registers over the tile's
+    // kStemRT output rows against the tile's first pixel (the shift).  The
+    // four warps' partials meet in one of two sred slots once per tile; warp 0
+    // combines them after the next barrier.  No async-proxy fence, no
+    // bulk-store wait, one barrier per staged chunk.
     const int grp = warp >= 6 ? 1 : 0, q4 = warp & 3;
     const uint32_t row = q4 * 32 + lane;
-    const bool leader = q4 == 0 && lane == 0;
     const uint32_t bar_id = 1 + grp;
+    const int et = q4 * 32 + lane, cq = et & 7, rg = et >> 3;
+    const int c = 32 * grp;
     uint8_t* sEpiG = sEpi + grp * 2 * (kBM * 128);
-    float* sredG = sred + grp * 256;
+    float* sredG = sred + grp * 576;  // [2 slots][4 warps x 32 columns x 2 partials, 32 shifts]
+    const bool col_ok = c + 4 * cq < a.K;
     int local = 0;
     uint32_t chunk_no = 0;
+    bool pend = false;  // the previous tile's statistics still to be combined by warp 0
+    int pt = 0, pslot = 0;
+    auto finish_stats = [&](uint32_t slot, int tile) {
+      if (q4 != 0) return;
+      const float* sr = sredG + slot * 288;
+      float t1 = sr[lane * 2], t2 = sr[lane * 2 + 1];
+      for (int w = 1; w < 4; ++w) {
+        t1 += sr[(w * 32 + lane) * 2];
+        t2 += sr[(w * 32 + lane) * 2 + 1];
+      }
+      if (c + lane < a.K) {
+        float* out = a.stats + static_cast<size_t>(tile) * 3 * a.K + c + lane;
+        out[0] = sr[256 + lane];
+        out[a.K] = t1;
+        out[2 * static_cast<size_t>(a.K)] = t2;
+      }
+    };
     for (int t = blockIdx.x; t < a.tiles; t += gridDim.x, ++local) {
       const int n = t / bands, p0 = (t - n * bands) * kStemRT;
       const int acc = local & 1;
       mbar_wait(&tfull[acc], (local >> 1) & 1);
       tc_fence_after();
-      int ci = 0;
+      if (c >= a.K) {  // this group has no channels: release the accumulator
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+        continue;
+      }
+      float4 sh = make_float4(0.f, 0.f, 0.f, 0.f), sa = sh, sq = sh;
       for (int i = 0; i < kStemRT; ++i) {
         const int p = p0 + i;
-        const uint32_t tbase = tmem + static_cast<uint32_t>((acc * kStemRT + i) * 64) +
-                               (static_cast<uint32_t>(q4 * 32) << 16);
-#pragma unroll 1
-        for (int c = 0; c < 64; c += 32) {
-          if (c >= a.K) break;
-          if ((ci++ & 1) != grp) continue;
-          float v[32];
-          tmem_ld32(tbase + static_cast<uint32_t>(c), v);
-          if (a.bias) {
-            if (c + 32 <= a.K) {
-              const float4* b4 = reinterpret_cast<const float4*>(a.bias + c);
+        float v[32];
+        tmem_ld32(tmem + static_cast<uint32_t>((acc * kStemRT + i) * 64 + c) + (static_cast<uint32_t>(q4 * 32) << 16),
+                  v);
+        if (i == kStemRT - 1) {  // the accumulator is drained: the MMA may reuse it
+          tc_fence_before();
+          mbar_arrive(&tempty[acc]);
+        }
+        if (a.bias) {  // staged in shared memory (zero past K)
+          const float4* b4 = reinterpret_cast<const float4*>(sbias + c);
 #pragma unroll
-              for (int q = 0; q < 8; ++q) {
-                const float4 bq = __ldg(b4 + q);
-                v[4 * q] += bq.x; v[4 * q + 1] += bq.y; v[4 * q + 2] += bq.z; v[4 * q + 3] += bq.w;
-              }
-            } else {
+          for (int q = 0; q < 8; ++q) {
+            const float4 bq = b4[q];
+            v[4 * q] += bq.x; v[4 * q + 1] += bq.y; v[4 * q + 2] += bq.z; v[4 * q + 3] += bq.w;
+          }
+        }
+        const uint32_t slot = chunk_no & 1u;
+        uint8_t* sb = sEpiG + slot * (kBM * 128);
+        const uint32_t buf = smem_u32(sb);
 #pragma unroll
-              for (int q = 0; q < 32; ++q)
-                if (c + q < a.K) v[q] += __ldg(a.bias + c + q);
-            }
-          }
-          const uint32_t buf = smem_u32(sEpiG) + (chunk_no & 1u) * (kBM * 128);
-          if (leader) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-          named_bar(bar_id, 128);
+        for (int q = 0; q < 8; ++q)
+          asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(buf + sw128_off(row, q)), "f"(v[4 * q]),
+                       "f"(v[4 * q + 1]), "f"(v[4 * q + 2]), "f"(v[4 * q + 3])
+                       : "memory");
+        // staged; the previous tile's statistics partials are visible; the
+        // buffer written two chunks ago is no longer read
+        named_bar(bar_id, 128);
+        if (pend) finish_stats(pslot, pt);
+        pend = false;
+        ++chunk_no;
+        if (p >= a.P) continue;
+        float4 u[8];
 #pragma unroll
-          for (int q = 0; q < 8; ++q)
-            asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(buf + sw128_off(row, q)), "f"(v[4 * q]),
-                         "f"(v[4 * q + 1]), "f"(v[4 * q + 2]), "f"(v[4 * q + 3])
-                         : "memory");
-          fence_proxy_async();
-          named_bar(bar_id, 128);
-          if (leader && p < a.P) {
-            tma_store_4d(&tmD, buf, c, 0, p, n);
-            bulk_commit();
+        for (int j = 0; j < 8; ++j) u[j] = *reinterpret_cast<const float4*>(sb + sw128_off(rg * 8 + j, cq));
+        if (i == 0) sh = *reinterpret_cast<const float4*>(sb + sw128_off(0, cq));
+        float* yrow = a.y + ((static_cast<size_t>(n) * a.P + p) * a.Q) * a.K + c + 4 * cq;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int r = rg * 8 + j;
+          if (r < a.Q) {
+            if (col_ok) *reinterpret_cast<float4*>(yrow + static_cast<size_t>(r) * a.K) = u[j];
+            const float d0 = u[j].x - sh.x, d1 = u[j].y - sh.y, d2 = u[j].z - sh.z, d3 = u[j].w - sh.w;
+            sa.x += d0; sa.y += d1; sa.z += d2; sa.w += d3;
+            sq.x = fmaf(d0, d0, sq.x); sq.y = fmaf(d1, d1, sq.y); sq.z = fmaf(d2, d2, sq.z); sq.w = fmaf(d3, d3, sq.w);
           }
-          if (a.stats && p < a.P) {
-            const uint8_t* sb = sEpiG + (chunk_no & 1u) * (kBM * 128);
-            float shift, t1, t2;
-            const int Q = a.Q;
-            chunk_column_stats(sb, [Q](int r) { return r < Q; }, sredG, shift, t1, t2, bar_id);
-            if (q4 == 0 && c + lane < a.K) {
-              float* out = a.stats + (static_cast<size_t>(n) * a.P + p) * 3 * a.K + c + lane;
-              out[0] = shift;
-              out[a.K] = t1;
-              out[2 * static_cast<size_t>(a.K)] = t2;
-            }
-          }
-          ++chunk_no;
         }
       }
-      tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      if (a.stats) {
+#pragma unroll
+        for (int off = 8; off <= 16; off <<= 1) {
+          sa.x += __shfl_xor_sync(0xffffffffu, sa.x, off); sa.y += __shfl_xor_sync(0xffffffffu, sa.y, off);
+          sa.z += __shfl_xor_sync(0xffffffffu, sa.z, off); sa.w += __shfl_xor_sync(0xffffffffu, sa.w, off);
+          sq.x += __shfl_xor_sync(0xffffffffu, sq.x, off); sq.y += __shfl_xor_sync(0xffffffffu, sq.y, off);
+          sq.z += __shfl_xor_sync(0xffffffffu, sq.z, off); sq.w += __shfl_xor_sync(0xffffffffu, sq.w, off);
+        }
+        if (lane < 8) {
+          float* o = sredG + (local & 1) * 288 + (q4 * 32 + 4 * cq) * 2;
+          o[0] = sa.x; o[1] = sq.x; o[2] = sa.y; o[3] = sq.y; o[4] = sa.z; o[5] = sq.z; o[6] = sa.w; o[7] = sq.w;
+          if (q4 == 0) *reinterpret_cast<float4*>(sredG + (local & 1) * 288 + 256 + 4 * cq) = sh;
+        }
+        pend = true;
+        pt = t;
+        pslot = local & 1;
+      }
     }
-    if (leader) bulk_wait_all();
+    named_bar(bar_id, 128);
+    if (pend) finish_stats(pslot, pt);
   }
   __syncthreads();
   if (warp == 5) {
@@ -1195,7 +1251,7 @@ cudaError_t conv_stem_fwd(const ConvShape& s, const float* xp, const float* w, f
   stem_weights_kernel<<<148, 256, 0, st>>>(const_cast<float*>(w), wp_scratch, s.K, s.R, s.S, Sp, 1);
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return err;
-  if (s.K <= 64 && g.sblocks == 1 && s.R <= 8) {
+  if (stem_rows_fwd_ok(s)) {
     CUtensorMap A, W, D;
     if (!make_stem_view(&A, xp, g, kBM, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;
     if (!make_tiled(&W, wp_scratch, s.K, s.R * Sp * 4, 64, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;
@@ -1211,7 +1267,8 @@ cudaError_t conv_stem_fwd(const ConvShape& s, const float* xp, const float* w, f
     ra.tiles = s.N * ((s.P + kStemRT - 1) / kStemRT);
     ra.bias = bias;
     ra.stats = stats;
-    const int smem = kStemRing * kBM * 128 + s.R * 64 * 128 + 4 * kBM * 128 + 512 + 2048 + 1024;
+    ra.y = y;
+    const int smem = kStemRing * kBM * 128 + s.R * 64 * 128 + 4 * kBM * 128 + 512 + 4608 + 272 + 1024;
     static int attr_smem = 0;  // the filter's share depends on R: raise the opt-in when a larger one comes
     if (smem > attr_smem) {
       err = cudaFuncSetAttribute(stem_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1319,7 +1376,7 @@ __global__ void __launch_bounds__(kSwThreads, 1)
                            const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmG,
                            const __grid_constant__ CUtensorMap tmM, StemWgArgs a) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   constexpr bool FUSED = MODE >= 1, GATHER = MODE == 2;
   static_assert(kSwG == 2, "warps 0-3 walk the k block's 2 rows as 2 x 2 pixel blocks");
   // box slots per stage (stride <= 2); GATHER: x in the B slots, then the pool windows

@@ -112,8 +112,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     tc_gemm_kernel(LA la, LB lb, EPI epi, int num_kb, int kb_per_split) {
   using L = GemmSmem<BN, STAGES, SPLIT3>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * L::A_BYTES;
   uint8_t* sA_lo = smem + L::LO_OFF;  // SPLIT3 only

@@ -11,6 +11,7 @@
 
 #include "bn_math.cuh"
 #include "kernels.hpp"
+#include "tc_common.cuh"
 
 namespace sn {
 namespace {
@@ -341,6 +342,129 @@ __global__ void __launch_bounds__(kStage2Threads) colred_stage2(const double* __
   }
 }
 
+// BN backward statistics (RedBnBwdOp), bulk-copy pipelined: block b owns the
+// contiguous rows [b*chunk, (b+1)*chunk) of dy and x; one producer thread
+// streams them through a kCbStages-deep shared-memory ring with 1D bulk
+// copies (8 KB per operand per stage), 8 consumer warps reduce from shared
+// memory.  The loop-carried load latency the register version exposes (one
+// 512-thread block per SM, loads then math per iteration: ~3 TB/s) is gone.
+// Position e of a stage always holds channel quad e % C4 (stages hold whole
+// numbers of rows' worth of quads: 512 % C4 == 0), consumer t reads positions
+// t and t + 256; per-position float sums, then per quad in position order in
+// double: a fixed order.
+constexpr int kCbConsumers = 256;
+constexpr int kCbThreads = kCbConsumers + 32;
+constexpr int kCbStageF4 = 512;
+constexpr int kCbStages = 6;
+constexpr int kCbBlocks = 2 * 148;  // one wave at 2 blocks / SM
+static_assert(kCbBlocks <= kRedChunks, "partials fit the reduction scratch");
+constexpr int kCbSmem = kCbStages * 2 * kCbStageF4 * 16;
+
+bool colred_bulk_ok(int C) {
+  const int C4 = C / 4;
+  return C % 4 == 0 && C4 >= 1 && C4 <= kCbStageF4 && kCbStageF4 % C4 == 0;
+}
+
+__global__ void __launch_bounds__(kCbThreads, 2)
+    colred_bulk_bn_bwd(RedBnBwdOp op, int64_t rows, int C, int64_t chunk, double* part) {
+  extern __shared__ __align__(128) float4 ring[];  // [stage][dy, x][kCbStageF4]
+  __shared__ uint64_t full[kCbStages], empty[kCbStages];
+  const int C4 = C / 4;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * chunk;
+  const int64_t r1 = r0 + chunk < rows ? r0 + chunk : rows;
+  const int64_t f0 = r0 * C4, nf = (r1 - r0) * C4;  // float4 range of this block
+  const int nst = static_cast<int>((nf + kCbStageF4 - 1) / kCbStageF4);
+  const int t = threadIdx.x, warp = t >> 5;
+  if (t == 0) {
+    for (int i = 0; i < kCbStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kCbConsumers / 32);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const float4* dy4 = reinterpret_cast<const float4*>(op.dy);
+  const float4* x4 = reinterpret_cast<const float4*>(op.x);
+  float4 a0 = zero4(), b0 = zero4(), a1 = zero4(), b1 = zero4();
+  const int nq = C4 > kCbConsumers ? 2 : 1;  // distinct quads per consumer
+  if (warp == kCbConsumers / 32) {
+    if (t == kCbConsumers) {
+      for (int it = 0; it < nst; ++it) {
+        const int s = it % kCbStages;
+        if (it >= kCbStages) mbar_wait(&empty[s], ((it / kCbStages) - 1) & 1);
+        const int64_t off = f0 + static_cast<int64_t>(it) * kCbStageF4;
+        const int n = static_cast<int>(nf - static_cast<int64_t>(it) * kCbStageF4 < kCbStageF4
+                                           ? nf - static_cast<int64_t>(it) * kCbStageF4
+                                           : kCbStageF4);
+        mbar_arrive_expect_tx(&full[s], 2u * n * 16u);
+        bulk_load_1d(ring + (s * 2) * kCbStageF4, dy4 + off, n * 16u, &full[s]);
+        bulk_load_1d(ring + (s * 2 + 1) * kCbStageF4, x4 + off, n * 16u, &full[s]);
+      }
+    }
+  } else {
+    const typename RedBnBwdOp::P p0 = op.prep4((t % C4) * 4, C);
+    const typename RedBnBwdOp::P p1 = op.prep4(((t + kCbConsumers) % C4) * 4, C);
+    for (int it = 0; it < nst; ++it) {
+      const int s = it % kCbStages;
+      mbar_wait(&full[s], (it / kCbStages) & 1);
+      const int64_t off = f0 + static_cast<int64_t>(it) * kCbStageF4;
+      const int64_t left = nf - static_cast<int64_t>(it) * kCbStageF4;
+      const int n = static_cast<int>(left < kCbStageF4 ? left : kCbStageF4);
+      if (t < n) {
+        const RedBnBwdOp::R r{ring[(s * 2) * kCbStageF4 + t], ring[(s * 2 + 1) * kCbStageF4 + t]};
+        op.side((off + t) * 4, r);
+        float4 fa, fb;
+        op.comp(p0, r, fa, fb);
+        add4(a0, fa);
+        add4(b0, fb);
+      }
+      const int e = t + kCbConsumers;
+      if (e < n) {
+        const RedBnBwdOp::R r{ring[(s * 2) * kCbStageF4 + e], ring[(s * 2 + 1) * kCbStageF4 + e]};
+        op.side((off + e) * 4, r);
+        float4 fa, fb;
+        op.comp(p1, r, fa, fb);
+        if (nq == 2) {
+          add4(a1, fa);
+          add4(b1, fb);
+        } else {
+          add4(a0, fa);
+          add4(b0, fb);
+        }
+      }
+      __syncwarp();
+      if ((t & 31) == 0) mbar_arrive(&empty[s]);
+    }
+  }
+  __syncthreads();  // the ring is free: reuse it for the per-position sums
+  float4* sa = ring;                        // [nq * 256]
+  float4* sb = ring + 2 * kCbConsumers;     // [nq * 256]
+  if (t < kCbConsumers) {
+    sa[t] = a0;
+    sb[t] = b0;
+    if (nq == 2) {
+      sa[t + kCbConsumers] = a1;
+      sb[t + kCbConsumers] = b1;
+    }
+  }
+  __syncthreads();
+  const int ne = nq * kCbConsumers;
+  for (int q = t; q < C4; q += blockDim.x) {
+    double A[4] = {0, 0, 0, 0}, Bv[4] = {0, 0, 0, 0};
+    for (int e = q; e < ne; e += C4) {
+      const float4 u = sa[e], v = sb[e];
+      A[0] += u.x; A[1] += u.y; A[2] += u.z; A[3] += u.w;
+      Bv[0] += v.x; Bv[1] += v.y; Bv[2] += v.z; Bv[3] += v.w;
+    }
+    double* pa = part + (static_cast<size_t>(blockIdx.x) * 2) * C + q * 4;
+    double* pb = pa + C;
+    for (int i = 0; i < 4; ++i) {
+      pa[i] = A[i];
+      pb[i] = Bv[i];
+    }
+  }
+}
+
 // Blocks of stage 1: enough rows per thread (>= ~64 float4 per operand) that
 // the double partials stay small next to the input, at most kRedChunks.
 template <class Op, class Fin>
@@ -355,6 +479,20 @@ cudaError_t colred(Op op, Fin fin, int64_t rows, int C, float* scratch_f, cudaSt
   const int64_t chunk = (rows + nb - 1) / nb;
   nb = (rows + chunk - 1) / chunk;
   if (nb < 1) nb = 1;
+  if constexpr (std::is_same<Op, RedBnBwdOp>::value) {
+    if (colred_bulk_ok(C)) {
+      int64_t nbb = (rows * (C / 4) + kCbStageF4 * 8 - 1) / (kCbStageF4 * 8);  // >= 8 stages per block
+      nbb = nbb < 1 ? 1 : (nbb > kCbBlocks ? kCbBlocks : nbb);
+      const int64_t ck = (rows + nbb - 1) / nbb;
+      nbb = (rows + ck - 1) / ck;
+      const cudaError_t ea = cudaFuncSetAttribute(colred_bulk_bn_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  kCbSmem);
+      if (ea != cudaSuccess) return ea;
+      colred_bulk_bn_bwd<<<static_cast<int>(nbb), kCbThreads, kCbSmem, st>>>(op, rows, C, ck, part);
+      colred_stage2<<<stage2_blocks(C), kStage2Threads, 0, st>>>(part, static_cast<int>(nbb), C, fin);
+      return cudaGetLastError();
+    }
+  }
   // RedBnBwdOp (two operands + side copies per row): one 512-thread block per
   // SM without a register cap beats two capped ones (eager A/B over the step:
   // 9.47 vs 9.52 ms, SN_COLRED_ROWS experiment)
