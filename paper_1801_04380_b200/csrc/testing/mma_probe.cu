@@ -17,7 +17,8 @@ __device__ __forceinline__ void umma_f16(uint32_t d, uint64_t ad, uint64_t bd, u
       : "memory");
 }
 
-__global__ void __launch_bounds__(128, 1) mma_rate_kernel(int n, int kind, int iters, int accs, long long* cycles) {
+__global__ void __launch_bounds__(128, 1) mma_rate_kernel(int m, int n, int kind, int iters, int accs,
+                                                          long long* cycles) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 65536);
@@ -36,10 +37,10 @@ __global__ void __launch_bounds__(128, 1) mma_rate_kernel(int n, int kind, int i
   const uint32_t tmem = *slot;
   if (threadIdx.x == 0) {
     const uint32_t a0 = smem_u32(smem), b0 = smem_u32(smem + 16384);
-    const uint32_t idesc = kind == 0 ? idesc_tf32(128, n, false, false)
-                           : kind == 2 ? idesc_tf32(128, n, true, true)
+    const uint32_t idesc = kind == 0 ? idesc_tf32(m, n, false, false)
+                           : kind == 2 ? idesc_tf32(m, n, true, true)
                                      : ((1u << 4) | (0u << 7) | (0u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
-                                        (static_cast<uint32_t>(128 >> 4) << 24));
+                                        (static_cast<uint32_t>(m >> 4) << 24));
     uint64_t ad[4], bd[4];
     for (int kk = 0; kk < 4; ++kk) {
       if (kind == 2) {  // MN-major SW128_BASE32B, 32-row boxes (as the wgrad kernels)
@@ -75,17 +76,21 @@ __global__ void __launch_bounds__(128, 1) mma_rate_kernel(int n, int kind, int i
 }  // namespace
 }  // namespace sn
 
-extern "C" long long sn_probe_mma_rate(int n, int kind, int iters, int accs, int ctas) {
+extern "C" long long sn_probe_mma_rate_m(int m, int n, int kind, int iters, int accs, int ctas) {
   long long* d = nullptr;
   cudaMalloc(&d, sizeof(long long));
   cudaMemset(d, 0, sizeof(long long));
   const int smem = 65536 + 64 + 1024;
   cudaFuncSetAttribute(sn::mma_rate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  sn::mma_rate_kernel<<<ctas, 128, smem>>>(n, kind, iters, accs, d);
+  sn::mma_rate_kernel<<<ctas, 128, smem>>>(m, n, kind, iters, accs, d);
   long long h = -1;
   if (cudaDeviceSynchronize() == cudaSuccess) cudaMemcpy(&h, d, sizeof h, cudaMemcpyDeviceToHost);
   cudaFree(d);
   return h;
+}
+
+extern "C" long long sn_probe_mma_rate(int n, int kind, int iters, int accs, int ctas) {
+  return sn_probe_mma_rate_m(128, n, kind, iters, accs, ctas);
 }
 
 // TMEM layout of an M = 64 tf32 MMA (cta_group::1): A [64][32] and B [64][32]
