@@ -270,13 +270,24 @@ int sn_exec_step_host(sn_exec* ex, const float* images_host, const int32_t* labe
                       int32_t update, float* loss_host, sn_step_timing* timing);
 /* End-to-end with a one-batch input pipeline (the data layer's prefetch):
  * runs the step on images_host/labels_host and, while it computes, copies
- * next_images_host/next_labels_host (may be NULL) into a device staging
- * buffer.  A call whose images_host is the batch staged by the previous call
- * only waits for what is left of that copy; otherwise it stages it first.  The
- * next_* host buffers must stay unchanged until the following call returns. */
+ * next_images_host/next_labels_host (may be NULL) in: the images straight into
+ * the executor's input buffer as soon as this step's DATA layer has laid its
+ * own out, the labels into a staging buffer.  A call whose images_host is the
+ * batch staged by the previous call only waits for what is left of that copy;
+ * otherwise it stages it first.  The next_* host buffers must stay unchanged
+ * until the following call returns; other entry points (sn_exec_step,
+ * sn_exec_step_host, sn_exec_inputs) drop a staged batch. */
 int sn_exec_step_host_pipelined(sn_exec* ex, const float* images_host, const int32_t* labels_host,
                                 const float* next_images_host, const int32_t* next_labels_host, int32_t update,
                                 float* loss_host, sn_step_timing* timing);
+/* End to end over n host batches (images NHWC fp32, labels int32; pinned for
+ * overlap) in one call -- the reference's training loop (memsched
+ * run_training iterations) on the B200: batch k+1 is copied in while step k
+ * computes (as sn_exec_step_host_pipelined), and every step's loss is read
+ * back into losses[k] while the next step runs, so the device never idles on
+ * the host between steps.  timing->step_ms = device ms per step (mean). */
+int sn_exec_train_host(sn_exec* ex, int32_t n, const float* const* images_host, const int32_t* const* labels_host,
+                       int32_t update, float* losses, sn_step_timing* timing);
 /* Copy a layer's current forward output (if resident in the arena) or its
  * gradient buffer to device memory `dst`; used by parity tests. */
 int sn_exec_read_tensor(sn_exec* ex, int32_t kind, int32_t layer, float* dst, int64_t n_floats);

@@ -134,13 +134,18 @@ struct sn_exec {
   float* wt_w = nullptr;
   std::vector<cudaEvent_t> events;
   cudaEvent_t t_begin = nullptr, t_end = nullptr;
-  // pipelined host input (sn_exec_step_host_pipelined): the next batch is
-  // copied into a staging buffer on s4 while the current step computes
+  // pipelined host input (sn_exec_step_host_pipelined, sn_exec_train_host):
+  // the next batch's images are copied host -> device on s4 straight into
+  // `images` once the running iteration has consumed them (inputs_free_ev,
+  // recorded inside the iteration right after the DATA layer laid them out,
+  // or at its end when consumers read `images` in place); its labels (read by
+  // the loss) go to a staging buffer copied on s0 right before the iteration
   cudaStream_t s4 = nullptr;
-  float* images_stage = nullptr;
   int32_t* labels_stage = nullptr;
-  cudaEvent_t staged_ev = nullptr, consumed_ev = nullptr;
+  cudaEvent_t staged_ev = nullptr, consumed_ev = nullptr, inputs_free_ev = nullptr;
   const void* staged_src = nullptr;
+  float* loss_pinned = nullptr;  // [2] loss slots of consecutive steps (sn_exec_train_host)
+  cudaEvent_t loss_ev[2] = {nullptr, nullptr};
   // compiled program
   std::vector<Action> prog;
   int64_t kernels_per_step = 0;
@@ -1922,6 +1927,15 @@ struct Compiler {
     ex->dmalloc(&ex->partial_w, std::max<int64_t>(outside, 64) * 4, sn_exec::M_WGRAD, "cudaMalloc(partial_w)");
   }
 
+  // The iteration no longer reads `images` after this point: the host input
+  // pipeline may copy the next batch in (an external record inside a graph).
+  void inputs_consumed() {
+    cur_layer = -1, cur_type = 3;
+    cudaEvent_t ev = ex->inputs_free_ev;
+    cudaStream_t st = ex->s0;
+    push([=] { ck(record_timer(ev, st), "record inputs free"); }, 0);
+  }
+
   // DATA layer: lay the user's images out the way the consumers read them.
   void prepare_inputs() {
     const LayerRt& d = ex->L[data_id];
@@ -1947,6 +1961,8 @@ struct Compiler {
     plan_fusions();
     size_wgrad_scratch();
     prepare_inputs();
+    const bool images_in_place = ex->data_buf == ex->images;
+    if (!images_in_place) inputs_consumed();
     for (size_t ti = 0; ti < P.tape.size(); ++ti) {
       const snp::Event& ev = P.tape[ti];
       cur_ti = ti;
@@ -2021,6 +2037,7 @@ struct Compiler {
       }, 0);
     }
     if (ex->dp() && next_bucket != ex->buckets.size()) xfail(SN_EK_INTERNAL, "data-parallel buckets not all issued");
+    if (images_in_place) inputs_consumed();
     uint32_t* it = ex->iteration;
     push([=] { ck(sn::bump_iteration(it, s0), "bump"); }, 1);
     ex->final_keys = where;
@@ -2092,6 +2109,10 @@ void destroy(sn_exec* ex) {
   if (ex->t_end) cudaEventDestroy(ex->t_end);
   if (ex->staged_ev) cudaEventDestroy(ex->staged_ev);
   if (ex->consumed_ev) cudaEventDestroy(ex->consumed_ev);
+  if (ex->inputs_free_ev) cudaEventDestroy(ex->inputs_free_ev);
+  for (cudaEvent_t e : ex->loss_ev)
+    if (e) cudaEventDestroy(e);
+  if (ex->loss_pinned) cudaFreeHost(ex->loss_pinned);
   if (ex->s4) cudaStreamDestroy(ex->s4);
   if (!ex->opt.stash)
     for (auto& kv : ex->stash)
@@ -2104,7 +2125,7 @@ void destroy(sn_exec* ex) {
   if (ex->data_buf && ex->data_buf != ex->images) cudaFree(ex->data_buf);
   void* bufs[] = {ex->arena, ex->params, ex->grads, ex->state, ex->images, ex->labels, ex->loss_rows, ex->loss,
                   ex->iteration, ex->wt_scratch, ex->partial, ex->red, ex->tstats, ex->pool_scratch,
-                  ex->partial_w, ex->red_w, ex->wt_w, ex->images_stage, ex->labels_stage,
+                  ex->partial_w, ex->red_w, ex->wt_w, ex->labels_stage,
                   const_cast<float**>(ex->ptr_table), ex->marker, ex->update_flag};
   for (void* b : bufs)
     if (b) cudaFree(b);
@@ -2149,6 +2170,8 @@ int sn_exec_create(const sn_plan* plan, const sn_net_desc* /*net*/, const sn_lay
     ck(cudaStreamCreateWithFlags(&ex->s3, cudaStreamNonBlocking), "stream");
     ck(cudaEventCreate(&ex->t_begin), "event");
     ck(cudaEventCreate(&ex->t_end), "event");
+    ck(cudaEventCreateWithFlags(&ex->inputs_free_ev, cudaEventDisableTiming), "event");
+    ck(cudaEventRecord(ex->inputs_free_ev, ex->s0), "record");
     setup_layers(ex, numerics);
     if (ex->opt.autotune) autotune(ex);
     alloc_device(ex);
@@ -2208,8 +2231,17 @@ int sn_exec_param_slice(sn_exec* ex, int32_t layer, int64_t* w_off, int64_t* w_n
   return SN_OK;
 }
 
+// Entry points outside the host input pipeline drop a batch it staged for
+// the next pipelined call (its image copy into `images` finishes first).
+void drop_stage(sn_exec* ex) {
+  if (!ex->staged_src) return;
+  ck(cudaStreamSynchronize(ex->s4), "sync staged input");
+  ex->staged_src = nullptr;
+}
+
 int sn_exec_inputs(sn_exec* ex, float** images, int32_t** labels, int64_t* image_floats) {
   if (!ex) return xset(SN_EK_INTERNAL, "null argument");
+  if (const int rc = xguard([&] { drop_stage(ex); })) return rc;
   if (images) *images = ex->images;
   if (labels) *labels = ex->labels;
   if (image_floats) *image_floats = ex->image_floats;
@@ -2222,6 +2254,7 @@ int sn_exec_step(sn_exec* ex, int32_t update, float* loss_host, sn_step_timing* 
   if (!ex) return xset(SN_EK_INTERNAL, "null argument");
   return xguard([&] {
     ck(cudaSetDevice(ex->device), "cudaSetDevice");
+    drop_stage(ex);
     PrecisionScope prec(ex);
     if (ex->opt.use_graph) ensure_graph(ex);
     ck(cudaEventRecord(ex->t_begin, ex->s0), "record");
@@ -2254,6 +2287,7 @@ int sn_exec_step_host(sn_exec* ex, const float* images_host, const int32_t* labe
   const int rc = xguard([&] {
     ck(cudaSetDevice(ex->device), "cudaSetDevice");
     PrecisionScope prec(ex);
+    drop_stage(ex);
     if (ex->opt.use_graph) ensure_graph(ex);
     ck(cudaEventRecord(ex->t_begin, ex->s0), "record");
     ck(cudaMemcpyAsync(ex->images, images_host, ex->image_floats * sizeof(float), cudaMemcpyHostToDevice, ex->s0),
@@ -2283,6 +2317,61 @@ int sn_exec_step_host(sn_exec* ex, const float* images_host, const int32_t* labe
   return rc;
 }
 
+namespace {
+
+void ensure_input_pipeline(sn_exec* ex) {
+  if (ex->s4) return;
+  ck(cudaStreamCreateWithFlags(&ex->s4, cudaStreamNonBlocking), "stream");
+  ex->dmalloc(&ex->labels_stage, static_cast<int64_t>(ex->B * sizeof(int32_t)), sn_exec::M_INPUT,
+              "cudaMalloc(labels_stage)");
+  ck(cudaEventCreateWithFlags(&ex->staged_ev, cudaEventDisableTiming), "event");
+  ck(cudaEventCreateWithFlags(&ex->consumed_ev, cudaEventDisableTiming), "event");
+  ck(cudaEventRecord(ex->consumed_ev, ex->s0), "record");
+  ck(cudaHostAlloc(reinterpret_cast<void**>(&ex->loss_pinned), 2 * sizeof(float), cudaHostAllocDefault),
+     "cudaHostAlloc(loss)");
+  for (auto& e : ex->loss_ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+}
+
+// Copy a host batch in on s4: images straight into `images` after the last
+// launched iteration consumed its own, labels into the staging buffer after
+// the last iteration's copy of it.
+void stage_batch(sn_exec* ex, const float* img, const int32_t* lab) {
+  ck(cudaStreamWaitEvent(ex->s4, ex->inputs_free_ev, 0), "wait");
+  ck(cudaMemcpyAsync(ex->images, img, ex->image_floats * sizeof(float), cudaMemcpyHostToDevice, ex->s4),
+     "images H2D");
+  ck(cudaStreamWaitEvent(ex->s4, ex->consumed_ev, 0), "wait");
+  ck(cudaMemcpyAsync(ex->labels_stage, lab, ex->B * sizeof(int32_t), cudaMemcpyHostToDevice, ex->s4), "labels H2D");
+  ck(cudaEventRecord(ex->staged_ev, ex->s4), "record");
+  ex->staged_src = img;
+}
+
+// One iteration on the staged batch (s0), plus the SGD update.
+void launch_staged(sn_exec* ex, int32_t update) {
+  ck(cudaStreamWaitEvent(ex->s0, ex->staged_ev, 0), "wait");
+  ck(cudaMemcpyAsync(ex->labels, ex->labels_stage, ex->B * sizeof(int32_t), cudaMemcpyDeviceToDevice, ex->s0),
+     "labels D2D");
+  ck(cudaEventRecord(ex->consumed_ev, ex->s0), "record");
+  ex->staged_src = nullptr;
+  if (ex->dp()) ck(cudaMemsetAsync(ex->update_flag, update ? 1 : 0, 4, ex->s0), "update flag");
+  if (ex->opt.use_graph)
+    ck(cudaGraphLaunch(ex->gexec, ex->s0), "GraphLaunch");
+  else
+    run_program(ex);
+  if (update && !ex->dp())
+    ck(sn::sgd_update(ex->params, ex->grads, ex->n_params, ex->opt.lr, ex->opt.grad_scale, ex->s0), "sgd");
+}
+
+void fill_timing(sn_exec* ex, int32_t update, float ms, sn_step_timing* timing) {
+  if (!timing) return;
+  timing->step_ms = ms;
+  timing->kernels = ex->kernels_per_step + (update ? 1 : 0);
+  timing->d2h_bytes = ex->d2h_bytes;
+  timing->h2d_bytes = ex->h2d_bytes;
+  timing->arena_high_water = ex->plan->plan.report.pool_high_water_bytes;
+}
+
+}  // namespace
+
 int sn_exec_step_host_pipelined(sn_exec* ex, const float* images_host, const int32_t* labels_host,
                                 const float* next_images_host, const int32_t* next_labels_host, int32_t update,
                                 float* loss_host, sn_step_timing* timing) {
@@ -2291,51 +2380,55 @@ int sn_exec_step_host_pipelined(sn_exec* ex, const float* images_host, const int
     ck(cudaSetDevice(ex->device), "cudaSetDevice");
     PrecisionScope prec(ex);
     if (ex->opt.use_graph) ensure_graph(ex);
-    const size_t ibytes = ex->image_floats * sizeof(float), lbytes = ex->B * sizeof(int32_t);
-    if (!ex->s4) {
-      ck(cudaStreamCreateWithFlags(&ex->s4, cudaStreamNonBlocking), "stream");
-      ex->dmalloc(&ex->images_stage, static_cast<int64_t>(ibytes), sn_exec::M_INPUT, "cudaMalloc(images_stage)");
-      ex->dmalloc(&ex->labels_stage, static_cast<int64_t>(lbytes), sn_exec::M_INPUT, "cudaMalloc(labels_stage)");
-      ck(cudaEventCreateWithFlags(&ex->staged_ev, cudaEventDisableTiming), "event");
-      ck(cudaEventCreateWithFlags(&ex->consumed_ev, cudaEventDisableTiming), "event");
-      ck(cudaEventRecord(ex->consumed_ev, ex->s0), "record");
-    }
-    auto stage = [&](const float* img, const int32_t* lab) {
-      ck(cudaStreamWaitEvent(ex->s4, ex->consumed_ev, 0), "wait");
-      ck(cudaMemcpyAsync(ex->images_stage, img, ibytes, cudaMemcpyHostToDevice, ex->s4), "images H2D");
-      ck(cudaMemcpyAsync(ex->labels_stage, lab, lbytes, cudaMemcpyHostToDevice, ex->s4), "labels H2D");
-      ck(cudaEventRecord(ex->staged_ev, ex->s4), "record");
-      ex->staged_src = img;
-    };
+    ensure_input_pipeline(ex);
     ck(cudaEventRecord(ex->t_begin, ex->s0), "record");
-    if (ex->staged_src != images_host) stage(images_host, labels_host);  // first call of a run
-    ck(cudaStreamWaitEvent(ex->s0, ex->staged_ev, 0), "wait");
-    ck(cudaMemcpyAsync(ex->images, ex->images_stage, ibytes, cudaMemcpyDeviceToDevice, ex->s0), "images D2D");
-    ck(cudaMemcpyAsync(ex->labels, ex->labels_stage, lbytes, cudaMemcpyDeviceToDevice, ex->s0), "labels D2D");
-    ck(cudaEventRecord(ex->consumed_ev, ex->s0), "record");
-    ex->staged_src = nullptr;
-    // stage the next batch now: the loss read below is a pageable copy that
-    // blocks the host until the step is done
-    if (next_images_host && next_labels_host) stage(next_images_host, next_labels_host);
-    if (ex->dp()) ck(cudaMemsetAsync(ex->update_flag, update ? 1 : 0, 4, ex->s0), "update flag");
-    if (ex->opt.use_graph)
-      ck(cudaGraphLaunch(ex->gexec, ex->s0), "GraphLaunch");
-    else
-      run_program(ex);
-    if (update && !ex->dp())
-      ck(sn::sgd_update(ex->params, ex->grads, ex->n_params, ex->opt.lr, ex->opt.grad_scale, ex->s0), "sgd");
+    if (ex->staged_src != images_host) stage_batch(ex, images_host, labels_host);  // first call of a run
+    launch_staged(ex, update);
+    // stage the next batch now (it waits for this iteration's DATA layer)
+    if (next_images_host && next_labels_host) stage_batch(ex, next_images_host, next_labels_host);
     ck(cudaMemcpyAsync(loss_host, ex->loss, sizeof(float), cudaMemcpyDeviceToHost, ex->s0), "loss D2H");
     ck(cudaEventRecord(ex->t_end, ex->s0), "record");
     ck(cudaStreamSynchronize(ex->s0), "sync");
-    if (timing) {
-      float ms = 0.f;
-      ck(cudaEventElapsedTime(&ms, ex->t_begin, ex->t_end), "elapsed");
-      timing->step_ms = ms;
-      timing->kernels = ex->kernels_per_step + (update ? 1 : 0);
-      timing->d2h_bytes = ex->d2h_bytes;
-      timing->h2d_bytes = ex->h2d_bytes;
-      timing->arena_high_water = ex->plan->plan.report.pool_high_water_bytes;
+    float ms = 0.f;
+    if (timing) ck(cudaEventElapsedTime(&ms, ex->t_begin, ex->t_end), "elapsed");
+    fill_timing(ex, update, ms, timing);
+  });
+  return rc;
+}
+
+int sn_exec_train_host(sn_exec* ex, int32_t n, const float* const* images_host, const int32_t* const* labels_host,
+                       int32_t update, float* losses, sn_step_timing* timing) {
+  if (!ex || n < 0 || (n > 0 && (!images_host || !labels_host || !losses))) return xset(SN_EK_INTERNAL, "null argument");
+  if (n == 0) return SN_OK;
+  const int rc = xguard([&] {
+    ck(cudaSetDevice(ex->device), "cudaSetDevice");
+    PrecisionScope prec(ex);
+    if (ex->opt.use_graph) ensure_graph(ex);
+    ensure_input_pipeline(ex);
+    for (int i = 0; i < n; ++i)
+      if (!images_host[i] || !labels_host[i]) xfail(SN_EK_INTERNAL, "null batch pointer");
+    ck(cudaEventRecord(ex->t_begin, ex->s0), "record");
+    if (ex->staged_src != images_host[0]) stage_batch(ex, images_host[0], labels_host[0]);
+    for (int k = 0; k < n; ++k) {
+      launch_staged(ex, update);
+      if (k + 1 < n) stage_batch(ex, images_host[k + 1], labels_host[k + 1]);
+      // step k's loss lands in a pinned slot; the host reads step k-1's while
+      // step k runs, so the device never waits for the host between steps
+      ck(cudaMemcpyAsync(ex->loss_pinned + (k & 1), ex->loss, sizeof(float), cudaMemcpyDeviceToHost, ex->s0),
+         "loss D2H");
+      ck(cudaEventRecord(ex->loss_ev[k & 1], ex->s0), "record");
+      if (k >= 1) {
+        ck(cudaEventSynchronize(ex->loss_ev[(k - 1) & 1]), "sync loss");
+        losses[k - 1] = ex->loss_pinned[(k - 1) & 1];
+      }
     }
+    ck(cudaEventRecord(ex->t_end, ex->s0), "record");
+    ck(cudaEventSynchronize(ex->loss_ev[(n - 1) & 1]), "sync loss");
+    losses[n - 1] = ex->loss_pinned[(n - 1) & 1];
+    ck(cudaStreamSynchronize(ex->s0), "sync");
+    float ms = 0.f;
+    if (timing) ck(cudaEventElapsedTime(&ms, ex->t_begin, ex->t_end), "elapsed");
+    fill_timing(ex, update, ms / n, timing);
   });
   return rc;
 }

@@ -273,13 +273,13 @@ __global__ void splitk_group_kernel(float* P, int splits, int per, int64_t MN) {
     float* p = P + static_cast<size_t>(s0) * MN + e;
     float acc = *p;
     int s = s0 + 1;
-    for (; s + 3 < s1; s += 4) {
-      const float a0 = P[static_cast<size_t>(s) * MN + e], a1 = P[static_cast<size_t>(s + 1) * MN + e];
-      const float a2 = P[static_cast<size_t>(s + 2) * MN + e], a3 = P[static_cast<size_t>(s + 3) * MN + e];
-      acc += a0;
-      acc += a1;
-      acc += a2;
-      acc += a3;
+    // 8 loads in flight, summed in split order
+    for (; s + 7 < s1; s += 8) {
+      float a[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a[u] = P[static_cast<size_t>(s + u) * MN + e];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc += a[u];
     }
     for (; s < s1; ++s) acc += P[static_cast<size_t>(s) * MN + e];
     *p = acc;
@@ -287,46 +287,58 @@ __global__ void splitk_group_kernel(float* P, int splits, int per, int64_t MN) {
 }
 
 // sstride: distance between consecutive summed slices, in slices (1, or the
-// group size after splitk_group_kernel).
-__global__ void splitk_reduce_kernel(const float* __restrict__ P, int splits, int M, int N, float* D,
-                                     const float* bias, int accumulate, int transpose, int sstride) {
+// group size after splitk_group_kernel).  One thread per element of a 32 x 32
+// tile (1024 threads), the slices read 8 at a time and summed in split order:
+// the reduction is a chain of L2 loads, so what matters is how many are in
+// flight (the round-1 version walked 4 elements x all splits one load at a
+// time per thread: ~20 us for 148 slices of a 576 x 64 weight gradient).
+constexpr int kRedTileThreads = 1024;
+__global__ void __launch_bounds__(kRedTileThreads) splitk_reduce_kernel(const float* __restrict__ P, int splits, int M,
+                                                                        int N, float* D, const float* bias,
+                                                                        int accumulate, int transpose, int sstride) {
   __shared__ float tile[32][33];
   const int m0 = blockIdx.y * 32, n0 = blockIdx.x * 32;
-  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
-  for (int i = ty; i < 32; i += 8) {
-    const int m = m0 + i, n = n0 + tx;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 32
+  {
+    const int m = m0 + ty, n = n0 + tx;
     float acc = 0.f;
     if (m < M && n < N) {
       const size_t stride = static_cast<size_t>(M) * N * sstride;
       const float* p = P + static_cast<size_t>(m) * N + n;
-      for (int s = 0; s < splits; ++s) acc += p[s * stride];
+      int s = 0;
+      for (; s + 7 < splits; s += 8) {
+        float a[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) a[u] = p[(s + u) * stride];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc += a[u];
+      }
+      for (; s < splits; ++s) acc += p[s * stride];
       if (bias) acc += bias[n];
     }
-    tile[i][tx] = acc;
+    tile[ty][tx] = acc;
   }
   if (!transpose) {
-    for (int i = ty; i < 32; i += 8) {
-      const int m = m0 + i, n = n0 + tx;
-      if (m < M && n < N) {
-        float* d = D + static_cast<size_t>(m) * N + n;
-        *d = accumulate ? *d + tile[i][tx] : tile[i][tx];
-      }
+    const int m = m0 + ty, n = n0 + tx;
+    if (m < M && n < N) {
+      float* d = D + static_cast<size_t>(m) * N + n;
+      *d = accumulate ? *d + tile[ty][tx] : tile[ty][tx];
     }
     return;
   }
   __syncthreads();
-  for (int i = ty; i < 32; i += 8) {
-    const int n = n0 + i, m = m0 + tx;
+  {
+    const int n = n0 + ty, m = m0 + tx;
     if (m < M && n < N) {
       float* d = D + static_cast<size_t>(n) * M + m;
-      *d = accumulate ? *d + tile[tx][i] : tile[tx][i];
+      *d = accumulate ? *d + tile[tx][ty] : tile[tx][ty];
     }
   }
 }
 
 cudaError_t splitk_reduce_impl(const float* P, int splits, int M, int N, float* D, const float* bias, int accumulate,
                           int transpose, cudaStream_t st) {
-  dim3 grid((N + 31) / 32, (M + 31) / 32), block(32, 8);
+  dim3 grid((N + 31) / 32, (M + 31) / 32), block(32, 32);
   // Few output tiles and many splits: first sum groups of splits with the whole
   // GPU (in place), then reduce the group sums in order.
   const int64_t MN = static_cast<int64_t>(M) * N;
@@ -336,11 +348,14 @@ cudaError_t splitk_reduce_impl(const float* P, int splits, int M, int N, float* 
     groups = std::max(groups, 2);
     const int per = (splits + groups - 1) / groups;
     groups = (splits + per - 1) / per;
-    const int bx = static_cast<int>(std::min<int64_t>((MN + 255) / 256, 148 * 4 / groups + 1));
+    // one element per thread (the grid is small next to a wave only for tiny MN)
+    const int bx = static_cast<int>(std::min<int64_t>((MN + 255) / 256, 65535));
+    if (xskip(32)) return cudaSuccess;
     splitk_group_kernel<<<dim3(bx, groups), 256, 0, st>>>(const_cast<float*>(P), splits, per, MN);
     splitk_reduce_kernel<<<grid, block, 0, st>>>(P, groups, M, N, D, bias, accumulate, transpose, per);
     return cudaGetLastError();
   }
+  if (xskip(32)) return cudaSuccess;
   splitk_reduce_kernel<<<grid, block, 0, st>>>(P, splits, M, N, D, bias, accumulate, transpose, 1);
   return cudaGetLastError();
 }
@@ -506,7 +521,9 @@ cudaError_t conv_dgrad(const ConvShape& s, const float* dy, const float* w, floa
   if (use_tma() && conv_tma_ok_dgrad_strided(s)) return conv_dgrad_strided_tma(s, dy, w, wt, dx, accumulate, st);
   dim3 grid((s.C + 31) / 32, (s.K + 31) / 32, s.R * s.S), block(32, 8);
   const bool tma = use_tma() && conv_tma_ok_dgrad(s);
+  if (xskip(64)) return cudaSuccess;
   transpose_w_kernel<<<grid, block, 0, st>>>(w, wt, s.K, s.R * s.S, s.C, tma ? 1 : 0);
+  if (xskip(1024)) transpose_w_kernel<<<grid, block, 0, st>>>(w, wt, s.K, s.R * s.S, s.C, tma ? 1 : 0);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (tma) {

@@ -129,6 +129,14 @@ void set_conv_tma(int on);
 // around its own launches (sn_exec_options.precision).
 void set_precision(int p);
 int precision();
+// A/B measurement hook, SN_XSKIP bitmask.  Skipping bits (results are wrong,
+// and operand values change the power draw, so read step times with care):
+// 1 BN-backward finaliser, 2 BN dx bias finaliser, 4 BN-backward statistics
+// pass, 8 BN dx pass, 16 halo wgrad64, 32 split-K reductions, 64 weight
+// transposes, 128 BN forward tile statistics.  Doubling bits (idempotent
+// launches issued twice: the step-time delta is their real cost in the graph):
+// 512 every BN statistics finaliser, 1024 every weight transpose.
+int xskip(int bit);
 // CTA-pair (cta_group::2) conv kernels: 0 off, 1 when the shape keeps the
 // pairs busy (default; env SN_CONV_PAIRS=0 turns them off), 2 always (tests).
 void set_conv_pairs(int mode);

@@ -360,6 +360,16 @@ constexpr int kCbBlocks = 2 * 148;  // one wave at 2 blocks / SM
 static_assert(kCbBlocks <= kRedChunks, "partials fit the reduction scratch");
 constexpr int kCbSmem = kCbStages * 2 * kCbStageF4 * 16;
 
+// Row chunks of colred_bulk_bn_bwd: block b owns rows [b*ck, (b+1)*ck), at
+// least 8 ring stages per block, at most one wave.
+int64_t bulk_chunk(int64_t rows, int C, int* nblocks) {
+  int64_t nbb = (rows * (C / 4) + kCbStageF4 * 8 - 1) / (kCbStageF4 * 8);
+  nbb = nbb < 1 ? 1 : (nbb > kCbBlocks ? kCbBlocks : nbb);
+  const int64_t ck = (rows + nbb - 1) / nbb;
+  *nblocks = static_cast<int>((rows + ck - 1) / ck);
+  return ck;
+}
+
 bool colred_bulk_ok(int C) {
   const int C4 = C / 4;
   return C % 4 == 0 && C4 >= 1 && C4 <= kCbStageF4 && kCbStageF4 % C4 == 0;
@@ -481,15 +491,14 @@ cudaError_t colred(Op op, Fin fin, int64_t rows, int C, float* scratch_f, cudaSt
   if (nb < 1) nb = 1;
   if constexpr (std::is_same<Op, RedBnBwdOp>::value) {
     if (colred_bulk_ok(C)) {
-      int64_t nbb = (rows * (C / 4) + kCbStageF4 * 8 - 1) / (kCbStageF4 * 8);  // >= 8 stages per block
-      nbb = nbb < 1 ? 1 : (nbb > kCbBlocks ? kCbBlocks : nbb);
-      const int64_t ck = (rows + nbb - 1) / nbb;
-      nbb = (rows + ck - 1) / ck;
+      int nbb = 0;
+      const int64_t ck = bulk_chunk(rows, C, &nbb);
       const cudaError_t ea = cudaFuncSetAttribute(colred_bulk_bn_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                   kCbSmem);
       if (ea != cudaSuccess) return ea;
-      colred_bulk_bn_bwd<<<static_cast<int>(nbb), kCbThreads, kCbSmem, st>>>(op, rows, C, ck, part);
-      colred_stage2<<<stage2_blocks(C), kStage2Threads, 0, st>>>(part, static_cast<int>(nbb), C, fin);
+      if (!xskip(4)) colred_bulk_bn_bwd<<<static_cast<int>(nbb), kCbThreads, kCbSmem, st>>>(op, rows, C, ck, part);
+      if (!xskip(1)) colred_stage2<<<stage2_blocks(C), kStage2Threads, 0, st>>>(part, static_cast<int>(nbb), C, fin);
+      if (xskip(512)) colred_stage2<<<stage2_blocks(C), kStage2Threads, 0, st>>>(part, static_cast<int>(nbb), C, fin);
       return cudaGetLastError();
     }
   }
@@ -1766,7 +1775,11 @@ cudaError_t bn_stats_from_tiles(const float* tiles, int ntiles, int tile_rows, c
   nb = std::max(1, std::min({nb, (ntiles + 3) / 4, kRedChunks}));
   const int chunk = (ntiles + nb - 1) / nb;
   nb = (ntiles + chunk - 1) / chunk;
+  if (xskip(128)) return cudaSuccess;
   tile_stats_stage1<<<dim3(nb, cgroups), kThreads, 0, st>>>(tiles, ntiles, tile_rows, rows, C, x, chunk, part);
+  colred_stage2<<<stage2_blocks(C), kStage2Threads, 0, st>>>(part, nb, C,
+                                                          BnStatsFin{x, rows, C, eps, momentum, stats, running});
+  if (xskip(512))
   colred_stage2<<<stage2_blocks(C), kStage2Threads, 0, st>>>(part, nb, C,
                                                           BnStatsFin{x, rows, C, eps, momentum, stats, running});
   return cudaGetLastError();
@@ -1790,6 +1803,15 @@ cudaError_t grad_copy2(const float* src, float* d1, int acc1, float* d2, int acc
   return cudaGetLastError();
 }
 
+int xskip(int bit) {
+  static int mask = -1;
+  if (mask < 0) {
+    const char* v = std::getenv("SN_XSKIP");
+    mask = v ? std::atoi(v) : 0;
+  }
+  return (mask & bit) != 0;
+}
+
 bool bn_bwd_bias_ok(int C) { return C % 4 == 0 && kThreads % (C / 4) == 0; }
 
 cudaError_t bn_bwd_dx(const float* x, const float* dy, int64_t rows, int C, const float* gamma, const float* beta,
@@ -1805,10 +1827,10 @@ cudaError_t bn_bwd_dx(const float* x, const float* dy, int64_t rows, int C, cons
     double* part = dbias ? reinterpret_cast<double*>(red_scratch + static_cast<int64_t>(kRedChunks) * 2 * C * 2 +
                                                      ((2 * C + 63) / 64) * 64)
                          : nullptr;
-    bn_dx_v4<<<nb, kThreads, 0, st>>>(reinterpret_cast<const float4*>(x), reinterpret_cast<const float4*>(dy), n / 4,
+    if (!xskip(8)) bn_dx_v4<<<nb, kThreads, 0, st>>>(reinterpret_cast<const float4*>(x), reinterpret_cast<const float4*>(dy), n / 4,
                                       rows, C, gamma, beta, stats, coef, reinterpret_cast<float4*>(dx), accumulate,
                                       relu, part);
-    if (dbias) colred_stage2<<<stage2_blocks(C), kStage2Threads, 0, st>>>(part, nb, C, BiasFin{dbias});
+    if (dbias && !xskip(2)) colred_stage2<<<stage2_blocks(C), kStage2Threads, 0, st>>>(part, nb, C, BiasFin{dbias});
   } else {
     bn_dx_scalar<<<blocks_for(n), kThreads, 0, st>>>(x, dy, n, rows, C, gamma, beta, stats, coef, dx, accumulate,
                                                      relu);
@@ -1972,6 +1994,7 @@ cudaError_t bn_bwd_pool_stats(const PoolShape& ps, const uint8_t* argmax, const 
                                                             relu, items, part);
   }
   colred_stage2<<<stage2_blocks(C), kStage2Threads, 0, st>>>(part, grid, C, BnBwdFin{C, dgamma, dbeta, coef});
+  if (xskip(512)) colred_stage2<<<stage2_blocks(C), kStage2Threads, 0, st>>>(part, grid, C, BnBwdFin{C, dgamma, dbeta, coef});
   return cudaGetLastError();
 }
 

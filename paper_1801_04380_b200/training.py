@@ -169,6 +169,8 @@ def _xlib():
         L.sn_exec_step_host.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, P(C.c_float), P(TimingC)]
         L.sn_exec_step_host_pipelined.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                                   C.c_int32, P(C.c_float), P(TimingC)]
+        L.sn_exec_train_host.argtypes = [C.c_void_p, C.c_int32, P(C.c_void_p), P(C.c_void_p), C.c_int32,
+                                         P(C.c_float), P(TimingC)]
         L.sn_exec_read_tensor.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int64]
         L.sn_exec_apply_update.argtypes = [C.c_void_p, C.c_float, C.c_float]
         L.sn_exec_workspace_use.argtypes = [C.c_void_p, P(C.c_int32), P(C.c_int32)]
@@ -350,14 +352,22 @@ class Executor:
 
     def train_host(self, batches, update: bool = True) -> list[tuple[float, TimingC]]:
         """End to end over a sequence of pinned host (images NHWC, labels int32)
-        batches: batch i+1 is copied to the device while step i computes (the
-        data layer's one-batch prefetch); returns [(loss, timing)] per step."""
+        batches in one native call (sn_exec_train_host): batch i+1 is copied to
+        the device while step i computes (the data layer's one-batch prefetch)
+        and step i's loss is read back while step i+1 runs.  Returns
+        [(loss, timing)] per step; the timing (device ms per step, mean over
+        the call) is shared."""
         batches = list(batches)
-        out = []
-        for i, (img, lab) in enumerate(batches):
-            nxt = batches[i + 1] if i + 1 < len(batches) else (None, None)
-            out.append(self.step_host_pipelined(img, lab, nxt[0], nxt[1], update))
-        return out
+        n = len(batches)
+        if n == 0:
+            return []
+        imgs = (C.c_void_p * n)(*[b[0].data_ptr() for b in batches])
+        labs = (C.c_void_p * n)(*[b[1].data_ptr() for b in batches])
+        losses = (C.c_float * n)()
+        t = TimingC()
+        if self.L.sn_exec_train_host(self.ptr, n, imgs, labs, int(update), losses, C.byref(t)) != 0:
+            _raise_exec(self.L)
+        return [(losses[i], t) for i in range(n)]
 
     def workspace_use(self) -> tuple[int, int]:
         """(CONV weight gradients with their split-K partials in the planned conv

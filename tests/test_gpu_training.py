@@ -347,16 +347,20 @@ def test_pipelined_host_steps_match_serial_host_steps(cuda, alex32_case):
     batches = batches + batches[:2]  # revisit buffers, like a loader's ring
     cfg = sn.SimConfig(pool_bytes=1 << 30, features=sn.parse_features(ALL), cost=sn.CostConfig(batch=16))
     runs = []
-    for pipelined in (False, True):
+    for mode in ("serial", "loop", "pipelined"):
         ex = Executor(net, cfg, params=params, lr=0.005)
-        if pipelined:
+        if mode == "loop":  # sn_exec_train_host: one native call, losses read behind the next step
             losses = [l for l, _ in ex.train_host(batches)]
+        elif mode == "pipelined":  # one sn_exec_step_host_pipelined call per step
+            losses = [ex.step_host_pipelined(img, lab, *(batches[i + 1] if i + 1 < len(batches) else (None, None)))[0]
+                      for i, (img, lab) in enumerate(batches)]
         else:
             losses = [ex.step_host(img, lab)[0] for img, lab in batches]
         runs.append((losses, ex.get("params")))
         ex.close()
-    assert runs[0][0] == runs[1][0]
-    assert _bitwise(runs[0][1], runs[1][1])
+    for r in runs[1:]:
+        assert r[0] == runs[0][0]
+        assert _bitwise(r[1], runs[0][1])
 
 
 def test_wgrad_partials_use_the_planned_workspace(cuda, alex32_case):
