@@ -36,7 +36,10 @@ from paper_1801_04380_b200.profiling import is_tensor, is_wgrad  # noqa: E402
 
 METRICS = ("gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,"
            "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active,"
-           "dram__throughput.avg.pct_of_peak_sustained_elapsed")
+           "dram__throughput.avg.pct_of_peak_sustained_elapsed,"
+           "l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed")
+# the last metric: tensor-core operand reads from shared memory (% of the SMEM
+# bandwidth the tensor pipe can draw) -- what bounds the N = 64 convolutions
 UNITS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-9, "nsecond": 1e-9, "us": 1e-6,
          "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3, "%": 1.0, "": 1.0}
 TYPES = ["fwd", "replay", "bwd", "other"]
@@ -161,7 +164,8 @@ def merge(args) -> None:
                      "dims": dims, "us": t * 1e6, "ev_us": ki["us"], "flops": flops, "dram": dram,
                      "tflops": flops / t / 1e12 if t and flops else None, "gbs": dram / t / 1e9 if t else None,
                      "tensor_pct": m.get("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active"),
-                     "dram_pct": m.get("dram__throughput.avg.pct_of_peak_sustained_elapsed")})
+                     "dram_pct": m.get("dram__throughput.avg.pct_of_peak_sustained_elapsed"),
+                     "tcsmem_pct": m.get("l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed")})
     tag = args.tag
     md = [f"# Per-launch table: {lt['net']} b{lt['batch']} ({lt['features']}, {lt['precision']})", "",
           f"Source: `tools/launch_table.py collect` + ncu `--profile-from-start off --metrics {METRICS}` over one "
@@ -176,13 +180,17 @@ def merge(args) -> None:
                   f"{(c['flops'] / c['s'] / 1e12) if c['flops'] else 0:.1f} |")
     md += ["", "`us` = ncu gpu__time_duration (cold); `ev us` = CUDA-event time of the same kernel in a node-by-node "
            "replay of the iteration (warm, `sn_exec_kernel_times`, median of 5); TF/s from the ncu time.", "",
-           "| # | layer | phase | kernel | GEMM | us | ev us | TF/s | tensor % | DRAM MB | GB/s | DRAM % |",
-           "|---|---|---|---|---|---|---|---|---|---|---|---|"]
+           "`TC smem %` = tensor-core operand reads from shared memory, % of their peak "
+           "(l1tex__data_pipe_tc_wavefronts_mem_shared): near 80-90 % a convolution is bound by its SMEM operand "
+           "traffic, not by the MMA rate.", "",
+           "| # | layer | phase | kernel | GEMM | us | ev us | TF/s | tensor % | TC smem % | DRAM MB | GB/s | DRAM % |",
+           "|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     for r in rows:
         md.append(f"| {r['i']} | {r['layer']} | {r['type']} | `{r['kernel']}` | {r['dims']} | {r['us']:.1f} | "
                   f"{r['ev_us']:.1f} | "
                   f"{'' if r['tflops'] is None else f'{r['tflops']:.0f}'} | "
-                  f"{'' if r['tensor_pct'] is None else f'{r['tensor_pct']:.0f}'} | {r['dram'] / 1e6:.1f} | "
+                  f"{'' if r['tensor_pct'] is None else f'{r['tensor_pct']:.0f}'} | "
+                  f"{'' if not r['tcsmem_pct'] else f'{r['tcsmem_pct']:.0f}'} | {r['dram'] / 1e6:.1f} | "
                   f"{'' if r['gbs'] is None else f'{r['gbs']:.0f}'} | "
                   f"{'' if r['dram_pct'] is None else f'{r['dram_pct']:.0f}'} |")
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)

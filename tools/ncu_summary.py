@@ -15,6 +15,7 @@ import sys
 KEYS = [
     ("gpu__time_duration.sum", "time"),
     ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor %"),
+    ("l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", "TC smem %"),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM %"),
     ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "L2 %"),
     ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM %"),
