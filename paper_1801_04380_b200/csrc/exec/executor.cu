@@ -1296,6 +1296,31 @@ struct Compiler {
       }
       case snp::JOIN: {
         const auto& pv = net.prev[lid];
+        auto ds = dense_at.find(cur_ti);
+        if (ds != dense_at.end() && !dense_off[ds->second.chain]) {
+          const DenseStep& d = ds->second;
+          if (d.k == 0)  // the chain's sums start from dy(J_1): every input's buffer must be fresh
+            for (int p : pv) {
+              auto it = fresh.find(ex->eff_owner[p]);
+              if (it == fresh.end() || !it->second) dense_off[d.chain] = 1;
+            }
+          if (!dense_off[d.chain]) {
+            if (d.k == 0)
+              for (int p : pv) fresh[ex->eff_owner[p]] = false;  // written from here on (deferred)
+            float* r = grad_ptr(ex->eff_owner[d.p0]);
+            const int acc_r = d.k == 0 ? 0 : 1;
+            std::vector<float*> dsts;
+            std::vector<int> accs;
+            for (int q : d.finals) {
+              dsts.push_back(grad_ptr(ex->eff_owner[q]));
+              accs.push_back(0);
+            }
+            const int k = static_cast<int>(dsts.size());
+            push([=] { ck(sn::grad_prefix(dy, r, acc_r, dsts.data(), accs.data(), k, n, st), "join_bwd_dense"); },
+                 sn::grad_prefix_launches(k));
+            break;
+          }
+        }
         if (join_to_bn[cur_ti] >= 0) {
           // deferred into the BN backward (see plan_fusions): record the pointers now
           const int ra = join_relu[cur_ti];
@@ -1379,6 +1404,21 @@ struct Compiler {
   };
   std::vector<char> join_copy_own;
   std::unordered_map<int, PendingJoin> pending_join;  // keyed by BN-backward tape index
+  // Dense JOIN chains (DenseNet-style blocks, JOIN = sum): JOIN backwards
+  // J_1 .. J_m in tape order whose input sets are nested, I(J_{k+1}) = I(J_k)
+  // minus one input q_k.  The gradient of q_k is complete after J_k: it is
+  // the running sum dy(J_1) + ... + dy(J_k), kept in the buffer of an input
+  // p0 common to the whole chain (whose gradient is the chain's full sum).
+  // Each J_k adds its dy into the running sum and writes the buffers of the
+  // inputs it finishes -- 2 + 2 tensor passes per JOIN instead of 1 + 2 |I(J)|
+  // -- bit-identical to the per-input backward (every buffer receives the same
+  // additions in the same order).
+  struct DenseStep {
+    int chain = -1, k = 0, p0 = -1;
+    std::vector<int> finals;  // inputs whose gradient is finished at this step
+  };
+  std::unordered_map<size_t, DenseStep> dense_at;  // JOIN backward tape index -> its step
+  std::vector<char> dense_off;                      // per chain: disabled (an input's buffer was not fresh)
   // stem BN backward -> stem CONV backward: the BN's dx pass runs inside the
   // stem weight gradient (sn::StemBnFuse), dx is never written
   std::vector<char> stem_bn_fuse_at;
@@ -1797,7 +1837,107 @@ struct Compiler {
       }
     }
     plan_pool_stats(reassoc);
+    plan_dense_chains();
     ex->elided = elide_out;
+  }
+
+  // Dense JOIN chains (see DenseStep).  A chain is kept only when, between its
+  // first JOIN backward and the step that finishes an input, nothing else
+  // reads, writes or frees that input's gradient buffer, and every input owns
+  // its buffer (no in-place aliasing, no side roots).
+  void plan_dense_chains() {
+    const char* env = std::getenv("SN_FUSE_DENSE");  // =0: the per-input JOIN backward (A/B)
+    if (env && env[0] == '0') return;
+    const size_t T = P.tape.size();
+    std::vector<size_t> jb;
+    for (size_t i = 0; i < T; ++i) {
+      const snp::Event& e = P.tape[i];
+      if (e.op == 'B' && net.kind[e.b] == snp::JOIN && net.prev[e.b].size() >= 2 && join_to_bn[i] < 0) jb.push_back(i);
+    }
+    auto inputs = [&](size_t ti) {
+      std::vector<int> v = net.prev[P.tape[ti].b];
+      std::sort(v.begin(), v.end());
+      return v;
+    };
+    std::vector<char> used(jb.size(), 0);
+    for (size_t a = 0; a < jb.size(); ++a) {
+      if (used[a]) continue;
+      std::vector<size_t> chain{jb[a]}, members{a};
+      std::vector<int> qs;
+      std::vector<int> cur = inputs(jb[a]);
+      const std::vector<int> all = cur;
+      for (size_t b = a + 1; b < jb.size(); ++b) {
+        if (used[b]) continue;
+        const std::vector<int> nx = inputs(jb[b]);
+        bool shares = false;
+        for (int x : nx) shares |= std::binary_search(cur.begin(), cur.end(), x);
+        if (!shares) continue;
+        if (nx.size() + 1 != cur.size() || !std::includes(cur.begin(), cur.end(), nx.begin(), nx.end())) break;
+        int q = -1;
+        for (int x : cur)
+          if (!std::binary_search(nx.begin(), nx.end(), x)) q = x;
+        qs.push_back(q);
+        chain.push_back(jb[b]);
+        members.push_back(b);
+        cur = nx;
+      }
+      if (chain.size() < 2) continue;
+      // every input owns its gradient buffer; the JOIN's size suits the float4 kernel
+      bool ok = std::adjacent_find(all.begin(), all.end()) == all.end();
+      const LayerRt& jl = ex->L[P.tape[chain[0]].b];
+      ok &= (static_cast<int64_t>(ex->B) * jl.per_sample) % 4 == 0;
+      for (int p : all) ok &= ex->eff_owner[p] == p && !ex->side_root[p];
+      if (!ok) continue;
+      std::vector<char> in_chain(net.n, 0);
+      for (size_t ti : chain) in_chain[P.tape[ti].b] = 1;
+      // nothing touches input p's gradient between the chain's start and fin (exclusive)
+      auto quiet = [&](int p, size_t fin) {
+        bool allocated = false;  // the buffer exists when the chain starts (the reference allocates it for J_1)
+        for (size_t j = chain[0]; j-- > 0;) {
+          const snp::Event& f = P.tape[j];
+          if (f.a != snp::K_GRAD || f.b != p || (f.op != 'A' && f.op != 'F')) continue;
+          allocated = f.op == 'A';
+          break;
+        }
+        if (!allocated) return false;
+        for (size_t j = chain[0] + 1; j < fin; ++j) {
+          const snp::Event& f = P.tape[j];
+          if ((f.op == 'F' || f.op == 'A') && f.a == snp::K_GRAD && f.b == p) return false;
+          if (f.op != 'B' || in_chain[f.b]) continue;
+          if (f.b == p) return false;  // p's own backward reads its gradient
+          for (int x : net.prev[f.b])
+            if (x == p) return false;  // another consumer writes it
+        }
+        return true;
+      };
+      for (size_t k = 0; k < qs.size() && ok; ++k) ok &= quiet(qs[k], chain[k]);
+      if (!ok) continue;
+      int p0 = -1;
+      for (int c : cur)
+        if (quiet(c, chain.back())) {
+          p0 = c;
+          break;
+        }
+      if (p0 < 0) continue;
+      for (int c : cur) ok &= quiet(c, chain.back());
+      if (!ok) continue;
+      const int id = static_cast<int>(dense_off.size());
+      dense_off.push_back(0);
+      for (size_t k = 0; k < chain.size(); ++k) {
+        DenseStep d;
+        d.chain = id;
+        d.k = static_cast<int>(k);
+        d.p0 = p0;
+        if (k < qs.size()) {
+          d.finals = {qs[k]};
+        } else {
+          for (int c : cur)
+            if (c != p0) d.finals.push_back(c);
+        }
+        dense_at[chain[k]] = d;
+      }
+      for (size_t m : members) used[m] = 1;
+    }
   }
 
   // BN -> ReLU -> max POOL (k3 s2 p1, saved argmax, H = 2P): pool-order BN

@@ -298,6 +298,12 @@ cudaError_t grad_copy(const float* src, float* dst, int64_t n, int accumulate, c
 // k-way JOIN backward in ceil(k/8) passes over dy (n % 4 == 0; destinations distinct)
 int grad_copy_multi_launches(int k);
 cudaError_t grad_copy_multi(const float* src, float* const* dsts, const int* accs, int k, int64_t n, cudaStream_t st);
+// Dense JOIN-chain backward step: r = (acc_r ? r + src : src), then dsts[t] =
+// (accs[t] ? dsts[t] + r : r).  Bit-identical to adding src into every buffer
+// one JOIN at a time (same additions, same order).
+int grad_prefix_launches(int k);
+cudaError_t grad_prefix(const float* src, float* r, int acc_r, float* const* dsts, const int* accs, int k, int64_t n,
+                        cudaStream_t st);
 
 cudaError_t sgd_update(float* params, const float* grads, int64_t n, float lr, float grad_scale,
                        cudaStream_t st);

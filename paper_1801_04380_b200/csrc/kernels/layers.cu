@@ -2265,7 +2265,52 @@ __global__ void grad_copy_multi_kernel(const float4* __restrict__ src, MultiDst 
     }
   }
 }
+// One step of a dense JOIN chain's backward (the executor's dense_chain): the
+// running sum r (+)= dy, then every destination d (+)= r.  The additions are
+// the ones the per-destination JOIN backward would make, in the same order.
+__global__ void grad_prefix_kernel(const float4* __restrict__ src, float4* r, int acc_r, MultiDst md, int64_t n4) {
+  const int64_t T = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i0 < n4; i0 += 2 * T) {
+    float4 v[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int64_t i = i0 + u * T;
+      v[u] = i < n4 ? src[i] : zero4();
+      if (acc_r && i < n4) add4(v[u], r[i]);
+      if (i < n4) r[i] = v[u];
+    }
+    for (int t = 0; t < md.k; ++t) {
+      float4* d = md.d[t];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int64_t i = i0 + u * T;
+        if (i >= n4) continue;
+        float4 w = v[u];
+        if (md.acc[t]) add4(w, d[i]);
+        d[i] = w;
+      }
+    }
+  }
+}
 }  // namespace
+
+int grad_prefix_launches(int k) { return 1 + (k > kMultiDst ? grad_copy_multi_launches(k - kMultiDst) : 0); }
+
+cudaError_t grad_prefix(const float* src, float* r, int acc_r, float* const* dsts, const int* accs, int k, int64_t n,
+                        cudaStream_t st) {
+  if (n % 4 != 0) return cudaErrorInvalidValue;
+  MultiDst md{};
+  md.k = std::min(kMultiDst, k);
+  for (int t = 0; t < md.k; ++t) {
+    md.d[t] = reinterpret_cast<float4*>(dsts[t]);
+    md.acc[t] = accs[t];
+  }
+  grad_prefix_kernel<<<elt_blocks(n / 4), kThreads, 0, st>>>(reinterpret_cast<const float4*>(src),
+                                                            reinterpret_cast<float4*>(r), acc_r, md, n / 4);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || k <= kMultiDst) return e;
+  return grad_copy_multi(r, dsts + kMultiDst, accs + kMultiDst, k - kMultiDst, n, st);
+}
 
 int grad_copy_multi_launches(int k) { return (k + kMultiDst - 1) / kMultiDst; }
 

@@ -334,6 +334,25 @@ def test_branchy_nets_match_oracle_and_are_schedule_invariant(cuda, kind):
     assert worst <= 3 * sens + 5e-3, (worst, sens)
 
 
+@pytest.mark.parametrize("feats", ["none", "liveness,offload,recompute=memory", ALL])
+def test_dense_join_chain_backward_is_bit_identical(cuda, monkeypatch, feats):
+    """DenseNet-style blocks: the nested JOIN-sum backwards run as one running
+    sum (each JOIN adds its dy once and writes the inputs it finishes) instead
+    of adding dy into every input's buffer -- same additions in the same order,
+    so the same bits as the per-input JOIN backward (SN_FUSE_DENSE=0), with
+    fewer launches when a chain applies."""
+    from paper_1801_04380_b200 import netgen
+    from paper_1801_04380_b200.training import init_parameters
+    net = netgen.gen_densenet(blocks=(3, 10, 4, 2), widths=(32, 32, 64, 64))
+    params = init_parameters(net, seed=8, head_scale=0.1)
+    images, labels = _inputs(net, 4, seed=9)
+    loss, grads, _, t = _run(net, 4, 8 << 30, feats, params, images, labels)
+    monkeypatch.setenv("SN_FUSE_DENSE", "0")
+    loss0, grads0, _, t0 = _run(net, 4, 8 << 30, feats, params, images, labels)
+    assert loss == loss0 and _bitwise(grads, grads0)
+    assert t.kernels < t0.kernels, (t.kernels, t0.kernels)
+
+
 def test_pipelined_host_steps_match_serial_host_steps(cuda, alex32_case):
     """The prefetching end-to-end call (sn_exec_step_host_pipelined) trains
     exactly like one synchronous sn_exec_step_host per batch."""
