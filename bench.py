@@ -437,14 +437,19 @@ def extras(args, net, cfg, ex, ms_per_step, local) -> dict:
             t_other += ms
     serial_ms = sum(p[0] for p in prof)
     peaks = measured_peaks()
+    # kernel level: every kernel of the iteration replayed node by node with a
+    # CUDA event pair around it (median of 5), FLOPs attributed per kernel.
+    # Timed BEFORE the cuBLAS peaks: the sustained GEMM leaves the board under
+    # its power cap for seconds, and kernels replayed right after it ran ~30 %
+    # slower (lower SM clock).  Clocks are sampled during the replay too.
+    from paper_1801_04380_b200.profiling import kernel_table
+    time.sleep(1.0)
+    with ClockSampler(local) as kclocks:
+        acts = kernel_table(ex, reps=5)
     tf32 = tf32_gemm_peaks(f"cuda:{local}")
     achieved = f_tensor / (t_tensor / 1e3) / 1e12 if t_tensor else 0.0
     traffic, why = step_traffic(args.net, args.batch)
     tr = traffic["per_step"] if traffic else {}
-    # kernel level: every kernel of the iteration replayed node by node with a
-    # CUDA event pair around it (median of 3), FLOPs attributed per kernel
-    from paper_1801_04380_b200.profiling import kernel_table
-    acts = kernel_table(ex, reps=3)
     ks = [k for a in acts for k in a["kernels"]]
     tk = [k for k in ks if k["flops"] > 0]
     k_us = sum(k["us"] for k in tk)
@@ -459,7 +464,8 @@ def extras(args, net, cfg, ex, ms_per_step, local) -> dict:
         "peak_source": "cuBLAS tf32 8192^3 burst (best of 10) measured in this run: every kernel is timed alone",
         "how": "achieved = SURVEY 8(d) GEMM FLOPs attributed to the %d tcgen05 kernels of one iteration / their summed "
                "CUDA-event durations (sn_exec_kernel_times: the iteration replayed node by node, an event pair around "
-               "each kernel, median of 3)" % len(tk),
+               "each kernel, median of 5, replayed before the cuBLAS peak runs)" % len(tk),
+        "kernel_clocks": kclocks.summary(),
         "kernel_us_per_step": round(k_us, 1), "algorithmic_tflop_per_step": round(f_tensor / 1e12, 4),
         "traffic": (tr.get("conv_fc_gemm", {}).get("dram_bytes_per_step") if traffic else None),
         "traffic_source": traffic["source"] if traffic else why,
@@ -487,7 +493,7 @@ def extras(args, net, cfg, ex, ms_per_step, local) -> dict:
         gbs = hl["dram_bytes_per_step"] / (hk_us / 1e6) / 1e9
         out["roofline_hbm_layers"].update(achieved=round(gbs, 1), frac=round(gbs / hbm_peak, 4),
                                           how="ncu DRAM bytes of these launches (same libsnexec digest) / their "
-                                              "summed CUDA-event durations this run (kernel replay, median of 3)")
+                                              "summed CUDA-event durations this run (kernel replay, median of 5)")
     out["time_by_layer_kind_ms"] = {k: round(v, 3) for k, v in sorted(by_kind.items(), key=lambda kv: -kv[1])}
 
     def side_run(label, cfg2, steps=5, **kw):

@@ -23,6 +23,16 @@
 //
 // Dgrad (stride 1) runs the same kernel over dy with the flipped, transposed
 // filter and padding R-1-pad.
+//
+// Stride 2 (phase mode): output (p, q) tap (r, s) reads padded input pixel
+// (2p + r, 2q + s), i.e. pixel (p + r/2, q + s/2) of the phase image
+// (r % 2, s % 2) = padded input rows / columns of one parity.  A strided TMA
+// box (elementStrides 2 along W and H) loads one phase image of the band per
+// 32-channel chunk -- TR*MT + (R-1)/2 phase rows x Wp = Q + (S-1)/2 columns --
+// and on the output grid (p, q'), q' < Wp, every tap of that phase is again a
+// uniform row shift ((r/2) Wp + s/2) of it.  Four phase boxes per chunk read
+// the input about once (the im2col kernel reads it R*S/4 = 2.25x and was
+// bound by that L2 -> SMEM traffic: 41 % tensor pipe on ResNet conv_s2b1).
 #include <cuda.h>
 
 #include <algorithm>
@@ -47,12 +57,15 @@ struct HaloArgs {
   int N;               // output channels (valid columns)
   int reduce;          // dgrad accumulate: TMA reduce-add store
   float* stats;        // BN statistics per sub-tile: [tile*MT + j][4][N] {shift, S1, S2, count}
+  int phase;           // 1: stride-2 phase mode (four phase boxes per chunk, see above)
 };
 
-template <int BN, int MT, int HST, int BST, int CG = 1>
+// EB: store-staging buffers per epilogue group (2: double-buffered; 1 frees
+// 32 KB for a deeper operand ring, the group waits for its previous store's read)
+template <int BN, int MT, int HST, int BST, int CG = 1, int EB = 2>
 struct HaloSmem {
   static constexpr int B_BYTES = (BN / CG) * 128;  // CTA pairs: each CTA stages half of the weight rows
-  static constexpr int EPI_BYTES = 2 * 2 * kBM * 128;  // two epilogue groups x double-buffered 16 KB chunks
+  static constexpr int EPI_BYTES = 2 * EB * kBM * 128;  // two epilogue groups x EB 16 KB chunks
   // halo ring first (dynamic size), then the fixed tail (barriers, TMEM slot, 2 x 1 KB statistics scratch)
   static constexpr int tail() { return BST * B_BYTES + EPI_BYTES + 512 + 2048 + 1024; }
 };
@@ -61,11 +74,11 @@ struct HaloSmem {
 // rank r owns rows [r TR*MT, (r+1) TR*MT) of it (its own halo boxes, its own
 // TMEM accumulators) and stages half of every weight tile; the even CTA issues
 // tcgen05.mma.cta_group::2 with M = 256 (as conv_tma.cu CG = 2).
-template <int BN, int MT, int HST, int BST, int CG = 1>
+template <int BN, int MT, int HST, int BST, int CG = 1, int EB = 2>
 __global__ void __launch_bounds__(kHaloFwdThreads, 1)
     tc_conv_halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
                         const __grid_constant__ CUtensorMap tmY, HaloArgs a) {
-  using L = HaloSmem<BN, MT, HST, BST, CG>;
+  using L = HaloSmem<BN, MT, HST, BST, CG, EB>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align_smem_1024(smem_raw);
   uint8_t* sH = smem;                                   // HST halo slots
@@ -118,7 +131,6 @@ __global__ void __launch_bounds__(kHaloFwdThreads, 1)
   if constexpr (CG == 2) cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int taps = a.R * a.S;
   const int rank = CG == 2 ? static_cast<int>(cluster_rank()) : 0;
   const int unit = blockIdx.x / CG, units = gridDim.x / CG;
 
@@ -142,15 +154,19 @@ __global__ void __launch_bounds__(kHaloFwdThreads, 1)
         int n, y0, n0;
         coords(t, n, y0, n0);
         for (int cc = 0; cc < a.cchunks; ++cc) {
+         for (int ph = 0; ph < (a.phase ? 4 : 1); ++ph) {
+          const int rho = ph >> 1, phi = ph & 1;
+          if (rho >= a.R || phi >= a.S) continue;  // a phase without taps (1-wide filter)
+          const int cx = a.phase ? phi - a.pad : -a.pad;
+          const int cy = a.phase ? 2 * y0 + rho - a.pad : y0 - a.pad;
           if (hwrap) mbar_wait(&hempty[hs], hph ^ 1);
           if (elect_one()) {
             if constexpr (CG == 1) {
               mbar_arrive_expect_tx(&hfull[hs], a.halo_bytes);
-              tma_load_4d(smem_u32(sH + hs * a.halo_slot), &tmX, &hfull[hs], cc * 32, -a.pad, y0 - a.pad, n);
+              tma_load_4d(smem_u32(sH + hs * a.halo_slot), &tmX, &hfull[hs], cc * 32, cx, cy, n);
             } else {
               if (rank == 0) mbar_arrive_expect_tx(&hfull[hs], 2 * a.halo_bytes);
-              tma2_load_4d(smem_u32(sH + hs * a.halo_slot), &tmX, mapa_u32(&hfull[hs], 0), cc * 32, -a.pad,
-                           y0 - a.pad, n);
+              tma2_load_4d(smem_u32(sH + hs * a.halo_slot), &tmX, mapa_u32(&hfull[hs], 0), cc * 32, cx, cy, n);
             }
           }
           __syncwarp();
@@ -159,7 +175,10 @@ __global__ void __launch_bounds__(kHaloFwdThreads, 1)
             hph ^= 1;
             hwrap = true;
           }
-          for (int tap = 0; tap < taps; ++tap) {
+          const int tstep = a.phase ? 2 : 1;
+          for (int r = a.phase ? rho : 0; r < a.R; r += tstep)
+          for (int sx = a.phase ? phi : 0; sx < a.S; sx += tstep) {
+            const int tap = r * a.S + sx;
             if (bwrap) mbar_wait(&bempty[bs], bph ^ 1);
             if (elect_one()) {
               if constexpr (CG == 1) {
@@ -178,6 +197,7 @@ __global__ void __launch_bounds__(kHaloFwdThreads, 1)
               bwrap = true;
             }
           }
+         }
         }
       }
     }
@@ -196,16 +216,22 @@ __global__ void __launch_bounds__(kHaloFwdThreads, 1)
         if (local >= 2) mbar_wait(&tempty[acc], ((local >> 1) - 1) & 1);
         tc_fence_after();
         const uint32_t d0 = tmem + static_cast<uint32_t>(acc * MT * BN);
+        bool first_mma = true;
         for (int cc = 0; cc < a.cchunks; ++cc) {
+         for (int ph = 0; ph < (a.phase ? 4 : 1); ++ph) {
+          const int rho = ph >> 1, phi = ph & 1;
+          if (rho >= a.R || phi >= a.S) continue;
           mbar_wait(&hfull[hs], hph);
           const uint64_t h0 = hdesc0 + hs * (a.halo_slot >> 4);
-          int r = 0, sx = 0;
-          for (int tap = 0; tap < taps; ++tap) {
+          const int tstep = a.phase ? 2 : 1, sh = a.phase ? 1 : 0;
+          for (int r = a.phase ? rho : 0; r < a.R; r += tstep)
+          for (int sx = a.phase ? phi : 0; sx < a.S; sx += tstep) {
             mbar_wait(&bfull[bs], bph);
             tc_fence_after();
-            const uint64_t ad = h0 + static_cast<uint32_t>(r * a.Wp + sx) * 8u;
+            const uint64_t ad = h0 + static_cast<uint32_t>((r >> sh) * a.Wp + (sx >> sh)) * 8u;
             const uint64_t bd = bdesc0 + bs * (L::B_BYTES >> 4);
-            const uint32_t first = (cc | tap) != 0 ? 1u : 0u;
+            const uint32_t first = first_mma ? 0u : 1u;
+            first_mma = false;
             if (elect_one()) {
               // sub-tiles innermost: consecutive MMAs feed different accumulators
 #pragma unroll
@@ -227,10 +253,6 @@ __global__ void __launch_bounds__(kHaloFwdThreads, 1)
               bs = 0;
               bph ^= 1;
             }
-            if (++sx == a.S) {
-              sx = 0;
-              ++r;
-            }
           }
           if (elect_one()) {
             if constexpr (CG == 1)
@@ -243,6 +265,7 @@ __global__ void __launch_bounds__(kHaloFwdThreads, 1)
             hs = 0;
             hph ^= 1;
           }
+         }
         }
         if (elect_one()) {
           if constexpr (CG == 1)
@@ -261,7 +284,7 @@ __global__ void __launch_bounds__(kHaloFwdThreads, 1)
     const uint32_t row = q4 * 32 + lane;
     const bool leader = q4 == 0 && lane == 0;
     const uint32_t bar_id = 1 + grp;
-    uint8_t* sEpiG = sEpi + grp * 2 * (kBM * 128);
+    uint8_t* sEpiG = sEpi + grp * EB * (kBM * 128);
     float* sred = sred0 + grp * 256;
     int local = 0;
     uint32_t chunk_no = 0;
@@ -297,8 +320,13 @@ __global__ void __launch_bounds__(kHaloFwdThreads, 1)
                 if (n0 + c + q < a.N) v[q] += __ldg(a.bias + n0 + c + q);
             }
           }
-          const uint32_t buf = smem_u32(sEpiG) + (chunk_no & 1u) * (kBM * 128);
-          if (leader) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          const uint32_t buf = smem_u32(sEpiG) + (EB == 2 ? (chunk_no & 1u) : 0u) * (kBM * 128);
+          if (leader) {
+            if constexpr (EB == 2)
+              asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            else
+              asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          }
           named_bar(bar_id, 128);
 #pragma unroll
           for (int q = 0; q < 8; ++q)
@@ -322,7 +350,7 @@ __global__ void __launch_bounds__(kHaloFwdThreads, 1)
             // junk rows (padded columns x' >= Q, rows past P) are skipped; the
             // shift is the sub-tile's row 0 (real unless the whole sub-tile lies
             // past P, then its count is 0 and the reduction skips it)
-            const uint8_t* sb = sEpiG + (chunk_no & 1u) * (kBM * 128);
+            const uint8_t* sb = sEpiG + (EB == 2 ? (chunk_no & 1u) : 0u) * (kBM * 128);
             const int Wp = a.Wp, TR = a.TR, Q = a.Q, rows_left = a.P - ys;
             float shift, t1, t2;
             chunk_column_stats(
@@ -381,14 +409,16 @@ struct HaloGeom {
   uint32_t halo_bytes, halo_slot;
 };
 
+// Stride 2 (phase mode): Wp = Q + (S-1)/2 phase columns, TR*MT + (R-1)/2
+// phase rows per box (the strided box spans twice that many input rows).
 template <int BN, int MT>
-bool halo_geom(int H, int W, int R, int S, int pad, int P, HaloGeom* g) {
-  g->Wp = W + 2 * pad;
+bool halo_geom(int H, int W, int R, int S, int pad, int P, HaloGeom* g, int stride = 1, int Q = 0) {
+  g->Wp = stride == 1 ? W + 2 * pad : Q + (S - 1) / 2;
   if (g->Wp > kBM || g->Wp > 256) return false;
   g->TR = std::min(kBM / g->Wp, P);
   g->MT = MT;
-  g->halo_rows = g->TR * MT + R - 1;
-  if (g->halo_rows > 256) return false;
+  g->halo_rows = stride == 1 ? g->TR * MT + R - 1 : g->TR * MT + (R - 1) / 2;
+  if (g->halo_rows * stride > 256) return false;
   g->halo_bytes = static_cast<uint32_t>(g->halo_rows) * g->Wp * 128;
   // the last sub-tile's junk GEMM rows (TR*Wp .. 127) read past the halo box
   const int over = std::max(0, kBM + S - g->TR * g->Wp);
@@ -398,13 +428,13 @@ bool halo_geom(int H, int W, int R, int S, int pad, int P, HaloGeom* g) {
   return true;
 }
 
-template <int BN, int MT, int HST, int BST, int CG>
+template <int BN, int MT, int HST, int BST, int CG, int EB = 2>
 cudaError_t launch_halo(const CUtensorMap& X, const CUtensorMap& Wm, const CUtensorMap& Y, HaloArgs a,
                         const HaloGeom& g, cudaStream_t st) {
-  using L = HaloSmem<BN, MT, HST, BST, CG>;
+  using L = HaloSmem<BN, MT, HST, BST, CG, EB>;
   const int smem = static_cast<int>(HST * g.halo_slot) + L::tail();
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  auto kern = tc_conv_halo_kernel<BN, MT, HST, BST, CG>;
+  auto kern = tc_conv_halo_kernel<BN, MT, HST, BST, CG, EB>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (err != cudaSuccess) return err;
   if constexpr (CG == 1) {
@@ -429,21 +459,35 @@ cudaError_t launch_halo(const CUtensorMap& X, const CUtensorMap& Wm, const CUten
 }
 
 // Variant table: (BN, MT, halo stages, weight stages, CTA group) fitting 227 KB.
-template <int BN, int MT, int HST, int BST, int CG = 1>
+template <int BN, int MT, int HST, int BST, int CG = 1, int EB = 2>
 bool halo_fits(const HaloGeom& g) {
-  return static_cast<int>(HST * g.halo_slot) + HaloSmem<BN, MT, HST, BST, CG>::tail() <= 227 * 1024;
+  return static_cast<int>(HST * g.halo_slot) + HaloSmem<BN, MT, HST, BST, CG, EB>::tail() <= 227 * 1024;
 }
 
-// variant id -> (BN, MT, CG): 1-3 single CTA BN 64/128/256, 4-6 the same as CTA pairs
-constexpr int kVarBN[7] = {0, 64, 128, 256, 64, 128, 256};
-constexpr int kVarMT[7] = {0, 3, 2, 1, 3, 2, 1};
-constexpr int kVarCG[7] = {0, 1, 1, 1, 2, 2, 2};
+// variant id -> (BN, MT, CG): 1-3 single CTA BN 64/128/256, 4-6 the same as
+// CTA pairs; 7-12 the stride-2 phase-mode kernels (three halo stages: a phase
+// box feeds only 1-4 taps, so the ring turns over four times per chunk)
+constexpr int kVarBN[13] = {0, 64, 128, 256, 64, 128, 256, 64, 128, 256, 64, 128, 256};
+constexpr int kVarMT[13] = {0, 3, 2, 1, 3, 2, 1, 3, 2, 1, 3, 2, 1};
+constexpr int kVarCG[13] = {0, 1, 1, 1, 2, 2, 2, 1, 1, 1, 2, 2, 2};
+
+template <int BN, int MT>
+bool geom_for(int v, int H, int W, int R, int S, int pad, int P, int Q, HaloGeom* g) {
+  return halo_geom<BN, MT>(H, W, R, S, pad, P, g, v >= 7 ? 2 : 1, Q);
+}
+bool geom_any(int v, int H, int W, int R, int S, int pad, int P, int Q, HaloGeom* g) {
+  switch (kVarBN[v]) {
+    case 64: return geom_for<64, 3>(v, H, W, R, S, pad, P, Q, g);
+    case 128: return geom_for<128, 2>(v, H, W, R, S, pad, P, Q, g);
+    default: return geom_for<256, 1>(v, H, W, R, S, pad, P, Q, g);
+  }
+}
 
 }  // namespace
 
-// Which variant a shape runs (0: none).  Stride 1, C % 32 == 0, K % 32 == 0,
-// padded rows fit one 128-row sub-tile, and the im2col kernel would re-read
-// the input R*S > 1 times.
+// Which variant a shape runs (0: none).  Stride 1 or 2, C % 32 == 0,
+// K % 32 == 0, padded rows fit one 128-row sub-tile, and the im2col kernel
+// would re-read the input R*S > 1 times (stride 2: R*S/4 > 1).
 int g_halo = -1;  // 0 off, 1 by shape (default; env SN_CONV_HALO=0 turns it off), 2 whenever legal (tests)
 int halo_mode() {
   if (g_halo < 0) {
@@ -455,62 +499,79 @@ int halo_mode() {
 
 int conv_halo_mode() { return halo_mode(); }
 
-int conv_halo_variant(int N, int H, int W, int C, int K, int R, int S, int pad, int P, int Q) {
+int conv_halo_variant(int N, int H, int W, int C, int K, int R, int S, int pad, int P, int Q, int stride) {
   if (halo_mode() == 0 || C % 32 != 0 || K % 32 != 0 || R * S <= 1 || !tma_encoders_ok()) return 0;
-  if (P != H + 2 * pad - R + 1 || Q != W + 2 * pad - S + 1 || pad < 0) return 0;
+  if (stride != 1 && stride != 2) return 0;
+  static const int s2_off = std::getenv("SN_CONV_HALO_S2") && std::getenv("SN_CONV_HALO_S2")[0] == '0';
+  if (stride == 2 && s2_off && halo_mode() == 1) return 0;  // A/B knob: the im2col kernel for stride 2
+  if (pad < 0 || P != (H + 2 * pad - R) / stride + 1 || Q != (W + 2 * pad - S) / stride + 1) return 0;
+  if (stride == 1 && (P != H + 2 * pad - R + 1 || Q != W + 2 * pad - S + 1)) return 0;
+  // stride 2: every phase image has taps (a 1-wide filter has none in the odd phases)
+  if (stride == 2 && (R < 2 || S < 2)) return 0;
   // by shape: real output rows must fill >= 3/4 of each 128-row sub-tile, and
   // K <= 128 (profiles/r01_conv_bench_halopair.txt, ResNet b256, CTA pairs:
   // stage 1 161 -> 118 us, stage 2 102 -> 94 us; at K = 256 the im2col
   // kernel's wider N amortises its operand traffic better: 80 vs 98 us)
-  const int Wp = W + 2 * pad;
+  const int Wp = stride == 1 ? W + 2 * pad : Q + (S - 1) / 2;
   if (halo_mode() == 1 && (Wp > kBM || std::min(kBM / Wp, P) * Q * 4 < 3 * kBM || K > 128)) return 0;
   HaloGeom g;
   const int bn = K <= 64 ? 64 : (K <= 128 ? 128 : 256);
+  const int base = stride == 2 ? 6 : 0;
   // CTA pairs halve the per-SM weight traffic; they need >= 148 pair tiles
   const int pm = conv_pairs_mode();
   int v = 0;
-  if (bn == 64) {
-    if (!halo_geom<64, 3>(H, W, R, S, pad, P, &g)) return 0;
-    v = halo_fits<64, 3, 2, 4>(g) ? 1 : 0;
-    if (pm != 0 && halo_fits<64, 3, 2, 8, 2>(g)) v = 4;
-  } else if (bn == 128) {
-    if (!halo_geom<128, 2>(H, W, R, S, pad, P, &g)) return 0;
-    v = halo_fits<128, 2, 2, 4>(g) ? 2 : 0;
-    if (pm != 0 && halo_fits<128, 2, 2, 8, 2>(g)) v = 5;
+  if (!geom_any(base + (bn == 64 ? 1 : bn == 128 ? 2 : 3), H, W, R, S, pad, P, Q, &g)) return 0;
+  if (stride == 1) {
+    if (bn == 64) {
+      v = halo_fits<64, 3, 2, 4>(g) ? 1 : 0;
+      if (pm != 0 && halo_fits<64, 3, 2, 8, 2>(g)) v = 4;
+    } else if (bn == 128) {
+      v = halo_fits<128, 2, 2, 4>(g) ? 2 : 0;
+      if (pm != 0 && halo_fits<128, 2, 2, 8, 2>(g)) v = 5;
+    } else {
+      v = halo_fits<256, 1, 2, 3>(g) ? 3 : 0;
+      if (pm != 0 && halo_fits<256, 1, 2, 6, 2>(g)) v = 6;
+    }
   } else {
-    if (!halo_geom<256, 1>(H, W, R, S, pad, P, &g)) return 0;
-    v = halo_fits<256, 1, 2, 3>(g) ? 3 : 0;
-    if (pm != 0 && halo_fits<256, 1, 2, 6, 2>(g)) v = 6;
+    if (bn == 64) {
+      v = halo_fits<64, 3, 2, 4>(g) ? 7 : 0;
+      if (pm != 0 && halo_fits<64, 3, 2, 8, 2>(g)) v = 10;
+    } else if (bn == 128) {
+      v = halo_fits<128, 2, 3, 3>(g) ? 8 : 0;
+      if (pm != 0 && halo_fits<128, 2, 3, 6, 2>(g)) v = 11;
+    } else {
+      v = halo_fits<256, 1, 3, 3>(g) ? 9 : 0;
+      if (pm != 0 && halo_fits<256, 1, 3, 6, 2>(g)) v = 12;
+    }
   }
-  if (v >= 4 && pm == 1) {
+  if (v && kVarCG[v] == 2 && pm == 1) {
     const int bands2 = (P + g.TR * g.MT * 2 - 1) / (g.TR * g.MT * 2);
     if (static_cast<int64_t>(N) * bands2 * ((K + bn - 1) / bn) < num_sms_h() / 2) v -= 3;
   }
   return v;
 }
 
-int conv_halo_stats_tiles(int N, int H, int W, int C, int K, int R, int S, int pad, int P, int Q) {
-  const int v = conv_halo_variant(N, H, W, C, K, R, S, pad, P, Q);
+int conv_halo_stats_tiles(int N, int H, int W, int C, int K, int R, int S, int pad, int P, int Q, int stride) {
+  const int v = conv_halo_variant(N, H, W, C, K, R, S, pad, P, Q, stride);
   if (!v) return 0;
   const int MT = kVarMT[v], CG = kVarCG[v];
-  const int Wp = W + 2 * pad;
+  const int Wp = stride == 1 ? W + 2 * pad : Q + (S - 1) / 2;
   const int TR = std::min(kBM / Wp, P);
   const int bands = (P + TR * MT * CG - 1) / (TR * MT * CG);
   return N * bands * CG * MT;
 }
 
-// y[N][P][Q][K] (+)= conv(x[N][H][W][C], w[K][R][S][C]) + bias, stride 1.
+// y[N][P][Q][K] (+)= conv(x[N][H][W][C], w[K][R][S][C]) + bias, stride 1 or 2.
 cudaError_t conv_halo(int N, int H, int W, int C, int K, int R, int S, int pad, int P, int Q, const float* x,
-                      const float* w, const float* bias, float* y, int accumulate, float* stats, cudaStream_t st) {
-  const int v = conv_halo_variant(N, H, W, C, K, R, S, pad, P, Q);
+                      const float* w, const float* bias, float* y, int accumulate, float* stats, cudaStream_t st,
+                      int stride) {
+  const int v = conv_halo_variant(N, H, W, C, K, R, S, pad, P, Q, stride);
   if (!v) return cudaErrorInvalidValue;
   HaloGeom g;
   const int BN = kVarBN[v], MT = kVarMT[v], CG = kVarCG[v];
-  if (BN == 64) halo_geom<64, 3>(H, W, R, S, pad, P, &g);
-  else if (BN == 128) halo_geom<128, 2>(H, W, R, S, pad, P, &g);
-  else halo_geom<256, 1>(H, W, R, S, pad, P, &g);
+  geom_any(v, H, W, R, S, pad, P, Q, &g);
   CUtensorMap X, Wm, Y;
-  if (!tma_map_nhwc(&X, x, N, H, W, C, g.Wp, g.halo_rows, 0)) return cudaErrorInvalidValue;
+  if (!tma_map_nhwc(&X, x, N, H, W, C, g.Wp, g.halo_rows, 0, stride)) return cudaErrorInvalidValue;
   if (!tma_map_2d(&Wm, w, K, static_cast<int64_t>(R) * S * C, BN / CG, 0)) return cudaErrorInvalidValue;
   if (!tma_map_nhwc(&Y, y, N, P, Q, K, g.Wp, g.TR, 0)) return cudaErrorInvalidValue;
   HaloArgs a{};
@@ -533,13 +594,20 @@ cudaError_t conv_halo(int N, int H, int W, int C, int K, int R, int S, int pad, 
   a.N = K;
   a.reduce = accumulate;
   a.stats = stats;
+  a.phase = stride == 2 ? 1 : 0;
   switch (v) {
     case 1: return launch_halo<64, 3, 2, 4, 1>(X, Wm, Y, a, g, st);
     case 2: return launch_halo<128, 2, 2, 4, 1>(X, Wm, Y, a, g, st);
     case 3: return launch_halo<256, 1, 2, 3, 1>(X, Wm, Y, a, g, st);
     case 4: return launch_halo<64, 3, 2, 8, 2>(X, Wm, Y, a, g, st);
     case 5: return launch_halo<128, 2, 2, 8, 2>(X, Wm, Y, a, g, st);
-    default: return launch_halo<256, 1, 2, 6, 2>(X, Wm, Y, a, g, st);
+    case 6: return launch_halo<256, 1, 2, 6, 2>(X, Wm, Y, a, g, st);
+    case 7: return launch_halo<64, 3, 2, 4, 1>(X, Wm, Y, a, g, st);
+    case 8: return launch_halo<128, 2, 3, 3, 1>(X, Wm, Y, a, g, st);
+    case 9: return launch_halo<256, 1, 3, 3, 1>(X, Wm, Y, a, g, st);
+    case 10: return launch_halo<64, 3, 2, 8, 2>(X, Wm, Y, a, g, st);
+    case 11: return launch_halo<128, 2, 3, 6, 2>(X, Wm, Y, a, g, st);
+    default: return launch_halo<256, 1, 3, 6, 2>(X, Wm, Y, a, g, st);
   }
 }
 

@@ -704,14 +704,17 @@ int bn_for_waves(int64_t M, int n) {
 
 bool tma_encoders_ok() { return load_encoders(); }
 
-bool tma_map_nhwc(CUtensorMap* m, const float* base, int N, int H, int W, int C, int box_w, int box_h, int swz) {
+bool tma_map_nhwc(CUtensorMap* m, const float* base, int N, int H, int W, int C, int box_w, int box_h, int swz,
+                  int es) {
   if (!load_encoders()) return false;
+  if (es < 1 || es > 8 || box_w * es > 256 || box_h * es > 256) return false;
   cuuint64_t dims[4] = {static_cast<cuuint64_t>(C), static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H),
                         static_cast<cuuint64_t>(N)};
   cuuint64_t strides[3] = {static_cast<cuuint64_t>(C) * 4, static_cast<cuuint64_t>(W) * C * 4,
                            static_cast<cuuint64_t>(H) * W * C * 4};
-  cuuint32_t box[4] = {32, static_cast<cuuint32_t>(box_w), static_cast<cuuint32_t>(box_h), 1};
-  cuuint32_t estr[4] = {1, 1, 1, 1};
+  // with element strides the box spans es x the elements it loads (TMA traversal stride)
+  cuuint32_t box[4] = {32, static_cast<cuuint32_t>(box_w * es), static_cast<cuuint32_t>(box_h * es), 1};
+  cuuint32_t estr[4] = {1, static_cast<cuuint32_t>(es), static_cast<cuuint32_t>(es), 1};
   return g_encode_tiled(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(base), dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE,
                         swz ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
@@ -754,8 +757,8 @@ int conv_fwd_stats_tiles(const ConvShape& s, bool stem, int* tile_rows) {
     return s.N * s.P;
   }
   if (!use_tma()) return 0;
-  if (s.stride == 1) {
-    const int ht = conv_halo_stats_tiles(s.N, s.H, s.W, s.C, s.K, s.R, s.S, s.pad, s.P, s.Q);
+  if (s.stride <= 2) {
+    const int ht = conv_halo_stats_tiles(s.N, s.H, s.W, s.C, s.K, s.R, s.S, s.pad, s.P, s.Q, s.stride);
     if (ht > 0) {
       *tile_rows = 0;
       return ht;

@@ -477,8 +477,8 @@ void set_conv_tma(int on) { g_use_tma = on ? 1 : 0; }
 
 cudaError_t conv_fwd(const ConvShape& s, const float* x, const float* w, const float* bias, float* y,
                      cudaStream_t st, float* stats) {
-  if (use_tma() && s.stride == 1 && conv_halo_variant(s.N, s.H, s.W, s.C, s.K, s.R, s.S, s.pad, s.P, s.Q))
-    return conv_halo(s.N, s.H, s.W, s.C, s.K, s.R, s.S, s.pad, s.P, s.Q, x, w, bias, y, 0, stats, st);
+  if (use_tma() && s.stride <= 2 && conv_halo_variant(s.N, s.H, s.W, s.C, s.K, s.R, s.S, s.pad, s.P, s.Q, s.stride))
+    return conv_halo(s.N, s.H, s.W, s.C, s.K, s.R, s.S, s.pad, s.P, s.Q, x, w, bias, y, 0, stats, st, s.stride);
   if (use_tma() && conv_tma_ok_fwd(s)) return conv_fwd_tma(s, x, w, bias, y, stats, st);
   if (stats) return cudaErrorInvalidValue;  // only the TMA kernels emit BN tile statistics
   switch (bn_for(s.K)) {

@@ -92,10 +92,12 @@ cudaError_t pad_channels(const float* raw, int C_raw, float* out, int Cs, int64_
 
 // Halo-tiled stride-1 convolution (conv_halo.cu): one TMA box per 32-channel
 // chunk serves every filter tap.  Variant 0 = not applicable to the shape.
-int conv_halo_variant(int N, int H, int W, int C, int K, int R, int S, int pad, int P, int Q);
-int conv_halo_stats_tiles(int N, int H, int W, int C, int K, int R, int S, int pad, int P, int Q);
+// stride 2: the phase-mode kernel (four strided phase boxes per chunk).
+int conv_halo_variant(int N, int H, int W, int C, int K, int R, int S, int pad, int P, int Q, int stride = 1);
+int conv_halo_stats_tiles(int N, int H, int W, int C, int K, int R, int S, int pad, int P, int Q, int stride = 1);
 cudaError_t conv_halo(int N, int H, int W, int C, int K, int R, int S, int pad, int P, int Q, const float* x,
-                      const float* w, const float* bias, float* y, int accumulate, float* stats, cudaStream_t st);
+                      const float* w, const float* bias, float* y, int accumulate, float* stats, cudaStream_t st,
+                      int stride = 1);
 void set_conv_halo(int mode);  // 0 off, 1 by shape (default; env SN_CONV_HALO=0), 2 whenever legal (tests)
 // Halo-tiled weight gradient, C, K multiples of 64 (64 x 64 sub-problems of
 // M = 64 MMAs, all taps per CTA): partial = conv_halo_wgrad_splits() * R*S*C*K
