@@ -1872,6 +1872,7 @@ static_assert(kPbBlocks <= kRedChunks, "partials fit the reduction scratch");
 
 template <bool GATHER>
 __global__ void __launch_bounds__(kPbThreads, 2) pool_bn_stats_kernel(  // kPbBlocks: one wave
+    // (3 or 4 blocks per SM cap the registers and spill: 260 / 408 vs 228 us)
     PoolShape s, const uchar4* __restrict__ arg, const float4* __restrict__ dyp, const float4* __restrict__ dym,
     const float4* __restrict__ x, const float* __restrict__ stats, const float* __restrict__ gamma,
     const float* __restrict__ beta, int relu, int items, double* part) {
@@ -1905,6 +1906,8 @@ __global__ void __launch_bounds__(kPbThreads, 2) pool_bn_stats_kernel(  // kPbBl
         g10 = dyp[(wrow + s.Q + k0) * C4 + c4];
       }
     }
+    static_assert(kPbRun == 8, "the unrolled run");
+#pragma unroll 4
     for (int k = k0; k < k1e; ++k) {
       float4 o[4];
       const int64_t r0 = ((static_cast<int64_t>(n) * s.H + 2 * m) * s.W + 2 * k) * C4 + c4;
@@ -1985,13 +1988,11 @@ cudaError_t bn_bwd_pool_stats(const PoolShape& ps, const uint8_t* argmax, const 
   const uchar4* arg = reinterpret_cast<const uchar4*>(argmax);
   if (dy_mat) {
     pool_bn_stats_kernel<false><<<grid, kPbThreads, 0, st>>>(ps, arg, nullptr, reinterpret_cast<const float4*>(dy_mat),
-                                                             reinterpret_cast<const float4*>(x), stats, gamma, beta,
-                                                             relu, items, part);
+                                   reinterpret_cast<const float4*>(x), stats, gamma, beta, relu, items, part);
   } else {
     if (!argmax || !dy_pool) return cudaErrorInvalidValue;
     pool_bn_stats_kernel<true><<<grid, kPbThreads, 0, st>>>(ps, arg, reinterpret_cast<const float4*>(dy_pool), nullptr,
-                                                            reinterpret_cast<const float4*>(x), stats, gamma, beta,
-                                                            relu, items, part);
+                                   reinterpret_cast<const float4*>(x), stats, gamma, beta, relu, items, part);
   }
   colred_stage2<<<stage2_blocks(C), kStage2Threads, 0, st>>>(part, grid, C, BnBwdFin{C, dgamma, dbeta, coef});
   if (xskip(512)) colred_stage2<<<stage2_blocks(C), kStage2Threads, 0, st>>>(part, grid, C, BnBwdFin{C, dgamma, dbeta, coef});
@@ -2042,7 +2043,9 @@ static bool pool_k3s2_band_ok(const PoolShape& s) { return pool_k3s2_band_cs(s) 
 static void pool_k3s2_band(const PoolShape& s, bool bnr, const float* x, float* y, uint8_t* argmax,
                            const float* stats, const float* gamma, const float* beta, float* y_relu,
                            cudaStream_t st) {
-  const int PB = 4, CS = pool_k3s2_band_cs(s);
+  // 14 output rows per block (ResNet stem: 4 bands per image): 195 vs 221 us
+  // at 4 rows (fewer halo-row reloads and block starts; 14, 28 tie)
+  const int PB = 14, CS = pool_k3s2_band_cs(s);
   const dim3 grid((s.P + PB - 1) / PB, s.N, s.C / 4 / CS);
   auto k = bnr ? pool_fwd_k3s2_band_kernel<true> : pool_fwd_k3s2_band_kernel<false>;
   k<<<grid, s.Q * CS, 0, st>>>(s, PB, CS, reinterpret_cast<const float4*>(x), reinterpret_cast<float4*>(y),
