@@ -287,58 +287,79 @@ __global__ void splitk_group_kernel(float* P, int splits, int per, int64_t MN) {
 }
 
 // sstride: distance between consecutive summed slices, in slices (1, or the
-// group size after splitk_group_kernel).  One thread per element of a 32 x 32
-// tile (1024 threads), the slices read 8 at a time and summed in split order:
-// the reduction is a chain of L2 loads, so what matters is how many are in
-// flight (the round-1 version walked 4 elements x all splits one load at a
-// time per thread: ~20 us for 148 slices of a 576 x 64 weight gradient).
-constexpr int kRedTileThreads = 1024;
-__global__ void __launch_bounds__(kRedTileThreads) splitk_reduce_kernel(const float* __restrict__ P, int splits, int M,
-                                                                        int N, float* D, const float* bias,
-                                                                        int accumulate, int transpose, int sstride) {
+// group size after splitk_group_kernel).  A 32 x 32 output tile per block of
+// 32 x 8 threads, 4 elements per thread (rows ty, ty+8, ty+16, ty+24), every
+// element's slices summed from +0 in split order (the same additions as one
+// thread per element).  The reduction is a chain of L2 / DRAM loads, so what
+// matters is how many are in flight per SM: 4 elements x 4 slices per step
+// (one element per thread and 1024-thread blocks took 29 us for the two
+// 9.4 MB slices of a ResNet stage-4 3x3 weight gradient: 8 waves of blocks
+// that each waited for one load round trip).
+constexpr int kRedTileRows = 8;
+__global__ void __launch_bounds__(32 * kRedTileRows) splitk_reduce_kernel(const float* __restrict__ P, int splits,
+                                                                          int M, int N, float* D, const float* bias,
+                                                                          int accumulate, int transpose, int sstride) {
   __shared__ float tile[32][33];
   const int m0 = blockIdx.y * 32, n0 = blockIdx.x * 32;
-  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 32
-  {
-    const int m = m0 + ty, n = n0 + tx;
-    float acc = 0.f;
-    if (m < M && n < N) {
-      const size_t stride = static_cast<size_t>(M) * N * sstride;
-      const float* p = P + static_cast<size_t>(m) * N + n;
-      int s = 0;
-      for (; s + 7 < splits; s += 8) {
-        float a[8];
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  constexpr int E = 32 / kRedTileRows;           // elements per thread
+  const size_t stride = static_cast<size_t>(M) * N * sstride;
+  const int n = n0 + tx;
+  const float* p[E];
+  bool ok[E];
+  float acc[E];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) a[u] = p[(s + u) * stride];
+  for (int j = 0; j < E; ++j) {
+    const int m = m0 + ty + kRedTileRows * j;
+    ok[j] = m < M && n < N;
+    p[j] = P + (ok[j] ? static_cast<size_t>(m) * N + n : 0);
+    acc[j] = 0.f;
+  }
+  int s = 0;
+  for (; s + 3 < splits; s += 4) {
+    float a[E][4];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) acc += a[u];
-      }
-      for (; s < splits; ++s) acc += p[s * stride];
-      if (bias) acc += bias[n];
-    }
-    tile[ty][tx] = acc;
+    for (int j = 0; j < E; ++j)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) a[j][u] = ok[j] ? p[j][(s + u) * stride] : 0.f;
+#pragma unroll
+    for (int j = 0; j < E; ++j)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[j] += a[j][u];
+  }
+  for (; s < splits; ++s)
+#pragma unroll
+    for (int j = 0; j < E; ++j)
+      if (ok[j]) acc[j] += p[j][s * stride];
+#pragma unroll
+  for (int j = 0; j < E; ++j) {
+    if (ok[j] && bias) acc[j] += bias[n];
+    tile[ty + kRedTileRows * j][tx] = acc[j];
   }
   if (!transpose) {
-    const int m = m0 + ty, n = n0 + tx;
-    if (m < M && n < N) {
-      float* d = D + static_cast<size_t>(m) * N + n;
-      *d = accumulate ? *d + tile[ty][tx] : tile[ty][tx];
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+      if (!ok[j]) continue;
+      float* d = D + static_cast<size_t>(m0 + ty + kRedTileRows * j) * N + n;
+      *d = accumulate ? *d + acc[j] : acc[j];
     }
     return;
   }
   __syncthreads();
-  {
-    const int n = n0 + ty, m = m0 + tx;
-    if (m < M && n < N) {
-      float* d = D + static_cast<size_t>(n) * M + m;
-      *d = accumulate ? *d + tile[tx][ty] : tile[tx][ty];
+#pragma unroll
+  for (int j = 0; j < E; ++j) {
+    const int nn = n0 + ty + kRedTileRows * j, m = m0 + tx;
+    if (m < M && nn < N) {
+      float* d = D + static_cast<size_t>(nn) * M + m;
+      const float v = tile[tx][ty + kRedTileRows * j];
+      *d = accumulate ? *d + v : v;
     }
   }
 }
 
 cudaError_t splitk_reduce_impl(const float* P, int splits, int M, int N, float* D, const float* bias, int accumulate,
                           int transpose, cudaStream_t st) {
-  dim3 grid((N + 31) / 32, (M + 31) / 32), block(32, 32);
+  dim3 grid((N + 31) / 32, (M + 31) / 32), block(32, kRedTileRows);
   // Few output tiles and many splits: first sum groups of splits with the whole
   // GPU (in place), then reduce the group sums in order.
   const int64_t MN = static_cast<int64_t>(M) * N;
