@@ -360,6 +360,12 @@ constexpr int kCbBlocks = 2 * 148;  // one wave at 2 blocks / SM
 static_assert(kCbBlocks <= kRedChunks, "partials fit the reduction scratch");
 constexpr int kCbSmem = kCbStages * 2 * kCbStageF4 * 16;
 
+// Float4 positions per ring stage: a whole number of rows' worth of channel
+// quads (512 when C/4 divides it, else the largest multiple of C/4 below 512:
+// Inception's C = 96, 224, 384 ... -- position e of every stage then holds quad
+// e % C4 and each consumer keeps one accumulator pair per position).
+__host__ __device__ inline int bulk_stage_f4(int C4) { return (kCbStageF4 / C4) * C4; }
+
 // Row chunks of colred_bulk_bn_bwd: block b owns rows [b*ck, (b+1)*ck), at
 // least 8 ring stages per block, at most one wave.
 int64_t bulk_chunk(int64_t rows, int C, int* nblocks) {
@@ -372,7 +378,7 @@ int64_t bulk_chunk(int64_t rows, int C, int* nblocks) {
 
 bool colred_bulk_ok(int C) {
   const int C4 = C / 4;
-  return C % 4 == 0 && C4 >= 1 && C4 <= kCbStageF4 && kCbStageF4 % C4 == 0;
+  return C % 4 == 0 && C4 >= 1 && C4 <= kCbStageF4;
 }
 
 __global__ void __launch_bounds__(kCbThreads, 2)
@@ -383,7 +389,8 @@ __global__ void __launch_bounds__(kCbThreads, 2)
   const int64_t r0 = static_cast<int64_t>(blockIdx.x) * chunk;
   const int64_t r1 = r0 + chunk < rows ? r0 + chunk : rows;
   const int64_t f0 = r0 * C4, nf = (r1 - r0) * C4;  // float4 range of this block
-  const int nst = static_cast<int>((nf + kCbStageF4 - 1) / kCbStageF4);
+  const int sf4 = bulk_stage_f4(C4);  // positions per stage
+  const int nst = static_cast<int>((nf + sf4 - 1) / sf4);
   const int t = threadIdx.x, warp = t >> 5;
   if (t == 0) {
     for (int i = 0; i < kCbStages; ++i) {
@@ -396,16 +403,17 @@ __global__ void __launch_bounds__(kCbThreads, 2)
   const float4* dy4 = reinterpret_cast<const float4*>(op.dy);
   const float4* x4 = reinterpret_cast<const float4*>(op.x);
   float4 a0 = zero4(), b0 = zero4(), a1 = zero4(), b1 = zero4();
-  const int nq = C4 > kCbConsumers ? 2 : 1;  // distinct quads per consumer
+  // distinct quads per consumer: positions t and t + 256 share a quad when
+  // C4 divides 256 (one accumulator pair), else each keeps its own
+  const int nq = (C4 > kCbConsumers || kCbConsumers % C4 != 0) ? 2 : 1;
   if (warp == kCbConsumers / 32) {
     if (t == kCbConsumers) {
       for (int it = 0; it < nst; ++it) {
         const int s = it % kCbStages;
         if (it >= kCbStages) mbar_wait(&empty[s], ((it / kCbStages) - 1) & 1);
-        const int64_t off = f0 + static_cast<int64_t>(it) * kCbStageF4;
-        const int n = static_cast<int>(nf - static_cast<int64_t>(it) * kCbStageF4 < kCbStageF4
-                                           ? nf - static_cast<int64_t>(it) * kCbStageF4
-                                           : kCbStageF4);
+        const int64_t off = f0 + static_cast<int64_t>(it) * sf4;
+        const int n = static_cast<int>(nf - static_cast<int64_t>(it) * sf4 < sf4 ? nf - static_cast<int64_t>(it) * sf4
+                                                                                  : sf4);
         mbar_arrive_expect_tx(&full[s], 2u * n * 16u);
         bulk_load_1d(ring + (s * 2) * kCbStageF4, dy4 + off, n * 16u, &full[s]);
         bulk_load_1d(ring + (s * 2 + 1) * kCbStageF4, x4 + off, n * 16u, &full[s]);
@@ -417,9 +425,9 @@ __global__ void __launch_bounds__(kCbThreads, 2)
     for (int it = 0; it < nst; ++it) {
       const int s = it % kCbStages;
       mbar_wait(&full[s], (it / kCbStages) & 1);
-      const int64_t off = f0 + static_cast<int64_t>(it) * kCbStageF4;
-      const int64_t left = nf - static_cast<int64_t>(it) * kCbStageF4;
-      const int n = static_cast<int>(left < kCbStageF4 ? left : kCbStageF4);
+      const int64_t off = f0 + static_cast<int64_t>(it) * sf4;
+      const int64_t left = nf - static_cast<int64_t>(it) * sf4;
+      const int n = static_cast<int>(left < sf4 ? left : sf4);
       if (t < n) {
         const RedBnBwdOp::R r{ring[(s * 2) * kCbStageF4 + t], ring[(s * 2 + 1) * kCbStageF4 + t]};
         op.side((off + t) * 4, r);
