@@ -73,6 +73,7 @@ struct LayerRt {
   sn::ConvKnobs kf{}, kd{}, kw{};
   int stats_tiles = 0, stats_rows = 0;  // CONV: BN statistics tiles its forward can emit
   uint8_t* argmax = nullptr;            // max POOL: per-output window argmax saved by the forward
+  float* wt_pre = nullptr;              // CONV: its dgrad weights, transformed once per step (prep_dgrad_weights)
 };
 
 struct Action {
@@ -114,6 +115,7 @@ struct sn_exec {
   float* loss = nullptr;
   uint32_t* iteration = nullptr;
   float* wt_scratch = nullptr;
+  sn::DgradPrepJob* prep_jobs = nullptr;  // the batched dgrad weight transforms (device table)
   float* partial = nullptr;
   int64_t partial_cap = 0;
   float* red = nullptr;
@@ -651,6 +653,8 @@ struct Compiler {
   std::unordered_map<int64_t, cudaEvent_t> side_reads;
   std::unordered_map<int, cudaEvent_t> wgrad_done;  // CONV layer -> its s3 weight-gradient completion
   bool used_s5 = false;
+  cudaEvent_t wt_ready = nullptr;  // every CONV's dgrad weights prepared (s3); s0 waits before the first dgrad
+  bool wt_waited = false;
   size_t next_bucket = 0;
   int data_id = -1;
 
@@ -1022,7 +1026,12 @@ struct Compiler {
         const float* w = ex->params + l.w_off;
         float* dw = ex->grads + l.w_off;
         float* db = ex->grads + l.b_off;
-        float* wt = ex->wt_scratch;
+        const int pre = l.wt_pre && dx ? 1 : 0;
+        float* wt = pre ? l.wt_pre : ex->wt_scratch;
+        if (pre && !wt_waited) {
+          s0_wait(wt_ready);
+          wt_waited = true;
+        }
         float* part = ex->partial;
         float* red = ex->red;
         if (conv_bias_done[lid]) db = nullptr;  // summed by the BN backward's dx pass
@@ -1087,7 +1096,7 @@ struct Compiler {
         int ndgrad = 0, nwgrad = 0;
         {
           sn::KnobScope ks(kd);
-          ndgrad = !dx ? 0 : sn::conv_dgrad_launches(cs);
+          ndgrad = !dx ? 0 : sn::conv_dgrad_launches(cs, pre);
         }
         {
           sn::KnobScope ks(kw);
@@ -1104,7 +1113,7 @@ struct Compiler {
           ck(cudaEventRecord(wdone, sw), "record");
           if (dx) {
             sn::KnobScope ks(kd);
-            ck(sn::conv_dgrad(cs, dy, w, wt, dx, acc, st), "conv_dgrad");
+            ck(sn::conv_dgrad(cs, dy, w, wt, dx, acc, st, pre), "conv_dgrad");
           }
         }, nwgrad + ndgrad);
         (void)nbias;
@@ -2095,11 +2104,67 @@ struct Compiler {
     }
   }
 
+  // The weights do not change within a step: every CONV's dgrad weight
+  // transform (flipped / transposed filter, sub-pixel blocks) runs at the start
+  // of the iteration as ONE batched launch on the side stream s3, overlapping
+  // the forward, into per-layer buffers outside the pool (sn_exec_memory:
+  // "dgrad weights") -- instead of one short launch per layer on the backward's
+  // dgrad chain (ResNet-2534g b16: 842 launches, ~2.4 us each in the graph).
+  static constexpr int kPrepMinJobs = 64;
+  void prep_dgrad_weights() {
+    const char* env = std::getenv("SN_DGRAD_PREP");  // A/B: 0 = never, 1 = always (tests)
+    if (env && env[0] == '0') return;
+    std::vector<sn::DgradPrepJob> jobs;
+    for (int i = 0; i < net.n; ++i) {
+      LayerRt& l = ex->L[i];
+      if (l.kind != snp::CONV || i == ex->stem_layer || net.prev[i].empty()) continue;
+      if (ex->eff_owner[net.prev[i][0]] < 0) continue;  // no input gradient: no dgrad
+      sn::KnobScope ks(l.kd);
+      sn::DgradPrepJob job{};
+      if (!sn::conv_dgrad_prep_job(l.conv, ex->params + l.w_off, nullptr, &job)) continue;
+      ex->dmalloc(&l.wt_pre, sn::conv_dgrad_scratch_floats(l.conv) * 4, sn_exec::M_PARAMS, "cudaMalloc(dgrad weights)");
+      job.wt = l.wt_pre;
+      jobs.push_back(job);
+    }
+    // Only deep nets gain: the batched launch at the step start contends with
+    // the first forward kernels (ResNet-50g b256, 13 jobs: 9.03 -> 9.11 ms),
+    // while ResNet-2534g b16 (842 jobs) saves 82.3 -> 80.5 ms.
+    if (static_cast<int>(jobs.size()) < kPrepMinJobs && !(env && env[0] == '1')) {
+      for (int i = 0; i < net.n; ++i)
+        if (ex->L[i].wt_pre) {
+          cudaFree(ex->L[i].wt_pre);
+          ex->mem[sn_exec::M_PARAMS] -= sn::conv_dgrad_scratch_floats(ex->L[i].conv) * 4;
+          ex->L[i].wt_pre = nullptr;
+        }
+      return;
+    }
+    ex->dmalloc(&ex->prep_jobs, static_cast<int64_t>(jobs.size() * sizeof(sn::DgradPrepJob)), sn_exec::M_OTHER,
+                "cudaMalloc(dgrad weight jobs)");
+    sn::DgradPrepJob* d_jobs = ex->prep_jobs;
+    ck(cudaMemcpy(d_jobs, jobs.data(), jobs.size() * sizeof(sn::DgradPrepJob), cudaMemcpyHostToDevice),
+       "memcpy(dgrad weight jobs)");
+    cur_layer = -1, cur_type = 3;
+    wt_ready = ex->new_event();
+    cudaEvent_t go = ex->new_event(), ready = wt_ready;  // locals: the action outlives this Compiler
+    used_s3 = true;
+    sn_exec* e = ex;
+    cudaStream_t s0 = ex->s0, s3 = ex->s3;
+    const int nj = static_cast<int>(jobs.size());
+    push([=] {
+      const cudaStream_t sw = e->serial ? s0 : s3;
+      ck(cudaEventRecord(go, s0), "record");
+      ck(cudaStreamWaitEvent(sw, go, 0), "wait");
+      ck(sn::conv_dgrad_prep_batch(d_jobs, nj, sw), "conv_dgrad_prep_batch");
+      ck(cudaEventRecord(ready, sw), "record");
+    }, 1);
+  }
+
   void compile() {
     for (int i = 0; i < net.n; ++i)
       if (ex->side_root[i]) fresh[i] = true;  // side gradient buffers: the first write overwrites
     plan_fusions();
     size_wgrad_scratch();
+    prep_dgrad_weights();
     prepare_inputs();
     const bool images_in_place = ex->data_buf == ex->images;
     if (!images_in_place) inputs_consumed();
@@ -2269,8 +2334,11 @@ void destroy(sn_exec* ex) {
                   const_cast<float**>(ex->ptr_table), ex->marker, ex->update_flag};
   for (void* b : bufs)
     if (b) cudaFree(b);
-  for (auto& l : ex->L)
+  for (auto& l : ex->L) {
     if (l.argmax) cudaFree(l.argmax);
+    if (l.wt_pre) cudaFree(l.wt_pre);
+  }
+  if (ex->prep_jobs) cudaFree(ex->prep_jobs);
   for (auto& kv : ex->side) cudaFree(kv.second);
   if (ex->s0) cudaStreamDestroy(ex->s0);
   if (ex->s1) cudaStreamDestroy(ex->s1);

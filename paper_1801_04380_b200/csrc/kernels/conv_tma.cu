@@ -1866,10 +1866,10 @@ cudaError_t conv_dgrad_strided_tma(const ConvShape& s, const float* dy, const fl
 // re-read dy with 64..256-wide tiles and 4..16 k blocks.  7 of the 16 (tap,
 // phase) weight blocks are zero (56% useful MMA work, at the full 256-wide rate).
 // wsub[(a*2+b)*C + c][(dr*2+ds)*K + k] = w[k][a-2dr+1][b-2ds+1][c] or 0.
-__global__ void subpix_weights_kernel(const float* __restrict__ w, float* __restrict__ wsub, int K, int C) {
+__device__ void subpix_weights_range(const float* __restrict__ w, float* __restrict__ wsub, int K, int C, int64_t i0,
+                                     int64_t step) {
   const int64_t total = static_cast<int64_t>(16) * C * K;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+  for (int64_t i = i0; i < total; i += step) {
     const int k = static_cast<int>(i % K);
     int64_t t = i / K;
     const int tap = static_cast<int>(t % 4);
@@ -1880,6 +1880,10 @@ __global__ void subpix_weights_kernel(const float* __restrict__ w, float* __rest
     wsub[i] = (r >= 0 && q >= 0) ? w[((static_cast<int64_t>(k) * 3 + r) * 3 + q) * C + c] : 0.f;
   }
 }
+__global__ void subpix_weights_kernel(const float* __restrict__ w, float* __restrict__ wsub, int K, int C) {
+  subpix_weights_range(w, wsub, K, C, blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x,
+                       static_cast<int64_t>(gridDim.x) * blockDim.x);
+}
 
 bool conv_dgrad_subpix_ok(const ConvShape& s) {
   return s.R == 3 && s.S == 3 && s.stride == 2 && s.pad == 1 && s.H == 2 * s.P && s.W == 2 * s.Q &&
@@ -1887,12 +1891,14 @@ bool conv_dgrad_subpix_ok(const ConvShape& s) {
 }
 
 cudaError_t conv_dgrad_subpix_tma(const ConvShape& s, const float* dy, const float* w, float* wt_scratch, float* dx,
-                                  int accumulate, cudaStream_t st) {
+                                  int accumulate, cudaStream_t st, int prepped) {
   if (!conv_dgrad_subpix_ok(s)) return cudaErrorInvalidValue;
-  const int64_t wn = static_cast<int64_t>(16) * s.C * s.K;
-  subpix_weights_kernel<<<std::min<int64_t>(1184, (wn + 255) / 256), 256, 0, st>>>(w, wt_scratch, s.K, s.C);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
+  if (!prepped) {
+    const int64_t wn = static_cast<int64_t>(16) * s.C * s.K;
+    subpix_weights_kernel<<<std::min<int64_t>(1184, (wn + 255) / 256), 256, 0, st>>>(w, wt_scratch, s.K, s.C);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
   // im2col over dy (P x Q grid), window 2x2 at (u, v); row/col P, Q read as 0
   CUtensorMap A, B, D;
   if (!make_im2col(&A, dy, s.N, s.P, s.Q, s.K, 0, 0, 0, 0, 1, kBM, CU_TENSOR_MAP_SWIZZLE_128B))
@@ -1988,6 +1994,45 @@ cudaError_t conv_wgrad_tma(const ConvShape& s, const float* x, const float* dy, 
     case 128: return launch<128, 1>(A, B, D, a, e, a.RSC, s.K, splits, st);
     default: return launch<256, 1>(A, B, D, a, e, a.RSC, s.K, splits, st);
   }
+}
+
+
+// Every layer's dgrad weight transform of a step in one launch: block row y =
+// job y, blocks along x walk that job's 32 x 32 transpose tiles (the same
+// element map as transpose_w_kernel in gemm_ops.cu) or its sub-pixel elements.
+__global__ void __launch_bounds__(256) dgrad_prep_batch_kernel(const DgradPrepJob* __restrict__ jobs) {
+  __shared__ float tile[32][33];
+  const DgradPrepJob j = jobs[blockIdx.y];
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  if (j.subpix) {
+    subpix_weights_range(j.w, j.wt, j.K, j.C, static_cast<int64_t>(blockIdx.x) * 256 + tid,
+                         static_cast<int64_t>(gridDim.x) * 256);
+    return;
+  }
+  const int tcx = (j.C + 31) / 32, tky = (j.K + 31) / 32;
+  const int nt = tcx * tky * j.RS;
+  for (int t = blockIdx.x; t < nt; t += gridDim.x) {
+    const int rs_in = t / (tcx * tky);
+    const int rem = t - rs_in * tcx * tky;
+    const int c0 = (rem % tcx) * 32, k0 = (rem / tcx) * 32;
+    const int rs = j.flip ? j.RS - 1 - rs_in : rs_in;
+    for (int i = threadIdx.y; i < 32; i += 8) {
+      const int k = k0 + i, c = c0 + threadIdx.x;
+      tile[i][threadIdx.x] = (k < j.K && c < j.C) ? j.w[(static_cast<size_t>(k) * j.RS + rs_in) * j.C + c] : 0.f;
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += 8) {
+      const int c = c0 + i, k = k0 + threadIdx.x;
+      if (k < j.K && c < j.C) j.wt[(static_cast<size_t>(c) * j.RS + rs) * j.K + k] = tile[threadIdx.x][i];
+    }
+    __syncthreads();
+  }
+}
+
+cudaError_t conv_dgrad_prep_batch(const DgradPrepJob* jobs, int njobs, cudaStream_t st) {
+  if (njobs <= 0) return cudaSuccess;
+  dgrad_prep_batch_kernel<<<dim3(64, njobs), dim3(32, 8), 0, st>>>(jobs);
+  return cudaGetLastError();
 }
 
 }  // namespace sn

@@ -525,10 +525,18 @@ void set_conv_knobs(const ConvKnobs& k) {
   set_conv_subpix(k.subpix);
 }
 
-int conv_dgrad_launches(const ConvShape& s) {
-  if (use_subpix(s)) return 2;
+int conv_dgrad_launches(const ConvShape& s, int prepped) {
+  if (use_subpix(s)) return prepped ? 1 : 2;
   if (use_tma() && conv_tma_ok_dgrad_strided(s)) return 2 * s.stride * s.stride;
-  return 2;
+  return prepped ? 1 : 2;
+}
+
+bool conv_dgrad_prep_job(const ConvShape& s, const float* w, float* wt, DgradPrepJob* job) {
+  const bool sub = use_subpix(s);
+  if (!sub && use_tma() && conv_tma_ok_dgrad_strided(s)) return false;
+  const bool tma = use_tma() && conv_tma_ok_dgrad(s);
+  *job = DgradPrepJob{w, wt, s.K, s.R * s.S, s.C, tma ? 1 : 0, sub ? 1 : 0};
+  return true;
 }
 
 int64_t conv_dgrad_scratch_floats(const ConvShape& s) {
@@ -537,14 +545,16 @@ int64_t conv_dgrad_scratch_floats(const ConvShape& s) {
 }
 
 cudaError_t conv_dgrad(const ConvShape& s, const float* dy, const float* w, float* wt, float* dx, int accumulate,
-                       cudaStream_t st) {
-  if (use_subpix(s)) return conv_dgrad_subpix_tma(s, dy, w, wt, dx, accumulate, st);
+                       cudaStream_t st, int prepped) {
+  if (use_subpix(s)) return conv_dgrad_subpix_tma(s, dy, w, wt, dx, accumulate, st, prepped);
   if (use_tma() && conv_tma_ok_dgrad_strided(s)) return conv_dgrad_strided_tma(s, dy, w, wt, dx, accumulate, st);
-  dim3 grid((s.C + 31) / 32, (s.K + 31) / 32, s.R * s.S), block(32, 8);
   const bool tma = use_tma() && conv_tma_ok_dgrad(s);
   if (xskip(64)) return cudaSuccess;
-  transpose_w_kernel<<<grid, block, 0, st>>>(w, wt, s.K, s.R * s.S, s.C, tma ? 1 : 0);
-  if (xskip(1024)) transpose_w_kernel<<<grid, block, 0, st>>>(w, wt, s.K, s.R * s.S, s.C, tma ? 1 : 0);
+  if (!prepped) {
+    dim3 grid((s.C + 31) / 32, (s.K + 31) / 32, s.R * s.S), block(32, 8);
+    transpose_w_kernel<<<grid, block, 0, st>>>(w, wt, s.K, s.R * s.S, s.C, tma ? 1 : 0);
+    if (xskip(1024)) transpose_w_kernel<<<grid, block, 0, st>>>(w, wt, s.K, s.R * s.S, s.C, tma ? 1 : 0);
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (tma) {

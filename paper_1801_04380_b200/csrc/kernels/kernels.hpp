@@ -25,8 +25,23 @@ cudaError_t conv_fwd(const ConvShape& s, const float* x, const float* w, const f
 // instead of 3).  The partial buffer needs tiles * 4 * K floats.
 int conv_fwd_stats_tiles(const ConvShape& s, bool stem, int* tile_rows);
 // dx[N*H*W][C] (+)= conv_transpose(dy, w); wt = scratch of K*R*S*C floats.
+// prepped: wt already holds this layer's transformed dgrad weights (the
+// executor prepares every layer's once per step, in one batched launch off the
+// backward's dgrad chain: conv_dgrad_prep_job / conv_dgrad_prep_batch).
 cudaError_t conv_dgrad(const ConvShape& s, const float* dy, const float* w, float* wt, float* dx,
-                       int accumulate, cudaStream_t st);
+                       int accumulate, cudaStream_t st, int prepped = 0);
+// One layer's dgrad weight transform: the flipped / transposed filter or the
+// sub-pixel blocks, exactly what conv_dgrad would launch first.
+struct DgradPrepJob {
+  const float* w;
+  float* wt;
+  int K, RS, C, flip, subpix;
+};
+// Fills *job for this shape's dgrad path under the current knobs; false when
+// that path transforms its weights otherwise (the phase-decomposed strided dgrad).
+bool conv_dgrad_prep_job(const ConvShape& s, const float* w, float* wt, DgradPrepJob* job);
+// All jobs (device array) in one launch.
+cudaError_t conv_dgrad_prep_batch(const DgradPrepJob* jobs, int njobs, cudaStream_t st);
 // dw[K][R*S*C] = sum_pixels im2col(x)^T dy ; db[K] = column sums of dy (skipped if db is null).
 // partial: scratch of splits*R*S*C*K floats (see conv_wgrad_splits).
 // the halo weight-gradient kernels: their partial-slice count is fixed by the
@@ -118,9 +133,9 @@ bool conv_tma_ok_dgrad_strided(const ConvShape& s);
 // must hold 16*C*K floats (conv_dgrad_scratch_floats)
 bool conv_dgrad_subpix_ok(const ConvShape& s);
 cudaError_t conv_dgrad_subpix_tma(const ConvShape& s, const float* dy, const float* w, float* wt_scratch, float* dx,
-                                  int accumulate, cudaStream_t st);
+                                  int accumulate, cudaStream_t st, int prepped = 0);
 void set_conv_subpix(int on);          // 0: phase-decomposed strided dgrad (A/B, tests)
-int conv_dgrad_launches(const ConvShape& s);          // kernels one conv_dgrad issues
+int conv_dgrad_launches(const ConvShape& s, int prepped = 0);  // kernels one conv_dgrad issues
 int64_t conv_dgrad_scratch_floats(const ConvShape& s);  // wt scratch conv_dgrad needs
 cudaError_t conv_dgrad_strided_tma(const ConvShape& s, const float* dy, const float* w, float* wt_scratch, float* dx,
                                    int accumulate, cudaStream_t st);

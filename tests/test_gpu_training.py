@@ -656,3 +656,22 @@ def test_stem_pool_gather_bit_identical_across_schedules(cuda, monkeypatch, feat
     monkeypatch.setenv("SN_FUSE_POOL_GATHER", "0")
     loss0, grads0, _, _ = _run(net, 8, 4 << 30, feats, params, images, labels)
     assert loss == loss0 and _bitwise(grads, grads0)
+
+
+@pytest.mark.parametrize("feats", ["none", ALL])
+def test_batched_dgrad_weight_prep_is_bit_identical(cuda, monkeypatch, feats):
+    """Every CONV's dgrad weight transform run once per step in one batched
+    launch on the side stream (SN_DGRAD_PREP=1; the default for nets with >= 64
+    such layers) gives exactly the per-dgrad transforms: flipped / transposed
+    stride-1 filters and the sub-pixel blocks of the stride-2 convolutions."""
+    from paper_1801_04380_b200.netgen import gen_resnet
+    from paper_1801_04380_b200.training import init_parameters
+    net = gen_resnet(1, 2, 2, 1)
+    params = init_parameters(net, seed=8, head_scale=0.1)
+    images, labels = _inputs(net, 4, seed=5)
+    monkeypatch.setenv("SN_DGRAD_PREP", "1")
+    loss1, grads1, _, t1 = _run(net, 4, 4 << 30, feats, params, images, labels)
+    monkeypatch.setenv("SN_DGRAD_PREP", "0")
+    loss0, grads0, _, t0 = _run(net, 4, 4 << 30, feats, params, images, labels)
+    assert t1.kernels < t0.kernels  # one batched launch replaces one per layer
+    assert loss1 == loss0 and _bitwise(grads1, grads0)
