@@ -494,6 +494,17 @@ def extras(args, net, cfg, ex, ms_per_step, local) -> dict:
         out["roofline_hbm_layers"].update(achieved=round(gbs, 1), frac=round(gbs / hbm_peak, 4),
                                           how="ncu DRAM bytes of these launches (same libsnexec digest) / their "
                                               "summed CUDA-event durations this run (kernel replay, median of 5)")
+    hb = tr.get("hbm_bulk") if traffic else None
+    if hb and hb.get("flat_kernel_indices") and len(ks) == traffic.get("launches"):
+        b_us = sum(ks[i]["us"] for i in hb["flat_kernel_indices"])
+        gbs = hb["dram_bytes_per_step"] / (b_us / 1e6) / 1e9
+        out["roofline_hbm_layers"]["bulk"] = {
+            "launches": hb["launches"], "min_bytes_per_launch": hb["min_bytes_per_launch"],
+            "traffic": hb["dram_bytes_per_step"], "kernel_us_per_step": round(b_us, 1), "achieved": round(gbs, 1),
+            "frac": round(gbs / hbm_peak, 4),
+            "how": "the HBM launches moving >= 50 MB each (BN statistics / dx passes, BN apply + JOIN, pool, stem "
+                   "pad): their ncu DRAM bytes / their summed CUDA-event durations this run; the rest of the class is "
+                   "short latency-bound launches (finalisers, tile statistics, weight transposes, split-K reductions)"}
     out["time_by_layer_kind_ms"] = {k: round(v, 3) for k, v in sorted(by_kind.items(), key=lambda kv: -kv[1])}
 
     def side_run(label, cfg2, steps=5, **kw):

@@ -124,6 +124,9 @@ def read_ncu(path: str) -> list[dict]:
     return list(launches.values())
 
 
+BULK = 50e6  # bytes per launch
+
+
 def merge(args) -> None:
     lt = json.load(open(args.json))
     launches = read_ncu(args.csv)
@@ -144,7 +147,10 @@ def merge(args) -> None:
         sys.exit(f"census / ncu launch names differ at {len(bad)} launches, first {bad[0]}")
     rows = []
     cls = collections.defaultdict(lambda: {"launches": 0, "s": 0.0, "dram": 0.0, "flops": 0.0})
-    for ((a, kname), L), ki in zip(zip(flat, launches), kinfo):
+    # the bulk HBM launches (>= BULK bytes each): where the layer kernels' roofline is decided;
+    # the many short launches (finalisers, tile statistics, weight transposes) are latency
+    bulk = {"launches": 0, "s": 0.0, "dram": 0.0, "flops": 0.0, "flat": []}
+    for fi, (((a, kname), L), ki) in enumerate(zip(zip(flat, launches), kinfo)):
         m = L["m"]
         t = m.get("gpu__time_duration.sum", 0.0)
         dram = m.get("dram__bytes_read.sum", 0.0) + m.get("dram__bytes_write.sum", 0.0)
@@ -160,6 +166,11 @@ def merge(args) -> None:
         c["s"] += t
         c["dram"] += dram
         c["flops"] += flops
+        if not tensor and dram >= BULK:
+            bulk["launches"] += 1
+            bulk["s"] += t
+            bulk["dram"] += dram
+            bulk["flat"].append(fi)
         rows.append({"i": a["i"], "layer": a.get("name", "-"), "type": a["type"], "kernel": L["name"][:70],
                      "dims": dims, "us": t * 1e6, "ev_us": ki["us"], "flops": flops, "dram": dram,
                      "tflops": flops / t / 1e12 if t and flops else None, "gbs": dram / t / 1e9 if t else None,
@@ -178,6 +189,9 @@ def merge(args) -> None:
         md.append(f"| {k} | {c['launches']} | {c['s'] * 1e3:.3f} | {c['s'] / tot:.3f} | {c['dram'] / 1e9:.3f} | "
                   f"{c['dram'] / c['s'] / 1e9:.0f} | {c['flops'] / 1e12:.4f} | "
                   f"{(c['flops'] / c['s'] / 1e12) if c['flops'] else 0:.1f} |")
+    if bulk["launches"]:
+        md.append(f"| of which hbm launches moving >= {BULK / 1e6:.0f} MB | {bulk['launches']} | {bulk['s'] * 1e3:.3f} | "
+                  f"{bulk['s'] / tot:.3f} | {bulk['dram'] / 1e9:.3f} | {bulk['dram'] / bulk['s'] / 1e9:.0f} | | |")
     md += ["", "`us` = ncu gpu__time_duration (cold); `ev us` = CUDA-event time of the same kernel in a node-by-node "
            "replay of the iteration (warm, `sn_exec_kernel_times`, median of 5); TF/s from the ncu time.", "",
            "`TC smem %` = tensor-core operand reads from shared memory, % of their peak "
@@ -201,6 +215,9 @@ def merge(args) -> None:
                "per_step": {("conv_fc_gemm" if k.startswith("tensor") else "hbm_layers"):
                             {"launches": c["launches"], "dram_bytes_per_step": c["dram"], "ncu_ms": c["s"] * 1e3,
                              "algorithmic_tflop": c["flops"] / 1e12} for k, c in cls.items()}}
+    traffic["per_step"]["hbm_bulk"] = {"min_bytes_per_launch": BULK, "launches": bulk["launches"],
+                                       "dram_bytes_per_step": bulk["dram"], "ncu_ms": bulk["s"] * 1e3,
+                                       "flat_kernel_indices": bulk["flat"]}
     with open(os.path.join(ROOT, "profiles", f"{tag}_step_traffic.json"), "w") as fh:
         json.dump(traffic, fh, indent=1)
     print(f"profiles/{tag}_launches.md, profiles/{tag}_step_traffic.json")
