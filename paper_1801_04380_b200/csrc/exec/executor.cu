@@ -880,6 +880,7 @@ struct Compiler {
         const float eps = l.num.bn_eps, mom = l.num.bn_momentum;
         const int compute = replay ? 0 : 1;
         float* red = ex->red;
+        if (fuse_next) bn_in_ptr[lid] = x;  // the deferred apply reads it (see bn_input)
         if (bn_tiles_now && !replay) {
           // statistics from the producing CONV's epilogue tiles
           const float* ts = ex->tstats;
@@ -908,7 +909,7 @@ struct Compiler {
         if (dead_at[cur_ti]) break;                                // output never read (plan_fusions)
         if (fused_bn >= 0) {
           const LayerRt& bl = ex->L[fused_bn];
-          const float* bx = ptr(snp::K_ACT, net.prev[fused_bn][0]);
+          const float* bx = bn_input(fused_bn);
           // the BN output this ReLU reads; not written when nothing else reads it
           float* by = elide_out[fused_bn] ? nullptr : const_cast<float*>(x);
           const float* g = ex->params + bl.w_off;
@@ -929,7 +930,7 @@ struct Compiler {
           const int ra = P.tape[pool_from[cur_ti]].b;
           const int bn = net.prev[ra][0];
           const LayerRt& bl = ex->L[bn];
-          const float* bx = ptr(snp::K_ACT, net.prev[bn][0]);
+          const float* bx = bn_input(bn);
           float* ry = elide_out[ra] ? nullptr : ptr(snp::K_ACT, ra);
           const float* g = ex->params + bl.w_off;
           const float* b = ex->params + bl.b_off;
@@ -970,7 +971,7 @@ struct Compiler {
           const int ra = P.tape[join_from[cur_ti]].b;
           const int bn = net.prev[ra][0];
           const LayerRt& bl = ex->L[bn];
-          const float* bx = ptr(snp::K_ACT, net.prev[bn][0]);
+          const float* bx = bn_input(bn);
           float* by = elide_out[bn] ? nullptr : ptr(snp::K_ACT, bn);
           float* ry = elide_out[ra] ? nullptr : ptr(snp::K_ACT, ra);
           const int other = net.prev[lid][0] == ra ? net.prev[lid][1] : net.prev[lid][0];
@@ -1395,6 +1396,17 @@ struct Compiler {
   // pair is fused as well, nothing reads the BN output, so it is not written.
   bool fuse_next = false;
   int fused_bn = -1;
+  // BN input of a deferred (fused) apply, recorded at the BN: the tape may free
+  // it before the consuming ReLU / POOL / JOIN runs (plan_fusions checks that
+  // nothing is allocated over it meanwhile)
+  std::unordered_map<int, const float*> bn_in_ptr;
+  const float* bn_input(int bn) {
+    const int p = net.prev[bn][0];
+    if (where.count(snp::key_code(snp::K_ACT, p))) return ptr(snp::K_ACT, p);
+    auto it = bn_in_ptr.find(bn);
+    if (it == bn_in_ptr.end()) xfail(SN_EK_INTERNAL, "fused BN apply: input neither resident nor recorded");
+    return it->second;
+  }
   size_t cur_ti = 0;
   // BN+ReLU (fused) forward / replay whose next compute action is the same op
   // of a 2-input JOIN reading the ReLU: the whole chain runs at the JOIN.
@@ -1461,6 +1473,7 @@ struct Compiler {
   bool bwd_skip = false, bwd_relu = false;
   std::vector<char> fuse_at, act_bwd_skip, bn_bwd_relu;
   std::vector<int> fused_into;
+  std::vector<char> fused_x_freed;  // that BN+ReLU fusion reads a BN input the tape freed before the ReLU
   std::vector<char> elide_out;  // per layer: output never materialised
   static bool is_compute(char op) { return op == 'C' || op == 'R' || op == 'B'; }
   bool bn_relu_pair(int act) const {
@@ -1472,6 +1485,7 @@ struct Compiler {
     const size_t T = P.tape.size();
     fuse_at.assign(T, 0);
     fused_into.assign(T, -1);
+    fused_x_freed.assign(T, 0);
     act_bwd_skip.assign(T, 0);
     bn_bwd_relu.assign(T, 0);
     elide_out.assign(net.n, 0);
@@ -1531,13 +1545,41 @@ struct Compiler {
       if ((e.op != 'C' && e.op != 'R') || net.kind[e.b] != snp::BN) continue;
       const int bn = e.b;
       if (ex->L[bn].C % 4 != 0 || net.prev[bn].empty()) continue;
+      // The BN input may be freed before the ReLU runs (DenseNet-style: the JOIN
+      // output feeding the BN is dropped right after the BN, for recompute): the
+      // fused apply at the ReLU still reads it, so that is allowed only while no
+      // allocation lands on its blocks, except the ReLU's own output at exactly
+      // those blocks (elementwise in place: each element read, then written).
+      const int bx = net.prev[bn][0];
+      int64_t xoff = -1, xblk = 0;
+      bool x_freed = false;
+      for (size_t j = i; j-- > 0;) {
+        const snp::Event& f = P.tape[j];
+        if (f.op == 'A' && f.a == snp::K_ACT && f.b == bx) {
+          xoff = f.c;
+          xblk = f.d;
+          break;
+        }
+      }
       for (size_t j = i + 1; j < T; ++j) {
         const snp::Event& f = P.tape[j];
-        if (f.op == 'F' && f.a == snp::K_ACT && (f.b == bn || f.b == net.prev[bn][0])) break;
+        if (f.op == 'F' && f.a == snp::K_ACT && f.b == bn) break;
+        if (f.op == 'F' && f.a == snp::K_ACT && f.b == bx) {
+          if (xoff < 0 || net.kind[bx] == snp::DATA) break;
+          x_freed = true;
+          continue;
+        }
+        if (x_freed && f.op == 'A' && overlap(f.c, f.d, xoff, xblk)) {
+          const bool own_out = f.a == snp::K_ACT && net.kind[f.b] == snp::ACT && net.prev[f.b].size() == 1 &&
+                               net.prev[f.b][0] == bn && f.c == xoff && f.d == xblk;
+          if (!own_out) break;
+          continue;
+        }
         if (f.op == 'C' || f.op == 'R' || f.op == 'B' || f.op == 'O' || f.op == 'P' || f.op == 'D') {
           if (f.op == e.op && net.kind[f.b] == snp::ACT && net.prev[f.b].size() == 1 && net.prev[f.b][0] == bn) {
             fuse_at[i] = 1;
             fused_into[j] = bn;
+            fused_x_freed[j] = x_freed ? 1 : 0;
           }
           break;
         }
@@ -1592,7 +1634,7 @@ struct Compiler {
     // read or written at the JOIN).
     std::vector<int> act_join_fused(net.n, 0);
     for (size_t i = 0; i < T; ++i) {
-      if (fused_into[i] < 0) continue;
+      if (fused_into[i] < 0 || fused_x_freed[i]) continue;  // launched at the ReLU only
       const snp::Event& e = P.tape[i];
       const int ra = e.b, bn = fused_into[i], bin = net.prev[bn][0];
       for (size_t j = i + 1; j < T; ++j) {
@@ -1620,7 +1662,7 @@ struct Compiler {
     for (size_t i = 0; i < T; ++i) {
       const snp::Event& e = P.tape[i];
       if ((e.op == 'C' || e.op == 'R') && net.kind[e.b] == snp::POOL) ++pool_fwd_n[e.b];
-      if (fused_into[i] < 0 || join_fuse_at[i] >= 0) continue;
+      if (fused_into[i] < 0 || fused_x_freed[i] || join_fuse_at[i] >= 0) continue;
       const int ra = e.b, bn = fused_into[i], bin = net.prev[bn][0];
       for (size_t j = i + 1; j < T; ++j) {
         const snp::Event& f = P.tape[j];
@@ -1743,7 +1785,17 @@ struct Compiler {
       bool read = false;
       for (size_t j = i + 1; j < T && !read; ++j) {
         const snp::Event& f = P.tape[j];
-        if (f.op == 'F' && f.a == snp::K_ACT && f.b == L) break;
+        if (f.op == 'F' && f.a == snp::K_ACT && f.b == L) {
+          // freed, but a deferred BN apply fused into the next compute event
+          // (a ReLU) may still read it as the BN input (see the fusion above)
+          for (size_t k = j + 1; k < T; ++k) {
+            if (!is_compute(P.tape[k].op)) continue;
+            read = fused_into[k] >= 0 && net.prev[fused_into[k]][0] == L && !dead_at[k] &&
+                   join_fuse_at[k] < 0 && pool_fuse_at[k] < 0;
+            break;
+          }
+          break;
+        }
         if ((f.op == 'C' || f.op == 'R') && f.b == L) break;
         read = reads_act(j, L);
       }

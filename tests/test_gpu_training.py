@@ -675,3 +675,24 @@ def test_batched_dgrad_weight_prep_is_bit_identical(cuda, monkeypatch, feats):
     loss0, grads0, _, t0 = _run(net, 4, 4 << 30, feats, params, images, labels)
     assert t1.kernels < t0.kernels  # one batched launch replaces one per layer
     assert loss1 == loss0 and _bitwise(grads1, grads0)
+
+
+@pytest.mark.parametrize("feats", [ALL, "liveness,offload,recompute=memory"])
+def test_bn_relu_fusion_over_a_freed_bn_input_is_bit_identical(cuda, monkeypatch, feats):
+    """DenseNet-style layers: the JOIN output feeding BN -> ReLU is dropped right
+    after the BN (recompute), before the ReLU runs; the fused BN apply at the
+    ReLU still reads it -- planned only when nothing is allocated over it in
+    between except the ReLU's own output at exactly its blocks (elementwise in
+    place), and the dead-replay analysis keeps the replays it reads.  Bit-
+    identical to one kernel per layer (SN_FUSE=0), with fewer kernels."""
+    from paper_1801_04380_b200 import netgen
+    from paper_1801_04380_b200.training import init_parameters
+    net = netgen.gen_densenet(blocks=(3, 3, 2, 2), widths=(32, 64, 64, 64))
+    params = init_parameters(net, seed=9, head_scale=0.1)
+    images, labels = _inputs(net, 4, seed=2)
+    monkeypatch.setenv("SN_FUSE_REASSOC", "0")
+    loss, grads, _, t = _run(net, 4, 8 << 30, feats, params, images, labels)
+    monkeypatch.setenv("SN_FUSE", "0")
+    loss0, grads0, _, t0 = _run(net, 4, 8 << 30, feats, params, images, labels)
+    assert t.kernels < t0.kernels
+    assert loss == loss0 and _bitwise(grads, grads0)
