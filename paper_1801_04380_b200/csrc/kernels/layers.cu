@@ -483,6 +483,105 @@ __global__ void __launch_bounds__(kCbThreads, 2)
   }
 }
 
+// The same bulk-copy ring for the single-operand reductions (BN forward
+// statistics of an input no CONV epilogue summed -- DenseNet's JOIN outputs --
+// and a CONV bias gradient no BN dx pass summed): one 8 KB stream per stage
+// instead of two; the register version (colred_stage1_v4) ran them at 2-3 TB/s.
+template <class Op>
+__global__ void __launch_bounds__(kCbThreads, 2)
+    colred_bulk1(Op op, const float4* __restrict__ src, int64_t rows, int C, int64_t chunk, double* part) {
+  extern __shared__ __align__(128) float4 ring[];  // [stage][kCbStageF4]
+  __shared__ uint64_t full[kCbStages], empty[kCbStages];
+  const int C4 = C / 4;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * chunk;
+  const int64_t r1 = r0 + chunk < rows ? r0 + chunk : rows;
+  const int64_t f0 = r0 * C4, nf = (r1 - r0) * C4;
+  const int sf4 = bulk_stage_f4(C4);
+  const int nst = static_cast<int>((nf + sf4 - 1) / sf4);
+  const int t = threadIdx.x, warp = t >> 5;
+  if (t == 0) {
+    for (int i = 0; i < kCbStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kCbConsumers / 32);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  float4 a0 = zero4(), b0 = zero4(), a1 = zero4(), b1 = zero4();
+  const int nq = (C4 > kCbConsumers || kCbConsumers % C4 != 0) ? 2 : 1;
+  if (warp == kCbConsumers / 32) {
+    if (t == kCbConsumers) {
+      for (int it = 0; it < nst; ++it) {
+        const int s = it % kCbStages;
+        if (it >= kCbStages) mbar_wait(&empty[s], ((it / kCbStages) - 1) & 1);
+        const int64_t left = nf - static_cast<int64_t>(it) * sf4;
+        const int n = static_cast<int>(left < sf4 ? left : sf4);
+        mbar_arrive_expect_tx(&full[s], n * 16u);
+        bulk_load_1d(ring + s * kCbStageF4, src + f0 + static_cast<int64_t>(it) * sf4, n * 16u, &full[s]);
+      }
+    }
+  } else {
+    const typename Op::P p0 = op.prep4((t % C4) * 4, C);
+    const typename Op::P p1 = op.prep4(((t + kCbConsumers) % C4) * 4, C);
+    for (int it = 0; it < nst; ++it) {
+      const int s = it % kCbStages;
+      mbar_wait(&full[s], (it / kCbStages) & 1);
+      const int64_t left = nf - static_cast<int64_t>(it) * sf4;
+      const int n = static_cast<int>(left < sf4 ? left : sf4);
+      if (t < n) {
+        const typename Op::R r{ring[s * kCbStageF4 + t]};
+        float4 fa, fb;
+        op.comp(p0, r, fa, fb);
+        add4(a0, fa);
+        add4(b0, fb);
+      }
+      const int e = t + kCbConsumers;
+      if (e < n) {
+        const typename Op::R r{ring[s * kCbStageF4 + e]};
+        float4 fa, fb;
+        op.comp(p1, r, fa, fb);
+        if (nq == 2) {
+          add4(a1, fa);
+          add4(b1, fb);
+        } else {
+          add4(a0, fa);
+          add4(b0, fb);
+        }
+      }
+      __syncwarp();
+      if ((t & 31) == 0) mbar_arrive(&empty[s]);
+    }
+  }
+  __syncthreads();
+  float4* sa = ring;
+  float4* sb = ring + 2 * kCbConsumers;
+  if (t < kCbConsumers) {
+    sa[t] = a0;
+    sb[t] = b0;
+    if (nq == 2) {
+      sa[t + kCbConsumers] = a1;
+      sb[t + kCbConsumers] = b1;
+    }
+  }
+  __syncthreads();
+  const int ne = nq * kCbConsumers;
+  for (int q = t; q < C4; q += blockDim.x) {
+    double A[4] = {0, 0, 0, 0}, Bv[4] = {0, 0, 0, 0};
+    for (int e = q; e < ne; e += C4) {
+      const float4 u = sa[e], v = sb[e];
+      A[0] += u.x; A[1] += u.y; A[2] += u.z; A[3] += u.w;
+      Bv[0] += v.x; Bv[1] += v.y; Bv[2] += v.z; Bv[3] += v.w;
+    }
+    double* pa = part + (static_cast<size_t>(blockIdx.x) * 2) * C + q * 4;
+    double* pb = pa + C;
+    for (int i = 0; i < 4; ++i) {
+      pa[i] = A[i];
+      pb[i] = Bv[i];
+    }
+  }
+}
+constexpr int kCb1Smem = kCbStages * kCbStageF4 * 16;
+
 // Blocks of stage 1: enough rows per thread (>= ~64 float4 per operand) that
 // the double partials stay small next to the input, at most kRedChunks.
 template <class Op, class Fin>
@@ -507,6 +606,21 @@ cudaError_t colred(Op op, Fin fin, int64_t rows, int C, float* scratch_f, cudaSt
       if (!xskip(4)) colred_bulk_bn_bwd<<<static_cast<int>(nbb), kCbThreads, kCbSmem, st>>>(op, rows, C, ck, part);
       if (!xskip(1)) colred_stage2<<<stage2_blocks(C), kStage2Threads, 0, st>>>(part, static_cast<int>(nbb), C, fin);
       if (xskip(512)) colred_stage2<<<stage2_blocks(C), kStage2Threads, 0, st>>>(part, static_cast<int>(nbb), C, fin);
+      return cudaGetLastError();
+    }
+  }
+  if constexpr (std::is_same<Op, RedBnStatsOp>::value || std::is_same<Op, RedBiasOp>::value) {
+    if (colred_bulk_ok(C)) {
+      int nbb = 0;
+      const int64_t ck = bulk_chunk(rows, C, &nbb);
+      const cudaError_t ea = cudaFuncSetAttribute(colred_bulk1<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  kCb1Smem);
+      if (ea != cudaSuccess) return ea;
+      const float* src;
+      if constexpr (std::is_same<Op, RedBnStatsOp>::value) src = op.x; else src = op.dy;
+      colred_bulk1<Op><<<static_cast<int>(nbb), kCbThreads, kCb1Smem, st>>>(
+          op, reinterpret_cast<const float4*>(src), rows, C, ck, part);
+      colred_stage2<<<stage2_blocks(C), kStage2Threads, 0, st>>>(part, static_cast<int>(nbb), C, fin);
       return cudaGetLastError();
     }
   }
