@@ -614,6 +614,10 @@ int conv_wgrad_splits(const ConvShape& s, int64_t partial_floats_cap) {
   // 16 splits leave most slots idle (80 of 296 CTAs, 34 % tensor pipe) -- go
   // to 64 splits there (the partials stay a few MB)
   if (best < 0.6) search(64, want, best);
+  // a single output tile (Inception's 3x3/2 stem on the 4-channel image: 36 x 32
+  // weights over 2.8 M output pixels) fills at most 64 of 296 slots even then:
+  // one split per slot (partials 296 x 36 x 32 floats)
+  if (best < 0.6) search(slots, want, best);
   return effective_splits(static_cast<int>(NPQ), static_cast<int>(want));
 }
 
